@@ -1,0 +1,169 @@
+/* credo_gpu.h — C-ABI of the B200-native hot path of the credo model-group
+ * pipeline (arXiv 2205.15757): replica inference, per-request agreement and
+ * the SHA-256 certificate digests.
+ *
+ * Plain C: pointers and sizes only, no C++ or torch types, no exceptions
+ * across the boundary. Every entry point returns CG_OK (0) or a CG_E* code;
+ * cg_last_error() holds the message. The C++ adapters a maintainer adds on
+ * the reference side (CudaExecutor : credo::ModelExecutor, ...) are shown in
+ * INTEGRATION.md.
+ *
+ * Reference interfaces replaced (paths relative to the reference's proj/):
+ *   cg_sha256_batch            crypto::hash            include/credo/crypto.hpp:26-30, src/crypto.cpp:22-39
+ *   cg_leaf_hash_batch         merkle::leaf_hash       include/credo/merkle.hpp:53, src/merkle.cpp:22-25
+ *   cg_merkle_root_batch       merkle::Tree::build     include/credo/merkle.hpp:55-70, src/merkle.cpp:47-67
+ *   cg_select_quorum_batch     distance::select_quorum include/credo/distance.hpp:65-67, src/distance.cpp:138-216
+ *                              (+ the ensemble_label vote, src/experiments.cpp:99-125)
+ *   cg_model_load_linear       LinearToyModel::from_file_bytes + load_group digest check
+ *                              include/credo/model.hpp:22-39, src/model.cpp:46-65, src/engine.cpp:67-97
+ *   cg_model_load_cnn          (new) ImageNet-class model behind the same seam, keyed by weights_digest
+ *   cg_exec_run                ModelExecutor::run      include/credo/model.hpp:41-51, src/model.cpp:67-73
+ *   cg_certify_batch           InferenceEngine::execute_batch (src/engine.cpp:269-306) +
+ *                              build_result_tree (src/messages.cpp:235-258) + Coordinator::try_attest's
+ *                              agreement, manifest and A tree (src/coordinator.cpp:727-849) for one batch
+ */
+#ifndef CREDO_GPU_H
+#define CREDO_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  CG_OK = 0,
+  CG_EINVAL = 1,  /* the reference throws std::invalid_argument */
+  CG_ECUDA = 2,   /* CUDA runtime / launch failure */
+  CG_ENCCL = 3,   /* NCCL failure */
+  CG_EDIGEST = 4, /* model file does not hash to its descriptor digest */
+  CG_ECODEC = 5,  /* malformed canonical bytes (reference CodecError) */
+  CG_ENOTSUP = 6  /* no sm_100a device / not built for this device */
+};
+
+/* distance::Metric (include/credo/distance.hpp:23-27) */
+enum { CG_EUCLIDEAN = 0, CG_MAX_MINUS_MIN = 1, CG_CHEBYSHEV = 2 };
+
+typedef struct cg_ctx cg_ctx;
+typedef struct cg_model cg_model;
+typedef struct cg_group cg_group;
+
+/* ---- context ---------------------------------------------------------- */
+int cg_ctx_create(int device, cg_ctx** out);
+void cg_ctx_destroy(cg_ctx* ctx);
+const char* cg_last_error(const cg_ctx* ctx);
+/* Make `stream` (a cudaStream_t) the context's launch stream. */
+int cg_ctx_set_stream(cg_ctx* ctx, void* stream);
+void* cg_ctx_stream(cg_ctx* ctx);
+int cg_ctx_synchronize(cg_ctx* ctx);
+/* Number of kernels this library has launched on the context so far. */
+uint64_t cg_ctx_launch_count(const cg_ctx* ctx);
+
+/* ---- digests ------------------------------------------------------------
+ * count messages msg i = buf[off[i] .. off[i]+len[i]) (host memory);
+ * out: count × 32 bytes. */
+int cg_sha256_batch(cg_ctx* ctx, const uint8_t* buf, const uint64_t* off,
+                    const uint64_t* len, uint64_t count, uint8_t* out);
+/* H(0x00 || leaf_i) for each message. */
+int cg_leaf_hash_batch(cg_ctx* ctx, const uint8_t* buf, const uint64_t* off,
+                       const uint64_t* len, uint64_t count, uint8_t* out);
+/* ntrees Merkle roots over precomputed leaf digests: tree t folds
+ * leaf_hashes[first_t .. first_t + n_leaves[t]) where first_t is the running
+ * sum of n_leaves. CG_EINVAL for an empty tree (Tree::build throws). */
+int cg_merkle_root_batch(cg_ctx* ctx, const uint8_t* leaf_hashes,
+                         const uint64_t* n_leaves, uint64_t ntrees,
+                         uint8_t* roots);
+
+/* ---- agreement ----------------------------------------------------------
+ * R requests; outs is R × n × v row-major (request, node, lane); row (r, i)
+ * is considered only when bit i of present[r] is set (present == NULL: all
+ * n present). eps[r] is the request's epsilon (override or group default).
+ * Writes selected node mask, diameter, satisfied flag, and (label != NULL)
+ * the ensemble label (-1: none). status[r] = -1 where the reference throws
+ * std::invalid_argument; the call then returns CG_EINVAL. */
+int cg_select_quorum_batch(cg_ctx* ctx, const double* outs,
+                           const uint32_t* present, const double* eps,
+                           uint32_t R, uint32_t n, uint32_t f, uint32_t v,
+                           uint32_t metric, uint32_t* selected,
+                           double* diameter, uint8_t* satisfied,
+                           int8_t* status, int64_t* label);
+
+/* ---- models (executor seam) --------------------------------------------- */
+/* LinearToyModel canonical file bytes; digest = descriptor weights_digest.
+ * Fails with CG_EDIGEST when SHA-256(file) != digest (src/engine.cpp:79). */
+int cg_model_load_linear(cg_ctx* ctx, const uint8_t* file, uint64_t len,
+                         const uint8_t digest[32], cg_model** out);
+/* CNN model file (format in DESIGN.md §3: canonical header + f32 tensors). */
+int cg_model_load_cnn(cg_ctx* ctx, const uint8_t* file, uint64_t len,
+                      const uint8_t digest[32], cg_model** out);
+void cg_model_free(cg_model* m);
+int cg_model_dims(const cg_model* m, uint64_t* input_dim, uint64_t* output_dim);
+/* One output row per input row, in order (ModelExecutor::run). Host memory:
+ * in is B × u, out is B × v, both f64 row-major. */
+int cg_exec_run(cg_ctx* ctx, cg_model* m, const double* in, uint64_t B,
+                uint64_t u, double* out, uint64_t v);
+
+/* ---- one batch through the whole hot path -------------------------------
+ * A model group replica set: models[p] answers for node p (the
+ * assigned_models bijection, src/domain.cpp:247-268). */
+int cg_group_create(cg_ctx* ctx, cg_model* const* models, uint32_t N,
+                    uint32_t f, uint32_t metric, double default_eps,
+                    const char* group_id, uint64_t group_id_len,
+                    uint64_t version, uint32_t max_batch, uint32_t topk,
+                    cg_group** out);
+void cg_group_free(cg_group* g);
+
+/* The ExecutionBatch (include/credo/engine.hpp:29-34) in struct-of-arrays
+ * form: the request fields of InferenceRequest (include/credo/domain.hpp:
+ * 99-115). inputs is B × u f64; host memory unless inputs_on_device. */
+typedef struct {
+  uint32_t B;
+  uint64_t u;
+  const uint8_t* request_ids; /* B × 32 */
+  const double* inputs;       /* B × u */
+  int inputs_on_device;
+  const uint8_t* has_eps;     /* B (NULL: no overrides) */
+  const double* eps;          /* B */
+  const uint8_t* client_pubs; /* B × 32 */
+  const uint8_t* nonces;      /* concatenated nonce bytes */
+  const uint64_t* nonce_lens; /* B */
+  const uint8_t* client_sigs; /* B × 64 */
+} cg_request_batch;
+
+/* Host-memory results. Optional arrays may be NULL. */
+typedef struct {
+  uint32_t* selected;     /* B: node mask of the agreed quorum */
+  double* diameter;       /* B */
+  uint8_t* satisfied;     /* B */
+  int64_t* label;         /* B: ensemble label, -1 none */
+  uint8_t* r_roots;       /* N × 32: per-provider result-tree roots */
+  uint8_t* a_root;        /* 32: attestation-tree root */
+  uint64_t* manifest_len; /* 1 */
+  uint8_t* manifest_kind; /* optional, ≤ N×B + B: 0 whole, 1 single, 2 failure */
+  uint32_t* manifest_node;/* optional */
+  uint32_t* manifest_op;  /* optional */
+  uint8_t* leaf_hashes;   /* optional N × B × 32 (provider-major) */
+  uint8_t* a_leaf_hashes; /* optional ≤ N×B + B × 32 */
+  double* outputs;        /* optional N × B × v (provider-major) */
+  uint32_t* topk_idx;     /* optional N × B × k */
+  double* topk_val;       /* optional N × B × k */
+} cg_certify_out;
+
+/* Runs batch → N replica forwards → softmax/top-k → agreement + label →
+ * result leaves, R roots, attestation manifest, A leaves, A root. With
+ * out == NULL the call only enqueues (results stay on the device; fetch with
+ * cg_group_fetch). */
+int cg_certify_batch(cg_group* g, const cg_request_batch* batch,
+                     cg_certify_out* out);
+int cg_group_fetch(cg_group* g, cg_certify_out* out);
+/* Agreement + digest path over precomputed replica outputs (host memory,
+ * N × B × v provider-major f64): the C5 sweep and fault-injection entry
+ * point (a corrupt replica is just a shifted output row). */
+int cg_certify_outputs(cg_group* g, const cg_request_batch* batch,
+                       const double* outputs, cg_certify_out* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CREDO_GPU_H */

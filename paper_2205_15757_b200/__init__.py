@@ -1,0 +1,10 @@
+"""B200-native hot path of the credo model-group pipeline (arXiv 2205.15757):
+replica inference, per-request agreement and certificate digests behind a
+C-ABI (include/credo_gpu.h). See DESIGN.md."""
+from .credo import (AgreementOutcome, CHEBYSHEV, Context, CredoError,
+                    CudaExecutor, DigestMismatch, EUCLIDEAN, InvalidArgument,
+                    MAX_MINUS_MIN, Model, ModelGroup, RequestBatch, lib)
+
+__all__ = ["AgreementOutcome", "CHEBYSHEV", "Context", "CredoError",
+           "CudaExecutor", "DigestMismatch", "EUCLIDEAN", "InvalidArgument",
+           "MAX_MINUS_MIN", "Model", "ModelGroup", "RequestBatch", "lib"]

@@ -1,0 +1,439 @@
+"""Python front-end over the C-ABI (``include/credo_gpu.h``).
+
+Mirrors the reference's hot-path interface names so callers (and the parity
+tests) read like the reference's own code:
+
+================================  ============================================
+reference (proj/)                 here
+================================  ============================================
+crypto::hash                      :meth:`Context.hash_batch`
+merkle::leaf_hash                 :meth:`Context.leaf_hash_batch`
+merkle::Tree::build(...).root()   :meth:`Context.merkle_roots`
+distance::select_quorum           :meth:`Context.select_quorum` /
+                                  :meth:`Context.select_quorum_batch`
+ModelExecutor::run                :class:`CudaExecutor`
+InferenceEngine::execute_batch +  :meth:`ModelGroup.certify`
+try_prepare/try_attest digests
+================================  ============================================
+
+There is no CPU fallback: constructing a :class:`Context` loads
+``libcredo_gpu.so`` and fails loudly when it (or an sm_100a device) is
+missing.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import struct
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libcredo_gpu.so")
+
+CG_OK, CG_EINVAL, CG_ECUDA, CG_ENCCL, CG_EDIGEST, CG_ECODEC, CG_ENOTSUP = range(7)
+EUCLIDEAN, MAX_MINUS_MIN, CHEBYSHEV = 0, 1, 2
+
+u64, u32, dbl, vp = C.c_uint64, C.c_uint32, C.c_double, C.c_void_p
+
+
+class CredoError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[{code}] {msg}")
+        self.code = code
+
+
+class InvalidArgument(CredoError, ValueError):
+    """Where the reference throws std::invalid_argument."""
+
+
+class DigestMismatch(CredoError):
+    pass
+
+
+class CodecError(CredoError, ValueError):
+    pass
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: build it with "
+                "`python -c 'import __graft_entry__ as g; g.build()'` "
+                "(no CPU fallback exists)")
+        L = C.CDLL(LIB_PATH)
+        L.cg_last_error.restype = C.c_char_p
+        L.cg_last_error.argtypes = [vp]
+        L.cg_ctx_create.argtypes = [C.c_int, C.POINTER(vp)]
+        L.cg_ctx_destroy.argtypes = [vp]
+        L.cg_ctx_set_stream.argtypes = [vp, vp]
+        L.cg_ctx_stream.restype = vp
+        L.cg_ctx_stream.argtypes = [vp]
+        L.cg_ctx_synchronize.argtypes = [vp]
+        L.cg_ctx_launch_count.restype = u64
+        L.cg_ctx_launch_count.argtypes = [vp]
+        L.cg_model_free.argtypes = [vp]
+        L.cg_group_free.argtypes = [vp]
+        _lib = L
+    return _lib
+
+
+def _p(a):
+    return C.c_void_p(a.ctypes.data) if a is not None else None
+
+
+# ---------------------------------------------------------------- context
+class Context:
+    """One context per process/GPU (cg_ctx)."""
+
+    def __init__(self, device: int = 0):
+        self.L = lib()
+        h = vp()
+        rc = self.L.cg_ctx_create(device, C.byref(h))
+        if rc != CG_OK:
+            raise CredoError(rc, f"cg_ctx_create(device={device}) failed "
+                                 "(needs an sm_100a B200)")
+        self.h = h
+        self.device = device
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.cg_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc: int):
+        if rc == CG_OK:
+            return
+        msg = self.L.cg_last_error(self.h).decode(errors="replace")
+        cls = {CG_EINVAL: InvalidArgument, CG_EDIGEST: DigestMismatch,
+               CG_ECODEC: CodecError}.get(rc, CredoError)
+        raise cls(rc, msg)
+
+    def set_stream(self, stream_ptr: int):
+        self._check(self.L.cg_ctx_set_stream(self.h, vp(stream_ptr)))
+
+    @property
+    def stream(self) -> int:
+        return self.L.cg_ctx_stream(self.h) or 0
+
+    def synchronize(self):
+        self._check(self.L.cg_ctx_synchronize(self.h))
+
+    def launch_count(self) -> int:
+        return int(self.L.cg_ctx_launch_count(self.h))
+
+    # -- digests ----------------------------------------------------------
+    def _msgs(self, msgs: Sequence[bytes]):
+        lens = np.array([len(m) for m in msgs], np.uint64)
+        offs = np.zeros(len(msgs), np.uint64)
+        if len(msgs) > 1:
+            offs[1:] = np.cumsum(lens[:-1])
+        return b"".join(msgs), offs, lens
+
+    def hash_batch(self, msgs: Sequence[bytes]) -> list[bytes]:
+        """crypto::hash over each message (crypto.cpp:22-27)."""
+        buf, offs, lens = self._msgs(msgs)
+        out = C.create_string_buffer(32 * max(1, len(msgs)))
+        self._check(self.L.cg_sha256_batch(self.h, buf, _p(offs), _p(lens),
+                                           u64(len(msgs)), out))
+        return [out.raw[32 * i:32 * i + 32] for i in range(len(msgs))]
+
+    def hash(self, data: bytes) -> bytes:
+        return self.hash_batch([data])[0]
+
+    def leaf_hash_batch(self, leaves: Sequence[bytes]) -> list[bytes]:
+        """merkle::leaf_hash = H(0x00 || leaf) (merkle.cpp:22-25)."""
+        buf, offs, lens = self._msgs(leaves)
+        out = C.create_string_buffer(32 * max(1, len(leaves)))
+        self._check(self.L.cg_leaf_hash_batch(self.h, buf, _p(offs), _p(lens),
+                                              u64(len(leaves)), out))
+        return [out.raw[32 * i:32 * i + 32] for i in range(len(leaves))]
+
+    def merkle_roots(self, trees: Sequence[Sequence[bytes]]) -> list[bytes]:
+        """Tree::build(...).root() over precomputed leaf hashes per tree."""
+        n = np.array([len(t) for t in trees], np.uint64)
+        buf = b"".join(b"".join(t) for t in trees)
+        out = C.create_string_buffer(32 * max(1, len(trees)))
+        self._check(self.L.cg_merkle_root_batch(self.h, buf, _p(n),
+                                                u64(len(trees)), out))
+        return [out.raw[32 * i:32 * i + 32] for i in range(len(trees))]
+
+    # -- agreement ----------------------------------------------------------
+    def select_quorum_batch(self, outs: np.ndarray, n: int, f: int,
+                            metric: int, eps, present=None, with_label=True):
+        """outs: (R, n, v). Returns dict of arrays; raises InvalidArgument
+        where distance::select_quorum would throw (status marks which)."""
+        outs = np.ascontiguousarray(outs, np.float64)
+        R, n_, v = outs.shape
+        assert n_ == n
+        eps = np.ascontiguousarray(np.broadcast_to(np.asarray(eps, np.float64), (R,)))
+        pres = None if present is None else np.ascontiguousarray(present, np.uint32)
+        sel = np.zeros(R, np.uint32)
+        diam = np.zeros(R, np.float64)
+        sat = np.zeros(R, np.uint8)
+        status = np.zeros(R, np.int8)
+        label = np.zeros(R, np.int64) if with_label else None
+        rc = self.L.cg_select_quorum_batch(self.h, _p(outs), _p(pres), _p(eps),
+                                           u32(R), u32(n), u32(f), u32(v),
+                                           u32(metric), _p(sel), _p(diam),
+                                           _p(sat), _p(status), _p(label))
+        res = dict(selected=sel, diameter=diam, satisfied=sat.astype(bool),
+                   status=status, label=label)
+        if rc != CG_OK:
+            err = InvalidArgument if rc == CG_EINVAL else CredoError
+            e = err(rc, self.L.cg_last_error(self.h).decode())
+            e.result = res
+            raise e
+        return res
+
+    def select_quorum(self, results: dict, n: int, f: int, metric: int,
+                      epsilon: float):
+        """distance::select_quorum(map<node, vector<double>>, n, f, m, eps)."""
+        if not results:
+            raise InvalidArgument(CG_EINVAL, "select_quorum: no results")
+        v = len(next(iter(results.values())))
+        outs = np.zeros((1, n, max(v, 1)), np.float64)
+        present = 0
+        for node, vec in results.items():
+            if node >= n or node >= 32:
+                raise InvalidArgument(CG_EINVAL, "node index out of range")
+            if len(vec) != v:
+                raise InvalidArgument(CG_EINVAL, "result dimensionality mismatch")
+            outs[0, node, :] = vec
+            present |= 1 << node
+        r = self.select_quorum_batch(outs, n, f, metric, [epsilon],
+                                     present=[present], with_label=False)
+        sel = int(r["selected"][0])
+        return AgreementOutcome(
+            selected={i for i in range(32) if sel >> i & 1},
+            diameter=float(r["diameter"][0]), satisfied=bool(r["satisfied"][0]))
+
+
+@dataclass
+class AgreementOutcome:
+    """distance::AgreementOutcome (distance.hpp:55-59)."""
+    selected: set = field(default_factory=set)
+    diameter: float = 0.0
+    satisfied: bool = False
+
+
+# ------------------------------------------------------------------ models
+class Model:
+    def __init__(self, ctx: Context, h, digest: bytes):
+        self.ctx, self.h, self.digest = ctx, h, digest
+        u, v = u64(), u64()
+        ctx.L.cg_model_dims(h, C.byref(u), C.byref(v))
+        self.input_dim, self.output_dim = u.value, v.value
+
+    @classmethod
+    def load_linear(cls, ctx: Context, file: bytes, digest: bytes) -> "Model":
+        """LinearToyModel::from_file_bytes + the load_group digest check."""
+        h = vp()
+        ctx._check(ctx.L.cg_model_load_linear(ctx.h, file, u64(len(file)),
+                                              digest, C.byref(h)))
+        return cls(ctx, h, digest)
+
+    @classmethod
+    def load_cnn(cls, ctx: Context, file: bytes, digest: bytes) -> "Model":
+        h = vp()
+        ctx._check(ctx.L.cg_model_load_cnn(ctx.h, file, u64(len(file)),
+                                           digest, C.byref(h)))
+        return cls(ctx, h, digest)
+
+    def free(self):
+        if self.h:
+            self.ctx.L.cg_model_free(self.h)
+            self.h = None
+
+
+class CudaExecutor:
+    """ModelExecutor::run (model.hpp:48-50): one output per input, in order."""
+
+    def __init__(self, ctx: Context):
+        self.ctx = ctx
+
+    def run(self, model: Model, inputs) -> np.ndarray:
+        x = np.ascontiguousarray(inputs, np.float64)
+        if x.ndim == 1:
+            x = x[None]
+        B, u = x.shape
+        y = np.zeros((B, model.output_dim), np.float64)
+        self.ctx._check(self.ctx.L.cg_exec_run(self.ctx.h, model.h, _p(x),
+                                               u64(B), u64(u), _p(y),
+                                               u64(model.output_dim)))
+        return y
+
+
+# ------------------------------------------------------------ request batch
+@dataclass
+class RequestBatch:
+    """ExecutionBatch (engine.hpp:29-34) in struct-of-arrays form."""
+    request_ids: np.ndarray          # (B, 32) uint8
+    inputs: object                   # (B, u) float64 ndarray, or device ptr
+    client_pubs: np.ndarray          # (B, 32) uint8
+    nonces: list                     # B × bytes
+    client_sigs: np.ndarray          # (B, 64) uint8
+    eps: Optional[list] = None       # B × (float | None)
+    u: Optional[int] = None
+    B: Optional[int] = None
+
+    @classmethod
+    def from_encoded(cls, encs: Sequence[bytes]) -> "RequestBatch":
+        """Decode InferenceRequest::encode bytes (domain.cpp:153-175)."""
+        ids, inputs, pubs, nonces, sigs, eps = [], [], [], [], [], []
+        for buf in encs:
+            off = 32
+            ids.append(np.frombuffer(buf[:32], np.uint8))
+            gl = struct.unpack(">I", buf[off:off + 4])[0]; off += 4 + gl
+            n = struct.unpack(">I", buf[off:off + 4])[0]; off += 4
+            inputs.append(np.frombuffer(buf[off:off + 8 * n], ">f8").astype(np.float64)); off += 8 * n
+            has = buf[off]; off += 1
+            if has:
+                eps.append(struct.unpack(">d", buf[off:off + 8])[0]); off += 8
+            else:
+                eps.append(None)
+            pubs.append(np.frombuffer(buf[off:off + 32], np.uint8)); off += 32
+            nl = struct.unpack(">I", buf[off:off + 4])[0]; off += 4
+            nonces.append(bytes(buf[off:off + nl])); off += nl
+            sigs.append(np.frombuffer(buf[off:off + 64], np.uint8)); off += 64
+            if off != len(buf):
+                raise CodecError(CG_ECODEC, "trailing bytes after value")
+        return cls(np.stack(ids), np.stack(inputs), np.stack(pubs), nonces,
+                   np.stack(sigs), eps if any(e is not None for e in eps) else None)
+
+
+class _CReqBatch(C.Structure):
+    _fields_ = [("B", u32), ("u", u64), ("request_ids", vp), ("inputs", vp),
+                ("inputs_on_device", C.c_int), ("has_eps", vp), ("eps", vp),
+                ("client_pubs", vp), ("nonces", vp), ("nonce_lens", vp),
+                ("client_sigs", vp)]
+
+
+class _COut(C.Structure):
+    _fields_ = [(n, vp) for n in (
+        "selected", "diameter", "satisfied", "label", "r_roots", "a_root",
+        "manifest_len", "manifest_kind", "manifest_node", "manifest_op",
+        "leaf_hashes", "a_leaf_hashes", "outputs", "topk_idx", "topk_val")]
+
+
+class ModelGroup:
+    """A model group's replica set on this GPU: models[p] answers as node p."""
+
+    def __init__(self, ctx: Context, models: Sequence[Model], f: int,
+                 metric: int, default_eps: float, group_id: bytes,
+                 version: int, max_batch: int, topk: int = 5):
+        self.ctx, self.models = ctx, list(models)
+        self.N, self.f, self.topk = len(models), f, topk
+        self.v = models[0].output_dim
+        self.u = models[0].input_dim
+        self.group_id, self.version = group_id, version
+        arr = (vp * len(models))(*[m.h for m in models])
+        h = vp()
+        ctx._check(ctx.L.cg_group_create(ctx.h, arr, u32(len(models)), u32(f),
+                                         u32(metric), dbl(default_eps),
+                                         group_id, u64(len(group_id)),
+                                         u64(version), u32(max_batch),
+                                         u32(topk), C.byref(h)))
+        self.h = h
+        self._keep = None
+
+    def free(self):
+        if self.h:
+            self.ctx.L.cg_group_free(self.h)
+            self.h = None
+
+    def _cbatch(self, b: RequestBatch):
+        on_dev = not isinstance(b.inputs, np.ndarray)
+        if on_dev:
+            inputs_ptr, B, u = int(b.inputs), int(b.B), int(b.u)
+        else:
+            x = np.ascontiguousarray(b.inputs, np.float64)
+            inputs_ptr, (B, u) = x.ctypes.data, x.shape
+        ids = np.ascontiguousarray(b.request_ids, np.uint8)
+        pubs = np.ascontiguousarray(b.client_pubs, np.uint8)
+        sigs = np.ascontiguousarray(b.client_sigs, np.uint8)
+        nl = np.array([len(n) for n in b.nonces], np.uint64)
+        nb = np.frombuffer(b"".join(b.nonces) or b"\0", np.uint8).copy()
+        has = eps = None
+        if b.eps is not None:
+            has = np.array([e is not None for e in b.eps], np.uint8)
+            eps = np.array([e or 0.0 for e in b.eps], np.float64)
+        keep = [ids, pubs, sigs, nl, nb, has, eps,
+                None if on_dev else x]
+        cb = _CReqBatch(B, u, ids.ctypes.data, inputs_ptr, int(on_dev),
+                        None if has is None else has.ctypes.data,
+                        None if eps is None else eps.ctypes.data,
+                        pubs.ctypes.data, nb.ctypes.data, nl.ctypes.data,
+                        sigs.ctypes.data)
+        return cb, keep, B
+
+    def certify(self, batch: RequestBatch, want_outputs: bool = False,
+                want_leaves: bool = False, sync: bool = True):
+        """One ExecutionBatch through the hot path. sync=False only enqueues
+        (results stay on the device; call :meth:`fetch`)."""
+        cb, keep, B = self._cbatch(batch)
+        self._keep = keep
+        if not sync:
+            self.ctx._check(self.ctx.L.cg_certify_batch(self.h, C.byref(cb), None))
+            self._lastB = B
+            return None
+        self._lastB = B
+        return self.fetch(want_outputs, want_leaves, _enqueue=(cb,))
+
+    def certify_outputs(self, batch: RequestBatch, outputs: np.ndarray,
+                        want_leaves: bool = False):
+        """Agreement + digests over precomputed (N, B, v) replica outputs
+        (C5 sweep / fault injection: a corrupt replica is a shifted row)."""
+        cb, keep, B = self._cbatch(batch)
+        o = np.ascontiguousarray(outputs, np.float64)
+        assert o.shape == (self.N, B, self.v)
+        self._keep = keep + [o]
+        self._lastB = B
+        return self.fetch(False, want_leaves, _enqueue=(cb,), _outputs=o)
+
+    def fetch(self, want_outputs=False, want_leaves=False, _enqueue=None,
+              _outputs=None):
+        B, N, v, k = self._lastB, self.N, self.v, self.topk
+        amax = N * B + B + N
+        r = dict(selected=np.zeros(B, np.uint32), diameter=np.zeros(B),
+                 satisfied=np.zeros(B, np.uint8), label=np.zeros(B, np.int64),
+                 r_roots=np.zeros((N, 32), np.uint8), a_root=np.zeros(32, np.uint8),
+                 manifest_len=np.zeros(1, np.uint64),
+                 manifest_kind=np.zeros(amax, np.uint8),
+                 manifest_node=np.zeros(amax, np.uint32),
+                 manifest_op=np.zeros(amax, np.uint32),
+                 a_leaf_hashes=np.zeros((amax, 32), np.uint8))
+        if want_leaves:
+            r["leaf_hashes"] = np.zeros((N, B, 32), np.uint8)
+        if want_outputs:
+            r["outputs"] = np.zeros((N, B, v), np.float64)
+            r["topk_idx"] = np.zeros((N, B, k), np.uint32)
+            r["topk_val"] = np.zeros((N, B, k), np.float64)
+        o = _COut(*[r[n].ctypes.data if n in r else None
+                    for n, _ in _COut._fields_])
+        if _outputs is not None:
+            rc = self.ctx.L.cg_certify_outputs(self.h, C.byref(_enqueue[0]),
+                                               _p(_outputs), C.byref(o))
+        elif _enqueue is not None:
+            rc = self.ctx.L.cg_certify_batch(self.h, C.byref(_enqueue[0]), C.byref(o))
+        else:
+            rc = self.ctx.L.cg_group_fetch(self.h, C.byref(o))
+        self.ctx._check(rc)
+        m = int(r["manifest_len"][0])
+        for key in ("manifest_kind", "manifest_node", "manifest_op", "a_leaf_hashes"):
+            r[key] = r[key][:m]
+        r["satisfied"] = r["satisfied"].astype(bool)
+        return r

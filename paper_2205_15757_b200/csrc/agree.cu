@@ -1,0 +1,507 @@
+// Agreement, label vote, attestation manifest, softmax/top-k and the fp64
+// LinearToyModel executor.
+//
+// Reference semantics (bit-exact targets):
+//   distance::delta / select_quorum   proj/src/distance.cpp:70-216
+//   argmax / ensemble_label           proj/src/experiments.cpp:99-125
+//   try_attest manifest               proj/src/coordinator.cpp:774-832
+//   LinearToyModel::run               proj/src/model.cpp:12-36
+// Every fp64 reduction that the reference performs sequentially is kept
+// sequential (and un-fused: __dmul_rn/__dadd_rn) so decisions match bit for
+// bit; parallelism comes from requests, pairs and subsets instead.
+#include "agree.cuh"
+#include "sha256.cuh"
+
+namespace cg {
+
+// --------------------------------------------------------------- delta
+__device__ __forceinline__ double delta_dev(uint32_t metric, const double* x,
+                                            const double* y, uint32_t v) {
+  if (metric == 0) {  // euclidean: acc += d*d in lane order, then sqrt
+    double acc = 0.0;
+#pragma unroll 4
+    for (uint32_t i = 0; i < v; i++) {
+      double d = __dsub_rn(__ldg(x + i), __ldg(y + i));
+      acc = __dadd_rn(acc, __dmul_rn(d, d));
+    }
+    return __dsqrt_rn(acc);
+  }
+  if (metric == 1) return fabs(__dsub_rn(__ldg(x), __ldg(y)));
+  double worst = 0.0;  // chebyshev: std::max(worst, |x-y|)
+  for (uint32_t i = 0; i < v; i++) {
+    double d = fabs(__dsub_rn(__ldg(x + i), __ldg(y + i)));
+    worst = (worst < d) ? d : worst;
+  }
+  return worst;
+}
+
+struct Cand {
+  uint32_t valid, size, mask;
+  double diam;
+};
+
+// better(a, b) of distance.cpp:128-134 on subset masks (positions ascend
+// with node ids, so the sorted-tuple order is decided by the lowest bit of
+// the symmetric difference).
+__device__ __forceinline__ bool cand_better(const Cand& a, const Cand& b) {
+  if (!a.valid) return false;
+  if (!b.valid) return true;
+  if (a.size != b.size) return a.size > b.size;
+  if (a.diam != b.diam) return a.diam < b.diam;
+  uint32_t d = a.mask ^ b.mask;
+  return d && (a.mask & (d & (0u - d)));
+}
+
+__device__ __forceinline__ Cand shfl_cand(const Cand& c, int src) {
+  Cand o;
+  o.valid = __shfl_sync(0xffffffffu, c.valid, src);
+  o.size = __shfl_sync(0xffffffffu, c.size, src);
+  o.mask = __shfl_sync(0xffffffffu, c.mask, src);
+  o.diam = __shfl_sync(0xffffffffu, c.diam, src);
+  return o;
+}
+
+constexpr int kQThreads = 128;
+constexpr int kMaxM = 20;
+
+// One CTA per request. outs(k, p, i) = outs[p*ps + k*rs + i].
+__global__ void __launch_bounds__(kQThreads) select_quorum_kernel(
+    const double* __restrict__ outs, uint64_t ps, uint64_t rs,
+    const uint32_t* __restrict__ present, const double* __restrict__ eps,
+    uint32_t R, uint32_t n, uint32_t f, uint32_t v, uint32_t metric,
+    uint32_t* __restrict__ selected, double* __restrict__ diameter,
+    uint8_t* __restrict__ satisfied, int8_t* __restrict__ status,
+    int64_t* __restrict__ label) {
+  __shared__ double dist[kMaxM * kMaxM];
+  __shared__ uint32_t nodes[kMaxM];
+  __shared__ Cand warp_best[kQThreads / 32];
+  __shared__ int s_m, s_bad;
+  __shared__ uint32_t s_arg[kMaxM];
+  __shared__ double s_argv[kMaxM];
+  const uint32_t k = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    uint32_t pm = present ? present[k] : ((n >= 32) ? 0xffffffffu : ((1u << n) - 1));
+    int m = 0, bad = 0;
+    // select_quorum argument checks (distance.cpp:141-165)
+    if (n == 0 || f >= n) bad = 1;
+    if (n < 32 && (pm >> n)) bad = 1;  // node index out of range
+    if (v == 0) bad = 1;               // empty result vector
+    for (uint32_t i = 0; i < 32; i++)
+      if (pm >> i & 1) {
+        if (m < kMaxM) nodes[m] = i;
+        m++;
+      }
+    if (!bad && (uint32_t)m < n - f) bad = 1;  // fewer than N-f present
+    if (m > kMaxM) bad = 1;                    // too many results
+    if (!bad && m >= 2 && metric == 1 && v != 1) bad = 1;  // scalar metric
+    if (!bad && m >= 2 && metric > 2) bad = 1;             // unknown metric
+    s_m = m;
+    s_bad = bad;
+  }
+  __syncthreads();
+  if (s_bad) {
+    if (tid == 0) {
+      status[k] = -1;
+      selected[k] = 0;
+      diameter[k] = 0.0;
+      satisfied[k] = 0;
+      if (label) label[k] = -1;
+    }
+    return;
+  }
+  const int m = s_m;
+  const uint32_t need = n - f;
+  // pairwise distances once (distance.cpp:167-174)
+  const int npairs = m * (m - 1) / 2;
+  for (int pr = tid; pr < npairs; pr += kQThreads) {
+    int i = 0, rem = pr;
+    while (rem >= m - 1 - i) { rem -= m - 1 - i; i++; }
+    int j = i + 1 + rem;
+    double d = delta_dev(metric, outs + nodes[i] * ps + k * rs,
+                         outs + nodes[j] * ps + k * rs, v);
+    dist[i * kMaxM + j] = d;
+    dist[j * kMaxM + i] = d;
+  }
+  __syncthreads();
+  // exhaustive subset scan (distance.cpp:178-205), masks striped over threads
+  const double e = eps[k];
+  Cand best{0, 0, 0, 0.0};
+  const uint32_t limit = 1u << m;
+  for (uint32_t mask = 1 + tid; mask < limit; mask += kQThreads) {
+    uint32_t size = __popc(mask);
+    if (size < need) continue;
+    double dm = 0.0;
+    bool ok = true;
+    for (int i = 0; i < m && ok; i++) {
+      if (!(mask >> i & 1)) continue;
+      for (int j = i + 1; j < m; j++) {
+        if (!(mask >> j & 1)) continue;
+        double x = dist[i * kMaxM + j];
+        dm = (dm < x) ? x : dm;
+        if (dm > e) { ok = false; break; }
+      }
+    }
+    if (!ok) continue;
+    Cand c{1, size, mask, dm};
+    if (cand_better(c, best)) best = c;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    Cand other = shfl_cand(best, lane ^ o);
+    if (cand_better(other, best)) best = other;
+  }
+  if (lane == 0) warp_best[warp] = best;
+  __syncthreads();
+  if (tid == 0) {
+    for (int w = 1; w < kQThreads / 32; w++)
+      if (cand_better(warp_best[w], best)) best = warp_best[w];
+    warp_best[0] = best;
+    uint32_t sel = 0;
+    if (best.valid)
+      for (int i = 0; i < m; i++)
+        if (best.mask >> i & 1) sel |= 1u << nodes[i];
+    status[k] = 0;
+    selected[k] = sel;
+    diameter[k] = best.valid ? best.diam : 0.0;
+    satisfied[k] = best.valid ? 1 : 0;
+  }
+  if (!label) return;
+  __syncthreads();
+  // ensemble_label (experiments.cpp:106-125) over the selected members:
+  // argmax per member (first maximum), votes > f, highest confidence wins.
+  best = warp_best[0];
+  if (!best.valid) {
+    if (tid == 0) label[k] = -1;
+    return;
+  }
+  for (int i = warp; i < m; i += kQThreads / 32) {
+    if (!(best.mask >> i & 1)) continue;
+    const double* row = outs + nodes[i] * ps + k * rs;
+    double bv = -INFINITY;
+    uint32_t bi = 0xffffffffu;
+    for (uint32_t t = lane; t < v; t += 32) {
+      double x = __ldg(row + t);
+      if (bi == 0xffffffffu || bv < x) { bv = x; bi = t; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      uint32_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      bool take = (oi != 0xffffffffu) &&
+                  (bi == 0xffffffffu || bv < ov || (!(ov < bv) && oi < bi));
+      if (take) { bv = ov; bi = oi; }
+    }
+    if (lane == 0) { s_arg[i] = bi; s_argv[i] = bv; }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int64_t win = -1;
+    double win_conf = -1.0;
+    // labels ascending; count and max confidence per label
+    for (int i = 0; i < m; i++) {
+      if (!(best.mask >> i & 1)) continue;
+      uint32_t l = s_arg[i];
+      bool seen_before = false;
+      for (int q = 0; q < i; q++)
+        if ((best.mask >> q & 1) && s_arg[q] == l) seen_before = true;
+      if (seen_before) continue;
+      uint32_t cnt = 0;
+      double conf = 0.0;
+      for (int q = 0; q < m; q++)
+        if ((best.mask >> q & 1) && s_arg[q] == l) {
+          cnt++;
+          conf = (conf < s_argv[q]) ? s_argv[q] : conf;
+        }
+      if (cnt <= f) continue;
+      // ascending label scan with strict >: a smaller label wins ties
+      if (conf > win_conf || (conf == win_conf && win >= 0 && (int64_t)l < win)) {
+        win = l;
+        win_conf = conf;
+      }
+    }
+    label[k] = win;
+  }
+}
+
+void launch_select_quorum(const double* outs, uint64_t ps, uint64_t rs,
+                          const uint32_t* present, const double* eps,
+                          uint32_t R, uint32_t n, uint32_t f, uint32_t v,
+                          uint32_t metric, uint32_t* selected, double* diameter,
+                          uint8_t* satisfied, int8_t* status, int64_t* label,
+                          cudaStream_t st) {
+  if (R == 0) return;
+  select_quorum_kernel<<<R, kQThreads, 0, st>>>(outs, ps, rs, present, eps, R,
+                                                n, f, v, metric, selected,
+                                                diameter, satisfied, status,
+                                                label);
+  CG_CHECK_LAUNCH();
+}
+
+// ----------------------------------------------------- attestation manifest
+// Single CTA. Manifest order (coordinator.cpp:774-832): whole_batch leaves
+// by node, then single leaves by (op, node), then failure leaves by op.
+// Whole-batch and failure leaf hashes are written here; single leaves are
+// long chains (the full request is re-hashed under tag 0x53), so this kernel
+// only assigns their manifest slots (single_pos) for the chain-job kernel.
+
+__device__ void sha256_local(const uint8_t* m, uint32_t len, uint8_t* out) {
+  uint32_t s[8], w[16];
+  sha256_iv(s);
+  uint32_t nblk = (len + 9 + 63) / 64;
+  for (uint32_t b = 0; b < nblk; b++) {
+    for (int i = 0; i < 16; i++) {
+      uint32_t x = 0;
+      for (int t = 0; t < 4; t++) {
+        uint32_t pos = b * 64 + 4 * i + t, byte = 0;
+        if (pos < len) byte = m[pos];
+        else if (pos == len) byte = 0x80;
+        else if (pos >= nblk * 64 - 8) byte = (uint32_t)((uint64_t)len * 8 >> (56 - 8 * (pos - (nblk * 64 - 8)))) & 0xff;
+        x = (x << 8) | byte;
+      }
+      w[i] = x;
+    }
+    sha256_compress(s, w);
+  }
+  store_digest(s, out);
+}
+
+constexpr int kManThreads = 1024;
+
+__global__ void __launch_bounds__(kManThreads) attest_manifest_kernel(
+    uint32_t B, uint32_t N, const uint32_t* __restrict__ sel,
+    const uint8_t* __restrict__ sat, const uint8_t* __restrict__ r_roots,
+    const uint8_t* __restrict__ req_ids, const uint8_t* __restrict__ gid,
+    uint32_t gid_len, uint64_t version, uint8_t* __restrict__ a_leaves,
+    int32_t* __restrict__ single_pos, uint8_t* __restrict__ kinds,
+    uint32_t* __restrict__ m_nodes, uint32_t* __restrict__ m_ops,
+    uint32_t* __restrict__ count) {
+  __shared__ uint32_t s_whole;
+  __shared__ uint32_t s_scan[kManThreads];
+  __shared__ uint32_t s_carry_single, s_carry_fail;
+  const int tid = threadIdx.x;
+  if (tid == 0) { s_whole = 0xffffffffu; s_carry_single = 0; s_carry_fail = 0; }
+  __syncthreads();
+  uint32_t acc = 0xffffffffu;
+  for (uint32_t k = tid; k < B; k += kManThreads) acc &= sat[k] ? sel[k] : 0u;
+  atomicAnd(&s_whole, acc);
+  __syncthreads();
+  const uint32_t all_nodes = (N >= 32) ? 0xffffffffu : ((1u << N) - 1);
+  const uint32_t whole = (B ? s_whole : 0u) & all_nodes;
+  const uint32_t nwhole = __popc(whole);
+  // whole-batch leaves: H(0x00 || 0x57 || R root of node p)
+  if (tid < 32 && (whole >> tid & 1)) {
+    uint32_t pos = __popc(whole & ((1u << tid) - 1));
+    sha256_tagged_digest_leaf(0x57, r_roots + 32 * tid, a_leaves + 32 * pos);
+    kinds[pos] = 0;
+    m_nodes[pos] = tid;
+    m_ops[pos] = 0;
+  }
+  // total singles for the failure offset
+  uint32_t local = 0;
+  for (uint32_t k = tid; k < B; k += kManThreads)
+    if (sat[k]) local += __popc(sel[k] & ~whole);
+  s_scan[tid] = local;
+  __syncthreads();
+  if (tid == 0) {
+    uint32_t t = 0;
+    for (int i = 0; i < kManThreads; i++) t += s_scan[i];
+    s_carry_fail = t;
+  }
+  __syncthreads();
+  const uint32_t nsingle = s_carry_fail;
+  // ordered passes over chunks of kManThreads ops
+  for (uint32_t base = 0; base < B; base += kManThreads) {
+    uint32_t k = base + tid;
+    uint32_t ns = 0, nf = 0;
+    if (k < B) {
+      if (sat[k]) ns = __popc(sel[k] & ~whole);
+      else nf = 1;
+    }
+    // exclusive scan of (ns | nf<<16) — B and N small enough for 16 bits
+    s_scan[tid] = ns | (nf << 16);
+    __syncthreads();
+    for (int o = 1; o < kManThreads; o <<= 1) {
+      uint32_t x = (tid >= o) ? s_scan[tid - o] : 0;
+      __syncthreads();
+      s_scan[tid] += x;
+      __syncthreads();
+    }
+    uint32_t incl = s_scan[tid];
+    uint32_t ex = incl - (ns | (nf << 16));
+    uint32_t spos = nwhole + s_carry_single + (ex & 0xffff);
+    uint32_t fpos = nwhole + nsingle + s_carry_fail - nsingle + (ex >> 16);
+    if (k < B) {
+      for (uint32_t p = 0; p < N; p++) single_pos[k * N + p] = -1;
+      if (sat[k]) {
+        uint32_t sm = sel[k] & ~whole;
+        for (uint32_t p = 0; p < N; p++)
+          if (sm >> p & 1) {
+            single_pos[k * N + p] = (int32_t)spos;
+            kinds[spos] = 1;
+            m_nodes[spos] = p;
+            m_ops[spos] = k;
+            spos++;
+          }
+      } else {
+        // failure leaf: 0x00 || 0x46 || FailureRecord (messages.cpp:260-297)
+        uint8_t msg[192];
+        uint32_t L = 0;
+        msg[L++] = 0x00;
+        msg[L++] = 0x46;
+        for (int i = 0; i < 32; i++) msg[L++] = req_ids[32 * k + i];
+        msg[L++] = (uint8_t)(gid_len >> 24); msg[L++] = (uint8_t)(gid_len >> 16);
+        msg[L++] = (uint8_t)(gid_len >> 8);  msg[L++] = (uint8_t)gid_len;
+        for (uint32_t i = 0; i < gid_len && L < 150; i++) msg[L++] = gid[i];
+        for (int i = 0; i < 8; i++) msg[L++] = (uint8_t)(version >> (56 - 8 * i));
+        const char reason[] = "quorum unsatisfied";
+        const uint32_t rl = sizeof(reason) - 1;
+        msg[L++] = 0; msg[L++] = 0; msg[L++] = 0; msg[L++] = (uint8_t)rl;
+        for (uint32_t i = 0; i < rl; i++) msg[L++] = (uint8_t)reason[i];
+        sha256_local(msg, L, a_leaves + 32 * fpos);
+        kinds[fpos] = 2;
+        m_nodes[fpos] = 0;
+        m_ops[fpos] = k;
+      }
+    }
+    __syncthreads();
+    if (tid == kManThreads - 1) {
+      s_carry_single += incl & 0xffff;
+      s_carry_fail += incl >> 16;
+    }
+    __syncthreads();
+  }
+  if (tid == 0) *count = nwhole + nsingle + (s_carry_fail - nsingle);
+}
+
+void launch_attest_manifest(uint32_t B, uint32_t N, const uint32_t* sel,
+                            const uint8_t* sat, const uint8_t* r_roots,
+                            const uint8_t* req_ids, const uint8_t* gid,
+                            uint32_t gid_len, uint64_t version,
+                            uint8_t* a_leaves, int32_t* single_pos,
+                            uint8_t* kinds, uint32_t* m_nodes, uint32_t* m_ops,
+                            uint32_t* count, cudaStream_t st) {
+  if (gid_len > 100) throw InvalidArgument("group id too long for failure leaf");
+  attest_manifest_kernel<<<1, kManThreads, 0, st>>>(
+      B, N, sel, sat, r_roots, req_ids, gid, gid_len, version, a_leaves,
+      single_pos, kinds, m_nodes, m_ops, count);
+  CG_CHECK_LAUNCH();
+}
+
+// ---------------------------------------------------------- softmax/top-k
+// One warp per row: peak = first max, exp(x - peak) lane-parallel, the sum
+// taken sequentially by lane 0 in lane order (model.cpp:26-34 sums in index
+// order), then division. Top-k over the probabilities: k largest, ties to
+// the lower index (consistent with argmax/std::max_element).
+constexpr int kSmWarps = 4;
+constexpr int kSmMaxV = 1024;
+
+template <typename Tin>
+__global__ void __launch_bounds__(32 * kSmWarps) softmax_topk_kernel(
+    const Tin* __restrict__ in, uint64_t in_ld, uint32_t rows, uint32_t v,
+    int do_softmax, double* __restrict__ out, uint64_t out_ld, uint32_t k,
+    uint32_t* __restrict__ topi, double* __restrict__ topv) {
+  __shared__ double buf[kSmWarps][kSmMaxV];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t row = blockIdx.x * kSmWarps + w;
+  if (row >= rows) return;
+  const Tin* x = in + row * in_ld;
+  double* b = buf[w];
+  double peak = -INFINITY;
+  for (uint32_t i = lane; i < v; i += 32) {
+    double t = (double)x[i];
+    b[i] = t;
+    peak = (peak < t) ? t : peak;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    double p2 = __shfl_xor_sync(0xffffffffu, peak, o);
+    peak = (peak < p2) ? p2 : peak;
+  }
+  if (do_softmax) {
+    for (uint32_t i = lane; i < v; i += 32) b[i] = exp(__dsub_rn(b[i], peak));
+    __syncwarp();
+    double sum = 0.0;
+    if (lane == 0)
+      for (uint32_t i = 0; i < v; i++) sum = __dadd_rn(sum, b[i]);
+    sum = __shfl_sync(0xffffffffu, sum, 0);
+    for (uint32_t i = lane; i < v; i += 32) b[i] = __ddiv_rn(b[i], sum);
+    __syncwarp();
+  }
+  double* o = out + row * out_ld;
+  for (uint32_t i = lane; i < v; i += 32) o[i] = b[i];
+  // top-k: lane-local candidates then warp arg-reduce, k rounds
+  uint32_t taken = 0;  // bit t: element lane + 32 t already chosen
+  for (uint32_t r = 0; r < k; r++) {
+    double bv = 0.0;
+    uint32_t bi = 0xffffffffu;
+    for (uint32_t t = 0; lane + 32 * t < v && t < 32; t++) {
+      if (taken >> t & 1) continue;
+      double y = b[lane + 32 * t];
+      if (bi == 0xffffffffu || bv < y) { bv = y; bi = lane + 32 * t; }
+    }
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) {
+      double ov = __shfl_xor_sync(0xffffffffu, bv, s);
+      uint32_t oi = __shfl_xor_sync(0xffffffffu, bi, s);
+      bool take = (oi != 0xffffffffu) &&
+                  (bi == 0xffffffffu || bv < ov || (!(ov < bv) && oi < bi));
+      if (take) { bv = ov; bi = oi; }
+    }
+    if (bi != 0xffffffffu && (bi & 31) == (uint32_t)lane) taken |= 1u << (bi >> 5);
+    if (lane == 0) {
+      topi[row * k + r] = bi;
+      topv[row * k + r] = bv;
+    }
+  }
+}
+
+void launch_softmax_topk_f32(const float* in, uint64_t in_ld, uint32_t rows,
+                             uint32_t v, int do_softmax, double* out,
+                             uint64_t out_ld, uint32_t k, uint32_t* topi,
+                             double* topv, cudaStream_t st) {
+  if (v > kSmMaxV) throw InvalidArgument("softmax: output dim > 1024");
+  softmax_topk_kernel<float><<<(unsigned)ceil_div(rows, kSmWarps), 32 * kSmWarps, 0, st>>>(
+      in, in_ld, rows, v, do_softmax, out, out_ld, k, topi, topv);
+  CG_CHECK_LAUNCH();
+}
+
+void launch_softmax_topk_f64(const double* in, uint64_t in_ld, uint32_t rows,
+                             uint32_t v, int do_softmax, double* out,
+                             uint64_t out_ld, uint32_t k, uint32_t* topi,
+                             double* topv, cudaStream_t st) {
+  if (v > kSmMaxV) throw InvalidArgument("softmax: output dim > 1024");
+  softmax_topk_kernel<double><<<(unsigned)ceil_div(rows, kSmWarps), 32 * kSmWarps, 0, st>>>(
+      in, in_ld, rows, v, do_softmax, out, out_ld, k, topi, topv);
+  CG_CHECK_LAUNCH();
+}
+
+// ------------------------------------------------ LinearToyModel (fp64)
+// y[row] = b[row] + sum_col W[row,col] * x[col], accumulated in column order
+// without fused multiply-add (model.cpp:20-25 on x86-64 SSE2). One thread
+// per (input, row); a warp covers 32 rows of one input so x is broadcast.
+__global__ void __launch_bounds__(128) linear_f64_kernel(
+    const double* __restrict__ W, const double* __restrict__ bias,
+    const double* __restrict__ X, uint32_t B, uint32_t u, uint32_t v,
+    double* __restrict__ Y) {
+  uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t rows_pad = (v + 31) / 32 * 32;
+  uint32_t i = (uint32_t)(t / rows_pad), row = (uint32_t)(t % rows_pad);
+  if (i >= B || row >= v) return;
+  const double* w = W + (uint64_t)row * u;
+  const double* x = X + (uint64_t)i * u;
+  double acc = bias[row];
+#pragma unroll 8
+  for (uint32_t c = 0; c < u; c++) acc = __dadd_rn(acc, __dmul_rn(__ldg(w + c), __ldg(x + c)));
+  Y[(uint64_t)i * v + row] = acc;
+}
+
+void launch_linear_f64(const double* W, const double* b, const double* X,
+                       uint32_t B, uint32_t u, uint32_t v, double* Y,
+                       cudaStream_t st) {
+  uint64_t total = (uint64_t)B * ((v + 31) / 32 * 32);
+  linear_f64_kernel<<<(unsigned)ceil_div(total, 128), 128, 0, st>>>(W, b, X, B, u, v, Y);
+  CG_CHECK_LAUNCH();
+}
+
+}  // namespace cg

@@ -1,0 +1,33 @@
+// Host launchers for agree.cu.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace cg {
+
+void launch_select_quorum(const double* outs, uint64_t ps, uint64_t rs,
+                          const uint32_t* present, const double* eps,
+                          uint32_t R, uint32_t n, uint32_t f, uint32_t v,
+                          uint32_t metric, uint32_t* selected, double* diameter,
+                          uint8_t* satisfied, int8_t* status, int64_t* label,
+                          cudaStream_t st);
+void launch_attest_manifest(uint32_t B, uint32_t N, const uint32_t* sel,
+                            const uint8_t* sat, const uint8_t* r_roots,
+                            const uint8_t* req_ids, const uint8_t* gid,
+                            uint32_t gid_len, uint64_t version,
+                            uint8_t* a_leaves, int32_t* single_pos,
+                            uint8_t* kinds, uint32_t* m_nodes, uint32_t* m_ops,
+                            uint32_t* count, cudaStream_t st);
+void launch_softmax_topk_f32(const float* in, uint64_t in_ld, uint32_t rows,
+                             uint32_t v, int do_softmax, double* out,
+                             uint64_t out_ld, uint32_t k, uint32_t* topi,
+                             double* topv, cudaStream_t st);
+void launch_softmax_topk_f64(const double* in, uint64_t in_ld, uint32_t rows,
+                             uint32_t v, int do_softmax, double* out,
+                             uint64_t out_ld, uint32_t k, uint32_t* topi,
+                             double* topv, cudaStream_t st);
+void launch_linear_f64(const double* W, const double* b, const double* X,
+                       uint32_t B, uint32_t u, uint32_t v, double* Y,
+                       cudaStream_t st);
+
+}  // namespace cg

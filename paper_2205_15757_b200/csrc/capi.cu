@@ -1,0 +1,934 @@
+// The C-ABI (include/credo_gpu.h) and the host-side runtime behind it:
+// contexts, device buffers, model residency, the batch former's canonical
+// framing bytes, and the per-batch certification pipeline.
+//
+// Pipeline for one ExecutionBatch (reference: InferenceEngine::execute_batch
+// proj/src/engine.cpp:269-306 -> Coordinator::try_prepare's R tree
+// proj/src/coordinator.cpp:588-624 -> try_attest proj/src/coordinator.cpp:
+// 727-849), all on the device:
+//   side stream : request midstates  SHA(0x00||0x52||request)[whole blocks]
+//   main stream : N replica forwards -> softmax/top-k -> (join) ->
+//                 result-leaf tails -> select_quorum + label -> R roots ->
+//                 manifest (+whole/failure A leaves) -> single A leaves ->
+//                 A root
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/credo_gpu.h"
+#include "agree.cuh"
+#include "cnn.cuh"
+#include "common.cuh"
+#include "digest.cuh"
+
+namespace cg {
+
+static std::atomic<uint64_t> g_launches{0};
+uint64_t launch_counter_add(uint64_t n) { return g_launches += n; }
+
+struct CodecError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct DigestError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+// ------------------------------------------------------------- buffers
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  void ensure(size_t count) {
+    if (count <= n) return;
+    release();
+    CG_CUDA(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)));
+    n = count;
+  }
+};
+
+template <typename T>
+struct PinBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  ~PinBuf() {
+    if (p) cudaFreeHost(p);
+  }
+  void ensure(size_t count) {
+    if (count <= n) return;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    CG_CUDA(cudaMallocHost(&p, std::max<size_t>(count, 1) * sizeof(T)));
+    n = count;
+  }
+};
+
+// ------------------------------------------------------ canonical bytes
+// codec.hpp:28-84: u64 BE, u32 BE length prefixes, bool byte, raw fixed.
+struct Enc {
+  std::vector<uint8_t> b;
+  void u8(uint8_t v) { b.push_back(v); }
+  void u32(uint32_t v) {
+    for (int s = 24; s >= 0; s -= 8) b.push_back((uint8_t)(v >> s));
+  }
+  void u64(uint64_t v) {
+    for (int s = 56; s >= 0; s -= 8) b.push_back((uint8_t)(v >> s));
+  }
+  void f64(double d) {
+    uint64_t v;
+    std::memcpy(&v, &d, 8);
+    u64(v);
+  }
+  void raw(const uint8_t* p, size_t n) { b.insert(b.end(), p, p + n); }
+  void bytes(const uint8_t* p, size_t n) {
+    u32((uint32_t)n);
+    raw(p, n);
+  }
+};
+
+// Host arena for the framing bytes of chain jobs. A raw segment is placed
+// at an arena offset congruent to its message offset mod 4 so that every
+// whole message word inside it is one aligned 32-bit load on the device.
+struct Arena {
+  std::vector<uint8_t> b;
+  size_t add(const uint8_t* p, size_t n, uint64_t msg_off) {
+    while ((b.size() & 3) != (msg_off & 3)) b.push_back(0);
+    size_t o = b.size();
+    b.insert(b.end(), p, p + n);
+    return o;
+  }
+};
+
+}  // namespace cg
+
+using namespace cg;
+
+// ------------------------------------------------------------------ ctx
+struct cg_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = true;
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+  std::string err;
+  std::mutex mu;
+  // scratch for the standalone digest / agreement entry points
+  DevBuf<uint8_t> d_bytes, d_out;
+  DevBuf<ChainJob> d_jobs;
+  DevBuf<double> d_f64;
+  DevBuf<uint32_t> d_u32a, d_u32b;
+  DevBuf<uint64_t> d_u64a, d_u64b;
+  DevBuf<uint8_t> d_u8;
+  DevBuf<int8_t> d_i8;
+  DevBuf<int64_t> d_i64;
+  DevBuf<double> d_f64b;
+};
+
+struct cg_model {
+  cg_ctx* ctx = nullptr;
+  int kind = 0;  // 0 linear, 1 cnn
+  uint64_t u = 0, v = 0;
+  bool softmax = false;
+  uint8_t digest[32];
+  DevBuf<double> W, b;          // linear
+  std::unique_ptr<CnnModel> cnn;  // cnn
+};
+
+namespace {
+
+int fail(cg_ctx* ctx, int code, const std::string& msg) {
+  if (ctx) ctx->err = msg;
+  return code;
+}
+
+template <typename Fn>
+int guarded(cg_ctx* ctx, Fn&& fn) {
+  if (!ctx) return CG_EINVAL;
+  try {
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    ctx->err.clear();
+    CG_CUDA(cudaSetDevice(ctx->device));
+    return fn();
+  } catch (const InvalidArgument& e) {
+    return fail(ctx, CG_EINVAL, e.what());
+  } catch (const std::invalid_argument& e) {
+    return fail(ctx, CG_EINVAL, e.what());
+  } catch (const CodecError& e) {
+    return fail(ctx, CG_ECODEC, e.what());
+  } catch (const DigestError& e) {
+    return fail(ctx, CG_EDIGEST, e.what());
+  } catch (const CudaError& e) {
+    return fail(ctx, CG_ECUDA, e.what());
+  } catch (const std::exception& e) {
+    return fail(ctx, CG_ECUDA, e.what());
+  }
+}
+
+// SHA-256 of count host messages on the device (one chain job each).
+// prefix_byte >= 0 prepends that byte (merkle leaf domain 0x00).
+void device_sha256_many(cg_ctx* ctx, const uint8_t* buf, const uint64_t* off,
+                        const uint64_t* len, uint64_t count, int prefix_byte,
+                        uint8_t* out_host) {
+  if (count == 0) return;
+  Arena ar;
+  std::vector<size_t> pos(count), pre(count);
+  const uint8_t pb = (uint8_t)prefix_byte;
+  for (uint64_t i = 0; i < count; i++) {
+    uint64_t moff = 0;
+    if (prefix_byte >= 0) {
+      pre[i] = ar.add(&pb, 1, 0);
+      moff = 1;
+    }
+    pos[i] = ar.add(buf + off[i], len[i], moff);
+  }
+  ctx->d_bytes.ensure(ar.b.size() + 16);
+  ctx->d_out.ensure(32 * count);
+  ctx->d_jobs.ensure(count);
+  std::vector<ChainJob> jobs(count);
+  const uint64_t base = (uint64_t)ctx->d_bytes.p;
+  for (uint64_t i = 0; i < count; i++) {
+    ChainJob& j = jobs[i];
+    std::memset(&j, 0, sizeof j);
+    uint64_t moff = 0;
+    if (prefix_byte >= 0) {
+      j.seg[j.nseg++] = ChainSeg{base + pre[i], 0, 1, kSegRaw, 0};
+      moff = 1;
+    }
+    if (len[i]) j.seg[j.nseg++] = ChainSeg{base + pos[i], moff, len[i], kSegRaw, 0};
+    j.final_ = 1;
+    j.total_len = moff + len[i];
+    j.blk_begin = 0;
+    j.blk_end = (j.total_len + 9 + 63) / 64;
+    j.digest_out = (uint64_t)(ctx->d_out.p + 32 * i);
+  }
+  CG_CUDA(cudaMemcpyAsync(ctx->d_bytes.p, ar.b.data(), ar.b.size(),
+                          cudaMemcpyHostToDevice, ctx->stream));
+  CG_CUDA(cudaMemcpyAsync(ctx->d_jobs.p, jobs.data(), count * sizeof(ChainJob),
+                          cudaMemcpyHostToDevice, ctx->stream));
+  launch_chain_jobs(ctx->d_jobs.p, (uint32_t)count, ctx->stream);
+  CG_CUDA(cudaMemcpyAsync(out_host, ctx->d_out.p, 32 * count,
+                          cudaMemcpyDeviceToHost, ctx->stream));
+  CG_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+void check_model_digest(cg_ctx* ctx, const uint8_t* file, uint64_t len,
+                        const uint8_t digest[32]) {
+  uint8_t got[32];
+  uint64_t off = 0;
+  device_sha256_many(ctx, file, &off, &len, 1, -1, got);
+  if (std::memcmp(got, digest, 32) != 0)
+    throw DigestError("model file does not match its weights digest");
+}
+
+}  // namespace
+
+extern "C" {
+
+int cg_ctx_create(int device, cg_ctx** out) {
+  if (!out) return CG_EINVAL;
+  *out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev)
+    return CG_ENOTSUP;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return CG_ECUDA;
+  if (prop.major != 10 || prop.minor != 0) return CG_ENOTSUP;  // sm_100a only
+  auto* c = new cg_ctx();
+  c->device = device;
+  if (cudaSetDevice(device) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_a, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_b, cudaEventDisableTiming) != cudaSuccess) {
+    delete c;
+    return CG_ECUDA;
+  }
+  *out = c;
+  return CG_OK;
+}
+
+void cg_ctx_destroy(cg_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaDeviceSynchronize();
+  if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+  if (ctx->side) cudaStreamDestroy(ctx->side);
+  if (ctx->ev_a) cudaEventDestroy(ctx->ev_a);
+  if (ctx->ev_b) cudaEventDestroy(ctx->ev_b);
+  delete ctx;
+}
+
+const char* cg_last_error(const cg_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int cg_ctx_set_stream(cg_ctx* ctx, void* stream) {
+  return guarded(ctx, [&] {
+    if (ctx->own_stream && ctx->stream) CG_CUDA(cudaStreamDestroy(ctx->stream));
+    ctx->stream = (cudaStream_t)stream;
+    ctx->own_stream = false;
+    return CG_OK;
+  });
+}
+
+void* cg_ctx_stream(cg_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+
+int cg_ctx_synchronize(cg_ctx* ctx) {
+  return guarded(ctx, [&] {
+    CG_CUDA(cudaStreamSynchronize(ctx->stream));
+    CG_CUDA(cudaStreamSynchronize(ctx->side));
+    return CG_OK;
+  });
+}
+
+uint64_t cg_ctx_launch_count(const cg_ctx*) { return g_launches.load(); }
+
+int cg_sha256_batch(cg_ctx* ctx, const uint8_t* buf, const uint64_t* off,
+                    const uint64_t* len, uint64_t count, uint8_t* out) {
+  return guarded(ctx, [&] {
+    device_sha256_many(ctx, buf, off, len, count, -1, out);
+    return CG_OK;
+  });
+}
+
+int cg_leaf_hash_batch(cg_ctx* ctx, const uint8_t* buf, const uint64_t* off,
+                       const uint64_t* len, uint64_t count, uint8_t* out) {
+  return guarded(ctx, [&] {
+    device_sha256_many(ctx, buf, off, len, count, 0x00, out);
+    return CG_OK;
+  });
+}
+
+int cg_merkle_root_batch(cg_ctx* ctx, const uint8_t* leaf_hashes,
+                         const uint64_t* n_leaves, uint64_t ntrees,
+                         uint8_t* roots) {
+  return guarded(ctx, [&] {
+    if (ntrees == 0) return CG_OK;
+    uint64_t total = 0, mx = 0;
+    std::vector<uint64_t> off(ntrees);
+    for (uint64_t t = 0; t < ntrees; t++) {
+      if (n_leaves[t] == 0) throw InvalidArgument("merkle: empty leaf list");
+      off[t] = total;
+      total += n_leaves[t];
+      mx = std::max(mx, n_leaves[t]);
+    }
+    ctx->d_bytes.ensure(32 * total);
+    ctx->d_out.ensure(32 * ntrees);
+    CG_CUDA(cudaMemcpyAsync(ctx->d_bytes.p, leaf_hashes, 32 * total,
+                            cudaMemcpyHostToDevice, ctx->stream));
+    if (mx <= 8192) {
+      ctx->d_u64a.ensure(ntrees);
+      ctx->d_u64b.ensure(ntrees);
+      CG_CUDA(cudaMemcpyAsync(ctx->d_u64a.p, off.data(), 8 * ntrees,
+                              cudaMemcpyHostToDevice, ctx->stream));
+      CG_CUDA(cudaMemcpyAsync(ctx->d_u64b.p, n_leaves, 8 * ntrees,
+                              cudaMemcpyHostToDevice, ctx->stream));
+      launch_merkle_trees(ctx->d_bytes.p, ctx->d_u64a.p, ctx->d_u64b.p, nullptr,
+                          (uint32_t)ntrees, mx, ctx->d_out.p, ctx->stream);
+    } else {
+      DevBuf<uint8_t> scratch;
+      scratch.ensure(merkle_big_scratch_bytes(mx));
+      for (uint64_t t = 0; t < ntrees; t++)
+        launch_merkle_big(ctx->d_bytes.p + 32 * off[t], n_leaves[t], scratch.p,
+                          ctx->d_out.p + 32 * t, ctx->stream);
+      CG_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
+    CG_CUDA(cudaMemcpyAsync(roots, ctx->d_out.p, 32 * ntrees,
+                            cudaMemcpyDeviceToHost, ctx->stream));
+    CG_CUDA(cudaStreamSynchronize(ctx->stream));
+    return CG_OK;
+  });
+}
+
+int cg_select_quorum_batch(cg_ctx* ctx, const double* outs,
+                           const uint32_t* present, const double* eps,
+                           uint32_t R, uint32_t n, uint32_t f, uint32_t v,
+                           uint32_t metric, uint32_t* selected,
+                           double* diameter, uint8_t* satisfied,
+                           int8_t* status, int64_t* label) {
+  return guarded(ctx, [&] {
+    if (R == 0) return CG_OK;
+    if (n > 20 || n == 0) {
+      for (uint32_t r = 0; r < R; r++) {
+        if (status) status[r] = -1;
+        selected[r] = 0; diameter[r] = 0; satisfied[r] = 0;
+        if (label) label[r] = -1;
+      }
+      throw InvalidArgument("select_quorum: bad n/f or too many results");
+    }
+    const size_t nv = (size_t)R * n * v;
+    ctx->d_f64.ensure(nv);
+    ctx->d_f64b.ensure(R);
+    ctx->d_u32a.ensure(R);
+    ctx->d_u32b.ensure(R);
+    ctx->d_u8.ensure(R);
+    ctx->d_i8.ensure(R);
+    ctx->d_i64.ensure(R);
+    DevBuf<double> d_diam;
+    d_diam.ensure(R);
+    cudaStream_t st = ctx->stream;
+    CG_CUDA(cudaMemcpyAsync(ctx->d_f64.p, outs, nv * 8, cudaMemcpyHostToDevice, st));
+    CG_CUDA(cudaMemcpyAsync(ctx->d_f64b.p, eps, 8 * (size_t)R, cudaMemcpyHostToDevice, st));
+    if (present)
+      CG_CUDA(cudaMemcpyAsync(ctx->d_u32a.p, present, 4 * (size_t)R,
+                              cudaMemcpyHostToDevice, st));
+    launch_select_quorum(ctx->d_f64.p, v, (uint64_t)n * v,
+                         present ? ctx->d_u32a.p : nullptr, ctx->d_f64b.p, R, n,
+                         f, v, metric, ctx->d_u32b.p, d_diam.p, ctx->d_u8.p,
+                         ctx->d_i8.p, label ? ctx->d_i64.p : nullptr, st);
+    std::vector<int8_t> stat(R);
+    CG_CUDA(cudaMemcpyAsync(selected, ctx->d_u32b.p, 4 * (size_t)R, cudaMemcpyDeviceToHost, st));
+    CG_CUDA(cudaMemcpyAsync(diameter, d_diam.p, 8 * (size_t)R, cudaMemcpyDeviceToHost, st));
+    CG_CUDA(cudaMemcpyAsync(satisfied, ctx->d_u8.p, (size_t)R, cudaMemcpyDeviceToHost, st));
+    CG_CUDA(cudaMemcpyAsync(stat.data(), ctx->d_i8.p, (size_t)R, cudaMemcpyDeviceToHost, st));
+    if (label)
+      CG_CUDA(cudaMemcpyAsync(label, ctx->d_i64.p, 8 * (size_t)R, cudaMemcpyDeviceToHost, st));
+    CG_CUDA(cudaStreamSynchronize(st));
+    bool bad = false;
+    for (uint32_t r = 0; r < R; r++) {
+      if (status) status[r] = stat[r];
+      bad |= stat[r] != 0;
+    }
+    if (bad) throw InvalidArgument("select_quorum: invalid argument for some request");
+    return CG_OK;
+  });
+}
+
+// ---------------------------------------------------------------- models
+// LinearToyModel::from_file_bytes (proj/src/model.cpp:46-60).
+int cg_model_load_linear(cg_ctx* ctx, const uint8_t* file, uint64_t len,
+                         const uint8_t digest[32], cg_model** out) {
+  return guarded(ctx, [&] {
+    *out = nullptr;
+    auto rd_u64 = [&](uint64_t& pos) {
+      if (pos + 8 > len) throw CodecError("unexpected end of input");
+      uint64_t v = 0;
+      for (int i = 0; i < 8; i++) v = (v << 8) | file[pos++];
+      return v;
+    };
+    auto rd_u32 = [&](uint64_t& pos) {
+      if (pos + 4 > len) throw CodecError("unexpected end of input");
+      uint32_t v = 0;
+      for (int i = 0; i < 4; i++) v = (v << 8) | file[pos++];
+      return v;
+    };
+    uint64_t pos = 0;
+    uint64_t in = rd_u64(pos), outd = rd_u64(pos);
+    if (pos + 1 > len) throw CodecError("unexpected end of input");
+    uint8_t sm = file[pos++];
+    if (sm > 1) throw CodecError("invalid boolean");
+    auto rd_list = [&](std::vector<double>& dst) {
+      uint32_t n = rd_u32(pos);
+      if ((uint64_t)n * 8 > len - pos) throw CodecError("f64 list count exceeds buffer");
+      dst.resize(n);
+      for (uint32_t i = 0; i < n; i++) {
+        uint64_t bits = rd_u64(pos);
+        std::memcpy(&dst[i], &bits, 8);
+      }
+    };
+    std::vector<double> W, b;
+    rd_list(W);
+    rd_list(b);
+    if (pos != len) throw CodecError("trailing bytes after value");
+    if (in < 1 || outd < 1 || W.size() != in * outd || b.size() != outd)
+      throw CodecError("model file shape mismatch");
+    check_model_digest(ctx, file, len, digest);
+    auto m = std::make_unique<cg_model>();
+    m->ctx = ctx;
+    m->kind = 0;
+    m->u = in;
+    m->v = outd;
+    m->softmax = sm == 1;
+    std::memcpy(m->digest, digest, 32);
+    m->W.ensure(W.size());
+    m->b.ensure(b.size());
+    CG_CUDA(cudaMemcpy(m->W.p, W.data(), 8 * W.size(), cudaMemcpyHostToDevice));
+    CG_CUDA(cudaMemcpy(m->b.p, b.data(), 8 * b.size(), cudaMemcpyHostToDevice));
+    *out = m.release();
+    return CG_OK;
+  });
+}
+
+int cg_model_load_cnn(cg_ctx* ctx, const uint8_t* file, uint64_t len,
+                      const uint8_t digest[32], cg_model** out) {
+  return guarded(ctx, [&] {
+    *out = nullptr;
+    std::unique_ptr<CnnModel> cnn;
+    try {
+      cnn = CnnModel::from_file(file, len);
+    } catch (const std::invalid_argument& e) {
+      throw CodecError(e.what());
+    }
+    check_model_digest(ctx, file, len, digest);
+    cnn->upload(ctx->stream);
+    CG_CUDA(cudaStreamSynchronize(ctx->stream));
+    auto m = std::make_unique<cg_model>();
+    m->ctx = ctx;
+    m->kind = 1;
+    m->u = cnn->input_dim();
+    m->v = cnn->output_dim();
+    m->softmax = cnn->softmax();
+    std::memcpy(m->digest, digest, 32);
+    m->cnn = std::move(cnn);
+    *out = m.release();
+    return CG_OK;
+  });
+}
+
+void cg_model_free(cg_model* m) {
+  if (!m) return;
+  if (m->ctx) cudaSetDevice(m->ctx->device);
+  delete m;
+}
+
+int cg_model_dims(const cg_model* m, uint64_t* input_dim, uint64_t* output_dim) {
+  if (!m) return CG_EINVAL;
+  if (input_dim) *input_dim = m->u;
+  if (output_dim) *output_dim = m->v;
+  return CG_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+// Pre-softmax forward of one replica over B device-resident f64 inputs.
+// Linear: f64 into pre64. CNN: f32 logits into pre32.
+void replica_forward(cg_model* m, const double* d_in, uint32_t B,
+                     double* pre64, float* pre32, cudaStream_t st) {
+  if (m->kind == 0) {
+    launch_linear_f64(m->W.p, m->b.p, d_in, B, (uint32_t)m->u, (uint32_t)m->v,
+                      pre64, st);
+  } else {
+    m->cnn->forward(d_in, B, pre32, st);
+  }
+}
+
+}  // namespace
+
+extern "C" int cg_exec_run(cg_ctx* ctx, cg_model* m, const double* in,
+                           uint64_t B, uint64_t u, double* out, uint64_t v) {
+  return guarded(ctx, [&] {
+    if (!m || m->ctx != ctx) throw InvalidArgument("model from another context");
+    if (u != m->u) throw InvalidArgument("model input dimension mismatch");
+    if (v != m->v) throw InvalidArgument("model output dimension mismatch");
+    if (B == 0) return CG_OK;
+    cudaStream_t st = ctx->stream;
+    DevBuf<double> d_in, d_pre, d_out, d_topv;
+    DevBuf<float> d_pre32;
+    DevBuf<uint32_t> d_topi;
+    d_in.ensure(B * u);
+    d_pre.ensure(B * v);
+    d_out.ensure(B * v);
+    d_topi.ensure(B);
+    d_topv.ensure(B);
+    if (m->kind == 1) d_pre32.ensure(B * v);
+    CG_CUDA(cudaMemcpyAsync(d_in.p, in, 8 * B * u, cudaMemcpyHostToDevice, st));
+    replica_forward(m, d_in.p, (uint32_t)B, d_pre.p, d_pre32.p, st);
+    if (m->kind == 0)
+      launch_softmax_topk_f64(d_pre.p, v, (uint32_t)B, (uint32_t)v, m->softmax,
+                              d_out.p, v, 1, d_topi.p, d_topv.p, st);
+    else
+      launch_softmax_topk_f32(d_pre32.p, v, (uint32_t)B, (uint32_t)v, m->softmax,
+                              d_out.p, v, 1, d_topi.p, d_topv.p, st);
+    CG_CUDA(cudaMemcpyAsync(out, d_out.p, 8 * B * v, cudaMemcpyDeviceToHost, st));
+    CG_CUDA(cudaStreamSynchronize(st));
+    return CG_OK;
+  });
+}
+
+// ------------------------------------------------------------------ group
+struct cg_group {
+  cg_ctx* ctx = nullptr;
+  std::vector<cg_model*> models;
+  uint32_t N = 0, f = 0, metric = 0, maxB = 0, topk = 1;
+  double eps_default = 0;
+  std::string gid;
+  uint64_t version = 0;
+  uint64_t u = 0, v = 0;
+  // device state
+  DevBuf<double> d_in, d_pre64, d_outs, d_topv, d_eps, d_diam;
+  DevBuf<float> d_pre32;
+  DevBuf<uint32_t> d_topi, d_mid, d_sel, d_mnodes, d_mops, d_count;
+  DevBuf<uint8_t> d_arena, d_leaf, d_rroots, d_aleaf, d_aroot, d_sat, d_kinds,
+      d_reqids, d_gid;
+  DevBuf<int8_t> d_status;
+  DevBuf<int64_t> d_label;
+  DevBuf<int32_t> d_single_pos;
+  DevBuf<ChainJob> d_jobs;
+  DevBuf<uint64_t> d_toff, d_tlen;
+  // host staging (pinned) + guard event so a refill never races its H2D
+  PinBuf<uint8_t> h_arena;
+  PinBuf<ChainJob> h_jobs;
+  PinBuf<double> h_eps;
+  PinBuf<uint8_t> h_reqids;
+  cudaEvent_t ev_staged = nullptr, ev_prefix = nullptr, ev_inputs = nullptr;
+  bool staged_pending = false;
+  uint32_t last_B = 0;
+};
+
+namespace {
+
+void certify_enqueue(cg_group* g, const cg_request_batch* bt,
+                     const double* precomputed_outputs) {
+  cg_ctx* ctx = g->ctx;
+  const uint32_t B = bt->B, N = g->N;
+  const uint64_t u = bt->u, v = g->v;
+  if (B == 0) throw InvalidArgument("empty batch");
+  if (B > g->maxB) throw InvalidArgument("batch larger than group max_batch");
+  if (u != g->u) throw InvalidArgument("request input dimension mismatch");
+  cudaStream_t st = ctx->stream, side = ctx->side;
+
+  // ---- framing bytes + chain jobs (host) ----
+  if (g->staged_pending) CG_CUDA(cudaEventSynchronize(g->ev_staged));
+  Arena ar;
+  std::vector<ChainJob> jobs;
+  jobs.reserve((size_t)B * (1 + 2 * N));
+  const uint8_t* gid = (const uint8_t*)g->gid.data();
+  const uint32_t gl = (uint32_t)g->gid.size();
+  struct ReqLayout {
+    size_t h, h53, t;
+    uint64_t lenH, lenT, P;
+  };
+  std::vector<ReqLayout> rl(B);
+  std::vector<size_t> res_off((size_t)B * N), dig_off((size_t)B * N);
+  uint64_t lenRes = 0;
+  uint64_t nonce_pos = 0;
+  for (uint32_t k = 0; k < B; k++) {
+    const uint8_t* rid = bt->request_ids + 32 * k;
+    Enc H;
+    H.u8(0x00);
+    H.u8(0x52);
+    H.raw(rid, 32);
+    H.bytes(gid, gl);
+    H.u32((uint32_t)u);
+    Enc T;
+    bool he = bt->has_eps && bt->has_eps[k];
+    T.u8(he ? 1 : 0);
+    if (he) T.f64(bt->eps[k]);
+    T.raw(bt->client_pubs + 32 * k, 32);
+    T.bytes(bt->nonces + nonce_pos, bt->nonce_lens[k]);
+    nonce_pos += bt->nonce_lens[k];
+    T.raw(bt->client_sigs + 64 * k, 64);
+    ReqLayout& L = rl[k];
+    L.lenH = H.b.size();
+    L.lenT = T.b.size();
+    L.P = L.lenH + 8 * u + L.lenT;
+    L.h = ar.add(H.b.data(), H.b.size(), 0);
+    H.b[1] = 0x53;  // single_attest_leaf tag (messages.cpp:283-290)
+    L.h53 = ar.add(H.b.data(), H.b.size(), 0);
+    L.t = ar.add(T.b.data(), T.b.size(), L.lenH + 8 * u);
+    for (uint32_t p = 0; p < N; p++) {
+      Enc R;  // InferenceResult::encode up to the output list (domain.cpp:218-225)
+      R.raw(rid, 32);
+      R.u64(p);
+      R.bytes(gid, gl);
+      R.u64(g->version);
+      R.u32((uint32_t)v);
+      lenRes = R.b.size();
+      res_off[(size_t)k * N + p] = ar.add(R.b.data(), R.b.size(), L.P);
+      dig_off[(size_t)k * N + p] =
+          ar.add(g->models[p]->digest, 32, L.P + lenRes + 8 * v);
+    }
+  }
+  g->h_arena.ensure(ar.b.size() + 64);
+  std::memcpy(g->h_arena.p, ar.b.data(), ar.b.size());
+  g->d_arena.ensure(ar.b.size() + 64);
+  const uint64_t A = (uint64_t)g->d_arena.p;
+  const double* d_in = bt->inputs_on_device ? bt->inputs : g->d_in.p;
+  const uint64_t IN = (uint64_t)d_in;
+  auto seg_raw = [](uint64_t ptr, uint64_t off, uint64_t len) {
+    return ChainSeg{ptr, off, len, kSegRaw, 0};
+  };
+  auto seg_f64 = [](uint64_t ptr, uint64_t off, uint64_t len) {
+    return ChainSeg{ptr, off, len, kSegF64, 0};
+  };
+  // prefix jobs: request midstates
+  for (uint32_t k = 0; k < B; k++) {
+    const ReqLayout& L = rl[k];
+    ChainJob j;
+    std::memset(&j, 0, sizeof j);
+    j.seg[0] = seg_raw(A + L.h, 0, L.lenH);
+    j.seg[1] = seg_f64(IN + 8 * u * k, L.lenH, 8 * u);
+    j.seg[2] = seg_raw(A + L.t, L.lenH + 8 * u, L.lenT);
+    j.nseg = 3;
+    j.final_ = 0;
+    j.total_len = L.P;
+    j.blk_begin = 0;
+    j.blk_end = L.P / 64;
+    j.state_out = (uint64_t)(g->d_mid.p + 8 * k);
+    jobs.push_back(j);
+  }
+  const uint64_t OUT = (uint64_t)g->d_outs.p;
+  // tail jobs: result leaves H(0x00||0x52||req||res), provider-major output
+  for (uint32_t p = 0; p < N; p++)
+    for (uint32_t k = 0; k < B; k++) {
+      const ReqLayout& L = rl[k];
+      ChainJob j;
+      std::memset(&j, 0, sizeof j);
+      j.seg[0] = seg_raw(A + L.h, 0, L.lenH);
+      j.seg[1] = seg_f64(IN + 8 * u * k, L.lenH, 8 * u);
+      j.seg[2] = seg_raw(A + L.t, L.lenH + 8 * u, L.lenT);
+      j.seg[3] = seg_raw(A + res_off[(size_t)k * N + p], L.P, lenRes);
+      j.seg[4] = seg_f64(OUT + 8 * v * ((uint64_t)p * B + k), L.P + lenRes, 8 * v);
+      j.seg[5] = seg_raw(A + dig_off[(size_t)k * N + p], L.P + lenRes + 8 * v, 32);
+      j.nseg = 6;
+      j.final_ = 1;
+      j.total_len = L.P + lenRes + 8 * v + 32;
+      j.blk_begin = L.P / 64;
+      j.blk_end = (j.total_len + 9 + 63) / 64;
+      j.state_in = j.blk_begin ? (uint64_t)(g->d_mid.p + 8 * k) : 0;
+      j.digest_out = (uint64_t)(g->d_leaf.p + 32 * ((uint64_t)p * B + k));
+      jobs.push_back(j);
+    }
+  // single attestation leaves H(0x00||0x53||req||res): slot chosen on device
+  for (uint32_t k = 0; k < B; k++)
+    for (uint32_t p = 0; p < N; p++) {
+      const ReqLayout& L = rl[k];
+      ChainJob j;
+      std::memset(&j, 0, sizeof j);
+      j.seg[0] = seg_raw(A + L.h53, 0, L.lenH);
+      j.seg[1] = seg_f64(IN + 8 * u * k, L.lenH, 8 * u);
+      j.seg[2] = seg_raw(A + L.t, L.lenH + 8 * u, L.lenT);
+      j.seg[3] = seg_raw(A + res_off[(size_t)k * N + p], L.P, lenRes);
+      j.seg[4] = seg_f64(OUT + 8 * v * ((uint64_t)p * B + k), L.P + lenRes, 8 * v);
+      j.seg[5] = seg_raw(A + dig_off[(size_t)k * N + p], L.P + lenRes + 8 * v, 32);
+      j.nseg = 6;
+      j.final_ = 1;
+      j.total_len = L.P + lenRes + 8 * v + 32;
+      j.blk_begin = 0;
+      j.blk_end = (j.total_len + 9 + 63) / 64;
+      j.digest_out = (uint64_t)g->d_aleaf.p;
+      j.skip_flag = (uint64_t)(g->d_single_pos.p + (uint64_t)k * N + p);
+      jobs.push_back(j);
+    }
+  g->h_jobs.ensure(jobs.size());
+  std::memcpy(g->h_jobs.p, jobs.data(), jobs.size() * sizeof(ChainJob));
+  g->h_eps.ensure(B);
+  g->h_reqids.ensure(32 * (size_t)B);
+  for (uint32_t k = 0; k < B; k++)
+    g->h_eps.p[k] = (bt->has_eps && bt->has_eps[k]) ? bt->eps[k] : g->eps_default;
+  std::memcpy(g->h_reqids.p, bt->request_ids, 32 * (size_t)B);
+  g->d_jobs.ensure(jobs.size());
+
+  // ---- uploads (main stream) ----
+  CG_CUDA(cudaMemcpyAsync(g->d_arena.p, g->h_arena.p, ar.b.size(),
+                          cudaMemcpyHostToDevice, st));
+  CG_CUDA(cudaMemcpyAsync(g->d_jobs.p, g->h_jobs.p, jobs.size() * sizeof(ChainJob),
+                          cudaMemcpyHostToDevice, st));
+  CG_CUDA(cudaMemcpyAsync(g->d_eps.p, g->h_eps.p, 8 * (size_t)B,
+                          cudaMemcpyHostToDevice, st));
+  CG_CUDA(cudaMemcpyAsync(g->d_reqids.p, g->h_reqids.p, 32 * (size_t)B,
+                          cudaMemcpyHostToDevice, st));
+  std::vector<uint64_t> toff(N), tlen(N, B);
+  for (uint32_t p = 0; p < N; p++) toff[p] = (uint64_t)p * B;
+  CG_CUDA(cudaMemcpyAsync(g->d_toff.p, toff.data(), 8 * N, cudaMemcpyHostToDevice, st));
+  CG_CUDA(cudaMemcpyAsync(g->d_tlen.p, tlen.data(), 8 * N, cudaMemcpyHostToDevice, st));
+  if (!bt->inputs_on_device)
+    CG_CUDA(cudaMemcpyAsync(g->d_in.p, bt->inputs, 8 * u * B,
+                            cudaMemcpyHostToDevice, st));
+  CG_CUDA(cudaEventRecord(g->ev_staged, st));
+  g->staged_pending = true;
+
+  // ---- side stream: request midstates, concurrent with the forwards ----
+  CG_CUDA(cudaStreamWaitEvent(side, g->ev_staged, 0));
+  launch_chain_jobs(g->d_jobs.p, B, side);
+  CG_CUDA(cudaEventRecord(g->ev_prefix, side));
+
+  // ---- main stream: replica forwards + softmax/top-k ----
+  if (precomputed_outputs) {
+    // agreement/digest-only mode (C5): N × B × v outputs supplied by the host
+    CG_CUDA(cudaMemcpyAsync(g->d_outs.p, precomputed_outputs,
+                            8 * (size_t)N * B * v, cudaMemcpyHostToDevice, st));
+  }
+  for (uint32_t p = 0; p < N && !precomputed_outputs; p++) {
+    cg_model* m = g->models[p];
+    double* outs = g->d_outs.p + (uint64_t)p * B * v;
+    uint32_t* ti = g->d_topi.p + (uint64_t)p * B * g->topk;
+    double* tv = g->d_topv.p + (uint64_t)p * B * g->topk;
+    replica_forward(m, d_in, B, g->d_pre64.p, g->d_pre32.p, st);
+    if (m->kind == 0)
+      launch_softmax_topk_f64(g->d_pre64.p, v, B, (uint32_t)v, m->softmax, outs,
+                              v, g->topk, ti, tv, st);
+    else
+      launch_softmax_topk_f32(g->d_pre32.p, v, B, (uint32_t)v, m->softmax, outs,
+                              v, g->topk, ti, tv, st);
+  }
+  CG_CUDA(cudaStreamWaitEvent(st, g->ev_prefix, 0));
+  // result leaves (tails from the shared request midstate)
+  launch_chain_jobs(g->d_jobs.p + B, N * B, st);
+  // agreement + label vote
+  launch_select_quorum(g->d_outs.p, (uint64_t)B * v, v, nullptr, g->d_eps.p, B,
+                       N, g->f, (uint32_t)v, g->metric, g->d_sel.p, g->d_diam.p,
+                       g->d_sat.p, g->d_status.p, g->d_label.p, st);
+  // per-provider R roots
+  launch_merkle_trees(g->d_leaf.p, g->d_toff.p, g->d_tlen.p, nullptr, N, B,
+                      g->d_rroots.p, st);
+  // attestation manifest, whole/failure A leaves, then single A leaves
+  launch_attest_manifest(B, N, g->d_sel.p, g->d_sat.p, g->d_rroots.p,
+                         g->d_reqids.p, g->d_gid.p, gl, g->version,
+                         g->d_aleaf.p, g->d_single_pos.p, g->d_kinds.p,
+                         g->d_mnodes.p, g->d_mops.p, g->d_count.p, st);
+  launch_chain_jobs(g->d_jobs.p + B + (uint64_t)N * B, N * B, st);
+  launch_merkle_trees(g->d_aleaf.p, nullptr, nullptr, g->d_count.p, 1,
+                      (uint64_t)N * B + B + N, g->d_aroot.p, st);
+  g->last_B = B;
+}
+
+void certify_fetch(cg_group* g, cg_certify_out* o) {
+  cudaStream_t st = g->ctx->stream;
+  const uint32_t B = g->last_B, N = g->N;
+  const uint64_t v = g->v;
+  auto d2h = [&](void* dst, const void* src, size_t n) {
+    if (dst) CG_CUDA(cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToHost, st));
+  };
+  std::vector<int8_t> status(B);
+  uint32_t count = 0;
+  d2h(status.data(), g->d_status.p, B);
+  d2h(&count, g->d_count.p, 4);
+  d2h(o->selected, g->d_sel.p, 4 * (size_t)B);
+  d2h(o->diameter, g->d_diam.p, 8 * (size_t)B);
+  d2h(o->satisfied, g->d_sat.p, B);
+  d2h(o->label, g->d_label.p, 8 * (size_t)B);
+  d2h(o->r_roots, g->d_rroots.p, 32 * (size_t)N);
+  d2h(o->a_root, g->d_aroot.p, 32);
+  d2h(o->leaf_hashes, g->d_leaf.p, 32 * (size_t)N * B);
+  d2h(o->outputs, g->d_outs.p, 8 * (size_t)N * B * v);
+  d2h(o->topk_idx, g->d_topi.p, 4 * (size_t)N * B * g->topk);
+  d2h(o->topk_val, g->d_topv.p, 8 * (size_t)N * B * g->topk);
+  CG_CUDA(cudaStreamSynchronize(st));
+  if (o->manifest_len) *o->manifest_len = count;
+  d2h(o->manifest_kind, g->d_kinds.p, count);
+  d2h(o->manifest_node, g->d_mnodes.p, 4 * (size_t)count);
+  d2h(o->manifest_op, g->d_mops.p, 4 * (size_t)count);
+  d2h(o->a_leaf_hashes, g->d_aleaf.p, 32 * (size_t)count);
+  CG_CUDA(cudaStreamSynchronize(st));
+  for (uint32_t k = 0; k < B; k++)
+    if (status[k] != 0) throw InvalidArgument("select_quorum: invalid argument");
+}
+
+}  // namespace
+
+extern "C" {
+
+int cg_group_create(cg_ctx* ctx, cg_model* const* models, uint32_t N,
+                    uint32_t f, uint32_t metric, double default_eps,
+                    const char* group_id, uint64_t group_id_len,
+                    uint64_t version, uint32_t max_batch, uint32_t topk,
+                    cg_group** out) {
+  return guarded(ctx, [&] {
+    *out = nullptr;
+    if (N == 0 || N > 20 || f >= N) throw InvalidArgument("bad n/f");
+    if (max_batch == 0) throw InvalidArgument("max_batch must be >= 1");
+    if (topk == 0) topk = 1;
+    auto g = std::make_unique<cg_group>();
+    g->ctx = ctx;
+    g->N = N;
+    g->f = f;
+    g->metric = metric;
+    g->eps_default = default_eps;
+    g->gid.assign(group_id, group_id_len);
+    g->version = version;
+    g->maxB = max_batch;
+    g->topk = topk;
+    for (uint32_t p = 0; p < N; p++) {
+      if (!models[p] || models[p]->ctx != ctx) throw InvalidArgument("bad model");
+      g->models.push_back(models[p]);
+    }
+    g->u = models[0]->u;
+    g->v = models[0]->v;
+    for (auto* m : g->models)
+      if (m->u != g->u || m->v != g->v)
+        throw InvalidArgument("models disagree on dimensions");
+    if (g->v > 1024) throw InvalidArgument("output dimension > 1024");
+    const uint64_t B = max_batch, v = g->v;
+    g->d_in.ensure(B * g->u);
+    g->d_pre64.ensure(B * v);
+    g->d_pre32.ensure(B * v);
+    g->d_outs.ensure((uint64_t)N * B * v);
+    g->d_topi.ensure((uint64_t)N * B * topk);
+    g->d_topv.ensure((uint64_t)N * B * topk);
+    g->d_eps.ensure(B);
+    g->d_diam.ensure(B);
+    g->d_mid.ensure(8 * B);
+    g->d_sel.ensure(B);
+    const uint64_t amax = (uint64_t)N * B + B + N;
+    g->d_mnodes.ensure(amax);
+    g->d_mops.ensure(amax);
+    g->d_kinds.ensure(amax);
+    g->d_count.ensure(1);
+    g->d_leaf.ensure(32 * (uint64_t)N * B);
+    g->d_rroots.ensure(32 * (uint64_t)N);
+    g->d_aleaf.ensure(32 * amax);
+    g->d_aroot.ensure(32);
+    g->d_sat.ensure(B);
+    g->d_status.ensure(B);
+    g->d_label.ensure(B);
+    g->d_single_pos.ensure((uint64_t)N * B);
+    g->d_reqids.ensure(32 * B);
+    g->d_toff.ensure(N);
+    g->d_tlen.ensure(N);
+    g->d_gid.ensure(g->gid.size() + 1);
+    CG_CUDA(cudaMemcpy(g->d_gid.p, g->gid.data(), g->gid.size(), cudaMemcpyHostToDevice));
+    CG_CUDA(cudaEventCreateWithFlags(&g->ev_staged, cudaEventDisableTiming));
+    CG_CUDA(cudaEventCreateWithFlags(&g->ev_prefix, cudaEventDisableTiming));
+    CG_CUDA(cudaEventCreateWithFlags(&g->ev_inputs, cudaEventDisableTiming));
+    for (auto* m : g->models)
+      if (m->kind == 1) m->cnn->reserve(max_batch);
+    *out = g.release();
+    return CG_OK;
+  });
+}
+
+void cg_group_free(cg_group* g) {
+  if (!g) return;
+  cudaSetDevice(g->ctx->device);
+  cudaStreamSynchronize(g->ctx->stream);
+  cudaStreamSynchronize(g->ctx->side);
+  if (g->ev_staged) cudaEventDestroy(g->ev_staged);
+  if (g->ev_prefix) cudaEventDestroy(g->ev_prefix);
+  if (g->ev_inputs) cudaEventDestroy(g->ev_inputs);
+  delete g;
+}
+
+int cg_certify_batch(cg_group* g, const cg_request_batch* batch,
+                     cg_certify_out* out) {
+  if (!g || !batch) return CG_EINVAL;
+  return guarded(g->ctx, [&] {
+    certify_enqueue(g, batch, nullptr);
+    if (out) certify_fetch(g, out);
+    return CG_OK;
+  });
+}
+
+int cg_certify_outputs(cg_group* g, const cg_request_batch* batch,
+                       const double* outputs, cg_certify_out* out) {
+  if (!g || !batch || !outputs) return CG_EINVAL;
+  return guarded(g->ctx, [&] {
+    certify_enqueue(g, batch, outputs);
+    if (out) certify_fetch(g, out);
+    return CG_OK;
+  });
+}
+
+int cg_group_fetch(cg_group* g, cg_certify_out* out) {
+  if (!g || !out) return CG_EINVAL;
+  return guarded(g->ctx, [&] {
+    certify_fetch(g, out);
+    return CG_OK;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,43 @@
+// Shared helpers for the credo B200 kernels (sm_100a only).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <stdexcept>
+#include <string>
+
+namespace cg {
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct InvalidArgument : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+
+#define CG_CUDA(call)                                                        \
+  do {                                                                       \
+    cudaError_t e_ = (call);                                                 \
+    if (e_ != cudaSuccess)                                                   \
+      throw ::cg::CudaError(std::string(#call) + ": " +                      \
+                            cudaGetErrorString(e_) + " @" + __FILE__ + ":" + \
+                            std::to_string(__LINE__));                       \
+  } while (0)
+
+// Every kernel launch site goes through CG_CHECK_LAUNCH, which also counts
+// the launch (reported as gpu_launches by bench.py).
+uint64_t launch_counter_add(uint64_t n);
+#define CG_CHECK_LAUNCH()              \
+  do {                                 \
+    CG_CUDA(cudaGetLastError());       \
+    ::cg::launch_counter_add(1);       \
+  } while (0)
+
+constexpr int kNumSMs = 148;
+
+__host__ __device__ inline uint64_t ceil_div(uint64_t a, uint64_t b) {
+  return (a + b - 1) / b;
+}
+
+}  // namespace cg

@@ -1,0 +1,168 @@
+// Certificate-digest kernels: SHA-256 chain jobs (request midstates, result
+// leaves, single-attestation leaves, flat message batches) and Merkle roots.
+//
+// Reference: crypto::hash (proj/src/crypto.cpp:22-39), merkle::leaf_hash /
+// Tree::build (proj/src/merkle.cpp:14-67), leaf constructions
+// (proj/src/messages.cpp:204-341).
+#include "digest.cuh"
+#include "sha256.cuh"
+
+namespace cg {
+
+// One thread per job. Latency-bound by design: a job is a Merkle-Damgard
+// chain, so parallelism comes from the number of jobs (requests × providers),
+// never from splitting a message. 32 jobs per warp, 2 warps per CTA keeps
+// chains spread over many SMs (each chain runs at the single-warp issue rate).
+__global__ void __launch_bounds__(64) chain_jobs_kernel(const ChainJob* jobs,
+                                                        uint32_t n) {
+  uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const ChainJob& j = jobs[t];
+  uint64_t digest_out = j.digest_out;
+  if (j.skip_flag) {  // slot assigned on device (single attestation leaves)
+    int32_t pos = *reinterpret_cast<const int32_t*>(j.skip_flag);
+    if (pos < 0) return;
+    digest_out += 32ull * (uint32_t)pos;
+  }
+  run_chain_job(j, digest_out);
+}
+
+void launch_chain_jobs(const ChainJob* d_jobs, uint32_t n, cudaStream_t st) {
+  if (n == 0) return;
+  const int tpb = 64;
+  chain_jobs_kernel<<<(unsigned)ceil_div(n, tpb), tpb, 0, st>>>(d_jobs, n);
+  CG_CHECK_LAUNCH();
+}
+
+// ---------------------------------------------------------------------------
+// Merkle roots. One CTA per tree; the level array lives in shared memory.
+// Tree t has leaves leaf[off[t] .. off[t]+len[t]) (32-byte digests), or a
+// device-resident count when count_dev != nullptr (the A tree, whose size the
+// attestation manifest decides on device).
+constexpr int kMerkleSmemLeaves = 8192;
+
+__global__ void __launch_bounds__(256) merkle_tree_kernel(
+    const uint8_t* __restrict__ leaves, const uint64_t* __restrict__ off,
+    const uint64_t* __restrict__ len, const uint32_t* __restrict__ count_dev,
+    uint64_t n_const, uint8_t* __restrict__ roots) {
+  extern __shared__ __align__(16) uint8_t sm[];  // (n/2 + 1) × 32 bytes
+  const uint32_t t = blockIdx.x;
+  uint64_t n = count_dev ? count_dev[t] : (len ? len[t] : n_const);
+  const uint8_t* L = leaves + 32 * (off ? off[t] : 0);
+  uint8_t* out = roots + 32 * t;
+  if (n == 0) {  // Tree::build throws on an empty list; the caller checks.
+    if (threadIdx.x < 8) reinterpret_cast<uint32_t*>(out)[threadIdx.x] = 0;
+    return;
+  }
+  if (n == 1) {
+    if (threadIdx.x < 8)
+      reinterpret_cast<uint32_t*>(out)[threadIdx.x] =
+          reinterpret_cast<const uint32_t*>(L)[threadIdx.x];
+    return;
+  }
+  // level 1 from global leaves
+  uint64_t m = (n + 1) / 2;
+  for (uint64_t i = threadIdx.x; i < m; i += blockDim.x) {
+    if (2 * i + 1 < n) {
+      sha256_internal_node(L + 64 * i, L + 64 * i + 32, sm + 32 * i);
+    } else {
+      const uint4* src = reinterpret_cast<const uint4*>(L + 64 * i);
+      uint4* dst = reinterpret_cast<uint4*>(sm + 32 * i);
+      dst[0] = src[0];
+      dst[1] = src[1];
+    }
+  }
+  __syncthreads();
+  n = m;
+  while (n > 1) {
+    m = (n + 1) / 2;
+    // in-place: node i reads 2i, 2i+1 and writes i; i <= 2i so process in
+    // two phases to avoid read-after-overwrite races.
+    uint4 tmp[2];
+    bool have = false;
+    uint64_t i = threadIdx.x;
+    // each thread handles at most m/blockDim.x nodes; stage via registers
+    for (uint64_t base = 0; base < m; base += blockDim.x) {
+      i = base + threadIdx.x;
+      have = i < m;
+      if (have) {
+        if (2 * i + 1 < n) {
+          uint8_t h[32];
+          sha256_internal_node(sm + 64 * i, sm + 64 * i + 32, h);
+          tmp[0] = reinterpret_cast<uint4*>(h)[0];
+          tmp[1] = reinterpret_cast<uint4*>(h)[1];
+        } else {
+          tmp[0] = reinterpret_cast<uint4*>(sm + 64 * i)[0];
+          tmp[1] = reinterpret_cast<uint4*>(sm + 64 * i)[1];
+        }
+      }
+      __syncthreads();
+      if (have) {
+        reinterpret_cast<uint4*>(sm + 32 * i)[0] = tmp[0];
+        reinterpret_cast<uint4*>(sm + 32 * i)[1] = tmp[1];
+      }
+      __syncthreads();
+    }
+    n = m;
+  }
+  if (threadIdx.x < 8)
+    reinterpret_cast<uint32_t*>(out)[threadIdx.x] =
+        reinterpret_cast<const uint32_t*>(sm)[threadIdx.x];
+}
+
+// One Merkle level in global memory for trees too big for one CTA.
+__global__ void merkle_level_kernel(const uint8_t* __restrict__ in, uint64_t n,
+                                    uint8_t* __restrict__ out) {
+  uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  uint64_t m = (n + 1) / 2;
+  if (i >= m) return;
+  if (2 * i + 1 < n) {
+    sha256_internal_node(in + 64 * i, in + 64 * i + 32, out + 32 * i);
+  } else {
+    const uint4* s = reinterpret_cast<const uint4*>(in + 64 * i);
+    uint4* d = reinterpret_cast<uint4*>(out + 32 * i);
+    d[0] = s[0];
+    d[1] = s[1];
+  }
+}
+
+void launch_merkle_trees(const uint8_t* d_leaves, const uint64_t* d_off,
+                         const uint64_t* d_len, const uint32_t* d_count,
+                         uint32_t ntrees, uint64_t max_leaves, uint8_t* d_roots,
+                         cudaStream_t st, uint64_t n_const) {
+  if (ntrees == 0) return;
+  if (max_leaves > kMerkleSmemLeaves)
+    throw InvalidArgument("merkle_tree: too many leaves for one CTA");
+  size_t smem = 32 * ((max_leaves + 1) / 2 + 1);
+  static bool attr_set = false;
+  if (!attr_set) {
+    CG_CUDA(cudaFuncSetAttribute(merkle_tree_kernel,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 32 * (kMerkleSmemLeaves / 2 + 1)));
+    attr_set = true;
+  }
+  merkle_tree_kernel<<<ntrees, 256, smem, st>>>(d_leaves, d_off, d_len,
+                                                d_count, n_const, d_roots);
+  CG_CHECK_LAUNCH();
+}
+
+size_t merkle_big_scratch_bytes(uint64_t n) { return 2 * 32 * ((n + 1) / 2 + 1); }
+
+void launch_merkle_big(const uint8_t* d_leaves, uint64_t n, uint8_t* d_scratch,
+                       uint8_t* d_root, cudaStream_t st) {
+  if (n == 0) throw InvalidArgument("merkle: empty leaf list");
+  uint8_t* bufs[2] = {d_scratch, d_scratch + 32 * ((n + 1) / 2 + 1)};
+  const uint8_t* in = d_leaves;
+  int which = 0;
+  while (n > kMerkleSmemLeaves) {
+    uint64_t m = (n + 1) / 2;
+    merkle_level_kernel<<<(unsigned)ceil_div(m, 256), 256, 0, st>>>(in, n, bufs[which]);
+    CG_CHECK_LAUNCH();
+    in = bufs[which];
+    which ^= 1;
+    n = m;
+  }
+  launch_merkle_trees(in, nullptr, nullptr, nullptr, 1, n, d_root, st, n);
+}
+
+}  // namespace cg

@@ -1,0 +1,20 @@
+// Host launchers for the digest kernels (digest.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "sha256.cuh"
+
+namespace cg {
+
+void launch_chain_jobs(const ChainJob* d_jobs, uint32_t n, cudaStream_t st);
+// ntrees trees; tree t = leaves [off[t], off[t]+len[t]) or count_dev[t].
+void launch_merkle_trees(const uint8_t* d_leaves, const uint64_t* d_off,
+                         const uint64_t* d_len, const uint32_t* d_count,
+                         uint32_t ntrees, uint64_t max_leaves, uint8_t* d_roots,
+                         cudaStream_t st, uint64_t n_const = 0);
+size_t merkle_big_scratch_bytes(uint64_t n);
+void launch_merkle_big(const uint8_t* d_leaves, uint64_t n, uint8_t* d_scratch,
+                       uint8_t* d_root, cudaStream_t st);
+
+}  // namespace cg

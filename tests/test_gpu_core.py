@@ -1,0 +1,207 @@
+"""GPU parity: SHA-256 / leaf / Merkle kernels, select_quorum + label vote,
+the fp64 LinearToyModel executor, and whole-batch certification — all through
+the C-ABI, bit-exact against the oracle and the reference's golden vectors."""
+import hashlib
+
+import numpy as np
+import pytest
+
+from conftest import golden, split_reqs
+
+pytestmark = pytest.mark.gpu
+
+
+def _msgs(g):
+    data, lens = g["data"].tobytes(), g["lens"]
+    out, off = [], 0
+    for n in lens:
+        out.append(data[off:off + int(n)])
+        off += int(n)
+    return out
+
+
+# ------------------------------------------------------------------ SHA-256
+def test_sha256_golden(ctx):
+    g = golden("sha256.npz")
+    msgs = _msgs(g)
+    got = ctx.hash_batch(msgs)
+    for m, d, want in zip(msgs, got, g["digests"]):
+        assert d == want.tobytes(), len(m)
+    assert ctx.hash(b"a" * 1000000) == g["million_a"].tobytes()
+
+
+def test_sha256_random_lengths(ctx, oracle):
+    rng = np.random.default_rng(1)
+    msgs = [rng.integers(0, 256, int(n), dtype=np.uint8).tobytes()
+            for n in rng.integers(0, 3000, 500)]
+    assert ctx.hash_batch(msgs) == [oracle.sha256(m) for m in msgs]
+
+
+def test_leaf_hash_and_merkle_golden(ctx):
+    g = golden("merkle.npz")
+    data, lens = g["leaf_data"].tobytes(), g["leaf_lens"]
+    leaves, off = [], 0
+    for n in lens:
+        leaves.append(data[off:off + int(n)])
+        off += int(n)
+    got = ctx.leaf_hash_batch(leaves)
+    assert got == [h.tobytes() for h in g["leaf_hashes"]]
+    trees, i = [], 0
+    for n in g["counts"]:
+        trees.append(got[i:i + int(n)])
+        i += int(n)
+    assert ctx.merkle_roots(trees) == [r.tobytes() for r in g["roots"]]
+
+
+def test_merkle_large_tree(ctx, oracle):
+    rng = np.random.default_rng(2)
+    for n in (8191, 8192, 8193, 20001):
+        leaves = [rng.integers(0, 256, 32, dtype=np.uint8).tobytes() for _ in range(n)]
+        assert ctx.merkle_roots([leaves]) == [oracle.merkle_root(leaves)]
+
+
+def test_merkle_empty_is_invalid(ctx):
+    from paper_2205_15757_b200 import InvalidArgument
+    with pytest.raises(InvalidArgument):
+        ctx.merkle_roots([[]])
+
+
+# --------------------------------------------------------------- agreement
+def test_select_quorum_golden(ctx):
+    g = golden("quorum.npz")
+    T = len(g["n"])
+    # group instances by (n, dim, metric, f) to batch them
+    keys = {}
+    for t in range(T):
+        keys.setdefault((int(g["n"][t]), int(g["dim"][t]), int(g["metric"][t]),
+                         int(g["f"][t])), []).append(t)
+    for (n, dim, metric, f), ts in keys.items():
+        outs = g["outs"][ts][:, :n, :dim]
+        r = ctx.select_quorum_batch(outs, n, f, metric, g["eps"][ts],
+                                    present=g["present"][ts])
+        assert np.array_equal(r["selected"], g["selected"][ts].astype(np.uint32))
+        assert np.array_equal(r["satisfied"], g["satisfied"][ts].astype(bool))
+        assert np.array_equal(r["diameter"], g["diameter"][ts])  # bit-exact
+        want_lab = np.where(g["satisfied"][ts] > 0, g["label"][ts], -1)
+        assert np.array_equal(r["label"], want_lab)
+
+
+def test_select_quorum_random_vs_oracle(ctx, oracle):
+    rng = np.random.default_rng(7)
+    for n, f, v in ((3, 1, 10), (4, 1, 1000), (8, 2, 1000), (7, 2, 3), (16, 5, 4)):
+        R = 300 if v < 1000 else 60
+        center = rng.uniform(0, 1, (R, 1, v))
+        outs = center + rng.uniform(-0.01, 0.01, (R, n, v))
+        shift = rng.random((R, n)) < 0.2
+        outs = outs + shift[..., None] * 3 * 0.05 / np.sqrt(v)
+        eps = np.full(R, 0.05 if v > 10 else 0.03)
+        r = ctx.select_quorum_batch(outs, n, f, 0, eps)
+        for k in range(R):
+            m, d, s = oracle.select_quorum(outs[k], list(range(n)), n, f, 0, eps[k])
+            assert (int(r["selected"][k]), float(r["diameter"][k]), bool(r["satisfied"][k])) == (m, d, s)
+            lab = oracle.ensemble_label(outs[k], m, f) if s else -1
+            assert int(r["label"][k]) == lab
+
+
+def test_select_quorum_pinned_and_errors(ctx):
+    from paper_2205_15757_b200 import EUCLIDEAN, InvalidArgument
+    # tests/test_distance.cpp:138-160
+    o = ctx.select_quorum({0: [1.00], 1: [1.01], 2: [1.02], 3: [5.0]}, 4, 1, EUCLIDEAN, 0.2)
+    assert o.satisfied and o.selected == {0, 1, 2}
+    o = ctx.select_quorum({i: [2.0] for i in range(4)}, 4, 1, EUCLIDEAN, 0.0)
+    assert o.satisfied and o.selected == {0, 1, 2, 3} and o.diameter == 0.0
+    o = ctx.select_quorum({0: [1.0], 1: [1.5], 2: [2.0], 3: [2.5]}, 4, 1, EUCLIDEAN, 0.2)
+    assert not o.satisfied and o.selected == set()
+    with pytest.raises(InvalidArgument):
+        ctx.select_quorum({0: [1.0], 1: [1.0]}, 4, 1, EUCLIDEAN, 1.0)
+
+
+# ---------------------------------------------------------- executor seam
+def test_linear_executor_bit_exact(ctx):
+    from oracle.oracle import parse_linear_model_file
+    from paper_2205_15757_b200 import CudaExecutor, DigestMismatch, Model
+    g = golden("c1_batch.npz")
+    ex = CudaExecutor(ctx)
+    for p in range(int(g["N"])):
+        m = Model.load_linear(ctx, g["files"][p].tobytes(), g["digests"][p].tobytes())
+        y = ex.run(m, g["inputs"])
+        assert np.array_equal(y, g["outputs"][p])  # LinearToyModel::run, fp64
+        m.free()
+    bad = bytearray(g["digests"][0].tobytes())
+    bad[0] ^= 1
+    with pytest.raises(DigestMismatch):
+        Model.load_linear(ctx, g["files"][0].tobytes(), bytes(bad))
+
+
+def test_linear_softmax_within_ulp(ctx, oracle):
+    from oracle.oracle import parse_linear_model_file
+    from paper_2205_15757_b200 import CudaExecutor, Model
+    g = golden("c1_batch.npz")
+    f = bytearray(g["files"][0].tobytes())
+    f[16] = 1  # softmax flag byte (model.cpp:38-46)
+    f = bytes(f)
+    m = Model.load_linear(ctx, f, hashlib.sha256(f).digest())
+    u, v, sm, W, b = parse_linear_model_file(f)
+    y = CudaExecutor(ctx).run(m, g["inputs"])
+    want = np.stack([oracle.linear_run(W, b, x, True) for x in g["inputs"]])
+    # exp() differs by <= 1 ulp between CUDA and glibc; stated tolerance 4 ulp
+    assert np.all(np.abs(y - want) <= 4 * np.spacing(want))
+
+
+# ------------------------------------------------------ whole-batch certify
+def _group(ctx, g, B):
+    from paper_2205_15757_b200 import EUCLIDEAN, Model, ModelGroup
+    models = [Model.load_linear(ctx, g["files"][p].tobytes(), g["digests"][p].tobytes())
+              for p in range(int(g["N"]))]
+    return ModelGroup(ctx, models, 1, EUCLIDEAN, float(g["eps"]),
+                      g["gid"].tobytes(), 1, max_batch=B, topk=3)
+
+
+def test_certify_batch_c1_bit_exact(ctx):
+    from paper_2205_15757_b200 import RequestBatch
+    g = golden("c1_batch.npz")
+    B = int(g["B"])
+    grp = _group(ctx, g, B)
+    batch = RequestBatch.from_encoded(split_reqs(g))
+    r = grp.certify(batch, want_outputs=True, want_leaves=True)
+    assert np.array_equal(r["outputs"], g["outputs"])
+    assert np.array_equal(r["leaf_hashes"], g["leaf_hashes"])
+    assert np.array_equal(r["selected"], g["honest_sel"].astype(np.uint32))
+    assert np.array_equal(r["diameter"], g["honest_diam"])
+    assert np.array_equal(r["satisfied"], g["honest_sat"].astype(bool))
+    assert np.array_equal(r["label"], g["honest_label"])
+    assert np.array_equal(r["r_roots"], g["honest_r_roots"])
+    assert np.array_equal(r["a_root"], g["honest_a_root"])
+    assert int(r["manifest_len"][0]) == int(g["honest_mlen"])
+    # top-1 of each replica output == argmax
+    assert np.array_equal(r["topk_idx"][..., 0], np.argmax(g["outputs"], axis=-1))
+
+
+@pytest.mark.parametrize("variant", ["honest", "partial_fault", "failure"])
+def test_certify_outputs_fault_variants(ctx, variant):
+    from paper_2205_15757_b200 import RequestBatch
+    g = golden("c1_batch.npz")
+    B = int(g["B"])
+    grp = _group(ctx, g, B)
+    batch = RequestBatch.from_encoded(split_reqs(g))
+    r = grp.certify_outputs(batch, g[f"{variant}_outputs"])
+    assert np.array_equal(r["selected"], g[f"{variant}_sel"].astype(np.uint32))
+    assert np.array_equal(r["satisfied"], g[f"{variant}_sat"].astype(bool))
+    assert np.array_equal(r["label"], g[f"{variant}_label"])
+    assert np.array_equal(r["r_roots"], g[f"{variant}_r_roots"])
+    assert int(r["manifest_len"][0]) == int(g[f"{variant}_mlen"])
+    assert np.array_equal(r["a_root"], g[f"{variant}_a_root"])
+
+
+def test_certify_batch_invariant(ctx):
+    """Batch == sequential (tests/test_engine.cpp:134-150): certifying a
+    request alone gives the same leaf hashes as inside the batch."""
+    from paper_2205_15757_b200 import RequestBatch
+    g = golden("c1_batch.npz")
+    B = int(g["B"])
+    grp = _group(ctx, g, B)
+    reqs = split_reqs(g)
+    full = grp.certify(RequestBatch.from_encoded(reqs), want_leaves=True)
+    for k in (0, 5, B - 1):
+        one = grp.certify(RequestBatch.from_encoded([reqs[k]]), want_leaves=True)
+        assert np.array_equal(one["leaf_hashes"][:, 0], full["leaf_hashes"][:, k])

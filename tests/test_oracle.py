@@ -1,0 +1,184 @@
+"""CPU: the plain-C oracle restatement pinned against the reference's own
+answers (golden fixtures generated from the compiled reference) and, where
+oracle/_ref was built, against the live reference."""
+import hashlib
+
+import numpy as np
+import pytest
+
+from conftest import golden, split_reqs
+
+
+def _msgs(g):
+    data, lens = g["data"].tobytes(), g["lens"]
+    out, off = [], 0
+    for n in lens:
+        out.append(data[off:off + int(n)])
+        off += int(n)
+    return out
+
+
+def test_sha256_kats(oracle):
+    # tests/test_codec.cpp:123-130 of the reference
+    assert oracle.sha256(b"").hex() == (
+        "e3b0c44298fc1c149afbf4c8996fb92427ae41e4649b934ca495991b7852b855")
+    assert oracle.sha256(b"abc").hex() == (
+        "ba7816bf8f01cfea414140de5dae2223b00361a396177a9cb410ff61f20015ad")
+
+
+def test_sha256_golden(oracle):
+    g = golden("sha256.npz")
+    for m, d in zip(_msgs(g), g["digests"]):
+        assert oracle.sha256(m) == d.tobytes()
+        assert hashlib.sha256(m).digest() == d.tobytes()
+    assert oracle.sha256(b"a" * 1000000) == g["million_a"].tobytes()
+
+
+def test_midstate_matches_streaming(oracle):
+    msg = bytes(range(256)) * 3
+    st = oracle.midstate(msg, 5)
+    assert st.shape == (8,)
+    # SHA of the message == compress(rest) from midstate: cross-check through
+    # oracle.sha256 of the whole message vs hashlib
+    assert oracle.sha256(msg) == hashlib.sha256(msg).digest()
+
+
+def test_merkle_golden(oracle):
+    g = golden("merkle.npz")
+    lh = g["leaf_hashes"]
+    data, lens = g["leaf_data"].tobytes(), g["leaf_lens"]
+    off = i = 0
+    for t, n in enumerate(g["counts"]):
+        leaves = []
+        for _ in range(int(n)):
+            leaf = data[off:off + int(lens[i])]
+            assert oracle.leaf_hash(leaf) == lh[i].tobytes()
+            leaves.append(lh[i].tobytes())
+            off += int(lens[i])
+            i += 1
+        assert oracle.merkle_root(leaves) == g["roots"][t].tobytes()
+    with pytest.raises(ValueError):
+        oracle.merkle_root([])
+
+
+def test_merkle_formulas(oracle):
+    # tests/test_merkle.cpp:51-69: 1-leaf root is the leaf hash; 2-leaf root
+    # is H(0x01 || L || R); promotion is not duplication (:147-152)
+    a, b, c = (oracle.leaf_hash(x) for x in (b"a", b"b", b"c"))
+    assert oracle.merkle_root([a]) == a
+    assert oracle.merkle_root([a, b]) == hashlib.sha256(b"\x01" + a + b).digest()
+    ab = hashlib.sha256(b"\x01" + a + b).digest()
+    assert oracle.merkle_root([a, b, c]) == hashlib.sha256(b"\x01" + ab + c).digest()
+    assert oracle.merkle_root([a, b, c]) != oracle.merkle_root([a, b, c, c])
+
+
+def test_select_quorum_golden(oracle):
+    g = golden("quorum.npz")
+    for t in range(len(g["n"])):
+        n, f, dim, metric = (int(g[k][t]) for k in ("n", "f", "dim", "metric"))
+        pres = int(g["present"][t])
+        idx = [i for i in range(n) if pres >> i & 1]
+        outs = g["outs"][t][idx][:, :dim]
+        mask, diam, sat = oracle.select_quorum(outs, idx, n, f, metric, float(g["eps"][t]))
+        assert mask == int(g["selected"][t]), t
+        assert sat == bool(g["satisfied"][t]), t
+        assert diam == float(g["diameter"][t]), t  # bit-exact
+        if sat:
+            lab = oracle.ensemble_label(g["outs"][t][:n, :dim], mask, f)
+            assert lab == int(g["label"][t]), t
+
+
+def test_select_quorum_errors(oracle):
+    # distance.cpp:141-165: fewer than N-f present, f >= n -> invalid_argument
+    with pytest.raises(ValueError):
+        oracle.select_quorum(np.ones((2, 1)), [0, 1], 4, 1, 0, 1.0)
+    with pytest.raises(ValueError):
+        oracle.select_quorum(np.ones((3, 1)), [0, 1, 2], 3, 3, 0, 1.0)
+
+
+def test_c1_golden_linear_and_leaves(oracle):
+    from oracle.oracle import parse_linear_model_file, parse_request
+    g = golden("c1_batch.npz")
+    N, B, v = int(g["N"]), int(g["B"]), int(g["v"])
+    reqs = split_reqs(g)
+    gid = g["gid"].tobytes()
+    for p in range(N):
+        u, v_, sm, W, b = parse_linear_model_file(g["files"][p].tobytes())
+        assert not sm and v_ == v
+        assert hashlib.sha256(g["files"][p].tobytes()).digest() == g["digests"][p].tobytes()
+        for k in range(B):
+            y = oracle.linear_run(W, b, g["inputs"][k], False)
+            assert np.array_equal(y, g["outputs"][p, k])  # bit-exact fp64
+    for k in range(B):
+        f = parse_request(reqs[k])
+        enc = oracle.request_encode(f["request_id"], f["group_id"], f["input"],
+                                    f["eps"], f["pub"], f["nonce"], f["sig"])
+        assert enc == reqs[k]
+        for p in range(N):
+            res = oracle.result_encode(f["request_id"], p, gid, 1,
+                                       g["outputs"][p, k], g["digests"][p].tobytes())
+            assert oracle.tagged_leaf_hash(0x52, enc, res) == g["leaf_hashes"][p, k].tobytes()
+
+
+@pytest.mark.parametrize("variant", ["honest", "partial_fault", "failure"])
+def test_c1_golden_certify(oracle, variant):
+    """Oracle restatement of the whole batch certification == reference."""
+    from oracle.oracle import parse_request
+    g = golden("c1_batch.npz")
+    N, B, eps = int(g["N"]), int(g["B"]), float(g["eps"])
+    gid = g["gid"].tobytes()
+    reqs = split_reqs(g)
+    outs = g[f"{variant}_outputs"]
+    sels, sats = [], []
+    for k in range(B):
+        f = parse_request(reqs[k])
+        e = f["eps"] if f["eps"] is not None else eps
+        mask, diam, sat = oracle.select_quorum(outs[:, k], list(range(N)), N, 1, 0, e)
+        assert mask == int(g[f"{variant}_sel"][k])
+        assert diam == float(g[f"{variant}_diam"][k])
+        assert sat == bool(g[f"{variant}_sat"][k])
+        lab = oracle.ensemble_label(outs[:, k], mask, 1) if sat else -1
+        assert lab == int(g[f"{variant}_label"][k])
+        sels.append(mask)
+        sats.append(sat)
+    # R roots from leaf hashes over this variant's outputs
+    leaves = {}
+    for p in range(N):
+        hs = []
+        for k in range(B):
+            f = parse_request(reqs[k])
+            res = oracle.result_encode(f["request_id"], p, gid, 1, outs[p, k],
+                                       g["digests"][p].tobytes())
+            hs.append(oracle.tagged_leaf_hash(0x52, reqs[k], res))
+            leaves[(k, p)] = res
+        assert oracle.merkle_root(hs) == g[f"{variant}_r_roots"][p].tobytes()
+    man = oracle.attest_manifest(sels, sats, N)
+    assert len(man) == int(g[f"{variant}_mlen"])
+    a_leaves = []
+    for kind, node, op in man:
+        if kind == 0:
+            a_leaves.append(oracle.leaf_hash(b"\x57" + g[f"{variant}_r_roots"][node].tobytes()))
+        elif kind == 1:
+            a_leaves.append(oracle.tagged_leaf_hash(0x53, reqs[op], leaves[(op, node)]))
+        else:
+            f = parse_request(reqs[op])
+            a_leaves.append(oracle.leaf_hash(oracle.failure_leaf(f["request_id"], gid, 1)))
+    assert oracle.merkle_root(a_leaves) == g[f"{variant}_a_root"].tobytes()
+
+
+def test_live_reference_cross_check(oracle):
+    from oracle.oracle import Reference
+    if not Reference.available():
+        pytest.skip("oracle/_ref not built here")
+    R = Reference()
+    rng = np.random.default_rng(5)
+    for _ in range(300):
+        n = int(rng.integers(3, 9))
+        f = max(1, (n - 1) // 3)
+        outs = rng.uniform(0, 1, (1, 7)) + rng.uniform(-0.05, 0.05, (n, 7)) * rng.choice([1, 40], (n, 1))
+        e = float(rng.uniform(0, 0.3))
+        assert oracle.select_quorum(outs, list(range(n)), n, f, 0, e) == \
+            R.select_quorum(outs, list(range(n)), n, f, 0, e)
+    for n in (0, 1, 63, 64, 65, 1000):
+        m = rng.integers(0, 256, n, dtype=np.uint8).tobytes()
+        assert oracle.sha256(m) == R.sha256(m)
