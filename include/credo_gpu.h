@@ -163,6 +163,15 @@ int cg_group_fetch(cg_group* g, cg_certify_out* out);
 int cg_certify_outputs(cg_group* g, const cg_request_batch* batch,
                        const double* outputs, cg_certify_out* out);
 
+/* ---- test hooks (not on the certified path) -----------------------------
+ * One tcgen05 conv-GEMM launch on host buffers (bf16 as uint16 bits). */
+int cg_dbg_conv_gemm(cg_ctx* ctx, const uint16_t* A, int rowsA,
+                     const uint16_t* B, int N, int Kc, int ntaps,
+                     const int* tap_off, const float* bias,
+                     const uint16_t* residual, int relu, int row_mode, int H,
+                     int W, int M, int rows_out, int out_f32, int BN, void* out,
+                     int max_ctas);
+
 #ifdef __cplusplus
 }
 #endif

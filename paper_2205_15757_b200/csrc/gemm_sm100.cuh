@@ -1,0 +1,58 @@
+// tcgen05 implicit-GEMM convolution for sm_100a.
+//
+//   D[m, n] = epi( sum_t sum_kb A[m + tap_off[t], kb] * B[n, t*Kc + kb] )
+//
+// A: bf16 activations, NHWC rows (row = pixel, K = channels, Kc % 64 == 0).
+//    A 3x3/stride-1 convolution runs over the zero-bordered ("padded") pixel
+//    grid so tap t is a constant row shift; TMA zero-fills rows outside the
+//    tensor. 1x1 convolutions and explicit im2col operands have one tap.
+// B: bf16 weights, [N, ntaps*Kc] K-major (BN folded).
+// epi: + bias[n] (+ residual) (ReLU) -> bf16 (or f32) with a row remap
+//    (identity / padded-grid -> compact / compact -> padded-grid interior).
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace cg {
+
+enum RowMode : int {
+  kRowIdentity = 0,     // out row = m
+  kRowPadToCompact = 1, // m on the (H+2)x(W+2) grid; interior -> compact row
+  kRowCompactToPad = 2, // m compact; written to the interior of the padded grid
+};
+
+struct ConvGemmArgs {
+  int M;           // GEMM rows (A row space)
+  int N;           // output channels
+  int Kc;          // channels per tap (multiple of 64)
+  int ntaps;       // 1 or 9
+  int tap_off[9];  // row shift per tap
+  const float* bias;                 // [N]
+  const __nv_bfloat16* residual;     // [rows_out, ld_res] or null
+  int ld_res;
+  void* out;                         // bf16 or f32 [rows_out, ld_out]
+  int ld_out;
+  int out_f32;
+  int relu;
+  int row_mode;
+  int H, W;                          // unpadded spatial dims (row remap)
+  int rows_out;                      // valid output rows (identity mode)
+};
+
+// One encoded operand (tensor map over a row-major bf16 [rows, cols] matrix
+// with a 64 x box_rows box and 128B swizzle).
+struct Operand {
+  CUtensorMap map;
+  const void* ptr = nullptr;
+  int rows = 0, cols = 0, box_rows = 0;
+};
+
+void make_operand(Operand& op, const void* ptr, int rows, int cols, int box_rows);
+
+// Launches the persistent warp-specialised kernel; BN in {64, 128, 256}.
+void launch_conv_gemm(const Operand& A, const Operand& B, const ConvGemmArgs& a,
+                      int BN, cudaStream_t st, int max_ctas = 0);
+
+}  // namespace cg

@@ -1,0 +1,119 @@
+"""GPU: the tcgen05/TMEM/TMA implicit-GEMM conv kernel against a plain fp32
+reference of the same op (torch on CPU, bf16-rounded operands).
+
+Tolerance: the kernel accumulates in fp32 (TMEM) and rounds the epilogue to
+bf16, so each element may differ from the fp32 reference by one bf16
+rounding: |got - ref| <= 2^-7 * |ref| + 1e-3."""
+import ctypes as C
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def bf16_bits(x: torch.Tensor) -> np.ndarray:
+    return x.to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16).copy()
+
+
+def run_gemm(ctx, A, Bw, N, Kc, ntaps, taps, bias, residual, relu, mode, H, W, M,
+             rows_out, out_f32, BN, max_ctas=0):
+    a = bf16_bits(A)
+    b = bf16_bits(Bw)
+    res = None if residual is None else bf16_bits(residual)
+    t = np.array(list(taps) + [0] * (9 - len(taps)), np.int32)
+    bias = np.ascontiguousarray(bias, np.float32)
+    out = np.zeros((rows_out, N), np.float32 if out_f32 else np.uint16)
+    rc = ctx.L.cg_dbg_conv_gemm(
+        ctx.h, a.ctypes.data_as(C.c_void_p), A.shape[0], b.ctypes.data_as(C.c_void_p),
+        N, Kc, ntaps, t.ctypes.data_as(C.c_void_p), bias.ctypes.data_as(C.c_void_p),
+        None if res is None else res.ctypes.data_as(C.c_void_p), relu, mode, H, W, M,
+        rows_out, out_f32, BN, out.ctypes.data_as(C.c_void_p), max_ctas)
+    assert rc == 0, ctx.L.cg_last_error(ctx.h)
+    if out_f32:
+        return torch.from_numpy(out)
+    return torch.from_numpy(out.view(np.int16)).view(torch.bfloat16).float()
+
+
+def close(got, ref):
+    err = (got - ref).abs()
+    lim = 2.0 ** -7 * ref.abs() + 1e-3
+    bad = (err > lim).sum().item()
+    assert bad == 0, f"{bad} mismatches, max err {err.max().item()}"
+
+
+def q(x):
+    return x.to(torch.bfloat16).float()
+
+
+@pytest.mark.parametrize("M,N,Kc,BN,relu,max_ctas", [
+    (300, 128, 256, 128, 1, 0), (128, 64, 64, 64, 0, 0), (1000, 512, 128, 256, 1, 0),
+    (2048, 256, 512, 128, 0, 3), (4096, 64, 576, 64, 1, 5), (777, 256, 64, 256, 0, 2)])
+def test_gemm_1x1(ctx, M, N, Kc, BN, relu, max_ctas):
+    g = torch.Generator().manual_seed(M + N)
+    A = torch.rand(M, Kc, generator=g) * 2 - 1
+    Bw = torch.rand(N, Kc, generator=g) * 2 - 1
+    bias = torch.rand(N, generator=g) - 0.5
+    got = run_gemm(ctx, A, Bw, N, Kc, 1, [0], bias, None, relu, 0, 0, 0, M, M, 0, BN, max_ctas)
+    ref = q(A) @ q(Bw).T + bias
+    if relu:
+        ref = ref.clamp_min(0)
+    close(got, ref)
+
+
+def test_gemm_residual_and_f32_tail(ctx):
+    g = torch.Generator().manual_seed(3)
+    M, N, Kc = 513, 256, 192
+    A = torch.rand(M, Kc, generator=g) * 2 - 1
+    Bw = torch.rand(N, Kc, generator=g) * 2 - 1
+    R = torch.rand(M, N, generator=g) * 2 - 1
+    bias = torch.rand(N, generator=g) - 0.5
+    got = run_gemm(ctx, A, Bw, N, Kc, 1, [0], bias, R, 1, 0, 0, 0, M, M, 0, 128)
+    close(got, (q(A) @ q(Bw).T + bias + q(R)).clamp_min(0))
+    # FC shape: N = 1000 (not a multiple of the tile), f32 logits
+    N = 1000
+    Bw = torch.rand(N, Kc, generator=g) * 2 - 1
+    bias = torch.rand(N, generator=g) - 0.5
+    got = run_gemm(ctx, A[:128], Bw, N, Kc, 1, [0], bias, None, 0, 0, 0, 0, 128, 128, 1, 128)
+    ref = q(A[:128]) @ q(Bw).T + bias
+    assert torch.allclose(got, ref, rtol=1e-4, atol=1e-3)
+
+
+@pytest.mark.parametrize("NB,H,C,Cout,BN", [(3, 7, 64, 128, 128), (2, 14, 128, 64, 64),
+                                            (2, 28, 64, 256, 256)])
+def test_conv3x3_padded_grid(ctx, NB, H, C, Cout, BN):
+    """3x3/stride-1/pad-1 conv as 9 row-shifted taps over the zero-bordered
+    grid (row mode PadToCompact) == torch conv2d."""
+    W = H
+    g = torch.Generator().manual_seed(H * C)
+    x = torch.rand(NB, C, H, W, generator=g) * 2 - 1
+    w = (torch.rand(Cout, C, 3, 3, generator=g) * 2 - 1) / 3
+    bias = torch.rand(Cout, generator=g) - 0.5
+    xp = torch.nn.functional.pad(q(x), (1, 1, 1, 1))            # NB,C,Hp,Wp
+    A = xp.permute(0, 2, 3, 1).reshape(-1, C)                   # padded NHWC rows
+    Wp = W + 2
+    taps = [(dr - 1) * Wp + (ds - 1) for dr in range(3) for ds in range(3)]
+    Bw = q(w).permute(0, 2, 3, 1).reshape(Cout, 9 * C)          # [Cout, (dr,ds,c)]
+    M = NB * (H + 2) * Wp
+    got = run_gemm(ctx, A, Bw, Cout, C, 9, taps, bias, None, 1, 1, H, W, M, NB * H * W, 0, BN)
+    ref = torch.nn.functional.conv2d(q(x), q(w), bias, padding=1).clamp_min(0)
+    ref = ref.permute(0, 2, 3, 1).reshape(-1, Cout)
+    close(got, ref)
+
+
+def test_compact_to_padded_interior(ctx):
+    NB, H, C, Cout = 2, 7, 64, 64
+    W, Wp = H, H + 2
+    g = torch.Generator().manual_seed(9)
+    A = torch.rand(NB * H * W, C, generator=g) * 2 - 1
+    Bw = torch.rand(Cout, C, generator=g) * 2 - 1
+    bias = torch.zeros(Cout)
+    rows_out = NB * (H + 2) * Wp
+    got = run_gemm(ctx, A, Bw, Cout, C, 1, [0], bias, None, 1, 2, H, W, NB * H * W,
+                   rows_out, 0, 64)
+    ref = (q(A) @ q(Bw).T).clamp_min(0).reshape(NB, H, W, Cout)
+    gp = got.reshape(NB, H + 2, Wp, Cout)
+    close(gp[:, 1:H + 1, 1:W + 1], ref)
+    assert gp[:, 0].abs().sum() == 0 and gp[:, H + 1].abs().sum() == 0
+    assert gp[:, :, 0].abs().sum() == 0 and gp[:, :, W + 1].abs().sum() == 0
