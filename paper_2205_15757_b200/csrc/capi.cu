@@ -569,6 +569,8 @@ struct cg_group {
   DevBuf<int32_t> d_single_pos;
   DevBuf<ChainJob> d_jobs;
   DevBuf<uint64_t> d_toff, d_tlen;
+  DevBuf<uint8_t> d_prep;  // shared CNN input operand
+  bool all_cnn = false;
   // host staging (pinned) + guard event so a refill never races its H2D
   PinBuf<uint8_t> h_arena;
   PinBuf<ChainJob> h_jobs;
@@ -753,12 +755,21 @@ void certify_enqueue(cg_group* g, const cg_request_batch* bt,
     CG_CUDA(cudaMemcpyAsync(g->d_outs.p, precomputed_outputs,
                             8 * (size_t)N * B * v, cudaMemcpyHostToDevice, st));
   }
+  // replica-independent input stage (CNN conv1 operand), once per batch
+  const void* prepped = nullptr;
+  if (!precomputed_outputs && g->all_cnn) {
+    g->models[0]->cnn->prepare_input(d_in, B, g->d_prep.p, st);
+    prepped = g->d_prep.p;
+  }
   for (uint32_t p = 0; p < N && !precomputed_outputs; p++) {
     cg_model* m = g->models[p];
     double* outs = g->d_outs.p + (uint64_t)p * B * v;
     uint32_t* ti = g->d_topi.p + (uint64_t)p * B * g->topk;
     double* tv = g->d_topv.p + (uint64_t)p * B * g->topk;
-    replica_forward(m, d_in, B, g->d_pre64.p, g->d_pre32.p, st);
+    if (m->kind == 1)
+      m->cnn->forward(d_in, B, g->d_pre32.p, st, prepped);
+    else
+      replica_forward(m, d_in, B, g->d_pre64.p, g->d_pre32.p, st);
     if (m->kind == 0)
       launch_softmax_topk_f64(g->d_pre64.p, v, B, (uint32_t)v, m->softmax, outs,
                               v, g->topk, ti, tv, st);
@@ -885,8 +896,12 @@ int cg_group_create(cg_ctx* ctx, cg_model* const* models, uint32_t N,
     CG_CUDA(cudaEventCreateWithFlags(&g->ev_staged, cudaEventDisableTiming));
     CG_CUDA(cudaEventCreateWithFlags(&g->ev_prefix, cudaEventDisableTiming));
     CG_CUDA(cudaEventCreateWithFlags(&g->ev_inputs, cudaEventDisableTiming));
-    for (auto* m : g->models)
+    g->all_cnn = true;
+    for (auto* m : g->models) {
       if (m->kind == 1) m->cnn->reserve(max_batch);
+      g->all_cnn = g->all_cnn && m->kind == 1;
+    }
+    if (g->all_cnn) g->d_prep.ensure(g->models[0]->cnn->prepared_bytes(max_batch));
     *out = g.release();
     return CG_OK;
   });

@@ -1,10 +1,604 @@
-// Placeholder until the tcgen05 forward lands.
+// ResNet (bottleneck, torchvision v1.5 layout) forward on the tcgen05
+// implicit-GEMM kernel. Activations are NHWC bf16; every convolution is one
+// conv_gemm launch with BN folded into the weights and bias/ReLU/residual
+// fused into the epilogue:
+//   1x1 conv           -> GEMM over compact pixel rows
+//   3x3 conv, stride 1 -> 9 row-shifted taps over a zero-bordered grid that
+//                         the preceding 1x1 conv writes directly (no im2col)
+//   3x3/1x1, stride 2  -> small gather kernel, then one-tap GEMM
+//   conv1 7x7/2        -> fused f64->bf16 im2col of the request input
+//   fc                 -> GEMM with f32 logits out
+#include <cuda_bf16.h>
+
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <map>
 #include <stdexcept>
 
 #include "cnn.cuh"
+#include "common.cuh"
+#include "gemm_sm100.cuh"
 
 namespace cg {
-std::unique_ptr<CnnModel> CnnModel::from_file(const uint8_t*, uint64_t) {
-  throw std::invalid_argument("cnn model files not supported yet");
+namespace {
+
+using bf16 = __nv_bfloat16;
+
+// ------------------------------------------------------------------ kernels
+// conv1 operand: f64 CHW image -> [B*Ho*Wo, Kp] bf16, K = (dr*7+ds)*3 + c,
+// stride 2, pad 3, zero beyond K = 147. Replica-independent.
+__global__ void conv1_im2col_kernel(const double* __restrict__ in, int B, int S,
+                                    int Ho, int Kp, bf16* __restrict__ out) {
+  const int chunks = Kp / 8;
+  size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  size_t row = t / chunks;
+  int ch = (int)(t - row * chunks);
+  if (row >= (size_t)B * Ho * Ho) return;
+  int n = (int)(row / (Ho * Ho)), rem = (int)(row - (size_t)n * Ho * Ho);
+  int ho = rem / Ho, wo = rem - ho * Ho;
+  __align__(16) bf16 v[8];
+#pragma unroll
+  for (int j = 0; j < 8; j++) {
+    int k = ch * 8 + j;
+    double x = 0.0;
+    if (k < 147) {
+      int tap = k / 3, c = k - tap * 3;
+      int dr = tap / 7, ds = tap - dr * 7;
+      int h = 2 * ho - 3 + dr, w = 2 * wo - 3 + ds;
+      if (h >= 0 && h < S && w >= 0 && w < S)
+        x = __ldg(in + (((size_t)n * 3 + c) * S + h) * S + w);
+    }
+    v[j] = __double2bfloat16(x);
+  }
+  *reinterpret_cast<uint4*>(out + row * Kp + ch * 8) = *reinterpret_cast<uint4*>(v);
 }
+
+// 3x3/2 max pool, pad 1 (torch pads with -inf).
+__global__ void maxpool3s2_kernel(const bf16* __restrict__ in, int B, int H, int C,
+                                  bf16* __restrict__ out) {
+  const int Ho = (H + 1) / 2, chunks = C / 8;
+  size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  size_t pix = t / chunks;
+  int ch = (int)(t - pix * chunks);
+  if (pix >= (size_t)B * Ho * Ho) return;
+  int n = (int)(pix / (Ho * Ho)), rem = (int)(pix - (size_t)n * Ho * Ho);
+  int ho = rem / Ho, wo = rem - ho * Ho;
+  float m[8];
+#pragma unroll
+  for (int j = 0; j < 8; j++) m[j] = -INFINITY;
+  for (int dr = 0; dr < 3; dr++) {
+    int h = 2 * ho - 1 + dr;
+    if (h < 0 || h >= H) continue;
+    for (int ds = 0; ds < 3; ds++) {
+      int w = 2 * wo - 1 + ds;
+      if (w < 0 || w >= H) continue;
+      uint4 q = __ldg(reinterpret_cast<const uint4*>(in + (((size_t)n * H + h) * H + w) * C + ch * 8));
+      const bf16* e = reinterpret_cast<const bf16*>(&q);
+#pragma unroll
+      for (int j = 0; j < 8; j++) m[j] = fmaxf(m[j], __bfloat162float(e[j]));
+    }
+  }
+  __align__(16) bf16 o[8];
+#pragma unroll
+  for (int j = 0; j < 8; j++) o[j] = __float2bfloat16(m[j]);
+  *reinterpret_cast<uint4*>(out + pix * C + ch * 8) = *reinterpret_cast<uint4*>(o);
+}
+
+// Stride-2 3x3 operand from the zero-bordered grid: [B*Ho*Wo, 9*C].
+__global__ void gather_s2_3x3_kernel(const bf16* __restrict__ pad, int B, int H,
+                                     int C, bf16* __restrict__ out) {
+  const int Ho = H / 2, Wp = H + 2, chunks = C / 8;
+  size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  size_t row = t / (9 * chunks);
+  int r = (int)(t - row * 9 * chunks);
+  if (row >= (size_t)B * Ho * Ho) return;
+  int tap = r / chunks, ch = r - tap * chunks;
+  int n = (int)(row / (Ho * Ho)), rem = (int)(row - (size_t)n * Ho * Ho);
+  int ho = rem / Ho, wo = rem - ho * Ho;
+  int dr = tap / 3, ds = tap - dr * 3;
+  const uint4* src = reinterpret_cast<const uint4*>(
+      pad + (((size_t)n * Wp + 2 * ho + dr) * Wp + 2 * wo + ds) * C + ch * 8);
+  *reinterpret_cast<uint4*>(out + row * 9 * C + tap * C + ch * 8) = __ldg(src);
+}
+
+// Stride-2 1x1 operand: [B*Ho*Wo, C] = in[n, 2ho, 2wo, :].
+__global__ void gather_s2_1x1_kernel(const bf16* __restrict__ in, int B, int H, int C,
+                                     bf16* __restrict__ out) {
+  const int Ho = H / 2, chunks = C / 8;
+  size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  size_t row = t / chunks;
+  int ch = (int)(t - row * chunks);
+  if (row >= (size_t)B * Ho * Ho) return;
+  int n = (int)(row / (Ho * Ho)), rem = (int)(row - (size_t)n * Ho * Ho);
+  int ho = rem / Ho, wo = rem - ho * Ho;
+  *reinterpret_cast<uint4*>(out + row * C + ch * 8) = __ldg(reinterpret_cast<const uint4*>(
+      in + (((size_t)n * H + 2 * ho) * H + 2 * wo) * C + ch * 8));
+}
+
+// Global average pool [B, HW, C] -> [B, C] (f32 sum in pixel order).
+__global__ void avgpool_kernel(const bf16* __restrict__ in, int B, int HW, int C,
+                               bf16* __restrict__ out) {
+  const int chunks = C / 8;
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= B * chunks) return;
+  int n = t / chunks, ch = t - n * chunks;
+  float s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int p = 0; p < HW; p++) {
+    uint4 q = __ldg(reinterpret_cast<const uint4*>(in + ((size_t)n * HW + p) * C + ch * 8));
+    const bf16* e = reinterpret_cast<const bf16*>(&q);
+#pragma unroll
+    for (int j = 0; j < 8; j++) s[j] += __bfloat162float(e[j]);
+  }
+  __align__(16) bf16 o[8];
+  const float inv = 1.0f / (float)HW;
+#pragma unroll
+  for (int j = 0; j < 8; j++) o[j] = __float2bfloat16(s[j] * inv);
+  *reinterpret_cast<uint4*>(out + (size_t)n * C + ch * 8) = *reinterpret_cast<uint4*>(o);
+}
+
+unsigned grid_for(size_t threads, int tpb = 256) { return (unsigned)ceil_div(threads, tpb); }
+
+// -------------------------------------------------------- model file parse
+// Canonical CNN model file, all big-endian:
+//   str "credo.cnn.v1" | str arch | u64 input_dim | u64 output_dim |
+//   bool softmax | u32 n | n × { str name | u32 ndim | u64 dim[ndim] |
+//   u32 count | count × f32 }
+struct HostTensor {
+  std::vector<int64_t> dims;
+  std::vector<float> v;
+};
+
+struct Reader {
+  const uint8_t* p;
+  uint64_t n, pos = 0;
+  void need(uint64_t k) {
+    if (n - pos < k) throw std::invalid_argument("cnn file: unexpected end of input");
+  }
+  uint64_t u64() {
+    need(8);
+    uint64_t v = 0;
+    for (int i = 0; i < 8; i++) v = (v << 8) | p[pos++];
+    return v;
+  }
+  uint32_t u32() {
+    need(4);
+    uint32_t v = 0;
+    for (int i = 0; i < 4; i++) v = (v << 8) | p[pos++];
+    return v;
+  }
+  std::string str() {
+    uint32_t l = u32();
+    need(l);
+    std::string s(reinterpret_cast<const char*>(p + pos), l);
+    pos += l;
+    return s;
+  }
+};
+
+uint16_t f2bf_bits(float f) {
+  bf16 b = __float2bfloat16(f);  // host conversion, round-to-nearest-even
+  uint16_t u;
+  std::memcpy(&u, &b, 2);
+  return u;
+}
+
+struct ConvW {
+  int cin = 0, cout = 0, k = 1, stride = 1;
+  int Kc = 0, ntaps = 1;        // GEMM K per tap and taps (Ktot = Kc * ntaps)
+  std::vector<uint16_t> hw;     // [cout][Ktot] bf16 bits, folded
+  std::vector<float> hb;        // [cout]
+  bf16* w = nullptr;
+  float* b = nullptr;
+  Operand opB;
+  int BN = 128;
+};
+
+struct Block {
+  ConvW c1, c2, c3, ds;
+  bool has_ds = false;
+  int width = 0, stride = 1, H_in = 0, H_out = 0, cin = 0, cout = 0;
+};
+
+int pick_bn(int rows, int N) {
+  int best = 64;
+  double best_cost = 1e30;
+  for (int bn : {256, 128, 64}) {
+    if (bn > N && bn != 64) continue;
+    long tiles = (long)((rows + 127) / 128) * ((N + bn - 1) / bn);
+    long waves = (tiles + kNumSMs - 1) / kNumSMs;
+    double cost = (double)waves * bn;  // per-tile time ~ BN for fixed M, K
+    if (cost < best_cost - 1e-9) { best_cost = cost; best = bn; }
+  }
+  return best;
+}
+
+class ResNet final : public CnnModel {
+ public:
+  ResNet(std::string arch, std::vector<int> layers, uint64_t in_dim, uint64_t out_dim,
+         bool sm, std::map<std::string, HostTensor>& T)
+      : arch_(std::move(arch)), in_dim_(in_dim), out_dim_(out_dim), softmax_(sm) {
+    S_ = (int)std::lround(std::sqrt((double)in_dim / 3.0));
+    if ((uint64_t)3 * S_ * S_ != in_dim || S_ % 32 != 0)
+      throw std::invalid_argument("cnn file: input_dim must be 3*S*S with S % 32 == 0");
+    // conv1 + bn1: K = 147 padded to 192 (3 k-blocks of 64)
+    fold(conv1_, T, "conv1.weight", "bn1", 7, 2, 192);
+    flops_ = 2.0 * (S_ / 2) * (S_ / 2) * 64 * 147;
+    int H = S_ / 4, cin = 64;
+    const int widths[4] = {64, 128, 256, 512};
+    for (int L = 0; L < 4; L++) {
+      for (int i = 0; i < layers[L]; i++) {
+        Block b;
+        std::string pre = "layer" + std::to_string(L + 1) + "." + std::to_string(i) + ".";
+        b.width = widths[L];
+        b.cin = cin;
+        b.cout = 4 * b.width;
+        b.stride = (i == 0 && L > 0) ? 2 : 1;
+        b.H_in = H;
+        b.H_out = H / b.stride;
+        fold(b.c1, T, pre + "conv1.weight", pre + "bn1", 1, 1, 0);
+        fold(b.c2, T, pre + "conv2.weight", pre + "bn2", 3, b.stride, 0);
+        fold(b.c3, T, pre + "conv3.weight", pre + "bn3", 1, 1, 0);
+        b.has_ds = T.count(pre + "downsample.0.weight") > 0;
+        if (b.has_ds) fold(b.ds, T, pre + "downsample.0.weight", pre + "downsample.1", 1, b.stride, 0);
+        if (b.c1.cin != cin || b.c3.cout != b.cout || b.c2.cin != b.width)
+          throw std::invalid_argument("cnn file: unexpected block shapes at " + pre);
+        double ho2 = (double)b.H_out * b.H_out;
+        flops_ += 2.0 * ((double)H * H * b.cin * b.width + ho2 * 9 * b.width * b.width +
+                         ho2 * b.width * b.cout + (b.has_ds ? ho2 * b.cin * b.cout : 0));
+        blocks_.push_back(std::move(b));
+        cin = 4 * widths[L];
+        H = blocks_.back().H_out;
+      }
+    }
+    H_last_ = H;
+    // fc
+    auto& fw = get(T, "fc.weight", {(int64_t)out_dim, (int64_t)cin});
+    auto& fb = get(T, "fc.bias", {(int64_t)out_dim});
+    fc_.cin = cin;
+    fc_.cout = (int)out_dim;
+    fc_.Kc = cin;
+    fc_.hw.resize((size_t)out_dim * cin);
+    for (size_t i = 0; i < fc_.hw.size(); i++) fc_.hw[i] = f2bf_bits(fw.v[i]);
+    fc_.hb = fb.v;
+    flops_ += 2.0 * cin * out_dim;
+  }
+
+  ~ResNet() override {
+    for (ConvW* c : all_convs()) {
+      if (c->w) cudaFree(c->w);
+      if (c->b) cudaFree(c->b);
+    }
+    for (void* p : bufs_) cudaFree(p);
+  }
+
+  void upload(cudaStream_t st) override {
+    for (ConvW* c : all_convs()) {
+      CG_CUDA(cudaMalloc(&c->w, c->hw.size() * 2));
+      CG_CUDA(cudaMalloc(&c->b, c->hb.size() * 4));
+      CG_CUDA(cudaMemcpyAsync(c->w, c->hw.data(), c->hw.size() * 2, cudaMemcpyHostToDevice, st));
+      CG_CUDA(cudaMemcpyAsync(c->b, c->hb.data(), c->hb.size() * 4, cudaMemcpyHostToDevice, st));
+    }
+    CG_CUDA(cudaStreamSynchronize(st));
+    for (ConvW* c : all_convs()) {
+      std::vector<uint16_t>().swap(c->hw);
+    }
+  }
+
+  void reserve(uint32_t maxB) override {
+    if (maxB <= maxB_) return;
+    for (void* p : bufs_) cudaFree(p);
+    bufs_.clear();
+    plans_.clear();
+    maxB_ = maxB;
+    const size_t B = maxB;
+    const int H1 = S_ / 2, H2 = S_ / 4;
+    auto alloc = [&](size_t elems) {
+      void* p = nullptr;
+      CG_CUDA(cudaMalloc(&p, std::max<size_t>(elems, 8) * 2));
+      CG_CUDA(cudaMemset(p, 0, std::max<size_t>(elems, 8) * 2));
+      bufs_.push_back(p);
+      return reinterpret_cast<bf16*>(p);
+    };
+    xcol_ = alloc(B * H1 * H1 * 192);
+    c1out_ = alloc(B * H1 * H1 * 64);
+    size_t act = 0, t2 = 0, dsz = 0, g3 = 0, g1 = 0;
+    for (auto& b : blocks_) {
+      act = std::max(act, B * b.H_out * b.H_out * b.cout);
+      act = std::max(act, B * b.H_in * b.H_in * b.cin);
+      t2 = std::max(t2, B * b.H_out * b.H_out * b.width);
+      if (b.has_ds) dsz = std::max(dsz, B * b.H_out * b.H_out * b.cout);
+      if (b.stride == 2) {
+        g3 = std::max(g3, B * b.H_out * b.H_out * 9 * b.width);
+        g1 = std::max(g1, B * b.H_out * b.H_out * b.cin);
+      }
+      auto key = std::make_pair(b.H_in, b.width);
+      if (!pads_.count(key)) pads_[key] = nullptr;
+    }
+    act_[0] = alloc(std::max(act, B * H2 * H2 * 64));
+    act_[1] = alloc(act);
+    t2_ = alloc(t2);
+    ds_ = alloc(dsz);
+    g3_ = alloc(g3);
+    g1_ = alloc(g1);
+    for (auto& kv : pads_) {
+      size_t Hp = kv.first.first + 2;
+      kv.second = alloc(B * Hp * Hp * kv.first.second);
+    }
+    pooled_ = alloc(B * fc_.cin);
+  }
+
+  size_t prepared_bytes(uint32_t B) const override {
+    return (size_t)B * (S_ / 2) * (S_ / 2) * 192 * 2;
+  }
+
+  void prepare_input(const double* d_in, uint32_t B, void* prepped, cudaStream_t st) override {
+    const int H1 = S_ / 2;
+    size_t threads = (size_t)B * H1 * H1 * (192 / 8);
+    conv1_im2col_kernel<<<grid_for(threads), 256, 0, st>>>(d_in, B, S_, H1, 192,
+                                                           reinterpret_cast<bf16*>(prepped));
+    CG_CHECK_LAUNCH();
+  }
+
+  void forward(const double* d_in, uint32_t B, float* logits, cudaStream_t st,
+               const void* prepped) override {
+    if (B > maxB_) reserve(B);
+    const bf16* x0 = reinterpret_cast<const bf16*>(prepped);
+    if (!x0) {
+      prepare_input(d_in, B, xcol_, st);
+      x0 = xcol_;
+    }
+    Plan& p = plan_for(B, x0, logits);
+    for (auto& s : p.steps) s(st);
+  }
+
+  uint64_t input_dim() const override { return in_dim_; }
+  uint64_t output_dim() const override { return out_dim_; }
+  bool softmax() const override { return softmax_; }
+  std::string arch() const override { return arch_; }
+  double flops_per_image() const override { return flops_; }
+
+ private:
+  struct Plan {
+    const void* x0 = nullptr;
+    float* logits = nullptr;
+    std::vector<std::function<void(cudaStream_t)>> steps;
+  };
+
+  static HostTensor& get(std::map<std::string, HostTensor>& T, const std::string& name,
+                         std::vector<int64_t> dims) {
+    auto it = T.find(name);
+    if (it == T.end()) throw std::invalid_argument("cnn file: missing tensor " + name);
+    if (!dims.empty() && it->second.dims != dims)
+      throw std::invalid_argument("cnn file: bad shape for " + name);
+    return it->second;
+  }
+
+  // Folds eval-mode BatchNorm into the preceding conv (torch BN eps 1e-5):
+  // w' = w * g / sqrt(var + eps), b' = beta - mean * g / sqrt(var + eps).
+  // Weight layout [cout][(dr*k + ds)*cin + c], zero-padded to Kpad.
+  void fold(ConvW& c, std::map<std::string, HostTensor>& T, const std::string& wname,
+            const std::string& bn, int k, int stride, int Kpad) {
+    auto it = T.find(wname);
+    if (it == T.end()) throw std::invalid_argument("cnn file: missing tensor " + wname);
+    const HostTensor& W = it->second;
+    if (W.dims.size() != 4 || W.dims[2] != k || W.dims[3] != k)
+      throw std::invalid_argument("cnn file: bad conv shape " + wname);
+    c.cout = (int)W.dims[0];
+    c.cin = (int)W.dims[1];
+    c.k = k;
+    c.stride = stride;
+    const int64_t co = c.cout;
+    auto& g = get(T, bn + ".weight", {co});
+    auto& be = get(T, bn + ".bias", {co});
+    auto& mu = get(T, bn + ".running_mean", {co});
+    auto& var = get(T, bn + ".running_var", {co});
+    const int K = k * k * c.cin;
+    const int Ktot = Kpad ? Kpad : K;
+    if (!Kpad && c.cin % 64) throw std::invalid_argument("cnn file: channels % 64 != 0");
+    c.ntaps = (k == 3 && !Kpad) ? 9 : 1;
+    c.Kc = (c.ntaps == 9) ? c.cin : Ktot;
+    c.hw.assign((size_t)c.cout * Ktot, 0);
+    c.hb.resize(c.cout);
+    for (int o = 0; o < c.cout; o++) {
+      double s = (double)g.v[o] / std::sqrt((double)var.v[o] + 1e-5);
+      c.hb[o] = (float)((double)be.v[o] - (double)mu.v[o] * s);
+      for (int ci = 0; ci < c.cin; ci++)
+        for (int dr = 0; dr < k; dr++)
+          for (int ds = 0; ds < k; ds++) {
+            float w = W.v[(((size_t)o * c.cin + ci) * k + dr) * k + ds];
+            c.hw[(size_t)o * Ktot + (dr * k + ds) * c.cin + ci] = f2bf_bits((float)(w * s));
+          }
+    }
+  }
+
+  std::vector<ConvW*> all_convs() {
+    std::vector<ConvW*> v{&conv1_, &fc_};
+    for (auto& b : blocks_) {
+      v.push_back(&b.c1);
+      v.push_back(&b.c2);
+      v.push_back(&b.c3);
+      if (b.has_ds) v.push_back(&b.ds);
+    }
+    return v;
+  }
+
+  // one fused GEMM step
+  void gemm_step(Plan& p, ConvW& c, const bf16* A, int rowsA, int M, int ntaps,
+                 const int* taps, const bf16* residual, int ldres, void* out, int ldout,
+                 int out_f32, int relu, int mode, int H, int rows_out) {
+    auto opA = std::make_shared<Operand>();
+    auto opB = std::make_shared<Operand>();
+    int BN = pick_bn(M, c.cout);
+    make_operand(*opA, A, rowsA, c.Kc, 128);
+    make_operand(*opB, c.w, c.cout, c.Kc * ntaps, BN);
+    ConvGemmArgs a{};
+    a.M = M;
+    a.N = c.cout;
+    a.Kc = c.Kc;
+    a.ntaps = ntaps;
+    for (int t = 0; t < ntaps; t++) a.tap_off[t] = taps[t];
+    a.bias = c.b;
+    a.residual = residual;
+    a.ld_res = ldres;
+    a.out = out;
+    a.ld_out = ldout;
+    a.out_f32 = out_f32;
+    a.relu = relu;
+    a.row_mode = mode;
+    a.H = H;
+    a.W = H;
+    a.rows_out = rows_out;
+    p.steps.push_back([opA, opB, a, BN](cudaStream_t st) {
+      launch_conv_gemm(*opA, *opB, a, BN, st);
+    });
+  }
+
+  Plan& plan_for(uint32_t B, const void* x0, float* logits) {
+    auto it = plans_.find(B);
+    if (it != plans_.end() && it->second.x0 == x0 && it->second.logits == logits)
+      return it->second;
+    Plan& p = plans_[B];
+    p = Plan{};
+    p.x0 = x0;
+    p.logits = logits;
+    const int H1 = S_ / 2, H2 = S_ / 4;
+    const int zero = 0;
+    // conv1 (im2col operand) -> c1out, then maxpool -> act_[0]
+    gemm_step(p, conv1_, reinterpret_cast<const bf16*>(x0), B * H1 * H1, B * H1 * H1, 1,
+              &zero, nullptr, 0, c1out_, 64, 0, 1, kRowIdentity, 0, B * H1 * H1);
+    {
+      bf16* in = c1out_;
+      bf16* out = act_[0];
+      p.steps.push_back([in, out, B, H1](cudaStream_t st) {
+        size_t th = (size_t)B * ((H1 + 1) / 2) * ((H1 + 1) / 2) * (64 / 8);
+        maxpool3s2_kernel<<<grid_for(th), 256, 0, st>>>(in, B, H1, 64, out);
+        CG_CHECK_LAUNCH();
+      });
+    }
+    (void)H2;
+    int cur = 0;
+    for (auto& b : blocks_) {
+      bf16* X = act_[cur];
+      bf16* Y = act_[cur ^ 1];
+      const int Hi = b.H_in, Ho = b.H_out, Hp = Hi + 2;
+      bf16* P = pads_.at({Hi, b.width});
+      // c1: 1x1 -> interior of the zero-bordered grid
+      gemm_step(p, b.c1, X, B * Hi * Hi, B * Hi * Hi, 1, &zero, nullptr, 0, P, b.width, 0, 1,
+                kRowCompactToPad, Hi, B * Hp * Hp);
+      // c2: 3x3
+      if (b.stride == 1) {
+        int taps[9];
+        for (int dr = 0; dr < 3; dr++)
+          for (int ds = 0; ds < 3; ds++) taps[dr * 3 + ds] = (dr - 1) * Hp + (ds - 1);
+        gemm_step(p, b.c2, P, B * Hp * Hp, B * Hp * Hp, 9, taps, nullptr, 0, t2_, b.width, 0,
+                  1, kRowPadToCompact, Hi, B * Ho * Ho);
+      } else {
+        bf16* G = g3_;
+        int C = b.width;
+        p.steps.push_back([P, G, B, Hi, C](cudaStream_t st) {
+          size_t th = (size_t)B * (Hi / 2) * (Hi / 2) * 9 * (C / 8);
+          gather_s2_3x3_kernel<<<grid_for(th), 256, 0, st>>>(P, B, Hi, C, G);
+          CG_CHECK_LAUNCH();
+        });
+        ConvW& c2 = b.c2;
+        // the 9-tap weights double as one K = 9*C operand (same (tap, c) order)
+        c2.Kc = 9 * C;
+        gemm_step(p, c2, G, B * Ho * Ho, B * Ho * Ho, 1, &zero, nullptr, 0, t2_, b.width, 0,
+                  1, kRowIdentity, 0, B * Ho * Ho);
+        c2.Kc = C;
+      }
+      // identity / downsample
+      const bf16* ident = X;
+      if (b.has_ds) {
+        const bf16* dsin = X;
+        if (b.stride == 2) {
+          bf16* G1 = g1_;
+          int C = b.cin;
+          p.steps.push_back([X, G1, B, Hi, C](cudaStream_t st) {
+            size_t th = (size_t)B * (Hi / 2) * (Hi / 2) * (C / 8);
+            gather_s2_1x1_kernel<<<grid_for(th), 256, 0, st>>>(X, B, Hi, C, G1);
+            CG_CHECK_LAUNCH();
+          });
+          dsin = G1;
+        }
+        gemm_step(p, b.ds, dsin, B * Ho * Ho, B * Ho * Ho, 1, &zero, nullptr, 0, ds_, b.cout,
+                  0, 0, kRowIdentity, 0, B * Ho * Ho);
+        ident = ds_;
+      }
+      // c3: 1x1 + residual + ReLU
+      gemm_step(p, b.c3, t2_, B * Ho * Ho, B * Ho * Ho, 1, &zero, ident, b.cout, Y, b.cout, 0,
+                1, kRowIdentity, 0, B * Ho * Ho);
+      cur ^= 1;
+    }
+    {
+      bf16* in = act_[cur];
+      bf16* out = pooled_;
+      int HW = H_last_ * H_last_, C = fc_.cin;
+      p.steps.push_back([in, out, B, HW, C](cudaStream_t st) {
+        avgpool_kernel<<<grid_for((size_t)B * C / 8), 256, 0, st>>>(in, B, HW, C, out);
+        CG_CHECK_LAUNCH();
+      });
+    }
+    gemm_step(p, fc_, pooled_, B, B, 1, &zero, nullptr, 0, logits, (int)out_dim_, 1, 0,
+              kRowIdentity, 0, B);
+    return p;
+  }
+
+  std::string arch_;
+  uint64_t in_dim_, out_dim_;
+  bool softmax_;
+  int S_ = 224, H_last_ = 7;
+  double flops_ = 0;
+  ConvW conv1_, fc_;
+  std::vector<Block> blocks_;
+  uint32_t maxB_ = 0;
+  std::vector<void*> bufs_;
+  bf16 *xcol_ = nullptr, *c1out_ = nullptr, *act_[2] = {nullptr, nullptr}, *t2_ = nullptr,
+       *ds_ = nullptr, *g3_ = nullptr, *g1_ = nullptr, *pooled_ = nullptr;
+  std::map<std::pair<int, int>, bf16*> pads_;
+  std::map<uint32_t, Plan> plans_;
+};
+
+}  // namespace
+
+std::unique_ptr<CnnModel> CnnModel::from_file(const uint8_t* file, uint64_t len) {
+  Reader r{file, len};
+  if (r.str() != "credo.cnn.v1") throw std::invalid_argument("cnn file: bad magic");
+  std::string arch = r.str();
+  uint64_t in_dim = r.u64(), out_dim = r.u64();
+  r.need(1);
+  uint8_t sm = file[r.pos++];
+  if (sm > 1) throw std::invalid_argument("cnn file: invalid boolean");
+  uint32_t n = r.u32();
+  std::map<std::string, HostTensor> T;
+  for (uint32_t i = 0; i < n; i++) {
+    std::string name = r.str();
+    HostTensor t;
+    uint32_t nd = r.u32();
+    if (nd > 8) throw std::invalid_argument("cnn file: too many dims");
+    uint64_t count = 1;
+    for (uint32_t d = 0; d < nd; d++) {
+      t.dims.push_back((int64_t)r.u64());
+      count *= (uint64_t)t.dims.back();
+    }
+    uint32_t c = r.u32();
+    if (c != count) throw std::invalid_argument("cnn file: count/shape mismatch");
+    r.need(4ull * c);
+    t.v.resize(c);
+    for (uint32_t k = 0; k < c; k++) {
+      uint32_t b = r.u32();
+      std::memcpy(&t.v[k], &b, 4);
+    }
+    T[name] = std::move(t);
+  }
+  if (r.pos != len) throw std::invalid_argument("cnn file: trailing bytes after value");
+  std::vector<int> layers;
+  if (arch == "resnet50") layers = {3, 4, 6, 3};
+  else if (arch == "resnet101") layers = {3, 4, 23, 3};
+  else if (arch == "resnet152") layers = {3, 8, 36, 3};
+  else throw std::invalid_argument("cnn file: unsupported arch " + arch);
+  return std::make_unique<ResNet>(arch, layers, in_dim, out_dim, sm == 1, T);
+}
+
 }  // namespace cg

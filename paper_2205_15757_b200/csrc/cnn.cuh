@@ -1,5 +1,8 @@
-// ImageNet-class replica executor (ResNet-50 family) behind the
-// ModelExecutor seam (reference proj/include/credo/model.hpp:41-51).
+// ImageNet-class replica executor (ResNet-50/101/152, bottleneck v1.5)
+// behind the ModelExecutor seam (reference proj/include/credo/model.hpp:
+// 41-51). The reference has no CNN path (its SPEC.md:8 replaces it with
+// LinearToyModel); the CPU restatement used as parity oracle is torchvision's
+// fp32 forward of the same state dict.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -14,16 +17,23 @@ class CnnModel {
  public:
   virtual ~CnnModel() = default;
   // Parses the canonical CNN model file. Throws
-  // std::invalid_argument on malformed bytes.
+  // std::invalid_argument on malformed bytes or an unsupported arch.
   static std::unique_ptr<CnnModel> from_file(const uint8_t* file, uint64_t len);
   virtual void upload(cudaStream_t st) = 0;
   virtual void reserve(uint32_t max_batch) = 0;
-  // d_in: B × input_dim f64 (CHW per image); logits: B × output_dim f32.
+  // Replica-independent input stage (f64 CHW -> bf16 conv1 operand); the
+  // group runs it once per batch and shares it across replicas.
+  virtual void prepare_input(const double* d_in, uint32_t B, void* prepped,
+                             cudaStream_t st) = 0;
+  virtual size_t prepared_bytes(uint32_t B) const = 0;
+  // logits: B × output_dim f32. prepped == nullptr -> prepares internally.
   virtual void forward(const double* d_in, uint32_t B, float* logits,
-                       cudaStream_t st) = 0;
+                       cudaStream_t st, const void* prepped = nullptr) = 0;
   virtual uint64_t input_dim() const = 0;
   virtual uint64_t output_dim() const = 0;
   virtual bool softmax() const = 0;
+  virtual std::string arch() const = 0;
+  virtual double flops_per_image() const = 0;  // 2 × MACs of the forward
 };
 
 }  // namespace cg
