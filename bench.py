@@ -1,0 +1,372 @@
+#!/usr/bin/env python
+"""Headline benchmark: certified inference requests/s for the ResNet-50 model
+group (BASELINE.json: configs[1] = C2: 3 replicas, f=1, batch 128, 224x224,
+random-init jittered weights, synthetic signed requests).
+
+A step = one ExecutionBatch through the whole hot path: 3 replica forwards
+(tcgen05 convs) -> softmax/top-k -> select_quorum + label vote -> result
+leaves (request midstates shared by the providers), R roots, attestation
+manifest + A root. A request counts as certified when its quorum is
+satisfied and all of that is produced.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+N>1 runs under torchrun, one rank per GPU, each rank certifying its own
+request stream for its own replica set (weak scaling, no data-path
+collective: requests are independent objects); the timed region is
+bracketed by barriers and the max over ranks is taken.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "certified inference requests/s (ResNet-50 group) at 1/2/4/8 B200 vs host CPU"
+UNIT = "req/s"
+SIZE = 224
+U = 3 * SIZE * SIZE
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p, "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0,
+                "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for n, v in zip(names, r[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------ setup
+def make_group(ctx, B, seed=0, eps=0.1):
+    from paper_2205_15757_b200 import EUCLIDEAN, Model, ModelGroup
+    from paper_2205_15757_b200.workload import resnet_group
+    files, digs, sds = resnet_group("resnet50", replicas=3, seed=seed, jitter=5e-3)
+    models = [Model.load_cnn(ctx, f, d) for f, d in zip(files, digs)]
+    grp = ModelGroup(ctx, models, 1, EUCLIDEAN, eps, b"group-0", 1, max_batch=B, topk=5)
+    return grp, models, files, digs, sds
+
+
+def bench_gpu(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2205_15757_b200 import Context, lib
+    from paper_2205_15757_b200.workload import signed_requests
+
+    torch.cuda.set_device(local_rank)
+    ctx = Context(local_rank)
+    stream = torch.cuda.current_stream()
+    ctx.set_stream(stream.cuda_stream)
+    B = args.batch
+    grp, models, files, digs, sds = make_group(ctx, B, seed=0)
+    L = lib()
+    L.cg_model_flops_per_input.restype = __import__("ctypes").c_double
+    L.cg_timing_read.argtypes = [__import__("ctypes").c_int,
+                                 __import__("ctypes").POINTER(__import__("ctypes").c_double),
+                                 __import__("ctypes").POINTER(__import__("ctypes").c_uint64)]
+    flops_img = L.cg_model_flops_per_input(models[0].h)
+
+    # Two rotating batches of 154 MB f64 inputs each (> 126 MB L2): pinned
+    # host copies for e2e, device copies for the device-resident value.
+    nb = 2
+    batches = [signed_requests(B, U, seed=100 * rank + i) for i in range(nb)]
+    host_in = [torch.from_numpy(b.inputs).pin_memory() for b in batches]
+    dev_in = [h.to(f"cuda:{local_rank}") for h in host_in]
+    from copy import copy
+    dev_batches, host_batches = [], []
+    for b, h, d in zip(batches, host_in, dev_in):
+        hb = copy(b)
+        hb.inputs = h.numpy()
+        host_batches.append(hb)
+        db = copy(b)
+        db.inputs, db.B, db.u = d.data_ptr(), B, U
+        dev_batches.append(db)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local_rank}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- warmup (also validates: every request must be certified) ----
+    for i in range(args.warmup):
+        r = grp.certify(host_batches[i % nb])
+    sat = float(np.mean(r["satisfied"]))
+    torch.cuda.synchronize()
+    if args.profile:  # ncu mode: a few plain steps, nothing else
+        for i in range(args.steps):
+            grp.certify(dev_batches[i % nb], sync=False)
+        torch.cuda.synchronize()
+        return {"profile": True, "satisfied": sat}
+
+    # ---- device-resident throughput (value) ----
+    l0 = ctx.launch_count()
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        e0.record(stream)
+        for i in range(args.steps):
+            grp.certify(dev_batches[i % nb], sync=False)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    launches = (ctx.launch_count() - l0) // args.steps
+    ms = max_over_ranks(e0.elapsed_time(e1))
+    res = grp.fetch()
+    sat_dev = float(np.mean(res["satisfied"]))
+    value = world * args.steps * B * sat_dev / (ms / 1e3)
+
+    # ---- end to end through the public API from pinned host memory ----
+    barrier()
+    torch.cuda.synchronize()
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2.record(stream)
+    certified = 0
+    for i in range(args.steps):
+        r = grp.certify(host_batches[i % nb])
+        certified += int(np.sum(r["satisfied"]))
+    e3.record(stream)
+    torch.cuda.synchronize()
+    ms_e2e = max_over_ranks(e2.elapsed_time(e3))
+    e2e = world * certified / (ms_e2e / 1e3)
+    h2d = B * U * 8
+    d2h = B * (4 + 8 + 1 + 8) + 3 * 32 + 32 + 8
+
+    # ---- attribution pass: per-kernel-class device time ----
+    import ctypes
+    L.cg_timing_enable(1)
+    for i in range(args.steps):
+        grp.certify(dev_batches[i % nb], sync=False)
+    torch.cuda.synchronize()
+    tg, ng = ctypes.c_double(), ctypes.c_uint64()
+    L.cg_timing_read(0, ctypes.byref(tg), ctypes.byref(ng))
+    tc, nc = ctypes.c_double(), ctypes.c_uint64()
+    L.cg_timing_read(1, ctypes.byref(tc), ctypes.byref(nc))
+    L.cg_timing_enable(0)
+    gemm_ms_step = tg.value / args.steps
+    chain_ms_step = tc.value / args.steps
+    pk, pk_src = peaks()
+    flops_step = 3 * B * flops_img
+    achieved = flops_step / (gemm_ms_step / 1e3) / 1e12
+    peak = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
+    roofline = {"bound": "tensor", "kernel": "conv_gemm (tcgen05 implicit-GEMM, all convs+fc)",
+                "achieved": round(achieved, 1), "peak": peak, "unit": "TFLOP/s",
+                "frac": round(achieved / peak, 4), "traffic": None,
+                "peak_source": f"{pk_src} bf16_tflops_sustained",
+                "algorithmic_flops_per_step": flops_step,
+                "gemm_ms_per_step": round(gemm_ms_step, 3),
+                "gemm_launches_per_step": int(ng.value) // args.steps,
+                "share_of_step": round(gemm_ms_step / (ms / args.steps), 3),
+                "sha_chain_ms_per_step_overlapped": round(chain_ms_step, 3)}
+
+    out = {"metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+           "data": "synthetic (random-init jittered ResNet-50 replicas, U(-1,1) f64 "
+                   "requests, Ed25519-signed)",
+           "config": {"workload": "C2: 3-replica ResNet-50 group, f=1, batch 128, "
+                                  "224x224 (BASELINE.json configs[1])",
+                      "model": "resnet50", "replicas": 3, "f": 1, "global_batch": B * world,
+                      "batch_per_gpu": B, "epsilon": 0.1, "distance": "euclidean",
+                      "seq_len": None, "parallelism": f"group-per-GPU x{world}",
+                      "l2": "inputs larger than L2: 2 rotating 154 MB f64 batches",
+                      "arith": "bf16 forward / f64 agreement / u32 SHA-256",
+                      "satisfied_fraction": sat_dev},
+           "e2e": {"value": round(e2e, 1), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                   "d2h_bytes_per_step": d2h, "ms_per_step": round(ms_e2e / args.steps, 3)},
+           "gpu_launches": int(launches),
+           "roofline": roofline,
+           "clocks": clk.summary()}
+    if rank == 0 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(files, digs, sds, batches[0], args)
+    return out
+
+
+# ------------------------------------------------------------ CPU baseline
+def cpu_path(sds, encs, inputs, digs, threads, R):
+    """The reference's CPU path for a sample: torchvision fp32 forward per
+    replica (restatement: the reference has no CNN), then the compiled
+    reference's select_quorum, ensemble_label, result leaves, R trees,
+    manifest and A tree (oracle/_ref ref_certify_batch)."""
+    import torch
+
+    from oracle import cnn_oracle
+    torch.set_num_threads(threads)
+    outs = []
+    for sd in sds:
+        m = cnn_oracle.build("resnet50", sd)
+        outs.append(cnn_oracle.softmax_f64(cnn_oracle.logits(m, inputs)))
+    outs = np.stack(outs)
+    h = R.batch_new(encs, 1)
+    r = R.certify_batch(h, 3, 1, 0, 0.1, outs, 1, digs, threads=threads)
+    R.batch_free(h)
+    return r
+
+
+def cpu_baseline(files, digs, sds, batch, args):
+    from oracle.oracle import Reference
+    from paper_2205_15757_b200.workload import encode_request
+    threads = os.cpu_count() or 1
+    S = args.cpu_sample
+    encs = [encode_request(batch, k) for k in range(S)]
+    kind = "reference" if Reference.available() else "port"
+    if kind != "reference":
+        return {"value": None, "unit": UNIT, "cores": threads, "kind": "port",
+                "sample": "oracle/_ref not built on this box"}
+    R = Reference()
+    models = [__import__("oracle.cnn_oracle", fromlist=["x"]).build("resnet50", sd) for sd in sds]
+    del models
+    cpu_path(sds, encs[:2], batch.inputs[:2], digs, threads, R)  # warm
+    t = time.perf_counter()
+    cpu_path(sds, encs, batch.inputs[:S], digs, threads, R)
+    dt = time.perf_counter() - t
+    return {"value": round(S / dt, 3), "unit": UNIT, "cores": threads, "kind": kind,
+            "sample": f"{S} requests x 3 replicas: torchvision fp32 forward (restated; "
+                      f"the reference has no CNN) + compiled reference select_quorum/"
+                      f"ensemble_label/result leaves/R+A trees, {dt:.1f} s"}
+
+
+def bench_reference(args, rank, world):
+    """--impl reference: the reference's CPU path on the host cores."""
+    if rank != 0:
+        return None
+    from oracle.oracle import Reference
+    from paper_2205_15757_b200.workload import encode_request, resnet_state_dicts, signed_requests
+    import hashlib
+    from paper_2205_15757_b200.workload import cnn_model_file
+    threads = os.cpu_count() or 1
+    sds = resnet_state_dicts("resnet50", 3, seed=0, jitter=5e-3)
+    digs = [hashlib.sha256(cnn_model_file("resnet50", sd, U, 1000, True)).digest() for sd in sds]
+    S = args.cpu_sample
+    batch = signed_requests(S, U, seed=0)
+    encs = [encode_request(batch, k) for k in range(S)]
+    if not Reference.available():
+        return {"impl": "reference", "unavailable": "oracle/_ref/libcredo_ref.so not built"}
+    R = Reference()
+    for _ in range(max(1, min(args.warmup, 1))):
+        cpu_path(sds, encs[:2], batch.inputs[:2], digs, threads, R)
+    t = time.perf_counter()
+    for _ in range(args.steps_ref):
+        cpu_path(sds, encs, batch.inputs, digs, threads, R)
+    dt = time.perf_counter() - t
+    v = args.steps_ref * S / dt
+    return {"impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": UNIT,
+            "n_gpus": world, "steps": args.steps_ref, "warmup": 1,
+            "ms_per_step": round(1e3 * dt / args.steps_ref, 1), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32 forward / f64 agreement",
+            "data": "synthetic", "config": {"workload": "C2 sample", "batch_per_step": S,
+                                            "model": "resnet50", "replicas": 3, "f": 1},
+            "cpu_baseline": {"value": round(v, 3), "unit": UNIT, "cores": threads,
+                             "kind": "reference",
+                             "sample": f"{S} requests per step, torchvision fp32 forward "
+                                       "(restated) + compiled reference agreement/digests"},
+            "e2e": {"value": round(v, 3), "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--batch", type=int, default=128)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-sample", type=int, default=8)
+    ap.add_argument("--steps-ref", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile", action="store_true",
+                    help="ncu mode: warmup + --steps plain steps, no report")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        if args.impl == "reference":
+            if rank != 0:
+                return
+        else:
+            import torch
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+    if args.impl == "reference":
+        out = bench_reference(args, rank, world)
+    else:
+        out = bench_gpu(args, rank, world, local_rank)
+    if rank == 0 and out is not None:
+        print(json.dumps(out), flush=True)
+    if world > 1 and args.impl != "reference":
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -163,6 +163,15 @@ int cg_group_fetch(cg_group* g, cg_certify_out* out);
 int cg_certify_outputs(cg_group* g, const cg_request_batch* batch,
                        const double* outputs, cg_certify_out* out);
 
+/* ---- measurement hooks ----------------------------------------------------
+ * Per-kernel-class device time from CUDA events recorded on each launching
+ * stream (0 conv GEMM, 1 SHA-256 chains, 2 agreement, 3 other).
+ * Enabling resets the counters. */
+void cg_timing_enable(int on);
+int cg_timing_read(int cls, double* total_ms, uint64_t* launches);
+/* Algorithmic FLOPs of one forward of one input (2 x MACs). */
+double cg_model_flops_per_input(const cg_model* m);
+
 /* ---- test hooks (not on the certified path) -----------------------------
  * One tcgen05 conv-GEMM launch on host buffers (bf16 as uint16 bits). */
 int cg_dbg_conv_gemm(cg_ctx* ctx, const uint16_t* A, int rowsA,

@@ -32,6 +32,43 @@ namespace cg {
 static std::atomic<uint64_t> g_launches{0};
 uint64_t launch_counter_add(uint64_t n) { return g_launches += n; }
 
+// ------------------------------------------------------------ kernel timers
+struct Timers {
+  std::mutex mu;
+  bool on = false;
+  std::vector<cudaEvent_t> pool;
+  size_t used = 0;
+  std::vector<std::pair<size_t, size_t>> spans[kTimeClasses];  // event indices
+  std::vector<size_t> open[kTimeClasses];
+  cudaEvent_t take() {
+    if (used == pool.size()) {
+      cudaEvent_t e;
+      CG_CUDA(cudaEventCreate(&e));
+      pool.push_back(e);
+    }
+    return pool[used++];
+  }
+};
+static Timers g_timers;
+
+void timer_begin(cudaStream_t st, int cls) {
+  if (!g_timers.on) return;
+  std::lock_guard<std::mutex> lk(g_timers.mu);
+  size_t i = g_timers.used;
+  CG_CUDA(cudaEventRecord(g_timers.take(), st));
+  g_timers.open[cls].push_back(i);
+}
+
+void timer_end(cudaStream_t st, int cls) {
+  if (!g_timers.on) return;
+  std::lock_guard<std::mutex> lk(g_timers.mu);
+  size_t i = g_timers.used;
+  CG_CUDA(cudaEventRecord(g_timers.take(), st));
+  size_t b = g_timers.open[cls].back();
+  g_timers.open[cls].pop_back();
+  g_timers.spans[cls].push_back({b, i});
+}
+
 struct CodecError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
@@ -294,6 +331,37 @@ int cg_ctx_synchronize(cg_ctx* ctx) {
 }
 
 uint64_t cg_ctx_launch_count(const cg_ctx*) { return g_launches.load(); }
+
+void cg_timing_enable(int on) {
+  std::lock_guard<std::mutex> lk(g_timers.mu);
+  g_timers.on = on != 0;
+  g_timers.used = 0;
+  for (auto& s : g_timers.spans) s.clear();
+  for (auto& o : g_timers.open) o.clear();
+}
+
+int cg_timing_read(int cls, double* total_ms, uint64_t* launches) {
+  if (cls < 0 || cls >= kTimeClasses) return CG_EINVAL;
+  std::lock_guard<std::mutex> lk(g_timers.mu);
+  double t = 0;
+  for (auto& sp : g_timers.spans[cls]) {
+    if (cudaEventSynchronize(g_timers.pool[sp.second]) != cudaSuccess) return CG_ECUDA;
+    float ms = 0;
+    if (cudaEventElapsedTime(&ms, g_timers.pool[sp.first], g_timers.pool[sp.second]) !=
+        cudaSuccess)
+      return CG_ECUDA;
+    t += ms;
+  }
+  if (total_ms) *total_ms = t;
+  if (launches) *launches = g_timers.spans[cls].size();
+  return CG_OK;
+}
+
+double cg_model_flops_per_input(const cg_model* m) {
+  if (!m) return 0;
+  if (m->kind == 1) return m->cnn->flops_per_image();
+  return 2.0 * (double)m->u * (double)m->v;
+}
 
 int cg_sha256_batch(cg_ctx* ctx, const uint8_t* buf, const uint64_t* off,
                     const uint64_t* len, uint64_t count, uint8_t* out) {

@@ -34,6 +34,12 @@ uint64_t launch_counter_add(uint64_t n);
     ::cg::launch_counter_add(1);       \
   } while (0)
 
+// Optional per-kernel-class device timing (CUDA events on the launching
+// stream), used by bench.py to attribute step time to the dominant kernel.
+enum TimerClass : int { kTimeGemm = 0, kTimeChain = 1, kTimeAgree = 2, kTimeAux = 3, kTimeClasses = 4 };
+void timer_begin(cudaStream_t st, int cls);
+void timer_end(cudaStream_t st, int cls);
+
 constexpr int kNumSMs = 148;
 
 __host__ __device__ inline uint64_t ceil_div(uint64_t a, uint64_t b) {

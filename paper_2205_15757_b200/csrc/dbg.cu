@@ -8,8 +8,70 @@
 #include "../../include/credo_gpu.h"
 #include "common.cuh"
 #include "gemm_sm100.cuh"
+#include "sha256.cuh"
 
 using namespace cg;
+
+// Cycles per SHA-256 block for one warp of 32 chains: mode 0 = compression
+// only (registers), mode 1 = the chain engine over an f64 segment.
+__global__ void sha_bench_kernel(int mode, uint64_t nblocks, const double* buf,
+                                 uint64_t per_thread_doubles, long long* cycles,
+                                 uint32_t* sink) {
+  uint32_t s[8], w[16];
+  sha256_iv(s);
+  for (int i = 0; i < 16; i++) w[i] = threadIdx.x * 16 + i;
+  long long t0 = clock64();
+  if (mode == 0) {
+    for (uint64_t b = 0; b < nblocks; b++) {
+      sha256_compress(s, w);
+      w[0] ^= s[0];
+    }
+  } else {
+    ChainJob j;
+    memset(&j, 0, sizeof j);
+    j.seg[0] = ChainSeg{(uint64_t)(buf + threadIdx.x * per_thread_doubles), 0,
+                        nblocks * 64, kSegF64, 0};
+    j.nseg = 1;
+    j.total_len = nblocks * 64;
+    j.blk_begin = 0;
+    j.blk_end = nblocks;
+    j.state_out = 0;
+    run_chain_job(j, 0);
+    s[0] = (uint32_t)j.blk_end;
+  }
+  long long t1 = clock64();
+  if (threadIdx.x == 0) *cycles = t1 - t0;
+  uint32_t acc = 0;
+  for (int i = 0; i < 8; i++) acc ^= s[i];
+  sink[threadIdx.x] = acc;
+}
+
+extern "C" int cg_dbg_sha_bench(cg_ctx* ctx, int mode, uint64_t nblocks,
+                                double* cycles_per_block) {
+  try {
+    cudaStream_t st = (cudaStream_t)cg_ctx_stream(ctx);
+    double* buf = nullptr;
+    long long* cyc = nullptr;
+    uint32_t* sink = nullptr;
+    uint64_t per = nblocks * 8 + 16;
+    CG_CUDA(cudaMalloc(&buf, 32 * per * 8));
+    CG_CUDA(cudaMemset(buf, 1, 32 * per * 8));
+    CG_CUDA(cudaMalloc(&cyc, 8));
+    CG_CUDA(cudaMalloc(&sink, 128));
+    sha_bench_kernel<<<1, 32, 0, st>>>(mode, nblocks, buf, per, cyc, sink);
+    CG_CHECK_LAUNCH();
+    long long c = 0;
+    CG_CUDA(cudaMemcpyAsync(&c, cyc, 8, cudaMemcpyDeviceToHost, st));
+    CG_CUDA(cudaStreamSynchronize(st));
+    *cycles_per_block = (double)c / (double)nblocks;
+    cudaFree(buf);
+    cudaFree(cyc);
+    cudaFree(sink);
+    return CG_OK;
+  } catch (const std::exception&) {
+    return CG_ECUDA;
+  }
+}
 
 extern "C" int cg_dbg_conv_gemm(cg_ctx* ctx, const uint16_t* A, int rowsA,
                                 const uint16_t* B, int N, int Kc, int ntaps,

@@ -30,8 +30,10 @@ __global__ void __launch_bounds__(64) chain_jobs_kernel(const ChainJob* jobs,
 void launch_chain_jobs(const ChainJob* d_jobs, uint32_t n, cudaStream_t st) {
   if (n == 0) return;
   const int tpb = 64;
+  timer_begin(st, kTimeChain);
   chain_jobs_kernel<<<(unsigned)ceil_div(n, tpb), tpb, 0, st>>>(d_jobs, n);
   CG_CHECK_LAUNCH();
+  timer_end(st, kTimeChain);
 }
 
 // ---------------------------------------------------------------------------

@@ -316,8 +316,10 @@ void launch_t(const Operand& A, const Operand& B, const ConvGemmArgs& a,
   int tiles = ((a.M + BM - 1) / BM) * ((a.N + BN - 1) / BN);
   int grid = tiles < kNumSMs ? tiles : kNumSMs;
   if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
+  timer_begin(st, kTimeGemm);
   conv_gemm_kernel<BN, STAGES><<<grid, kThreads, smem, st>>>(A.map, B.map, a);
   CG_CHECK_LAUNCH();
+  timer_end(st, kTimeGemm);
 }
 
 }  // namespace
