@@ -617,6 +617,36 @@ extern "C" int cg_exec_run(cg_ctx* ctx, cg_model* m, const double* in,
   });
 }
 
+// Test hook: iters forwards of one CNN replica over B device-resident random
+// inputs; average device ms per forward (CUDA events on the ctx stream).
+extern "C" int cg_dbg_forward_bench(cg_ctx* ctx, cg_model* m, uint32_t B, int iters,
+                                    double* ms_per_forward) {
+  return guarded(ctx, [&] {
+    if (!m || m->kind != 1) throw InvalidArgument("cnn model required");
+    cudaStream_t st = ctx->stream;
+    DevBuf<double> d_in;
+    DevBuf<float> d_out;
+    d_in.ensure((size_t)B * m->u);
+    d_out.ensure((size_t)B * m->v);
+    CG_CUDA(cudaMemsetAsync(d_in.p, 0, 8 * (size_t)B * m->u, st));
+    m->cnn->reserve(B);
+    m->cnn->forward(d_in.p, B, d_out.p, st);  // warm (plan + tensor maps)
+    cudaEvent_t e0, e1;
+    CG_CUDA(cudaEventCreate(&e0));
+    CG_CUDA(cudaEventCreate(&e1));
+    CG_CUDA(cudaEventRecord(e0, st));
+    for (int i = 0; i < iters; i++) m->cnn->forward(d_in.p, B, d_out.p, st);
+    CG_CUDA(cudaEventRecord(e1, st));
+    CG_CUDA(cudaEventSynchronize(e1));
+    float ms = 0;
+    CG_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    *ms_per_forward = ms / iters;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return CG_OK;
+  });
+}
+
 // ------------------------------------------------------------------ group
 struct cg_group {
   cg_ctx* ctx = nullptr;

@@ -200,6 +200,9 @@ struct Block {
   int width = 0, stride = 1, H_in = 0, H_out = 0, cin = 0, cout = 0;
 };
 
+// Tile width: minimise waves x BN / eff(BN), where eff reflects that a
+// 128 x 64 tile is shared-memory-bandwidth bound (A is re-read per 64
+// columns) while 128 x 256 streams A once per 256 columns. Ties -> wider.
 int pick_bn(int rows, int N) {
   int best = 64;
   double best_cost = 1e30;
@@ -207,8 +210,9 @@ int pick_bn(int rows, int N) {
     if (bn > N && bn != 64) continue;
     long tiles = (long)((rows + 127) / 128) * ((N + bn - 1) / bn);
     long waves = (tiles + kNumSMs - 1) / kNumSMs;
-    double cost = (double)waves * bn;  // per-tile time ~ BN for fixed M, K
-    if (cost < best_cost - 1e-9) { best_cost = cost; best = bn; }
+    double eff = bn == 256 ? 1.0 : (bn == 128 ? 0.9 : 0.6);
+    double cost = (double)waves * bn / eff;
+    if (cost < best_cost * 0.999) { best_cost = cost; best = bn; }
   }
   return best;
 }

@@ -13,7 +13,8 @@
 namespace cg {
 namespace {
 
-constexpr int BM = 128, BK = 64, kThreads = 192;
+constexpr int BM = 128, BK = 64, kThreads = 320;  // 2 + 8 warps
+constexpr int kEpiWarps = 8, kStgLd = 36;        // staging row stride (floats)
 constexpr int A_BYTES = BM * BK * 2;
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
@@ -34,9 +35,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n"
       "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
       "@!p bra WAIT_%=;\n}" ::"r"(su32(b)),
-      "r"(parity)
+      "r"(parity), "r"(0x989680)
       : "memory");
 }
 __device__ __forceinline__ void tma_load_2d(const CUtensorMap* tm, uint64_t* bar,
@@ -46,6 +47,41 @@ __device__ __forceinline__ void tma_load_2d(const CUtensorMap* tm, uint64_t* bar
       " [%0], [%1, {%3, %4}], [%2];" ::"r"(su32(dst)),
       "l"(tm), "r"(su32(bar)), "r"(x), "r"(y)
       : "memory");
+}
+__device__ __forceinline__ void sts_f32(uint32_t addr, float v) {
+  asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+}
+__device__ __forceinline__ float lds_f32(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts_v4(uint32_t addr, uint32_t x, uint32_t y, uint32_t z,
+                                       uint32_t w) {
+  asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(x), "r"(y), "r"(z),
+               "r"(w)
+               : "memory");
+}
+__device__ __forceinline__ float4 lds_f4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(addr)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ uint2 lds_u2(uint32_t addr) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr) : "memory");
+  return v;
+}
+__device__ __forceinline__ void stg_u2(void* p, uint2 v) {
+  asm volatile("st.global.v2.u32 [%0], {%1, %2};" ::"l"(p), "r"(v.x), "r"(v.y) : "memory");
+}
+__device__ __forceinline__ void stg_f4(void* p, float4 v) {
+  asm volatile("st.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y),
+               "f"(v.z), "f"(v.w)
+               : "memory");
 }
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -105,16 +141,16 @@ __device__ __forceinline__ int remap_row(int M, int rows_out, int mode, int H,
   return img * HpWp + (h + 1) * Wp + w + 1;
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, int kResSlots>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                      const __grid_constant__ CUtensorMap tmB,
+                     const __grid_constant__ CUtensorMap tmR,
                      const ConvGemmArgs a) {
   constexpr int B_BYTES = BN * BK * 2;
   constexpr uint32_t TMEM_COLS = 2 * BN;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024 - (su32(smem_raw) & 1023)) & 1023);
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * A_BYTES;
   uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
@@ -123,6 +159,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   int* s_tap = reinterpret_cast<int*>(tmem_slot + 4);
+  float* s_epi = reinterpret_cast<float*>(s_tap + 12);  // 8 warps x 32 x 36 fp32
+  uint64_t* rfull = reinterpret_cast<uint64_t*>(s_epi + kEpiWarps * 32 * kStgLd);
+  uint64_t* rempty = rfull + (kResSlots > 0 ? kResSlots : 1);
+  // residual ring: kResSlots x [128 rows x 32 cols] bf16, TMA-filled
+  uint8_t* s_res = reinterpret_cast<uint8_t*>(rempty + (kResSlots > 0 ? kResSlots : 1));
+  s_res += (128 - (su32(s_res) & 127)) & 127;
+  const bool res_tma = kResSlots > 0 && a.residual != nullptr && a.row_mode == kRowIdentity;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int num_n = (a.N + BN - 1) / BN, num_m = (a.M + BM - 1) / BM;
@@ -142,8 +185,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int s = 0; s < 2; s++) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], 4);
+      mbar_init(&tempty[s], kEpiWarps);
     }
+    for (int s = 0; s < kResSlots; s++) {
+      mbar_init(&rfull[s], 1);
+      mbar_init(&rempty[s], 4);
+    }
+    if (res_tma) asm volatile("prefetch.tensormap [%0];" ::"l"(&tmR) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -201,72 +249,105 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
-  } else {  // ------------------------------ epilogue (warps 2..5)
-    const int q = warp & 3;  // TMEM lane quarter this warp may access
-    int acc = 0;
+  } else {  // ------------------------------ epilogue (warps 2..9)
+    // Warp w owns TMEM lanes [32q, 32q+32), q = w % 4 (= tile rows), and the
+    // 32-column chunks c with c % 2 == h, h = (w - 2) / 4. Per chunk:
+    // (1) lane = row: tcgen05.ld 32 accumulators -> a private 32x36 fp32 smem
+    //     tile (16-byte vector stores, conflict-free);
+    // (2) lane = (row group, 4-column group): bias, residual (TMA-streamed
+    //     ring), ReLU, bf16 pack and an 8-byte store: each store instruction
+    //     writes 4 contiguous 64-byte row segments.
+    const int q = warp & 3, h = (warp - 2) >> 2;
+    const uint32_t stg_a = su32(s_epi + (warp - 2) * (32 * kStgLd));
+    const int rr = lane >> 3, cgp = lane & 7;
+    constexpr int CPT = BN / 32;  // 32-column chunks per tile
+    const bool issuer = res_tma && warp == 2 && lane == 0;
+    int next_issue = 0;
+    // residual chunk g of this CTA's sequence -> TMA into ring slot g % kResSlots
+    auto issue_upto = [&](int last) {
+      if constexpr (kResSlots > 0) {
+        for (; next_issue <= last; next_issue++) {
+          const int hh = next_issue;
+          const int i = hh / CPT, c = hh - i * CPT;
+          const int t = blockIdx.x + i * gridDim.x;
+          if (t >= tiles) { next_issue = 0x7fffffff; return; }
+          const int slot = hh % kResSlots;
+          if (hh >= kResSlots) mbar_wait(&rempty[slot], ((hh / kResSlots) - 1) & 1);
+          mbar_expect_tx(&rfull[slot], 128 * 32 * 2);
+          tma_load_2d(&tmR, &rfull[slot], s_res + slot * (128 * 32 * 2),
+                      (t % num_n) * BN + c * 32, (t / num_n) * BM);
+        }
+      }
+    };
+    if (issuer) issue_upto(kResSlots - 2);
+    int tile_i = 0, acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, tile_i++) {
       const int m0 = (t / num_n) * BM, n0 = (t % num_n) * BN;
+      const int my_orow = remap_row(a.M, a.rows_out, a.row_mode, a.H, a.W, m0 + q * 32 + lane);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const int m = m0 + q * 32 + lane;
-      const int orow = remap_row(a.M, a.rows_out, a.row_mode, a.H, a.W, m);
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; c++) {
+      for (int c = h; c < CPT; c += 2) {
+        const int g = tile_i * CPT + c;
+        if (issuer) issue_upto(g + kResSlots - 1);
         uint32_t v[32];
         tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, v);
-        const int n = n0 + c * 32;
-        if (orow < 0 || n >= a.N) continue;
-        float x[32];
-        const float* bp = a.bias + n;
+        if (c + 2 >= CPT) {  // this warp's last chunk: hand TMEM back early
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[acc]);
+        }
 #pragma unroll
-        for (int j = 0; j < 32; j++)
-          x[j] = __uint_as_float(v[j]) + ((n + j < a.N) ? __ldg(bp + j) : 0.f);
-        if (a.residual) {
-          const uint4* rp = reinterpret_cast<const uint4*>(
-              a.residual + (size_t)orow * a.ld_res + n);
+        for (int j = 0; j < 8; j++)
+          sts_v4(stg_a + 4 * (lane * kStgLd + 4 * j), v[4 * j], v[4 * j + 1], v[4 * j + 2],
+                 v[4 * j + 3]);
+        __syncwarp();
+        const int n = n0 + c * 32 + cgp * 4;
+        const bool col_ok = n < a.N;
+        float b4[4] = {0.f, 0.f, 0.f, 0.f};
+        if (col_ok) {
+          const float4 bb = __ldg(reinterpret_cast<const float4*>(a.bias + n));
+          b4[0] = bb.x; b4[1] = bb.y; b4[2] = bb.z; b4[3] = bb.w;
+        }
+        const int slot = kResSlots > 0 ? g % kResSlots : 0;
+        const uint32_t rs_a = su32(s_res + slot * (128 * 32 * 2) + (q * 32) * 64 + cgp * 8);
+        if (res_tma) mbar_wait(&rfull[slot], (g / (kResSlots > 0 ? kResSlots : 1)) & 1);
+#pragma unroll 4
+        for (int it = 0; it < 8; it++) {
+          const int r = it * 4 + rr;
+          const int orow = __shfl_sync(0xffffffffu, my_orow, r);
+          const bool ok = orow >= 0 && col_ok;
+          const float4 acc4 = lds_f4(stg_a + 4 * (r * kStgLd + cgp * 4));
+          float x[4] = {acc4.x + b4[0], acc4.y + b4[1], acc4.z + b4[2], acc4.w + b4[3]};
+          if (a.residual) {
+            uint2 rv = make_uint2(0, 0);
+            if (res_tma) rv = lds_u2(rs_a + r * 64);
+            else if (ok) rv = __ldg(reinterpret_cast<const uint2*>(a.residual + (size_t)orow * a.ld_res + n));
+            x[0] += __uint_as_float(rv.x << 16);
+            x[1] += __uint_as_float(rv.x & 0xffff0000u);
+            x[2] += __uint_as_float(rv.y << 16);
+            x[3] += __uint_as_float(rv.y & 0xffff0000u);
+          }
+          if (a.relu) {
 #pragma unroll
-          for (int j = 0; j < 4; j++) {
-            uint4 r4 = __ldg(rp + j);
-            const __nv_bfloat162* r2 = reinterpret_cast<const __nv_bfloat162*>(&r4);
-#pragma unroll
-            for (int e = 0; e < 4; e++) {
-              float2 f = __bfloat1622float2(r2[e]);
-              x[8 * j + 2 * e] += f.x;
-              x[8 * j + 2 * e + 1] += f.y;
+            for (int e = 0; e < 4; e++) x[e] = fmaxf(x[e], 0.f);
+          }
+          if (ok) {
+            if (a.out_f32) {
+              stg_f4(reinterpret_cast<float*>(a.out) + (size_t)orow * a.ld_out + n,
+                     make_float4(x[0], x[1], x[2], x[3]));
+            } else {
+              __nv_bfloat162 o0 = __floats2bfloat162_rn(x[0], x[1]);
+              __nv_bfloat162 o1 = __floats2bfloat162_rn(x[2], x[3]);
+              stg_u2(reinterpret_cast<__nv_bfloat16*>(a.out) + (size_t)orow * a.ld_out + n,
+                     make_uint2(*reinterpret_cast<uint32_t*>(&o0), *reinterpret_cast<uint32_t*>(&o1)));
             }
           }
         }
-        if (a.relu) {
-#pragma unroll
-          for (int j = 0; j < 32; j++) x[j] = fmaxf(x[j], 0.f);
-        }
-        if (a.out_f32) {
-          float* op = reinterpret_cast<float*>(a.out) + (size_t)orow * a.ld_out + n;
-          if (n + 32 <= a.N) {
-#pragma unroll
-            for (int j = 0; j < 8; j++)
-              reinterpret_cast<float4*>(op)[j] =
-                  make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]);
-          } else {
-#pragma unroll
-            for (int j = 0; j < 32; j++)
-              if (n + j < a.N) op[j] = x[j];
-          }
-        } else {
-          __nv_bfloat16* op =
-              reinterpret_cast<__nv_bfloat16*>(a.out) + (size_t)orow * a.ld_out + n;
-          uint4 o4[4];
-          __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(o4);
-#pragma unroll
-          for (int j = 0; j < 16; j++) o2[j] = __floats2bfloat162_rn(x[2 * j], x[2 * j + 1]);
-#pragma unroll
-          for (int j = 0; j < 4; j++) reinterpret_cast<uint4*>(op)[j] = o4[j];
-        }
+        __syncwarp();
+        if (res_tma && lane == 0) mbar_arrive(&rempty[slot]);
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
   }
@@ -298,18 +379,21 @@ EncodeFn get_encode() {
   return fn;
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, int kResSlots>
 constexpr int smem_bytes() {
-  return STAGES * (A_BYTES + BN * BK * 2) + 2 * STAGES * 8 + 4 * 8 + 16 + 64 + 1024;
+  return STAGES * (A_BYTES + BN * BK * 2) + 2 * STAGES * 8 + 4 * 8 + 16 + 48 + 4 * 32 * 33 * 4 +
+         2 * (kResSlots > 0 ? kResSlots : 1) * 8 + 128 + kResSlots * 128 * 32 * 2 + 1024 +
+         (kEpiWarps * kStgLd - 4 * 33) * 32 * 4;
 }
 
-template <int BN, int STAGES>
-void launch_t(const Operand& A, const Operand& B, const ConvGemmArgs& a,
-              cudaStream_t st, int max_ctas) {
+template <int BN, int STAGES, int RS>
+void launch_t(const Operand& A, const Operand& B, const CUtensorMap& R,
+              const ConvGemmArgs& a, cudaStream_t st, int max_ctas) {
   static bool attr = false;
-  constexpr int smem = smem_bytes<BN, STAGES>();
+  constexpr int smem = smem_bytes<BN, STAGES, RS>();
+  static_assert(smem <= 232448, "smem budget");
   if (!attr) {
-    CG_CUDA(cudaFuncSetAttribute(conv_gemm_kernel<BN, STAGES>,
+    CG_CUDA(cudaFuncSetAttribute(conv_gemm_kernel<BN, STAGES, RS>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr = true;
   }
@@ -317,7 +401,7 @@ void launch_t(const Operand& A, const Operand& B, const ConvGemmArgs& a,
   int grid = tiles < kNumSMs ? tiles : kNumSMs;
   if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
   timer_begin(st, kTimeGemm);
-  conv_gemm_kernel<BN, STAGES><<<grid, kThreads, smem, st>>>(A.map, B.map, a);
+  conv_gemm_kernel<BN, STAGES, RS><<<grid, kThreads, smem, st>>>(A.map, B.map, R, a);
   CG_CHECK_LAUNCH();
   timer_end(st, kTimeGemm);
 }
@@ -348,10 +432,35 @@ void launch_conv_gemm(const Operand& A, const Operand& B, const ConvGemmArgs& a,
   if (a.Kc % 64 || a.ntaps < 1 || a.ntaps > 9) throw InvalidArgument("conv_gemm: bad K");
   if (A.box_rows != BM || B.box_rows != BN) throw InvalidArgument("conv_gemm: box mismatch");
   if (!a.out_f32 && (a.N % 32)) throw InvalidArgument("conv_gemm: bf16 out needs N%32==0");
-  switch (BN) {
-    case 64: launch_t<64, 8>(A, B, a, st, max_ctas); break;
-    case 128: launch_t<128, 6>(A, B, a, st, max_ctas); break;
-    case 256: launch_t<256, 4>(A, B, a, st, max_ctas); break;
+  if (a.out_f32 && (a.N % 4)) throw InvalidArgument("conv_gemm: f32 out needs N%4==0");
+  // residual operand: [rows_out, ld_res] bf16, box 32 cols x 128 rows, no swizzle
+  CUtensorMap R;
+  if (a.residual && a.row_mode == kRowIdentity) {
+    if (a.ld_res % 8 || reinterpret_cast<uintptr_t>(a.residual) % 16)
+      throw InvalidArgument("conv_gemm: residual must be 16B aligned");
+    cuuint64_t dims[2] = {(cuuint64_t)a.ld_res, (cuuint64_t)a.rows_out};
+    cuuint64_t strides[1] = {(cuuint64_t)a.ld_res * 2};
+    cuuint32_t box[2] = {32, 128};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = get_encode()(&R, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                              const_cast<__nv_bfloat16*>(a.residual), dims, strides, box, estr,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw CudaError("residual tensor map failed");
+  } else {
+    R = A.map;  // unused
+  }
+  // Residual layers are 1x1 with small K: trade mainloop stages for a deep
+  // residual ring (88 KB in flight per SM) so the epilogue streams at HBM rate.
+  const bool res = a.residual && a.row_mode == kRowIdentity;
+  switch (BN * 2 + (res ? 1 : 0)) {
+    case 128: launch_t<64, 7, 0>(A, B, R, a, st, max_ctas); break;
+    case 129: launch_t<64, 4, 10>(A, B, R, a, st, max_ctas); break;
+    case 256: launch_t<128, 5, 0>(A, B, R, a, st, max_ctas); break;
+    case 257: launch_t<128, 3, 10>(A, B, R, a, st, max_ctas); break;
+    case 512: launch_t<256, 3, 0>(A, B, R, a, st, max_ctas); break;
+    case 513: launch_t<256, 2, 10>(A, B, R, a, st, max_ctas); break;
     default: throw InvalidArgument("conv_gemm: BN must be 64, 128 or 256");
   }
 }
