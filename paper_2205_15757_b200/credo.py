@@ -393,6 +393,26 @@ class ModelGroup:
         self._lastB = B
         return self.fetch(want_outputs, want_leaves, _enqueue=(cb,))
 
+    def ingest(self, batch: RequestBatch) -> int:
+        """InferenceEngine::submit's hot part: frame, upload and start the
+        request-midstate chains. Returns a ticket for :meth:`certify_ticket`."""
+        cb, keep, B = self._cbatch(batch)
+        t = C.c_uint64()
+        self.ctx._check(self.ctx.L.cg_ingest_batch(self.h, C.byref(cb), C.byref(t)))
+        self._inflight = getattr(self, "_inflight", {})
+        self._inflight[t.value] = (keep, B)   # host inputs may still be in flight
+        return t.value
+
+    def certify_ticket(self, ticket: int, sync: bool = True, want_outputs=False,
+                       want_leaves=False):
+        keep, B = self._inflight.pop(ticket)
+        self._lastB = B
+        if not sync:
+            self.ctx._check(self.ctx.L.cg_certify_ticket(self.h, C.c_uint64(ticket), None))
+            self._keep = keep
+            return None
+        return self.fetch(want_outputs, want_leaves, _ticket=ticket)
+
     def certify_outputs(self, batch: RequestBatch, outputs: np.ndarray,
                         want_leaves: bool = False):
         """Agreement + digests over precomputed (N, B, v) replica outputs
@@ -405,7 +425,7 @@ class ModelGroup:
         return self.fetch(False, want_leaves, _enqueue=(cb,), _outputs=o)
 
     def fetch(self, want_outputs=False, want_leaves=False, _enqueue=None,
-              _outputs=None):
+              _outputs=None, _ticket=None):
         B, N, v, k = self._lastB, self.N, self.v, self.topk
         amax = N * B + B + N
         r = dict(selected=np.zeros(B, np.uint32), diameter=np.zeros(B),
@@ -424,7 +444,9 @@ class ModelGroup:
             r["topk_val"] = np.zeros((N, B, k), np.float64)
         o = _COut(*[r[n].ctypes.data if n in r else None
                     for n, _ in _COut._fields_])
-        if _outputs is not None:
+        if _ticket is not None:
+            rc = self.ctx.L.cg_certify_ticket(self.h, C.c_uint64(_ticket), C.byref(o))
+        elif _outputs is not None:
             rc = self.ctx.L.cg_certify_outputs(self.h, C.byref(_enqueue[0]),
                                                _p(_outputs), C.byref(o))
         elif _enqueue is not None:

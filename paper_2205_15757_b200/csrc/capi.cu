@@ -648,6 +648,34 @@ extern "C" int cg_dbg_forward_bench(cg_ctx* ctx, cg_model* m, uint32_t B, int it
 }
 
 // ------------------------------------------------------------------ group
+// One in-flight ExecutionBatch: its framing bytes, chain jobs, request
+// midstates and (for host inputs) its device copy of the inputs. Ingest runs
+// on the slot's own stream so the prefix chains of several batches proceed
+// concurrently with each other and with the replica forwards.
+struct IngestSlot {
+  bool used = false, ever = false;
+  uint64_t ticket = 0;
+  uint32_t B = 0;
+  const double* d_in_ptr = nullptr;
+  DevBuf<double> d_in, d_eps;
+  DevBuf<uint8_t> d_arena, d_reqids;
+  DevBuf<ChainJob> d_jobs;
+  DevBuf<uint32_t> d_mid;
+  DevBuf<uint64_t> d_tree;  // per-provider tree offsets then lengths
+  PinBuf<uint8_t> h_arena, h_reqids;
+  PinBuf<ChainJob> h_jobs;
+  PinBuf<double> h_eps;
+  PinBuf<uint64_t> h_tree;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev_staged = nullptr, ev_prefix = nullptr, ev_done = nullptr;
+  ~IngestSlot() {
+    if (stream) cudaStreamDestroy(stream);
+    if (ev_staged) cudaEventDestroy(ev_staged);
+    if (ev_prefix) cudaEventDestroy(ev_prefix);
+    if (ev_done) cudaEventDestroy(ev_done);
+  }
+};
+
 struct cg_group {
   cg_ctx* ctx = nullptr;
   std::vector<cg_model*> models;
@@ -656,43 +684,46 @@ struct cg_group {
   std::string gid;
   uint64_t version = 0;
   uint64_t u = 0, v = 0;
-  // device state
-  DevBuf<double> d_in, d_pre64, d_outs, d_topv, d_eps, d_diam;
+  // per-batch results, written on the main stream by certify
+  DevBuf<double> d_pre64, d_outs, d_topv, d_diam;
   DevBuf<float> d_pre32;
-  DevBuf<uint32_t> d_topi, d_mid, d_sel, d_mnodes, d_mops, d_count;
-  DevBuf<uint8_t> d_arena, d_leaf, d_rroots, d_aleaf, d_aroot, d_sat, d_kinds,
-      d_reqids, d_gid;
+  DevBuf<uint32_t> d_topi, d_sel, d_mnodes, d_mops, d_count;
+  DevBuf<uint8_t> d_leaf, d_rroots, d_aleaf, d_aroot, d_sat, d_kinds, d_gid;
   DevBuf<int8_t> d_status;
   DevBuf<int64_t> d_label;
   DevBuf<int32_t> d_single_pos;
-  DevBuf<ChainJob> d_jobs;
-  DevBuf<uint64_t> d_toff, d_tlen;
   DevBuf<uint8_t> d_prep;  // shared CNN input operand
   bool all_cnn = false;
-  // host staging (pinned) + guard event so a refill never races its H2D
-  PinBuf<uint8_t> h_arena;
-  PinBuf<ChainJob> h_jobs;
-  PinBuf<double> h_eps;
-  PinBuf<uint8_t> h_reqids;
-  cudaEvent_t ev_staged = nullptr, ev_prefix = nullptr, ev_inputs = nullptr;
-  bool staged_pending = false;
+  std::vector<std::unique_ptr<IngestSlot>> slots;
+  uint64_t next_ticket = 1;
   uint32_t last_B = 0;
 };
 
 namespace {
 
-void certify_enqueue(cg_group* g, const cg_request_batch* bt,
-                     const double* precomputed_outputs) {
-  cg_ctx* ctx = g->ctx;
+IngestSlot& slot_for(cg_group* g, uint64_t ticket) {
+  IngestSlot& s = *g->slots[ticket % g->slots.size()];
+  if (!s.used || s.ticket != ticket) throw InvalidArgument("unknown or already certified ticket");
+  return s;
+}
+
+// InferenceEngine::submit's hot part (engine.cpp:182-209): take the batch,
+// build the canonical framing bytes of every leaf it will need, upload, and
+// start the request-midstate chains H(0x00||0x52||request)[whole blocks].
+uint64_t ingest(cg_group* g, const cg_request_batch* bt) {
   const uint32_t B = bt->B, N = g->N;
   const uint64_t u = bt->u, v = g->v;
   if (B == 0) throw InvalidArgument("empty batch");
   if (B > g->maxB) throw InvalidArgument("batch larger than group max_batch");
   if (u != g->u) throw InvalidArgument("request input dimension mismatch");
-  cudaStream_t st = ctx->stream, side = ctx->side;
-
-  // ---- framing bytes + chain jobs (host) ----
-  if (g->staged_pending) CG_CUDA(cudaEventSynchronize(g->ev_staged));
+  const uint64_t ticket = g->next_ticket;
+  IngestSlot& S = *g->slots[ticket % g->slots.size()];
+  if (S.used) throw InvalidArgument("ingest ring full: certify an outstanding ticket first");
+  cudaStream_t st = S.stream;
+  if (S.ever) {
+    CG_CUDA(cudaEventSynchronize(S.ev_staged));      // pinned staging reusable
+    CG_CUDA(cudaStreamWaitEvent(st, S.ev_done, 0));  // device buffers reusable
+  }
   Arena ar;
   std::vector<ChainJob> jobs;
   jobs.reserve((size_t)B * (1 + 2 * N));
@@ -704,17 +735,16 @@ void certify_enqueue(cg_group* g, const cg_request_batch* bt,
   };
   std::vector<ReqLayout> rl(B);
   std::vector<size_t> res_off((size_t)B * N), dig_off((size_t)B * N);
-  uint64_t lenRes = 0;
-  uint64_t nonce_pos = 0;
+  uint64_t lenRes = 0, nonce_pos = 0;
   for (uint32_t k = 0; k < B; k++) {
     const uint8_t* rid = bt->request_ids + 32 * k;
-    Enc H;
+    Enc H;  // 0x00 (leaf domain) || 0x52 (result leaf) || request body head
     H.u8(0x00);
     H.u8(0x52);
     H.raw(rid, 32);
     H.bytes(gid, gl);
     H.u32((uint32_t)u);
-    Enc T;
+    Enc T;  // request tail after the f64 input list (domain.cpp:144-158)
     bool he = bt->has_eps && bt->has_eps[k];
     T.u8(he ? 1 : 0);
     if (he) T.f64(bt->eps[k]);
@@ -739,23 +769,39 @@ void certify_enqueue(cg_group* g, const cg_request_batch* bt,
       R.u32((uint32_t)v);
       lenRes = R.b.size();
       res_off[(size_t)k * N + p] = ar.add(R.b.data(), R.b.size(), L.P);
-      dig_off[(size_t)k * N + p] =
-          ar.add(g->models[p]->digest, 32, L.P + lenRes + 8 * v);
+      dig_off[(size_t)k * N + p] = ar.add(g->models[p]->digest, 32, L.P + lenRes + 8 * v);
     }
   }
-  g->h_arena.ensure(ar.b.size() + 64);
-  std::memcpy(g->h_arena.p, ar.b.data(), ar.b.size());
-  g->d_arena.ensure(ar.b.size() + 64);
-  const uint64_t A = (uint64_t)g->d_arena.p;
-  const double* d_in = bt->inputs_on_device ? bt->inputs : g->d_in.p;
-  const uint64_t IN = (uint64_t)d_in;
+  S.d_arena.ensure(ar.b.size() + 64);
+  S.h_arena.ensure(ar.b.size() + 64);
+  std::memcpy(S.h_arena.p, ar.b.data(), ar.b.size());
+  const uint64_t A = (uint64_t)S.d_arena.p;
+  S.d_in_ptr = bt->inputs_on_device ? bt->inputs : S.d_in.p;
+  const uint64_t IN = (uint64_t)S.d_in_ptr;
+  const uint64_t OUT = (uint64_t)g->d_outs.p;
   auto seg_raw = [](uint64_t ptr, uint64_t off, uint64_t len) {
     return ChainSeg{ptr, off, len, kSegRaw, 0};
   };
   auto seg_f64 = [](uint64_t ptr, uint64_t off, uint64_t len) {
     return ChainSeg{ptr, off, len, kSegF64, 0};
   };
-  // prefix jobs: request midstates
+  auto leaf_job = [&](uint32_t k, uint32_t p, size_t head) {
+    const ReqLayout& L = rl[k];
+    ChainJob j;
+    std::memset(&j, 0, sizeof j);
+    j.seg[0] = seg_raw(A + head, 0, L.lenH);
+    j.seg[1] = seg_f64(IN + 8 * u * k, L.lenH, 8 * u);
+    j.seg[2] = seg_raw(A + L.t, L.lenH + 8 * u, L.lenT);
+    j.seg[3] = seg_raw(A + res_off[(size_t)k * N + p], L.P, lenRes);
+    j.seg[4] = seg_f64(OUT + 8 * v * ((uint64_t)p * B + k), L.P + lenRes, 8 * v);
+    j.seg[5] = seg_raw(A + dig_off[(size_t)k * N + p], L.P + lenRes + 8 * v, 32);
+    j.nseg = 6;
+    j.final_ = 1;
+    j.total_len = L.P + lenRes + 8 * v + 32;
+    j.blk_end = (j.total_len + 9 + 63) / 64;
+    return j;
+  };
+  // [0, B): request midstates
   for (uint32_t k = 0; k < B; k++) {
     const ReqLayout& L = rl[k];
     ChainJob j;
@@ -764,135 +810,109 @@ void certify_enqueue(cg_group* g, const cg_request_batch* bt,
     j.seg[1] = seg_f64(IN + 8 * u * k, L.lenH, 8 * u);
     j.seg[2] = seg_raw(A + L.t, L.lenH + 8 * u, L.lenT);
     j.nseg = 3;
-    j.final_ = 0;
     j.total_len = L.P;
-    j.blk_begin = 0;
     j.blk_end = L.P / 64;
-    j.state_out = (uint64_t)(g->d_mid.p + 8 * k);
+    j.state_out = (uint64_t)(S.d_mid.p + 8 * k);
     jobs.push_back(j);
   }
-  const uint64_t OUT = (uint64_t)g->d_outs.p;
-  // tail jobs: result leaves H(0x00||0x52||req||res), provider-major output
+  // [B, B + N*B): result leaves H(0x00||0x52||req||res) from the midstate
   for (uint32_t p = 0; p < N; p++)
     for (uint32_t k = 0; k < B; k++) {
-      const ReqLayout& L = rl[k];
-      ChainJob j;
-      std::memset(&j, 0, sizeof j);
-      j.seg[0] = seg_raw(A + L.h, 0, L.lenH);
-      j.seg[1] = seg_f64(IN + 8 * u * k, L.lenH, 8 * u);
-      j.seg[2] = seg_raw(A + L.t, L.lenH + 8 * u, L.lenT);
-      j.seg[3] = seg_raw(A + res_off[(size_t)k * N + p], L.P, lenRes);
-      j.seg[4] = seg_f64(OUT + 8 * v * ((uint64_t)p * B + k), L.P + lenRes, 8 * v);
-      j.seg[5] = seg_raw(A + dig_off[(size_t)k * N + p], L.P + lenRes + 8 * v, 32);
-      j.nseg = 6;
-      j.final_ = 1;
-      j.total_len = L.P + lenRes + 8 * v + 32;
-      j.blk_begin = L.P / 64;
-      j.blk_end = (j.total_len + 9 + 63) / 64;
-      j.state_in = j.blk_begin ? (uint64_t)(g->d_mid.p + 8 * k) : 0;
+      ChainJob j = leaf_job(k, p, rl[k].h);
+      j.blk_begin = rl[k].P / 64;
+      j.state_in = j.blk_begin ? (uint64_t)(S.d_mid.p + 8 * k) : 0;
       j.digest_out = (uint64_t)(g->d_leaf.p + 32 * ((uint64_t)p * B + k));
       jobs.push_back(j);
     }
-  // single attestation leaves H(0x00||0x53||req||res): slot chosen on device
+  // [B + N*B, B + 2*N*B): single attestation leaves H(0x00||0x53||req||res);
+  // the manifest kernel decides on device which run and where they land
   for (uint32_t k = 0; k < B; k++)
     for (uint32_t p = 0; p < N; p++) {
-      const ReqLayout& L = rl[k];
-      ChainJob j;
-      std::memset(&j, 0, sizeof j);
-      j.seg[0] = seg_raw(A + L.h53, 0, L.lenH);
-      j.seg[1] = seg_f64(IN + 8 * u * k, L.lenH, 8 * u);
-      j.seg[2] = seg_raw(A + L.t, L.lenH + 8 * u, L.lenT);
-      j.seg[3] = seg_raw(A + res_off[(size_t)k * N + p], L.P, lenRes);
-      j.seg[4] = seg_f64(OUT + 8 * v * ((uint64_t)p * B + k), L.P + lenRes, 8 * v);
-      j.seg[5] = seg_raw(A + dig_off[(size_t)k * N + p], L.P + lenRes + 8 * v, 32);
-      j.nseg = 6;
-      j.final_ = 1;
-      j.total_len = L.P + lenRes + 8 * v + 32;
-      j.blk_begin = 0;
-      j.blk_end = (j.total_len + 9 + 63) / 64;
+      ChainJob j = leaf_job(k, p, rl[k].h53);
       j.digest_out = (uint64_t)g->d_aleaf.p;
       j.skip_flag = (uint64_t)(g->d_single_pos.p + (uint64_t)k * N + p);
       jobs.push_back(j);
     }
-  g->h_jobs.ensure(jobs.size());
-  std::memcpy(g->h_jobs.p, jobs.data(), jobs.size() * sizeof(ChainJob));
-  g->h_eps.ensure(B);
-  g->h_reqids.ensure(32 * (size_t)B);
+  S.h_jobs.ensure(jobs.size());
+  S.d_jobs.ensure(jobs.size());
+  std::memcpy(S.h_jobs.p, jobs.data(), jobs.size() * sizeof(ChainJob));
   for (uint32_t k = 0; k < B; k++)
-    g->h_eps.p[k] = (bt->has_eps && bt->has_eps[k]) ? bt->eps[k] : g->eps_default;
-  std::memcpy(g->h_reqids.p, bt->request_ids, 32 * (size_t)B);
-  g->d_jobs.ensure(jobs.size());
-
-  // ---- uploads (main stream) ----
-  CG_CUDA(cudaMemcpyAsync(g->d_arena.p, g->h_arena.p, ar.b.size(),
+    S.h_eps.p[k] = (bt->has_eps && bt->has_eps[k]) ? bt->eps[k] : g->eps_default;
+  std::memcpy(S.h_reqids.p, bt->request_ids, 32 * (size_t)B);
+  for (uint32_t p = 0; p < N; p++) {
+    S.h_tree.p[p] = (uint64_t)p * B;
+    S.h_tree.p[N + p] = B;
+  }
+  CG_CUDA(cudaMemcpyAsync(S.d_arena.p, S.h_arena.p, ar.b.size(), cudaMemcpyHostToDevice, st));
+  CG_CUDA(cudaMemcpyAsync(S.d_jobs.p, S.h_jobs.p, jobs.size() * sizeof(ChainJob),
                           cudaMemcpyHostToDevice, st));
-  CG_CUDA(cudaMemcpyAsync(g->d_jobs.p, g->h_jobs.p, jobs.size() * sizeof(ChainJob),
-                          cudaMemcpyHostToDevice, st));
-  CG_CUDA(cudaMemcpyAsync(g->d_eps.p, g->h_eps.p, 8 * (size_t)B,
-                          cudaMemcpyHostToDevice, st));
-  CG_CUDA(cudaMemcpyAsync(g->d_reqids.p, g->h_reqids.p, 32 * (size_t)B,
-                          cudaMemcpyHostToDevice, st));
-  std::vector<uint64_t> toff(N), tlen(N, B);
-  for (uint32_t p = 0; p < N; p++) toff[p] = (uint64_t)p * B;
-  CG_CUDA(cudaMemcpyAsync(g->d_toff.p, toff.data(), 8 * N, cudaMemcpyHostToDevice, st));
-  CG_CUDA(cudaMemcpyAsync(g->d_tlen.p, tlen.data(), 8 * N, cudaMemcpyHostToDevice, st));
+  CG_CUDA(cudaMemcpyAsync(S.d_eps.p, S.h_eps.p, 8 * (size_t)B, cudaMemcpyHostToDevice, st));
+  CG_CUDA(cudaMemcpyAsync(S.d_reqids.p, S.h_reqids.p, 32 * (size_t)B, cudaMemcpyHostToDevice, st));
+  CG_CUDA(cudaMemcpyAsync(S.d_tree.p, S.h_tree.p, 16 * (size_t)N, cudaMemcpyHostToDevice, st));
   if (!bt->inputs_on_device)
-    CG_CUDA(cudaMemcpyAsync(g->d_in.p, bt->inputs, 8 * u * B,
-                            cudaMemcpyHostToDevice, st));
-  CG_CUDA(cudaEventRecord(g->ev_staged, st));
-  g->staged_pending = true;
+    CG_CUDA(cudaMemcpyAsync(S.d_in.p, bt->inputs, 8 * u * B, cudaMemcpyHostToDevice, st));
+  CG_CUDA(cudaEventRecord(S.ev_staged, st));
+  launch_chain_jobs(S.d_jobs.p, B, st);
+  CG_CUDA(cudaEventRecord(S.ev_prefix, st));
+  S.used = true;
+  S.ever = true;
+  S.ticket = ticket;
+  S.B = B;
+  g->next_ticket++;
+  return ticket;
+}
 
-  // ---- side stream: request midstates, concurrent with the forwards ----
-  CG_CUDA(cudaStreamWaitEvent(side, g->ev_staged, 0));
-  launch_chain_jobs(g->d_jobs.p, B, side);
-  CG_CUDA(cudaEventRecord(g->ev_prefix, side));
-
-  // ---- main stream: replica forwards + softmax/top-k ----
+// execute_batch + try_prepare's R trees + try_attest (engine.cpp:269-306,
+// coordinator.cpp:588-624, 727-849) on the main stream.
+void certify(cg_group* g, uint64_t ticket, const double* precomputed_outputs) {
+  IngestSlot& S = slot_for(g, ticket);
+  cg_ctx* ctx = g->ctx;
+  const uint32_t B = S.B, N = g->N;
+  const uint64_t v = g->v;
+  const uint32_t gl = (uint32_t)g->gid.size();
+  cudaStream_t st = ctx->stream;
+  CG_CUDA(cudaStreamWaitEvent(st, S.ev_staged, 0));
   if (precomputed_outputs) {
-    // agreement/digest-only mode (C5): N × B × v outputs supplied by the host
-    CG_CUDA(cudaMemcpyAsync(g->d_outs.p, precomputed_outputs,
-                            8 * (size_t)N * B * v, cudaMemcpyHostToDevice, st));
+    // agreement/digest-only mode (C5): N x B x v outputs supplied by the host
+    CG_CUDA(cudaMemcpyAsync(g->d_outs.p, precomputed_outputs, 8 * (size_t)N * B * v,
+                            cudaMemcpyHostToDevice, st));
+  } else {
+    const void* prepped = nullptr;
+    if (g->all_cnn) {  // replica-independent input stage, once per batch
+      g->models[0]->cnn->prepare_input(S.d_in_ptr, B, g->d_prep.p, st);
+      prepped = g->d_prep.p;
+    }
+    for (uint32_t p = 0; p < N; p++) {
+      cg_model* m = g->models[p];
+      double* outs = g->d_outs.p + (uint64_t)p * B * v;
+      uint32_t* ti = g->d_topi.p + (uint64_t)p * B * g->topk;
+      double* tv = g->d_topv.p + (uint64_t)p * B * g->topk;
+      if (m->kind == 1) {
+        m->cnn->forward(S.d_in_ptr, B, g->d_pre32.p, st, prepped);
+        launch_softmax_topk_f32(g->d_pre32.p, v, B, (uint32_t)v, m->softmax, outs, v,
+                                g->topk, ti, tv, st);
+      } else {
+        replica_forward(m, S.d_in_ptr, B, g->d_pre64.p, g->d_pre32.p, st);
+        launch_softmax_topk_f64(g->d_pre64.p, v, B, (uint32_t)v, m->softmax, outs, v,
+                                g->topk, ti, tv, st);
+      }
+    }
   }
-  // replica-independent input stage (CNN conv1 operand), once per batch
-  const void* prepped = nullptr;
-  if (!precomputed_outputs && g->all_cnn) {
-    g->models[0]->cnn->prepare_input(d_in, B, g->d_prep.p, st);
-    prepped = g->d_prep.p;
-  }
-  for (uint32_t p = 0; p < N && !precomputed_outputs; p++) {
-    cg_model* m = g->models[p];
-    double* outs = g->d_outs.p + (uint64_t)p * B * v;
-    uint32_t* ti = g->d_topi.p + (uint64_t)p * B * g->topk;
-    double* tv = g->d_topv.p + (uint64_t)p * B * g->topk;
-    if (m->kind == 1)
-      m->cnn->forward(d_in, B, g->d_pre32.p, st, prepped);
-    else
-      replica_forward(m, d_in, B, g->d_pre64.p, g->d_pre32.p, st);
-    if (m->kind == 0)
-      launch_softmax_topk_f64(g->d_pre64.p, v, B, (uint32_t)v, m->softmax, outs,
-                              v, g->topk, ti, tv, st);
-    else
-      launch_softmax_topk_f32(g->d_pre32.p, v, B, (uint32_t)v, m->softmax, outs,
-                              v, g->topk, ti, tv, st);
-  }
-  CG_CUDA(cudaStreamWaitEvent(st, g->ev_prefix, 0));
-  // result leaves (tails from the shared request midstate)
-  launch_chain_jobs(g->d_jobs.p + B, N * B, st);
-  // agreement + label vote
-  launch_select_quorum(g->d_outs.p, (uint64_t)B * v, v, nullptr, g->d_eps.p, B,
-                       N, g->f, (uint32_t)v, g->metric, g->d_sel.p, g->d_diam.p,
-                       g->d_sat.p, g->d_status.p, g->d_label.p, st);
-  // per-provider R roots
-  launch_merkle_trees(g->d_leaf.p, g->d_toff.p, g->d_tlen.p, nullptr, N, B,
-                      g->d_rroots.p, st);
-  // attestation manifest, whole/failure A leaves, then single A leaves
-  launch_attest_manifest(B, N, g->d_sel.p, g->d_sat.p, g->d_rroots.p,
-                         g->d_reqids.p, g->d_gid.p, gl, g->version,
-                         g->d_aleaf.p, g->d_single_pos.p, g->d_kinds.p,
-                         g->d_mnodes.p, g->d_mops.p, g->d_count.p, st);
-  launch_chain_jobs(g->d_jobs.p + B + (uint64_t)N * B, N * B, st);
-  launch_merkle_trees(g->d_aleaf.p, nullptr, nullptr, g->d_count.p, 1,
-                      (uint64_t)N * B + B + N, g->d_aroot.p, st);
+  CG_CUDA(cudaStreamWaitEvent(st, S.ev_prefix, 0));
+  launch_chain_jobs(S.d_jobs.p + B, N * B, st);  // result leaves
+  launch_select_quorum(g->d_outs.p, (uint64_t)B * v, v, nullptr, S.d_eps.p, B, N, g->f,
+                       (uint32_t)v, g->metric, g->d_sel.p, g->d_diam.p, g->d_sat.p,
+                       g->d_status.p, g->d_label.p, st);
+  launch_merkle_trees(g->d_leaf.p, S.d_tree.p, S.d_tree.p + N, nullptr, N, B, g->d_rroots.p,
+                      st);
+  launch_attest_manifest(B, N, g->d_sel.p, g->d_sat.p, g->d_rroots.p, S.d_reqids.p,
+                         g->d_gid.p, gl, g->version, g->d_aleaf.p, g->d_single_pos.p,
+                         g->d_kinds.p, g->d_mnodes.p, g->d_mops.p, g->d_count.p, st);
+  launch_chain_jobs(S.d_jobs.p + B + (uint64_t)N * B, N * B, st);  // single A leaves
+  launch_merkle_trees(g->d_aleaf.p, nullptr, nullptr, g->d_count.p, 1, (uint64_t)N * B + B + N,
+                      g->d_aroot.p, st);
+  CG_CUDA(cudaEventRecord(S.ev_done, st));
+  S.used = false;
   g->last_B = B;
 }
 
@@ -900,6 +920,7 @@ void certify_fetch(cg_group* g, cg_certify_out* o) {
   cudaStream_t st = g->ctx->stream;
   const uint32_t B = g->last_B, N = g->N;
   const uint64_t v = g->v;
+  if (B == 0) throw InvalidArgument("nothing certified yet");
   auto d2h = [&](void* dst, const void* src, size_t n) {
     if (dst) CG_CUDA(cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToHost, st));
   };
@@ -941,6 +962,7 @@ int cg_group_create(cg_ctx* ctx, cg_model* const* models, uint32_t N,
     *out = nullptr;
     if (N == 0 || N > 20 || f >= N) throw InvalidArgument("bad n/f");
     if (max_batch == 0) throw InvalidArgument("max_batch must be >= 1");
+    if (group_id_len > 100) throw InvalidArgument("group id longer than 100 bytes");
     if (topk == 0) topk = 1;
     auto g = std::make_unique<cg_group>();
     g->ctx = ctx;
@@ -959,19 +981,15 @@ int cg_group_create(cg_ctx* ctx, cg_model* const* models, uint32_t N,
     g->u = models[0]->u;
     g->v = models[0]->v;
     for (auto* m : g->models)
-      if (m->u != g->u || m->v != g->v)
-        throw InvalidArgument("models disagree on dimensions");
+      if (m->u != g->u || m->v != g->v) throw InvalidArgument("models disagree on dimensions");
     if (g->v > 1024) throw InvalidArgument("output dimension > 1024");
     const uint64_t B = max_batch, v = g->v;
-    g->d_in.ensure(B * g->u);
     g->d_pre64.ensure(B * v);
     g->d_pre32.ensure(B * v);
     g->d_outs.ensure((uint64_t)N * B * v);
     g->d_topi.ensure((uint64_t)N * B * topk);
     g->d_topv.ensure((uint64_t)N * B * topk);
-    g->d_eps.ensure(B);
     g->d_diam.ensure(B);
-    g->d_mid.ensure(8 * B);
     g->d_sel.ensure(B);
     const uint64_t amax = (uint64_t)N * B + B + N;
     g->d_mnodes.ensure(amax);
@@ -986,20 +1004,38 @@ int cg_group_create(cg_ctx* ctx, cg_model* const* models, uint32_t N,
     g->d_status.ensure(B);
     g->d_label.ensure(B);
     g->d_single_pos.ensure((uint64_t)N * B);
-    g->d_reqids.ensure(32 * B);
-    g->d_toff.ensure(N);
-    g->d_tlen.ensure(N);
     g->d_gid.ensure(g->gid.size() + 1);
     CG_CUDA(cudaMemcpy(g->d_gid.p, g->gid.data(), g->gid.size(), cudaMemcpyHostToDevice));
-    CG_CUDA(cudaEventCreateWithFlags(&g->ev_staged, cudaEventDisableTiming));
-    CG_CUDA(cudaEventCreateWithFlags(&g->ev_prefix, cudaEventDisableTiming));
-    CG_CUDA(cudaEventCreateWithFlags(&g->ev_inputs, cudaEventDisableTiming));
     g->all_cnn = true;
     for (auto* m : g->models) {
       if (m->kind == 1) m->cnn->reserve(max_batch);
       g->all_cnn = g->all_cnn && m->kind == 1;
     }
     if (g->all_cnn) g->d_prep.ensure(g->models[0]->cnn->prepared_bytes(max_batch));
+    // ingest ring: enough batches in flight to hide the request-midstate
+    // chains (latency ~ request bytes / 64 compressions) behind the forwards
+    const int depth = 5;
+    const size_t arena_max = (size_t)B * (512 + 160 * N) + 1024;
+    for (int i = 0; i < depth; i++) {
+      auto S = std::make_unique<IngestSlot>();
+      CG_CUDA(cudaStreamCreateWithFlags(&S->stream, cudaStreamNonBlocking));
+      CG_CUDA(cudaEventCreateWithFlags(&S->ev_staged, cudaEventDisableTiming));
+      CG_CUDA(cudaEventCreateWithFlags(&S->ev_prefix, cudaEventDisableTiming));
+      CG_CUDA(cudaEventCreateWithFlags(&S->ev_done, cudaEventDisableTiming));
+      S->d_in.ensure(B * g->u);
+      S->d_eps.ensure(B);
+      S->d_arena.ensure(arena_max);
+      S->d_reqids.ensure(32 * B);
+      S->d_jobs.ensure(B * (1 + 2 * N));
+      S->d_mid.ensure(8 * B);
+      S->d_tree.ensure(2 * N);
+      S->h_arena.ensure(arena_max);
+      S->h_reqids.ensure(32 * B);
+      S->h_jobs.ensure(B * (1 + 2 * N));
+      S->h_eps.ensure(B);
+      S->h_tree.ensure(2 * N);
+      g->slots.push_back(std::move(S));
+    }
     *out = g.release();
     return CG_OK;
   });
@@ -1009,18 +1045,32 @@ void cg_group_free(cg_group* g) {
   if (!g) return;
   cudaSetDevice(g->ctx->device);
   cudaStreamSynchronize(g->ctx->stream);
-  cudaStreamSynchronize(g->ctx->side);
-  if (g->ev_staged) cudaEventDestroy(g->ev_staged);
-  if (g->ev_prefix) cudaEventDestroy(g->ev_prefix);
-  if (g->ev_inputs) cudaEventDestroy(g->ev_inputs);
+  for (auto& s : g->slots) cudaStreamSynchronize(s->stream);
   delete g;
+}
+
+int cg_ingest_batch(cg_group* g, const cg_request_batch* batch, uint64_t* ticket) {
+  if (!g || !batch || !ticket) return CG_EINVAL;
+  return guarded(g->ctx, [&] {
+    *ticket = ingest(g, batch);
+    return CG_OK;
+  });
+}
+
+int cg_certify_ticket(cg_group* g, uint64_t ticket, cg_certify_out* out) {
+  if (!g) return CG_EINVAL;
+  return guarded(g->ctx, [&] {
+    certify(g, ticket, nullptr);
+    if (out) certify_fetch(g, out);
+    return CG_OK;
+  });
 }
 
 int cg_certify_batch(cg_group* g, const cg_request_batch* batch,
                      cg_certify_out* out) {
   if (!g || !batch) return CG_EINVAL;
   return guarded(g->ctx, [&] {
-    certify_enqueue(g, batch, nullptr);
+    certify(g, ingest(g, batch), nullptr);
     if (out) certify_fetch(g, out);
     return CG_OK;
   });
@@ -1030,7 +1080,7 @@ int cg_certify_outputs(cg_group* g, const cg_request_batch* batch,
                        const double* outputs, cg_certify_out* out) {
   if (!g || !batch || !outputs) return CG_EINVAL;
   return guarded(g->ctx, [&] {
-    certify_enqueue(g, batch, outputs);
+    certify(g, ingest(g, batch), outputs);
     if (out) certify_fetch(g, out);
     return CG_OK;
   });

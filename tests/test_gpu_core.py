@@ -205,3 +205,25 @@ def test_certify_batch_invariant(ctx):
     for k in (0, 5, B - 1):
         one = grp.certify(RequestBatch.from_encoded([reqs[k]]), want_leaves=True)
         assert np.array_equal(one["leaf_hashes"][:, 0], full["leaf_hashes"][:, k])
+
+
+def test_ingest_ahead_and_out_of_order(ctx):
+    """Tickets ingested ahead certify to the same results in any order; a
+    full ring is an error, not a hang."""
+    from paper_2205_15757_b200 import InvalidArgument, RequestBatch
+    g = golden("c1_batch.npz")
+    grp = _group(ctx, g, int(g["B"]))
+    reqs = split_reqs(g)
+    b = RequestBatch.from_encoded(reqs)
+    half = RequestBatch.from_encoded(reqs[:6])
+    want = grp.certify(b)
+    want_half = grp.certify(half)
+    t = [grp.ingest(b), grp.ingest(half), grp.ingest(b), grp.ingest(half), grp.ingest(b)]
+    with pytest.raises(InvalidArgument):
+        grp.ingest(b)
+    order = [3, 0, 4, 1, 2]
+    for i in order:
+        r = grp.certify_ticket(t[i])
+        w = want if i % 2 == 0 else want_half
+        assert np.array_equal(r["a_root"], w["a_root"]) and np.array_equal(r["r_roots"], w["r_roots"])
+    assert np.array_equal(want["a_root"], g["honest_a_root"])
