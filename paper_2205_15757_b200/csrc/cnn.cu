@@ -26,32 +26,75 @@ namespace {
 using bf16 = __nv_bfloat16;
 
 // ------------------------------------------------------------------ kernels
-// conv1 operand: f64 CHW image -> [B*Ho*Wo, Kp] bf16, K = (dr*7+ds)*3 + c,
-// stride 2, pad 3, zero beyond K = 147. Replica-independent.
-__global__ void conv1_im2col_kernel(const double* __restrict__ in, int B, int S,
-                                    int Ho, int Kp, bf16* __restrict__ out) {
-  const int chunks = Kp / 8;
+// Pass 1 of the conv1 operand: f64 CHW -> bf16 NHWC4 on a grid padded by 3
+// (channel 3 and the border are zero). Coalesced on both sides: adjacent
+// threads read adjacent doubles of each channel plane and write 8 B each.
+__global__ void chw_to_nhwc4_pad3_kernel(const double* __restrict__ in, int B, int S,
+                                         uint2* __restrict__ out) {
+  const int Sp = S + 6;
   size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  size_t row = t / chunks;
-  int ch = (int)(t - row * chunks);
-  if (row >= (size_t)B * Ho * Ho) return;
-  int n = (int)(row / (Ho * Ho)), rem = (int)(row - (size_t)n * Ho * Ho);
-  int ho = rem / Ho, wo = rem - ho * Ho;
-  __align__(16) bf16 v[8];
+  if (t >= (size_t)B * Sp * Sp) return;
+  int n = (int)(t / ((size_t)Sp * Sp)), rem = (int)(t - (size_t)n * Sp * Sp);
+  int hp = rem / Sp, wp = rem - hp * Sp;
+  int h = hp - 3, w = wp - 3;
+  const bool inside = h >= 0 && h < S && w >= 0 && w < S;
+  __align__(8) bf16 b[4];
 #pragma unroll
-  for (int j = 0; j < 8; j++) {
-    int k = ch * 8 + j;
-    double x = 0.0;
-    if (k < 147) {
-      int tap = k / 3, c = k - tap * 3;
-      int dr = tap / 7, ds = tap - dr * 7;
-      int h = 2 * ho - 3 + dr, w = 2 * wo - 3 + ds;
-      if (h >= 0 && h < S && w >= 0 && w < S)
-        x = __ldg(in + (((size_t)n * 3 + c) * S + h) * S + w);
-    }
-    v[j] = __double2bfloat16(x);
+  for (int k = 0; k < 3; k++)  // one f64 -> bf16 rounding, as the direct im2col
+    b[k] = __double2bfloat16(inside ? __ldg(in + (((size_t)n * 3 + k) * S + h) * S + w) : 0.0);
+  b[3] = __float2bfloat16(0.f);
+  out[t] = *reinterpret_cast<uint2*>(b);
+}
+
+// Pass 2: [B*Ho*Wo, 192] im2col from the padded NHWC4 grid (K = (dr*7+ds)*3+c,
+// zero beyond 147). A warp builds 32 consecutive output rows: lane = row,
+// taps loaded as 8-byte pixels (adjacent lanes read pixels 16 B apart), the
+// row assembled 16 B at a time in a padded smem tile (row stride 25 x 16 B,
+// conflict-free), then written out as one contiguous 12 KB block.
+constexpr int kIm2colWarps = 3;
+__global__ void __launch_bounds__(32 * kIm2colWarps) conv1_im2col_nhwc4_kernel(
+    const uint2* __restrict__ px, int B, int S, int Ho, bf16* __restrict__ out) {
+  __shared__ uint4 tile[kIm2colWarps][32 * 25];
+  const int Sp = S + 6, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const size_t rows = (size_t)B * Ho * Ho;
+  const size_t row0 = ((size_t)blockIdx.x * kIm2colWarps + w) * 32;
+  if (row0 >= rows) return;
+  const size_t row = row0 + lane;
+  const bool valid = row < rows;
+  int n = 0, ho = 0, wo = 0;
+  if (valid) {
+    n = (int)(row / (Ho * Ho));
+    int rem = (int)(row - (size_t)n * Ho * Ho);
+    ho = rem / Ho;
+    wo = rem - ho * Ho;
   }
-  *reinterpret_cast<uint4*>(out + row * Kp + ch * 8) = *reinterpret_cast<uint4*>(v);
+  const uint2* base = px + ((size_t)n * Sp + 2 * ho) * Sp + 2 * wo;
+  uint4* my = &tile[w][lane * 25];
+  uint32_t buf[4] = {0, 0, 0, 0};  // 8 bf16 = one 16-byte chunk
+  int fill = 0, chunk = 0;
+  auto put = [&](uint32_t bf16_bits) {  // append one bf16
+    if (fill & 1) buf[fill >> 1] |= bf16_bits << 16;
+    else buf[fill >> 1] = bf16_bits;
+    if (++fill == 8) {
+      my[chunk++] = make_uint4(buf[0], buf[1], buf[2], buf[3]);
+      fill = 0;
+    }
+  };
+#pragma unroll 1
+  for (int dr = 0; dr < 7; dr++) {
+#pragma unroll
+    for (int ds = 0; ds < 7; ds++) {
+      uint2 p = valid ? __ldg(base + dr * Sp + ds) : make_uint2(0, 0);
+      put(p.x & 0xffffu);
+      put(p.x >> 16);
+      put(p.y & 0xffffu);
+    }
+  }
+  while (chunk < 24) put(0);  // K 147 -> 192
+  __syncwarp();
+  const size_t nrow = rows - row0 < 32 ? rows - row0 : 32;
+  uint4* dst = reinterpret_cast<uint4*>(out + row0 * 192);
+  for (int i = lane; i < (int)nrow * 24; i += 32) dst[i] = tile[w][(i / 24) * 25 + i % 24];
 }
 
 // 3x3/2 max pool, pad 1 (torch pads with -inf).
@@ -305,6 +348,7 @@ class ResNet final : public CnnModel {
       return reinterpret_cast<bf16*>(p);
     };
     xcol_ = alloc(B * H1 * H1 * 192);
+    nhwc4_ = alloc(B * (S_ + 6) * (S_ + 6) * 4);
     c1out_ = alloc(B * H1 * H1 * 64);
     size_t act = 0, t2 = 0, dsz = 0, g3 = 0, g1 = 0;
     for (auto& b : blocks_) {
@@ -337,10 +381,16 @@ class ResNet final : public CnnModel {
   }
 
   void prepare_input(const double* d_in, uint32_t B, void* prepped, cudaStream_t st) override {
-    const int H1 = S_ / 2;
-    size_t threads = (size_t)B * H1 * H1 * (192 / 8);
-    conv1_im2col_kernel<<<grid_for(threads), 256, 0, st>>>(d_in, B, S_, H1, 192,
-                                                           reinterpret_cast<bf16*>(prepped));
+    const int H1 = S_ / 2, Sp = S_ + 6;
+    if (B > maxB_) reserve(B);
+    // two coalesced passes: f64 CHW -> bf16 NHWC4 (pad 3), then im2col
+    chw_to_nhwc4_pad3_kernel<<<grid_for((size_t)B * Sp * Sp), 256, 0, st>>>(
+        d_in, B, S_, reinterpret_cast<uint2*>(nhwc4_));
+    CG_CHECK_LAUNCH();
+    size_t rows = (size_t)B * H1 * H1;
+    conv1_im2col_nhwc4_kernel<<<(unsigned)ceil_div(rows, 32 * kIm2colWarps), 32 * kIm2colWarps,
+                                0, st>>>(reinterpret_cast<const uint2*>(nhwc4_), B, S_, H1,
+                                         reinterpret_cast<bf16*>(prepped));
     CG_CHECK_LAUNCH();
   }
 
@@ -558,7 +608,7 @@ class ResNet final : public CnnModel {
   std::vector<Block> blocks_;
   uint32_t maxB_ = 0;
   std::vector<void*> bufs_;
-  bf16 *xcol_ = nullptr, *c1out_ = nullptr, *act_[2] = {nullptr, nullptr}, *t2_ = nullptr,
+  bf16 *xcol_ = nullptr, *nhwc4_ = nullptr, *c1out_ = nullptr, *act_[2] = {nullptr, nullptr}, *t2_ = nullptr,
        *ds_ = nullptr, *g3_ = nullptr, *g1_ = nullptr, *pooled_ = nullptr;
   std::map<std::pair<int, int>, bf16*> pads_;
   std::map<uint32_t, Plan> plans_;

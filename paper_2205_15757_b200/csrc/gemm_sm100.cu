@@ -78,6 +78,19 @@ __device__ __forceinline__ uint2 lds_u2(uint32_t addr) {
 __device__ __forceinline__ void stg_u2(void* p, uint2 v) {
   asm volatile("st.global.v2.u32 [%0], {%1, %2};" ::"l"(p), "r"(v.x), "r"(v.y) : "memory");
 }
+__device__ __forceinline__ uint4 lds_u4(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(addr)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ void stg_u4(void* p, uint4 v) {
+  asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y),
+               "r"(v.z), "r"(v.w)
+               : "memory");
+}
 __device__ __forceinline__ void stg_f4(void* p, float4 v) {
   asm volatile("st.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y),
                "f"(v.z), "f"(v.w)
@@ -259,7 +272,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     //     writes 4 contiguous 64-byte row segments.
     const int q = warp & 3, h = (warp - 2) >> 2;
     const uint32_t stg_a = su32(s_epi + (warp - 2) * (32 * kStgLd));
-    const int rr = lane >> 3, cgp = lane & 7;
+    const int rr8 = lane >> 2, cg8 = lane & 3;
     constexpr int CPT = BN / 32;  // 32-column chunks per tile
     const bool issuer = res_tma && warp == 2 && lane == 0;
     int next_issue = 0;
@@ -303,45 +316,61 @@ __global__ void __launch_bounds__(kThreads, 1)
           sts_v4(stg_a + 4 * (lane * kStgLd + 4 * j), v[4 * j], v[4 * j + 1], v[4 * j + 2],
                  v[4 * j + 3]);
         __syncwarp();
-        const int n = n0 + c * 32 + cgp * 4;
+        // phase 2: lane = (row rr8 of 8, 8-column group cg8 of 4): 16-byte
+        // stores, each warp store instruction covers 8 rows x 64 B.
+        const int n = n0 + c * 32 + cg8 * 8;
         const bool col_ok = n < a.N;
-        float b4[4] = {0.f, 0.f, 0.f, 0.f};
+        float b8[8];
         if (col_ok) {
-          const float4 bb = __ldg(reinterpret_cast<const float4*>(a.bias + n));
-          b4[0] = bb.x; b4[1] = bb.y; b4[2] = bb.z; b4[3] = bb.w;
+          const float4 b0 = __ldg(reinterpret_cast<const float4*>(a.bias + n));
+          const float4 b1 = __ldg(reinterpret_cast<const float4*>(a.bias + n + 4));
+          b8[0] = b0.x; b8[1] = b0.y; b8[2] = b0.z; b8[3] = b0.w;
+          b8[4] = b1.x; b8[5] = b1.y; b8[6] = b1.z; b8[7] = b1.w;
+        } else {
+#pragma unroll
+          for (int e = 0; e < 8; e++) b8[e] = 0.f;
         }
         const int slot = kResSlots > 0 ? g % kResSlots : 0;
-        const uint32_t rs_a = su32(s_res + slot * (128 * 32 * 2) + (q * 32) * 64 + cgp * 8);
+        const uint32_t rs_a = su32(s_res + slot * (128 * 32 * 2) + (q * 32) * 64 + cg8 * 16);
         if (res_tma) mbar_wait(&rfull[slot], (g / (kResSlots > 0 ? kResSlots : 1)) & 1);
-#pragma unroll 4
-        for (int it = 0; it < 8; it++) {
-          const int r = it * 4 + rr;
+#pragma unroll 2
+        for (int it = 0; it < 4; it++) {
+          const int r = it * 8 + rr8;
           const int orow = __shfl_sync(0xffffffffu, my_orow, r);
           const bool ok = orow >= 0 && col_ok;
-          const float4 acc4 = lds_f4(stg_a + 4 * (r * kStgLd + cgp * 4));
-          float x[4] = {acc4.x + b4[0], acc4.y + b4[1], acc4.z + b4[2], acc4.w + b4[3]};
+          const float4 p0 = lds_f4(stg_a + 4 * (r * kStgLd + cg8 * 8));
+          const float4 p1 = lds_f4(stg_a + 4 * (r * kStgLd + cg8 * 8 + 4));
+          float x[8] = {p0.x + b8[0], p0.y + b8[1], p0.z + b8[2], p0.w + b8[3],
+                        p1.x + b8[4], p1.y + b8[5], p1.z + b8[6], p1.w + b8[7]};
           if (a.residual) {
-            uint2 rv = make_uint2(0, 0);
-            if (res_tma) rv = lds_u2(rs_a + r * 64);
-            else if (ok) rv = __ldg(reinterpret_cast<const uint2*>(a.residual + (size_t)orow * a.ld_res + n));
-            x[0] += __uint_as_float(rv.x << 16);
-            x[1] += __uint_as_float(rv.x & 0xffff0000u);
-            x[2] += __uint_as_float(rv.y << 16);
-            x[3] += __uint_as_float(rv.y & 0xffff0000u);
+            uint4 rv = make_uint4(0, 0, 0, 0);
+            if (res_tma) rv = lds_u4(rs_a + r * 64);
+            else if (ok) rv = __ldg(reinterpret_cast<const uint4*>(a.residual + (size_t)orow * a.ld_res + n));
+            const uint32_t w[4] = {rv.x, rv.y, rv.z, rv.w};
+#pragma unroll
+            for (int e = 0; e < 4; e++) {
+              x[2 * e] += __uint_as_float(w[e] << 16);
+              x[2 * e + 1] += __uint_as_float(w[e] & 0xffff0000u);
+            }
           }
           if (a.relu) {
 #pragma unroll
-            for (int e = 0; e < 4; e++) x[e] = fmaxf(x[e], 0.f);
+            for (int e = 0; e < 8; e++) x[e] = fmaxf(x[e], 0.f);
           }
           if (ok) {
             if (a.out_f32) {
-              stg_f4(reinterpret_cast<float*>(a.out) + (size_t)orow * a.ld_out + n,
-                     make_float4(x[0], x[1], x[2], x[3]));
+              float* op = reinterpret_cast<float*>(a.out) + (size_t)orow * a.ld_out + n;
+              stg_f4(op, make_float4(x[0], x[1], x[2], x[3]));
+              stg_f4(op + 4, make_float4(x[4], x[5], x[6], x[7]));
             } else {
-              __nv_bfloat162 o0 = __floats2bfloat162_rn(x[0], x[1]);
-              __nv_bfloat162 o1 = __floats2bfloat162_rn(x[2], x[3]);
-              stg_u2(reinterpret_cast<__nv_bfloat16*>(a.out) + (size_t)orow * a.ld_out + n,
-                     make_uint2(*reinterpret_cast<uint32_t*>(&o0), *reinterpret_cast<uint32_t*>(&o1)));
+              uint32_t o[4];
+#pragma unroll
+              for (int e = 0; e < 4; e++) {
+                __nv_bfloat162 t = __floats2bfloat162_rn(x[2 * e], x[2 * e + 1]);
+                o[e] = *reinterpret_cast<uint32_t*>(&t);
+              }
+              stg_u4(reinterpret_cast<__nv_bfloat16*>(a.out) + (size_t)orow * a.ld_out + n,
+                     make_uint4(o[0], o[1], o[2], o[3]));
             }
           }
         }
@@ -432,7 +461,7 @@ void launch_conv_gemm(const Operand& A, const Operand& B, const ConvGemmArgs& a,
   if (a.Kc % 64 || a.ntaps < 1 || a.ntaps > 9) throw InvalidArgument("conv_gemm: bad K");
   if (A.box_rows != BM || B.box_rows != BN) throw InvalidArgument("conv_gemm: box mismatch");
   if (!a.out_f32 && (a.N % 32)) throw InvalidArgument("conv_gemm: bf16 out needs N%32==0");
-  if (a.out_f32 && (a.N % 4)) throw InvalidArgument("conv_gemm: f32 out needs N%4==0");
+  if (a.out_f32 && (a.N % 8)) throw InvalidArgument("conv_gemm: f32 out needs N%8==0");
   // residual operand: [rows_out, ld_res] bf16, box 32 cols x 128 rows, no swizzle
   CUtensorMap R;
   if (a.residual && a.row_mode == kRowIdentity) {
