@@ -161,7 +161,7 @@ int cg_group_fetch(cg_group* g, cg_certify_out* out);
  * InferenceEngine::submit (src/engine.cpp:182-209) — framing bytes, upload,
  * and the request-midstate SHA-256 chains started on a per-batch stream —
  * and certify = execute_batch + R trees + try_attest for that ticket. Up to
- * 5 batches may be ingested ahead; tickets are certified in any order. */
+ * 8 batches may be ingested ahead; tickets are certified in any order. */
 int cg_ingest_batch(cg_group* g, const cg_request_batch* batch, uint64_t* ticket);
 int cg_certify_ticket(cg_group* g, uint64_t ticket, cg_certify_out* out);
 /* Agreement + digest path over precomputed replica outputs (host memory,

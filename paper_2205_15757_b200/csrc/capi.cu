@@ -26,6 +26,7 @@
 #include "cnn.cuh"
 #include "common.cuh"
 #include "digest.cuh"
+#include "gemm_sm100.cuh"
 
 namespace cg {
 
@@ -852,7 +853,7 @@ uint64_t ingest(cg_group* g, const cg_request_batch* bt) {
   if (!bt->inputs_on_device)
     CG_CUDA(cudaMemcpyAsync(S.d_in.p, bt->inputs, 8 * u * B, cudaMemcpyHostToDevice, st));
   CG_CUDA(cudaEventRecord(S.ev_staged, st));
-  launch_chain_jobs(S.d_jobs.p, B, st);
+  launch_chain_jobs(S.d_jobs.p, B, st, /*exclusive_sm=*/true);
   CG_CUDA(cudaEventRecord(S.ev_prefix, st));
   S.used = true;
   S.ever = true;
@@ -877,6 +878,12 @@ void certify(cg_group* g, uint64_t ticket, const double* precomputed_outputs) {
     CG_CUDA(cudaMemcpyAsync(g->d_outs.p, precomputed_outputs, 8 * (size_t)N * B * v,
                             cudaMemcpyHostToDevice, st));
   } else {
+    // leave one SM per in-flight midstate-chain CTA to the chains
+    int chain_ctas = 0;
+    for (auto& o : g->slots)
+      if (o.get() != &S && o->used && cudaEventQuery(o->ev_prefix) == cudaErrorNotReady)
+        chain_ctas += (int)ceil_div(o->B, 64);
+    set_gemm_sm_budget(kNumSMs - chain_ctas);
     const void* prepped = nullptr;
     if (g->all_cnn) {  // replica-independent input stage, once per batch
       g->models[0]->cnn->prepare_input(S.d_in_ptr, B, g->d_prep.p, st);
@@ -897,6 +904,7 @@ void certify(cg_group* g, uint64_t ticket, const double* precomputed_outputs) {
                                 g->topk, ti, tv, st);
       }
     }
+    set_gemm_sm_budget(kNumSMs);
   }
   CG_CUDA(cudaStreamWaitEvent(st, S.ev_prefix, 0));
   launch_chain_jobs(S.d_jobs.p + B, N * B, st);  // result leaves
@@ -1014,7 +1022,7 @@ int cg_group_create(cg_ctx* ctx, cg_model* const* models, uint32_t N,
     if (g->all_cnn) g->d_prep.ensure(g->models[0]->cnn->prepared_bytes(max_batch));
     // ingest ring: enough batches in flight to hide the request-midstate
     // chains (latency ~ request bytes / 64 compressions) behind the forwards
-    const int depth = 5;
+    const int depth = 8;
     const size_t arena_max = (size_t)B * (512 + 160 * N) + 1024;
     for (int i = 0; i < depth; i++) {
       auto S = std::make_unique<IngestSlot>();

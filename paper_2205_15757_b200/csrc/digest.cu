@@ -27,11 +27,22 @@ __global__ void __launch_bounds__(64) chain_jobs_kernel(const ChainJob* jobs,
   run_chain_job(j, digest_out);
 }
 
-void launch_chain_jobs(const ChainJob* d_jobs, uint32_t n, cudaStream_t st) {
+void launch_chain_jobs(const ChainJob* d_jobs, uint32_t n, cudaStream_t st,
+                       bool exclusive_sm) {
   if (n == 0) return;
   const int tpb = 64;
+  // exclusive_sm: claim (unused) shared memory so the CTA can never share an
+  // SM with a persistent GEMM CTA (~200 KB); long chains then run on their
+  // own SMs instead of slowing one statically scheduled GEMM CTA.
+  static bool attr = false;
+  if (!attr) {
+    CG_CUDA(cudaFuncSetAttribute(chain_jobs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 kChainExclusiveSmem));
+    attr = true;
+  }
   timer_begin(st, kTimeChain);
-  chain_jobs_kernel<<<(unsigned)ceil_div(n, tpb), tpb, 0, st>>>(d_jobs, n);
+  chain_jobs_kernel<<<(unsigned)ceil_div(n, tpb), tpb, exclusive_sm ? kChainExclusiveSmem : 0,
+                      st>>>(d_jobs, n);
   CG_CHECK_LAUNCH();
   timer_end(st, kTimeChain);
 }

@@ -427,7 +427,8 @@ void launch_t(const Operand& A, const Operand& B, const CUtensorMap& R,
     attr = true;
   }
   int tiles = ((a.M + BM - 1) / BM) * ((a.N + BN - 1) / BN);
-  int grid = tiles < kNumSMs ? tiles : kNumSMs;
+  const int budget = gemm_sm_budget();
+  int grid = tiles < budget ? tiles : budget;
   if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
   timer_begin(st, kTimeGemm);
   conv_gemm_kernel<BN, STAGES, RS><<<grid, kThreads, smem, st>>>(A.map, B.map, R, a);
@@ -436,6 +437,12 @@ void launch_t(const Operand& A, const Operand& B, const CUtensorMap& R,
 }
 
 }  // namespace
+
+static std::atomic<int> g_sm_budget{kNumSMs};
+void set_gemm_sm_budget(int sms) {
+  g_sm_budget = sms < 1 ? 1 : (sms > kNumSMs ? kNumSMs : sms);
+}
+int gemm_sm_budget() { return g_sm_budget.load(); }
 
 void make_operand(Operand& op, const void* ptr, int rows, int cols, int box_rows) {
   if (cols % 64 != 0) throw InvalidArgument("operand K must be a multiple of 64");

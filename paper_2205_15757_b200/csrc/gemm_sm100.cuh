@@ -51,6 +51,12 @@ struct Operand {
 
 void make_operand(Operand& op, const void* ptr, int rows, int cols, int box_rows);
 
+// SMs the persistent GEMM grid may occupy (default all 148). The certify
+// pipeline lowers it while request-midstate chains run on their own SMs, so
+// no statically scheduled GEMM CTA ever shares an SM with a chain CTA.
+void set_gemm_sm_budget(int sms);
+int gemm_sm_budget();
+
 // Launches the persistent warp-specialised kernel; BN in {64, 128, 256}.
 void launch_conv_gemm(const Operand& A, const Operand& B, const ConvGemmArgs& a,
                       int BN, cudaStream_t st, int max_ctas = 0);
