@@ -11,6 +11,7 @@
 #include <cuda_bf16.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <map>
@@ -246,6 +247,8 @@ struct Block {
 // Tile width: minimise waves x BN / eff(BN), where eff reflects that a
 // 128 x 64 tile is shared-memory-bandwidth bound (A is re-read per 64
 // columns) while 128 x 256 streams A once per 256 columns. Ties -> wider.
+int kSmallKMaxBN = 256;  // env CREDO_SMALLK_BN overrides (tuning)
+
 int pick_bn(int rows, int N) {
   int best = 64;
   double best_cost = 1e30;
@@ -484,6 +487,10 @@ class ResNet final : public CnnModel {
     auto opA = std::make_shared<Operand>();
     auto opB = std::make_shared<Operand>();
     int BN = pick_bn(M, c.cout);
+    if (const char* e = std::getenv("CREDO_SMALLK_BN")) kSmallKMaxBN = std::atoi(e);
+    // Small-K 1x1 layers are epilogue/HBM bound: narrower tiles halve the
+    // serial per-warp epilogue work per tile (the MMA has nothing to hide it).
+    if (c.Kc * ntaps <= 128 && BN > kSmallKMaxBN) BN = kSmallKMaxBN;
     make_operand(*opA, A, rowsA, c.Kc, 128);
     make_operand(*opB, c.w, c.cout, c.Kc * ntaps, BN);
     ConvGemmArgs a{};

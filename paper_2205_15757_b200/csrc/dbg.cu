@@ -73,6 +73,68 @@ extern "C" int cg_dbg_sha_bench(cg_ctx* ctx, int mode, uint64_t nblocks,
   }
 }
 
+// Timing + CTA-0 event trace of one 1x1 conv GEMM shape on device-resident
+// random operands (no host copies in the timed launch).
+extern "C" int cg_dbg_gemm_trace(cg_ctx* ctx, int M, int N, int K, int BN, int residual,
+                                 long long* trace_host, double* us) {
+  try {
+    cudaStream_t st = (cudaStream_t)cg_ctx_stream(ctx);
+    void *dA, *dB, *dbias, *dres = nullptr, *dout;
+    long long* dtr;
+    CG_CUDA(cudaMalloc(&dA, (size_t)M * K * 2));
+    CG_CUDA(cudaMalloc(&dB, (size_t)N * K * 2));
+    CG_CUDA(cudaMalloc(&dbias, (size_t)N * 4));
+    CG_CUDA(cudaMalloc(&dout, (size_t)M * N * 2));
+    CG_CUDA(cudaMalloc(&dtr, 8 * 64 * 8));
+    CG_CUDA(cudaMemset(dA, 0x11, (size_t)M * K * 2));
+    CG_CUDA(cudaMemset(dB, 0x11, (size_t)N * K * 2));
+    CG_CUDA(cudaMemset(dbias, 0, (size_t)N * 4));
+    CG_CUDA(cudaMemset(dtr, 0, 8 * 64 * 8));
+    if (residual) {
+      CG_CUDA(cudaMalloc(&dres, (size_t)M * N * 2));
+      CG_CUDA(cudaMemset(dres, 0x11, (size_t)M * N * 2));
+    }
+    Operand oa, ob;
+    make_operand(oa, dA, M, K, 128);
+    make_operand(ob, dB, N, K, BN);
+    ConvGemmArgs a{};
+    a.M = M;
+    a.N = N;
+    a.Kc = K;
+    a.ntaps = 1;
+    a.bias = (const float*)dbias;
+    a.residual = (const __nv_bfloat16*)dres;
+    a.ld_res = N;
+    a.out = dout;
+    a.ld_out = N;
+    a.relu = 1;
+    a.rows_out = M;
+    launch_conv_gemm(oa, ob, a, BN, st);  // warm
+    cudaEvent_t e0, e1;
+    CG_CUDA(cudaEventCreate(&e0));
+    CG_CUDA(cudaEventCreate(&e1));
+    CG_CUDA(cudaEventRecord(e0, st));
+    for (int i = 0; i < 5; i++) launch_conv_gemm(oa, ob, a, BN, st);
+    CG_CUDA(cudaEventRecord(e1, st));
+    a.trace = dtr;
+    launch_conv_gemm(oa, ob, a, BN, st);
+    CG_CUDA(cudaStreamSynchronize(st));
+    float ms = 0;
+    CG_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    *us = 1000.0 * ms / 5;
+    CG_CUDA(cudaMemcpy(trace_host, dtr, 8 * 64 * 8, cudaMemcpyDeviceToHost));
+    cudaFree(dA);
+    cudaFree(dB);
+    cudaFree(dbias);
+    cudaFree(dout);
+    cudaFree(dtr);
+    if (dres) cudaFree(dres);
+    return CG_OK;
+  } catch (const std::exception&) {
+    return CG_ECUDA;
+  }
+}
+
 extern "C" int cg_dbg_conv_gemm(cg_ctx* ctx, const uint16_t* A, int rowsA,
                                 const uint16_t* B, int N, int Kc, int ntaps,
                                 const int* tap_off, const float* bias,

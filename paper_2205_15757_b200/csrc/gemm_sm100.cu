@@ -13,7 +13,8 @@
 namespace cg {
 namespace {
 
-constexpr int BM = 128, BK = 64, kThreads = 320;  // 2 + 8 warps
+// warps: 0 TMA producer, 1 MMA issuer, 2-9 epilogue, 10 residual loader
+constexpr int BM = 128, BK = 64, kThreads = 352;
 constexpr int kEpiWarps = 8, kStgLd = 36;        // staging row stride (floats)
 constexpr int A_BYTES = BM * BK * 2;
 
@@ -31,14 +32,27 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
 }
+#ifndef CG_MBAR_SUSPEND_NS
+#define CG_MBAR_SUSPEND_NS 0  // 0: hardware default try_wait window (no hint)
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+#if CG_MBAR_SUSPEND_NS > 0
   asm volatile(
       "{\n\t.reg .pred p;\n"
       "WAIT_%=:\n\t"
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
       "@!p bra WAIT_%=;\n}" ::"r"(su32(b)),
-      "r"(parity), "r"(0x989680)
+      "r"(parity), "r"(CG_MBAR_SUSPEND_NS)
       : "memory");
+#else
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(su32(b)),
+      "r"(parity)
+      : "memory");
+#endif
 }
 __device__ __forceinline__ void tma_load_2d(const CUtensorMap* tm, uint64_t* bar,
                                             void* dst, int x, int y) {
@@ -122,6 +136,33 @@ __device__ __forceinline__ uint64_t smem_desc_sw128(const void* p) {
   return ((addr >> 4) & 0x3FFFull) | (1ull << 16) | (64ull << 32) | (1ull << 46) |
          (2ull << 61);
 }
+// tcgen05.ld without the wait (the registers are valid after tmem_ld_wait).
+__device__ __forceinline__ void tmem_ld32_issue(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+        "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]),
+        "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]),
+        "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+        "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]),
+        "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+}
+// Waits for outstanding tcgen05.ld; the "+r" operands keep the compiler from
+// reading v[] before the wait.
+__device__ __forceinline__ void tmem_ld_wait(uint32_t (&v)[32]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]),
+                 "+r"(v[6]), "+r"(v[7]), "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]),
+                 "+r"(v[12]), "+r"(v[13]), "+r"(v[14]), "+r"(v[15]), "+r"(v[16]),
+                 "+r"(v[17]), "+r"(v[18]), "+r"(v[19]), "+r"(v[20]), "+r"(v[21]),
+                 "+r"(v[22]), "+r"(v[23]), "+r"(v[24]), "+r"(v[25]), "+r"(v[26]),
+                 "+r"(v[27]), "+r"(v[28]), "+r"(v[29]), "+r"(v[30]), "+r"(v[31])
+               :
+               : "memory");
+}
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
@@ -135,6 +176,32 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
         "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// TMA bulk store of a [32 rows x 32 cols] bf16 box from (64B-swizzled) smem.
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* tm, uint32_t src, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(tm),
+      "r"(src), "r"(x), "r"(y)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {  // <= N groups still reading smem
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+// 16-byte chunk j of 64-byte row r under the 64B TMA swizzle (addr bits
+// [4,6) ^= bits [7,9)).
+__device__ __forceinline__ uint32_t sw64(int r, int j) {
+  return (uint32_t)(r * 64 + 16 * (j ^ ((r >> 1) & 3)));
 }
 
 __device__ __forceinline__ int remap_row(int M, int rows_out, int mode, int H,
@@ -154,31 +221,40 @@ __device__ __forceinline__ int remap_row(int M, int rows_out, int mode, int H,
   return img * HpWp + (h + 1) * Wp + w + 1;
 }
 
+#define CG_TRACE(slot, i)                                             \
+  do {                                                                \
+    if (a.trace && blockIdx.x == 0 && (i) < 64 && (lane == 0))        \
+      a.trace[(slot) * 64 + (i)] = clock64();                         \
+  } while (0)
+
 template <int BN, int STAGES, int kResSlots>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                      const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmR,
+                     const __grid_constant__ CUtensorMap tmO,
                      const ConvGemmArgs a) {
   constexpr int B_BYTES = BN * BK * 2;
   constexpr uint32_t TMEM_COLS = 2 * BN;
   extern __shared__ uint8_t smem_raw[];
+  // 1024-aligned regions first: operand ring (128B swizzle), residual ring and
+  // output staging (64B swizzle), then barriers.
   uint8_t* smem = smem_raw + ((1024 - (su32(smem_raw) & 1023)) & 1023);
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
+  uint8_t* s_res = sB + STAGES * B_BYTES;  // kResSlots x [128 x 32] bf16 (SW64)
+  float* s_epi = reinterpret_cast<float*>(s_res + kResSlots * 8192);  // 36 KB
+  uint64_t* full = reinterpret_cast<uint64_t*>(s_epi + kEpiWarps * 32 * kStgLd);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  int* s_tap = reinterpret_cast<int*>(tmem_slot + 4);
-  float* s_epi = reinterpret_cast<float*>(s_tap + 12);  // 8 warps x 32 x 36 fp32
-  uint64_t* rfull = reinterpret_cast<uint64_t*>(s_epi + kEpiWarps * 32 * kStgLd);
+  uint64_t* rfull = tempty + 2;
   uint64_t* rempty = rfull + (kResSlots > 0 ? kResSlots : 1);
-  // residual ring: kResSlots x [128 rows x 32 cols] bf16, TMA-filled
-  uint8_t* s_res = reinterpret_cast<uint8_t*>(rempty + (kResSlots > 0 ? kResSlots : 1));
-  s_res += (128 - (su32(s_res) & 127)) & 127;
-  const bool res_tma = kResSlots > 0 && a.residual != nullptr && a.row_mode == kRowIdentity;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rempty + (kResSlots > 0 ? kResSlots : 1));
+  int* s_tap = reinterpret_cast<int*>(tmem_slot + 4);
+  // identity rows + bf16 out: thread-per-row epilogue, TMA bulk stores
+  const bool tma_out = a.row_mode == kRowIdentity && !a.out_f32;
+  const bool res_tma = kResSlots > 0 && a.residual != nullptr && tma_out;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int num_n = (a.N + BN - 1) / BN, num_m = (a.M + BM - 1) / BM;
@@ -223,11 +299,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {  // ---------------- TMA producer
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+      int ti = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x, ti++) {
         const int m0 = (t / num_n) * BM, n0 = (t % num_n) * BN;
+        CG_TRACE(0, ti);
         for (int kb = 0; kb < num_k; kb++) {
           const int tap = kb / kpt, cb = kb - tap * kpt;
           mbar_wait(&empty[stage], phase ^ 1);
+          if (kb == 0) CG_TRACE(1, ti);
           mbar_expect_tx(&full[stage], A_BYTES + B_BYTES);
           tma_load_2d(&tmA, &full[stage], sA + stage * A_BYTES, cb * BK,
                       m0 + s_tap[tap]);
@@ -243,12 +322,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                              ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
       int stage = 0, acc = 0;
       uint32_t phase = 0, acc_phase = 0;
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+      int ti = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x, ti++) {
         mbar_wait(&tempty[acc], acc_phase ^ 1);
+        CG_TRACE(2, ti);
         tc_fence_after();
         const uint32_t d = tmem + acc * BN;
         for (int kb = 0; kb < num_k; kb++) {
           mbar_wait(&full[stage], phase);
+          if (kb == 0) CG_TRACE(3, ti);
           tc_fence_after();
           const uint64_t ad = smem_desc_sw128(sA + stage * A_BYTES);
           const uint64_t bd = smem_desc_sw128(sB + stage * B_BYTES);
@@ -259,63 +341,122 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
         umma_commit(&tfull[acc]);
+        CG_TRACE(4, ti);
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
+  } else if (warp == 10) {
+    // ---------------- residual loader: streams [128 x 32] residual chunks
+    // through the ring in epilogue order, as far ahead as the slots allow.
+    if (res_tma && lane == 0) {
+      constexpr int CPT = BN / 32;
+      int g = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x)
+        for (int c = 0; c < CPT; c++, g++) {
+          const int slot = g % (kResSlots > 0 ? kResSlots : 1);
+          if (g >= kResSlots) mbar_wait(&rempty[slot], ((g / kResSlots) - 1) & 1);
+          mbar_expect_tx(&rfull[slot], 128 * 32 * 2);
+          tma_load_2d(&tmR, &rfull[slot], s_res + slot * 8192, (t % num_n) * BN + c * 32,
+                      (t / num_n) * BM);
+        }
+    }
   } else {  // ------------------------------ epilogue (warps 2..9)
     // Warp w owns TMEM lanes [32q, 32q+32), q = w % 4 (= tile rows), and the
-    // 32-column chunks c with c % 2 == h, h = (w - 2) / 4. Per chunk:
-    // (1) lane = row: tcgen05.ld 32 accumulators -> a private 32x36 fp32 smem
-    //     tile (16-byte vector stores, conflict-free);
-    // (2) lane = (row group, 4-column group): bias, residual (TMA-streamed
-    //     ring), ReLU, bf16 pack and an 8-byte store: each store instruction
-    //     writes 4 contiguous 64-byte row segments.
+    // 32-column chunks c with c % 2 == h, h = (w - 2) / 4. Two paths:
+    //  * identity rows, bf16 out (tma_out): thread = row, see below;
+    //  * remapped rows / f32 out: (1) lane = row: tcgen05.ld -> a private
+    //    32x36 fp32 smem tile; (2) lane = (row group, 8-column group): bias,
+    //    ReLU, pack, 16-byte stores covering 8 rows x 64 B per instruction.
     const int q = warp & 3, h = (warp - 2) >> 2;
     const uint32_t stg_a = su32(s_epi + (warp - 2) * (32 * kStgLd));
     const int rr8 = lane >> 2, cg8 = lane & 3;
     constexpr int CPT = BN / 32;  // 32-column chunks per tile
-    const bool issuer = res_tma && warp == 2 && lane == 0;
-    int next_issue = 0;
-    // residual chunk g of this CTA's sequence -> TMA into ring slot g % kResSlots
-    auto issue_upto = [&](int last) {
-      if constexpr (kResSlots > 0) {
-        for (; next_issue <= last; next_issue++) {
-          const int hh = next_issue;
-          const int i = hh / CPT, c = hh - i * CPT;
-          const int t = blockIdx.x + i * gridDim.x;
-          if (t >= tiles) { next_issue = 0x7fffffff; return; }
-          const int slot = hh % kResSlots;
-          if (hh >= kResSlots) mbar_wait(&rempty[slot], ((hh / kResSlots) - 1) & 1);
-          mbar_expect_tx(&rfull[slot], 128 * 32 * 2);
-          tma_load_2d(&tmR, &rfull[slot], s_res + slot * (128 * 32 * 2),
-                      (t % num_n) * BN + c * 32, (t / num_n) * BM);
-        }
-      }
-    };
-    if (issuer) issue_upto(kResSlots - 2);
     int tile_i = 0, acc = 0;
     uint32_t acc_phase = 0;
     for (int t = blockIdx.x; t < tiles; t += gridDim.x, tile_i++) {
       const int m0 = (t / num_n) * BM, n0 = (t % num_n) * BN;
       const int my_orow = remap_row(a.M, a.rows_out, a.row_mode, a.H, a.W, m0 + q * 32 + lane);
       mbar_wait(&tfull[acc], acc_phase);
+      if (warp == 2) CG_TRACE(5, tile_i);
       tc_fence_after();
+      // TMEM reads are software-pipelined: chunk c+2's tcgen05.ld is in flight
+      // while chunk c is biased, stored and written out.
+      const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16) + acc * BN;
+      uint32_t v[32];
+      if (h < CPT) tmem_ld32_issue(trow + h * 32, v);
 #pragma unroll 1
       for (int c = h; c < CPT; c += 2) {
         const int g = tile_i * CPT + c;
-        if (issuer) issue_upto(g + kResSlots - 1);
-        uint32_t v[32];
-        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, v);
+        tmem_ld_wait(v);
         if (c + 2 >= CPT) {  // this warp's last chunk: hand TMEM back early
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&tempty[acc]);
+        }
+        if (tma_out) {
+          // thread = row: bias (+ residual row from the 64B-swizzled ring) +
+          // ReLU + bf16 in registers, 4 swizzled 16-byte smem stores, one TMA
+          // bulk store of the warp's 32 x 32 box. Two staging buffers per
+          // warp; the older bulk store must have finished reading its buffer.
+          const int n = n0 + c * 32;
+          float x[32];
+#pragma unroll
+          for (int j = 0; j < 8; j++) {
+            const float4 b4 = __ldg(reinterpret_cast<const float4*>(a.bias + n) + j);
+            x[4 * j] = __uint_as_float(v[4 * j]) + b4.x;
+            x[4 * j + 1] = __uint_as_float(v[4 * j + 1]) + b4.y;
+            x[4 * j + 2] = __uint_as_float(v[4 * j + 2]) + b4.z;
+            x[4 * j + 3] = __uint_as_float(v[4 * j + 3]) + b4.w;
+          }
+          if (c + 2 < CPT) tmem_ld32_issue(trow + (c + 2) * 32, v);
+          const int slot = kResSlots > 0 ? g % kResSlots : 0;
+          if (res_tma) {
+            mbar_wait(&rfull[slot], (g / (kResSlots > 0 ? kResSlots : 1)) & 1);
+            const uint32_t rb = su32(s_res + slot * 8192 + q * 32 * 64);
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+              const uint4 rv = lds_u4(rb + sw64(lane, j));
+              const uint32_t w[4] = {rv.x, rv.y, rv.z, rv.w};
+#pragma unroll
+              for (int e = 0; e < 4; e++) {
+                x[8 * j + 2 * e] += __uint_as_float(w[e] << 16);
+                x[8 * j + 2 * e + 1] += __uint_as_float(w[e] & 0xffff0000u);
+              }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&rempty[slot]);
+          }
+          if (a.relu) {
+#pragma unroll
+            for (int j = 0; j < 32; j++) x[j] = fmaxf(x[j], 0.f);
+          }
+          uint32_t o[16];
+#pragma unroll
+          for (int j = 0; j < 16; j++) {
+            __nv_bfloat162 t2 = __floats2bfloat162_rn(x[2 * j], x[2 * j + 1]);
+            o[j] = *reinterpret_cast<uint32_t*>(&t2);
+          }
+          const int buf = (c / 2) & 1;  // this warp's chunks alternate buffers
+          const uint32_t sb = stg_a + buf * 2048;
+          if (lane == 0) bulk_wait_read<1>();
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 4; j++)
+            sts_v4(sb + sw64(lane, j), o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
+          fence_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tmO, sb, n, m0 + q * 32);
+            bulk_commit();
+          }
+          continue;
         }
 #pragma unroll
         for (int j = 0; j < 8; j++)
           sts_v4(stg_a + 4 * (lane * kStgLd + 4 * j), v[4 * j], v[4 * j + 1], v[4 * j + 2],
                  v[4 * j + 3]);
         __syncwarp();
+        if (c + 2 < CPT) tmem_ld32_issue(trow + (c + 2) * 32, v);
         // phase 2: lane = (row rr8 of 8, 8-column group cg8 of 4): 16-byte
         // stores, each warp store instruction covers 8 rows x 64 B.
         const int n = n0 + c * 32 + cg8 * 8;
@@ -377,6 +518,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
         if (res_tma && lane == 0) mbar_arrive(&rempty[slot]);
       }
+      if (warp == 2) CG_TRACE(6, tile_i);
+      if (warp == 9) CG_TRACE(7, tile_i);
+      if (tma_out && lane == 0 && t + (int)gridDim.x >= tiles) bulk_wait_all();
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
   }
@@ -410,13 +554,12 @@ EncodeFn get_encode() {
 
 template <int BN, int STAGES, int kResSlots>
 constexpr int smem_bytes() {
-  return STAGES * (A_BYTES + BN * BK * 2) + 2 * STAGES * 8 + 4 * 8 + 16 + 48 + 4 * 32 * 33 * 4 +
-         2 * (kResSlots > 0 ? kResSlots : 1) * 8 + 128 + kResSlots * 128 * 32 * 2 + 1024 +
-         (kEpiWarps * kStgLd - 4 * 33) * 32 * 4;
+  return 1024 + STAGES * (A_BYTES + BN * BK * 2) + kResSlots * 8192 + kEpiWarps * 32 * kStgLd * 4 +
+         8 * (2 * STAGES + 4 + 2 * (kResSlots > 0 ? kResSlots : 1)) + 16 + 48;
 }
 
 template <int BN, int STAGES, int RS>
-void launch_t(const Operand& A, const Operand& B, const CUtensorMap& R,
+void launch_t(const Operand& A, const Operand& B, const CUtensorMap& R, const CUtensorMap& O,
               const ConvGemmArgs& a, cudaStream_t st, int max_ctas) {
   static bool attr = false;
   constexpr int smem = smem_bytes<BN, STAGES, RS>();
@@ -431,7 +574,7 @@ void launch_t(const Operand& A, const Operand& B, const CUtensorMap& R,
   int grid = tiles < budget ? tiles : budget;
   if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
   timer_begin(st, kTimeGemm);
-  conv_gemm_kernel<BN, STAGES, RS><<<grid, kThreads, smem, st>>>(A.map, B.map, R, a);
+  conv_gemm_kernel<BN, STAGES, RS><<<grid, kThreads, smem, st>>>(A.map, B.map, R, O, a);
   CG_CHECK_LAUNCH();
   timer_end(st, kTimeGemm);
 }
@@ -469,34 +612,45 @@ void launch_conv_gemm(const Operand& A, const Operand& B, const ConvGemmArgs& a,
   if (A.box_rows != BM || B.box_rows != BN) throw InvalidArgument("conv_gemm: box mismatch");
   if (!a.out_f32 && (a.N % 32)) throw InvalidArgument("conv_gemm: bf16 out needs N%32==0");
   if (a.out_f32 && (a.N % 8)) throw InvalidArgument("conv_gemm: f32 out needs N%8==0");
-  // residual operand: [rows_out, ld_res] bf16, box 32 cols x 128 rows, no swizzle
-  CUtensorMap R;
-  if (a.residual && a.row_mode == kRowIdentity) {
+  // [rows, ld] bf16 map with a 32-column box and the 64B swizzle (64-byte box
+  // rows): the residual ring (128-row box) and the output stage (32-row box).
+  auto map64 = [](CUtensorMap& m, const void* p, int ld, int rows, int box_rows) {
+    cuuint64_t dims[2] = {(cuuint64_t)ld, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+    cuuint32_t box[2] = {32, (cuuint32_t)box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = get_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(p),
+                              dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                              CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw CudaError("epilogue tensor map failed");
+  };
+  const bool tma_out = a.row_mode == kRowIdentity && !a.out_f32;
+  CUtensorMap R, O;
+  if (tma_out) {
+    if (a.ld_out % 8 || reinterpret_cast<uintptr_t>(a.out) % 16)
+      throw InvalidArgument("conv_gemm: output must be 16B aligned");
+    map64(O, a.out, a.ld_out, a.rows_out, 32);
+  } else {
+    O = A.map;  // unused
+  }
+  if (a.residual && tma_out) {
     if (a.ld_res % 8 || reinterpret_cast<uintptr_t>(a.residual) % 16)
       throw InvalidArgument("conv_gemm: residual must be 16B aligned");
-    cuuint64_t dims[2] = {(cuuint64_t)a.ld_res, (cuuint64_t)a.rows_out};
-    cuuint64_t strides[1] = {(cuuint64_t)a.ld_res * 2};
-    cuuint32_t box[2] = {32, 128};
-    cuuint32_t estr[2] = {1, 1};
-    CUresult r = get_encode()(&R, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
-                              const_cast<__nv_bfloat16*>(a.residual), dims, strides, box, estr,
-                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) throw CudaError("residual tensor map failed");
+    map64(R, a.residual, a.ld_res, a.rows_out, 128);
   } else {
     R = A.map;  // unused
   }
   // Residual layers are 1x1 with small K: trade mainloop stages for a deep
   // residual ring (88 KB in flight per SM) so the epilogue streams at HBM rate.
-  const bool res = a.residual && a.row_mode == kRowIdentity;
+  const bool res = a.residual && tma_out;
   switch (BN * 2 + (res ? 1 : 0)) {
-    case 128: launch_t<64, 7, 0>(A, B, R, a, st, max_ctas); break;
-    case 129: launch_t<64, 4, 10>(A, B, R, a, st, max_ctas); break;
-    case 256: launch_t<128, 5, 0>(A, B, R, a, st, max_ctas); break;
-    case 257: launch_t<128, 3, 10>(A, B, R, a, st, max_ctas); break;
-    case 512: launch_t<256, 3, 0>(A, B, R, a, st, max_ctas); break;
-    case 513: launch_t<256, 2, 10>(A, B, R, a, st, max_ctas); break;
+    case 128: launch_t<64, 7, 0>(A, B, R, O, a, st, max_ctas); break;
+    case 129: launch_t<64, 4, 10>(A, B, R, O, a, st, max_ctas); break;
+    case 256: launch_t<128, 5, 0>(A, B, R, O, a, st, max_ctas); break;
+    case 257: launch_t<128, 3, 10>(A, B, R, O, a, st, max_ctas); break;
+    case 512: launch_t<256, 3, 0>(A, B, R, O, a, st, max_ctas); break;
+    case 513: launch_t<256, 2, 10>(A, B, R, O, a, st, max_ctas); break;
     default: throw InvalidArgument("conv_gemm: BN must be 64, 128 or 256");
   }
 }

@@ -39,6 +39,7 @@ struct ConvGemmArgs {
   int row_mode;
   int H, W;                          // unpadded spatial dims (row remap)
   int rows_out;                      // valid output rows (identity mode)
+  long long* trace;                  // debug: CTA-0 event timestamps or null
 };
 
 // One encoded operand (tensor map over a row-major bf16 [rows, cols] matrix
