@@ -882,7 +882,7 @@ void certify(cg_group* g, uint64_t ticket, const double* precomputed_outputs) {
     int chain_ctas = 0;
     for (auto& o : g->slots)
       if (o.get() != &S && o->used && cudaEventQuery(o->ev_prefix) == cudaErrorNotReady)
-        chain_ctas += (int)ceil_div(o->B, 64);
+        chain_ctas += (int)ceil_div(o->B, kChainExclusiveThreads);
     set_gemm_sm_budget(kNumSMs - chain_ctas);
     const void* prepped = nullptr;
     if (g->all_cnn) {  // replica-independent input stage, once per batch

@@ -13,7 +13,7 @@ namespace cg {
 // chain, so parallelism comes from the number of jobs (requests × providers),
 // never from splitting a message. 32 jobs per warp, 2 warps per CTA keeps
 // chains spread over many SMs (each chain runs at the single-warp issue rate).
-__global__ void __launch_bounds__(64) chain_jobs_kernel(const ChainJob* jobs,
+__global__ void __launch_bounds__(128) chain_jobs_kernel(const ChainJob* jobs,
                                                         uint32_t n) {
   uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n) return;
@@ -30,7 +30,8 @@ __global__ void __launch_bounds__(64) chain_jobs_kernel(const ChainJob* jobs,
 void launch_chain_jobs(const ChainJob* d_jobs, uint32_t n, cudaStream_t st,
                        bool exclusive_sm) {
   if (n == 0) return;
-  const int tpb = 64;
+  // exclusive launches: one warp per SMSP of a reserved SM (128 chains/CTA)
+  const int tpb = exclusive_sm ? kChainExclusiveThreads : 64;
   // exclusive_sm: claim (unused) shared memory so the CTA can never share an
   // SM with a persistent GEMM CTA (~200 KB); long chains then run on their
   // own SMs instead of slowing one statically scheduled GEMM CTA.

@@ -8,6 +8,7 @@
 namespace cg {
 
 constexpr int kChainExclusiveSmem = 120 * 1024;
+constexpr int kChainExclusiveThreads = 128;
 void launch_chain_jobs(const ChainJob* d_jobs, uint32_t n, cudaStream_t st,
                        bool exclusive_sm = false);
 // ntrees trees; tree t = leaves [off[t], off[t]+len[t]) or count_dev[t].
