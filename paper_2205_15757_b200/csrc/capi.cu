@@ -695,6 +695,8 @@ struct cg_group {
   DevBuf<int32_t> d_single_pos;
   DevBuf<uint8_t> d_prep;  // shared CNN input operand
   bool all_cnn = false;
+  bool group_plan_ok = std::getenv("CREDO_NO_GROUP") == nullptr;  // false: per replica
+  std::unique_ptr<CnnGroupPlan> gplan;   // grouped per-layer launches
   std::vector<std::unique_ptr<IngestSlot>> slots;
   uint64_t next_ticket = 1;
   uint32_t last_B = 0;
@@ -889,7 +891,34 @@ void certify(cg_group* g, uint64_t ticket, const double* precomputed_outputs) {
       g->models[0]->cnn->prepare_input(S.d_in_ptr, B, g->d_prep.p, st);
       prepped = g->d_prep.p;
     }
-    for (uint32_t p = 0; p < N; p++) {
+    // Same-architecture CNN replicas: one grouped GEMM launch per layer.
+    if (g->all_cnn && g->group_plan_ok && (!g->gplan || g->gplan->batch() != B)) {
+      std::vector<CnnModel*> ms;
+      std::vector<float*> lg;
+      for (uint32_t p = 0; p < N; p++) {
+        ms.push_back(g->models[p]->cnn.get());
+        lg.push_back(g->d_pre32.p + (uint64_t)p * B * v);
+      }
+      g->gplan = CnnGroupPlan::build(ms, B, g->d_prep.p, lg);
+      g->group_plan_ok = g->gplan != nullptr;
+    }
+    const bool grouped = g->all_cnn && g->gplan && g->gplan->batch() == B;
+    if (grouped) {
+      g->gplan->run(st);
+      bool same_sm = true;
+      for (uint32_t p = 1; p < N; p++) same_sm &= g->models[p]->softmax == g->models[0]->softmax;
+      if (same_sm) {  // softmax/top-k of all N x B rows in one launch
+        launch_softmax_topk_f32(g->d_pre32.p, v, N * B, (uint32_t)v, g->models[0]->softmax,
+                                g->d_outs.p, v, g->topk, g->d_topi.p, g->d_topv.p, st);
+      } else {
+        for (uint32_t p = 0; p < N; p++)
+          launch_softmax_topk_f32(g->d_pre32.p + (uint64_t)p * B * v, v, B, (uint32_t)v,
+                                  g->models[p]->softmax, g->d_outs.p + (uint64_t)p * B * v, v,
+                                  g->topk, g->d_topi.p + (uint64_t)p * B * g->topk,
+                                  g->d_topv.p + (uint64_t)p * B * g->topk, st);
+      }
+    }
+    for (uint32_t p = 0; p < N && !grouped; p++) {
       cg_model* m = g->models[p];
       double* outs = g->d_outs.p + (uint64_t)p * B * v;
       uint32_t* ti = g->d_topi.p + (uint64_t)p * B * g->topk;
@@ -993,7 +1022,7 @@ int cg_group_create(cg_ctx* ctx, cg_model* const* models, uint32_t N,
     if (g->v > 1024) throw InvalidArgument("output dimension > 1024");
     const uint64_t B = max_batch, v = g->v;
     g->d_pre64.ensure(B * v);
-    g->d_pre32.ensure(B * v);
+    g->d_pre32.ensure((uint64_t)N * B * v);  // per-replica logits (grouped forward)
     g->d_outs.ensure((uint64_t)N * B * v);
     g->d_topi.ensure((uint64_t)N * B * topk);
     g->d_topv.ensure((uint64_t)N * B * topk);

@@ -249,12 +249,12 @@ struct Block {
 // columns) while 128 x 256 streams A once per 256 columns. Ties -> wider.
 int kSmallKMaxBN = 256;  // env CREDO_SMALLK_BN overrides (tuning)
 
-int pick_bn(int rows, int N) {
+int pick_bn(int rows, int N, int replicas = 1) {
   int best = 64;
   double best_cost = 1e30;
   for (int bn : {256, 128, 64}) {
     if (bn > N && bn != 64) continue;
-    long tiles = (long)((rows + 127) / 128) * ((N + bn - 1) / bn);
+    long tiles = (long)replicas * ((rows + 127) / 128) * ((N + bn - 1) / bn);
     long waves = (tiles + kNumSMs - 1) / kNumSMs;
     double eff = bn == 256 ? 1.0 : (bn == 128 ? 0.9 : 0.6);
     double cost = (double)waves * bn / eff;
@@ -414,6 +414,136 @@ class ResNet final : public CnnModel {
   bool softmax() const override { return softmax_; }
   std::string arch() const override { return arch_; }
   double flops_per_image() const override { return flops_; }
+  int image_size() const { return S_; }
+  size_t num_blocks() const { return blocks_.size(); }
+
+  // One launch of the forward, described per replica (nothing launched):
+  // a GEMM (shape + this replica's operands) or an auxiliary kernel.
+  struct GemmDesc {
+    ConvW* c = nullptr;
+    const bf16* A = nullptr;
+    int rowsA = 0, M = 0, Kc = 0, ntaps = 1, taps[9] = {0};
+    const bf16* res = nullptr;
+    int ldres = 0;
+    void* out = nullptr;
+    int ldout = 0, out_f32 = 0, relu = 0, mode = 0, H = 0, rows_out = 0;
+  };
+  struct Op {
+    bool gemm = false;
+    GemmDesc g;
+    std::function<void(cudaStream_t)> aux;
+  };
+
+  // The forward as a list of launches (csrc/cnn.cu header comment).
+  std::vector<Op> ops(uint32_t B, const void* x0, float* logits) {
+    std::vector<Op> L;
+    auto gemm = [&](ConvW& c, const bf16* A, int rowsA, int M, int Kc, int ntaps,
+                    const int* taps, const bf16* residual, int ldres, void* out, int ldout,
+                    int out_f32, int relu, int mode, int H, int rows_out) {
+      Op o;
+      o.gemm = true;
+      GemmDesc& g = o.g;
+      g.c = &c;
+      g.A = A;
+      g.rowsA = rowsA;
+      g.M = M;
+      g.Kc = Kc;
+      g.ntaps = ntaps;
+      for (int t = 0; t < ntaps; t++) g.taps[t] = taps[t];
+      g.res = residual;
+      g.ldres = ldres;
+      g.out = out;
+      g.ldout = ldout;
+      g.out_f32 = out_f32;
+      g.relu = relu;
+      g.mode = mode;
+      g.H = H;
+      g.rows_out = rows_out;
+      L.push_back(std::move(o));
+    };
+    auto aux = [&](std::function<void(cudaStream_t)> f) {
+      Op o;
+      o.aux = std::move(f);
+      L.push_back(std::move(o));
+    };
+    const int H1 = S_ / 2;
+    const int zero = 0;
+    // conv1 (im2col operand) -> c1out, then maxpool -> act_[0]
+    gemm(conv1_, reinterpret_cast<const bf16*>(x0), B * H1 * H1, B * H1 * H1, conv1_.Kc, 1,
+         &zero, nullptr, 0, c1out_, 64, 0, 1, kRowIdentity, 0, B * H1 * H1);
+    {
+      bf16* in = c1out_;
+      bf16* out = act_[0];
+      aux([in, out, B, H1](cudaStream_t st) {
+        size_t th = (size_t)B * ((H1 + 1) / 2) * ((H1 + 1) / 2) * (64 / 8);
+        maxpool3s2_kernel<<<grid_for(th), 256, 0, st>>>(in, B, H1, 64, out);
+        CG_CHECK_LAUNCH();
+      });
+    }
+    int cur = 0;
+    for (auto& b : blocks_) {
+      bf16* X = act_[cur];
+      bf16* Y = act_[cur ^ 1];
+      const int Hi = b.H_in, Ho = b.H_out, Hp = Hi + 2;
+      bf16* P = pads_.at({Hi, b.width});
+      // c1: 1x1 -> interior of the zero-bordered grid
+      gemm(b.c1, X, B * Hi * Hi, B * Hi * Hi, b.c1.Kc, 1, &zero, nullptr, 0, P, b.width, 0, 1,
+           kRowCompactToPad, Hi, B * Hp * Hp);
+      // c2: 3x3
+      if (b.stride == 1) {
+        int taps[9];
+        for (int dr = 0; dr < 3; dr++)
+          for (int ds = 0; ds < 3; ds++) taps[dr * 3 + ds] = (dr - 1) * Hp + (ds - 1);
+        gemm(b.c2, P, B * Hp * Hp, B * Hp * Hp, b.c2.Kc, 9, taps, nullptr, 0, t2_, b.width, 0,
+             1, kRowPadToCompact, Hi, B * Ho * Ho);
+      } else {
+        bf16* G = g3_;
+        int C = b.width;
+        aux([P, G, B, Hi, C](cudaStream_t st) {
+          size_t th = (size_t)B * (Hi / 2) * (Hi / 2) * 9 * (C / 8);
+          gather_s2_3x3_kernel<<<grid_for(th), 256, 0, st>>>(P, B, Hi, C, G);
+          CG_CHECK_LAUNCH();
+        });
+        // the 9-tap weights double as one K = 9*C operand (same (tap, c) order)
+        gemm(b.c2, G, B * Ho * Ho, B * Ho * Ho, 9 * C, 1, &zero, nullptr, 0, t2_, b.width, 0,
+             1, kRowIdentity, 0, B * Ho * Ho);
+      }
+      // identity / downsample
+      const bf16* ident = X;
+      if (b.has_ds) {
+        const bf16* dsin = X;
+        if (b.stride == 2) {
+          bf16* G1 = g1_;
+          int C = b.cin;
+          aux([X, G1, B, Hi, C](cudaStream_t st) {
+            size_t th = (size_t)B * (Hi / 2) * (Hi / 2) * (C / 8);
+            gather_s2_1x1_kernel<<<grid_for(th), 256, 0, st>>>(X, B, Hi, C, G1);
+            CG_CHECK_LAUNCH();
+          });
+          dsin = G1;
+        }
+        gemm(b.ds, dsin, B * Ho * Ho, B * Ho * Ho, b.ds.Kc, 1, &zero, nullptr, 0, ds_, b.cout,
+             0, 0, kRowIdentity, 0, B * Ho * Ho);
+        ident = ds_;
+      }
+      // c3: 1x1 + residual + ReLU
+      gemm(b.c3, t2_, B * Ho * Ho, B * Ho * Ho, b.c3.Kc, 1, &zero, ident, b.cout, Y, b.cout, 0,
+           1, kRowIdentity, 0, B * Ho * Ho);
+      cur ^= 1;
+    }
+    {
+      bf16* in = act_[cur];
+      bf16* out = pooled_;
+      int HW = H_last_ * H_last_, C = fc_.cin;
+      aux([in, out, B, HW, C](cudaStream_t st) {
+        avgpool_kernel<<<grid_for((size_t)B * C / 8), 256, 0, st>>>(in, B, HW, C, out);
+        CG_CHECK_LAUNCH();
+      });
+    }
+    gemm(fc_, pooled_, B, B, fc_.Kc, 1, &zero, nullptr, 0, logits, (int)out_dim_, 1, 0,
+         kRowIdentity, 0, B);
+    return L;
+  }
 
  private:
   struct Plan {
@@ -480,41 +610,6 @@ class ResNet final : public CnnModel {
     return v;
   }
 
-  // one fused GEMM step
-  void gemm_step(Plan& p, ConvW& c, const bf16* A, int rowsA, int M, int ntaps,
-                 const int* taps, const bf16* residual, int ldres, void* out, int ldout,
-                 int out_f32, int relu, int mode, int H, int rows_out) {
-    auto opA = std::make_shared<Operand>();
-    auto opB = std::make_shared<Operand>();
-    int BN = pick_bn(M, c.cout);
-    if (const char* e = std::getenv("CREDO_SMALLK_BN")) kSmallKMaxBN = std::atoi(e);
-    // Small-K 1x1 layers are epilogue/HBM bound: narrower tiles halve the
-    // serial per-warp epilogue work per tile (the MMA has nothing to hide it).
-    if (c.Kc * ntaps <= 128 && BN > kSmallKMaxBN) BN = kSmallKMaxBN;
-    make_operand(*opA, A, rowsA, c.Kc, 128);
-    make_operand(*opB, c.w, c.cout, c.Kc * ntaps, BN);
-    ConvGemmArgs a{};
-    a.M = M;
-    a.N = c.cout;
-    a.Kc = c.Kc;
-    a.ntaps = ntaps;
-    for (int t = 0; t < ntaps; t++) a.tap_off[t] = taps[t];
-    a.bias = c.b;
-    a.residual = residual;
-    a.ld_res = ldres;
-    a.out = out;
-    a.ld_out = ldout;
-    a.out_f32 = out_f32;
-    a.relu = relu;
-    a.row_mode = mode;
-    a.H = H;
-    a.W = H;
-    a.rows_out = rows_out;
-    p.steps.push_back([opA, opB, a, BN](cudaStream_t st) {
-      launch_conv_gemm(*opA, *opB, a, BN, st);
-    });
-  }
-
   Plan& plan_for(uint32_t B, const void* x0, float* logits) {
     auto it = plans_.find(B);
     if (it != plans_.end() && it->second.x0 == x0 && it->second.logits == logits)
@@ -523,89 +618,55 @@ class ResNet final : public CnnModel {
     p = Plan{};
     p.x0 = x0;
     p.logits = logits;
-    const int H1 = S_ / 2, H2 = S_ / 4;
-    const int zero = 0;
-    // conv1 (im2col operand) -> c1out, then maxpool -> act_[0]
-    gemm_step(p, conv1_, reinterpret_cast<const bf16*>(x0), B * H1 * H1, B * H1 * H1, 1,
-              &zero, nullptr, 0, c1out_, 64, 0, 1, kRowIdentity, 0, B * H1 * H1);
-    {
-      bf16* in = c1out_;
-      bf16* out = act_[0];
-      p.steps.push_back([in, out, B, H1](cudaStream_t st) {
-        size_t th = (size_t)B * ((H1 + 1) / 2) * ((H1 + 1) / 2) * (64 / 8);
-        maxpool3s2_kernel<<<grid_for(th), 256, 0, st>>>(in, B, H1, 64, out);
-        CG_CHECK_LAUNCH();
-      });
+    for (Op& o : ops(B, x0, logits)) {
+      if (o.gemm) p.steps.push_back(make_gemm_step({&o.g}));
+      else p.steps.push_back(std::move(o.aux));
     }
-    (void)H2;
-    int cur = 0;
-    for (auto& b : blocks_) {
-      bf16* X = act_[cur];
-      bf16* Y = act_[cur ^ 1];
-      const int Hi = b.H_in, Ho = b.H_out, Hp = Hi + 2;
-      bf16* P = pads_.at({Hi, b.width});
-      // c1: 1x1 -> interior of the zero-bordered grid
-      gemm_step(p, b.c1, X, B * Hi * Hi, B * Hi * Hi, 1, &zero, nullptr, 0, P, b.width, 0, 1,
-                kRowCompactToPad, Hi, B * Hp * Hp);
-      // c2: 3x3
-      if (b.stride == 1) {
-        int taps[9];
-        for (int dr = 0; dr < 3; dr++)
-          for (int ds = 0; ds < 3; ds++) taps[dr * 3 + ds] = (dr - 1) * Hp + (ds - 1);
-        gemm_step(p, b.c2, P, B * Hp * Hp, B * Hp * Hp, 9, taps, nullptr, 0, t2_, b.width, 0,
-                  1, kRowPadToCompact, Hi, B * Ho * Ho);
-      } else {
-        bf16* G = g3_;
-        int C = b.width;
-        p.steps.push_back([P, G, B, Hi, C](cudaStream_t st) {
-          size_t th = (size_t)B * (Hi / 2) * (Hi / 2) * 9 * (C / 8);
-          gather_s2_3x3_kernel<<<grid_for(th), 256, 0, st>>>(P, B, Hi, C, G);
-          CG_CHECK_LAUNCH();
-        });
-        ConvW& c2 = b.c2;
-        // the 9-tap weights double as one K = 9*C operand (same (tap, c) order)
-        c2.Kc = 9 * C;
-        gemm_step(p, c2, G, B * Ho * Ho, B * Ho * Ho, 1, &zero, nullptr, 0, t2_, b.width, 0,
-                  1, kRowIdentity, 0, B * Ho * Ho);
-        c2.Kc = C;
-      }
-      // identity / downsample
-      const bf16* ident = X;
-      if (b.has_ds) {
-        const bf16* dsin = X;
-        if (b.stride == 2) {
-          bf16* G1 = g1_;
-          int C = b.cin;
-          p.steps.push_back([X, G1, B, Hi, C](cudaStream_t st) {
-            size_t th = (size_t)B * (Hi / 2) * (Hi / 2) * (C / 8);
-            gather_s2_1x1_kernel<<<grid_for(th), 256, 0, st>>>(X, B, Hi, C, G1);
-            CG_CHECK_LAUNCH();
-          });
-          dsin = G1;
-        }
-        gemm_step(p, b.ds, dsin, B * Ho * Ho, B * Ho * Ho, 1, &zero, nullptr, 0, ds_, b.cout,
-                  0, 0, kRowIdentity, 0, B * Ho * Ho);
-        ident = ds_;
-      }
-      // c3: 1x1 + residual + ReLU
-      gemm_step(p, b.c3, t2_, B * Ho * Ho, B * Ho * Ho, 1, &zero, ident, b.cout, Y, b.cout, 0,
-                1, kRowIdentity, 0, B * Ho * Ho);
-      cur ^= 1;
-    }
-    {
-      bf16* in = act_[cur];
-      bf16* out = pooled_;
-      int HW = H_last_ * H_last_, C = fc_.cin;
-      p.steps.push_back([in, out, B, HW, C](cudaStream_t st) {
-        avgpool_kernel<<<grid_for((size_t)B * C / 8), 256, 0, st>>>(in, B, HW, C, out);
-        CG_CHECK_LAUNCH();
-      });
-    }
-    gemm_step(p, fc_, pooled_, B, B, 1, &zero, nullptr, 0, logits, (int)out_dim_, 1, 0,
-              kRowIdentity, 0, B);
     return p;
   }
 
+ public:
+  // One (grouped) GEMM launch over R replicas' descriptors of the same layer:
+  // tensor maps encoded once here, the returned step just launches.
+  static std::function<void(cudaStream_t)> make_gemm_step(const std::vector<const GemmDesc*>& ds) {
+    const GemmDesc& d0 = *ds[0];
+    const int R = (int)ds.size();
+    int BN = pick_bn(d0.M, d0.c->cout, R);
+    if (const char* e = std::getenv("CREDO_SMALLK_BN")) kSmallKMaxBN = std::atoi(e);
+    if (d0.Kc * d0.ntaps <= 128 && BN > kSmallKMaxBN) BN = kSmallKMaxBN;
+    std::vector<Operand> A(R), Bm(R);
+    ConvGemmGroup g;
+    g.n = R;
+    for (int r = 0; r < R; r++) {
+      const GemmDesc& d = *ds[r];
+      make_operand(A[r], d.A, d.rowsA, d.Kc, 128);
+      make_operand(Bm[r], d.c->w, d.c->cout, d.Kc * d.ntaps, BN);
+      g.A[r] = &A[r];
+      g.B[r] = &Bm[r];
+      g.bias[r] = d.c->b;
+      g.residual[r] = d.res;
+      g.out[r] = d.out;
+    }
+    ConvGemmArgs a{};
+    a.M = d0.M;
+    a.N = d0.c->cout;
+    a.Kc = d0.Kc;
+    a.ntaps = d0.ntaps;
+    for (int t = 0; t < d0.ntaps; t++) a.tap_off[t] = d0.taps[t];
+    a.ld_res = d0.ldres;
+    a.ld_out = d0.ldout;
+    a.out_f32 = d0.out_f32;
+    a.relu = d0.relu;
+    a.row_mode = d0.mode;
+    a.H = d0.H;
+    a.W = d0.H;
+    a.rows_out = d0.rows_out;
+    auto p = std::make_shared<PreparedGemm>();
+    prepare_conv_gemm(*p, g, a, BN);
+    return [p](cudaStream_t st) { launch_prepared(*p, st); };
+  }
+
+ private:
   std::string arch_;
   uint64_t in_dim_, out_dim_;
   bool softmax_;
@@ -621,7 +682,54 @@ class ResNet final : public CnnModel {
   std::map<uint32_t, Plan> plans_;
 };
 
+class ResNetGroupPlan final : public CnnGroupPlan {
+ public:
+  uint32_t B = 0;
+  std::vector<std::function<void(cudaStream_t)>> steps;
+  void run(cudaStream_t st) override {
+    for (auto& f : steps) f(st);
+  }
+  uint32_t batch() const override { return B; }
+};
+
 }  // namespace
+
+std::unique_ptr<CnnGroupPlan> CnnGroupPlan::build(const std::vector<CnnModel*>& models,
+                                                  uint32_t B, const void* prepped,
+                                                  const std::vector<float*>& logits) {
+  if (models.size() < 2 || models.size() > (size_t)kMaxGroup) return nullptr;
+  std::vector<ResNet*> rs;
+  for (CnnModel* m : models) {
+    auto* r = dynamic_cast<ResNet*>(m);
+    if (!r) return nullptr;
+    rs.push_back(r);
+  }
+  for (ResNet* r : rs)
+    if (r->arch() != rs[0]->arch() || r->image_size() != rs[0]->image_size() ||
+        r->num_blocks() != rs[0]->num_blocks() || r->output_dim() != rs[0]->output_dim())
+      return nullptr;
+  std::vector<std::vector<ResNet::Op>> ops;
+  for (size_t i = 0; i < rs.size(); i++) {
+    rs[i]->reserve(B);
+    ops.push_back(rs[i]->ops(B, prepped, logits[i]));
+  }
+  auto plan = std::make_unique<ResNetGroupPlan>();
+  plan->B = B;
+  for (size_t k = 0; k < ops[0].size(); k++) {
+    if (ops[0][k].gemm) {
+      std::vector<const ResNet::GemmDesc*> ds;
+      for (auto& o : ops) ds.push_back(&o[k].g);
+      plan->steps.push_back(ResNet::make_gemm_step(ds));
+    } else {
+      std::vector<std::function<void(cudaStream_t)>> fs;
+      for (auto& o : ops) fs.push_back(o[k].aux);
+      plan->steps.push_back([fs](cudaStream_t st) {
+        for (auto& f : fs) f(st);
+      });
+    }
+  }
+  return plan;
+}
 
 std::unique_ptr<CnnModel> CnnModel::from_file(const uint8_t* file, uint64_t len) {
   Reader r{file, len};

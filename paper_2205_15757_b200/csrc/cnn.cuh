@@ -36,4 +36,19 @@ class CnnModel {
   virtual double flops_per_image() const = 0;  // 2 × MACs of the forward
 };
 
+// The forward of several replicas of one architecture executed layer by
+// layer with one grouped GEMM launch per layer (3x the tiles of a single
+// replica: small late-stage layers fill the GPU in balanced waves).
+class CnnGroupPlan {
+ public:
+  virtual ~CnnGroupPlan() = default;
+  // nullptr when the models cannot be grouped (different architectures or
+  // input shapes). prepped: the shared conv1 operand; logits[r]: B x classes.
+  static std::unique_ptr<CnnGroupPlan> build(const std::vector<CnnModel*>& models, uint32_t B,
+                                             const void* prepped,
+                                             const std::vector<float*>& logits);
+  virtual void run(cudaStream_t st) = 0;
+  virtual uint32_t batch() const = 0;
+};
+
 }  // namespace cg

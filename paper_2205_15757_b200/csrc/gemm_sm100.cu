@@ -10,6 +10,8 @@
 #include "common.cuh"
 #include "gemm_sm100.cuh"
 
+#include <cstring>
+
 namespace cg {
 namespace {
 
@@ -229,11 +231,7 @@ __device__ __forceinline__ int remap_row(int M, int rows_out, int mode, int H,
 
 template <int BN, int STAGES, int kResSlots>
 __global__ void __launch_bounds__(kThreads, 1)
-    conv_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
-                     const __grid_constant__ CUtensorMap tmB,
-                     const __grid_constant__ CUtensorMap tmR,
-                     const __grid_constant__ CUtensorMap tmO,
-                     const ConvGemmArgs a) {
+    conv_gemm_kernel(const __grid_constant__ GemmGroupParams gp, const ConvGemmArgs a) {
   constexpr int B_BYTES = BN * BK * 2;
   constexpr uint32_t TMEM_COLS = 2 * BN;
   extern __shared__ uint8_t smem_raw[];
@@ -254,20 +252,31 @@ __global__ void __launch_bounds__(kThreads, 1)
   int* s_tap = reinterpret_cast<int*>(tmem_slot + 4);
   // identity rows + bf16 out: thread-per-row epilogue, TMA bulk stores
   const bool tma_out = a.row_mode == kRowIdentity && !a.out_f32;
-  const bool res_tma = kResSlots > 0 && a.residual != nullptr && tma_out;
+  const bool res_tma = kResSlots > 0 && gp.residual[0] != nullptr && tma_out;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int num_n = (a.N + BN - 1) / BN, num_m = (a.M + BM - 1) / BM;
-  const int tiles = num_m * num_n;
+  // tiles are replica-major: t -> (replica r, m block, n block)
+  const int tiles_per = num_m * num_n, tiles = tiles_per * gp.n;
   const int kpt = a.Kc / BK, num_k = a.ntaps * kpt;
+  auto coords = [&](int t, int& r, int& m0, int& n0) {
+    r = t / tiles_per;
+    const int tt = t - r * tiles_per;
+    m0 = (tt / num_n) * BM;
+    n0 = (tt % num_n) * BN;
+  };
 
   if (warp == 0 && lane == 0) {
 #pragma unroll
     for (int i = 0; i < 9; i++) s_tap[i] = a.tap_off[i];
   }
   if (warp == 0 && lane == 0) {
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+    for (int r = 0; r < gp.n; r++) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&gp.A[r]) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&gp.B[r]) : "memory");
+      if (tma_out) asm volatile("prefetch.tensormap [%0];" ::"l"(&gp.O[r]) : "memory");
+      if (res_tma) asm volatile("prefetch.tensormap [%0];" ::"l"(&gp.R[r]) : "memory");
+    }
     for (int s = 0; s < STAGES; s++) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -280,7 +289,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&rfull[s], 1);
       mbar_init(&rempty[s], 4);
     }
-    if (res_tma) asm volatile("prefetch.tensormap [%0];" ::"l"(&tmR) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -301,16 +309,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       int ti = 0;
       for (int t = blockIdx.x; t < tiles; t += gridDim.x, ti++) {
-        const int m0 = (t / num_n) * BM, n0 = (t % num_n) * BN;
+        int r, m0, n0;
+        coords(t, r, m0, n0);
         CG_TRACE(0, ti);
         for (int kb = 0; kb < num_k; kb++) {
           const int tap = kb / kpt, cb = kb - tap * kpt;
           mbar_wait(&empty[stage], phase ^ 1);
           if (kb == 0) CG_TRACE(1, ti);
           mbar_expect_tx(&full[stage], A_BYTES + B_BYTES);
-          tma_load_2d(&tmA, &full[stage], sA + stage * A_BYTES, cb * BK,
+          tma_load_2d(&gp.A[r], &full[stage], sA + stage * A_BYTES, cb * BK,
                       m0 + s_tap[tap]);
-          tma_load_2d(&tmB, &full[stage], sB + stage * B_BYTES, kb * BK, n0);
+          tma_load_2d(&gp.B[r], &full[stage], sB + stage * B_BYTES, kb * BK, n0);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -351,14 +360,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (res_tma && lane == 0) {
       constexpr int CPT = BN / 32;
       int g = 0;
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x)
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        int r, m0, n0;
+        coords(t, r, m0, n0);
         for (int c = 0; c < CPT; c++, g++) {
           const int slot = g % (kResSlots > 0 ? kResSlots : 1);
           if (g >= kResSlots) mbar_wait(&rempty[slot], ((g / kResSlots) - 1) & 1);
           mbar_expect_tx(&rfull[slot], 128 * 32 * 2);
-          tma_load_2d(&tmR, &rfull[slot], s_res + slot * 8192, (t % num_n) * BN + c * 32,
-                      (t / num_n) * BM);
+          tma_load_2d(&gp.R[r], &rfull[slot], s_res + slot * 8192, n0 + c * 32, m0);
         }
+      }
     }
   } else {  // ------------------------------ epilogue (warps 2..9)
     // Warp w owns TMEM lanes [32q, 32q+32), q = w % 4 (= tile rows), and the
@@ -372,9 +383,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int rr8 = lane >> 2, cg8 = lane & 3;
     constexpr int CPT = BN / 32;  // 32-column chunks per tile
     int tile_i = 0, acc = 0;
+    int stage_seq = 0;  // staging buffer sequence across all of this warp's chunks
     uint32_t acc_phase = 0;
     for (int t = blockIdx.x; t < tiles; t += gridDim.x, tile_i++) {
-      const int m0 = (t / num_n) * BM, n0 = (t % num_n) * BN;
+      int r_, m0, n0;
+      coords(t, r_, m0, n0);
+      const float* bias_r = gp.bias[r_];
+      const __nv_bfloat16* res_r = gp.residual[r_];
+      void* out_r = gp.out[r_];
       const int my_orow = remap_row(a.M, a.rows_out, a.row_mode, a.H, a.W, m0 + q * 32 + lane);
       mbar_wait(&tfull[acc], acc_phase);
       if (warp == 2) CG_TRACE(5, tile_i);
@@ -402,7 +418,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           float x[32];
 #pragma unroll
           for (int j = 0; j < 8; j++) {
-            const float4 b4 = __ldg(reinterpret_cast<const float4*>(a.bias + n) + j);
+            const float4 b4 = __ldg(reinterpret_cast<const float4*>(bias_r + n) + j);
             x[4 * j] = __uint_as_float(v[4 * j]) + b4.x;
             x[4 * j + 1] = __uint_as_float(v[4 * j + 1]) + b4.y;
             x[4 * j + 2] = __uint_as_float(v[4 * j + 2]) + b4.z;
@@ -436,7 +452,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             __nv_bfloat162 t2 = __floats2bfloat162_rn(x[2 * j], x[2 * j + 1]);
             o[j] = *reinterpret_cast<uint32_t*>(&t2);
           }
-          const int buf = (c / 2) & 1;  // this warp's chunks alternate buffers
+          const int buf = stage_seq++ & 1;  // this warp's chunks alternate buffers
           const uint32_t sb = stg_a + buf * 2048;
           if (lane == 0) bulk_wait_read<1>();
           __syncwarp();
@@ -446,7 +462,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           fence_async_smem();
           __syncwarp();
           if (lane == 0) {
-            tma_store_2d(&tmO, sb, n, m0 + q * 32);
+            tma_store_2d(&gp.O[r_], sb, n, m0 + q * 32);
             bulk_commit();
           }
           continue;
@@ -463,17 +479,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool col_ok = n < a.N;
         float b8[8];
         if (col_ok) {
-          const float4 b0 = __ldg(reinterpret_cast<const float4*>(a.bias + n));
-          const float4 b1 = __ldg(reinterpret_cast<const float4*>(a.bias + n + 4));
+          const float4 b0 = __ldg(reinterpret_cast<const float4*>(bias_r + n));
+          const float4 b1 = __ldg(reinterpret_cast<const float4*>(bias_r + n + 4));
           b8[0] = b0.x; b8[1] = b0.y; b8[2] = b0.z; b8[3] = b0.w;
           b8[4] = b1.x; b8[5] = b1.y; b8[6] = b1.z; b8[7] = b1.w;
         } else {
 #pragma unroll
           for (int e = 0; e < 8; e++) b8[e] = 0.f;
         }
-        const int slot = kResSlots > 0 ? g % kResSlots : 0;
-        const uint32_t rs_a = su32(s_res + slot * (128 * 32 * 2) + (q * 32) * 64 + cg8 * 16);
-        if (res_tma) mbar_wait(&rfull[slot], (g / (kResSlots > 0 ? kResSlots : 1)) & 1);
 #pragma unroll 2
         for (int it = 0; it < 4; it++) {
           const int r = it * 8 + rr8;
@@ -483,10 +496,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           const float4 p1 = lds_f4(stg_a + 4 * (r * kStgLd + cg8 * 8 + 4));
           float x[8] = {p0.x + b8[0], p0.y + b8[1], p0.z + b8[2], p0.w + b8[3],
                         p1.x + b8[4], p1.y + b8[5], p1.z + b8[6], p1.w + b8[7]};
-          if (a.residual) {
+          if (res_r) {
             uint4 rv = make_uint4(0, 0, 0, 0);
-            if (res_tma) rv = lds_u4(rs_a + r * 64);
-            else if (ok) rv = __ldg(reinterpret_cast<const uint4*>(a.residual + (size_t)orow * a.ld_res + n));
+            if (ok) rv = __ldg(reinterpret_cast<const uint4*>(res_r + (size_t)orow * a.ld_res + n));
             const uint32_t w[4] = {rv.x, rv.y, rv.z, rv.w};
 #pragma unroll
             for (int e = 0; e < 4; e++) {
@@ -500,7 +512,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           if (ok) {
             if (a.out_f32) {
-              float* op = reinterpret_cast<float*>(a.out) + (size_t)orow * a.ld_out + n;
+              float* op = reinterpret_cast<float*>(out_r) + (size_t)orow * a.ld_out + n;
               stg_f4(op, make_float4(x[0], x[1], x[2], x[3]));
               stg_f4(op + 4, make_float4(x[4], x[5], x[6], x[7]));
             } else {
@@ -510,13 +522,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 __nv_bfloat162 t = __floats2bfloat162_rn(x[2 * e], x[2 * e + 1]);
                 o[e] = *reinterpret_cast<uint32_t*>(&t);
               }
-              stg_u4(reinterpret_cast<__nv_bfloat16*>(a.out) + (size_t)orow * a.ld_out + n,
+              stg_u4(reinterpret_cast<__nv_bfloat16*>(out_r) + (size_t)orow * a.ld_out + n,
                      make_uint4(o[0], o[1], o[2], o[3]));
             }
           }
         }
         __syncwarp();
-        if (res_tma && lane == 0) mbar_arrive(&rempty[slot]);
       }
       if (warp == 2) CG_TRACE(6, tile_i);
       if (warp == 9) CG_TRACE(7, tile_i);
@@ -559,8 +570,7 @@ constexpr int smem_bytes() {
 }
 
 template <int BN, int STAGES, int RS>
-void launch_t(const Operand& A, const Operand& B, const CUtensorMap& R, const CUtensorMap& O,
-              const ConvGemmArgs& a, cudaStream_t st, int max_ctas) {
+void launch_t(const PreparedGemm& p, cudaStream_t st, int max_ctas) {
   static bool attr = false;
   constexpr int smem = smem_bytes<BN, STAGES, RS>();
   static_assert(smem <= 232448, "smem budget");
@@ -569,12 +579,13 @@ void launch_t(const Operand& A, const Operand& B, const CUtensorMap& R, const CU
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr = true;
   }
-  int tiles = ((a.M + BM - 1) / BM) * ((a.N + BN - 1) / BN);
+  const ConvGemmArgs& a = p.args;
+  int tiles = ((a.M + BM - 1) / BM) * ((a.N + BN - 1) / BN) * p.gp.n;
   const int budget = gemm_sm_budget();
   int grid = tiles < budget ? tiles : budget;
   if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
   timer_begin(st, kTimeGemm);
-  conv_gemm_kernel<BN, STAGES, RS><<<grid, kThreads, smem, st>>>(A.map, B.map, R, O, a);
+  conv_gemm_kernel<BN, STAGES, RS><<<grid, kThreads, smem, st>>>(p.gp, a);
   CG_CHECK_LAUNCH();
   timer_end(st, kTimeGemm);
 }
@@ -606,53 +617,81 @@ void make_operand(Operand& op, const void* ptr, int rows, int cols, int box_rows
   op.box_rows = box_rows;
 }
 
-void launch_conv_gemm(const Operand& A, const Operand& B, const ConvGemmArgs& a,
-                      int BN, cudaStream_t st, int max_ctas) {
+// [rows, ld] bf16 map with a 32-column box and the 64B swizzle (64-byte box
+// rows): the residual ring (128-row box) and the output stage (32-row box).
+static void map64(CUtensorMap& m, const void* p, int ld, int rows, int box_rows) {
+  cuuint64_t dims[2] = {(cuuint64_t)ld, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+  cuuint32_t box[2] = {32, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = get_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(p), dims,
+                            strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                            CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw CudaError("epilogue tensor map failed");
+}
+
+void prepare_conv_gemm(PreparedGemm& p, const ConvGemmGroup& g, const ConvGemmArgs& a, int BN) {
   if (a.Kc % 64 || a.ntaps < 1 || a.ntaps > 9) throw InvalidArgument("conv_gemm: bad K");
-  if (A.box_rows != BM || B.box_rows != BN) throw InvalidArgument("conv_gemm: box mismatch");
   if (!a.out_f32 && (a.N % 32)) throw InvalidArgument("conv_gemm: bf16 out needs N%32==0");
   if (a.out_f32 && (a.N % 8)) throw InvalidArgument("conv_gemm: f32 out needs N%8==0");
-  // [rows, ld] bf16 map with a 32-column box and the 64B swizzle (64-byte box
-  // rows): the residual ring (128-row box) and the output stage (32-row box).
-  auto map64 = [](CUtensorMap& m, const void* p, int ld, int rows, int box_rows) {
-    cuuint64_t dims[2] = {(cuuint64_t)ld, (cuuint64_t)rows};
-    cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
-    cuuint32_t box[2] = {32, (cuuint32_t)box_rows};
-    cuuint32_t estr[2] = {1, 1};
-    CUresult r = get_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(p),
-                              dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                              CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) throw CudaError("epilogue tensor map failed");
-  };
+  if (g.n < 1 || g.n > kMaxGroup) throw InvalidArgument("conv_gemm: group size 1..4");
+  if (BN != 64 && BN != 128 && BN != 256) throw InvalidArgument("conv_gemm: BN 64/128/256");
   const bool tma_out = a.row_mode == kRowIdentity && !a.out_f32;
-  CUtensorMap R, O;
-  if (tma_out) {
-    if (a.ld_out % 8 || reinterpret_cast<uintptr_t>(a.out) % 16)
-      throw InvalidArgument("conv_gemm: output must be 16B aligned");
-    map64(O, a.out, a.ld_out, a.rows_out, 32);
-  } else {
-    O = A.map;  // unused
+  std::memset(&p.gp, 0, sizeof p.gp);
+  p.gp.n = g.n;
+  for (int r = 0; r < g.n; r++) {
+    if (g.A[r]->box_rows != BM || g.B[r]->box_rows != BN)
+      throw InvalidArgument("conv_gemm: box mismatch");
+    if ((g.residual[r] != nullptr) != (g.residual[0] != nullptr))
+      throw InvalidArgument("conv_gemm: residual on some replicas only");
+    p.gp.A[r] = g.A[r]->map;
+    p.gp.B[r] = g.B[r]->map;
+    p.gp.bias[r] = g.bias[r];
+    p.gp.residual[r] = g.residual[r];
+    p.gp.out[r] = g.out[r];
+    if (tma_out) {
+      if (a.ld_out % 8 || reinterpret_cast<uintptr_t>(g.out[r]) % 16)
+        throw InvalidArgument("conv_gemm: output must be 16B aligned");
+      map64(p.gp.O[r], g.out[r], a.ld_out, a.rows_out, 32);
+      if (g.residual[r]) {
+        if (a.ld_res % 8 || reinterpret_cast<uintptr_t>(g.residual[r]) % 16)
+          throw InvalidArgument("conv_gemm: residual must be 16B aligned");
+        map64(p.gp.R[r], g.residual[r], a.ld_res, a.rows_out, 128);
+      }
+    }
   }
-  if (a.residual && tma_out) {
-    if (a.ld_res % 8 || reinterpret_cast<uintptr_t>(a.residual) % 16)
-      throw InvalidArgument("conv_gemm: residual must be 16B aligned");
-    map64(R, a.residual, a.ld_res, a.rows_out, 128);
-  } else {
-    R = A.map;  // unused
-  }
+  p.args = a;
+  p.BN = BN;
   // Residual layers are 1x1 with small K: trade mainloop stages for a deep
-  // residual ring (88 KB in flight per SM) so the epilogue streams at HBM rate.
-  const bool res = a.residual && tma_out;
-  switch (BN * 2 + (res ? 1 : 0)) {
-    case 128: launch_t<64, 7, 0>(A, B, R, O, a, st, max_ctas); break;
-    case 129: launch_t<64, 4, 10>(A, B, R, O, a, st, max_ctas); break;
-    case 256: launch_t<128, 5, 0>(A, B, R, O, a, st, max_ctas); break;
-    case 257: launch_t<128, 3, 10>(A, B, R, O, a, st, max_ctas); break;
-    case 512: launch_t<256, 3, 0>(A, B, R, O, a, st, max_ctas); break;
-    case 513: launch_t<256, 2, 10>(A, B, R, O, a, st, max_ctas); break;
+  // residual ring so the epilogue streams at HBM rate.
+  p.res = g.residual[0] != nullptr && tma_out;
+}
+
+void launch_prepared(const PreparedGemm& p, cudaStream_t st, int max_ctas) {
+  switch (p.BN * 2 + (p.res ? 1 : 0)) {
+    case 128: launch_t<64, 7, 0>(p, st, max_ctas); break;
+    case 129: launch_t<64, 4, 10>(p, st, max_ctas); break;
+    case 256: launch_t<128, 5, 0>(p, st, max_ctas); break;
+    case 257: launch_t<128, 3, 10>(p, st, max_ctas); break;
+    case 512: launch_t<256, 3, 0>(p, st, max_ctas); break;
+    case 513: launch_t<256, 2, 10>(p, st, max_ctas); break;
     default: throw InvalidArgument("conv_gemm: BN must be 64, 128 or 256");
   }
+}
+
+void launch_conv_gemm(const Operand& A, const Operand& B, const ConvGemmArgs& a, int BN,
+                      cudaStream_t st, int max_ctas) {
+  ConvGemmGroup g;
+  g.n = 1;
+  g.A[0] = &A;
+  g.B[0] = &B;
+  g.bias[0] = a.bias;
+  g.residual[0] = a.residual;
+  g.out[0] = a.out;
+  PreparedGemm p;
+  prepare_conv_gemm(p, g, a, BN);
+  launch_prepared(p, st, max_ctas);
 }
 
 }  // namespace cg

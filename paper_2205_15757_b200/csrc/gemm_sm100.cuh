@@ -52,6 +52,40 @@ struct Operand {
 
 void make_operand(Operand& op, const void* ptr, int rows, int cols, int box_rows);
 
+// One launch over up to kMaxGroup replicas: the same GEMM shape on each
+// replica's own activations/weights (tiles are replica-major), so small
+// layers of a model group fill the GPU in one wave-balanced launch.
+constexpr int kMaxGroup = 4;
+struct ConvGemmGroup {
+  int n = 0;
+  const Operand* A[kMaxGroup];
+  const Operand* B[kMaxGroup];
+  const float* bias[kMaxGroup];
+  const __nv_bfloat16* residual[kMaxGroup];
+  void* out[kMaxGroup];
+};
+
+// Kernel parameters of a grouped launch (all tensor maps pre-encoded).
+struct GemmGroupParams {
+  CUtensorMap A[kMaxGroup], B[kMaxGroup], R[kMaxGroup], O[kMaxGroup];
+  const float* bias[kMaxGroup];
+  const __nv_bfloat16* residual[kMaxGroup];
+  void* out[kMaxGroup];
+  int n;
+};
+
+struct PreparedGemm {
+  GemmGroupParams gp;
+  ConvGemmArgs args;
+  int BN = 128;
+  bool res = false;
+};
+
+// Encodes every tensor map of a (grouped) launch once; launch_prepared then
+// costs one kernel launch (plans cache PreparedGemm per layer).
+void prepare_conv_gemm(PreparedGemm& p, const ConvGemmGroup& g, const ConvGemmArgs& a, int BN);
+void launch_prepared(const PreparedGemm& p, cudaStream_t st, int max_ctas = 0);
+
 // SMs the persistent GEMM grid may occupy (default all 148). The certify
 // pipeline lowers it while request-midstate chains run on their own SMs, so
 // no statically scheduled GEMM CTA ever shares an SM with a chain CTA.

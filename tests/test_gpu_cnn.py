@@ -117,3 +117,19 @@ def test_resnet50_group_certify_digests(ctx, r50, oracle):
             a.append(oracle.leaf_hash(oracle.failure_leaf(batch.request_ids[op].tobytes(), gid, 1)))
     assert r["a_root"].tobytes() == oracle.merkle_root(a)
     grp.free()
+
+
+def test_grouped_forward_equals_per_replica(ctx, r50):
+    """The grouped (one launch per layer for all replicas) forward inside
+    certify produces bit-identical replica outputs to exec_run per replica."""
+    from paper_2205_15757_b200 import EUCLIDEAN, CudaExecutor, ModelGroup
+    from paper_2205_15757_b200.workload import signed_requests
+    grp = ModelGroup(ctx, r50["models"], 1, EUCLIDEAN, 0.1, b"group-0", 1, max_batch=4)
+    batch = signed_requests(4, 3 * 224 * 224, seed=9)
+    r = grp.certify(batch, want_outputs=True)
+    ex = CudaExecutor(ctx)
+    for p in range(3):
+        y = ex.run(r50["models"][p], batch.inputs)
+        print(p, np.abs(r["outputs"][p] - y).max(), np.argmax(y, -1), np.argmax(r["outputs"][p], -1))
+        assert np.array_equal(r["outputs"][p], y)
+    grp.free()

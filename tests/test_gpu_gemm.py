@@ -117,3 +117,19 @@ def test_compact_to_padded_interior(ctx):
     close(gp[:, 1:H + 1, 1:W + 1], ref)
     assert gp[:, 0].abs().sum() == 0 and gp[:, H + 1].abs().sum() == 0
     assert gp[:, :, 0].abs().sum() == 0 and gp[:, :, W + 1].abs().sum() == 0
+
+
+@pytest.mark.parametrize("BN", [64, 128, 256])
+def test_gemm_many_tiles_per_cta_tma_store(ctx, BN):
+    """Many tiles per CTA through the TMA-store epilogue (staging buffers are
+    reused across tiles): catches write-after-read races on smem staging."""
+    g = torch.Generator().manual_seed(BN)
+    M, N, Kc = 128 * 40, 256, 64
+    A = torch.rand(M, Kc, generator=g) * 2 - 1
+    Bw = torch.rand(N, Kc, generator=g) * 2 - 1
+    R = torch.rand(M, N, generator=g) * 2 - 1
+    bias = torch.rand(N, generator=g) - 0.5
+    for res in (None, R):
+        got = run_gemm(ctx, A, Bw, N, Kc, 1, [0], bias, res, 1, 0, 0, 0, M, M, 0, BN, max_ctas=2)
+        ref = q(A) @ q(Bw).T + bias + (0 if res is None else q(res))
+        close(got, ref.clamp_min(0))
