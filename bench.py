@@ -15,6 +15,11 @@ N>1 runs under torchrun, one rank per GPU, each rank certifying its own
 request stream for its own replica set (weak scaling, no data-path
 collective: requests are independent objects); the timed region is
 bracketed by barriers and the max over ranks is taken.
+
+--mode replica (N>1): the reference's own deployment shape — an N-replica
+group, rank k serving replica assigned_models(N, G, k) (domain.cpp:247-268),
+every rank certifying the SAME request stream; replica outputs and R roots
+are exchanged with one NCCL all-gather per batch (cg_group_create_dist).
 """
 from __future__ import annotations
 
@@ -65,6 +70,10 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t0 = time.time()  # nvidia-smi takes a moment to produce its first row
+            while not self.rows and time.time() - t0 < 5:
+                time.sleep(0.05)
+            self.rows.clear()
         except Exception:
             self.proc = None
         return self
@@ -107,6 +116,26 @@ def make_group(ctx, B, seed=0, eps=0.1):
     return grp, models, files, digs, sds
 
 
+def replica_f(world):
+    return (world - 1) // 2  # quorum of a strict majority
+
+
+def make_dist_group(ctx, B, rank, world, seed=0, eps=0.1):
+    """Replica-parallel group: rank serves one replica of a world-replica
+    group; NCCL communicator from rank 0's unique id."""
+    from paper_2205_15757_b200 import EUCLIDEAN, Context, Model, ModelGroup
+    from paper_2205_15757_b200.dist import assigned_models, share_bytes
+    from paper_2205_15757_b200.workload import resnet_group
+    files, digs, sds = resnet_group("resnet50", replicas=world, seed=seed, jitter=5e-3)
+    uid = share_bytes(Context.nccl_unique_id() if rank == 0 else None)
+    ctx.init_nccl(uid, world, rank)
+    (p,) = assigned_models(world, world, rank)
+    m = Model.load_cnn(ctx, files[p], digs[p])
+    grp = ModelGroup.create_dist(ctx, m, digs, replica_f(world), EUCLIDEAN, eps, b"group-0",
+                                 1, max_batch=B, topk=5)
+    return grp, [m], files, digs, sds
+
+
 def bench_gpu(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -119,7 +148,14 @@ def bench_gpu(args, rank, world, local_rank):
     stream = torch.cuda.current_stream()
     ctx.set_stream(stream.cuda_stream)
     B = args.batch
-    grp, models, files, digs, sds = make_group(ctx, B, seed=0)
+    replica = args.mode == "replica"
+    if replica:
+        grp, models, files, digs, sds = make_dist_group(ctx, B, rank, world)
+    else:
+        grp, models, files, digs, sds = make_group(ctx, B, seed=0)
+    # group mode: each rank its own stream; replica mode: one shared stream
+    seed_base = 0 if replica else 100 * rank
+    jobs = 1 if replica else world  # independent request streams
     L = lib()
     L.cg_model_flops_per_input.restype = __import__("ctypes").c_double
     L.cg_timing_read.argtypes = [__import__("ctypes").c_int,
@@ -130,7 +166,7 @@ def bench_gpu(args, rank, world, local_rank):
     # Two rotating batches of 154 MB f64 inputs each (> 126 MB L2): pinned
     # host copies for e2e, device copies for the device-resident value.
     nb = 2
-    batches = [signed_requests(B, U, seed=100 * rank + i) for i in range(nb)]
+    batches = [signed_requests(B, U, seed=seed_base + i) for i in range(nb)]
     host_in = [torch.from_numpy(b.inputs).pin_memory() for b in batches]
     dev_in = [h.to(f"cuda:{local_rank}") for h in host_in]
     from copy import copy
@@ -194,7 +230,7 @@ def bench_gpu(args, rank, world, local_rank):
     while pend:
         grp.certify_ticket(pend.popleft(), sync=False)
     torch.cuda.synchronize()
-    value = world * args.steps * B * sat_dev / (ms / 1e3)
+    value = jobs * args.steps * B * sat_dev / (ms / 1e3)
 
     # ---- end to end through the public API from pinned host memory ----
     pend = deque(grp.ingest(host_batches[j % nb]) for j in range(D))
@@ -210,12 +246,12 @@ def bench_gpu(args, rank, world, local_rank):
     e3.record(stream)
     torch.cuda.synchronize()
     ms_e2e = max_over_ranks(e2.elapsed_time(e3))
-    e2e = world * certified / (ms_e2e / 1e3)
+    e2e = jobs * certified / (ms_e2e / 1e3)
     while pend:
         grp.certify_ticket(pend.popleft(), sync=False)
     torch.cuda.synchronize()
     h2d = B * U * 8
-    d2h = B * (4 + 8 + 1 + 8) + 3 * 32 + 32 + 8
+    d2h = B * (4 + 8 + 1 + 8) + grp.N * 32 + 32 + 8
 
     # ---- attribution pass: per-kernel-class device time (same pipeline) ----
     import ctypes
@@ -237,7 +273,7 @@ def bench_gpu(args, rank, world, local_rank):
     gemm_ms_step = tg.value / args.steps
     chain_ms_step = tc.value / args.steps
     pk, pk_src = peaks()
-    flops_step = 3 * B * flops_img
+    flops_step = len(models) * B * flops_img  # this rank's replicas
     achieved = flops_step / (gemm_ms_step / 1e3) / 1e12
     peak = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
     roofline = {"bound": "tensor", "kernel": "conv_gemm (tcgen05 implicit-GEMM, all convs+fc)",
@@ -272,7 +308,14 @@ def bench_gpu(args, rank, world, local_rank):
            "gpu_launches": int(launches),
            "roofline": roofline,
            "clocks": clk.summary()}
-    if rank == 0 and not args.no_cpu_baseline:
+    if replica:
+        out["scaling"] = "strong"
+        out["config"].update(
+            workload=f"{world}-replica ResNet-50 group, one replica per GPU, f={replica_f(world)}, "
+                     f"batch {B}, 224x224; outputs + R roots all-gathered over NCCL",
+            replicas=world, f=replica_f(world), global_batch=B,
+            parallelism=f"replica-parallel x{world} (rank = provider)")
+    if rank == 0 and not args.no_cpu_baseline and not replica:
         out["cpu_baseline"] = cpu_baseline(files, digs, sds, batches[0], args)
     return out
 
@@ -372,6 +415,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--depth", type=int, default=6,
                     help="batches ingested ahead of certification (ring holds 8)")
+    ap.add_argument("--mode", default="group", choices=["group", "replica"],
+                    help="group: a whole 3-replica group per GPU (weak scaling); "
+                         "replica: one replica per GPU, NCCL all-gather (N>1)")
     ap.add_argument("--profile", action="store_true",
                     help="ncu mode: warmup + --steps plain steps, no report")
     args = ap.parse_args()
@@ -379,6 +425,8 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.mode == "replica" and world < 2:
+        ap.error("--mode replica needs torchrun with >= 2 ranks")
     if world > 1:
         import torch.distributed as dist
         if args.impl == "reference":

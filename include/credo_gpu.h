@@ -170,6 +170,23 @@ int cg_certify_ticket(cg_group* g, uint64_t ticket, cg_certify_out* out);
 int cg_certify_outputs(cg_group* g, const cg_request_batch* batch,
                        const double* outputs, cg_certify_out* out);
 
+/* ---- replica-parallel groups (one model owner's replica per GPU) ---------
+ * The SURVEY §8(e) / north-star mapping: rank r of an NCCL communicator is
+ * node r of the group and runs only replica r. Every rank ingests the same
+ * batch; certify computes rank r's outputs, result leaves and R root, one
+ * ncclAllGather over NVLink brings every provider's outputs and R root to
+ * every rank, and each rank then runs select_quorum, the label vote and the
+ * attestation tree (every reference node attests, coordinator.cpp:727-865).
+ * cg_nccl_unique_id on rank 0, broadcast the 128 bytes out of band. */
+int cg_nccl_unique_id(uint8_t out[128]);
+int cg_ctx_init_nccl(cg_ctx* ctx, const uint8_t id[128], int nranks, int rank);
+/* all_digests: nranks x 32 weights digests (provider order); my_model must
+ * be provider `rank`'s model. */
+int cg_group_create_dist(cg_ctx* ctx, cg_model* my_model, const uint8_t* all_digests,
+                         uint32_t f, uint32_t metric, double default_eps,
+                         const char* group_id, uint64_t group_id_len, uint64_t version,
+                         uint32_t max_batch, uint32_t topk, cg_group** out);
+
 /* ---- measurement hooks ----------------------------------------------------
  * Per-kernel-class device time from CUDA events recorded on each launching
  * stream (0 conv GEMM, 1 SHA-256 chains, 2 agreement, 3 other).

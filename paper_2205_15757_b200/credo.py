@@ -132,6 +132,19 @@ class Context:
     def synchronize(self):
         self._check(self.L.cg_ctx_synchronize(self.h))
 
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        rc = lib().cg_nccl_unique_id(buf)
+        if rc != CG_OK:
+            raise CredoError(rc, "ncclGetUniqueId failed")
+        return buf.raw
+
+    def init_nccl(self, uid: bytes, nranks: int, rank: int):
+        """One rank per GPU; uid from rank 0's nccl_unique_id()."""
+        assert len(uid) == 128
+        self._check(self.L.cg_ctx_init_nccl(self.h, uid, nranks, rank))
+
     def launch_count(self) -> int:
         return int(self.L.cg_ctx_launch_count(self.h))
 
@@ -349,6 +362,26 @@ class ModelGroup:
                                          u32(topk), C.byref(h)))
         self.h = h
         self._keep = None
+
+    @classmethod
+    def create_dist(cls, ctx: Context, my_model: Model, digests: Sequence[bytes],
+                    f: int, metric: int, default_eps: float, group_id: bytes,
+                    version: int, max_batch: int, topk: int = 5) -> "ModelGroup":
+        """Replica-parallel group: this rank (ctx.init_nccl) is provider
+        `rank` and runs only my_model; digests lists every provider's."""
+        self = cls.__new__(cls)
+        self.ctx, self.models = ctx, [my_model]
+        self.N, self.f, self.topk = len(digests), f, topk
+        self.v, self.u = my_model.output_dim, my_model.input_dim
+        self.group_id, self.version = group_id, version
+        h = vp()
+        ctx._check(ctx.L.cg_group_create_dist(ctx.h, my_model.h, b"".join(digests), u32(f),
+                                              u32(metric), dbl(default_eps), group_id,
+                                              u64(len(group_id)), u64(version),
+                                              u32(max_batch), u32(topk), C.byref(h)))
+        self.h = h
+        self._keep = None
+        return self
 
     def free(self):
         if self.h:

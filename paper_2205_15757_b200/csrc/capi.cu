@@ -12,8 +12,10 @@
 //                 manifest (+whole/failure A leaves) -> single A leaves ->
 //                 A root
 #include <cuda_runtime.h>
+#include <nccl.h>
 
 #include <algorithm>
+#include <array>
 #include <atomic>
 #include <cstring>
 #include <memory>
@@ -174,6 +176,9 @@ struct cg_ctx {
   DevBuf<int8_t> d_i8;
   DevBuf<int64_t> d_i64;
   DevBuf<double> d_f64b;
+  // replica-parallel groups: one NCCL communicator over the ranks (one per GPU)
+  ncclComm_t comm = nullptr;
+  int rank = 0, nranks = 1;
 };
 
 struct cg_model {
@@ -303,6 +308,7 @@ void cg_ctx_destroy(cg_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   cudaDeviceSynchronize();
+  if (ctx->comm) ncclCommDestroy(ctx->comm);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
   if (ctx->side) cudaStreamDestroy(ctx->side);
   if (ctx->ev_a) cudaEventDestroy(ctx->ev_a);
@@ -332,6 +338,32 @@ int cg_ctx_synchronize(cg_ctx* ctx) {
 }
 
 uint64_t cg_ctx_launch_count(const cg_ctx*) { return g_launches.load(); }
+
+int cg_nccl_unique_id(uint8_t out[128]) {
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return CG_ENCCL;
+  static_assert(sizeof(id) == 128, "ncclUniqueId size");
+  std::memcpy(out, &id, 128);
+  return CG_OK;
+}
+
+int cg_ctx_init_nccl(cg_ctx* ctx, const uint8_t id[128], int nranks, int rank) {
+  return guarded(ctx, [&] {
+    if (nranks < 1 || rank < 0 || rank >= nranks) throw InvalidArgument("bad rank/nranks");
+    if (ctx->comm) throw InvalidArgument("NCCL already initialised on this context");
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, 128);
+    ncclResult_t r = ncclCommInitRank(&ctx->comm, nranks, uid, rank);
+    if (r != ncclSuccess) {
+      ctx->comm = nullptr;
+      ctx->err = std::string("ncclCommInitRank: ") + ncclGetErrorString(r);
+      return CG_ENCCL;
+    }
+    ctx->rank = rank;
+    ctx->nranks = nranks;
+    return CG_OK;
+  });
+}
 
 void cg_timing_enable(int on) {
   std::lock_guard<std::mutex> lk(g_timers.mu);
@@ -679,7 +711,10 @@ struct IngestSlot {
 
 struct cg_group {
   cg_ctx* ctx = nullptr;
-  std::vector<cg_model*> models;
+  std::vector<cg_model*> models;          // local replicas (dist: just this rank's)
+  std::vector<std::array<uint8_t, 32>> digests;  // weights digest of every provider
+  bool dist = false;                      // replica-parallel over the ctx's NCCL ranks
+  uint32_t rank = 0;                      // this rank's provider index (dist)
   uint32_t N = 0, f = 0, metric = 0, maxB = 0, topk = 1;
   double eps_default = 0;
   std::string gid;
@@ -772,7 +807,7 @@ uint64_t ingest(cg_group* g, const cg_request_batch* bt) {
       R.u32((uint32_t)v);
       lenRes = R.b.size();
       res_off[(size_t)k * N + p] = ar.add(R.b.data(), R.b.size(), L.P);
-      dig_off[(size_t)k * N + p] = ar.add(g->models[p]->digest, 32, L.P + lenRes + 8 * v);
+      dig_off[(size_t)k * N + p] = ar.add(g->digests[p].data(), 32, L.P + lenRes + 8 * v);
     }
   }
   S.d_arena.ensure(ar.b.size() + 64);
@@ -892,7 +927,7 @@ void certify(cg_group* g, uint64_t ticket, const double* precomputed_outputs) {
       prepped = g->d_prep.p;
     }
     // Same-architecture CNN replicas: one grouped GEMM launch per layer.
-    if (g->all_cnn && g->group_plan_ok && (!g->gplan || g->gplan->batch() != B)) {
+    if (!g->dist && g->all_cnn && g->group_plan_ok && (!g->gplan || g->gplan->batch() != B)) {
       std::vector<CnnModel*> ms;
       std::vector<float*> lg;
       for (uint32_t p = 0; p < N; p++) {
@@ -902,7 +937,7 @@ void certify(cg_group* g, uint64_t ticket, const double* precomputed_outputs) {
       g->gplan = CnnGroupPlan::build(ms, B, g->d_prep.p, lg);
       g->group_plan_ok = g->gplan != nullptr;
     }
-    const bool grouped = g->all_cnn && g->gplan && g->gplan->batch() == B;
+    const bool grouped = !g->dist && g->all_cnn && g->gplan && g->gplan->batch() == B;
     if (grouped) {
       g->gplan->run(st);
       bool same_sm = true;
@@ -918,8 +953,9 @@ void certify(cg_group* g, uint64_t ticket, const double* precomputed_outputs) {
                                   g->d_topv.p + (uint64_t)p * B * g->topk, st);
       }
     }
-    for (uint32_t p = 0; p < N && !grouped; p++) {
-      cg_model* m = g->models[p];
+    for (uint32_t li = 0; li < (uint32_t)g->models.size() && !grouped; li++) {
+      const uint32_t p = g->dist ? g->rank : li;  // provider index of local replica li
+      cg_model* m = g->models[li];
       double* outs = g->d_outs.p + (uint64_t)p * B * v;
       uint32_t* ti = g->d_topi.p + (uint64_t)p * B * g->topk;
       double* tv = g->d_topv.p + (uint64_t)p * B * g->topk;
@@ -936,12 +972,31 @@ void certify(cg_group* g, uint64_t ticket, const double* precomputed_outputs) {
     set_gemm_sm_budget(kNumSMs);
   }
   CG_CUDA(cudaStreamWaitEvent(st, S.ev_prefix, 0));
-  launch_chain_jobs(S.d_jobs.p + B, N * B, st);  // result leaves
+  if (g->dist) {
+    // This rank is provider `rank`: its own result leaves and R root
+    // (try_prepare), then one NCCL all-gather of every provider's outputs
+    // and R root over NVLink; agreement and the attestation are then
+    // computed on every rank, as every reference node attests.
+    const uint32_t r = g->rank;
+    launch_chain_jobs(S.d_jobs.p + B + (uint64_t)r * B, B, st);
+    launch_merkle_trees(g->d_leaf.p + 32 * (uint64_t)r * B, nullptr, S.d_tree.p + N, nullptr, 1,
+                        B, g->d_rroots.p + 32 * r, st);
+    ncclResult_t e1, e2, e3;
+    e1 = ncclGroupStart();
+    e2 = ncclAllGather(g->d_outs.p + (uint64_t)r * B * v, g->d_outs.p, (size_t)B * v,
+                       ncclDouble, ctx->comm, st);
+    e3 = ncclAllGather(g->d_rroots.p + 32 * r, g->d_rroots.p, 32, ncclUint8, ctx->comm, st);
+    ncclResult_t e4 = ncclGroupEnd();
+    if (e1 != ncclSuccess || e2 != ncclSuccess || e3 != ncclSuccess || e4 != ncclSuccess)
+      throw CudaError(std::string("ncclAllGather: ") + ncclGetErrorString(e4));
+  } else {
+    launch_chain_jobs(S.d_jobs.p + B, N * B, st);  // result leaves
+    launch_merkle_trees(g->d_leaf.p, S.d_tree.p, S.d_tree.p + N, nullptr, N, B,
+                        g->d_rroots.p, st);
+  }
   launch_select_quorum(g->d_outs.p, (uint64_t)B * v, v, nullptr, S.d_eps.p, B, N, g->f,
                        (uint32_t)v, g->metric, g->d_sel.p, g->d_diam.p, g->d_sat.p,
                        g->d_status.p, g->d_label.p, st);
-  launch_merkle_trees(g->d_leaf.p, S.d_tree.p, S.d_tree.p + N, nullptr, N, B, g->d_rroots.p,
-                      st);
   launch_attest_manifest(B, N, g->d_sel.p, g->d_sat.p, g->d_rroots.p, S.d_reqids.p,
                          g->d_gid.p, gl, g->version, g->d_aleaf.p, g->d_single_pos.p,
                          g->d_kinds.p, g->d_mnodes.p, g->d_mops.p, g->d_count.p, st);
@@ -986,15 +1041,12 @@ void certify_fetch(cg_group* g, cg_certify_out* o) {
     if (status[k] != 0) throw InvalidArgument("select_quorum: invalid argument");
 }
 
-}  // namespace
-
-extern "C" {
-
-int cg_group_create(cg_ctx* ctx, cg_model* const* models, uint32_t N,
-                    uint32_t f, uint32_t metric, double default_eps,
-                    const char* group_id, uint64_t group_id_len,
-                    uint64_t version, uint32_t max_batch, uint32_t topk,
-                    cg_group** out) {
+// Shared by cg_group_create (all N replicas local) and cg_group_create_dist
+// (this rank's replica only; the N providers are the ctx's NCCL ranks).
+int create_group(cg_ctx* ctx, cg_model* const* models, uint32_t nlocal, uint32_t N,
+                 const uint8_t* all_digests, bool dist, uint32_t f, uint32_t metric,
+                 double default_eps, const char* group_id, uint64_t group_id_len,
+                 uint64_t version, uint32_t max_batch, uint32_t topk, cg_group** out) {
   return guarded(ctx, [&] {
     *out = nullptr;
     if (N == 0 || N > 20 || f >= N) throw InvalidArgument("bad n/f");
@@ -1011,10 +1063,19 @@ int cg_group_create(cg_ctx* ctx, cg_model* const* models, uint32_t N,
     g->version = version;
     g->maxB = max_batch;
     g->topk = topk;
-    for (uint32_t p = 0; p < N; p++) {
+    g->dist = dist;
+    g->rank = dist ? (uint32_t)ctx->rank : 0;
+    for (uint32_t p = 0; p < nlocal; p++) {
       if (!models[p] || models[p]->ctx != ctx) throw InvalidArgument("bad model");
       g->models.push_back(models[p]);
     }
+    for (uint32_t p = 0; p < N; p++) {
+      std::array<uint8_t, 32> d;
+      std::memcpy(d.data(), dist ? all_digests + 32 * p : models[p]->digest, 32);
+      g->digests.push_back(d);
+    }
+    if (dist && std::memcmp(g->digests[g->rank].data(), models[0]->digest, 32) != 0)
+      throw InvalidArgument("this rank's model is not provider `rank` of the group");
     g->u = models[0]->u;
     g->v = models[0]->v;
     for (auto* m : g->models)
@@ -1076,6 +1137,28 @@ int cg_group_create(cg_ctx* ctx, cg_model* const* models, uint32_t N,
     *out = g.release();
     return CG_OK;
   });
+}
+
+}  // namespace
+
+extern "C" {
+
+int cg_group_create(cg_ctx* ctx, cg_model* const* models, uint32_t N,
+                    uint32_t f, uint32_t metric, double default_eps,
+                    const char* group_id, uint64_t group_id_len,
+                    uint64_t version, uint32_t max_batch, uint32_t topk,
+                    cg_group** out) {
+  return create_group(ctx, models, N, N, nullptr, false, f, metric, default_eps, group_id,
+                      group_id_len, version, max_batch, topk, out);
+}
+
+int cg_group_create_dist(cg_ctx* ctx, cg_model* my_model, const uint8_t* all_digests,
+                         uint32_t f, uint32_t metric, double default_eps,
+                         const char* group_id, uint64_t group_id_len, uint64_t version,
+                         uint32_t max_batch, uint32_t topk, cg_group** out) {
+  if (!ctx || !ctx->comm) return fail(ctx, CG_EINVAL, "cg_ctx_init_nccl first");
+  return create_group(ctx, &my_model, 1, (uint32_t)ctx->nranks, all_digests, true, f, metric,
+                      default_eps, group_id, group_id_len, version, max_batch, topk, out);
 }
 
 void cg_group_free(cg_group* g) {
