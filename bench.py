@@ -200,6 +200,23 @@ def bench_gpu(args, rank, world, local_rank):
             grp.certify(dev_batches[i % nb], sync=False)
         torch.cuda.synchronize()
         return {"profile": True, "satisfied": sat}
+    if args.trace:  # kineto/CUPTI timeline of the pipelined loop (all streams)
+        from collections import deque
+
+        from torch.profiler import ProfilerActivity, profile
+        pend = deque(grp.ingest(dev_batches[j % nb]) for j in range(args.depth))
+        torch.cuda.synchronize()
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            for i in range(args.steps):
+                grp.certify_ticket(pend.popleft(), sync=False)
+                pend.append(grp.ingest(dev_batches[(i + args.depth) % nb]))
+            torch.cuda.synchronize()
+        while pend:
+            grp.certify_ticket(pend.popleft(), sync=False)
+        torch.cuda.synchronize()
+        if rank == 0:
+            prof.export_chrome_trace(args.trace)
+        return {"trace": args.trace}
 
     # ---- device-resident throughput (value) ----
     # Pipelined like the reference's own engine: a batch is ingested (framing
@@ -266,6 +283,11 @@ def bench_gpu(args, rank, world, local_rank):
     L.cg_timing_read(0, ctypes.byref(tg), ctypes.byref(ng))
     tc, nc = ctypes.c_double(), ctypes.c_uint64()
     L.cg_timing_read(1, ctypes.byref(tc), ctypes.byref(nc))
+    breakdown = {}
+    for cls, name in ((2, "agree_trees_ms"), (3, "aux_ms"), (4, "nccl_ms")):
+        t, n = ctypes.c_double(), ctypes.c_uint64()
+        L.cg_timing_read(cls, ctypes.byref(t), ctypes.byref(n))
+        breakdown[name] = round(t.value / args.steps, 3)
     L.cg_timing_enable(0)
     while pend:
         grp.certify_ticket(pend.popleft(), sync=False)
@@ -284,7 +306,8 @@ def bench_gpu(args, rank, world, local_rank):
                 "gemm_ms_per_step": round(gemm_ms_step, 3),
                 "gemm_launches_per_step": int(ng.value) // args.steps,
                 "share_of_step": round(gemm_ms_step / (ms / args.steps), 3),
-                "sha_chain_ms_per_step_overlapped": round(chain_ms_step, 3)}
+                "sha_chain_ms_per_step_overlapped": round(chain_ms_step, 3),
+                "other_ms_per_step": breakdown}
 
     out = {"metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup,
@@ -413,11 +436,14 @@ def main():
                     help="requests in the bounded CPU-baseline sample (~10 s of CPU work)")
     ap.add_argument("--steps-ref", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--depth", type=int, default=6,
-                    help="batches ingested ahead of certification (ring holds 8)")
+    ap.add_argument("--depth", type=int, default=12,
+                    help="batches ingested ahead of certification (ring holds 16)")
     ap.add_argument("--mode", default="group", choices=["group", "replica"],
                     help="group: a whole 3-replica group per GPU (weak scaling); "
                          "replica: one replica per GPU, NCCL all-gather (N>1)")
+    ap.add_argument("--trace", default=None,
+                    help="write a CUPTI timeline (chrome trace JSON) of --steps "
+                         "pipelined steps instead of timing")
     ap.add_argument("--profile", action="store_true",
                     help="ncu mode: warmup + --steps plain steps, no report")
     args = ap.parse_args()
@@ -428,6 +454,9 @@ def main():
     if args.mode == "replica" and world < 2:
         ap.error("--mode replica needs torchrun with >= 2 ranks")
     if world > 1:
+        # NCCL writes its version banner to stdout at the default level; keep
+        # stdout to the one JSON line
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/tmp/credo_nccl.%h.%p.log")
         import torch.distributed as dist
         if args.impl == "reference":
             if rank != 0:

@@ -981,12 +981,14 @@ void certify(cg_group* g, uint64_t ticket, const double* precomputed_outputs) {
     launch_chain_jobs(S.d_jobs.p + B + (uint64_t)r * B, B, st);
     launch_merkle_trees(g->d_leaf.p + 32 * (uint64_t)r * B, nullptr, S.d_tree.p + N, nullptr, 1,
                         B, g->d_rroots.p + 32 * r, st);
+    timer_begin(st, kTimeComm);
     ncclResult_t e1, e2, e3;
     e1 = ncclGroupStart();
     e2 = ncclAllGather(g->d_outs.p + (uint64_t)r * B * v, g->d_outs.p, (size_t)B * v,
                        ncclDouble, ctx->comm, st);
     e3 = ncclAllGather(g->d_rroots.p + 32 * r, g->d_rroots.p, 32, ncclUint8, ctx->comm, st);
     ncclResult_t e4 = ncclGroupEnd();
+    timer_end(st, kTimeComm);
     if (e1 != ncclSuccess || e2 != ncclSuccess || e3 != ncclSuccess || e4 != ncclSuccess)
       throw CudaError(std::string("ncclAllGather: ") + ncclGetErrorString(e4));
   } else {
@@ -994,6 +996,7 @@ void certify(cg_group* g, uint64_t ticket, const double* precomputed_outputs) {
     launch_merkle_trees(g->d_leaf.p, S.d_tree.p, S.d_tree.p + N, nullptr, N, B,
                         g->d_rroots.p, st);
   }
+  timer_begin(st, kTimeAgree);
   launch_select_quorum(g->d_outs.p, (uint64_t)B * v, v, nullptr, S.d_eps.p, B, N, g->f,
                        (uint32_t)v, g->metric, g->d_sel.p, g->d_diam.p, g->d_sat.p,
                        g->d_status.p, g->d_label.p, st);
@@ -1003,6 +1006,7 @@ void certify(cg_group* g, uint64_t ticket, const double* precomputed_outputs) {
   launch_chain_jobs(S.d_jobs.p + B + (uint64_t)N * B, N * B, st);  // single A leaves
   launch_merkle_trees(g->d_aleaf.p, nullptr, nullptr, g->d_count.p, 1, (uint64_t)N * B + B + N,
                       g->d_aroot.p, st);
+  timer_end(st, kTimeAgree);
   CG_CUDA(cudaEventRecord(S.ev_done, st));
   S.used = false;
   g->last_B = B;
@@ -1111,8 +1115,9 @@ int create_group(cg_ctx* ctx, cg_model* const* models, uint32_t nlocal, uint32_t
     }
     if (g->all_cnn) g->d_prep.ensure(g->models[0]->cnn->prepared_bytes(max_batch));
     // ingest ring: enough batches in flight to hide the request-midstate
-    // chains (latency ~ request bytes / 64 compressions) behind the forwards
-    const int depth = 8;
+    // chains (latency ~ request bytes / 64 compressions, ~30 ms for a C2
+    // request) behind the forwards of the batches certified meanwhile
+    const int depth = 16;
     const size_t arena_max = (size_t)B * (512 + 160 * N) + 1024;
     for (int i = 0; i < depth; i++) {
       auto S = std::make_unique<IngestSlot>();

@@ -386,6 +386,7 @@ class ResNet final : public CnnModel {
   void prepare_input(const double* d_in, uint32_t B, void* prepped, cudaStream_t st) override {
     const int H1 = S_ / 2, Sp = S_ + 6;
     if (B > maxB_) reserve(B);
+    timer_begin(st, kTimeAux);
     // two coalesced passes: f64 CHW -> bf16 NHWC4 (pad 3), then im2col
     chw_to_nhwc4_pad3_kernel<<<grid_for((size_t)B * Sp * Sp), 256, 0, st>>>(
         d_in, B, S_, reinterpret_cast<uint2*>(nhwc4_));
@@ -395,6 +396,7 @@ class ResNet final : public CnnModel {
                                 0, st>>>(reinterpret_cast<const uint2*>(nhwc4_), B, S_, H1,
                                          reinterpret_cast<bf16*>(prepped));
     CG_CHECK_LAUNCH();
+    timer_end(st, kTimeAux);
   }
 
   void forward(const double* d_in, uint32_t B, float* logits, cudaStream_t st,
@@ -463,7 +465,11 @@ class ResNet final : public CnnModel {
     };
     auto aux = [&](std::function<void(cudaStream_t)> f) {
       Op o;
-      o.aux = std::move(f);
+      o.aux = [f](cudaStream_t st) {
+        timer_begin(st, kTimeAux);
+        f(st);
+        timer_end(st, kTimeAux);
+      };
       L.push_back(std::move(o));
     };
     const int H1 = S_ / 2;

@@ -36,7 +36,14 @@ uint64_t launch_counter_add(uint64_t n);
 
 // Optional per-kernel-class device timing (CUDA events on the launching
 // stream), used by bench.py to attribute step time to the dominant kernel.
-enum TimerClass : int { kTimeGemm = 0, kTimeChain = 1, kTimeAgree = 2, kTimeAux = 3, kTimeClasses = 4 };
+enum TimerClass : int {
+  kTimeGemm = 0,   // conv_gemm launches
+  kTimeChain = 1,  // SHA-256 chain jobs
+  kTimeAgree = 2,  // softmax/top-k, select_quorum, manifest, Merkle trees
+  kTimeAux = 3,    // CNN input prep, gathers, pools
+  kTimeComm = 4,   // NCCL exchange (replica-parallel groups)
+  kTimeClasses = 5
+};
 void timer_begin(cudaStream_t st, int cls);
 void timer_end(cudaStream_t st, int cls);
 

@@ -12,31 +12,41 @@
 
 using namespace cg;
 
-// Cycles per SHA-256 block for one warp of 32 chains: mode 0 = compression
-// only (registers), mode 1 = the chain engine over an f64 segment.
+// Cycles per SHA-256 block for one warp of 32 chains: mode 0 = unrolled
+// compression only (registers), 1 = rolled compression only, 2..4 = the
+// chain engine over an f64 segment with run_chain_job<mode - 2>; +8 = all
+// lanes read the same stream (coalesced).
 __global__ void sha_bench_kernel(int mode, uint64_t nblocks, const double* buf,
                                  uint64_t per_thread_doubles, long long* cycles,
                                  uint32_t* sink) {
   uint32_t s[8], w[16];
   sha256_iv(s);
   for (int i = 0; i < 16; i++) w[i] = threadIdx.x * 16 + i;
+  const uint64_t lane_off = (mode & 8) ? 0 : threadIdx.x * per_thread_doubles;
+  mode &= 7;  // +16 (host): 128 threads = one warp per SMSP
   long long t0 = clock64();
   if (mode == 0) {
     for (uint64_t b = 0; b < nblocks; b++) {
-      sha256_compress(s, w);
+      sha256_compress<false>(s, w);
+      w[0] ^= s[0];
+    }
+  } else if (mode == 1) {
+    for (uint64_t b = 0; b < nblocks; b++) {
+      sha256_compress<true>(s, w);
       w[0] ^= s[0];
     }
   } else {
     ChainJob j;
     memset(&j, 0, sizeof j);
-    j.seg[0] = ChainSeg{(uint64_t)(buf + threadIdx.x * per_thread_doubles), 0,
-                        nblocks * 64, kSegF64, 0};
+    j.seg[0] = ChainSeg{(uint64_t)(buf + lane_off), 1, nblocks * 64, kSegF64, 0};
     j.nseg = 1;
-    j.total_len = nblocks * 64;
-    j.blk_begin = 0;
+    j.total_len = nblocks * 64 + 1;
+    j.blk_begin = 1;
     j.blk_end = nblocks;
-    j.state_out = 0;
-    run_chain_job(j, 0);
+    j.state_out = (uint64_t)(sink + 128 + 8 * threadIdx.x);
+    if (mode == 2) run_chain_job<0>(j, 0);
+    else if (mode == 3) run_chain_job<1>(j, 0);
+    else run_chain_job<2>(j, 0);
     s[0] = (uint32_t)j.blk_end;
   }
   long long t1 = clock64();
@@ -54,11 +64,11 @@ extern "C" int cg_dbg_sha_bench(cg_ctx* ctx, int mode, uint64_t nblocks,
     long long* cyc = nullptr;
     uint32_t* sink = nullptr;
     uint64_t per = nblocks * 8 + 16;
-    CG_CUDA(cudaMalloc(&buf, 32 * per * 8));
-    CG_CUDA(cudaMemset(buf, 1, 32 * per * 8));
+    CG_CUDA(cudaMalloc(&buf, 128 * per * 8));
+    CG_CUDA(cudaMemset(buf, 1, 128 * per * 8));
     CG_CUDA(cudaMalloc(&cyc, 8));
-    CG_CUDA(cudaMalloc(&sink, 128));
-    sha_bench_kernel<<<1, 32, 0, st>>>(mode, nblocks, buf, per, cyc, sink);
+    CG_CUDA(cudaMalloc(&sink, 4 * (128 + 8 * 128)));
+    sha_bench_kernel<<<1, (mode & 16) ? 128 : 32, 0, st>>>(mode & 15, nblocks, buf, per, cyc, sink);
     CG_CHECK_LAUNCH();
     long long c = 0;
     CG_CUDA(cudaMemcpyAsync(&c, cyc, 8, cudaMemcpyDeviceToHost, st));

@@ -59,39 +59,99 @@ __device__ __forceinline__ void sha256_iv(uint32_t s[8]) {
   s[6] = 0x1f83d9abu; s[7] = 0x5be0cd19u;
 }
 
-// FIPS 180-4 compression, fully unrolled; the 64-entry message schedule is a
-// rolling 16-word window so everything stays in registers.
+static __constant__ uint32_t kSha256K[64] = {
+    0x428a2f98u, 0x71374491u, 0xb5c0fbcfu, 0xe9b5dba5u, 0x3956c25bu, 0x59f111f1u,
+    0x923f82a4u, 0xab1c5ed5u, 0xd807aa98u, 0x12835b01u, 0x243185beu, 0x550c7dc3u,
+    0x72be5d74u, 0x80deb1feu, 0x9bdc06a7u, 0xc19bf174u, 0xe49b69c1u, 0xefbe4786u,
+    0x0fc19dc6u, 0x240ca1ccu, 0x2de92c6fu, 0x4a7484aau, 0x5cb0a9dcu, 0x76f988dau,
+    0x983e5152u, 0xa831c66du, 0xb00327c8u, 0xbf597fc7u, 0xc6e00bf3u, 0xd5a79147u,
+    0x06ca6351u, 0x14292967u, 0x27b70a85u, 0x2e1b2138u, 0x4d2c6dfcu, 0x53380d13u,
+    0x650a7354u, 0x766a0abbu, 0x81c2c92eu, 0x92722c85u, 0xa2bfe8a1u, 0xa81a664bu,
+    0xc24b8b70u, 0xc76c51a3u, 0xd192e819u, 0xd6990624u, 0xf40e3585u, 0x106aa070u,
+    0x19a4c116u, 0x1e376c08u, 0x2748774cu, 0x34b0bcb5u, 0x391c0cb3u, 0x4ed8aa4au,
+    0x5b9cca4fu, 0x682e6ff3u, 0x748f82eeu, 0x78a5636fu, 0x84c87814u, 0x8cc70208u,
+    0x90befffau, 0xa4506cebu, 0xbef9a3f7u, 0xc67178f2u};
+
+// Measured on B200 (tools/shabench.py): a round is ALU-pipe bound (~21
+// SHF/LOP3/IADD3 at half rate per SMSP = ~42 cycles). Moving the additions,
+// shifts or a rotation onto the FMA pipe as IMADs made it slower (longer
+// dependent chains), so rounds stay on the ALU pipe.
+// One FIPS 180-4 round; i is the round index within its 16-round group so
+// the rolling 16-word schedule window indices are compile-time constants.
+template <int i, bool kSched>
+__device__ __forceinline__ void sha256_round(uint32_t& a, uint32_t& b, uint32_t& c,
+                                             uint32_t& d, uint32_t& e, uint32_t& f,
+                                             uint32_t& g, uint32_t& h, uint32_t w[16],
+                                             uint32_t k) {
+  if (kSched) {
+    uint32_t x = w[(i + 1) & 15], y = w[(i + 14) & 15];
+    uint32_t s0 = rotr32(x, 7) ^ rotr32(x, 18) ^ (x >> 3);
+    uint32_t s1 = rotr32(y, 17) ^ rotr32(y, 19) ^ (y >> 10);
+    w[i & 15] += s0 + w[(i + 9) & 15] + s1;
+  }
+  const uint32_t S1 = rotr32(e, 6) ^ rotr32(e, 11) ^ rotr32(e, 25);
+  const uint32_t ch = (e & f) ^ (~e & g);
+  const uint32_t S0 = rotr32(a, 2) ^ rotr32(a, 13) ^ rotr32(a, 22);
+  const uint32_t maj = (a & b) | (c & (a | b));
+  const uint32_t t1 = h + S1 + ch + k + w[i & 15];
+  h = g; g = f; f = e; e = d + t1;
+  d = c; c = b; b = a; a = t1 + S0 + maj;
+}
+
+#define CG_SHA_R(n) \
+  sha256_round<n, kSched>(a, b, c, d, e, f, g, h, w, kSha256K[r + n]);
+template <bool kSched>
+__device__ __forceinline__ void sha256_16rounds(uint32_t& a, uint32_t& b, uint32_t& c,
+                                                uint32_t& d, uint32_t& e, uint32_t& f,
+                                                uint32_t& g, uint32_t& h, uint32_t w[16],
+                                                int r) {
+  CG_SHA_R(0) CG_SHA_R(1) CG_SHA_R(2) CG_SHA_R(3) CG_SHA_R(4) CG_SHA_R(5)
+  CG_SHA_R(6) CG_SHA_R(7) CG_SHA_R(8) CG_SHA_R(9) CG_SHA_R(10) CG_SHA_R(11)
+  CG_SHA_R(12) CG_SHA_R(13) CG_SHA_R(14) CG_SHA_R(15)
+}
+#undef CG_SHA_R
+
+// FIPS 180-4 compression of one block into s. kRolled == false: all 64
+// rounds unrolled with immediate constants (~1.5k instructions; used by the
+// short digests). kRolled == true: rounds 16-63 as a 3-trip loop over one
+// 16-round body with K from constant memory (~1/3 the code, so a chain loop
+// stays resident in the SMSP's instruction cache).
+template <bool kRolled = false>
 __device__ __forceinline__ void sha256_compress(uint32_t s[8], uint32_t w[16]) {
-  constexpr uint32_t K[64] = {
-      0x428a2f98u, 0x71374491u, 0xb5c0fbcfu, 0xe9b5dba5u, 0x3956c25bu,
-      0x59f111f1u, 0x923f82a4u, 0xab1c5ed5u, 0xd807aa98u, 0x12835b01u,
-      0x243185beu, 0x550c7dc3u, 0x72be5d74u, 0x80deb1feu, 0x9bdc06a7u,
-      0xc19bf174u, 0xe49b69c1u, 0xefbe4786u, 0x0fc19dc6u, 0x240ca1ccu,
-      0x2de92c6fu, 0x4a7484aau, 0x5cb0a9dcu, 0x76f988dau, 0x983e5152u,
-      0xa831c66du, 0xb00327c8u, 0xbf597fc7u, 0xc6e00bf3u, 0xd5a79147u,
-      0x06ca6351u, 0x14292967u, 0x27b70a85u, 0x2e1b2138u, 0x4d2c6dfcu,
-      0x53380d13u, 0x650a7354u, 0x766a0abbu, 0x81c2c92eu, 0x92722c85u,
-      0xa2bfe8a1u, 0xa81a664bu, 0xc24b8b70u, 0xc76c51a3u, 0xd192e819u,
-      0xd6990624u, 0xf40e3585u, 0x106aa070u, 0x19a4c116u, 0x1e376c08u,
-      0x2748774cu, 0x34b0bcb5u, 0x391c0cb3u, 0x4ed8aa4au, 0x5b9cca4fu,
-      0x682e6ff3u, 0x748f82eeu, 0x78a5636fu, 0x84c87814u, 0x8cc70208u,
-      0x90befffau, 0xa4506cebu, 0xbef9a3f7u, 0xc67178f2u};
   uint32_t a = s[0], b = s[1], c = s[2], d = s[3];
   uint32_t e = s[4], f = s[5], g = s[6], h = s[7];
+  if (!kRolled) {
+    constexpr uint32_t KI[64] = {
+        0x428a2f98u, 0x71374491u, 0xb5c0fbcfu, 0xe9b5dba5u, 0x3956c25bu, 0x59f111f1u,
+        0x923f82a4u, 0xab1c5ed5u, 0xd807aa98u, 0x12835b01u, 0x243185beu, 0x550c7dc3u,
+        0x72be5d74u, 0x80deb1feu, 0x9bdc06a7u, 0xc19bf174u, 0xe49b69c1u, 0xefbe4786u,
+        0x0fc19dc6u, 0x240ca1ccu, 0x2de92c6fu, 0x4a7484aau, 0x5cb0a9dcu, 0x76f988dau,
+        0x983e5152u, 0xa831c66du, 0xb00327c8u, 0xbf597fc7u, 0xc6e00bf3u, 0xd5a79147u,
+        0x06ca6351u, 0x14292967u, 0x27b70a85u, 0x2e1b2138u, 0x4d2c6dfcu, 0x53380d13u,
+        0x650a7354u, 0x766a0abbu, 0x81c2c92eu, 0x92722c85u, 0xa2bfe8a1u, 0xa81a664bu,
+        0xc24b8b70u, 0xc76c51a3u, 0xd192e819u, 0xd6990624u, 0xf40e3585u, 0x106aa070u,
+        0x19a4c116u, 0x1e376c08u, 0x2748774cu, 0x34b0bcb5u, 0x391c0cb3u, 0x4ed8aa4au,
+        0x5b9cca4fu, 0x682e6ff3u, 0x748f82eeu, 0x78a5636fu, 0x84c87814u, 0x8cc70208u,
+        0x90befffau, 0xa4506cebu, 0xbef9a3f7u, 0xc67178f2u};
 #pragma unroll
-  for (int i = 0; i < 64; i++) {
-    if (i >= 16) {
-      uint32_t x = w[(i - 15) & 15], y = w[(i - 2) & 15];
-      uint32_t s0 = rotr32(x, 7) ^ rotr32(x, 18) ^ (x >> 3);
-      uint32_t s1 = rotr32(y, 17) ^ rotr32(y, 19) ^ (y >> 10);
-      w[i & 15] += s0 + w[(i - 7) & 15] + s1;
+    for (int i = 0; i < 64; i++) {
+      if (i >= 16) {
+        uint32_t x = w[(i - 15) & 15], y = w[(i - 2) & 15];
+        uint32_t s0 = rotr32(x, 7) ^ rotr32(x, 18) ^ (x >> 3);
+        uint32_t s1 = rotr32(y, 17) ^ rotr32(y, 19) ^ (y >> 10);
+        w[i & 15] += s0 + w[(i - 7) & 15] + s1;
+      }
+      uint32_t t1 = h + (rotr32(e, 6) ^ rotr32(e, 11) ^ rotr32(e, 25)) +
+                    ((e & f) ^ (~e & g)) + KI[i] + w[i & 15];
+      uint32_t t2 = (rotr32(a, 2) ^ rotr32(a, 13) ^ rotr32(a, 22)) +
+                    ((a & b) | (c & (a | b)));
+      h = g; g = f; f = e; e = d + t1;
+      d = c; c = b; b = a; a = t1 + t2;
     }
-    uint32_t t1 = h + (rotr32(e, 6) ^ rotr32(e, 11) ^ rotr32(e, 25)) +
-                  ((e & f) ^ (~e & g)) + K[i] + w[i & 15];
-    uint32_t t2 = (rotr32(a, 2) ^ rotr32(a, 13) ^ rotr32(a, 22)) +
-                  ((a & b) | (c & (a | b)));
-    h = g; g = f; f = e; e = d + t1;
-    d = c; c = b; b = a; a = t1 + t2;
+  } else {
+    sha256_16rounds<false>(a, b, c, d, e, f, g, h, w, 0);
+#pragma unroll 1
+    for (int r = 16; r < 64; r += 16) sha256_16rounds<true>(a, b, c, d, e, f, g, h, w, r);
   }
   s[0] += a; s[1] += b; s[2] += c; s[3] += d;
   s[4] += e; s[5] += f; s[6] += g; s[7] += h;
@@ -212,9 +272,18 @@ __device__ __forceinline__ void f64_window_words(const F64Window& win,
   }
 }
 
-// Runs one job in the calling thread.
+// Runs one job in the calling thread. kLoop selects the fast-run code shape
+// (cycles per block on B200, tools/shabench.py): 0 = two unrolled
+// compressions per trip (~4.9k: the 48 KB loop misses the SMSP instruction
+// cache), 1 = one rolled compression per trip with window rotation (~3.3k,
+// default), 2 = one unrolled compression per trip (~3.4k).
+#ifndef CG_CHAIN_LOOP
+#define CG_CHAIN_LOOP 1
+#endif
+template <int kLoop = CG_CHAIN_LOOP>
 __device__ __forceinline__ void run_chain_job(const ChainJob& j,
                                               uint64_t digest_out) {
+  constexpr bool kRolled = kLoop == 1;
   uint32_t s[8];
   if (j.state_in) {
     const uint32_t* si = reinterpret_cast<const uint32_t*>(j.state_in);
@@ -247,7 +316,7 @@ __device__ __forceinline__ void run_chain_job(const ChainJob& j,
 #pragma unroll 1
   for (; blk < run_b; blk++) {
     load_block_slow(j, blk, nblk_total, w);
-    sha256_compress(s, w);
+    sha256_compress<kRolled>(s, w);
   }
   if (run_e > run_b) {
     const ChainSeg& g = j.seg[fs];
@@ -262,25 +331,35 @@ __device__ __forceinline__ void run_chain_job(const ChainJob& j,
     f64_window_load(base, d + 8, dmax, Bw);
     uint64_t n = run_e - run_b;
     uint64_t i = 0;
+    if (kLoop == 0) {
 #pragma unroll 1
-    for (; i + 2 <= n; i += 2) {
-      f64_window_words(A, o, w);
-      f64_window_load(base, d + 8 * (i + 2), dmax, A);
-      sha256_compress(s, w);
-      f64_window_words(Bw, o, w);
-      f64_window_load(base, d + 8 * (i + 3), dmax, Bw);
-      sha256_compress(s, w);
-    }
-    if (i < n) {
-      f64_window_words(A, o, w);
-      sha256_compress(s, w);
+      for (; i + 2 <= n; i += 2) {
+        f64_window_words(A, o, w);
+        f64_window_load(base, d + 8 * (i + 2), dmax, A);
+        sha256_compress<kRolled>(s, w);
+        f64_window_words(Bw, o, w);
+        f64_window_load(base, d + 8 * (i + 3), dmax, Bw);
+        sha256_compress<kRolled>(s, w);
+      }
+      if (i < n) {
+        f64_window_words(A, o, w);
+        sha256_compress<kRolled>(s, w);
+      }
+    } else {
+#pragma unroll 1
+      for (; i < n; i++) {
+        f64_window_words(A, o, w);
+        A = Bw;
+        f64_window_load(base, d + 8 * (i + 2), dmax, Bw);
+        sha256_compress<kRolled>(s, w);
+      }
     }
     blk = run_e;
   }
 #pragma unroll 1
   for (; blk < nblk_total; blk++) {
     load_block_slow(j, blk, nblk_total, w);
-    sha256_compress(s, w);
+    sha256_compress<kRolled>(s, w);
   }
   if (j.state_out) {
     uint32_t* so = reinterpret_cast<uint32_t*>(j.state_out);

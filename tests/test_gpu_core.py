@@ -218,10 +218,11 @@ def test_ingest_ahead_and_out_of_order(ctx):
     half = RequestBatch.from_encoded(reqs[:6])
     want = grp.certify(b)
     want_half = grp.certify(half)
-    t = [grp.ingest(b if i % 2 == 0 else half) for i in range(8)]
+    ring = 16  # cg_group ingest ring depth
+    t = [grp.ingest(b if i % 2 == 0 else half) for i in range(ring)]
     with pytest.raises(InvalidArgument):
         grp.ingest(b)
-    order = [3, 0, 7, 4, 1, 6, 2, 5]
+    order = [(5 * i + 3) % ring for i in range(ring)]  # a permutation
     for i in order:
         r = grp.certify_ticket(t[i])
         w = want if i % 2 == 0 else want_half
