@@ -387,6 +387,84 @@ def cpu_baseline(files, digs, sds, batch, args):
                       f"ensemble_label/result leaves/R+A trees, {dt:.1f} s"}
 
 
+# ------------------------------------------------------------- C5 sweep
+def bench_c5(args, local_rank):
+    """C5 (BASELINE.json configs[4]): agreement + compact label digests over
+    R precomputed per-replica results resident in HBM (cg_agree_device, one
+    launch per step). One JSON line per (R, n, v)."""
+    import torch
+
+    from paper_2205_15757_b200 import Context
+    from paper_2205_15757_b200.workload import signed_requests  # noqa: F401  (import check)
+    torch.cuda.set_device(local_rank)
+    dev = torch.device(f"cuda:{local_rank}")
+    ctx = Context(local_rank)
+    stream = torch.cuda.current_stream()
+    ctx.set_stream(stream.cuda_stream)
+    pk, pk_src = peaks()
+    hbm = pk.get("hbm_gbs", 6650.0)
+    lines = []
+    for spec in args.c5.split(","):
+        R, n, v = (int(float(x)) for x in spec.split("x"))
+        f = 1 if n <= 4 else 2
+        outs = torch.empty(n * R * v, dtype=torch.float64, device=dev)
+        ids = torch.empty(R * 32, dtype=torch.uint8, device=dev)
+        ctx.synth_outputs(0xC5, R, n, v, 0.05, 0.1, outs.data_ptr(), ids.data_ptr())
+        eps = torch.full((R,), 0.05, dtype=torch.float64, device=dev)
+        sel = torch.empty(R, dtype=torch.int32, device=dev)
+        diam = torch.empty(R, dtype=torch.float64, device=dev)
+        sat = torch.empty(R, dtype=torch.uint8, device=dev)
+        st = torch.empty(R, dtype=torch.int8, device=dev)
+        lab = torch.empty(R, dtype=torch.int64, device=dev)
+        dig = torch.empty(R * 32, dtype=torch.uint8, device=dev)
+        flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > L2
+
+        def step():
+            ctx.agree_device(outs.data_ptr(), R * v, v, eps.data_ptr(), R, n, f, v, 0,
+                             sel.data_ptr(), diam.data_ptr(), sat.data_ptr(), st.data_ptr(),
+                             lab.data_ptr(), ids.data_ptr(), 1, dig.data_ptr())
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize()
+        l0 = ctx.launch_count()
+        ms = 0.0
+        with ClockSampler(local_rank) as clk:
+            for _ in range(args.steps):
+                flush.zero_()  # L2 flush between timed launches (outside the events)
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                step()
+                e1.record(stream)
+                torch.cuda.synchronize()
+                ms += e0.elapsed_time(e1)
+        launches = (ctx.launch_count() - l0) // args.steps
+        per = ms / args.steps
+        bytes_req = n * v * 8 + 8 + 32 + (4 + 8 + 1 + 1 + 8 + 32)
+        achieved = bytes_req * R / (per / 1e3) / 1e9
+        satf = float(sat.float().mean().item())
+        lines.append({
+            "metric": "C5 agreement + label-digest results/s (device-resident)",
+            "value": round(R / (per / 1e3), 1), "unit": "req/s", "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(per, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64 agreement / u32 SHA-256", "data": "synthetic (device generator)",
+            "config": {"workload": f"C5 R={R} n={n} f={f} v={v} euclidean eps=0.05",
+                       "l2": "256 MB buffer written between timed launches",
+                       "satisfied_fraction": round(satf, 4)},
+            "gpu_launches": int(launches),
+            "roofline": {"bound": "hbm", "kernel": "agree_rows_kernel" if R >= 4096 else
+                         "select_quorum_kernel + label_digest_kernel",
+                         "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
+                         "frac": round(achieved / hbm, 4), "traffic": None,
+                         "peak_source": f"{pk_src} hbm_gbs",
+                         "algorithmic_bytes_per_request": bytes_req},
+            "clocks": clk.summary()})
+        del outs, ids, flush
+        torch.cuda.empty_cache()
+    return lines
+
+
 def bench_reference(args, rank, world):
     """--impl reference: the reference's CPU path on the host cores."""
     if rank != 0:
@@ -441,6 +519,12 @@ def main():
     ap.add_argument("--mode", default="group", choices=["group", "replica"],
                     help="group: a whole 3-replica group per GPU (weak scaling); "
                          "replica: one replica per GPU, NCCL all-gather (N>1)")
+    ap.add_argument("--workload", default="c2", choices=["c2", "c5"],
+                    help="c2: the headline certified-request pipeline; c5: "
+                         "agreement + label-digest sweep (one line per --c5 spec)")
+    ap.add_argument("--c5", default="1e6x8x1000,1e6x4x1000,1e6x8x10,1e5x8x1000,1e4x8x1000,"
+                                    "1e3x8x1000",
+                    help="comma list of RxNxV for --workload c5")
     ap.add_argument("--trace", default=None,
                     help="write a CUPTI timeline (chrome trace JSON) of --steps "
                          "pipelined steps instead of timing")
@@ -467,6 +551,10 @@ def main():
             dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
     if args.impl == "reference":
         out = bench_reference(args, rank, world)
+    elif args.workload == "c5":
+        for line in bench_c5(args, local_rank):
+            print(json.dumps(line), flush=True)
+        return
     else:
         out = bench_gpu(args, rank, world, local_rank)
     if rank == 0 and out is not None:

@@ -89,6 +89,21 @@ int cg_select_quorum_batch(cg_ctx* ctx, const double* outs,
                            double* diameter, uint8_t* satisfied,
                            int8_t* status, int64_t* label);
 
+/* Device-resident form for large sweeps (C5): every pointer is device
+ * memory, the work is enqueued on the context stream and the call returns
+ * without synchronising. outs(k, p, t) = outs[p*ps + k*rs + t]; all n
+ * results present. label / label_digest may be NULL. label_digest[k] =
+ * SHA-256(0x4C || req_ids[k] || u64be version || u64be label[k]) (new; the
+ * north star's compact agreed-label digest). */
+int cg_agree_device(cg_ctx* ctx, const double* outs, uint64_t ps, uint64_t rs,
+                    const double* eps, uint32_t R, uint32_t n, uint32_t f, uint32_t v,
+                    uint32_t metric, const uint8_t* req_ids, uint64_t version,
+                    uint32_t* selected, double* diameter, uint8_t* satisfied,
+                    int8_t* status, int64_t* label, uint8_t* label_digest);
+/* The compact label digests alone, host buffers (R × 32 ids, R labels). */
+int cg_label_digest_batch(cg_ctx* ctx, const uint8_t* req_ids, const int64_t* labels,
+                          uint32_t R, uint64_t version, uint8_t* out);
+
 /* ---- models (executor seam) --------------------------------------------- */
 /* LinearToyModel canonical file bytes; digest = descriptor weights_digest.
  * Fails with CG_EDIGEST when SHA-256(file) != digest (src/engine.cpp:79). */
@@ -189,12 +204,19 @@ int cg_group_create_dist(cg_ctx* ctx, cg_model* my_model, const uint8_t* all_dig
 
 /* ---- measurement hooks ----------------------------------------------------
  * Per-kernel-class device time from CUDA events recorded on each launching
- * stream (0 conv GEMM, 1 SHA-256 chains, 2 agreement, 3 other).
- * Enabling resets the counters. */
+ * stream (0 conv GEMM, 1 SHA-256 chains, 2 agreement + trees, 3 CNN
+ * auxiliary kernels, 4 NCCL exchange). Enabling resets the counters. */
 void cg_timing_enable(int on);
 int cg_timing_read(int cls, double* total_ms, uint64_t* launches);
 /* Algorithmic FLOPs of one forward of one input (2 x MACs). */
 double cg_model_flops_per_input(const cg_model* m);
+/* C5 synthetic sweep input, generated on the device: per
+ * request k a centre U(0,1)^v, each replica p = centre + U(-a, a) per lane
+ * with a = eps/(8 sqrt(v)) (honest euclidean spread ~eps/10), and with
+ * probability shift_frac a replica shifted by 3 eps/sqrt(v) on every lane
+ * (euclidean distance ~3 eps: the accuracy_experiment "beyond" shift). outs(k, p, t) = outs[p*R*v + k*v + t]; req_ids R × 32. */
+int cg_synth_outputs(cg_ctx* ctx, uint64_t seed, uint32_t R, uint32_t n, uint32_t v,
+                     double eps, double shift_frac, double* outs, uint8_t* req_ids);
 
 /* ---- test hooks (not on the certified path) -----------------------------
  * One tcgen05 conv-GEMM launch on host buffers (bf16 as uint16 bits). */

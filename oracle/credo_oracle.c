@@ -430,3 +430,39 @@ uint64_t oc_attest_manifest(uint64_t B, uint64_t N, const uint64_t* sel_mask,
     if (!satisfied[k]) { kinds[cnt] = 2; nodes[cnt] = 0; ops[cnt] = k; cnt++; }
   return cnt;
 }
+
+/* ------------------------------------------------------ C5 agreement sweep */
+void oc_label_digest(const uint8_t req_id[32], uint64_t version, int64_t label,
+                     uint8_t out[32]) {
+  uint8_t m[49];
+  m[0] = 0x4C;
+  memcpy(m + 1, req_id, 32);
+  for (int i = 0; i < 8; i++) m[33 + i] = (uint8_t)(version >> (56 - 8 * i));
+  const uint64_t l = (uint64_t)label;
+  for (int i = 0; i < 8; i++) m[41 + i] = (uint8_t)(l >> (56 - 8 * i));
+  oc_sha256(m, sizeof m, out);
+}
+
+int oc_agree_batch(const double* outs, uint64_t R, uint64_t n, uint64_t f,
+                   uint64_t v, uint32_t metric, const double* eps,
+                   const uint8_t* req_ids, uint64_t version, uint64_t* sel,
+                   double* diam, uint8_t* sat, int64_t* label, uint8_t* digest) {
+  double* rows = (double*)malloc(n * v * sizeof(double));
+  uint64_t idx[64];
+  int rc = 0;
+  for (uint64_t i = 0; i < n && i < 64; i++) idx[i] = i;
+  for (uint64_t k = 0; k < R && rc == 0; k++) {
+    for (uint64_t p = 0; p < n; p++)
+      memcpy(rows + p * v, outs + p * R * v + k * v, v * sizeof(double));
+    int s = 0;
+    if (oc_select_quorum(rows, idx, n, v, n, f, metric, eps[k], &sel[k], &diam[k], &s) != 0) {
+      rc = -1;
+      break;
+    }
+    sat[k] = (uint8_t)s;
+    label[k] = s ? oc_ensemble_label(rows, n, v, sel[k], f) : -1;
+    if (req_ids && digest) oc_label_digest(req_ids + 32 * k, version, label[k], digest + 32 * k);
+  }
+  free(rows);
+  return rc;
+}

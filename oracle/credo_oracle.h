@@ -84,6 +84,18 @@ uint64_t oc_failure_leaf(const uint8_t req_id[32], const char* gid,
                          uint64_t gid_len, uint64_t version, const char* reason,
                          uint64_t reason_len, uint8_t* out);
 
+/* Compact agreed-label digest (new, north star / SURVEY §8(d) C5 "D2"):
+ * SHA-256(0x4C || req_id[32] || u64be version || u64be label). */
+void oc_label_digest(const uint8_t req_id[32], uint64_t version, int64_t label,
+                     uint8_t out[32]);
+/* C5 batch: outs(k, p, t) = outs[p*R*v + k*v + t], all n present; per
+ * request select_quorum + ensemble_label + label digest (NULL ids: none).
+ * Returns 0 or -1 (invalid arguments, as select_quorum). */
+int oc_agree_batch(const double* outs, uint64_t R, uint64_t n, uint64_t f,
+                   uint64_t v, uint32_t metric, const double* eps,
+                   const uint8_t* req_ids, uint64_t version, uint64_t* sel,
+                   double* diam, uint8_t* sat, int64_t* label, uint8_t* digest);
+
 #ifdef __cplusplus
 }
 #endif

@@ -139,6 +139,33 @@ class Oracle:
         return self.L.oc_ensemble_label(_p(outs), u64(outs.shape[0]),
                                         u64(outs.shape[1]), u64(mask), u64(f))
 
+    def label_digest(self, req_id: bytes, version: int, label: int) -> bytes:
+        out = C.create_string_buffer(32)
+        self.L.oc_label_digest(req_id, u64(version), C.c_int64(label), out)
+        return out.raw
+
+    def agree_batch(self, outs: np.ndarray, f: int, metric: int, eps, req_ids=None,
+                    version: int = 0):
+        """outs (n, R, v): per request select_quorum + ensemble_label (+ the
+        compact label digests when req_ids (R, 32) are given)."""
+        outs = np.ascontiguousarray(outs, np.float64)
+        n, R, v = outs.shape
+        eps = np.ascontiguousarray(np.broadcast_to(eps, (R,)), np.float64)
+        sel = np.zeros(R, np.uint64)
+        diam = np.zeros(R)
+        sat = np.zeros(R, np.uint8)
+        lab = np.zeros(R, np.int64)
+        dig = np.zeros((R, 32), np.uint8)
+        ids = None if req_ids is None else np.ascontiguousarray(req_ids, np.uint8)
+        rc = self.L.oc_agree_batch(_p(outs), u64(R), u64(n), u64(f), u64(v), u32(metric),
+                                   _p(eps), None if ids is None else _p(ids), u64(version),
+                                   _p(sel), _p(diam), _p(sat), _p(lab),
+                                   None if ids is None else _p(dig))
+        if rc != 0:
+            raise ValueError("select_quorum: invalid argument")
+        return dict(selected=sel.astype(np.uint32), diameter=diam, satisfied=sat.astype(bool),
+                    label=lab, digest=dig if ids is not None else None)
+
     def argmax(self, v) -> int:
         v = np.ascontiguousarray(v, np.float64)
         return self.L.oc_argmax(_p(v), u64(v.size))

@@ -212,6 +212,38 @@ class Context:
             raise e
         return res
 
+    def agree_device(self, outs_ptr: int, ps: int, rs: int, eps_ptr: int, R: int, n: int,
+                     f: int, v: int, metric: int, sel_ptr: int, diam_ptr: int, sat_ptr: int,
+                     status_ptr: int, label_ptr: int = 0, req_ids_ptr: int = 0,
+                     version: int = 0, digest_ptr: int = 0):
+        """cg_agree_device: device pointers (e.g. torch tensors' data_ptr()),
+        enqueued on this context's stream without a host sync."""
+        vp_ = lambda x: vp(x) if x else None  # noqa: E731
+        L = self.L
+        L.cg_agree_device.argtypes = [vp, vp, u64, u64, vp, u32, u32, u32, u32, u32, vp, u64,
+                                      vp, vp, vp, vp, vp, vp]
+        self._check(L.cg_agree_device(self.h, vp_(outs_ptr), ps, rs, vp_(eps_ptr), R, n, f, v,
+                                      metric, vp_(req_ids_ptr), version, vp_(sel_ptr),
+                                      vp_(diam_ptr), vp_(sat_ptr), vp_(status_ptr),
+                                      vp_(label_ptr), vp_(digest_ptr)))
+
+    def label_digests(self, req_ids: np.ndarray, labels: np.ndarray, version: int) -> np.ndarray:
+        """SHA-256(0x4C || id || u64be version || u64be label) per request."""
+        ids = np.ascontiguousarray(req_ids, np.uint8).reshape(-1, 32)
+        lab = np.ascontiguousarray(labels, np.int64)
+        out = np.zeros((len(lab), 32), np.uint8)
+        self._check(self.L.cg_label_digest_batch(self.h, _p(ids), _p(lab), u32(len(lab)),
+                                                 u64(version), _p(out)))
+        return out
+
+    def synth_outputs(self, seed: int, R: int, n: int, v: int, eps: float, shift_frac: float,
+                      outs_ptr: int, ids_ptr: int = 0):
+        """C5 synthetic per-replica outputs generated on the device."""
+        L = self.L
+        L.cg_synth_outputs.argtypes = [vp, u64, u32, u32, u32, dbl, dbl, vp, vp]
+        self._check(L.cg_synth_outputs(self.h, seed, R, n, v, eps, shift_frac, vp(outs_ptr),
+                                       vp(ids_ptr) if ids_ptr else None))
+
     def select_quorum(self, results: dict, n: int, f: int, metric: int,
                       epsilon: float):
         """distance::select_quorum(map<node, vector<double>>, n, f, m, eps)."""

@@ -238,6 +238,213 @@ void launch_select_quorum(const double* outs, uint64_t ps, uint64_t rs,
   CG_CHECK_LAUNCH();
 }
 
+// ------------------------------------------- agreement, throughput form (C5)
+// One thread per request, for large batches with all M <= 8 results present:
+// the thread streams its M rows once (16-byte loads, each row sequential so
+// every sector is consumed whole) and keeps all M(M-1)/2 pair accumulators,
+// the per-row argmax and the running state in registers. The sums stay
+// sequential and un-fused per pair, so distances equal distance.cpp:70-117
+// bit for bit; the subset search visits sizes M, M-1, ... and stops at the
+// first size with a valid subset, which is the same winner as the exhaustive
+// scan of distance.cpp:178-205 (size is the first criterion). Optional
+// epilogue: the compact label digest (sha256_label_digest) per request.
+template <int M>
+__device__ __forceinline__ void agree_step(const double (&x)[M], uint32_t t, int metric,
+                                           double (&acc)[M * (M - 1) / 2], double (&bv)[M],
+                                           uint32_t (&bi)[M]) {
+  int p = 0;
+#pragma unroll
+  for (int i = 0; i < M; i++)
+#pragma unroll
+    for (int j = i + 1; j < M; j++, p++) {
+      double d = __dsub_rn(x[i], x[j]);
+      if (metric == 0) {
+        acc[p] = __dadd_rn(acc[p], __dmul_rn(d, d));
+      } else {
+        d = fabs(d);
+        acc[p] = (acc[p] < d) ? d : acc[p];
+      }
+    }
+#pragma unroll
+  for (int i = 0; i < M; i++)
+    if (bv[i] < x[i]) {  // std::max_element: first maximum
+      bv[i] = x[i];
+      bi[i] = t;
+    }
+}
+
+__device__ __forceinline__ double ld_stream(const double* p) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double2 ld_stream2(const double* p) {
+  double2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];"
+               : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+}
+
+template <int M>
+__global__ void __launch_bounds__(128) agree_rows_kernel(
+    const double* __restrict__ outs, uint64_t ps, uint64_t rs, const double* __restrict__ eps,
+    uint32_t R, uint32_t f, uint32_t v, int metric, int vec2,
+    const uint8_t* __restrict__ req_ids, uint64_t version, uint32_t* __restrict__ selected,
+    double* __restrict__ diameter, uint8_t* __restrict__ satisfied,
+    int8_t* __restrict__ status, int64_t* __restrict__ label, uint8_t* __restrict__ digest) {
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= R) return;
+  constexpr int P = M * (M - 1) / 2;
+  const double* row = outs + (uint64_t)k * rs;
+  double acc[P], bv[M];
+  uint32_t bi[M];
+#pragma unroll
+  for (int p = 0; p < P; p++) acc[p] = 0.0;
+#pragma unroll
+  for (int i = 0; i < M; i++) {
+    bv[i] = __ldg(row + i * ps);
+    bi[i] = 0;
+  }
+  uint32_t t = 0;
+  if (vec2) {  // 4 lanes per trip: 2M independent 16-byte loads in flight
+#pragma unroll 1
+    for (; t + 4 <= v; t += 4) {
+      double2 q0[M], q1[M];
+#pragma unroll
+      for (int i = 0; i < M; i++) {
+        q0[i] = ld_stream2(row + i * ps + t);
+        q1[i] = ld_stream2(row + i * ps + t + 2);
+      }
+      double x[M];
+#pragma unroll
+      for (int i = 0; i < M; i++) x[i] = q0[i].x;
+      agree_step<M>(x, t, metric, acc, bv, bi);
+#pragma unroll
+      for (int i = 0; i < M; i++) x[i] = q0[i].y;
+      agree_step<M>(x, t + 1, metric, acc, bv, bi);
+#pragma unroll
+      for (int i = 0; i < M; i++) x[i] = q1[i].x;
+      agree_step<M>(x, t + 2, metric, acc, bv, bi);
+#pragma unroll
+      for (int i = 0; i < M; i++) x[i] = q1[i].y;
+      agree_step<M>(x, t + 3, metric, acc, bv, bi);
+    }
+  }
+#pragma unroll 1
+  for (; t < v; t++) {
+    double x[M];
+#pragma unroll
+    for (int i = 0; i < M; i++) x[i] = ld_stream(row + i * ps + t);
+    agree_step<M>(x, t, metric, acc, bv, bi);
+  }
+  if (metric == 0) {
+#pragma unroll
+    for (int p = 0; p < P; p++) acc[p] = __dsqrt_rn(acc[p]);
+  }
+  // subset search, sizes descending (need = n - f with n = M)
+  const double e = eps[k];
+  const int need = M - (int)f;
+  Cand best{0, 0, 0, 0.0};
+  for (int s = M; s >= need && !best.valid; s--) {
+#pragma unroll 1
+    for (uint32_t mask = 1; mask < (1u << M); mask++) {
+      if (__popc(mask) != s) continue;
+      double dm = 0.0;
+      bool ok = true;
+      int p = 0;
+#pragma unroll
+      for (int i = 0; i < M; i++)
+#pragma unroll
+        for (int j = i + 1; j < M; j++, p++)
+          if (ok && (mask >> i & 1) && (mask >> j & 1)) {
+            dm = (dm < acc[p]) ? acc[p] : dm;
+            if (dm > e) ok = false;
+          }
+      if (!ok) continue;
+      Cand c{1, (uint32_t)s, mask, dm};
+      if (cand_better(c, best)) best = c;
+    }
+  }
+  status[k] = 0;
+  selected[k] = best.valid ? best.mask : 0;
+  diameter[k] = best.valid ? best.diam : 0.0;
+  satisfied[k] = best.valid ? 1 : 0;
+  int64_t win = -1;
+  if (best.valid) {  // ensemble_label over the quorum members
+    double win_conf = -1.0;
+#pragma unroll
+    for (int i = 0; i < M; i++) {
+      if (!(best.mask >> i & 1)) continue;
+      const uint32_t l = bi[i];
+      bool seen = false;
+#pragma unroll
+      for (int q = 0; q < i; q++)
+        if ((best.mask >> q & 1) && bi[q] == l) seen = true;
+      if (seen) continue;
+      uint32_t cnt = 0;
+      double conf = 0.0;
+#pragma unroll
+      for (int q = 0; q < M; q++)
+        if ((best.mask >> q & 1) && bi[q] == l) {
+          cnt++;
+          conf = (conf < bv[q]) ? bv[q] : conf;
+        }
+      if (cnt <= f) continue;
+      if (conf > win_conf || (conf == win_conf && win >= 0 && (int64_t)l < win)) {
+        win = l;
+        win_conf = conf;
+      }
+    }
+  }
+  if (label) label[k] = win;
+  if (digest) sha256_label_digest(req_ids + 32ull * k, version, win, digest + 32ull * k);
+}
+
+bool agree_rows_eligible(uint32_t R, uint32_t n, uint32_t f, uint32_t v, uint32_t metric,
+                         const uint32_t* present) {
+  return present == nullptr && n >= 2 && n <= 8 && f < n && v >= 1 &&
+         (metric == 0 || metric == 2) && R >= kAgreeRowsMinBatch;
+}
+
+void launch_agree_rows(const double* outs, uint64_t ps, uint64_t rs, const double* eps,
+                       uint32_t R, uint32_t n, uint32_t f, uint32_t v, uint32_t metric,
+                       const uint8_t* req_ids, uint64_t version, uint32_t* selected,
+                       double* diameter, uint8_t* satisfied, int8_t* status, int64_t* label,
+                       uint8_t* digest, cudaStream_t st) {
+  if (R == 0) return;
+  const int vec2 = ((ps | rs) % 2 == 0) && ((uintptr_t)outs % 16 == 0);
+  const unsigned grid = (unsigned)ceil_div(R, 128);
+#define CG_AGREE(MM)                                                                    \
+  case MM:                                                                              \
+    agree_rows_kernel<MM><<<grid, 128, 0, st>>>(outs, ps, rs, eps, R, f, v, (int)metric, \
+                                                vec2, req_ids, version, selected,       \
+                                                diameter, satisfied, status, label,     \
+                                                digest);                                \
+    break;
+  switch (n) {
+    CG_AGREE(2) CG_AGREE(3) CG_AGREE(4) CG_AGREE(5) CG_AGREE(6) CG_AGREE(7) CG_AGREE(8)
+    default: throw InvalidArgument("agree_rows: n out of range");
+  }
+#undef CG_AGREE
+  CG_CHECK_LAUNCH();
+}
+
+// Compact label digests alone (labels already on the device).
+__global__ void label_digest_kernel(const uint8_t* __restrict__ req_ids,
+                                    const int64_t* __restrict__ label, uint32_t R,
+                                    uint64_t version, uint8_t* __restrict__ out) {
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < R) sha256_label_digest(req_ids + 32ull * k, version, label[k], out + 32ull * k);
+}
+
+void launch_label_digest(const uint8_t* req_ids, const int64_t* label, uint32_t R,
+                         uint64_t version, uint8_t* out, cudaStream_t st) {
+  if (R == 0) return;
+  label_digest_kernel<<<(unsigned)ceil_div(R, 128), 128, 0, st>>>(req_ids, label, R, version,
+                                                                  out);
+  CG_CHECK_LAUNCH();
+}
+
 // ----------------------------------------------------- attestation manifest
 // Single CTA. Manifest order (coordinator.cpp:774-832): whole_batch leaves
 // by node, then single leaves by (op, node), then failure leaves by op.

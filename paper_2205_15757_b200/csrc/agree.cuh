@@ -11,6 +11,18 @@ void launch_select_quorum(const double* outs, uint64_t ps, uint64_t rs,
                           uint32_t metric, uint32_t* selected, double* diameter,
                           uint8_t* satisfied, int8_t* status, int64_t* label,
                           cudaStream_t st);
+// Throughput form of select_quorum + ensemble_label (+ optional compact
+// label digests) for large all-present batches with n <= 8 (C5 sweep).
+constexpr uint32_t kAgreeRowsMinBatch = 4096;
+bool agree_rows_eligible(uint32_t R, uint32_t n, uint32_t f, uint32_t v, uint32_t metric,
+                         const uint32_t* present);
+void launch_agree_rows(const double* outs, uint64_t ps, uint64_t rs, const double* eps,
+                       uint32_t R, uint32_t n, uint32_t f, uint32_t v, uint32_t metric,
+                       const uint8_t* req_ids, uint64_t version, uint32_t* selected,
+                       double* diameter, uint8_t* satisfied, int8_t* status, int64_t* label,
+                       uint8_t* digest, cudaStream_t st);
+void launch_label_digest(const uint8_t* req_ids, const int64_t* label, uint32_t R,
+                         uint64_t version, uint8_t* out, cudaStream_t st);
 void launch_attest_manifest(uint32_t B, uint32_t N, const uint32_t* sel,
                             const uint8_t* sat, const uint8_t* r_roots,
                             const uint8_t* req_ids, const uint8_t* gid,

@@ -485,10 +485,15 @@ int cg_select_quorum_batch(cg_ctx* ctx, const double* outs,
     if (present)
       CG_CUDA(cudaMemcpyAsync(ctx->d_u32a.p, present, 4 * (size_t)R,
                               cudaMemcpyHostToDevice, st));
-    launch_select_quorum(ctx->d_f64.p, v, (uint64_t)n * v,
-                         present ? ctx->d_u32a.p : nullptr, ctx->d_f64b.p, R, n,
-                         f, v, metric, ctx->d_u32b.p, d_diam.p, ctx->d_u8.p,
-                         ctx->d_i8.p, label ? ctx->d_i64.p : nullptr, st);
+    if (agree_rows_eligible(R, n, f, v, metric, present))
+      launch_agree_rows(ctx->d_f64.p, v, (uint64_t)n * v, ctx->d_f64b.p, R, n, f, v, metric,
+                        nullptr, 0, ctx->d_u32b.p, d_diam.p, ctx->d_u8.p, ctx->d_i8.p,
+                        label ? ctx->d_i64.p : nullptr, nullptr, st);
+    else
+      launch_select_quorum(ctx->d_f64.p, v, (uint64_t)n * v,
+                           present ? ctx->d_u32a.p : nullptr, ctx->d_f64b.p, R, n,
+                           f, v, metric, ctx->d_u32b.p, d_diam.p, ctx->d_u8.p,
+                           ctx->d_i8.p, label ? ctx->d_i64.p : nullptr, st);
     std::vector<int8_t> stat(R);
     CG_CUDA(cudaMemcpyAsync(selected, ctx->d_u32b.p, 4 * (size_t)R, cudaMemcpyDeviceToHost, st));
     CG_CUDA(cudaMemcpyAsync(diameter, d_diam.p, 8 * (size_t)R, cudaMemcpyDeviceToHost, st));
@@ -503,6 +508,48 @@ int cg_select_quorum_batch(cg_ctx* ctx, const double* outs,
       bad |= stat[r] != 0;
     }
     if (bad) throw InvalidArgument("select_quorum: invalid argument for some request");
+    return CG_OK;
+  });
+}
+
+// Device-resident agreement sweep (C5): everything already in HBM, enqueued
+// on the ctx stream without a host sync.
+int cg_agree_device(cg_ctx* ctx, const double* outs, uint64_t ps, uint64_t rs,
+                    const double* eps, uint32_t R, uint32_t n, uint32_t f, uint32_t v,
+                    uint32_t metric, const uint8_t* req_ids, uint64_t version,
+                    uint32_t* selected, double* diameter, uint8_t* satisfied, int8_t* status,
+                    int64_t* label, uint8_t* label_digest) {
+  return guarded(ctx, [&] {
+    if (R == 0) return CG_OK;
+    if (n == 0 || n > 20) throw InvalidArgument("select_quorum: bad n or too many results");
+    if (label_digest && (!label || !req_ids))
+      throw InvalidArgument("label digests need label and request id buffers");
+    cudaStream_t st = ctx->stream;
+    if (agree_rows_eligible(R, n, f, v, metric, nullptr)) {
+      launch_agree_rows(outs, ps, rs, eps, R, n, f, v, metric, req_ids, version, selected,
+                        diameter, satisfied, status, label, label_digest, st);
+    } else {
+      launch_select_quorum(outs, ps, rs, nullptr, eps, R, n, f, v, metric, selected, diameter,
+                           satisfied, status, label, st);
+      if (label_digest) launch_label_digest(req_ids, label, R, version, label_digest, st);
+    }
+    return CG_OK;
+  });
+}
+
+int cg_label_digest_batch(cg_ctx* ctx, const uint8_t* req_ids, const int64_t* labels,
+                          uint32_t R, uint64_t version, uint8_t* out) {
+  return guarded(ctx, [&] {
+    if (R == 0) return CG_OK;
+    ctx->d_u8.ensure(32 * (size_t)R);
+    ctx->d_i64.ensure(R);
+    ctx->d_out.ensure(32 * (size_t)R);
+    cudaStream_t st = ctx->stream;
+    CG_CUDA(cudaMemcpyAsync(ctx->d_u8.p, req_ids, 32 * (size_t)R, cudaMemcpyHostToDevice, st));
+    CG_CUDA(cudaMemcpyAsync(ctx->d_i64.p, labels, 8 * (size_t)R, cudaMemcpyHostToDevice, st));
+    launch_label_digest(ctx->d_u8.p, ctx->d_i64.p, R, version, ctx->d_out.p, st);
+    CG_CUDA(cudaMemcpyAsync(out, ctx->d_out.p, 32 * (size_t)R, cudaMemcpyDeviceToHost, st));
+    CG_CUDA(cudaStreamSynchronize(st));
     return CG_OK;
   });
 }

@@ -200,3 +200,55 @@ extern "C" int cg_dbg_conv_gemm(cg_ctx* ctx, const uint16_t* A, int rowsA,
     return CG_ECUDA;
   }
 }
+
+// ------------------------------------------------- C5 synthetic generator
+namespace {
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {  // splitmix64 finaliser
+  z += 0x9e3779b97f4a7c15ull;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+__device__ __forceinline__ double unit(uint64_t h) {  // [0, 1)
+  return (double)(h >> 11) * (1.0 / 9007199254740992.0);
+}
+__global__ void synth_outputs_kernel(uint64_t seed, uint32_t R, uint32_t n, uint32_t v,
+                                     double eps, double shift_frac, double* outs) {
+  const uint64_t total = (uint64_t)R * v;
+  const double jit = eps / (8.0 * sqrt((double)v));  // honest euclidean spread ~ eps/10
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = e / v, t = e % v;
+    const double c = unit(mix64(seed ^ mix64(k * 0x100000001b3ull + t)));
+    for (uint32_t p = 0; p < n; p++) {
+      const uint64_t hk = mix64(seed + 0x51ull + mix64(k * 64 + p));
+      const double shift = unit(hk) < shift_frac ? 3.0 * eps / sqrt((double)v) : 0.0;
+      const double j = (unit(mix64(hk ^ (t * 0x9e3779b97f4a7c15ull))) * 2.0 - 1.0) * jit;
+      outs[(uint64_t)p * total + e] = c + j + shift;
+    }
+  }
+}
+__global__ void synth_ids_kernel(uint64_t seed, uint32_t R, uint8_t* ids) {
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= R) return;
+  uint64_t* o = reinterpret_cast<uint64_t*>(ids + 32ull * k);
+  for (int i = 0; i < 4; i++) o[i] = mix64(seed * 31 + k * 4ull + i);
+}
+}  // namespace
+
+extern "C" int cg_synth_outputs(cg_ctx* ctx, uint64_t seed, uint32_t R, uint32_t n, uint32_t v,
+                                double eps, double shift_frac, double* outs, uint8_t* req_ids) {
+  try {
+    cudaStream_t st = (cudaStream_t)cg_ctx_stream(ctx);
+    if (R == 0) return CG_OK;
+    synth_outputs_kernel<<<148 * 8, 256, 0, st>>>(seed, R, n, v, eps, shift_frac, outs);
+    CG_CHECK_LAUNCH();
+    if (req_ids) {
+      synth_ids_kernel<<<(unsigned)ceil_div(R, 128), 128, 0, st>>>(seed, R, req_ids);
+      CG_CHECK_LAUNCH();
+    }
+    return CG_OK;
+  } catch (const std::exception&) {
+    return CG_ECUDA;
+  }
+}

@@ -418,4 +418,35 @@ __device__ __forceinline__ void sha256_tagged_digest_leaf(uint8_t tag,
   store_digest(s, out);
 }
 
+// Compact agreed-label digest (SURVEY §8(d) C5 "D2"; new, no reference
+// equivalent, composed like the reference's leaves from Encoder fields):
+// SHA-256(0x4C || request_id[32] || u64be version || u64be label), label -1
+// = no agreed label. 49 bytes: one block.
+constexpr uint8_t kLabelDigestTag = 0x4C;
+__device__ __forceinline__ void sha256_label_digest(const uint8_t* rid, uint64_t version,
+                                                    int64_t label, uint8_t* out) {
+  const uint32_t* rp = reinterpret_cast<const uint32_t*>(rid);  // 4-byte aligned
+  uint32_t r[8];
+#pragma unroll
+  for (int i = 0; i < 8; i++) r[i] = bswap32(rp[i]);
+  const uint32_t vh = (uint32_t)(version >> 32), vl = (uint32_t)version;
+  const uint64_t lu = (uint64_t)label;
+  const uint32_t lh = (uint32_t)(lu >> 32), ll = (uint32_t)lu;
+  uint32_t w[16], s[8];
+  sha256_iv(s);
+  w[0] = ((uint32_t)kLabelDigestTag << 24) | (r[0] >> 8);
+#pragma unroll
+  for (int i = 1; i < 8; i++) w[i] = (r[i - 1] << 24) | (r[i] >> 8);
+  w[8] = (r[7] << 24) | (vh >> 8);
+  w[9] = (vh << 24) | (vl >> 8);
+  w[10] = (vl << 24) | (lh >> 8);
+  w[11] = (lh << 24) | (ll >> 8);
+  w[12] = (ll << 24) | 0x00800000u;
+  w[13] = 0;
+  w[14] = 0;
+  w[15] = 49 * 8;
+  sha256_compress(s, w);
+  store_digest(s, out);
+}
+
 }  // namespace cg

@@ -182,3 +182,31 @@ def test_live_reference_cross_check(oracle):
     for n in (0, 1, 63, 64, 65, 1000):
         m = rng.integers(0, 256, n, dtype=np.uint8).tobytes()
         assert oracle.sha256(m) == R.sha256(m)
+
+
+def test_label_digest_layout(oracle):
+    """The compact agreed-label digest (new, C5 'D2') is plain SHA-256 over
+    0x4C || id || u64be version || u64be label; pinned by the SHA KATs."""
+    import hashlib
+    rng = np.random.default_rng(9)
+    for label in (-1, 0, 7, 999, 2**40):
+        rid = rng.integers(0, 256, 32, dtype=np.uint8).tobytes()
+        want = hashlib.sha256(b"\x4c" + rid + (3).to_bytes(8, "big")
+                              + label.to_bytes(8, "big", signed=True)).digest()
+        assert oracle.label_digest(rid, 3, label) == want
+
+
+def test_agree_batch_matches_per_request(oracle):
+    rng = np.random.default_rng(10)
+    n, R, v = 5, 40, 7
+    outs = rng.random((n, R, v))
+    outs[rng.random((n, R)) < 0.2] += 0.5
+    eps = rng.choice([0.2, 0.6, 1.0], R)
+    ids = rng.integers(0, 256, (R, 32), dtype=np.uint8)
+    r = oracle.agree_batch(outs, 1, 0, eps, ids, version=2)
+    for k in range(R):
+        mask, diam, sat = oracle.select_quorum(outs[:, k], np.arange(n), n, 1, 0, eps[k])
+        assert (mask, diam, sat) == (int(r["selected"][k]), r["diameter"][k], r["satisfied"][k])
+        lab = oracle.ensemble_label(outs[:, k], mask, 1) if sat else -1
+        assert lab == r["label"][k]
+        assert r["digest"][k].tobytes() == oracle.label_digest(ids[k].tobytes(), 2, lab)
