@@ -14,27 +14,6 @@
 
 namespace cg {
 
-// --------------------------------------------------------------- delta
-__device__ __forceinline__ double delta_dev(uint32_t metric, const double* x,
-                                            const double* y, uint32_t v) {
-  if (metric == 0) {  // euclidean: acc += d*d in lane order, then sqrt
-    double acc = 0.0;
-#pragma unroll 4
-    for (uint32_t i = 0; i < v; i++) {
-      double d = __dsub_rn(__ldg(x + i), __ldg(y + i));
-      acc = __dadd_rn(acc, __dmul_rn(d, d));
-    }
-    return __dsqrt_rn(acc);
-  }
-  if (metric == 1) return fabs(__dsub_rn(__ldg(x), __ldg(y)));
-  double worst = 0.0;  // chebyshev: std::max(worst, |x-y|)
-  for (uint32_t i = 0; i < v; i++) {
-    double d = fabs(__dsub_rn(__ldg(x + i), __ldg(y + i)));
-    worst = (worst < d) ? d : worst;
-  }
-  return worst;
-}
-
 struct Cand {
   uint32_t valid, size, mask;
   double diam;
@@ -63,6 +42,15 @@ __device__ __forceinline__ Cand shfl_cand(const Cand& c, int src) {
 
 constexpr int kQThreads = 128;
 constexpr int kMaxM = 20;
+constexpr int kQChunk = 64;                                            // lanes per smem chunk
+constexpr int kQPairsPerThread = (kMaxM * (kMaxM - 1) / 2 + kQThreads - 1) / kQThreads;
+constexpr int kQPrefetch = (kMaxM * kQChunk + kQThreads - 1) / kQThreads;
+
+// metric 1 (max_minus_min) is defined on scalars only: |x0 - y0|
+__device__ __forceinline__ double rows_first(const double* outs, const uint32_t* nodes, int i,
+                                             uint64_t ps, uint32_t k, uint64_t rs) {
+  return __ldg(outs + nodes[i] * ps + k * rs);
+}
 
 // One CTA per request. outs(k, p, i) = outs[p*ps + k*rs + i].
 __global__ void __launch_bounds__(kQThreads) select_quorum_kernel(
@@ -112,16 +100,102 @@ __global__ void __launch_bounds__(kQThreads) select_quorum_kernel(
   }
   const int m = s_m;
   const uint32_t need = n - f;
-  // pairwise distances once (distance.cpp:167-174)
+  // Pairwise distances once (distance.cpp:167-174) plus every row's argmax
+  // (experiments.cpp:99-101), in one pass: the m rows stream through shared
+  // memory in chunks of kQChunk lanes (coalesced loads, next chunk prefetched
+  // into registers), one thread per pair keeps its sequential un-fused sum,
+  // threads m.. of the last warp scan rows for the first maximum.
+  extern __shared__ double q_rows[];  // 2 buffers x m rows x (kQChunk + 1)
   const int npairs = m * (m - 1) / 2;
-  for (int pr = tid; pr < npairs; pr += kQThreads) {
-    int i = 0, rem = pr;
+  const int stride = kQChunk + 1;     // +1: rows land on distinct banks
+  int pi[kQPairsPerThread], pj[kQPairsPerThread];
+  double acc[kQPairsPerThread];
+#pragma unroll
+  for (int q = 0; q < kQPairsPerThread; q++) {
+    const int pr = tid + q * kQThreads;
+    int i = 0, rem = pr < npairs ? pr : 0;
     while (rem >= m - 1 - i) { rem -= m - 1 - i; i++; }
-    int j = i + 1 + rem;
-    double d = delta_dev(metric, outs + nodes[i] * ps + k * rs,
-                         outs + nodes[j] * ps + k * rs, v);
-    dist[i * kMaxM + j] = d;
-    dist[j * kMaxM + i] = d;
+    pi[q] = i;
+    pj[q] = i + 1 + rem;
+    acc[q] = 0.0;
+  }
+  const int arow = tid - (kQThreads - 32);  // argmax row of this thread (last warp)
+  double abv = 0.0;
+  uint32_t abi = 0;
+  if (arow >= 0 && arow < m) abv = __ldg(outs + nodes[arow] * ps + k * rs);
+  const int per = (m * kQChunk + kQThreads - 1) / kQThreads;  // prefetch slots
+  double pf[kQPrefetch];
+  auto fetch = [&](uint32_t c0) {
+#pragma unroll
+    for (int q = 0; q < kQPrefetch; q++) {
+      const int e = tid + q * kQThreads;
+      if (q < per && e < m * kQChunk) {
+        const int r = e / kQChunk, t = e % kQChunk;
+        pf[q] = (c0 + t < v) ? __ldg(outs + nodes[r] * ps + k * rs + c0 + t) : 0.0;
+      }
+    }
+  };
+  auto stash = [&](int buf) {
+#pragma unroll
+    for (int q = 0; q < kQPrefetch; q++) {
+      const int e = tid + q * kQThreads;
+      if (q < per && e < m * kQChunk)
+        q_rows[(buf * m + e / kQChunk) * stride + e % kQChunk] = pf[q];
+    }
+  };
+  fetch(0);
+  stash(0);
+  __syncthreads();
+  int buf = 0;
+  for (uint32_t c0 = 0; c0 < v; c0 += kQChunk) {
+    const bool more = c0 + kQChunk < v;
+    if (more) fetch(c0 + kQChunk);
+    const int len = (int)min((uint32_t)kQChunk, v - c0);
+    const double* rows = q_rows + buf * m * stride;
+#pragma unroll
+    for (int q = 0; q < kQPairsPerThread; q++) {
+      if (tid + q * kQThreads >= npairs) continue;
+      const double* x = rows + pi[q] * stride;
+      const double* y = rows + pj[q] * stride;
+      double a = acc[q];
+      if (metric == 0) {
+        for (int t = 0; t < len; t++) {
+          const double d = __dsub_rn(x[t], y[t]);
+          a = __dadd_rn(a, __dmul_rn(d, d));
+        }
+      } else {
+        for (int t = 0; t < len; t++) {
+          const double d = fabs(__dsub_rn(x[t], y[t]));
+          a = (a < d) ? d : a;
+        }
+      }
+      acc[q] = a;
+    }
+    if (arow >= 0 && arow < m) {
+      const double* x = rows + arow * stride;
+      for (int t = 0; t < len; t++)
+        if (abv < x[t]) {  // std::max_element: first maximum
+          abv = x[t];
+          abi = c0 + t;
+        }
+    }
+    if (more) stash(buf ^ 1);
+    __syncthreads();
+    buf ^= 1;
+  }
+#pragma unroll
+  for (int q = 0; q < kQPairsPerThread; q++) {
+    if (tid + q * kQThreads >= npairs) continue;
+    double d = acc[q];
+    if (metric == 0) d = __dsqrt_rn(d);
+    else if (metric == 1) d = fabs(__dsub_rn(rows_first(outs, nodes, pi[q], ps, k, rs),
+                                             rows_first(outs, nodes, pj[q], ps, k, rs)));
+    dist[pi[q] * kMaxM + pj[q]] = d;
+    dist[pj[q] * kMaxM + pi[q]] = d;
+  }
+  if (arow >= 0 && arow < m) {
+    s_arg[arow] = abi;
+    s_argv[arow] = abv;
   }
   __syncthreads();
   // exhaustive subset scan (distance.cpp:178-205), masks striped over threads
@@ -175,25 +249,6 @@ __global__ void __launch_bounds__(kQThreads) select_quorum_kernel(
     if (tid == 0) label[k] = -1;
     return;
   }
-  for (int i = warp; i < m; i += kQThreads / 32) {
-    if (!(best.mask >> i & 1)) continue;
-    const double* row = outs + nodes[i] * ps + k * rs;
-    double bv = -INFINITY;
-    uint32_t bi = 0xffffffffu;
-    for (uint32_t t = lane; t < v; t += 32) {
-      double x = __ldg(row + t);
-      if (bi == 0xffffffffu || bv < x) { bv = x; bi = t; }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-      uint32_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      bool take = (oi != 0xffffffffu) &&
-                  (bi == 0xffffffffu || bv < ov || (!(ov < bv) && oi < bi));
-      if (take) { bv = ov; bi = oi; }
-    }
-    if (lane == 0) { s_arg[i] = bi; s_argv[i] = bv; }
-  }
   __syncthreads();
   if (tid == 0) {
     int64_t win = -1;
@@ -231,7 +286,8 @@ void launch_select_quorum(const double* outs, uint64_t ps, uint64_t rs,
                           uint8_t* satisfied, int8_t* status, int64_t* label,
                           cudaStream_t st) {
   if (R == 0) return;
-  select_quorum_kernel<<<R, kQThreads, 0, st>>>(outs, ps, rs, present, eps, R,
+  const size_t smem = 2ull * kMaxM * (kQChunk + 1) * sizeof(double);
+  select_quorum_kernel<<<R, kQThreads, smem, st>>>(outs, ps, rs, present, eps, R,
                                                 n, f, v, metric, selected,
                                                 diameter, satisfied, status,
                                                 label);
@@ -278,6 +334,13 @@ __device__ __forceinline__ double ld_stream(const double* p) {
   asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
   return v;
 }
+// 256-bit load (sm_100): one whole 32-byte sector per lane, so a warp's 32
+// strided rows cost 32 L1 wavefronts per 1 KB instead of per 512 B.
+__device__ __forceinline__ void ld_stream4(const double* p, double& a, double& b, double& c,
+                                           double& d) {
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f64 {%0, %1, %2, %3}, [%4];"
+               : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
+}
 __device__ __forceinline__ double2 ld_stream2(const double* p) {
   double2 v;
   asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];"
@@ -288,7 +351,7 @@ __device__ __forceinline__ double2 ld_stream2(const double* p) {
 template <int M>
 __global__ void __launch_bounds__(128) agree_rows_kernel(
     const double* __restrict__ outs, uint64_t ps, uint64_t rs, const double* __restrict__ eps,
-    uint32_t R, uint32_t f, uint32_t v, int metric, int vec2,
+    uint32_t R, uint32_t f, uint32_t v, int metric, int vec,
     const uint8_t* __restrict__ req_ids, uint64_t version, uint32_t* __restrict__ selected,
     double* __restrict__ diameter, uint8_t* __restrict__ satisfied,
     int8_t* __restrict__ status, int64_t* __restrict__ label, uint8_t* __restrict__ digest) {
@@ -306,28 +369,24 @@ __global__ void __launch_bounds__(128) agree_rows_kernel(
     bi[i] = 0;
   }
   uint32_t t = 0;
-  if (vec2) {  // 4 lanes per trip: 2M independent 16-byte loads in flight
+  if (vec >= 2) {  // 4 lanes per trip: M 32-byte (or 2M 16-byte) loads in flight
 #pragma unroll 1
     for (; t + 4 <= v; t += 4) {
-      double2 q0[M], q1[M];
+      double q[4][M];
 #pragma unroll
       for (int i = 0; i < M; i++) {
-        q0[i] = ld_stream2(row + i * ps + t);
-        q1[i] = ld_stream2(row + i * ps + t + 2);
+        if (vec == 4) {
+          ld_stream4(row + i * ps + t, q[0][i], q[1][i], q[2][i], q[3][i]);
+        } else {
+          double2 a = ld_stream2(row + i * ps + t), b = ld_stream2(row + i * ps + t + 2);
+          q[0][i] = a.x;
+          q[1][i] = a.y;
+          q[2][i] = b.x;
+          q[3][i] = b.y;
+        }
       }
-      double x[M];
 #pragma unroll
-      for (int i = 0; i < M; i++) x[i] = q0[i].x;
-      agree_step<M>(x, t, metric, acc, bv, bi);
-#pragma unroll
-      for (int i = 0; i < M; i++) x[i] = q0[i].y;
-      agree_step<M>(x, t + 1, metric, acc, bv, bi);
-#pragma unroll
-      for (int i = 0; i < M; i++) x[i] = q1[i].x;
-      agree_step<M>(x, t + 2, metric, acc, bv, bi);
-#pragma unroll
-      for (int i = 0; i < M; i++) x[i] = q1[i].y;
-      agree_step<M>(x, t + 3, metric, acc, bv, bi);
+      for (int e = 0; e < 4; e++) agree_step<M>(q[e], t + e, metric, acc, bv, bi);
     }
   }
 #pragma unroll 1
@@ -346,9 +405,14 @@ __global__ void __launch_bounds__(128) agree_rows_kernel(
   const int need = M - (int)f;
   Cand best{0, 0, 0, 0.0};
   for (int s = M; s >= need && !best.valid; s--) {
+    // the size-s subsets in increasing order (Gosper's next combination)
 #pragma unroll 1
-    for (uint32_t mask = 1; mask < (1u << M); mask++) {
-      if (__popc(mask) != s) continue;
+    for (uint32_t mask = (1u << s) - 1; mask < (1u << M);) {
+      const uint32_t cur = mask;
+      {
+        const uint32_t c = mask & (0u - mask), r = mask + c;
+        mask = (((r ^ mask) >> 2) >> (__ffs(c) - 1)) | r;
+      }
       double dm = 0.0;
       bool ok = true;
       int p = 0;
@@ -356,12 +420,12 @@ __global__ void __launch_bounds__(128) agree_rows_kernel(
       for (int i = 0; i < M; i++)
 #pragma unroll
         for (int j = i + 1; j < M; j++, p++)
-          if (ok && (mask >> i & 1) && (mask >> j & 1)) {
+          if (ok && (cur >> i & 1) && (cur >> j & 1)) {
             dm = (dm < acc[p]) ? acc[p] : dm;
             if (dm > e) ok = false;
           }
       if (!ok) continue;
-      Cand c{1, (uint32_t)s, mask, dm};
+      Cand c{1, (uint32_t)s, cur, dm};
       if (cand_better(c, best)) best = c;
     }
   }
@@ -412,12 +476,15 @@ void launch_agree_rows(const double* outs, uint64_t ps, uint64_t rs, const doubl
                        double* diameter, uint8_t* satisfied, int8_t* status, int64_t* label,
                        uint8_t* digest, cudaStream_t st) {
   if (R == 0) return;
-  const int vec2 = ((ps | rs) % 2 == 0) && ((uintptr_t)outs % 16 == 0);
+  // widest row load every row start allows (32 B, 16 B, else scalar)
+  const int vec = ((ps | rs) % 4 == 0 && (uintptr_t)outs % 32 == 0)   ? 4
+                  : ((ps | rs) % 2 == 0 && (uintptr_t)outs % 16 == 0) ? 2
+                                                                      : 1;
   const unsigned grid = (unsigned)ceil_div(R, 128);
 #define CG_AGREE(MM)                                                                    \
   case MM:                                                                              \
     agree_rows_kernel<MM><<<grid, 128, 0, st>>>(outs, ps, rs, eps, R, f, v, (int)metric, \
-                                                vec2, req_ids, version, selected,       \
+                                                vec, req_ids, version, selected,       \
                                                 diameter, satisfied, status, label,     \
                                                 digest);                                \
     break;

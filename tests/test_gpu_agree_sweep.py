@@ -36,7 +36,8 @@ def _sweep(ctx, seed, R, n, f, v, metric, eps_choices, shift=0.1):
 
 
 @pytest.mark.parametrize("n,f,v,metric", [(8, 2, 1000, 0), (4, 1, 1000, 0), (8, 2, 10, 0),
-                                          (4, 1, 10, 2), (8, 3, 1000, 2), (3, 1, 10, 0)])
+                                          (4, 1, 10, 2), (8, 3, 1000, 2), (3, 1, 10, 0),
+                                          (4, 1, 7, 0)])
 def test_agree_device_bit_exact(ctx, oracle, n, f, v, metric):
     R = 6000  # above the throughput-form threshold (kAgreeRowsMinBatch = 4096)
     # generator eps 0.05: honest euclidean spread ~0.005, faulty ~0.15;
