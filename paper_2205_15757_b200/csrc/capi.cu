@@ -776,7 +776,7 @@ struct cg_group {
   DevBuf<int64_t> d_label;
   DevBuf<int32_t> d_single_pos;
   DevBuf<uint8_t> d_prep;  // shared CNN input operand
-  bool all_cnn = false;
+  bool all_cnn = false, same_prep = false;
   bool group_plan_ok = std::getenv("CREDO_NO_GROUP") == nullptr;  // false: per replica
   std::unique_ptr<CnnGroupPlan> gplan;   // grouped per-layer launches
   std::vector<std::unique_ptr<IngestSlot>> slots;
@@ -969,12 +969,12 @@ void certify(cg_group* g, uint64_t ticket, const double* precomputed_outputs) {
         chain_ctas += (int)ceil_div(o->B, kChainExclusiveThreads);
     set_gemm_sm_budget(kNumSMs - chain_ctas);
     const void* prepped = nullptr;
-    if (g->all_cnn) {  // replica-independent input stage, once per batch
+    if (g->same_prep) {  // replica-independent input stage, once per batch
       g->models[0]->cnn->prepare_input(S.d_in_ptr, B, g->d_prep.p, st);
       prepped = g->d_prep.p;
     }
     // Same-architecture CNN replicas: one grouped GEMM launch per layer.
-    if (!g->dist && g->all_cnn && g->group_plan_ok && (!g->gplan || g->gplan->batch() != B)) {
+    if (!g->dist && g->same_prep && g->group_plan_ok && (!g->gplan || g->gplan->batch() != B)) {
       std::vector<CnnModel*> ms;
       std::vector<float*> lg;
       for (uint32_t p = 0; p < N; p++) {
@@ -984,7 +984,7 @@ void certify(cg_group* g, uint64_t ticket, const double* precomputed_outputs) {
       g->gplan = CnnGroupPlan::build(ms, B, g->d_prep.p, lg);
       g->group_plan_ok = g->gplan != nullptr;
     }
-    const bool grouped = !g->dist && g->all_cnn && g->gplan && g->gplan->batch() == B;
+    const bool grouped = !g->dist && g->same_prep && g->gplan && g->gplan->batch() == B;
     if (grouped) {
       g->gplan->run(st);
       bool same_sm = true;
@@ -1160,7 +1160,12 @@ int create_group(cg_ctx* ctx, cg_model* const* models, uint32_t nlocal, uint32_t
       if (m->kind == 1) m->cnn->reserve(max_batch);
       g->all_cnn = g->all_cnn && m->kind == 1;
     }
-    if (g->all_cnn) g->d_prep.ensure(g->models[0]->cnn->prepared_bytes(max_batch));
+    // one shared input stage when every replica consumes the same operand
+    // (heterogeneous groups: each replica prepares its own)
+    g->same_prep = g->all_cnn;
+    for (auto* m : g->models)
+      g->same_prep = g->same_prep && m->cnn->prep_kind() == g->models[0]->cnn->prep_kind();
+    if (g->same_prep) g->d_prep.ensure(g->models[0]->cnn->prepared_bytes(max_batch));
     // ingest ring: enough batches in flight to hide the request-midstate
     // chains (latency ~ request bytes / 64 compressions, ~30 ms for a C2
     // request) behind the forwards of the batches certified meanwhile

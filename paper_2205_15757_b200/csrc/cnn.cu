@@ -382,6 +382,7 @@ class ResNet final : public CnnModel {
   size_t prepared_bytes(uint32_t B) const override {
     return (size_t)B * (S_ / 2) * (S_ / 2) * 192 * 2;
   }
+  std::string prep_kind() const override { return "im2col7x7s2k192/" + std::to_string(S_); }
 
   void prepare_input(const double* d_in, uint32_t B, void* prepped, cudaStream_t st) override {
     const int H1 = S_ / 2, Sp = S_ + 6;
@@ -688,6 +689,619 @@ class ResNet final : public CnnModel {
   std::map<uint32_t, Plan> plans_;
 };
 
+// ------------------------------------------------ VGG-16 and MobileNetV2
+// The heterogeneous-group architectures (BASELINE configs[2]), on the same
+// tcgen05 conv GEMM. Channel counts are padded to multiples of 64 with zero
+// weights (zero bias), so padded channels carry exact zeros end to end.
+
+// 3x3 im2col straight from the f64 CHW request input: [B*Ho*Ho, 64] bf16,
+// K = (dr*3 + ds)*3 + c for the 27 real taps, zero beyond (pad 1).
+__global__ void im2col3x3_f64_kernel(const double* __restrict__ in, int B, int S, int stride,
+                                     int Ho, bf16* __restrict__ out) {
+  const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t row = t >> 3;
+  const int chunk = (int)(t & 7);
+  if (row >= (size_t)B * Ho * Ho) return;
+  const int n = (int)(row / ((size_t)Ho * Ho)), rem = (int)(row - (size_t)n * Ho * Ho);
+  const int ho = rem / Ho, wo = rem - ho * Ho;
+  __align__(16) bf16 o[8];
+#pragma unroll
+  for (int j = 0; j < 8; j++) {
+    const int k = chunk * 8 + j;
+    double x = 0.0;
+    if (k < 27) {
+      const int tap = k / 3, c = k - tap * 3, dr = tap / 3, ds = tap - dr * 3;
+      const int h = ho * stride - 1 + dr, w = wo * stride - 1 + ds;
+      if (h >= 0 && h < S && w >= 0 && w < S) x = __ldg(in + (((size_t)n * 3 + c) * S + h) * S + w);
+    }
+    o[j] = __double2bfloat16(x);
+  }
+  *reinterpret_cast<uint4*>(out + row * 64 + chunk * 8) = *reinterpret_cast<uint4*>(o);
+}
+
+// 2x2/2 max pool, compact NHWC in; out compact, or the interior of a
+// zero-bordered (H/2+2)^2 grid when padded_out.
+__global__ void maxpool2x2_kernel(const bf16* __restrict__ in, int B, int H, int C,
+                                  int padded_out, bf16* __restrict__ out) {
+  const int Ho = H / 2, chunks = C / 8;
+  const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t pix = t / chunks;
+  const int ch = (int)(t - pix * chunks);
+  if (pix >= (size_t)B * Ho * Ho) return;
+  const int n = (int)(pix / (Ho * Ho)), rem = (int)(pix - (size_t)n * Ho * Ho);
+  const int ho = rem / Ho, wo = rem - ho * Ho;
+  float m[8];
+#pragma unroll
+  for (int j = 0; j < 8; j++) m[j] = -INFINITY;
+#pragma unroll
+  for (int d = 0; d < 4; d++) {
+    const int h = 2 * ho + (d >> 1), w = 2 * wo + (d & 1);
+    const uint4 q =
+        __ldg(reinterpret_cast<const uint4*>(in + (((size_t)n * H + h) * H + w) * C + ch * 8));
+    const bf16* e = reinterpret_cast<const bf16*>(&q);
+#pragma unroll
+    for (int j = 0; j < 8; j++) m[j] = fmaxf(m[j], __bfloat162float(e[j]));
+  }
+  __align__(16) bf16 o[8];
+#pragma unroll
+  for (int j = 0; j < 8; j++) o[j] = __float2bfloat16(m[j]);
+  const size_t orow = padded_out ? ((size_t)n * (Ho + 2) + ho + 1) * (Ho + 2) + wo + 1 : pix;
+  *reinterpret_cast<uint4*>(out + orow * C + ch * 8) = *reinterpret_cast<uint4*>(o);
+}
+
+// Depthwise 3x3 (pad 1, stride 1/2) + folded-BN bias + ReLU6, NHWC bf16,
+// f32 weights [9][C] tap-major; thread = (output pixel, 8 channels).
+__global__ void dw3x3_kernel(const bf16* __restrict__ in, int B, int H, int C, int stride,
+                             const float* __restrict__ w, const float* __restrict__ bias,
+                             bf16* __restrict__ out) {
+  const int Ho = (H - 1) / stride + 1, chunks = C / 8;
+  const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t pix = t / chunks;
+  const int ch = (int)(t - pix * chunks);
+  if (pix >= (size_t)B * Ho * Ho) return;
+  const int n = (int)(pix / (Ho * Ho)), rem = (int)(pix - (size_t)n * Ho * Ho);
+  const int ho = rem / Ho, wo = rem - ho * Ho;
+  const int c0 = ch * 8;
+  float acc[8];
+  {
+    const float4 b0 = __ldg(reinterpret_cast<const float4*>(bias + c0));
+    const float4 b1 = __ldg(reinterpret_cast<const float4*>(bias + c0 + 4));
+    acc[0] = b0.x; acc[1] = b0.y; acc[2] = b0.z; acc[3] = b0.w;
+    acc[4] = b1.x; acc[5] = b1.y; acc[6] = b1.z; acc[7] = b1.w;
+  }
+#pragma unroll
+  for (int tap = 0; tap < 9; tap++) {
+    const int h = ho * stride - 1 + tap / 3, x = wo * stride - 1 + tap % 3;
+    if (h < 0 || h >= H || x < 0 || x >= H) continue;
+    const uint4 q =
+        __ldg(reinterpret_cast<const uint4*>(in + (((size_t)n * H + h) * H + x) * C + c0));
+    const bf16* e = reinterpret_cast<const bf16*>(&q);
+    const float4 w0 = __ldg(reinterpret_cast<const float4*>(w + tap * C + c0));
+    const float4 w1 = __ldg(reinterpret_cast<const float4*>(w + tap * C + c0 + 4));
+    const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+    for (int j = 0; j < 8; j++) acc[j] = fmaf(__bfloat162float(e[j]), wv[j], acc[j]);
+  }
+  __align__(16) bf16 o[8];
+#pragma unroll
+  for (int j = 0; j < 8; j++) o[j] = __float2bfloat16(fminf(fmaxf(acc[j], 0.f), 6.f));
+  *reinterpret_cast<uint4*>(out + pix * C + c0) = *reinterpret_cast<uint4*>(o);
+}
+
+int pad64(int c) { return (c + 63) / 64 * 64; }
+
+HostTensor& tensor(std::map<std::string, HostTensor>& T, const std::string& name,
+                   std::vector<int64_t> dims) {
+  auto it = T.find(name);
+  if (it == T.end()) throw std::invalid_argument("cnn file: missing tensor " + name);
+  if (!dims.empty() && it->second.dims != dims)
+    throw std::invalid_argument("cnn file: bad shape for " + name);
+  return it->second;
+}
+
+// Per-output-channel scale/shift of an eval BatchNorm (eps 1e-5), or the
+// conv/linear bias (bn empty), or zero.
+void affine(std::map<std::string, HostTensor>& T, const std::string& bn, const std::string& bias,
+            int cout, std::vector<double>& scale, std::vector<double>& shift) {
+  scale.assign(cout, 1.0);
+  shift.assign(cout, 0.0);
+  if (!bn.empty()) {
+    const int64_t co = cout;
+    auto& g = tensor(T, bn + ".weight", {co});
+    auto& be = tensor(T, bn + ".bias", {co});
+    auto& mu = tensor(T, bn + ".running_mean", {co});
+    auto& var = tensor(T, bn + ".running_var", {co});
+    for (int o = 0; o < cout; o++) {
+      scale[o] = (double)g.v[o] / std::sqrt((double)var.v[o] + 1e-5);
+      shift[o] = (double)be.v[o] - (double)mu.v[o] * scale[o];
+    }
+  } else if (!bias.empty()) {
+    auto& b = tensor(T, bias, {(int64_t)cout});
+    for (int o = 0; o < cout; o++) shift[o] = b.v[o];
+  }
+}
+
+// A conv (k x k) or linear layer (k == 0) as GEMM weights [cout_p][K]:
+//   Kim2col > 0 : one tap, K = Kim2col, column (dr*k+ds)*cin + c
+//   k == 3      : 9 taps over a padded grid, column tap*cin_p + c
+//   k == 1 / 0  : one tap, column c (hwc: linear input in (h, w, c) order
+//                 from torch's (c, h, w) flatten, hwc = {C, H, W})
+void load_gemm_layer(ConvW& c, std::map<std::string, HostTensor>& T, const std::string& wname,
+                     const std::string& bn, const std::string& bias, int k, int stride,
+                     int Kim2col, const int* hwc = nullptr, bool pad_out = true) {
+  auto it = T.find(wname);
+  if (it == T.end()) throw std::invalid_argument("cnn file: missing tensor " + wname);
+  const HostTensor& W = it->second;
+  const int kk = k == 0 ? 1 : k;
+  if ((k == 0 && W.dims.size() != 2) ||
+      (k > 0 && (W.dims.size() != 4 || W.dims[2] != k || W.dims[3] != k)))
+    throw std::invalid_argument("cnn file: bad layer shape " + wname);
+  c.cout = (int)W.dims[0];
+  c.cin = (int)W.dims[1];
+  c.k = kk;
+  c.stride = stride;
+  const int cout_p = pad_out ? pad64(c.cout) : c.cout, cin_p = pad64(c.cin);
+  c.ntaps = (k == 3 && !Kim2col) ? 9 : 1;
+  c.Kc = Kim2col ? Kim2col : cin_p;
+  const int Ktot = c.Kc * c.ntaps;
+  std::vector<double> sc, sh;
+  affine(T, bn, bias, c.cout, sc, sh);
+  c.hw.assign((size_t)cout_p * Ktot, 0);
+  c.hb.assign(cout_p, 0.f);
+  for (int o = 0; o < c.cout; o++) {
+    c.hb[o] = (float)sh[o];
+    for (int ci = 0; ci < c.cin; ci++)
+      for (int dr = 0; dr < kk; dr++)
+        for (int ds = 0; ds < kk; ds++) {
+          const float w = W.v[(((size_t)o * c.cin + ci) * kk + dr) * kk + ds];
+          size_t col;
+          if (Kim2col) col = (size_t)(dr * kk + ds) * c.cin + ci;
+          else if (c.ntaps == 9) col = (size_t)(dr * 3 + ds) * cin_p + ci;
+          else if (hwc) {  // torch flatten index ci = (ch * H + h) * W + w
+            const int C = hwc[0], H = hwc[1], Wd = hwc[2];
+            const int ch = ci / (H * Wd), r = ci - ch * H * Wd, h = r / Wd, x = r - h * Wd;
+            col = ((size_t)h * Wd + x) * C + ch;
+          } else col = ci;
+          c.hw[(size_t)o * Ktot + col] = f2bf_bits((float)(w * sc[o]));
+        }
+  }
+  c.cout = cout_p;  // the GEMM's N (padded)
+}
+
+struct DwW {
+  int C = 0, stride = 1;  // C padded
+  std::vector<float> hw, hb;
+  float *w = nullptr, *b = nullptr;
+};
+
+void load_dw(DwW& d, std::map<std::string, HostTensor>& T, const std::string& wname,
+             const std::string& bn, int stride) {
+  auto& W = tensor(T, wname, {});
+  if (W.dims.size() != 4 || W.dims[1] != 1 || W.dims[2] != 3 || W.dims[3] != 3)
+    throw std::invalid_argument("cnn file: bad depthwise shape " + wname);
+  const int C = (int)W.dims[0];
+  d.C = pad64(C);
+  d.stride = stride;
+  std::vector<double> sc, sh;
+  affine(T, bn, "", C, sc, sh);
+  d.hw.assign((size_t)9 * d.C, 0.f);
+  d.hb.assign(d.C, 0.f);
+  for (int c = 0; c < C; c++) {
+    d.hb[c] = (float)sh[c];
+    for (int tap = 0; tap < 9; tap++) d.hw[(size_t)tap * d.C + c] = (float)(W.v[c * 9 + tap] * sc[c]);
+  }
+}
+
+// Shared plumbing of the sequential nets: device buffers, the cached launch
+// plan per (batch, input, logits), upload of GEMM and depthwise weights.
+class SeqNet : public CnnModel {
+ public:
+  SeqNet(std::string arch, uint64_t in_dim, uint64_t out_dim, bool sm)
+      : arch_(std::move(arch)), in_dim_(in_dim), out_dim_(out_dim), softmax_(sm) {
+    S_ = (int)std::lround(std::sqrt((double)in_dim / 3.0));
+    if ((uint64_t)3 * S_ * S_ != in_dim || S_ % 32 != 0)
+      throw std::invalid_argument("cnn file: input_dim must be 3*S*S with S % 32 == 0");
+  }
+  ~SeqNet() override {
+    for (ConvW* c : gemms_) {
+      if (c->w) cudaFree(c->w);
+      if (c->b) cudaFree(c->b);
+    }
+    for (DwW* d : dws_) {
+      if (d->w) cudaFree(d->w);
+      if (d->b) cudaFree(d->b);
+    }
+    for (void* p : bufs_) cudaFree(p);
+  }
+  void upload(cudaStream_t st) override {
+    for (ConvW* c : gemms_) {
+      CG_CUDA(cudaMalloc(&c->w, c->hw.size() * 2));
+      CG_CUDA(cudaMalloc(&c->b, c->hb.size() * 4));
+      CG_CUDA(cudaMemcpyAsync(c->w, c->hw.data(), c->hw.size() * 2, cudaMemcpyHostToDevice, st));
+      CG_CUDA(cudaMemcpyAsync(c->b, c->hb.data(), c->hb.size() * 4, cudaMemcpyHostToDevice, st));
+    }
+    for (DwW* d : dws_) {
+      CG_CUDA(cudaMalloc(&d->w, d->hw.size() * 4));
+      CG_CUDA(cudaMalloc(&d->b, d->hb.size() * 4));
+      CG_CUDA(cudaMemcpyAsync(d->w, d->hw.data(), d->hw.size() * 4, cudaMemcpyHostToDevice, st));
+      CG_CUDA(cudaMemcpyAsync(d->b, d->hb.data(), d->hb.size() * 4, cudaMemcpyHostToDevice, st));
+    }
+    CG_CUDA(cudaStreamSynchronize(st));
+    for (ConvW* c : gemms_) std::vector<uint16_t>().swap(c->hw);
+  }
+  void reserve(uint32_t maxB) override {
+    if (maxB <= maxB_) return;
+    for (void* p : bufs_) cudaFree(p);
+    bufs_.clear();
+    plans_.clear();
+    maxB_ = maxB;
+    alloc_buffers(maxB);
+  }
+  size_t prepared_bytes(uint32_t B) const override { return (size_t)B * rows0_ * 64 * 2; }
+  std::string prep_kind() const override {
+    return "im2col3x3s" + std::to_string(stride0_) + "k64/" + std::to_string(S_);
+  }
+  void prepare_input(const double* d_in, uint32_t B, void* prepped, cudaStream_t st) override {
+    if (B > maxB_) reserve(B);
+    timer_begin(st, kTimeAux);
+    const int Ho = S_ / stride0_;
+    im2col3x3_f64_kernel<<<grid_for((size_t)B * Ho * Ho * 8), 256, 0, st>>>(
+        d_in, (int)B, S_, stride0_, Ho, reinterpret_cast<bf16*>(prepped));
+    CG_CHECK_LAUNCH();
+    timer_end(st, kTimeAux);
+  }
+  void forward(const double* d_in, uint32_t B, float* logits, cudaStream_t st,
+               const void* prepped) override {
+    if (B > maxB_) reserve(B);
+    const void* x0 = prepped;
+    if (!x0) {
+      prepare_input(d_in, B, xcol_, st);
+      x0 = xcol_;
+    }
+    auto it = plans_.find(B);
+    if (it == plans_.end() || it->second.x0 != x0 || it->second.logits != logits) {
+      Plan& p = plans_[B];
+      p = Plan{};
+      p.x0 = x0;
+      p.logits = logits;
+      for (ResNet::Op& o : ops(B, reinterpret_cast<const bf16*>(x0), logits)) {
+        if (o.gemm) p.steps.push_back(ResNet::make_gemm_step({&o.g}));
+        else p.steps.push_back(std::move(o.aux));
+      }
+      it = plans_.find(B);
+    }
+    for (auto& s : it->second.steps) s(st);
+  }
+  uint64_t input_dim() const override { return in_dim_; }
+  uint64_t output_dim() const override { return out_dim_; }
+  bool softmax() const override { return softmax_; }
+  std::string arch() const override { return arch_; }
+  double flops_per_image() const override { return flops_; }
+
+ protected:
+  struct Plan {
+    const void* x0 = nullptr;
+    float* logits = nullptr;
+    std::vector<std::function<void(cudaStream_t)>> steps;
+  };
+  virtual void alloc_buffers(uint32_t B) = 0;
+  virtual std::vector<ResNet::Op> ops(uint32_t B, const bf16* x0, float* logits) = 0;
+
+  bf16* alloc(size_t elems) {
+    void* p = nullptr;
+    CG_CUDA(cudaMalloc(&p, std::max<size_t>(elems, 8) * 2));
+    CG_CUDA(cudaMemset(p, 0, std::max<size_t>(elems, 8) * 2));
+    bufs_.push_back(p);
+    return reinterpret_cast<bf16*>(p);
+  }
+  static void push_gemm(std::vector<ResNet::Op>& L, ConvW& c, const bf16* A, int rowsA, int M,
+                        const int* taps, const bf16* res, int ldres, void* out, int ldout,
+                        int out_f32, int act, int mode, int H, int rows_out) {
+    ResNet::Op o;
+    o.gemm = true;
+    ResNet::GemmDesc& g = o.g;
+    g.c = &c;
+    g.A = A;
+    g.rowsA = rowsA;
+    g.M = M;
+    g.Kc = c.Kc;
+    g.ntaps = c.ntaps;
+    for (int t = 0; t < c.ntaps; t++) g.taps[t] = taps ? taps[t] : 0;
+    g.res = res;
+    g.ldres = ldres;
+    g.out = out;
+    g.ldout = ldout;
+    g.out_f32 = out_f32;
+    g.relu = act;
+    g.mode = mode;
+    g.H = H;
+    g.rows_out = rows_out;
+    L.push_back(std::move(o));
+  }
+  static void push_aux(std::vector<ResNet::Op>& L, std::function<void(cudaStream_t)> f) {
+    ResNet::Op o;
+    o.aux = [f](cudaStream_t st) {
+      timer_begin(st, kTimeAux);
+      f(st);
+      timer_end(st, kTimeAux);
+    };
+    L.push_back(std::move(o));
+  }
+
+  std::string arch_;
+  uint64_t in_dim_, out_dim_;
+  bool softmax_;
+  int S_ = 224, stride0_ = 1;
+  size_t rows0_ = 0;  // conv0 output pixels per image
+  double flops_ = 0;
+  std::vector<ConvW*> gemms_;
+  std::vector<DwW*> dws_;
+  uint32_t maxB_ = 0;
+  std::vector<void*> bufs_;
+  bf16* xcol_ = nullptr;
+  std::map<uint32_t, Plan> plans_;
+};
+
+// torchvision vgg16 (no BN): 13 3x3 convs (ReLU) in 5 stages with 2x2 max
+// pools, then 3 linear layers. conv0 from an im2col of the input; every
+// other 3x3 conv runs 9 row-shifted taps over a zero-bordered grid written
+// in place by its producer (PadToPad) or by the pool kernel.
+class Vgg16 final : public SeqNet {
+ public:
+  Vgg16(uint64_t in_dim, uint64_t out_dim, bool sm, std::map<std::string, HostTensor>& T)
+      : SeqNet("vgg16", in_dim, out_dim, sm) {
+    const int cfg[] = {64, 64, 0, 128, 128, 0, 256, 256, 256, 0, 512, 512, 512, 0,
+                       512, 512, 512, 0};
+    int idx = 0, H = S_, cin = 3;
+    for (int v : cfg) {
+      if (v == 0) {
+        pool_after_.back() = true;
+        H /= 2;
+        idx += 1;
+        continue;
+      }
+      convs_.emplace_back();
+      ConvW& c = convs_.back();
+      const std::string pre = "features." + std::to_string(idx);
+      load_gemm_layer(c, T, pre + ".weight", "", pre + ".bias", 3, 1, convs_.size() == 1 ? 64 : 0);
+      if (c.cin != cin) throw std::invalid_argument("cnn file: unexpected vgg16 shapes");
+      flops_ += 2.0 * H * H * 9.0 * cin * v;
+      Hs_.push_back(H);
+      pool_after_.push_back(false);
+      cin = v;
+      idx += 2;
+    }
+    H_last_ = H;
+    const int hwc[3] = {cin, H, H};
+    const int fc_in = cin * H * H;
+    load_gemm_layer(fc_[0], T, "classifier.0.weight", "", "classifier.0.bias", 0, 1, 0, hwc);
+    load_gemm_layer(fc_[1], T, "classifier.3.weight", "", "classifier.3.bias", 0, 1, 0);
+    load_gemm_layer(fc_[2], T, "classifier.6.weight", "", "classifier.6.bias", 0, 1, 0, nullptr,
+                    false);
+    if (fc_[0].cin != fc_in || fc_[2].cout != (int)out_dim)
+      throw std::invalid_argument("cnn file: unexpected vgg16 classifier shapes");
+    flops_ += 2.0 * ((double)fc_in * 4096 + 4096.0 * 4096 + 4096.0 * out_dim);
+    for (auto& c : convs_) gemms_.push_back(&c);
+    for (auto& c : fc_) gemms_.push_back(&c);
+    stride0_ = 1;
+    rows0_ = (size_t)S_ * S_;
+  }
+
+ protected:
+  void alloc_buffers(uint32_t B) override {
+    xcol_ = alloc((size_t)B * rows0_ * 64);
+    pads_.assign(convs_.size(), nullptr);
+    compact_.assign(convs_.size(), nullptr);
+    for (size_t i = 0; i < convs_.size(); i++) {
+      const size_t H = Hs_[i], C = convs_[i].cout, Hp = H + 2;
+      // output grid of conv i: padded (consumed by conv i+1) or compact (pool)
+      if (pool_after_[i]) compact_[i] = alloc((size_t)B * H * H * C);
+      else pads_[i] = alloc((size_t)B * Hp * Hp * C);
+    }
+    // pool outputs feed the next conv's padded grid (or the classifier)
+    pool_out_.assign(convs_.size(), nullptr);
+    for (size_t i = 0; i < convs_.size(); i++)
+      if (pool_after_[i]) {
+        const size_t Ho = Hs_[i] / 2, C = convs_[i].cout;
+        pool_out_[i] = alloc(i + 1 < convs_.size() ? (size_t)B * (Ho + 2) * (Ho + 2) * C
+                                                   : (size_t)B * Ho * Ho * C);
+      }
+    fcbuf_[0] = alloc((size_t)B * 4096);
+    fcbuf_[1] = alloc((size_t)B * 4096);
+  }
+  std::vector<ResNet::Op> ops(uint32_t B, const bf16* x0, float* logits) override {
+    std::vector<ResNet::Op> L;
+    const int b = (int)B;
+    const bf16* in = x0;  // conv0: im2col rows; later: a padded grid
+    for (size_t i = 0; i < convs_.size(); i++) {
+      ConvW& c = convs_[i];
+      const int H = Hs_[i], Hp = H + 2, rows_pad = b * Hp * Hp;
+      void* out = pool_after_[i] ? (void*)compact_[i] : (void*)pads_[i];
+      if (i == 0) {
+        push_gemm(L, c, in, b * H * H, b * H * H, nullptr, nullptr, 0, out, c.cout, 0, 1,
+                  pool_after_[i] ? kRowIdentity : kRowCompactToPad, H, b * H * H);
+      } else {
+        int taps[9];
+        for (int dr = 0; dr < 3; dr++)
+          for (int ds = 0; ds < 3; ds++) taps[dr * 3 + ds] = (dr - 1) * Hp + (ds - 1);
+        push_gemm(L, c, in, rows_pad, rows_pad, taps, nullptr, 0, out, c.cout, 0, 1,
+                  pool_after_[i] ? kRowPadToCompact : kRowPadToPad, H, b * H * H);
+      }
+      if (pool_after_[i]) {
+        const bf16* src = compact_[i];
+        bf16* dst = pool_out_[i];
+        const int C = c.cout, padded = i + 1 < convs_.size();
+        push_aux(L, [src, dst, b, H, C, padded](cudaStream_t st) {
+          size_t th = (size_t)b * (H / 2) * (H / 2) * (C / 8);
+          maxpool2x2_kernel<<<grid_for(th), 256, 0, st>>>(src, b, H, C, padded, dst);
+          CG_CHECK_LAUNCH();
+        });
+        in = dst;
+      } else {
+        in = pads_[i];
+      }
+    }
+    // classifier: (h, w, c) flatten matches the permuted fc0 columns
+    push_gemm(L, fc_[0], in, b, b, nullptr, nullptr, 0, fcbuf_[0], 4096, 0, 1, kRowIdentity, 0, b);
+    push_gemm(L, fc_[1], fcbuf_[0], b, b, nullptr, nullptr, 0, fcbuf_[1], 4096, 0, 1,
+              kRowIdentity, 0, b);
+    push_gemm(L, fc_[2], fcbuf_[1], b, b, nullptr, nullptr, 0, logits, (int)out_dim_, 1, 0,
+              kRowIdentity, 0, b);
+    return L;
+  }
+
+ private:
+  std::vector<ConvW> convs_;
+  std::vector<int> Hs_;
+  std::vector<bool> pool_after_;
+  ConvW fc_[3];
+  int H_last_ = 7;
+  std::vector<bf16*> pads_, compact_, pool_out_;
+  bf16* fcbuf_[2] = {nullptr, nullptr};
+};
+
+// torchvision mobilenet_v2: conv0 3x3/2 (ReLU6), 17 inverted residual
+// blocks (1x1 expand ReLU6 -> depthwise 3x3 ReLU6 -> 1x1 linear project,
+// + identity when stride 1 and cin == cout), 1x1 to 1280 (ReLU6), global
+// average pool, linear. Expand/project/head are GEMMs (residual fused into
+// the project epilogue); the depthwise conv is a CUDA-core NHWC kernel.
+class MobileNetV2 final : public SeqNet {
+ public:
+  MobileNetV2(uint64_t in_dim, uint64_t out_dim, bool sm, std::map<std::string, HostTensor>& T)
+      : SeqNet("mobilenet_v2", in_dim, out_dim, sm) {
+    stride0_ = 2;
+    int H = S_ / 2;
+    rows0_ = (size_t)H * H;
+    load_gemm_layer(conv0_, T, "features.0.0.weight", "features.0.1", "", 3, 2, 64);
+    flops_ += 2.0 * H * H * 27 * 32;
+    const int setting[7][4] = {{1, 16, 1, 1}, {6, 24, 2, 2}, {6, 32, 3, 2}, {6, 64, 4, 2},
+                               {6, 96, 3, 1}, {6, 160, 3, 2}, {6, 320, 1, 1}};
+    int cin = 32, f = 1;
+    blocks_.reserve(17);
+    for (auto& s : setting)
+      for (int i = 0; i < s[2]; i++, f++) {
+        blocks_.emplace_back();
+        Blk& b = blocks_.back();
+        const int stride = i == 0 ? s[3] : 1, hidden = cin * s[0];
+        const std::string pre = "features." + std::to_string(f) + ".conv.";
+        b.expand = s[0] != 1;
+        int k = 0;
+        if (b.expand) {
+          load_gemm_layer(b.pw1, T, pre + "0.0.weight", pre + "0.1", "", 1, 1, 0);
+          flops_ += 2.0 * H * H * cin * hidden;
+          k = 1;
+        }
+        load_dw(b.dw, T, pre + std::to_string(k) + ".0.weight", pre + std::to_string(k) + ".1",
+                stride);
+        const int Ho = (H - 1) / stride + 1;
+        flops_ += 2.0 * Ho * Ho * 9 * hidden;
+        load_gemm_layer(b.pw2, T, pre + std::to_string(k + 1) + ".weight",
+                        pre + std::to_string(k + 2), "", 1, 1, 0);
+        flops_ += 2.0 * Ho * Ho * hidden * s[1];
+        b.H = H;
+        b.Ho = Ho;
+        b.cin = pad64(cin);
+        b.hidden = pad64(hidden);
+        b.cout = pad64(s[1]);
+        b.residual = stride == 1 && cin == s[1];
+        if (b.dw.C != b.hidden || b.pw2.cout != b.cout)
+          throw std::invalid_argument("cnn file: unexpected mobilenet_v2 shapes at " + pre);
+        cin = s[1];
+        H = Ho;
+      }
+    load_gemm_layer(head_, T, "features.18.0.weight", "features.18.1", "", 1, 1, 0);
+    flops_ += 2.0 * H * H * cin * 1280;
+    load_gemm_layer(fc_, T, "classifier.1.weight", "", "classifier.1.bias", 0, 1, 0, nullptr,
+                    false);
+    if (fc_.cout != (int)out_dim) throw std::invalid_argument("cnn file: bad classifier");
+    flops_ += 2.0 * 1280.0 * out_dim;
+    H_last_ = H;
+    gemms_.push_back(&conv0_);
+    for (auto& b : blocks_) {
+      if (b.expand) gemms_.push_back(&b.pw1);
+      gemms_.push_back(&b.pw2);
+      dws_.push_back(&b.dw);
+    }
+    gemms_.push_back(&head_);
+    gemms_.push_back(&fc_);
+  }
+
+ protected:
+  void alloc_buffers(uint32_t B) override {
+    xcol_ = alloc((size_t)B * rows0_ * 64);
+    size_t act = (size_t)B * rows0_ * conv0_.cout, hid = 0;
+    for (auto& b : blocks_) {
+      act = std::max(act, (size_t)B * b.Ho * b.Ho * b.cout);
+      hid = std::max(hid, (size_t)B * b.H * b.H * b.hidden);
+    }
+    act_[0] = alloc(act);
+    act_[1] = alloc(act);
+    e_ = alloc(hid);
+    d_ = alloc(hid);
+    head_out_ = alloc((size_t)B * H_last_ * H_last_ * 1280);
+    pooled_ = alloc((size_t)B * 1280);
+  }
+  std::vector<ResNet::Op> ops(uint32_t B, const bf16* x0, float* logits) override {
+    std::vector<ResNet::Op> L;
+    const int b = (int)B;
+    const int H0 = S_ / 2;
+    push_gemm(L, conv0_, x0, b * H0 * H0, b * H0 * H0, nullptr, nullptr, 0, act_[0],
+              conv0_.cout, 0, 2, kRowIdentity, 0, b * H0 * H0);
+    int cur = 0;
+    for (auto& k : blocks_) {
+      bf16* X = act_[cur];
+      bf16* Y = act_[cur ^ 1];
+      const bf16* dwin = X;
+      if (k.expand) {
+        push_gemm(L, k.pw1, X, b * k.H * k.H, b * k.H * k.H, nullptr, nullptr, 0, e_, k.hidden,
+                  0, 2, kRowIdentity, 0, b * k.H * k.H);
+        dwin = e_;
+      }
+      {
+        const DwW* dw = &k.dw;
+        bf16* D = d_;
+        const int H = k.H, C = k.hidden, s = k.dw.stride, Ho = k.Ho;
+        push_aux(L, [dwin, dw, D, b, H, C, s, Ho](cudaStream_t st) {
+          size_t th = (size_t)b * Ho * Ho * (C / 8);
+          dw3x3_kernel<<<grid_for(th), 256, 0, st>>>(dwin, b, H, C, s, dw->w, dw->b, D);
+          CG_CHECK_LAUNCH();
+        });
+      }
+      push_gemm(L, k.pw2, d_, b * k.Ho * k.Ho, b * k.Ho * k.Ho, nullptr,
+                k.residual ? X : nullptr, k.residual ? k.cout : 0, Y, k.cout, 0, 0,
+                kRowIdentity, 0, b * k.Ho * k.Ho);
+      cur ^= 1;
+    }
+    const int HW = H_last_ * H_last_;
+    push_gemm(L, head_, act_[cur], b * HW, b * HW, nullptr, nullptr, 0, head_out_, 1280, 0, 2,
+              kRowIdentity, 0, b * HW);
+    {
+      bf16* in = head_out_;
+      bf16* out = pooled_;
+      push_aux(L, [in, out, b, HW](cudaStream_t st) {
+        avgpool_kernel<<<grid_for((size_t)b * 1280 / 8), 256, 0, st>>>(in, b, HW, 1280, out);
+        CG_CHECK_LAUNCH();
+      });
+    }
+    push_gemm(L, fc_, pooled_, b, b, nullptr, nullptr, 0, logits, (int)out_dim_, 1, 0,
+              kRowIdentity, 0, b);
+    return L;
+  }
+
+ private:
+  struct Blk {
+    ConvW pw1, pw2;
+    DwW dw;
+    bool expand = false, residual = false;
+    int H = 0, Ho = 0, cin = 0, hidden = 0, cout = 0;
+  };
+  ConvW conv0_, head_, fc_;
+  std::vector<Blk> blocks_;
+  int H_last_ = 7;
+  bf16 *act_[2] = {nullptr, nullptr}, *e_ = nullptr, *d_ = nullptr, *head_out_ = nullptr,
+       *pooled_ = nullptr;
+};
+
 class ResNetGroupPlan final : public CnnGroupPlan {
  public:
   uint32_t B = 0;
@@ -772,6 +1386,9 @@ std::unique_ptr<CnnModel> CnnModel::from_file(const uint8_t* file, uint64_t len)
   if (arch == "resnet50") layers = {3, 4, 6, 3};
   else if (arch == "resnet101") layers = {3, 4, 23, 3};
   else if (arch == "resnet152") layers = {3, 8, 36, 3};
+  else if (arch == "vgg16") return std::make_unique<Vgg16>(in_dim, out_dim, sm == 1, T);
+  else if (arch == "mobilenet_v2")
+    return std::make_unique<MobileNetV2>(in_dim, out_dim, sm == 1, T);
   else throw std::invalid_argument("cnn file: unsupported arch " + arch);
   return std::make_unique<ResNet>(arch, layers, in_dim, out_dim, sm == 1, T);
 }

@@ -1,4 +1,5 @@
-// ImageNet-class replica executor (ResNet-50/101/152, bottleneck v1.5)
+// ImageNet-class replica executors (ResNet-50/101/152 bottleneck v1.5,
+// VGG-16, MobileNetV2)
 // behind the ModelExecutor seam (reference proj/include/credo/model.hpp:
 // 41-51). The reference has no CNN path (its SPEC.md:8 replaces it with
 // LinearToyModel); the CPU restatement used as parity oracle is torchvision's
@@ -26,6 +27,8 @@ class CnnModel {
   virtual void prepare_input(const double* d_in, uint32_t B, void* prepped,
                              cudaStream_t st) = 0;
   virtual size_t prepared_bytes(uint32_t B) const = 0;
+  // Models with equal prep_kind() can share one prepared input.
+  virtual std::string prep_kind() const = 0;
   // logits: B × output_dim f32. prepped == nullptr -> prepares internally.
   virtual void forward(const double* d_in, uint32_t B, float* logits,
                        cudaStream_t st, const void* prepped = nullptr) = 0;

@@ -211,11 +211,11 @@ __device__ __forceinline__ int remap_row(int M, int rows_out, int mode, int H,
   if (m >= M) return -1;
   if (mode == kRowIdentity) return m < rows_out ? m : -1;
   const int Wp = W + 2, HpWp = (H + 2) * Wp;
-  if (mode == kRowPadToCompact) {
+  if (mode == kRowPadToCompact || mode == kRowPadToPad) {
     int img = m / HpWp, rem = m - img * HpWp;
     int hp = rem / Wp, wp = rem - hp * Wp;
     if (hp < 1 || hp > H || wp < 1 || wp > W) return -1;
-    return (img * H + hp - 1) * W + wp - 1;
+    return mode == kRowPadToPad ? m : (img * H + hp - 1) * W + wp - 1;
   }
   const int HW = H * W;
   int img = m / HW, rem = m - img * HW;
@@ -443,8 +443,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (lane == 0) mbar_arrive(&rempty[slot]);
           }
           if (a.relu) {
+            const float hi = a.relu == 2 ? 6.f : INFINITY;  // ReLU / ReLU6
 #pragma unroll
-            for (int j = 0; j < 32; j++) x[j] = fmaxf(x[j], 0.f);
+            for (int j = 0; j < 32; j++) x[j] = fminf(fmaxf(x[j], 0.f), hi);
           }
           uint32_t o[16];
 #pragma unroll
@@ -507,8 +508,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
           if (a.relu) {
+            const float hi = a.relu == 2 ? 6.f : INFINITY;
 #pragma unroll
-            for (int e = 0; e < 8; e++) x[e] = fmaxf(x[e], 0.f);
+            for (int e = 0; e < 8; e++) x[e] = fminf(fmaxf(x[e], 0.f), hi);
           }
           if (ok) {
             if (a.out_f32) {

@@ -21,6 +21,8 @@ enum RowMode : int {
   kRowIdentity = 0,     // out row = m
   kRowPadToCompact = 1, // m on the (H+2)x(W+2) grid; interior -> compact row
   kRowCompactToPad = 2, // m compact; written to the interior of the padded grid
+  kRowPadToPad = 3,     // m on the padded grid; interior rows written in place
+                        // (the zero border of the output grid is never touched)
 };
 
 struct ConvGemmArgs {
@@ -35,7 +37,7 @@ struct ConvGemmArgs {
   void* out;                         // bf16 or f32 [rows_out, ld_out]
   int ld_out;
   int out_f32;
-  int relu;
+  int relu;        // 0 none, 1 ReLU, 2 ReLU6
   int row_mode;
   int H, W;                          // unpadded spatial dims (row remap)
   int rows_out;                      // valid output rows (identity mode)

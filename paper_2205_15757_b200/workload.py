@@ -78,6 +78,28 @@ def resnet_group(arch: str = "resnet50", replicas: int = 3, seed: int = 0,
     return files, [hashlib.sha256(f).digest() for f in files], sds
 
 
+CNN_ARCHS = ("resnet50", "resnet101", "resnet152", "vgg16", "mobilenet_v2")
+HETERO_GROUP = ("resnet50", "resnet101", "vgg16", "mobilenet_v2")  # BASELINE configs[2]
+
+
+def hetero_group(archs=HETERO_GROUP, seed: int = 0, image: int = 224, classes: int = 1000,
+                 softmax: bool = True):
+    """A heterogeneous model group: replica p is architecture archs[p]
+    (torchvision init under torch.manual_seed(seed + p), eval BN).
+    Returns (files, digests, state_dicts)."""
+    import torch
+    import torchvision
+    files, sds = [], []
+    for p, arch in enumerate(archs):
+        if arch not in CNN_ARCHS:
+            raise ValueError(f"unsupported architecture {arch}")
+        torch.manual_seed(seed + p)
+        sd = getattr(torchvision.models, arch)(weights=None).eval().state_dict()
+        sds.append(sd)
+        files.append(cnn_model_file(arch, sd, 3 * image * image, classes, softmax))
+    return files, [hashlib.sha256(f).digest() for f in files], sds
+
+
 def _sodium():
     for p in glob.glob("/opt/prime-rl/.venv/lib/python3.12/site-packages/pyzmq.libs/libsodium*.so*"):
         try:

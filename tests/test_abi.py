@@ -55,3 +55,15 @@ def test_no_gpu_context_fails_loudly():
         pytest.skip("GPU present")
     with pytest.raises(p.CredoError):
         p.Context(0)
+
+
+def test_library_loaded_before_torch():
+    """libcredo_gpu.so resolves libnccl.so.2 to the copy torch uses, so
+    loading it first must not break a later `import torch` (the two NCCL
+    builds export different symbol sets)."""
+    import subprocess
+    import sys
+    from paper_2205_15757_b200.credo import LIB_PATH
+    code = f"import ctypes; ctypes.CDLL({LIB_PATH!r}); import torch; print('ok')"
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]

@@ -12,6 +12,7 @@ per class, and top-1 agreement whenever the CPU top-2 logit margin exceeds 1.0.
 """
 import numpy as np
 import pytest
+from conftest import check_certificate
 
 pytestmark = pytest.mark.gpu
 
@@ -72,50 +73,13 @@ def test_resnet50_batch_invariant(ctx, r50):
 
 def test_resnet50_group_certify_digests(ctx, r50, oracle):
     from paper_2205_15757_b200 import EUCLIDEAN, ModelGroup
-    from paper_2205_15757_b200.workload import encode_request, signed_requests
+    from paper_2205_15757_b200.workload import signed_requests
     gid = b"group-0"
     grp = ModelGroup(ctx, r50["models"], 1, EUCLIDEAN, 0.1, gid, 1, max_batch=8, topk=5)
     batch = signed_requests(B_TEST, 3 * 224 * 224, seed=5, group_id=gid,
                             eps=[None, 0.2, None, None, 0.01, None])
     r = grp.certify(batch, want_outputs=True, want_leaves=True)
-    outs = r["outputs"]
-    N = 3
-    sels, sats = [], []
-    for k in range(B_TEST):
-        e = 0.1 if batch.eps[k] is None else batch.eps[k]
-        m, d, s = oracle.select_quorum(outs[:, k], list(range(N)), N, 1, EUCLIDEAN, e)
-        assert (int(r["selected"][k]), float(r["diameter"][k]), bool(r["satisfied"][k])) == (m, d, s)
-        lab = oracle.ensemble_label(outs[:, k], m, 1) if s else -1
-        assert int(r["label"][k]) == lab
-        sels.append(m)
-        sats.append(s)
-        for p in range(N):
-            idx, val = oracle.topk(outs[p, k], 5)
-            assert np.array_equal(r["topk_idx"][p, k], idx)
-    leaves = {}
-    for p in range(N):
-        hs = []
-        for k in range(B_TEST):
-            req = encode_request(batch, k, gid)
-            res = oracle.result_encode(batch.request_ids[k].tobytes(), p, gid, 1,
-                                       outs[p, k], r50["digests"][p])
-            h = oracle.tagged_leaf_hash(0x52, req, res)
-            assert r["leaf_hashes"][p, k].tobytes() == h, (p, k)
-            hs.append(h)
-            leaves[(k, p)] = (req, res)
-        assert r["r_roots"][p].tobytes() == oracle.merkle_root(hs)
-    man = oracle.attest_manifest(sels, sats, N)
-    assert int(r["manifest_len"][0]) == len(man)
-    a = []
-    for kind, node, op in man:
-        if kind == 0:
-            a.append(oracle.leaf_hash(b"\x57" + r["r_roots"][node].tobytes()))
-        elif kind == 1:
-            req, res = leaves[(op, node)]
-            a.append(oracle.tagged_leaf_hash(0x53, req, res))
-        else:
-            a.append(oracle.leaf_hash(oracle.failure_leaf(batch.request_ids[op].tobytes(), gid, 1)))
-    assert r["a_root"].tobytes() == oracle.merkle_root(a)
+    check_certificate(r, batch, r50["digests"], 1, 0.1, gid, oracle)
     grp.free()
 
 
