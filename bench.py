@@ -116,6 +116,20 @@ def make_group(ctx, B, seed=0, eps=0.1):
     return grp, models, files, digs, sds
 
 
+C3_EPS = 1.5  # >= sqrt(2): random-init nets of different families do not agree tightly
+
+
+def make_hetero_group(ctx, B, seed=0, eps=C3_EPS):
+    """C3 (BASELINE.json configs[2]): ResNet-50, ResNet-101, VGG-16,
+    MobileNetV2, one replica each, f = 1."""
+    from paper_2205_15757_b200 import EUCLIDEAN, Model, ModelGroup
+    from paper_2205_15757_b200.workload import HETERO_GROUP, hetero_group
+    files, digs, sds = hetero_group(HETERO_GROUP, seed=seed)
+    models = [Model.load_cnn(ctx, f, d) for f, d in zip(files, digs)]
+    grp = ModelGroup(ctx, models, 1, EUCLIDEAN, eps, b"group-0", 1, max_batch=B, topk=5)
+    return grp, models, files, digs, sds
+
+
 def replica_f(world):
     return (world - 1) // 2  # quorum of a strict majority
 
@@ -151,6 +165,8 @@ def bench_gpu(args, rank, world, local_rank):
     replica = args.mode == "replica"
     if replica:
         grp, models, files, digs, sds = make_dist_group(ctx, B, rank, world)
+    elif args.workload == "c3":
+        grp, models, files, digs, sds = make_hetero_group(ctx, B)
     else:
         grp, models, files, digs, sds = make_group(ctx, B, seed=0)
     # group mode: each rank its own stream; replica mode: one shared stream
@@ -161,7 +177,7 @@ def bench_gpu(args, rank, world, local_rank):
     L.cg_timing_read.argtypes = [__import__("ctypes").c_int,
                                  __import__("ctypes").POINTER(__import__("ctypes").c_double),
                                  __import__("ctypes").POINTER(__import__("ctypes").c_uint64)]
-    flops_img = L.cg_model_flops_per_input(models[0].h)
+    flops_img = sum(L.cg_model_flops_per_input(m.h) for m in models)  # this rank's replicas
 
     # Two rotating batches of 154 MB f64 inputs each (> 126 MB L2): pinned
     # host copies for e2e, device copies for the device-resident value.
@@ -244,6 +260,7 @@ def bench_gpu(args, rank, world, local_rank):
     ms = max_over_ranks(e0.elapsed_time(e1))
     res = grp.fetch()
     sat_dev = float(np.mean(res["satisfied"]))
+    label_frac = float(np.mean(res["label"] >= 0))
     while pend:
         grp.certify_ticket(pend.popleft(), sync=False)
     torch.cuda.synchronize()
@@ -295,7 +312,7 @@ def bench_gpu(args, rank, world, local_rank):
     gemm_ms_step = tg.value / args.steps
     chain_ms_step = tc.value / args.steps
     pk, pk_src = peaks()
-    flops_step = len(models) * B * flops_img  # this rank's replicas
+    flops_step = B * flops_img
     achieved = flops_step / (gemm_ms_step / 1e3) / 1e12
     peak = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
     roofline = {"bound": "tensor", "kernel": "conv_gemm (tcgen05 implicit-GEMM, all convs+fc)",
@@ -331,6 +348,14 @@ def bench_gpu(args, rank, world, local_rank):
            "gpu_launches": int(launches),
            "roofline": roofline,
            "clocks": clk.summary()}
+    if args.workload == "c3":
+        from paper_2205_15757_b200.workload import HETERO_GROUP
+        out["metric"] = METRIC.replace("(ResNet-50 group)", "(heterogeneous group)")
+        out["config"].update(
+            workload="C3: heterogeneous 4-replica group (ResNet-50, ResNet-101, VGG-16, "
+                     f"MobileNetV2), f=1, batch {B}, 224x224 (BASELINE.json configs[2])",
+            model="+".join(HETERO_GROUP), replicas=4, f=1, epsilon=C3_EPS,
+            labels_agreed_fraction=label_frac)
     if replica:
         out["scaling"] = "strong"
         out["config"].update(
@@ -339,12 +364,14 @@ def bench_gpu(args, rank, world, local_rank):
             replicas=world, f=replica_f(world), global_batch=B,
             parallelism=f"replica-parallel x{world} (rank = provider)")
     if rank == 0 and not args.no_cpu_baseline and not replica:
-        out["cpu_baseline"] = cpu_baseline(files, digs, sds, batches[0], args)
+        archs = [m.arch for m in models] if args.workload == "c3" else ["resnet50"] * 3
+        out["cpu_baseline"] = cpu_baseline(archs, digs, sds, batches[0], args,
+                                           grp.default_eps)
     return out
 
 
 # ------------------------------------------------------------ CPU baseline
-def cpu_path(sds, encs, inputs, digs, threads, R):
+def cpu_path(archs, sds, encs, inputs, digs, threads, R, eps=0.1):
     """The reference's CPU path for a sample: torchvision fp32 forward per
     replica (restatement: the reference has no CNN), then the compiled
     reference's select_quorum, ensemble_label, result leaves, R trees,
@@ -354,17 +381,17 @@ def cpu_path(sds, encs, inputs, digs, threads, R):
     from oracle import cnn_oracle
     torch.set_num_threads(threads)
     outs = []
-    for sd in sds:
-        m = cnn_oracle.build("resnet50", sd)
+    for arch, sd in zip(archs, sds):
+        m = cnn_oracle.build(arch, sd)
         outs.append(cnn_oracle.softmax_f64(cnn_oracle.logits(m, inputs)))
     outs = np.stack(outs)
     h = R.batch_new(encs, 1)
-    r = R.certify_batch(h, 3, 1, 0, 0.1, outs, 1, digs, threads=threads)
+    r = R.certify_batch(h, len(archs), 1, 0, eps, outs, 1, digs, threads=threads)
     R.batch_free(h)
     return r
 
 
-def cpu_baseline(files, digs, sds, batch, args):
+def cpu_baseline(archs, digs, sds, batch, args, eps=0.1):
     from oracle.oracle import Reference
     from paper_2205_15757_b200.workload import encode_request
     threads = os.cpu_count() or 1
@@ -375,14 +402,13 @@ def cpu_baseline(files, digs, sds, batch, args):
         return {"value": None, "unit": UNIT, "cores": threads, "kind": "port",
                 "sample": "oracle/_ref not built on this box"}
     R = Reference()
-    models = [__import__("oracle.cnn_oracle", fromlist=["x"]).build("resnet50", sd) for sd in sds]
-    del models
-    cpu_path(sds, encs[:2], batch.inputs[:2], digs, threads, R)  # warm
+    cpu_path(archs, sds, encs[:2], batch.inputs[:2], digs, threads, R, eps)  # warm
     t = time.perf_counter()
-    cpu_path(sds, encs, batch.inputs[:S], digs, threads, R)
+    cpu_path(archs, sds, encs, batch.inputs[:S], digs, threads, R, eps)
     dt = time.perf_counter() - t
     return {"value": round(S / dt, 3), "unit": UNIT, "cores": threads, "kind": kind,
-            "sample": f"{S} requests x 3 replicas: torchvision fp32 forward (restated; "
+            "sample": f"{S} requests x {len(archs)} replicas ({'+'.join(sorted(set(archs)))}): "
+                      f"torchvision fp32 forward (restated; "
                       f"the reference has no CNN) + compiled reference select_quorum/"
                       f"ensemble_label/result leaves/R+A trees, {dt:.1f} s"}
 
@@ -483,10 +509,10 @@ def bench_reference(args, rank, world):
         return {"impl": "reference", "unavailable": "oracle/_ref/libcredo_ref.so not built"}
     R = Reference()
     for _ in range(max(1, min(args.warmup, 1))):
-        cpu_path(sds, encs[:2], batch.inputs[:2], digs, threads, R)
+        cpu_path(["resnet50"] * 3, sds, encs[:2], batch.inputs[:2], digs, threads, R)
     t = time.perf_counter()
     for _ in range(args.steps_ref):
-        cpu_path(sds, encs, batch.inputs, digs, threads, R)
+        cpu_path(["resnet50"] * 3, sds, encs, batch.inputs, digs, threads, R)
     dt = time.perf_counter() - t
     v = args.steps_ref * S / dt
     return {"impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": UNIT,
@@ -519,9 +545,10 @@ def main():
     ap.add_argument("--mode", default="group", choices=["group", "replica"],
                     help="group: a whole 3-replica group per GPU (weak scaling); "
                          "replica: one replica per GPU, NCCL all-gather (N>1)")
-    ap.add_argument("--workload", default="c2", choices=["c2", "c5"],
-                    help="c2: the headline certified-request pipeline; c5: "
-                         "agreement + label-digest sweep (one line per --c5 spec)")
+    ap.add_argument("--workload", default="c2", choices=["c2", "c3", "c5"],
+                    help="c2: the headline certified-request pipeline (3x ResNet-50); "
+                         "c3: the heterogeneous 4-replica group; c5: agreement + "
+                         "label-digest sweep (one line per --c5 spec)")
     ap.add_argument("--c5", default="1e6x8x1000,1e6x4x1000,1e6x8x10,1e5x8x1000,1e4x8x1000,"
                                     "1e3x8x1000",
                     help="comma list of RxNxV for --workload c5")

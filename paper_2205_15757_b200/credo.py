@@ -277,8 +277,8 @@ class AgreementOutcome:
 
 # ------------------------------------------------------------------ models
 class Model:
-    def __init__(self, ctx: Context, h, digest: bytes):
-        self.ctx, self.h, self.digest = ctx, h, digest
+    def __init__(self, ctx: Context, h, digest: bytes, arch: str = "linear"):
+        self.ctx, self.h, self.digest, self.arch = ctx, h, digest, arch
         u, v = u64(), u64()
         ctx.L.cg_model_dims(h, C.byref(u), C.byref(v))
         self.input_dim, self.output_dim = u.value, v.value
@@ -296,7 +296,10 @@ class Model:
         h = vp()
         ctx._check(ctx.L.cg_model_load_cnn(ctx.h, file, u64(len(file)),
                                            digest, C.byref(h)))
-        return cls(ctx, h, digest)
+        # canonical header: str magic | str arch | ...
+        ml = int.from_bytes(file[0:4], "big")
+        al = int.from_bytes(file[4 + ml:8 + ml], "big")
+        return cls(ctx, h, digest, file[8 + ml:8 + ml + al].decode())
 
     def free(self):
         if self.h:
@@ -385,6 +388,7 @@ class ModelGroup:
         self.v = models[0].output_dim
         self.u = models[0].input_dim
         self.group_id, self.version = group_id, version
+        self.default_eps = default_eps
         arr = (vp * len(models))(*[m.h for m in models])
         h = vp()
         ctx._check(ctx.L.cg_group_create(ctx.h, arr, u32(len(models)), u32(f),
@@ -406,6 +410,7 @@ class ModelGroup:
         self.N, self.f, self.topk = len(digests), f, topk
         self.v, self.u = my_model.output_dim, my_model.input_dim
         self.group_id, self.version = group_id, version
+        self.default_eps = default_eps
         h = vp()
         ctx._check(ctx.L.cg_group_create_dist(ctx.h, my_model.h, b"".join(digests), u32(f),
                                               u32(metric), dbl(default_eps), group_id,
