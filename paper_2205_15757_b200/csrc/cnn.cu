@@ -129,10 +129,10 @@ __global__ void maxpool3s2_kernel(const bf16* __restrict__ in, int B, int H, int
   *reinterpret_cast<uint4*>(out + pix * C + ch * 8) = *reinterpret_cast<uint4*>(o);
 }
 
-// Stride-2 3x3 operand from the zero-bordered grid: [B*Ho*Wo, 9*C].
-__global__ void gather_s2_3x3_kernel(const bf16* __restrict__ pad, int B, int H,
-                                     int C, bf16* __restrict__ out) {
-  const int Ho = H / 2, Wp = H + 2, chunks = C / 8;
+// 3x3 operand (stride 1 or 2) from the zero-bordered grid: [B*Ho*Wo, 9*C].
+__global__ void gather3x3_kernel(const bf16* __restrict__ pad, int B, int H, int C,
+                                 int stride, bf16* __restrict__ out) {
+  const int Ho = H / stride, Wp = H + 2, chunks = C / 8;
   size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   size_t row = t / (9 * chunks);
   int r = (int)(t - row * 9 * chunks);
@@ -142,7 +142,7 @@ __global__ void gather_s2_3x3_kernel(const bf16* __restrict__ pad, int B, int H,
   int ho = rem / Ho, wo = rem - ho * Ho;
   int dr = tap / 3, ds = tap - dr * 3;
   const uint4* src = reinterpret_cast<const uint4*>(
-      pad + (((size_t)n * Wp + 2 * ho + dr) * Wp + 2 * wo + ds) * C + ch * 8);
+      pad + (((size_t)n * Wp + stride * ho + dr) * Wp + stride * wo + ds) * C + ch * 8);
   *reinterpret_cast<uint4*>(out + row * 9 * C + tap * C + ch * 8) = __ldg(src);
 }
 
@@ -359,10 +359,8 @@ class ResNet final : public CnnModel {
       act = std::max(act, B * b.H_in * b.H_in * b.cin);
       t2 = std::max(t2, B * b.H_out * b.H_out * b.width);
       if (b.has_ds) dsz = std::max(dsz, B * b.H_out * b.H_out * b.cout);
-      if (b.stride == 2) {
-        g3 = std::max(g3, B * b.H_out * b.H_out * 9 * b.width);
-        g1 = std::max(g1, B * b.H_out * b.H_out * b.cin);
-      }
+      if (b.stride == 2) g3 = std::max(g3, B * b.H_out * b.H_out * 9 * b.width);
+      if (b.stride == 2) g1 = std::max(g1, B * b.H_out * b.H_out * b.cin);
       auto key = std::make_pair(b.H_in, b.width);
       if (!pads_.count(key)) pads_[key] = nullptr;
     }
@@ -496,8 +494,11 @@ class ResNet final : public CnnModel {
       // c1: 1x1 -> interior of the zero-bordered grid
       gemm(b.c1, X, B * Hi * Hi, B * Hi * Hi, b.c1.Kc, 1, &zero, nullptr, 0, P, b.width, 0, 1,
            kRowCompactToPad, Hi, B * Hp * Hp);
-      // c2: 3x3
-      if (b.stride == 1) {
+      // c2: 3x3 (implicit over the padded grid, or gathered on small grids)
+      // (gathering the 7x7 stage too was measured: the gather traffic cost
+      // more than the padded rows' MMA work it saves)
+      const bool gather = b.stride == 2;
+      if (!gather) {
         int taps[9];
         for (int dr = 0; dr < 3; dr++)
           for (int ds = 0; ds < 3; ds++) taps[dr * 3 + ds] = (dr - 1) * Hp + (ds - 1);
@@ -505,10 +506,10 @@ class ResNet final : public CnnModel {
              1, kRowPadToCompact, Hi, B * Ho * Ho);
       } else {
         bf16* G = g3_;
-        int C = b.width;
-        aux([P, G, B, Hi, C](cudaStream_t st) {
-          size_t th = (size_t)B * (Hi / 2) * (Hi / 2) * 9 * (C / 8);
-          gather_s2_3x3_kernel<<<grid_for(th), 256, 0, st>>>(P, B, Hi, C, G);
+        const int C = b.width, s = b.stride;
+        aux([P, G, B, Hi, C, s](cudaStream_t st) {
+          size_t th = (size_t)B * (Hi / s) * (Hi / s) * 9 * (C / 8);
+          gather3x3_kernel<<<grid_for(th), 256, 0, st>>>(P, B, Hi, C, s, G);
           CG_CHECK_LAUNCH();
         });
         // the 9-tap weights double as one K = 9*C operand (same (tap, c) order)

@@ -256,14 +256,17 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int num_n = (a.N + BN - 1) / BN, num_m = (a.M + BM - 1) / BM;
-  // tiles are replica-major: t -> (replica r, m block, n block)
-  const int tiles_per = num_m * num_n, tiles = tiles_per * gp.n;
+  // tile order t -> (m block, replica r, n block): the replicas' tiles of one
+  // row block run back to back, so an operand they share (the conv1 im2col
+  // of the batch) is read from HBM once and from L2 by the other replicas
+  const int tiles = num_m * num_n * gp.n;
   const int kpt = a.Kc / BK, num_k = a.ntaps * kpt;
   auto coords = [&](int t, int& r, int& m0, int& n0) {
-    r = t / tiles_per;
-    const int tt = t - r * tiles_per;
-    m0 = (tt / num_n) * BM;
-    n0 = (tt % num_n) * BN;
+    const int per_m = gp.n * num_n;
+    const int mb = t / per_m, rem = t - mb * per_m;
+    r = rem / num_n;
+    m0 = mb * BM;
+    n0 = (rem - r * num_n) * BN;
   };
 
   if (warp == 0 && lane == 0) {
