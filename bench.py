@@ -315,9 +315,19 @@ def bench_gpu(args, rank, world, local_rank):
     flops_step = B * flops_img
     achieved = flops_step / (gemm_ms_step / 1e3) / 1e12
     peak = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
+    traffic, traffic_src = None, None
+    if args.workload == "c2" and not replica:
+        try:  # DRAM bytes of one step's GEMM launches, from the committed ncu capture
+            with open(os.path.join(ROOT, "profiles", "r01_gemm_step_traffic.json")) as f:
+                tj = json.load(f)
+            traffic, traffic_src = tj["traffic_bytes_per_step"], tj["source"]
+        except Exception:
+            pass
     roofline = {"bound": "tensor", "kernel": "conv_gemm (tcgen05 implicit-GEMM, all convs+fc)",
                 "achieved": round(achieved, 1), "peak": peak, "unit": "TFLOP/s",
-                "frac": round(achieved / peak, 4), "traffic": None,
+                "frac": round(achieved / peak, 4), "traffic": traffic,
+                "traffic_unit": "DRAM bytes per step (all conv_gemm launches)",
+                "traffic_source": traffic_src,
                 "peak_source": f"{pk_src} bf16_tflops_sustained",
                 "algorithmic_flops_per_step": flops_step,
                 "gemm_ms_per_step": round(gemm_ms_step, 3),

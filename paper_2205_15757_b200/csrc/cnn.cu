@@ -5,7 +5,9 @@
 //   1x1 conv           -> GEMM over compact pixel rows
 //   3x3 conv, stride 1 -> 9 row-shifted taps over a zero-bordered grid that
 //                         the preceding 1x1 conv writes directly (no im2col)
-//   3x3/1x1, stride 2  -> small gather kernel, then one-tap GEMM
+//   3x3, stride 2      -> c1 writes its zero-bordered grid phase split (4
+//                         parity planes), so the 3x3 is 9 row shifts over
+//                         the planes (no im2col); 1x1/2 downsample: gather
 //   conv1 7x7/2        -> fused f64->bf16 im2col of the request input
 //   fc                 -> GEMM with f32 logits out
 #include <cuda_bf16.h>
@@ -127,23 +129,6 @@ __global__ void maxpool3s2_kernel(const bf16* __restrict__ in, int B, int H, int
 #pragma unroll
   for (int j = 0; j < 8; j++) o[j] = __float2bfloat16(m[j]);
   *reinterpret_cast<uint4*>(out + pix * C + ch * 8) = *reinterpret_cast<uint4*>(o);
-}
-
-// 3x3 operand (stride 1 or 2) from the zero-bordered grid: [B*Ho*Wo, 9*C].
-__global__ void gather3x3_kernel(const bf16* __restrict__ pad, int B, int H, int C,
-                                 int stride, bf16* __restrict__ out) {
-  const int Ho = H / stride, Wp = H + 2, chunks = C / 8;
-  size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  size_t row = t / (9 * chunks);
-  int r = (int)(t - row * 9 * chunks);
-  if (row >= (size_t)B * Ho * Ho) return;
-  int tap = r / chunks, ch = r - tap * chunks;
-  int n = (int)(row / (Ho * Ho)), rem = (int)(row - (size_t)n * Ho * Ho);
-  int ho = rem / Ho, wo = rem - ho * Ho;
-  int dr = tap / 3, ds = tap - dr * 3;
-  const uint4* src = reinterpret_cast<const uint4*>(
-      pad + (((size_t)n * Wp + stride * ho + dr) * Wp + stride * wo + ds) * C + ch * 8);
-  *reinterpret_cast<uint4*>(out + row * 9 * C + tap * C + ch * 8) = __ldg(src);
 }
 
 // Stride-2 1x1 operand: [B*Ho*Wo, C] = in[n, 2ho, 2wo, :].
@@ -353,13 +338,12 @@ class ResNet final : public CnnModel {
     xcol_ = alloc(B * H1 * H1 * 192);
     nhwc4_ = alloc(B * (S_ + 6) * (S_ + 6) * 4);
     c1out_ = alloc(B * H1 * H1 * 64);
-    size_t act = 0, t2 = 0, dsz = 0, g3 = 0, g1 = 0;
+    size_t act = 0, t2 = 0, dsz = 0, g1 = 0;
     for (auto& b : blocks_) {
       act = std::max(act, B * b.H_out * b.H_out * b.cout);
       act = std::max(act, B * b.H_in * b.H_in * b.cin);
       t2 = std::max(t2, B * b.H_out * b.H_out * b.width);
       if (b.has_ds) dsz = std::max(dsz, B * b.H_out * b.H_out * b.cout);
-      if (b.stride == 2) g3 = std::max(g3, B * b.H_out * b.H_out * 9 * b.width);
       if (b.stride == 2) g1 = std::max(g1, B * b.H_out * b.H_out * b.cin);
       auto key = std::make_pair(b.H_in, b.width);
       if (!pads_.count(key)) pads_[key] = nullptr;
@@ -368,7 +352,6 @@ class ResNet final : public CnnModel {
     act_[1] = alloc(act);
     t2_ = alloc(t2);
     ds_ = alloc(dsz);
-    g3_ = alloc(g3);
     g1_ = alloc(g1);
     for (auto& kv : pads_) {
       size_t Hp = kv.first.first + 2;
@@ -491,38 +474,37 @@ class ResNet final : public CnnModel {
       bf16* Y = act_[cur ^ 1];
       const int Hi = b.H_in, Ho = b.H_out, Hp = Hi + 2;
       bf16* P = pads_.at({Hi, b.width});
-      // c1: 1x1 -> interior of the zero-bordered grid
-      gemm(b.c1, X, B * Hi * Hi, B * Hi * Hi, b.c1.Kc, 1, &zero, nullptr, 0, P, b.width, 0, 1,
-           kRowCompactToPad, Hi, B * Hp * Hp);
-      // c2: 3x3 (implicit over the padded grid, or gathered on small grids)
-      // (gathering the 7x7 stage too was measured: the gather traffic cost
-      // more than the padded rows' MMA work it saves)
-      const bool gather = b.stride == 2;
-      if (!gather) {
+      if (b.stride == 1) {
+        // c1: 1x1 -> interior of the zero-bordered grid
+        gemm(b.c1, X, B * Hi * Hi, B * Hi * Hi, b.c1.Kc, 1, &zero, nullptr, 0, P, b.width, 0, 1,
+             kRowCompactToPad, Hi, B * Hp * Hp);
+        // c2: 3x3 as 9 row shifts of the padded grid
         int taps[9];
         for (int dr = 0; dr < 3; dr++)
           for (int ds = 0; ds < 3; ds++) taps[dr * 3 + ds] = (dr - 1) * Hp + (ds - 1);
         gemm(b.c2, P, B * Hp * Hp, B * Hp * Hp, b.c2.Kc, 9, taps, nullptr, 0, t2_, b.width, 0,
              1, kRowPadToCompact, Hi, B * Ho * Ho);
       } else {
-        bf16* G = g3_;
-        const int C = b.width, s = b.stride;
-        aux([P, G, B, Hi, C, s](cudaStream_t st) {
-          size_t th = (size_t)B * (Hi / s) * (Hi / s) * 9 * (C / 8);
-          gather3x3_kernel<<<grid_for(th), 256, 0, st>>>(P, B, Hi, C, s, G);
-          CG_CHECK_LAUNCH();
-        });
-        // the 9-tap weights double as one K = 9*C operand (same (tap, c) order)
-        gemm(b.c2, G, B * Ho * Ho, B * Ho * Ho, 9 * C, 1, &zero, nullptr, 0, t2_, b.width, 0,
-             1, kRowIdentity, 0, B * Ho * Ho);
+        // Stride 2: c1 writes the phase split of its zero-bordered grid; the
+        // stride-2 3x3 is then 9 row shifts (plane base + p*Wq + q) over an
+        // (Ho+1)^2 plane-00 grid.
+        gemm(b.c1, X, B * Hi * Hi, B * Hi * Hi, b.c1.Kc, 1, &zero, nullptr, 0, P, b.width, 0, 1,
+             kRowCompactToPhasePad, Hi, B * Hp * Hp);
+        const int Wq = Ho + 1, plane = B * Wq * Wq;
+        int taps[9];
+        for (int dr = 0; dr < 3; dr++)
+          for (int ds = 0; ds < 3; ds++)
+            taps[dr * 3 + ds] = ((dr & 1) * 2 + (ds & 1)) * plane + (dr >> 1) * Wq + (ds >> 1);
+        gemm(b.c2, P, 4 * plane, plane, b.c2.Kc, 9, taps, nullptr, 0, t2_, b.width, 0, 1,
+             kRowPhaseGridToCompact, Ho, B * Ho * Ho);
       }
-      // identity / downsample
+      // identity / downsample (stride 2: the decimated input X[2h, 2w])
       const bf16* ident = X;
       if (b.has_ds) {
         const bf16* dsin = X;
         if (b.stride == 2) {
           bf16* G1 = g1_;
-          int C = b.cin;
+          const int C = b.cin;
           aux([X, G1, B, Hi, C](cudaStream_t st) {
             size_t th = (size_t)B * (Hi / 2) * (Hi / 2) * (C / 8);
             gather_s2_1x1_kernel<<<grid_for(th), 256, 0, st>>>(X, B, Hi, C, G1);
@@ -685,7 +667,7 @@ class ResNet final : public CnnModel {
   uint32_t maxB_ = 0;
   std::vector<void*> bufs_;
   bf16 *xcol_ = nullptr, *nhwc4_ = nullptr, *c1out_ = nullptr, *act_[2] = {nullptr, nullptr}, *t2_ = nullptr,
-       *ds_ = nullptr, *g3_ = nullptr, *g1_ = nullptr, *pooled_ = nullptr;
+       *ds_ = nullptr, *g1_ = nullptr, *pooled_ = nullptr;
   std::map<std::pair<int, int>, bf16*> pads_;
   std::map<uint32_t, Plan> plans_;
 };

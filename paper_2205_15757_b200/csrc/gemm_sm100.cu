@@ -210,6 +210,20 @@ __device__ __forceinline__ int remap_row(int M, int rows_out, int mode, int H,
                                          int W, int m) {
   if (m >= M) return -1;
   if (mode == kRowIdentity) return m < rows_out ? m : -1;
+  if (mode == kRowPhaseGridToCompact) {  // H, W = output dims, grid (H+1)(W+1)
+    const int Wq = W + 1, HqWq = (H + 1) * Wq;
+    const int n = m / HqWq, rem = m - n * HqWq, i = rem / Wq, j = rem - i * Wq;
+    return (i < H && j < W) ? (n * H + i) * W + j : -1;
+  }
+  if (mode == kRowCompactToPhasePad) {
+    // compact (n, h, w) -> padded (h+1, w+1) -> plane (row & 1, col & 1) of
+    // the phase-split zero-bordered grid; planes stacked ab-major, image next
+    const int HW = H * W, Bn = M / HW;
+    const int n = m / HW, rem = m - n * HW;
+    const int h = rem / W + 1, w = rem - (rem / W) * W + 1;
+    const int Hq = (H + 2) >> 1, Wq = (W + 2) >> 1;
+    return ((((h & 1) * 2 + (w & 1)) * Bn + n) * Hq + (h >> 1)) * Wq + (w >> 1);
+  }
   const int Wp = W + 2, HpWp = (H + 2) * Wp;
   if (mode == kRowPadToCompact || mode == kRowPadToPad) {
     int img = m / HpWp, rem = m - img * HpWp;
@@ -395,6 +409,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const __nv_bfloat16* res_r = gp.residual[r_];
       void* out_r = gp.out[r_];
       const int my_orow = remap_row(a.M, a.rows_out, a.row_mode, a.H, a.W, m0 + q * 32 + lane);
+
       mbar_wait(&tfull[acc], acc_phase);
       if (warp == 2) CG_TRACE(5, tile_i);
       tc_fence_after();

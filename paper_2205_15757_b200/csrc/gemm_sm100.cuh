@@ -23,6 +23,13 @@ enum RowMode : int {
   kRowCompactToPad = 2, // m compact; written to the interior of the padded grid
   kRowPadToPad = 3,     // m on the padded grid; interior rows written in place
                         // (the zero border of the output grid is never touched)
+  // Phase-split grid for stride-2 3x3 convs: the zero-bordered grid stored
+  // as 4 planes (row parity a, column parity b), plane ab holding padded
+  // pixels (2i+a, 2j+b), so the stride-2 3x3 becomes 9 constant row shifts
+  // (plane base + p*Wq + q) instead of a gather.
+  kRowCompactToPhasePad = 4,  // m compact (H x W) -> phase-split padded grid
+  kRowPhaseGridToCompact = 5, // m on an (H+1) x (W+1) plane-00 grid -> compact
+                              // H x W (H, W = output dims)
 };
 
 struct ConvGemmArgs {
