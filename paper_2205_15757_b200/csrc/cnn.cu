@@ -83,7 +83,9 @@ __global__ void __launch_bounds__(32 * kIm2colWarps) conv1_im2col_nhwc4_kernel(
       fill = 0;
     }
   };
-#pragma unroll 1
+  // fully unrolled: every put() position is a compile-time constant, so the
+  // 8-value staging buffer stays in registers
+#pragma unroll
   for (int dr = 0; dr < 7; dr++) {
 #pragma unroll
     for (int ds = 0; ds < 7; ds++) {
@@ -93,7 +95,8 @@ __global__ void __launch_bounds__(32 * kIm2colWarps) conv1_im2col_nhwc4_kernel(
       put(p.y & 0xffffu);
     }
   }
-  while (chunk < 24) put(0);  // K 147 -> 192
+#pragma unroll
+  for (int k = 147; k < 192; k++) put(0);  // K 147 -> 192
   __syncwarp();
   const size_t nrow = rows - row0 < 32 ? rows - row0 : 32;
   uint4* dst = reinterpret_cast<uint4*>(out + row0 * 192);
