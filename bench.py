@@ -381,7 +381,14 @@ def bench_gpu(args, rank, world, local_rank):
 
 
 # ------------------------------------------------------------ CPU baseline
-def cpu_path(archs, sds, encs, inputs, digs, threads, R, eps=0.1):
+def cpu_models(archs, sds):
+    """The replicas as torchvision CPU modules (loaded once, like the
+    reference's InferenceEngine::load_group, outside any timed region)."""
+    from oracle import cnn_oracle
+    return [cnn_oracle.build(arch, sd) for arch, sd in zip(archs, sds)]
+
+
+def cpu_path(models, encs, inputs, digs, threads, R, eps=0.1):
     """The reference's CPU path for a sample: torchvision fp32 forward per
     replica (restatement: the reference has no CNN), then the compiled
     reference's select_quorum, ensemble_label, result leaves, R trees,
@@ -391,12 +398,11 @@ def cpu_path(archs, sds, encs, inputs, digs, threads, R, eps=0.1):
     from oracle import cnn_oracle
     torch.set_num_threads(threads)
     outs = []
-    for arch, sd in zip(archs, sds):
-        m = cnn_oracle.build(arch, sd)
+    for m in models:
         outs.append(cnn_oracle.softmax_f64(cnn_oracle.logits(m, inputs)))
     outs = np.stack(outs)
     h = R.batch_new(encs, 1)
-    r = R.certify_batch(h, len(archs), 1, 0, eps, outs, 1, digs, threads=threads)
+    r = R.certify_batch(h, len(models), 1, 0, eps, outs, 1, digs, threads=threads)
     R.batch_free(h)
     return r
 
@@ -412,15 +418,124 @@ def cpu_baseline(archs, digs, sds, batch, args, eps=0.1):
         return {"value": None, "unit": UNIT, "cores": threads, "kind": "port",
                 "sample": "oracle/_ref not built on this box"}
     R = Reference()
-    cpu_path(archs, sds, encs[:2], batch.inputs[:2], digs, threads, R, eps)  # warm
+    models = cpu_models(archs, sds)
+    cpu_path(models, encs[:2], batch.inputs[:2], digs, threads, R, eps)  # warm
     t = time.perf_counter()
-    cpu_path(archs, sds, encs, batch.inputs[:S], digs, threads, R, eps)
+    cpu_path(models, encs, batch.inputs[:S], digs, threads, R, eps)
     dt = time.perf_counter() - t
     return {"value": round(S / dt, 3), "unit": UNIT, "cores": threads, "kind": kind,
             "sample": f"{S} requests x {len(archs)} replicas ({'+'.join(sorted(set(archs)))}): "
                       f"torchvision fp32 forward (restated; "
                       f"the reference has no CNN) + compiled reference select_quorum/"
                       f"ensemble_label/result leaves/R+A trees, {dt:.1f} s"}
+
+
+# ------------------------------------------------------------ C4 update
+def bench_c4(args, rank, world, local_rank):
+    """C4 (BASELINE.json configs[3]): an N-replica ResNet-50 group, one model
+    owner per GPU (rank = provider, replica outputs + R roots all-gathered
+    over NCCL; on one GPU the N replicas are time-sliced), f = (N-1)//3,
+    batch 512, with a model-version update mid-stream: in the middle third
+    of the timed steps both versions are live, so every batch is certified
+    under v1 and v2 (engine.cpp:196-206: one batch per live version); the
+    host-side version fold (state.cpp:23-45) keeps one certificate per
+    request, so a request counts once."""
+    import torch
+    import torch.distributed as dist
+    from collections import deque
+
+    from paper_2205_15757_b200 import EUCLIDEAN, Context, Model, ModelGroup
+    from paper_2205_15757_b200.dist import assigned_models, share_bytes
+    from paper_2205_15757_b200.workload import resnet_group, signed_requests
+    torch.cuda.set_device(local_rank)
+    ctx = Context(local_rank)
+    stream = torch.cuda.current_stream()
+    ctx.set_stream(stream.cuda_stream)
+    B, N = args.batch, (world if world > 1 else args.replicas)
+    f = (N - 1) // 3
+    eps = 0.1
+    if world > 1:
+        uid = share_bytes(Context.nccl_unique_id() if rank == 0 else None)
+        ctx.init_nccl(uid, world, rank)
+    groups, keep = [], []
+    for version, salt in ((1, 0), (2, 1000)):  # v2: a new jitter salt (harness.cpp:601-602)
+        files, digs, _ = resnet_group("resnet50", replicas=N, seed=0, jitter=5e-3, salt=salt)
+        if world > 1:
+            (p,) = assigned_models(world, N, rank)
+            ms = [Model.load_cnn(ctx, files[p], digs[p])]
+            g = ModelGroup.create_dist(ctx, ms[0], digs, f, EUCLIDEAN, eps, b"group-0", version,
+                                       max_batch=B, topk=5)
+        else:
+            ms = [Model.load_cnn(ctx, fl, d) for fl, d in zip(files, digs)]
+            g = ModelGroup(ctx, ms, f, EUCLIDEAN, eps, b"group-0", version, max_batch=B, topk=5)
+        groups.append(g)
+        keep.append(ms)
+    nb = 2
+    batches = [signed_requests(B, U, seed=7 + i) for i in range(nb)]
+    from copy import copy
+    dev = []
+    for b in batches:
+        d = torch.from_numpy(b.inputs).to(f"cuda:{local_rank}")
+        db = copy(b)
+        db.inputs, db.B, db.u = d.data_ptr(), B, U
+        db._keep = d
+        dev.append(db)
+    K, D = args.steps, min(args.depth, 6)
+
+    def live(i):  # versions live for timed step i (warm-up steps: v1 only)
+        if i < K // 3:
+            return [0]
+        return [0, 1] if i < 2 * K // 3 else [1]
+
+    for i in range(args.warmup):  # untimed, both versions
+        for g in groups:
+            g.certify(dev[i % nb])
+    torch.cuda.synchronize()
+    pend = [deque(), deque()]
+    for j in range(min(D, K)):
+        for v in live(j):
+            pend[v].append(groups[v].ingest(dev[j % nb]))
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    certs = 0
+    with ClockSampler(local_rank) as clk:
+        e0.record(stream)
+        for i in range(K):
+            for v in live(i):
+                groups[v].certify_ticket(pend[v].popleft(), sync=False)
+            certs += len(live(i))
+            j = i + D
+            if j < K:
+                for v in live(j):
+                    pend[v].append(groups[v].ingest(dev[j % nb]))
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local_rank}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    sat = float(np.mean(groups[1].fetch()["satisfied"]))
+    value = K * B * sat / (ms / 1e3)
+    out = {"metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
+           "steps": K, "warmup": args.warmup, "ms_per_step": round(ms / K, 3),
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+           "data": "synthetic (random-init jittered ResNet-50 replicas, v2 = new jitter salt)",
+           "config": {"workload": f"C4: {N}-replica ResNet-50 group, f={f}, batch {B}, "
+                                  f"{'one model owner per GPU' if world > 1 else 'time-sliced on 1 GPU'}"
+                                  ", v1 -> v2 update mid-stream (BASELINE.json configs[3])",
+                      "model": "resnet50", "replicas": N, "f": f, "global_batch": B,
+                      "update_window_steps": [K // 3, 2 * K // 3],
+                      "certifications_per_request": round(certs / K, 3),
+                      "satisfied_fraction": sat,
+                      "parallelism": f"replica-parallel x{world}" if world > 1 else "1 GPU",
+                      "l2": "inputs larger than L2: 2 rotating 617 MB f64 batches"},
+           "clocks": clk.summary()}
+    for g in groups:
+        g.free()
+    return out
 
 
 # ------------------------------------------------------------- C5 sweep
@@ -518,11 +633,12 @@ def bench_reference(args, rank, world):
     if not Reference.available():
         return {"impl": "reference", "unavailable": "oracle/_ref/libcredo_ref.so not built"}
     R = Reference()
+    models = cpu_models(["resnet50"] * 3, sds)
     for _ in range(max(1, min(args.warmup, 1))):
-        cpu_path(["resnet50"] * 3, sds, encs[:2], batch.inputs[:2], digs, threads, R)
+        cpu_path(models, encs[:2], batch.inputs[:2], digs, threads, R)
     t = time.perf_counter()
     for _ in range(args.steps_ref):
-        cpu_path(["resnet50"] * 3, sds, encs, batch.inputs, digs, threads, R)
+        cpu_path(models, encs, batch.inputs, digs, threads, R)
     dt = time.perf_counter() - t
     v = args.steps_ref * S / dt
     return {"impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": UNIT,
@@ -539,12 +655,22 @@ def bench_reference(args, rank, world):
                     "d2h_bytes_per_step": 0}}
 
 
+_JSON_OUT = None
+
+
+def emit(obj):
+    f = _JSON_OUT or sys.stdout
+    f.write(json.dumps(obj) + "\n")
+    f.flush()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--batch", type=int, default=128)
+    ap.add_argument("--batch", type=int, default=None,
+                    help="requests per batch (default 128; 512 for --workload c4)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-sample", type=int, default=64,
                     help="requests in the bounded CPU-baseline sample (~10 s of CPU work)")
@@ -555,10 +681,12 @@ def main():
     ap.add_argument("--mode", default="group", choices=["group", "replica"],
                     help="group: a whole 3-replica group per GPU (weak scaling); "
                          "replica: one replica per GPU, NCCL all-gather (N>1)")
-    ap.add_argument("--workload", default="c2", choices=["c2", "c3", "c5"],
+    ap.add_argument("--workload", default="c2", choices=["c2", "c3", "c4", "c5"],
                     help="c2: the headline certified-request pipeline (3x ResNet-50); "
                          "c3: the heterogeneous 4-replica group; c5: agreement + "
                          "label-digest sweep (one line per --c5 spec)")
+    ap.add_argument("--replicas", type=int, default=8,
+                    help="--workload c4: group size on one GPU (N GPUs: N replicas)")
     ap.add_argument("--c5", default="1e6x8x1000,1e6x4x1000,1e6x8x10,1e5x8x1000,1e4x8x1000,"
                                     "1e3x8x1000",
                     help="comma list of RxNxV for --workload c5")
@@ -569,15 +697,21 @@ def main():
                     help="ncu mode: warmup + --steps plain steps, no report")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.batch is None:
+        args.batch = 512 if args.workload == "c4" else 128
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.mode == "replica" and world < 2:
         ap.error("--mode replica needs torchrun with >= 2 ranks")
+    # Native libraries (NCCL's version banner) may print to fd 1; route it to
+    # stderr while working so stdout carries exactly the JSON line(s).
+    json_fd = os.dup(1)
+    sys.stdout.flush()
+    os.dup2(2, 1)
+    global _JSON_OUT
+    _JSON_OUT = os.fdopen(json_fd, "w")
     if world > 1:
-        # NCCL writes its version banner to stdout at the default level; keep
-        # stdout to the one JSON line
-        os.environ.setdefault("NCCL_DEBUG_FILE", "/tmp/credo_nccl.%h.%p.log")
         import torch.distributed as dist
         if args.impl == "reference":
             if rank != 0:
@@ -588,14 +722,16 @@ def main():
             dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
     if args.impl == "reference":
         out = bench_reference(args, rank, world)
+    elif args.workload == "c4":
+        out = bench_c4(args, rank, world, local_rank)
     elif args.workload == "c5":
         for line in bench_c5(args, local_rank):
-            print(json.dumps(line), flush=True)
+            emit(line)
         return
     else:
         out = bench_gpu(args, rank, world, local_rank)
     if rank == 0 and out is not None:
-        print(json.dumps(out), flush=True)
+        emit(out)
     if world > 1 and args.impl != "reference":
         import torch.distributed as dist
         dist.destroy_process_group()
