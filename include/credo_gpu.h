@@ -185,6 +185,17 @@ int cg_certify_ticket(cg_group* g, uint64_t ticket, cg_certify_out* out);
 int cg_certify_outputs(cg_group* g, const cg_request_batch* batch,
                        const double* outputs, cg_certify_out* out);
 
+/* verify_request's digests for a batch (domain.cpp:177-216, :238-241):
+ * signing_digests[k] = InferenceRequest::signing_digest() = SHA-256(0x01 ||
+ * body), canonical_ids[k] = SHA-256(client_pub || 0x1F || nonce), and
+ * status[k] = 0 ok, 1 empty nonce, 2 empty input, 3 bad epsilon override,
+ * 4 request id != canonical id. verify_request's last step, Ed25519
+ * verify(client_pub, signing_digest, client_sig), stays on the host.
+ * Output pointers may be NULL. */
+int cg_request_digests(cg_ctx* ctx, const cg_request_batch* batch, const char* group_id,
+                       uint64_t group_id_len, uint8_t* signing_digests,
+                       uint8_t* canonical_ids, int8_t* status);
+
 /* ---- replica-parallel groups (one model owner's replica per GPU) ---------
  * The SURVEY §8(e) / north-star mapping: rank r of an NCCL communicator is
  * node r of the group and runs only replica r. Every rank ingests the same

@@ -244,6 +244,18 @@ class Context:
         self._check(L.cg_synth_outputs(self.h, seed, R, n, v, eps, shift_frac, vp(outs_ptr),
                                        vp(ids_ptr) if ids_ptr else None))
 
+    def request_digests(self, batch: "RequestBatch", group_id: bytes):
+        """verify_request's device part for a batch: (signing digests
+        SHA-256(0x01 || body), canonical ids, status 0 ok / 1 empty nonce /
+        2 empty input / 3 bad epsilon / 4 id mismatch)."""
+        cb, keep, B = ModelGroup._cbatch(batch)
+        sig = np.zeros((B, 32), np.uint8)
+        ids = np.zeros((B, 32), np.uint8)
+        st = np.zeros(B, np.int8)
+        self._check(self.L.cg_request_digests(self.h, C.byref(cb), group_id, u64(len(group_id)),
+                                              _p(sig), _p(ids), _p(st)))
+        return sig, ids, st
+
     def select_quorum(self, results: dict, n: int, f: int, metric: int,
                       epsilon: float):
         """distance::select_quorum(map<node, vector<double>>, n, f, m, eps)."""
@@ -425,7 +437,8 @@ class ModelGroup:
             self.ctx.L.cg_group_free(self.h)
             self.h = None
 
-    def _cbatch(self, b: RequestBatch):
+    @staticmethod
+    def _cbatch(b: RequestBatch):
         on_dev = not isinstance(b.inputs, np.ndarray)
         if on_dev:
             inputs_ptr, B, u = int(b.inputs), int(b.B), int(b.u)

@@ -15,6 +15,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cmath>
 #include <array>
 #include <atomic>
 #include <cstring>
@@ -1224,6 +1225,112 @@ void cg_group_free(cg_group* g) {
   cudaStreamSynchronize(g->ctx->stream);
   for (auto& s : g->slots) cudaStreamSynchronize(s->stream);
   delete g;
+}
+
+// verify_request's digests for a batch (domain.cpp:177-216): signing digest
+// SHA-256(0x01 || body) -- one 1.2 MB chain per ImageNet request, streamed
+// from the f64 input like the result leaves -- and canonical_request_id
+// SHA-256(pub || 0x1F || nonce), plus the structural checks. The Ed25519
+// check over the digest is the caller's (host) step.
+int cg_request_digests(cg_ctx* ctx, const cg_request_batch* bt, const char* group_id,
+                       uint64_t group_id_len, uint8_t* signing_digests, uint8_t* canonical_ids,
+                       int8_t* status) {
+  if (!ctx || !bt) return CG_EINVAL;
+  return guarded(ctx, [&] {
+    const uint32_t B = bt->B;
+    const uint64_t u = bt->u;
+    if (B == 0) return CG_OK;
+    cudaStream_t st = ctx->stream;
+    const double* d_in = bt->inputs;
+    if (!bt->inputs_on_device) {
+      ctx->d_f64.ensure((size_t)B * u);
+      CG_CUDA(cudaMemcpyAsync(ctx->d_f64.p, bt->inputs, 8 * (size_t)B * u,
+                              cudaMemcpyHostToDevice, st));
+      d_in = ctx->d_f64.p;
+    }
+    Arena ar;
+    struct L {
+      size_t h, t, id;
+      uint64_t lh, lt, lid;
+    };
+    std::vector<L> lay(B);
+    uint64_t nonce_pos = 0;
+    for (uint32_t k = 0; k < B; k++) {
+      const uint8_t* nonce = bt->nonces + nonce_pos;
+      const uint64_t nl = bt->nonce_lens[k];
+      nonce_pos += nl;
+      Enc H;  // kRequestSigTag || encode_request_body up to the input list
+      H.u8(0x01);
+      H.raw(bt->request_ids + 32 * k, 32);
+      H.bytes((const uint8_t*)group_id, group_id_len);
+      H.u32((uint32_t)u);
+      Enc T;
+      const bool he = bt->has_eps && bt->has_eps[k];
+      T.u8(he ? 1 : 0);
+      if (he) T.f64(bt->eps[k]);
+      T.raw(bt->client_pubs + 32 * k, 32);
+      T.bytes(nonce, nl);
+      Enc I;  // canonical_request_id preimage
+      I.raw(bt->client_pubs + 32 * k, 32);
+      I.u8(0x1F);
+      I.raw(nonce, nl);
+      L& l = lay[k];
+      l.lh = H.b.size();
+      l.lt = T.b.size();
+      l.lid = I.b.size();
+      l.h = ar.add(H.b.data(), l.lh, 0);
+      l.t = ar.add(T.b.data(), l.lt, l.lh + 8 * u);
+      l.id = ar.add(I.b.data(), l.lid, 0);
+      if (status) {
+        int8_t s8 = 0;
+        if (nl == 0) s8 = 1;
+        else if (u == 0) s8 = 2;
+        else if (he && !(bt->eps[k] >= 0.0 && std::isfinite(bt->eps[k]))) s8 = 3;
+        status[k] = s8;
+      }
+    }
+    ctx->d_bytes.ensure(ar.b.size() + 16);
+    ctx->d_out.ensure(64 * (size_t)B);
+    ctx->d_jobs.ensure(2 * (size_t)B);
+    std::vector<ChainJob> jobs(2 * (size_t)B);
+    const uint64_t A = (uint64_t)ctx->d_bytes.p;
+    for (uint32_t k = 0; k < B; k++) {
+      const L& l = lay[k];
+      ChainJob& j = jobs[k];
+      std::memset(&j, 0, sizeof j);
+      j.seg[0] = ChainSeg{A + l.h, 0, l.lh, kSegRaw, 0};
+      j.seg[1] = ChainSeg{(uint64_t)(d_in + u * k), l.lh, 8 * u, kSegF64, 0};
+      j.seg[2] = ChainSeg{A + l.t, l.lh + 8 * u, l.lt, kSegRaw, 0};
+      j.nseg = 3;
+      j.final_ = 1;
+      j.total_len = l.lh + 8 * u + l.lt;
+      j.blk_end = (j.total_len + 9 + 63) / 64;
+      j.digest_out = (uint64_t)(ctx->d_out.p + 32 * k);
+      ChainJob& c = jobs[B + k];
+      std::memset(&c, 0, sizeof c);
+      c.seg[0] = ChainSeg{A + l.id, 0, l.lid, kSegRaw, 0};
+      c.nseg = 1;
+      c.final_ = 1;
+      c.total_len = l.lid;
+      c.blk_end = (l.lid + 9 + 63) / 64;
+      c.digest_out = (uint64_t)(ctx->d_out.p + 32 * ((size_t)B + k));
+    }
+    CG_CUDA(cudaMemcpyAsync(ctx->d_bytes.p, ar.b.data(), ar.b.size(), cudaMemcpyHostToDevice, st));
+    CG_CUDA(cudaMemcpyAsync(ctx->d_jobs.p, jobs.data(), jobs.size() * sizeof(ChainJob),
+                            cudaMemcpyHostToDevice, st));
+    launch_chain_jobs(ctx->d_jobs.p, 2 * B, st);
+    std::vector<uint8_t> dig(64 * (size_t)B);
+    CG_CUDA(cudaMemcpyAsync(dig.data(), ctx->d_out.p, dig.size(), cudaMemcpyDeviceToHost, st));
+    CG_CUDA(cudaStreamSynchronize(st));
+    if (signing_digests) std::memcpy(signing_digests, dig.data(), 32 * (size_t)B);
+    if (canonical_ids) std::memcpy(canonical_ids, dig.data() + 32 * (size_t)B, 32 * (size_t)B);
+    if (status)
+      for (uint32_t k = 0; k < B; k++)
+        if (status[k] == 0 &&
+            std::memcmp(dig.data() + 32 * ((size_t)B + k), bt->request_ids + 32 * k, 32) != 0)
+          status[k] = 4;
+    return CG_OK;
+  });
 }
 
 int cg_ingest_batch(cg_group* g, const cg_request_batch* batch, uint64_t* ticket) {
