@@ -75,6 +75,21 @@ int cg_merkle_root_batch(cg_ctx* ctx, const uint8_t* leaf_hashes,
                          const uint64_t* n_leaves, uint64_t ntrees,
                          uint8_t* roots);
 
+/* merkle::Tree::auth_path (merkle.cpp:69-84) of `count` leaf indices in the
+ * tree over n precomputed leaf hashes; root (may be NULL) = Tree::root().
+ * Fixed-stride paths: siblings count x 64 x 32 bytes, sides count x 64
+ * (0 = Side::left, 1 = Side::right), lens count (steps, bottom level first).
+ * CG_EINVAL for n == 0 (Tree::build throws) or an index >= n
+ * (std::out_of_range). */
+int cg_merkle_auth_paths(cg_ctx* ctx, const uint8_t* leaf_hashes, uint64_t n,
+                         const uint64_t* indices, uint32_t count, uint8_t* siblings,
+                         uint8_t* sides, uint32_t* lens, uint8_t* root);
+/* merkle::get_merkle_root(path, leaf) (merkle.cpp:86-93) for count paths,
+ * each leaf given by its hash leaf_hash(leaf); same path layout. */
+int cg_merkle_path_roots(cg_ctx* ctx, const uint8_t* leaf_hashes, const uint8_t* siblings,
+                         const uint8_t* sides, const uint32_t* lens, uint32_t count,
+                         uint8_t* roots);
+
 /* ---- agreement ----------------------------------------------------------
  * R requests; outs is R × n × v row-major (request, node, lane); row (r, i)
  * is considered only when bit i of present[r] is set (present == NULL: all
@@ -195,6 +210,14 @@ int cg_certify_outputs(cg_group* g, const cg_request_batch* batch,
 int cg_request_digests(cg_ctx* ctx, const cg_request_batch* batch, const char* group_id,
                        uint64_t group_id_len, uint8_t* signing_digests,
                        uint8_t* canonical_ids, int8_t* status);
+
+/* Certificate assembly for the last certified batch (ProxyCore::
+ * assemble_response, proxy.cpp:80-186): auth paths in provider `tree`'s
+ * result tree (tree < N; leaf k = request k) or, tree == N, in the
+ * attestation tree (leaf i = manifest entry i). Same path layout as
+ * cg_merkle_auth_paths. */
+int cg_group_auth_paths(cg_group* g, uint32_t tree, const uint64_t* indices, uint32_t count,
+                        uint8_t* siblings, uint8_t* sides, uint32_t* lens);
 
 /* ---- replica-parallel groups (one model owner's replica per GPU) ---------
  * The SURVEY §8(e) / north-star mapping: rank r of an NCCL communicator is

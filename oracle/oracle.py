@@ -316,6 +316,25 @@ class Reference:
     def verify_request(self, enc: bytes) -> int:
         return self.L.ref_verify_request(enc, u64(len(enc)))
 
+    def auth_path(self, leaves: list[bytes], index: int):
+        """Tree::build(leaves).auth_path(index) -> [(sibling, side)]."""
+        lens = np.array([len(x) for x in leaves], np.uint64)
+        sib = C.create_string_buffer(32 * 64)
+        sides = C.create_string_buffer(64)
+        k = self.L.ref_auth_path(b"".join(leaves), _p(lens), u64(len(leaves)), u64(index),
+                                 sib, sides)
+        assert k >= 0
+        return [(sib.raw[32 * i:32 * i + 32], sides.raw[i]) for i in range(k)]
+
+    def path_root(self, leaf: bytes, path) -> bytes:
+        """merkle::get_merkle_root(path, leaf)."""
+        sib = b"".join(s for s, _ in path) or b"\0"
+        sides = bytes(d for _, d in path) or b"\0"
+        out = C.create_string_buffer(32)
+        assert self.L.ref_path_root(leaf, u64(len(leaf)), sib, sides, C.c_uint32(len(path)),
+                                    out) == 0
+        return out.raw
+
     def signing_digest(self, enc: bytes) -> bytes:
         out = C.create_string_buffer(32)
         assert self.L.ref_signing_digest(enc, u64(len(enc)), out) == 0

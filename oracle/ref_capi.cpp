@@ -117,6 +117,49 @@ int ref_merkle_root(const uint8_t* leaves, const uint64_t* lens, uint64_t n,
   }
 }
 
+// merkle::Tree::build(leaves).auth_path(index) (merkle.cpp:69-84): writes
+// up to 64 steps (sibling 32 B, side 0 left / 1 right); returns the step
+// count or -1.
+int ref_auth_path(const uint8_t* leaves, const uint64_t* lens, uint64_t n, uint64_t index,
+                  uint8_t* siblings, uint8_t* sides) {
+  try {
+    std::vector<Bytes> ls;
+    uint64_t off = 0;
+    for (uint64_t i = 0; i < n; i++) {
+      ls.emplace_back(leaves + off, leaves + off + lens[i]);
+      off += lens[i];
+    }
+    merkle::AuthPath p = merkle::Tree::build(ls).auth_path(index);
+    if (p.siblings.size() > 64) return -1;
+    for (size_t i = 0; i < p.siblings.size(); i++) {
+      std::memcpy(siblings + 32 * i, p.siblings[i].sibling.data.data(), 32);
+      sides[i] = p.siblings[i].side == merkle::Side::left ? 0 : 1;
+    }
+    return (int)p.siblings.size();
+  } catch (const std::exception&) {
+    return -1;
+  }
+}
+
+// merkle::get_merkle_root(path, leaf) (merkle.cpp:86-93).
+int ref_path_root(const uint8_t* leaf, uint64_t leaf_len, const uint8_t* siblings,
+                  const uint8_t* sides, uint32_t steps, uint8_t* root_out) {
+  try {
+    merkle::AuthPath p;
+    for (uint32_t i = 0; i < steps; i++) {
+      merkle::PathStep st;
+      std::memcpy(st.sibling.data.data(), siblings + 32 * i, 32);
+      st.side = sides[i] ? merkle::Side::right : merkle::Side::left;
+      p.siblings.push_back(st);
+    }
+    Hash32 r = merkle::get_merkle_root(p, ByteView(leaf, leaf_len));
+    std::memcpy(root_out, r.data.data(), 32);
+    return 0;
+  } catch (const std::exception&) {
+    return -1;
+  }
+}
+
 uint64_t ref_model_file_len(uint64_t in, uint64_t out) {
   return 8 + 8 + 1 + 4 + 8 * in * out + 4 + 8 * out;
 }

@@ -89,6 +89,24 @@ def _p(a):
     return C.c_void_p(a.ctypes.data) if a is not None else None
 
 
+def _unpack_paths(sib, sides, lens, count):
+    return [[(sib[t, k].tobytes(), int(sides[t, k])) for k in range(int(lens[t]))]
+            for t in range(count)]
+
+
+def _pack_paths(paths):
+    c = max(len(paths), 1)
+    sib = np.zeros((c, 64, 32), np.uint8)
+    sides = np.zeros((c, 64), np.uint8)
+    lens = np.zeros(c, np.uint32)
+    for t, p in enumerate(paths):
+        lens[t] = len(p)
+        for k, (s, d) in enumerate(p):
+            sib[t, k] = np.frombuffer(s, np.uint8)
+            sides[t, k] = d
+    return sib, sides, lens
+
+
 # ---------------------------------------------------------------- context
 class Context:
     """One context per process/GPU (cg_ctx)."""
@@ -183,6 +201,30 @@ class Context:
         self._check(self.L.cg_merkle_root_batch(self.h, buf, _p(n),
                                                 u64(len(trees)), out))
         return [out.raw[32 * i:32 * i + 32] for i in range(len(trees))]
+
+    def auth_paths(self, leaf_hashes: Sequence[bytes], indices):
+        """Tree::build over the leaf hashes; auth_path(i) for each index as
+        [(sibling, side)] (side 0 = left, 1 = right), plus the root."""
+        n = len(leaf_hashes)
+        idx = np.ascontiguousarray(indices, np.uint64)
+        c = len(idx)
+        sib = np.zeros((max(c, 1), 64, 32), np.uint8)
+        sides = np.zeros((max(c, 1), 64), np.uint8)
+        lens = np.zeros(max(c, 1), np.uint32)
+        root = np.zeros(32, np.uint8)
+        self._check(self.L.cg_merkle_auth_paths(self.h, b"".join(leaf_hashes) or b"\0", u64(n),
+                                                _p(idx), u32(c), _p(sib), _p(sides), _p(lens),
+                                                _p(root)))
+        return _unpack_paths(sib, sides, lens, c), root.tobytes()
+
+    def path_roots(self, leaf_hashes: Sequence[bytes], paths) -> list[bytes]:
+        """merkle::get_merkle_root for each (leaf hash, path)."""
+        sib, sides, lens = _pack_paths(paths)
+        out = np.zeros((max(len(paths), 1), 32), np.uint8)
+        self._check(self.L.cg_merkle_path_roots(self.h, b"".join(leaf_hashes) or b"\0",
+                                                _p(sib), _p(sides), _p(lens), u32(len(paths)),
+                                                _p(out)))
+        return [out[i].tobytes() for i in range(len(paths))]
 
     # -- agreement ----------------------------------------------------------
     def select_quorum_batch(self, outs: np.ndarray, n: int, f: int,
@@ -431,6 +473,18 @@ class ModelGroup:
         self.h = h
         self._keep = None
         return self
+
+    def auth_paths(self, tree: int, indices):
+        """Paths in provider `tree`'s result tree (tree < N) or the
+        attestation tree (tree == N) of the last certified batch."""
+        idx = np.ascontiguousarray(indices, np.uint64)
+        c = len(idx)
+        sib = np.zeros((max(c, 1), 64, 32), np.uint8)
+        sides = np.zeros((max(c, 1), 64), np.uint8)
+        lens = np.zeros(max(c, 1), np.uint32)
+        self.ctx._check(self.ctx.L.cg_group_auth_paths(self.h, u32(tree), _p(idx), u32(c),
+                                                       _p(sib), _p(sides), _p(lens)))
+        return _unpack_paths(sib, sides, lens, c)
 
     def free(self):
         if self.h:

@@ -1333,6 +1333,104 @@ int cg_request_digests(cg_ctx* ctx, const cg_request_batch* bt, const char* grou
   });
 }
 
+// ---------------------------------------------------- authentication paths
+namespace {
+void auth_paths_device(cg_ctx* ctx, const uint8_t* d_leaves, uint64_t n, const uint64_t* indices,
+                       uint32_t count, uint8_t* siblings, uint8_t* sides, uint32_t* lens,
+                       uint8_t* root) {
+  if (n == 0) throw InvalidArgument("merkle: empty leaf list");
+  for (uint32_t i = 0; i < count; i++)
+    if (indices[i] >= n) throw InvalidArgument("merkle: leaf index out of range");
+  cudaStream_t st = ctx->stream;
+  DevBuf<uint8_t> levels, sib, sd;
+  DevBuf<uint64_t> idx;
+  DevBuf<uint32_t> ln;
+  levels.ensure(32 * merkle_levels_nodes(n));
+  const auto off = launch_merkle_levels(d_leaves, n, levels.p, st);
+  idx.ensure(count);
+  sib.ensure((size_t)count * kMaxPathSteps * 32);
+  sd.ensure((size_t)count * kMaxPathSteps);
+  ln.ensure(count);
+  if (count) {
+    CG_CUDA(cudaMemcpyAsync(idx.p, indices, 8 * (size_t)count, cudaMemcpyHostToDevice, st));
+    launch_auth_paths(levels.p, off, n, idx.p, count, sib.p, sd.p, ln.p, st);
+    CG_CUDA(cudaMemcpyAsync(siblings, sib.p, (size_t)count * kMaxPathSteps * 32,
+                            cudaMemcpyDeviceToHost, st));
+    CG_CUDA(cudaMemcpyAsync(sides, sd.p, (size_t)count * kMaxPathSteps, cudaMemcpyDeviceToHost,
+                            st));
+    CG_CUDA(cudaMemcpyAsync(lens, ln.p, 4 * (size_t)count, cudaMemcpyDeviceToHost, st));
+  }
+  if (root)
+    CG_CUDA(cudaMemcpyAsync(root, levels.p + 32 * off.back(), 32, cudaMemcpyDeviceToHost, st));
+  CG_CUDA(cudaStreamSynchronize(st));
+}
+}  // namespace
+
+int cg_merkle_auth_paths(cg_ctx* ctx, const uint8_t* leaf_hashes, uint64_t n,
+                         const uint64_t* indices, uint32_t count, uint8_t* siblings,
+                         uint8_t* sides, uint32_t* lens, uint8_t* root) {
+  return guarded(ctx, [&] {
+    DevBuf<uint8_t> leaves;
+    leaves.ensure(32 * std::max<uint64_t>(n, 1));
+    CG_CUDA(cudaMemcpyAsync(leaves.p, leaf_hashes, 32 * n, cudaMemcpyHostToDevice, ctx->stream));
+    auth_paths_device(ctx, leaves.p, n, indices, count, siblings, sides, lens, root);
+    return CG_OK;
+  });
+}
+
+int cg_merkle_path_roots(cg_ctx* ctx, const uint8_t* leaf_hashes, const uint8_t* siblings,
+                         const uint8_t* sides, const uint32_t* lens, uint32_t count,
+                         uint8_t* roots) {
+  return guarded(ctx, [&] {
+    if (count == 0) return CG_OK;
+    for (uint32_t i = 0; i < count; i++)
+      if (lens[i] > (uint32_t)kMaxPathSteps) throw InvalidArgument("merkle: path too long");
+    cudaStream_t st = ctx->stream;
+    DevBuf<uint8_t> lh, sib, sd, out;
+    DevBuf<uint32_t> ln;
+    lh.ensure(32 * (size_t)count);
+    sib.ensure((size_t)count * kMaxPathSteps * 32);
+    sd.ensure((size_t)count * kMaxPathSteps);
+    ln.ensure(count);
+    out.ensure(32 * (size_t)count);
+    CG_CUDA(cudaMemcpyAsync(lh.p, leaf_hashes, 32 * (size_t)count, cudaMemcpyHostToDevice, st));
+    CG_CUDA(cudaMemcpyAsync(sib.p, siblings, (size_t)count * kMaxPathSteps * 32,
+                            cudaMemcpyHostToDevice, st));
+    CG_CUDA(cudaMemcpyAsync(sd.p, sides, (size_t)count * kMaxPathSteps, cudaMemcpyHostToDevice, st));
+    CG_CUDA(cudaMemcpyAsync(ln.p, lens, 4 * (size_t)count, cudaMemcpyHostToDevice, st));
+    launch_path_roots(lh.p, sib.p, sd.p, ln.p, count, out.p, st);
+    CG_CUDA(cudaMemcpyAsync(roots, out.p, 32 * (size_t)count, cudaMemcpyDeviceToHost, st));
+    CG_CUDA(cudaStreamSynchronize(st));
+    return CG_OK;
+  });
+}
+
+int cg_group_auth_paths(cg_group* g, uint32_t tree, const uint64_t* indices, uint32_t count,
+                        uint8_t* siblings, uint8_t* sides, uint32_t* lens) {
+  if (!g) return CG_EINVAL;
+  return guarded(g->ctx, [&] {
+    const uint32_t B = g->last_B, N = g->N;
+    if (B == 0) throw InvalidArgument("nothing certified yet");
+    if (tree > N) throw InvalidArgument("tree index out of range");
+    if (g->dist && tree < N && tree != g->rank)
+      throw InvalidArgument("replica-parallel group: only this rank's result tree is local");
+    const uint8_t* leaves;
+    uint64_t n;
+    if (tree < N) {  // provider `tree`'s R tree: its B result leaves
+      leaves = g->d_leaf.p + 32 * (uint64_t)tree * B;
+      n = B;
+    } else {  // the attestation tree, manifest order
+      uint32_t cnt = 0;
+      CG_CUDA(cudaMemcpyAsync(&cnt, g->d_count.p, 4, cudaMemcpyDeviceToHost, g->ctx->stream));
+      CG_CUDA(cudaStreamSynchronize(g->ctx->stream));
+      leaves = g->d_aleaf.p;
+      n = cnt;
+    }
+    auth_paths_device(g->ctx, leaves, n, indices, count, siblings, sides, lens, nullptr);
+    return CG_OK;
+  });
+}
+
 int cg_ingest_batch(cg_group* g, const cg_request_batch* batch, uint64_t* ticket) {
   if (!g || !batch || !ticket) return CG_EINVAL;
   return guarded(g->ctx, [&] {

@@ -5,6 +5,8 @@
 // Tree::build (proj/src/merkle.cpp:14-67), leaf constructions
 // (proj/src/messages.cpp:204-341).
 #include "digest.cuh"
+
+#include <vector>
 #include "sha256.cuh"
 
 namespace cg {
@@ -177,6 +179,118 @@ void launch_merkle_big(const uint8_t* d_leaves, uint64_t n, uint8_t* d_scratch,
     n = m;
   }
   launch_merkle_trees(in, nullptr, nullptr, nullptr, 1, n, d_root, st, n);
+}
+
+// ------------------------------------------------------ authentication paths
+// Tree::build's level arrays in global memory (level 0 = the leaf hashes),
+// then Tree::auth_path (merkle.cpp:69-84) for many indices at once, and
+// get_merkle_root (merkle.cpp:86-93) for many (leaf hash, path) pairs: one
+// thread per path, 2 compressions per step. kMaxPathSteps covers 2^64 leaves.
+std::vector<uint64_t> launch_merkle_levels(const uint8_t* d_leaves, uint64_t n,
+                                           uint8_t* d_levels, cudaStream_t st) {
+  if (n == 0) throw InvalidArgument("merkle: empty leaf list");
+  std::vector<uint64_t> off{0};
+  CG_CUDA(cudaMemcpyAsync(d_levels, d_leaves, 32 * n, cudaMemcpyDeviceToDevice, st));
+  uint64_t cur = 0;
+  while (n > 1) {
+    const uint64_t m = (n + 1) / 2;
+    merkle_level_kernel<<<(unsigned)ceil_div(m, 256), 256, 0, st>>>(d_levels + 32 * cur, n,
+                                                                      d_levels + 32 * (cur + n));
+    CG_CHECK_LAUNCH();
+    cur += n;
+    off.push_back(cur);
+    n = m;
+  }
+  return off;  // level l starts at node off[l]; the root is the last node
+}
+
+uint64_t merkle_levels_nodes(uint64_t n) {
+  uint64_t t = 0;
+  while (n > 1) {
+    t += n;
+    n = (n + 1) / 2;
+  }
+  return t + 1;
+}
+
+__global__ void auth_path_kernel(const uint8_t* __restrict__ levels, PathLevels lv,
+                                 const uint64_t* __restrict__ idx, uint32_t count,
+                                 uint8_t* __restrict__ sib, uint8_t* __restrict__ sides,
+                                 uint32_t* __restrict__ lens) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= count) return;
+  uint64_t i = idx[t];
+  uint32_t k = 0;
+  uint64_t n = lv.n;
+  for (int l = 0; l + 1 < lv.nlevels; l++) {
+    const uint8_t* level = levels + 32 * lv.off[l];
+    const uint8_t* s = nullptr;
+    uint8_t side = 0;
+    if (i & 1) {
+      s = level + 32 * (i - 1);
+      side = 0;  // Side::left
+    } else if (i + 1 < n) {
+      s = level + 32 * (i + 1);
+      side = 1;  // Side::right
+    }
+    if (s) {
+      const uint4* src = reinterpret_cast<const uint4*>(s);
+      uint4* dst = reinterpret_cast<uint4*>(sib + ((uint64_t)t * kMaxPathSteps + k) * 32);
+      dst[0] = src[0];
+      dst[1] = src[1];
+      sides[(uint64_t)t * kMaxPathSteps + k] = side;
+      k++;
+    }
+    i >>= 1;
+    n = (n + 1) / 2;
+  }
+  lens[t] = k;
+}
+
+__global__ void path_root_kernel(const uint8_t* __restrict__ leaf_hashes,
+                                 const uint8_t* __restrict__ sib,
+                                 const uint8_t* __restrict__ sides,
+                                 const uint32_t* __restrict__ lens, uint32_t count,
+                                 uint8_t* __restrict__ roots) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= count) return;
+  __align__(16) uint8_t h[32];
+  reinterpret_cast<uint4*>(h)[0] = reinterpret_cast<const uint4*>(leaf_hashes + 32ull * t)[0];
+  reinterpret_cast<uint4*>(h)[1] = reinterpret_cast<const uint4*>(leaf_hashes + 32ull * t)[1];
+  const uint32_t k = lens[t] < kMaxPathSteps ? lens[t] : kMaxPathSteps;
+  for (uint32_t s = 0; s < k; s++) {
+    const uint8_t* sb = sib + ((uint64_t)t * kMaxPathSteps + s) * 32;
+    __align__(16) uint8_t o[32];
+    if (sides[(uint64_t)t * kMaxPathSteps + s] == 0) sha256_internal_node(sb, h, o);
+    else sha256_internal_node(h, sb, o);
+    reinterpret_cast<uint4*>(h)[0] = reinterpret_cast<uint4*>(o)[0];
+    reinterpret_cast<uint4*>(h)[1] = reinterpret_cast<uint4*>(o)[1];
+  }
+  reinterpret_cast<uint4*>(roots + 32ull * t)[0] = reinterpret_cast<uint4*>(h)[0];
+  reinterpret_cast<uint4*>(roots + 32ull * t)[1] = reinterpret_cast<uint4*>(h)[1];
+}
+
+void launch_auth_paths(const uint8_t* d_levels, const std::vector<uint64_t>& off, uint64_t n,
+                       const uint64_t* d_idx, uint32_t count, uint8_t* d_sib, uint8_t* d_sides,
+                       uint32_t* d_lens, cudaStream_t st) {
+  if (count == 0) return;
+  PathLevels lv{};
+  lv.n = n;
+  lv.nlevels = (int)off.size();
+  if (lv.nlevels > kMaxPathSteps + 1) throw InvalidArgument("merkle: tree too deep");
+  for (size_t l = 0; l < off.size(); l++) lv.off[l] = off[l];
+  auth_path_kernel<<<(unsigned)ceil_div(count, 128), 128, 0, st>>>(d_levels, lv, d_idx, count,
+                                                                   d_sib, d_sides, d_lens);
+  CG_CHECK_LAUNCH();
+}
+
+void launch_path_roots(const uint8_t* d_leaf_hashes, const uint8_t* d_sib, const uint8_t* d_sides,
+                       const uint32_t* d_lens, uint32_t count, uint8_t* d_roots,
+                       cudaStream_t st) {
+  if (count == 0) return;
+  path_root_kernel<<<(unsigned)ceil_div(count, 128), 128, 0, st>>>(d_leaf_hashes, d_sib, d_sides,
+                                                                   d_lens, count, d_roots);
+  CG_CHECK_LAUNCH();
 }
 
 }  // namespace cg

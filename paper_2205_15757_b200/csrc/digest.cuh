@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <vector>
+
 #include "sha256.cuh"
 
 namespace cg {
@@ -19,5 +21,24 @@ void launch_merkle_trees(const uint8_t* d_leaves, const uint64_t* d_off,
 size_t merkle_big_scratch_bytes(uint64_t n);
 void launch_merkle_big(const uint8_t* d_leaves, uint64_t n, uint8_t* d_scratch,
                        uint8_t* d_root, cudaStream_t st);
+
+// Authentication paths (merkle.cpp:69-93). Paths are fixed-stride:
+// kMaxPathSteps slots of a 32-byte sibling, a side byte (0 = Side::left,
+// 1 = Side::right) per slot, and a step count.
+constexpr int kMaxPathSteps = 64;
+struct PathLevels {
+  uint64_t n;
+  int nlevels;
+  uint64_t off[kMaxPathSteps + 1];
+};
+uint64_t merkle_levels_nodes(uint64_t n);
+std::vector<uint64_t> launch_merkle_levels(const uint8_t* d_leaves, uint64_t n,
+                                           uint8_t* d_levels, cudaStream_t st);
+void launch_auth_paths(const uint8_t* d_levels, const std::vector<uint64_t>& off, uint64_t n,
+                       const uint64_t* d_idx, uint32_t count, uint8_t* d_sib, uint8_t* d_sides,
+                       uint32_t* d_lens, cudaStream_t st);
+void launch_path_roots(const uint8_t* d_leaf_hashes, const uint8_t* d_sib, const uint8_t* d_sides,
+                       const uint32_t* d_lens, uint32_t count, uint8_t* d_roots,
+                       cudaStream_t st);
 
 }  // namespace cg
