@@ -145,12 +145,34 @@ extern "C" int cg_dbg_gemm_trace(cg_ctx* ctx, int M, int N, int K, int BN, int r
   }
 }
 
+static int dbg_conv_gemm(cg_ctx* ctx, const uint16_t* A, int rowsA, const uint16_t* B, int N,
+                         int Kc, int ntaps, const int* tap_off, const float* bias,
+                         const uint16_t* residual, int relu, int row_mode, int H, int W, int M,
+                         int rows_out, int out_f32, int BN, void* out, int max_ctas, int halo_lo);
+
 extern "C" int cg_dbg_conv_gemm(cg_ctx* ctx, const uint16_t* A, int rowsA,
                                 const uint16_t* B, int N, int Kc, int ntaps,
                                 const int* tap_off, const float* bias,
                                 const uint16_t* residual, int relu, int row_mode,
                                 int H, int W, int M, int rows_out, int out_f32,
                                 int BN, void* out, int max_ctas) {
+  return dbg_conv_gemm(ctx, A, rowsA, B, N, Kc, ntaps, tap_off, bias, residual, relu, row_mode,
+                       H, W, M, rows_out, out_f32, BN, out, max_ctas, 0);
+}
+
+extern "C" int cg_dbg_conv_gemm_halo(cg_ctx* ctx, const uint16_t* A, int rowsA,
+                                     const uint16_t* B, int N, int Kc, int ntaps,
+                                     const int* tap_off, const float* bias, int relu,
+                                     int row_mode, int H, int W, int M, int rows_out, int BN,
+                                     void* out, int halo_lo) {
+  return dbg_conv_gemm(ctx, A, rowsA, B, N, Kc, ntaps, tap_off, bias, nullptr, relu, row_mode, H,
+                       W, M, rows_out, 0, BN, out, 0, halo_lo);
+}
+
+static int dbg_conv_gemm(cg_ctx* ctx, const uint16_t* A, int rowsA, const uint16_t* B, int N,
+                         int Kc, int ntaps, const int* tap_off, const float* bias,
+                         const uint16_t* residual, int relu, int row_mode, int H, int W, int M,
+                         int rows_out, int out_f32, int BN, void* out, int max_ctas, int halo_lo) {
   try {
     cudaStream_t st = (cudaStream_t)cg_ctx_stream(ctx);
     void *dA, *dB, *dbias, *dres = nullptr, *dout;
@@ -168,7 +190,7 @@ extern "C" int cg_dbg_conv_gemm(cg_ctx* ctx, const uint16_t* A, int rowsA,
       CG_CUDA(cudaMemcpy(dres, residual, (size_t)rows_out * N * 2, cudaMemcpyHostToDevice));
     }
     Operand oa, ob;
-    make_operand(oa, dA, rowsA, Kc, 128);
+    make_operand(oa, dA, rowsA, Kc, 128 + 2 * halo_lo);
     make_operand(ob, dB, N, ntaps * Kc, BN);
     ConvGemmArgs a{};
     a.M = M;
@@ -187,6 +209,7 @@ extern "C" int cg_dbg_conv_gemm(cg_ctx* ctx, const uint16_t* A, int rowsA,
     a.H = H;
     a.W = W;
     a.rows_out = rows_out;
+    a.halo_lo = halo_lo;
     launch_conv_gemm(oa, ob, a, BN, st, max_ctas);
     CG_CUDA(cudaStreamSynchronize(st));
     CG_CUDA(cudaMemcpy(out, dout, outsz, cudaMemcpyDeviceToHost));

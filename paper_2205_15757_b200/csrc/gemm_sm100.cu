@@ -10,6 +10,7 @@
 #include "common.cuh"
 #include "gemm_sm100.cuh"
 
+#include <cstdlib>
 #include <cstring>
 
 namespace cg {
@@ -19,6 +20,7 @@ namespace {
 constexpr int BM = 128, BK = 64, kThreads = 352;
 constexpr int kEpiWarps = 8, kStgLd = 36;        // staging row stride (floats)
 constexpr int A_BYTES = BM * BK * 2;
+constexpr int kHaloBytes = 256 * BK * 2;  // largest halo box (BM + 2*halo_lo <= 256 rows)
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -138,6 +140,15 @@ __device__ __forceinline__ uint64_t smem_desc_sw128(const void* p) {
   return ((addr >> 4) & 0x3FFFull) | (1ull << 16) | (64ull << 32) | (1ull << 46) |
          (2ull << 61);
 }
+// The same tile starting at an arbitrary 128-byte row of a TMA-written halo
+// (halo mode). Measured on B200: the UMMA read applies the 128B swizzle on
+// absolute smem address bits, exactly like the TMA write, so the start
+// address alone selects the row and the base-offset field [49,52) stays 0
+// (setting it to (addr >> 7) & 7 reads the wrong rows).
+__device__ __forceinline__ uint64_t smem_desc_sw128_row(uint32_t addr, int) {
+  return (((uint64_t)addr >> 4) & 0x3FFFull) | (1ull << 16) | (64ull << 32) | (1ull << 46) |
+         (2ull << 61);
+}
 // tcgen05.ld without the wait (the registers are valid after tmem_ld_wait).
 __device__ __forceinline__ void tmem_ld32_issue(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile(
@@ -243,7 +254,7 @@ __device__ __forceinline__ int remap_row(int M, int rows_out, int mode, int H,
       a.trace[(slot) * 64 + (i)] = clock64();                         \
   } while (0)
 
-template <int BN, int STAGES, int kResSlots>
+template <int BN, int STAGES, int kResSlots, int HALO, int RESB>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_gemm_kernel(const __grid_constant__ GemmGroupParams gp, const ConvGemmArgs a) {
   constexpr int B_BYTES = BN * BK * 2;
@@ -253,8 +264,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   // output staging (64B swizzle), then barriers.
   uint8_t* smem = smem_raw + ((1024 - (su32(smem_raw) & 1023)) & 1023);
   uint8_t* sA = smem;
-  uint8_t* sB = smem + STAGES * A_BYTES;
-  uint8_t* s_res = sB + STAGES * B_BYTES;  // kResSlots x [128 x 32] bf16 (SW64)
+  uint8_t* sB = smem + (HALO > 0 ? HALO * kHaloBytes : STAGES * A_BYTES);
+  uint8_t* s_res = sB + (RESB > STAGES ? RESB : STAGES) * B_BYTES;  // residual ring (SW64)
   float* s_epi = reinterpret_cast<float*>(s_res + kResSlots * 8192);  // 36 KB
   uint64_t* full = reinterpret_cast<uint64_t*>(s_epi + kEpiWarps * 32 * kStgLd);
   uint64_t* empty = full + STAGES;
@@ -262,7 +273,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tempty = tfull + 2;
   uint64_t* rfull = tempty + 2;
   uint64_t* rempty = rfull + (kResSlots > 0 ? kResSlots : 1);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rempty + (kResSlots > 0 ? kResSlots : 1));
+  uint64_t* hfull = rempty + (kResSlots > 0 ? kResSlots : 1);  // halo ring
+  uint64_t* hempty = hfull + (HALO > 0 ? HALO : 1);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(hempty + (HALO > 0 ? HALO : 1));
   int* s_tap = reinterpret_cast<int*>(tmem_slot + 4);
   // identity rows + bf16 out: thread-per-row epilogue, TMA bulk stores
   const bool tma_out = a.row_mode == kRowIdentity && !a.out_f32;
@@ -306,6 +319,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&rfull[s], 1);
       mbar_init(&rempty[s], 4);
     }
+    for (int s = 0; s < HALO; s++) {
+      mbar_init(&hfull[s], 1);
+      mbar_init(&hempty[s], 1);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -325,10 +342,48 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       int ti = 0;
+      int hs = 0;
+      uint32_t hphase = 0;
       for (int t = blockIdx.x; t < tiles; t += gridDim.x, ti++) {
         int r, m0, n0;
         coords(t, r, m0, n0);
         CG_TRACE(0, ti);
+        if constexpr (RESB > 0) {
+          // resident weights: this CTA's (replica, n block) never changes
+          // (grid % replicas == 0, one n block), so all RESB tiles of B are
+          // loaded once; per tile only the halo boxes stream
+          if (ti == 0) {
+            mbar_expect_tx(&full[0], RESB * B_BYTES);
+            for (int j = 0; j < RESB; j++)
+              tma_load_2d(&gp.B[r], &full[0], sB + j * B_BYTES, j * BK, n0);
+          }
+          const int hrows = BM + 2 * a.halo_lo;
+          for (int cb = 0; cb < kpt; cb++) {
+            mbar_wait(&hempty[hs], hphase ^ 1);
+            mbar_expect_tx(&hfull[hs], hrows * BK * 2);
+            tma_load_2d(&gp.A[r], &hfull[hs], sA + hs * kHaloBytes, cb * BK, m0 - a.halo_lo);
+            if (++hs == HALO) { hs = 0; hphase ^= 1; }
+          }
+          continue;
+        }
+        if constexpr (HALO > 0) {
+          // per channel block: one halo box, then the 9 taps' weight tiles
+          const int hrows = BM + 2 * a.halo_lo;
+          for (int cb = 0; cb < kpt; cb++) {
+            mbar_wait(&hempty[hs], hphase ^ 1);
+            mbar_expect_tx(&hfull[hs], hrows * BK * 2);
+            tma_load_2d(&gp.A[r], &hfull[hs], sA + hs * kHaloBytes, cb * BK, m0 - a.halo_lo);
+            if (++hs == HALO) { hs = 0; hphase ^= 1; }
+            for (int tap = 0; tap < a.ntaps; tap++) {
+              mbar_wait(&empty[stage], phase ^ 1);
+              mbar_expect_tx(&full[stage], B_BYTES);
+              tma_load_2d(&gp.B[r], &full[stage], sB + stage * B_BYTES, (tap * kpt + cb) * BK,
+                          n0);
+              if (++stage == STAGES) { stage = 0; phase ^= 1; }
+            }
+          }
+          continue;
+        }
         for (int kb = 0; kb < num_k; kb++) {
           const int tap = kb / kpt, cb = kb - tap * kpt;
           mbar_wait(&empty[stage], phase ^ 1);
@@ -346,20 +401,75 @@ __global__ void __launch_bounds__(kThreads, 1)
       // kind::f16 instruction descriptor: D f32, A/B bf16, K-major, M=128, N=BN
       const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) |
                              ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
-      int stage = 0, acc = 0;
-      uint32_t phase = 0, acc_phase = 0;
+      int stage = 0, acc = 0, hs = 0;
+      uint32_t phase = 0, acc_phase = 0, hphase = 0;
       int ti = 0;
       for (int t = blockIdx.x; t < tiles; t += gridDim.x, ti++) {
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         CG_TRACE(2, ti);
         tc_fence_after();
         const uint32_t d = tmem + acc * BN;
+        if constexpr (RESB > 0) {
+          if (ti == 0) {
+            mbar_wait(&full[0], 0);
+            tc_fence_after();
+          }
+          // 9 taps unrolled: tap offsets come from the kernel parameters and
+          // every descriptor is uniform arithmetic (no per-MMA register moves)
+          const uint32_t sA_u = su32(sA), sB_u = su32(sB);
+          for (int cb = 0; cb < kpt; cb++) {
+            mbar_wait(&hfull[hs], hphase);
+            tc_fence_after();
+            const uint32_t hbase = sA_u + (uint32_t)(hs * kHaloBytes + a.halo_lo * 128);
+#pragma unroll
+            for (int tap = 0; tap < 9; tap++) {
+              const uint64_t ad = smem_desc_sw128_row(hbase + (uint32_t)(a.tap_off[tap] * 128), 0);
+              const uint64_t bd =
+                  smem_desc_sw128_row(sB_u + (uint32_t)((tap * kpt + cb) * B_BYTES), 0);
+#pragma unroll
+              for (int k = 0; k < BK / 16; k++)
+                umma_bf16(d, ad + 2 * k, bd + 2 * k, idesc, (cb | tap | k) != 0);
+            }
+            umma_commit(&hempty[hs]);
+            if (++hs == HALO) { hs = 0; hphase ^= 1; }
+          }
+          umma_commit(&tfull[acc]);
+          if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+          continue;
+        }
+        if constexpr (HALO > 0) {
+          const uint32_t sA_u = su32(sA), sB_u = su32(sB);
+          for (int cb = 0; cb < kpt; cb++) {
+            mbar_wait(&hfull[hs], hphase);
+            tc_fence_after();
+            const uint32_t hbase = sA_u + (uint32_t)(hs * kHaloBytes + a.halo_lo * 128);
+#pragma unroll
+            for (int tap = 0; tap < 9; tap++) {
+              mbar_wait(&full[stage], phase);
+              tc_fence_after();
+              const uint64_t ad = smem_desc_sw128_row(hbase + (uint32_t)(a.tap_off[tap] * 128), 0);
+              const uint64_t bd = smem_desc_sw128_row(sB_u + (uint32_t)(stage * B_BYTES), 0);
+#pragma unroll
+              for (int k = 0; k < BK / 16; k++)
+                umma_bf16(d, ad + 2 * k, bd + 2 * k, idesc, (cb | tap | k) != 0);
+              umma_commit(&empty[stage]);
+              if (++stage == STAGES) { stage = 0; phase ^= 1; }
+            }
+            umma_commit(&hempty[hs]);
+            if (++hs == HALO) { hs = 0; hphase ^= 1; }
+          }
+          umma_commit(&tfull[acc]);
+          if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+          continue;
+        }
+        const uint64_t ad0 = smem_desc_sw128(sA), bd0 = smem_desc_sw128(sB);
         for (int kb = 0; kb < num_k; kb++) {
           mbar_wait(&full[stage], phase);
           if (kb == 0) CG_TRACE(3, ti);
           tc_fence_after();
-          const uint64_t ad = smem_desc_sw128(sA + stage * A_BYTES);
-          const uint64_t bd = smem_desc_sw128(sB + stage * B_BYTES);
+          // stage offsets added to the 14-bit start-address field (uniform adds)
+          const uint64_t ad = ad0 + (uint64_t)((stage * A_BYTES) >> 4);
+          const uint64_t bd = bd0 + (uint64_t)((stage * B_BYTES) >> 4);
 #pragma unroll
           for (int k = 0; k < BK / 16; k++)  // UMMA_K = 16 (32 bytes)
             umma_bf16(d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
@@ -583,19 +693,22 @@ EncodeFn get_encode() {
   return fn;
 }
 
-template <int BN, int STAGES, int kResSlots>
+template <int BN, int STAGES, int kResSlots, int HALO, int RESB>
 constexpr int smem_bytes() {
-  return 1024 + STAGES * (A_BYTES + BN * BK * 2) + kResSlots * 8192 + kEpiWarps * 32 * kStgLd * 4 +
-         8 * (2 * STAGES + 4 + 2 * (kResSlots > 0 ? kResSlots : 1)) + 16 + 48;
+  return 1024 + (HALO > 0 ? HALO * kHaloBytes : STAGES * A_BYTES) +
+         (RESB > STAGES ? RESB : STAGES) * BN * BK * 2 +
+         kResSlots * 8192 + kEpiWarps * 32 * kStgLd * 4 +
+         8 * (2 * STAGES + 4 + 2 * (kResSlots > 0 ? kResSlots : 1) + 2 * (HALO > 0 ? HALO : 1)) +
+         16 + 48;
 }
 
-template <int BN, int STAGES, int RS>
+template <int BN, int STAGES, int RS, int HALO = 0, int RESB = 0>
 void launch_t(const PreparedGemm& p, cudaStream_t st, int max_ctas) {
   static bool attr = false;
-  constexpr int smem = smem_bytes<BN, STAGES, RS>();
+  constexpr int smem = smem_bytes<BN, STAGES, RS, HALO, RESB>();
   static_assert(smem <= 232448, "smem budget");
   if (!attr) {
-    CG_CUDA(cudaFuncSetAttribute(conv_gemm_kernel<BN, STAGES, RS>,
+    CG_CUDA(cudaFuncSetAttribute(conv_gemm_kernel<BN, STAGES, RS, HALO, RESB>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr = true;
   }
@@ -604,8 +717,12 @@ void launch_t(const PreparedGemm& p, cudaStream_t st, int max_ctas) {
   const int budget = gemm_sm_budget();
   int grid = tiles < budget ? tiles : budget;
   if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
+  if (RESB > 0) {  // each CTA keeps one replica's weights: grid % replicas == 0
+    grid -= grid % p.gp.n;
+    if (grid < p.gp.n) throw InvalidArgument("conv_gemm: grid too small for resident weights");
+  }
   timer_begin(st, kTimeGemm);
-  conv_gemm_kernel<BN, STAGES, RS><<<grid, kThreads, smem, st>>>(p.gp, a);
+  conv_gemm_kernel<BN, STAGES, RS, HALO, RESB><<<grid, kThreads, smem, st>>>(p.gp, a);
   CG_CHECK_LAUNCH();
   timer_end(st, kTimeGemm);
 }
@@ -660,8 +777,13 @@ void prepare_conv_gemm(PreparedGemm& p, const ConvGemmGroup& g, const ConvGemmAr
   const bool tma_out = a.row_mode == kRowIdentity && !a.out_f32;
   std::memset(&p.gp, 0, sizeof p.gp);
   p.gp.n = g.n;
+  if (a.halo_lo < 0 || BM + 2 * a.halo_lo > 256) throw InvalidArgument("conv_gemm: halo too wide");
+  if (a.halo_lo > 0 && a.ntaps != 9) throw InvalidArgument("conv_gemm: halo needs 9 taps");
+  for (int t = 0; a.halo_lo > 0 && t < a.ntaps; t++)
+    if (a.tap_off[t] < -a.halo_lo || a.tap_off[t] > a.halo_lo)
+      throw InvalidArgument("conv_gemm: tap outside the halo");
   for (int r = 0; r < g.n; r++) {
-    if (g.A[r]->box_rows != BM || g.B[r]->box_rows != BN)
+    if (g.A[r]->box_rows != BM + 2 * a.halo_lo || g.B[r]->box_rows != BN)
       throw InvalidArgument("conv_gemm: box mismatch");
     if ((g.residual[r] != nullptr) != (g.residual[0] != nullptr))
       throw InvalidArgument("conv_gemm: residual on some replicas only");
@@ -689,8 +811,23 @@ void prepare_conv_gemm(PreparedGemm& p, const ConvGemmGroup& g, const ConvGemmAr
 }
 
 void launch_prepared(const PreparedGemm& p, cudaStream_t st, int max_ctas) {
+  if (p.args.halo_lo > 0) {
+    if (p.res) throw InvalidArgument("conv_gemm: halo mode has no residual ring");
+    // small weight sets (one n block, 9 x 64-channel taps): keep B resident
+    if (p.BN == 64 && p.args.N <= 64 && p.args.Kc == 64 && p.args.ntaps == 9 &&
+        std::getenv("CREDO_NO_RESB") == nullptr) {
+      launch_t<64, 1, 0, 3, 9>(p, st, max_ctas);
+      return;
+    }
+    switch (p.BN) {
+      case 64: launch_t<64, 8, 0, 3>(p, st, max_ctas); return;
+      case 128: launch_t<128, 6, 0, 2>(p, st, max_ctas); return;
+      case 256: launch_t<256, 3, 0, 2>(p, st, max_ctas); return;
+      default: throw InvalidArgument("conv_gemm: BN must be 64, 128 or 256");
+    }
+  }
   switch (p.BN * 2 + (p.res ? 1 : 0)) {
-    case 128: launch_t<64, 7, 0>(p, st, max_ctas); break;
+    case 128: launch_t<64, 7, 0>(p, st, max_ctas); break;  // (p.BN * 2 + residual)
     case 129: launch_t<64, 4, 10>(p, st, max_ctas); break;
     case 256: launch_t<128, 5, 0>(p, st, max_ctas); break;
     case 257: launch_t<128, 3, 10>(p, st, max_ctas); break;

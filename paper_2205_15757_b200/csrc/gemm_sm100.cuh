@@ -49,6 +49,12 @@ struct ConvGemmArgs {
   int H, W;                          // unpadded spatial dims (row remap)
   int rows_out;                      // valid output rows (identity mode)
   long long* trace;                  // debug: CTA-0 event timestamps or null
+  // Halo mode (3x3 taps = row shifts within [-halo_lo, +halo_lo]): per
+  // channel block ONE TMA box of BM + 2*halo_lo rows feeds all 9 taps from
+  // shared memory (each tap's MMA reads it at its row offset), instead of
+  // one BM-row box per tap. 0 = off. The A operand's box must then have
+  // BM + 2*halo_lo (<= 256) rows.
+  int halo_lo;
 };
 
 // One encoded operand (tensor map over a row-major bf16 [rows, cols] matrix

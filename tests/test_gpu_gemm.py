@@ -102,6 +102,43 @@ def test_conv3x3_padded_grid(ctx, NB, H, C, Cout, BN):
     close(got, ref)
 
 
+def run_halo(ctx, A, Bw, N, Kc, taps, bias, H, W, M, rows_out, BN, halo_lo):
+    a = bf16_bits(A)
+    b = bf16_bits(Bw)
+    t = np.array(list(taps), np.int32)
+    bias = np.ascontiguousarray(bias, np.float32)
+    out = np.zeros((rows_out, N), np.uint16)
+    rc = ctx.L.cg_dbg_conv_gemm_halo(
+        ctx.h, a.ctypes.data_as(C.c_void_p), A.shape[0], b.ctypes.data_as(C.c_void_p), N, Kc,
+        9, t.ctypes.data_as(C.c_void_p), bias.ctypes.data_as(C.c_void_p), 1, 1, H, W, M,
+        rows_out, BN, out.ctypes.data_as(C.c_void_p), halo_lo)
+    assert rc == 0, ctx.L.cg_last_error(ctx.h)
+    return torch.from_numpy(out.view(np.int16)).view(torch.bfloat16).float()
+
+
+@pytest.mark.parametrize("NB,H,C,Cout,BN", [(3, 7, 64, 128, 128), (2, 14, 128, 64, 64),
+                                            (2, 28, 64, 256, 256), (2, 56, 64, 64, 64)])
+def test_conv3x3_halo(ctx, NB, H, C, Cout, BN):
+    """Halo mode: one (128 + 2*(W+3))-row box per channel block feeds all 9
+    taps (MMA descriptors at arbitrary row offsets inside the 128B-swizzled
+    halo) == torch conv2d."""
+    W = H
+    g = torch.Generator().manual_seed(H * C + 1)
+    x = torch.rand(NB, C, H, W, generator=g) * 2 - 1
+    w = (torch.rand(Cout, C, 3, 3, generator=g) * 2 - 1) / 3
+    bias = torch.rand(Cout, generator=g) - 0.5
+    xp = torch.nn.functional.pad(q(x), (1, 1, 1, 1))
+    A = xp.permute(0, 2, 3, 1).reshape(-1, C)
+    Wp = W + 2
+    taps = [(dr - 1) * Wp + (ds - 1) for dr in range(3) for ds in range(3)]
+    Bw = q(w).permute(0, 2, 3, 1).reshape(Cout, 9 * C)
+    M = NB * (H + 2) * Wp
+    ref = torch.nn.functional.conv2d(q(x), q(w), bias, padding=1).clamp_min(0)
+    ref = ref.permute(0, 2, 3, 1).reshape(-1, Cout)
+    got = run_halo(ctx, A, Bw, Cout, C, taps, bias, H, W, M, NB * H * W, BN, Wp + 1)
+    close(got, ref)
+
+
 def test_compact_to_padded_interior(ctx):
     NB, H, C, Cout = 2, 7, 64, 64
     W, Wp = H, H + 2

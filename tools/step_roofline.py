@@ -1,0 +1,75 @@
+"""Per-launch roofline of the conv GEMM launches of one C2 step (3 replicas
+grouped per launch, batch B), from an ncu CSV of `-k regex:conv_gemm`
+launches with gpu__time_duration.sum, dram__bytes_read.sum and
+dram__bytes_write.sum. floor = max(FLOPs / peak, compulsory bytes / peak BW)
+with the measured peaks (MEASURED_PEAKS.json); launch order = csrc/cnn.cu
+ResNet::ops (conv1, per block c1, c2, [ds], c3, fc).
+
+  python tools/step_roofline.py <ncu.csv> [B] [replicas]
+"""
+import collections
+import csv
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SC = {'byte': 1, 'Kbyte': 1e3, 'Mbyte': 1e6, 'Gbyte': 1e9, 'ns': 1e-3, 'nsecond': 1e-3,
+      'us': 1, 'usecond': 1, 'ms': 1e3, 'msecond': 1e3}
+
+
+def plan(B, R, S=224):
+    L = []
+    px = lambda h: B * h * h  # noqa: E731
+    H1, H = S // 2, S // 4
+    L.append(("conv1 7x7/2", 2 * px(H1) * 64 * 147 * R, px(H1) * 192 * 2 + R * px(H1) * 64 * 2))
+    cin = 64
+    for stage, (w, n) in enumerate(((64, 3), (128, 4), (256, 6), (512, 3))):
+        for i in range(n):
+            s = 2 if (i == 0 and stage > 0) else 1
+            Ho, cout = H // s, 4 * w
+            L.append((f"l{stage + 1}.{i} c1 1x1 {cin}->{w}", 2 * px(H) * cin * w * R,
+                      R * (px(H) * cin * 2 + px(H) * w * 2)))
+            L.append((f"l{stage + 1}.{i} c2 3x3{'/2' if s == 2 else ''} {w}",
+                      2 * px(Ho) * 9 * w * w * R, R * (px(H) * w * 2 + px(Ho) * w * 2)))
+            if i == 0:
+                L.append((f"l{stage + 1}.{i} ds 1x1 {cin}->{cout}", 2 * px(Ho) * cin * cout * R,
+                          R * (px(Ho) * cin * 2 + px(Ho) * cout * 2)))
+            L.append((f"l{stage + 1}.{i} c3 1x1 {w}->{cout} +res", 2 * px(Ho) * w * cout * R,
+                      R * (px(Ho) * w * 2 + 2 * px(Ho) * cout * 2)))
+            H, cin = Ho, cout
+    L.append(("fc", 2 * B * cin * 1000 * R, R * (B * cin * 2 + B * 1000 * 4)))
+    return L
+
+
+def main():
+    path = sys.argv[1]
+    B = int(sys.argv[2]) if len(sys.argv) > 2 else 128
+    R = int(sys.argv[3]) if len(sys.argv) > 3 else 3
+    pk = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    bw, fl = pk["hbm_gbs"] * 1e9, pk.get("bf16_tflops_sustained", pk["bf16_tflops"]) * 1e12
+    rows = list(csv.reader(open(path)))
+    hi = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
+    ix = {h: i for i, h in enumerate(rows[hi])}
+    per = collections.OrderedDict()
+    for r in rows[hi + 1:]:
+        d = per.setdefault(int(r[ix["ID"]]), {})
+        d[r[ix["Metric Name"]]] = float(r[ix["Metric Value"]].replace(",", "")) * SC[r[ix["Metric Unit"]]]
+    P = plan(B, R)
+    print(f"{'launch':30s} {'us':>7s} {'floor':>7s} {'eff':>5s} {'TFLOP/s':>8s} "
+          f"{'DRAM TB/s':>9s} {'traffic/compulsory':>9s}")
+    T = F = 0.0
+    for (name, f, b), d in zip(P, per.values()):
+        t = d["gpu__time_duration.sum"]
+        traffic = d["dram__bytes_read.sum"] + d["dram__bytes_write.sum"]
+        floor = max(f / fl, b / bw) * 1e6
+        T += t
+        F += floor
+        print(f"{name:30s} {t:7.1f} {floor:7.1f} {floor / t:5.2f} {f / t / 1e6:8.1f} "
+              f"{traffic / t / 1e6:9.2f} {traffic / b:9.2f}")
+    print(f"{'TOTAL':30s} {T:7.1f} {F:7.1f} {F / T:5.2f}   (peaks: {fl / 1e12:.0f} TFLOP/s, "
+          f"{bw / 1e12:.2f} TB/s)")
+
+
+if __name__ == "__main__":
+    main()
