@@ -373,7 +373,7 @@ def bench_gpu(args, rank, world, local_rank):
                      f"batch {B}, 224x224; outputs + R roots all-gathered over NCCL",
             replicas=world, f=replica_f(world), global_batch=B,
             parallelism=f"replica-parallel x{world} (rank = provider)")
-    if rank == 0 and not args.no_cpu_baseline and not replica:
+    if world == 1 and not args.no_cpu_baseline:  # the CPU baseline is timed at N=1 only
         archs = [m.arch for m in models] if args.workload == "c3" else ["resnet50"] * 3
         out["cpu_baseline"] = cpu_baseline(archs, digs, sds, batches[0], args,
                                            grp.default_eps)

@@ -1118,6 +1118,7 @@ class Vgg16 final : public SeqNet {
           for (int ds = 0; ds < 3; ds++) taps[dr * 3 + ds] = (dr - 1) * Hp + (ds - 1);
         push_gemm(L, c, in, rows_pad, rows_pad, taps, nullptr, 0, out, c.cout, 0, 1,
                   pool_after_[i] ? kRowPadToCompact : kRowPadToPad, H, b * H * H);
+        if (kUseHalo && 128 + 2 * (Hp + 1) <= 256) L.back().g.halo_lo = Hp + 1;
       }
       if (pool_after_[i]) {
         const bf16* src = compact_[i];
