@@ -130,6 +130,32 @@ def make_hetero_group(ctx, B, seed=0, eps=C3_EPS):
     return grp, models, files, digs, sds
 
 
+def resnet50_gemm_plan(B, R, S=224):
+    """(name, FLOPs, compulsory HBM bytes) of each conv GEMM launch of one
+    grouped ResNet-50 forward over R replicas, in csrc/cnn.cu ResNet::ops
+    order (conv1, per block c1, c2, [ds], c3, fc); same model as
+    tools/step_roofline.py."""
+    L = []
+    px = lambda h: B * h * h  # noqa: E731
+    H1, H = S // 2, S // 4
+    L.append(("conv1", 2 * px(H1) * 64 * 147 * R, px(H1) * 192 * 2 + R * px(H1) * 64 * 2))
+    cin = 64
+    for stage, (w, n) in enumerate(((64, 3), (128, 4), (256, 6), (512, 3))):
+        for i in range(n):
+            s = 2 if (i == 0 and stage > 0) else 1
+            Ho, cout = H // s, 4 * w
+            L.append(("c1", 2 * px(H) * cin * w * R, R * (px(H) * cin * 2 + px(H) * w * 2)))
+            L.append(("c2", 2 * px(Ho) * 9 * w * w * R, R * (px(H) * w * 2 + px(Ho) * w * 2)))
+            if i == 0:
+                L.append(("ds", 2 * px(Ho) * cin * cout * R,
+                          R * (px(Ho) * cin * 2 + px(Ho) * cout * 2)))
+            L.append(("c3", 2 * px(Ho) * w * cout * R,
+                      R * (px(Ho) * w * 2 + 2 * px(Ho) * cout * 2)))
+            H, cin = Ho, cout
+    L.append(("fc", 2 * B * cin * 1000 * R, R * (B * cin * 2 + B * 1000 * 4)))
+    return L
+
+
 def replica_f(world):
     return (world - 1) // 2  # quorum of a strict majority
 
@@ -242,10 +268,10 @@ def bench_gpu(args, rank, world, local_rank):
     # batch and ingests one future batch.
     from collections import deque
     D = args.depth
-    l0 = ctx.launch_count()
     pend = deque(grp.ingest(dev_batches[j % nb]) for j in range(D))
     barrier()
     torch.cuda.synchronize()
+    l0 = ctx.launch_count()  # kernels launched inside the timed region only
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local_rank) as clk:
         e0.record(stream)
@@ -256,7 +282,7 @@ def bench_gpu(args, rank, world, local_rank):
         host_ms = 1e3 * (time.perf_counter() - h0) / args.steps
         e1.record(stream)
         torch.cuda.synchronize()
-    launches = (ctx.launch_count() - l0) // (args.steps + D)
+    launches = round((ctx.launch_count() - l0) / args.steps)
     ms = max_over_ranks(e0.elapsed_time(e1))
     res = grp.fetch()
     sat_dev = float(np.mean(res["satisfied"]))
@@ -300,6 +326,24 @@ def bench_gpu(args, rank, world, local_rank):
     L.cg_timing_read(0, ctypes.byref(tg), ctypes.byref(ng))
     tc, nc = ctypes.c_double(), ctypes.c_uint64()
     L.cg_timing_read(1, ctypes.byref(tc), ctypes.byref(nc))
+    # per-launch GEMM times -> efficiency against each layer's own roofline
+    # floor max(FLOPs / tensor peak, compulsory bytes / HBM peak)
+    spans = (ctypes.c_double * int(ng.value))()
+    cnt = ctypes.c_uint64()
+    L.cg_timing_spans.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_uint64,
+                                  ctypes.POINTER(ctypes.c_uint64)]
+    L.cg_timing_spans(0, spans, ng.value, ctypes.byref(cnt))
+    floor_eff = None
+    if args.workload == "c2" and not replica:
+        plan = resnet50_gemm_plan(B, len(models))
+        if len(plan) and cnt.value == len(plan) * args.steps:
+            pk0, _ = peaks()
+            fl = pk0.get("bf16_tflops_sustained", pk0["bf16_tflops"]) * 1e12
+            bw = pk0.get("hbm_gbs", 6650.0) * 1e9
+            floors = sum(max(f / fl, b / bw) for _, f, b in plan) * args.steps * 1e3
+            floor_eff = {"frac": round(floors / sum(spans), 4),
+                         "floor_ms_per_step": round(floors / args.steps, 3),
+                         "compulsory_bytes_per_step": int(sum(b for _, _, b in plan))}
     breakdown = {}
     for cls, name in ((2, "agree_trees_ms"), (3, "aux_ms"), (4, "nccl_ms")):
         t, n = ctypes.c_double(), ctypes.c_uint64()
@@ -334,7 +378,8 @@ def bench_gpu(args, rank, world, local_rank):
                 "gemm_launches_per_step": int(ng.value) // args.steps,
                 "share_of_step": round(gemm_ms_step / (ms / args.steps), 3),
                 "sha_chain_ms_per_step_overlapped": round(chain_ms_step, 3),
-                "other_ms_per_step": breakdown}
+                "other_ms_per_step": breakdown,
+                "per_layer_floor": floor_eff}
 
     out = {"metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup,
@@ -672,8 +717,8 @@ def main():
     ap.add_argument("--batch", type=int, default=None,
                     help="requests per batch (default 128; 512 for --workload c4)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cpu-sample", type=int, default=64,
-                    help="requests in the bounded CPU-baseline sample (~10 s of CPU work)")
+    ap.add_argument("--cpu-sample", type=int, default=256,
+                    help="requests in the bounded CPU-baseline sample (~10-30 s of CPU work)")
     ap.add_argument("--steps-ref", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--depth", type=int, default=12,

@@ -242,6 +242,8 @@ int cg_group_create_dist(cg_ctx* ctx, cg_model* my_model, const uint8_t* all_dig
  * auxiliary kernels, 4 NCCL exchange). Enabling resets the counters. */
 void cg_timing_enable(int on);
 int cg_timing_read(int cls, double* total_ms, uint64_t* launches);
+/* The individual launch durations of a class in launch order (up to cap). */
+int cg_timing_spans(int cls, double* ms_out, uint64_t cap, uint64_t* count);
 /* Algorithmic FLOPs of one forward of one input (2 x MACs). */
 double cg_model_flops_per_input(const cg_model* m);
 /* C5 synthetic sweep input, generated on the device: per

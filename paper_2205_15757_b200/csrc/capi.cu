@@ -391,6 +391,22 @@ int cg_timing_read(int cls, double* total_ms, uint64_t* launches) {
   return CG_OK;
 }
 
+int cg_timing_spans(int cls, double* ms_out, uint64_t cap, uint64_t* count) {
+  if (cls < 0 || cls >= kTimeClasses) return CG_EINVAL;
+  std::lock_guard<std::mutex> lk(g_timers.mu);
+  const auto& sp = g_timers.spans[cls];
+  for (size_t i = 0; i < sp.size() && i < cap; i++) {
+    if (cudaEventSynchronize(g_timers.pool[sp[i].second]) != cudaSuccess) return CG_ECUDA;
+    float ms = 0;
+    if (cudaEventElapsedTime(&ms, g_timers.pool[sp[i].first], g_timers.pool[sp[i].second]) !=
+        cudaSuccess)
+      return CG_ECUDA;
+    ms_out[i] = ms;
+  }
+  if (count) *count = sp.size();
+  return CG_OK;
+}
+
 double cg_model_flops_per_input(const cg_model* m) {
   if (!m) return 0;
   if (m->kind == 1) return m->cnn->flops_per_image();
