@@ -672,23 +672,25 @@ def bench_reference(args, rank, world):
     threads = os.cpu_count() or 1
     sds = resnet_state_dicts("resnet50", 3, seed=0, jitter=5e-3)
     digs = [hashlib.sha256(cnn_model_file("resnet50", sd, U, 1000, True)).digest() for sd in sds]
-    S = args.cpu_sample
+    # K steps of a bounded sample each, so the whole run stays within a few
+    # minutes whatever --steps is: about 2 x cpu_sample requests in total
+    K = max(1, args.steps)
+    S = max(4, (2 * args.cpu_sample) // K)
     batch = signed_requests(S, U, seed=0)
     encs = [encode_request(batch, k) for k in range(S)]
     if not Reference.available():
         return {"impl": "reference", "unavailable": "oracle/_ref/libcredo_ref.so not built"}
     R = Reference()
     models = cpu_models(["resnet50"] * 3, sds)
-    for _ in range(max(1, min(args.warmup, 1))):
-        cpu_path(models, encs[:2], batch.inputs[:2], digs, threads, R)
+    cpu_path(models, encs[:2], batch.inputs[:2], digs, threads, R)  # one small warm-up
     t = time.perf_counter()
-    for _ in range(args.steps_ref):
+    for _ in range(K):
         cpu_path(models, encs, batch.inputs, digs, threads, R)
     dt = time.perf_counter() - t
-    v = args.steps_ref * S / dt
+    v = K * S / dt
     return {"impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": UNIT,
-            "n_gpus": world, "steps": args.steps_ref, "warmup": 1,
-            "ms_per_step": round(1e3 * dt / args.steps_ref, 1), "higher_is_better": True,
+            "n_gpus": world, "steps": K, "warmup": 1,
+            "ms_per_step": round(1e3 * dt / K, 1), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32 forward / f64 agreement",
             "data": "synthetic", "config": {"workload": "C2 sample", "batch_per_step": S,
                                             "model": "resnet50", "replicas": 3, "f": 1},
@@ -719,7 +721,6 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-sample", type=int, default=256,
                     help="requests in the bounded CPU-baseline sample (~10-30 s of CPU work)")
-    ap.add_argument("--steps-ref", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--depth", type=int, default=12,
                     help="batches ingested ahead of certification (ring holds 16)")
