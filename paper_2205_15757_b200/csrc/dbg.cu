@@ -83,6 +83,68 @@ extern "C" int cg_dbg_sha_bench(cg_ctx* ctx, int mode, uint64_t nblocks,
   }
 }
 
+// Timing + CTA-0 event trace of one halo-mode 3x3 conv (B images of H x H,
+// C -> N channels) over a padded grid of device-resident operands.
+extern "C" int cg_dbg_halo_trace(cg_ctx* ctx, int B, int H, int C, int N, int BN,
+                                 long long* trace_host, double* us) {
+  try {
+    cudaStream_t st = (cudaStream_t)cg_ctx_stream(ctx);
+    const int Hp = H + 2, rows = B * Hp * Hp;
+    void *dA, *dB, *dbias, *dout;
+    long long* dtr;
+    CG_CUDA(cudaMalloc(&dA, (size_t)rows * C * 2));
+    CG_CUDA(cudaMalloc(&dB, (size_t)N * 9 * C * 2));
+    CG_CUDA(cudaMalloc(&dbias, (size_t)N * 4));
+    CG_CUDA(cudaMalloc(&dout, (size_t)B * H * H * N * 2));
+    CG_CUDA(cudaMalloc(&dtr, 8 * 64 * 8));
+    CG_CUDA(cudaMemset(dA, 0x11, (size_t)rows * C * 2));
+    CG_CUDA(cudaMemset(dB, 0x11, (size_t)N * 9 * C * 2));
+    CG_CUDA(cudaMemset(dbias, 0, (size_t)N * 4));
+    CG_CUDA(cudaMemset(dtr, 0, 8 * 64 * 8));
+    Operand oa, ob;
+    make_operand(oa, dA, rows, C, 128 + 2 * (Hp + 1));
+    make_operand(ob, dB, N, 9 * C, BN);
+    ConvGemmArgs a{};
+    a.M = rows;
+    a.N = N;
+    a.Kc = C;
+    a.ntaps = 9;
+    for (int dr = 0; dr < 3; dr++)
+      for (int ds = 0; ds < 3; ds++) a.tap_off[dr * 3 + ds] = (dr - 1) * Hp + (ds - 1);
+    a.bias = (const float*)dbias;
+    a.out = dout;
+    a.ld_out = N;
+    a.relu = 1;
+    a.row_mode = kRowPadToCompact;
+    a.H = H;
+    a.W = H;
+    a.rows_out = B * H * H;
+    a.halo_lo = Hp + 1;
+    launch_conv_gemm(oa, ob, a, BN, st);  // warm
+    cudaEvent_t e0, e1;
+    CG_CUDA(cudaEventCreate(&e0));
+    CG_CUDA(cudaEventCreate(&e1));
+    CG_CUDA(cudaEventRecord(e0, st));
+    for (int i = 0; i < 5; i++) launch_conv_gemm(oa, ob, a, BN, st);
+    CG_CUDA(cudaEventRecord(e1, st));
+    a.trace = dtr;
+    launch_conv_gemm(oa, ob, a, BN, st);
+    CG_CUDA(cudaStreamSynchronize(st));
+    float ms = 0;
+    CG_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    *us = 1000.0 * ms / 5;
+    CG_CUDA(cudaMemcpy(trace_host, dtr, 8 * 64 * 8, cudaMemcpyDeviceToHost));
+    cudaFree(dA);
+    cudaFree(dB);
+    cudaFree(dbias);
+    cudaFree(dout);
+    cudaFree(dtr);
+    return CG_OK;
+  } catch (const std::exception&) {
+    return CG_ECUDA;
+  }
+}
+
 // Timing + CTA-0 event trace of one 1x1 conv GEMM shape on device-resident
 // random operands (no host copies in the timed launch).
 extern "C" int cg_dbg_gemm_trace(cg_ctx* ctx, int M, int N, int K, int BN, int residual,

@@ -419,6 +419,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t sA_u = su32(sA), sB_u = su32(sB);
           for (int cb = 0; cb < kpt; cb++) {
             mbar_wait(&hfull[hs], hphase);
+            if (cb == 0) CG_TRACE(3, ti);
             tc_fence_after();
             const uint32_t hbase = sA_u + (uint32_t)(hs * kHaloBytes + a.halo_lo * 128);
 #pragma unroll
@@ -434,6 +435,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (++hs == HALO) { hs = 0; hphase ^= 1; }
           }
           umma_commit(&tfull[acc]);
+          CG_TRACE(4, ti);
           if (++acc == 2) { acc = 0; acc_phase ^= 1; }
           continue;
         }
