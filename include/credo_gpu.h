@@ -57,6 +57,10 @@ const char* cg_last_error(const cg_ctx* ctx);
 int cg_ctx_set_stream(cg_ctx* ctx, void* stream);
 void* cg_ctx_stream(cg_ctx* ctx);
 int cg_ctx_synchronize(cg_ctx* ctx);
+/* Makes the context stream wait for every certification tail enqueued so
+ * far (tails run on an internal stream, overlapping the next forwards). */
+int cg_ctx_join(cg_ctx* ctx);
+
 /* Number of kernels this library has launched on the context so far. */
 uint64_t cg_ctx_launch_count(const cg_ctx* ctx);
 
@@ -187,11 +191,15 @@ typedef struct {
 int cg_certify_batch(cg_group* g, const cg_request_batch* batch,
                      cg_certify_out* out);
 int cg_group_fetch(cg_group* g, cg_certify_out* out);
+/* Results of a certified ticket whose ingest slot has not been reused yet
+ * (the ring holds 16 batches), e.g. to read batch i back while batch i+1's
+ * forwards run. */
+int cg_group_fetch_ticket(cg_group* g, uint64_t ticket, cg_certify_out* out);
 /* The same path split at the reference's own seam: ingest = the hot part of
  * InferenceEngine::submit (src/engine.cpp:182-209) — framing bytes, upload,
  * and the request-midstate SHA-256 chains started on a per-batch stream —
  * and certify = execute_batch + R trees + try_attest for that ticket. Up to
- * 8 batches may be ingested ahead; tickets are certified in any order. */
+ * 16 batches may be ingested ahead; tickets are certified in any order. */
 int cg_ingest_batch(cg_group* g, const cg_request_batch* batch, uint64_t* ticket);
 int cg_certify_ticket(cg_group* g, uint64_t ticket, cg_certify_out* out);
 /* Agreement + digest path over precomputed replica outputs (host memory,

@@ -150,6 +150,10 @@ class Context:
     def synchronize(self):
         self._check(self.L.cg_ctx_synchronize(self.h))
 
+    def join(self):
+        """The context stream waits for all certification tails so far."""
+        self._check(self.L.cg_ctx_join(self.h))
+
     @staticmethod
     def nccl_unique_id() -> bytes:
         buf = C.create_string_buffer(128)
@@ -544,6 +548,10 @@ class ModelGroup:
                        want_leaves=False):
         keep, B = self._inflight.pop(ticket)
         self._lastB = B
+        self._doneB = getattr(self, "_doneB", {})
+        self._doneB[ticket] = B
+        if len(self._doneB) > 64:
+            self._doneB.pop(next(iter(self._doneB)))
         if not sync:
             self.ctx._check(self.ctx.L.cg_certify_ticket(self.h, C.c_uint64(ticket), None))
             self._keep = keep
@@ -561,9 +569,15 @@ class ModelGroup:
         self._lastB = B
         return self.fetch(False, want_leaves, _enqueue=(cb,), _outputs=o)
 
+    def fetch_ticket(self, ticket: int, want_outputs=False, want_leaves=False):
+        """Results of an already certified ticket (its slot not yet reused),
+        e.g. batch i read back while batch i+1's forwards run."""
+        return self.fetch(want_outputs, want_leaves, _fetch_ticket=ticket)
+
     def fetch(self, want_outputs=False, want_leaves=False, _enqueue=None,
-              _outputs=None, _ticket=None):
-        B, N, v, k = self._lastB, self.N, self.v, self.topk
+              _outputs=None, _ticket=None, _fetch_ticket=None):
+        B = self._lastB if _fetch_ticket is None else self._doneB[_fetch_ticket]
+        N, v, k = self.N, self.v, self.topk
         amax = N * B + B + N
         r = dict(selected=np.zeros(B, np.uint32), diameter=np.zeros(B),
                  satisfied=np.zeros(B, np.uint8), label=np.zeros(B, np.int64),
@@ -588,6 +602,8 @@ class ModelGroup:
                                                _p(_outputs), C.byref(o))
         elif _enqueue is not None:
             rc = self.ctx.L.cg_certify_batch(self.h, C.byref(_enqueue[0]), C.byref(o))
+        elif _fetch_ticket is not None:
+            rc = self.ctx.L.cg_group_fetch_ticket(self.h, C.c_uint64(_fetch_ticket), C.byref(o))
         else:
             rc = self.ctx.L.cg_group_fetch(self.h, C.byref(o))
         self.ctx._check(rc)

@@ -180,6 +180,10 @@ struct cg_ctx {
   // replica-parallel groups: one NCCL communicator over the ranks (one per GPU)
   ncclComm_t comm = nullptr;
   int rank = 0, nranks = 1;
+  // certification tails (result leaves, agreement, trees) of every group of
+  // this context, in issue order: they overlap the next batch's forwards,
+  // and one stream keeps the NCCL exchanges in the same order on all ranks
+  cudaStream_t tail = nullptr;
 };
 
 struct cg_model {
@@ -312,6 +316,7 @@ void cg_ctx_destroy(cg_ctx* ctx) {
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
   if (ctx->side) cudaStreamDestroy(ctx->side);
+  if (ctx->tail) cudaStreamDestroy(ctx->tail);
   if (ctx->ev_a) cudaEventDestroy(ctx->ev_a);
   if (ctx->ev_b) cudaEventDestroy(ctx->ev_b);
   delete ctx;
@@ -334,6 +339,17 @@ int cg_ctx_synchronize(cg_ctx* ctx) {
   return guarded(ctx, [&] {
     CG_CUDA(cudaStreamSynchronize(ctx->stream));
     CG_CUDA(cudaStreamSynchronize(ctx->side));
+    if (ctx->tail) CG_CUDA(cudaStreamSynchronize(ctx->tail));
+    return CG_OK;
+  });
+}
+
+int cg_ctx_join(cg_ctx* ctx) {
+  return guarded(ctx, [&] {
+    if (ctx->tail) {
+      CG_CUDA(cudaEventRecord(ctx->ev_a, ctx->tail));
+      CG_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_a, 0));
+    }
     return CG_OK;
   });
 }
@@ -749,10 +765,24 @@ extern "C" int cg_dbg_forward_bench(cg_ctx* ctx, cg_model* m, uint32_t B, int it
 // midstates and (for host inputs) its device copy of the inputs. Ingest runs
 // on the slot's own stream so the prefix chains of several batches proceed
 // concurrently with each other and with the replica forwards.
+// A certified batch's device results; they live in the batch's ingest slot
+// until the slot is reused (ring depth later), so the tail of batch i can
+// run while batch i+1's forwards write their own slot.
+struct BatchResults {
+  DevBuf<double> d_outs, d_topv, d_diam;
+  DevBuf<uint32_t> d_topi, d_sel, d_mnodes, d_mops, d_count;
+  DevBuf<uint8_t> d_leaf, d_rroots, d_aleaf, d_aroot, d_sat, d_kinds;
+  DevBuf<int8_t> d_status;
+  DevBuf<int64_t> d_label;
+  DevBuf<int32_t> d_single_pos;
+};
+
 struct IngestSlot {
-  bool used = false, ever = false;
+  bool used = false, ever = false, certified = false;
   uint64_t ticket = 0;
   uint32_t B = 0;
+  BatchResults res;
+  cudaEvent_t ev_fwd = nullptr;  // replica outputs written (main stream)
   const double* d_in_ptr = nullptr;
   DevBuf<double> d_in, d_eps;
   DevBuf<uint8_t> d_arena, d_reqids;
@@ -770,6 +800,7 @@ struct IngestSlot {
     if (ev_staged) cudaEventDestroy(ev_staged);
     if (ev_prefix) cudaEventDestroy(ev_prefix);
     if (ev_done) cudaEventDestroy(ev_done);
+    if (ev_fwd) cudaEventDestroy(ev_fwd);
   }
 };
 
@@ -784,15 +815,12 @@ struct cg_group {
   std::string gid;
   uint64_t version = 0;
   uint64_t u = 0, v = 0;
-  // per-batch results, written on the main stream by certify
-  DevBuf<double> d_pre64, d_outs, d_topv, d_diam;
+  // forward scratch (main stream); per-batch results live in the slots
+  DevBuf<double> d_pre64;
   DevBuf<float> d_pre32;
-  DevBuf<uint32_t> d_topi, d_sel, d_mnodes, d_mops, d_count;
-  DevBuf<uint8_t> d_leaf, d_rroots, d_aleaf, d_aroot, d_sat, d_kinds, d_gid;
-  DevBuf<int8_t> d_status;
-  DevBuf<int64_t> d_label;
-  DevBuf<int32_t> d_single_pos;
+  DevBuf<uint8_t> d_gid;
   DevBuf<uint8_t> d_prep;  // shared CNN input operand
+  IngestSlot* last = nullptr;  // the last certified batch (fetch, paths)
   bool all_cnn = false, same_prep = false;
   bool group_plan_ok = std::getenv("CREDO_NO_GROUP") == nullptr;  // false: per replica
   std::unique_ptr<CnnGroupPlan> gplan;   // grouped per-layer launches
@@ -880,7 +908,7 @@ uint64_t ingest(cg_group* g, const cg_request_batch* bt) {
   const uint64_t A = (uint64_t)S.d_arena.p;
   S.d_in_ptr = bt->inputs_on_device ? bt->inputs : S.d_in.p;
   const uint64_t IN = (uint64_t)S.d_in_ptr;
-  const uint64_t OUT = (uint64_t)g->d_outs.p;
+  const uint64_t OUT = (uint64_t)S.res.d_outs.p;
   auto seg_raw = [](uint64_t ptr, uint64_t off, uint64_t len) {
     return ChainSeg{ptr, off, len, kSegRaw, 0};
   };
@@ -923,7 +951,7 @@ uint64_t ingest(cg_group* g, const cg_request_batch* bt) {
       ChainJob j = leaf_job(k, p, rl[k].h);
       j.blk_begin = rl[k].P / 64;
       j.state_in = j.blk_begin ? (uint64_t)(S.d_mid.p + 8 * k) : 0;
-      j.digest_out = (uint64_t)(g->d_leaf.p + 32 * ((uint64_t)p * B + k));
+      j.digest_out = (uint64_t)(S.res.d_leaf.p + 32 * ((uint64_t)p * B + k));
       jobs.push_back(j);
     }
   // [B + N*B, B + 2*N*B): single attestation leaves H(0x00||0x53||req||res);
@@ -931,8 +959,8 @@ uint64_t ingest(cg_group* g, const cg_request_batch* bt) {
   for (uint32_t k = 0; k < B; k++)
     for (uint32_t p = 0; p < N; p++) {
       ChainJob j = leaf_job(k, p, rl[k].h53);
-      j.digest_out = (uint64_t)g->d_aleaf.p;
-      j.skip_flag = (uint64_t)(g->d_single_pos.p + (uint64_t)k * N + p);
+      j.digest_out = (uint64_t)S.res.d_aleaf.p;
+      j.skip_flag = (uint64_t)(S.res.d_single_pos.p + (uint64_t)k * N + p);
       jobs.push_back(j);
     }
   S.h_jobs.ensure(jobs.size());
@@ -958,6 +986,7 @@ uint64_t ingest(cg_group* g, const cg_request_batch* bt) {
   CG_CUDA(cudaEventRecord(S.ev_prefix, st));
   S.used = true;
   S.ever = true;
+  S.certified = false;
   S.ticket = ticket;
   S.B = B;
   g->next_ticket++;
@@ -965,25 +994,44 @@ uint64_t ingest(cg_group* g, const cg_request_batch* bt) {
 }
 
 // execute_batch + try_prepare's R trees + try_attest (engine.cpp:269-306,
-// coordinator.cpp:588-624, 727-849) on the main stream.
+// coordinator.cpp:588-624, 727-849). The replica forwards run on the main
+// stream; the certification tail (result leaves, R trees, [NCCL exchange],
+// select_quorum + label, manifest, A tree) runs on the context's tail stream
+// behind the slot's ev_fwd, overlapping the next batch's forwards.
+cudaStream_t tail_stream(cg_ctx* ctx) {
+  if (!ctx->tail) {
+    int lo = 0, hi = 0;
+    CG_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CG_CUDA(cudaStreamCreateWithPriority(&ctx->tail, cudaStreamNonBlocking, hi));
+  }
+  return ctx->tail;
+}
+
 void certify(cg_group* g, uint64_t ticket, const double* precomputed_outputs) {
   IngestSlot& S = slot_for(g, ticket);
+  BatchResults& R = S.res;
   cg_ctx* ctx = g->ctx;
   const uint32_t B = S.B, N = g->N;
   const uint64_t v = g->v;
   const uint32_t gl = (uint32_t)g->gid.size();
   cudaStream_t st = ctx->stream;
+  cudaStream_t tl = tail_stream(ctx);
   CG_CUDA(cudaStreamWaitEvent(st, S.ev_staged, 0));
   if (precomputed_outputs) {
     // agreement/digest-only mode (C5): N x B x v outputs supplied by the host
-    CG_CUDA(cudaMemcpyAsync(g->d_outs.p, precomputed_outputs, 8 * (size_t)N * B * v,
+    CG_CUDA(cudaMemcpyAsync(R.d_outs.p, precomputed_outputs, 8 * (size_t)N * B * v,
                             cudaMemcpyHostToDevice, st));
   } else {
-    // leave one SM per in-flight midstate-chain CTA to the chains
+    // leave one SM per in-flight chain CTA (request midstates of batches
+    // ingested ahead, result leaves of tails still running) to the chains
     int chain_ctas = 0;
-    for (auto& o : g->slots)
-      if (o.get() != &S && o->used && cudaEventQuery(o->ev_prefix) == cudaErrorNotReady)
+    for (auto& o : g->slots) {
+      if (o.get() == &S || !o->ever) continue;
+      if (o->used && cudaEventQuery(o->ev_prefix) == cudaErrorNotReady)
         chain_ctas += (int)ceil_div(o->B, kChainExclusiveThreads);
+      else if (o->certified && cudaEventQuery(o->ev_done) == cudaErrorNotReady)
+        chain_ctas += (int)ceil_div((uint64_t)o->B * (g->dist ? 1 : N), kChainExclusiveThreads);
+    }
     set_gemm_sm_budget(kNumSMs - chain_ctas);
     const void* prepped = nullptr;
     if (g->same_prep) {  // replica-independent input stage, once per batch
@@ -1008,21 +1056,21 @@ void certify(cg_group* g, uint64_t ticket, const double* precomputed_outputs) {
       for (uint32_t p = 1; p < N; p++) same_sm &= g->models[p]->softmax == g->models[0]->softmax;
       if (same_sm) {  // softmax/top-k of all N x B rows in one launch
         launch_softmax_topk_f32(g->d_pre32.p, v, N * B, (uint32_t)v, g->models[0]->softmax,
-                                g->d_outs.p, v, g->topk, g->d_topi.p, g->d_topv.p, st);
+                                R.d_outs.p, v, g->topk, R.d_topi.p, R.d_topv.p, st);
       } else {
         for (uint32_t p = 0; p < N; p++)
           launch_softmax_topk_f32(g->d_pre32.p + (uint64_t)p * B * v, v, B, (uint32_t)v,
-                                  g->models[p]->softmax, g->d_outs.p + (uint64_t)p * B * v, v,
-                                  g->topk, g->d_topi.p + (uint64_t)p * B * g->topk,
-                                  g->d_topv.p + (uint64_t)p * B * g->topk, st);
+                                  g->models[p]->softmax, R.d_outs.p + (uint64_t)p * B * v, v,
+                                  g->topk, R.d_topi.p + (uint64_t)p * B * g->topk,
+                                  R.d_topv.p + (uint64_t)p * B * g->topk, st);
       }
     }
     for (uint32_t li = 0; li < (uint32_t)g->models.size() && !grouped; li++) {
       const uint32_t p = g->dist ? g->rank : li;  // provider index of local replica li
       cg_model* m = g->models[li];
-      double* outs = g->d_outs.p + (uint64_t)p * B * v;
-      uint32_t* ti = g->d_topi.p + (uint64_t)p * B * g->topk;
-      double* tv = g->d_topv.p + (uint64_t)p * B * g->topk;
+      double* outs = R.d_outs.p + (uint64_t)p * B * v;
+      uint32_t* ti = R.d_topi.p + (uint64_t)p * B * g->topk;
+      double* tv = R.d_topv.p + (uint64_t)p * B * g->topk;
       if (m->kind == 1) {
         m->cnn->forward(S.d_in_ptr, B, g->d_pre32.p, st, prepped);
         launch_softmax_topk_f32(g->d_pre32.p, v, B, (uint32_t)v, m->softmax, outs, v,
@@ -1035,75 +1083,82 @@ void certify(cg_group* g, uint64_t ticket, const double* precomputed_outputs) {
     }
     set_gemm_sm_budget(kNumSMs);
   }
-  CG_CUDA(cudaStreamWaitEvent(st, S.ev_prefix, 0));
+  CG_CUDA(cudaEventRecord(S.ev_fwd, st));
+  // ---- the tail, on the tail stream
+  CG_CUDA(cudaStreamWaitEvent(tl, S.ev_fwd, 0));
+  CG_CUDA(cudaStreamWaitEvent(tl, S.ev_prefix, 0));
   if (g->dist) {
     // This rank is provider `rank`: its own result leaves and R root
     // (try_prepare), then one NCCL all-gather of every provider's outputs
     // and R root over NVLink; agreement and the attestation are then
     // computed on every rank, as every reference node attests.
     const uint32_t r = g->rank;
-    launch_chain_jobs(S.d_jobs.p + B + (uint64_t)r * B, B, st);
-    launch_merkle_trees(g->d_leaf.p + 32 * (uint64_t)r * B, nullptr, S.d_tree.p + N, nullptr, 1,
-                        B, g->d_rroots.p + 32 * r, st);
-    timer_begin(st, kTimeComm);
+    launch_chain_jobs(S.d_jobs.p + B + (uint64_t)r * B, B, tl, /*exclusive_sm=*/true);
+    launch_merkle_trees(R.d_leaf.p + 32 * (uint64_t)r * B, nullptr, S.d_tree.p + N, nullptr, 1,
+                        B, R.d_rroots.p + 32 * r, tl);
+    timer_begin(tl, kTimeComm);
     ncclResult_t e1, e2, e3;
     e1 = ncclGroupStart();
-    e2 = ncclAllGather(g->d_outs.p + (uint64_t)r * B * v, g->d_outs.p, (size_t)B * v,
-                       ncclDouble, ctx->comm, st);
-    e3 = ncclAllGather(g->d_rroots.p + 32 * r, g->d_rroots.p, 32, ncclUint8, ctx->comm, st);
+    e2 = ncclAllGather(R.d_outs.p + (uint64_t)r * B * v, R.d_outs.p, (size_t)B * v, ncclDouble,
+                       ctx->comm, tl);
+    e3 = ncclAllGather(R.d_rroots.p + 32 * r, R.d_rroots.p, 32, ncclUint8, ctx->comm, tl);
     ncclResult_t e4 = ncclGroupEnd();
-    timer_end(st, kTimeComm);
+    timer_end(tl, kTimeComm);
     if (e1 != ncclSuccess || e2 != ncclSuccess || e3 != ncclSuccess || e4 != ncclSuccess)
       throw CudaError(std::string("ncclAllGather: ") + ncclGetErrorString(e4));
   } else {
-    launch_chain_jobs(S.d_jobs.p + B, N * B, st);  // result leaves
-    launch_merkle_trees(g->d_leaf.p, S.d_tree.p, S.d_tree.p + N, nullptr, N, B,
-                        g->d_rroots.p, st);
+    launch_chain_jobs(S.d_jobs.p + B, N * B, tl, /*exclusive_sm=*/true);  // result leaves
+    launch_merkle_trees(R.d_leaf.p, S.d_tree.p, S.d_tree.p + N, nullptr, N, B, R.d_rroots.p, tl);
   }
-  timer_begin(st, kTimeAgree);
-  launch_select_quorum(g->d_outs.p, (uint64_t)B * v, v, nullptr, S.d_eps.p, B, N, g->f,
-                       (uint32_t)v, g->metric, g->d_sel.p, g->d_diam.p, g->d_sat.p,
-                       g->d_status.p, g->d_label.p, st);
-  launch_attest_manifest(B, N, g->d_sel.p, g->d_sat.p, g->d_rroots.p, S.d_reqids.p,
-                         g->d_gid.p, gl, g->version, g->d_aleaf.p, g->d_single_pos.p,
-                         g->d_kinds.p, g->d_mnodes.p, g->d_mops.p, g->d_count.p, st);
-  launch_chain_jobs(S.d_jobs.p + B + (uint64_t)N * B, N * B, st);  // single A leaves
-  launch_merkle_trees(g->d_aleaf.p, nullptr, nullptr, g->d_count.p, 1, (uint64_t)N * B + B + N,
-                      g->d_aroot.p, st);
-  timer_end(st, kTimeAgree);
-  CG_CUDA(cudaEventRecord(S.ev_done, st));
+  timer_begin(tl, kTimeAgree);
+  launch_select_quorum(R.d_outs.p, (uint64_t)B * v, v, nullptr, S.d_eps.p, B, N, g->f,
+                       (uint32_t)v, g->metric, R.d_sel.p, R.d_diam.p, R.d_sat.p, R.d_status.p,
+                       R.d_label.p, tl);
+  launch_attest_manifest(B, N, R.d_sel.p, R.d_sat.p, R.d_rroots.p, S.d_reqids.p, g->d_gid.p, gl,
+                         g->version, R.d_aleaf.p, R.d_single_pos.p, R.d_kinds.p, R.d_mnodes.p,
+                         R.d_mops.p, R.d_count.p, tl);
+  launch_chain_jobs(S.d_jobs.p + B + (uint64_t)N * B, N * B, tl);  // single A leaves
+  launch_merkle_trees(R.d_aleaf.p, nullptr, nullptr, R.d_count.p, 1, (uint64_t)N * B + B + N,
+                      R.d_aroot.p, tl);
+  timer_end(tl, kTimeAgree);
+  CG_CUDA(cudaEventRecord(S.ev_done, tl));
   S.used = false;
+  S.certified = true;
+  g->last = &S;
   g->last_B = B;
 }
 
-void certify_fetch(cg_group* g, cg_certify_out* o) {
+void certify_fetch(cg_group* g, cg_certify_out* o, const IngestSlot* slot = nullptr) {
   cudaStream_t st = g->ctx->stream;
-  const uint32_t B = g->last_B, N = g->N;
+  if (!slot) slot = g->last;
+  if (!slot || !slot->certified) throw InvalidArgument("nothing certified yet");
+  const uint32_t B = slot->B, N = g->N;
   const uint64_t v = g->v;
-  if (B == 0) throw InvalidArgument("nothing certified yet");
+  const BatchResults& R = slot->res;
+  CG_CUDA(cudaStreamWaitEvent(st, slot->ev_done, 0));
   auto d2h = [&](void* dst, const void* src, size_t n) {
     if (dst) CG_CUDA(cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToHost, st));
   };
   std::vector<int8_t> status(B);
   uint32_t count = 0;
-  d2h(status.data(), g->d_status.p, B);
-  d2h(&count, g->d_count.p, 4);
-  d2h(o->selected, g->d_sel.p, 4 * (size_t)B);
-  d2h(o->diameter, g->d_diam.p, 8 * (size_t)B);
-  d2h(o->satisfied, g->d_sat.p, B);
-  d2h(o->label, g->d_label.p, 8 * (size_t)B);
-  d2h(o->r_roots, g->d_rroots.p, 32 * (size_t)N);
-  d2h(o->a_root, g->d_aroot.p, 32);
-  d2h(o->leaf_hashes, g->d_leaf.p, 32 * (size_t)N * B);
-  d2h(o->outputs, g->d_outs.p, 8 * (size_t)N * B * v);
-  d2h(o->topk_idx, g->d_topi.p, 4 * (size_t)N * B * g->topk);
-  d2h(o->topk_val, g->d_topv.p, 8 * (size_t)N * B * g->topk);
+  d2h(status.data(), R.d_status.p, B);
+  d2h(&count, R.d_count.p, 4);
+  d2h(o->selected, R.d_sel.p, 4 * (size_t)B);
+  d2h(o->diameter, R.d_diam.p, 8 * (size_t)B);
+  d2h(o->satisfied, R.d_sat.p, B);
+  d2h(o->label, R.d_label.p, 8 * (size_t)B);
+  d2h(o->r_roots, R.d_rroots.p, 32 * (size_t)N);
+  d2h(o->a_root, R.d_aroot.p, 32);
+  d2h(o->leaf_hashes, R.d_leaf.p, 32 * (size_t)N * B);
+  d2h(o->outputs, R.d_outs.p, 8 * (size_t)N * B * v);
+  d2h(o->topk_idx, R.d_topi.p, 4 * (size_t)N * B * g->topk);
+  d2h(o->topk_val, R.d_topv.p, 8 * (size_t)N * B * g->topk);
   CG_CUDA(cudaStreamSynchronize(st));
   if (o->manifest_len) *o->manifest_len = count;
-  d2h(o->manifest_kind, g->d_kinds.p, count);
-  d2h(o->manifest_node, g->d_mnodes.p, 4 * (size_t)count);
-  d2h(o->manifest_op, g->d_mops.p, 4 * (size_t)count);
-  d2h(o->a_leaf_hashes, g->d_aleaf.p, 32 * (size_t)count);
+  d2h(o->manifest_kind, R.d_kinds.p, count);
+  d2h(o->manifest_node, R.d_mnodes.p, 4 * (size_t)count);
+  d2h(o->manifest_op, R.d_mops.p, 4 * (size_t)count);
+  d2h(o->a_leaf_hashes, R.d_aleaf.p, 32 * (size_t)count);
   CG_CUDA(cudaStreamSynchronize(st));
   for (uint32_t k = 0; k < B; k++)
     if (status[k] != 0) throw InvalidArgument("select_quorum: invalid argument");
@@ -1152,24 +1207,7 @@ int create_group(cg_ctx* ctx, cg_model* const* models, uint32_t nlocal, uint32_t
     const uint64_t B = max_batch, v = g->v;
     g->d_pre64.ensure(B * v);
     g->d_pre32.ensure((uint64_t)N * B * v);  // per-replica logits (grouped forward)
-    g->d_outs.ensure((uint64_t)N * B * v);
-    g->d_topi.ensure((uint64_t)N * B * topk);
-    g->d_topv.ensure((uint64_t)N * B * topk);
-    g->d_diam.ensure(B);
-    g->d_sel.ensure(B);
-    const uint64_t amax = (uint64_t)N * B + B + N;
-    g->d_mnodes.ensure(amax);
-    g->d_mops.ensure(amax);
-    g->d_kinds.ensure(amax);
-    g->d_count.ensure(1);
-    g->d_leaf.ensure(32 * (uint64_t)N * B);
-    g->d_rroots.ensure(32 * (uint64_t)N);
-    g->d_aleaf.ensure(32 * amax);
-    g->d_aroot.ensure(32);
-    g->d_sat.ensure(B);
-    g->d_status.ensure(B);
-    g->d_label.ensure(B);
-    g->d_single_pos.ensure((uint64_t)N * B);
+    const uint64_t amax = (uint64_t)N * B + B + N;  // manifest entries
     g->d_gid.ensure(g->gid.size() + 1);
     CG_CUDA(cudaMemcpy(g->d_gid.p, g->gid.data(), g->gid.size(), cudaMemcpyHostToDevice));
     g->all_cnn = true;
@@ -1206,6 +1244,24 @@ int create_group(cg_ctx* ctx, cg_model* const* models, uint32_t nlocal, uint32_t
       S->h_jobs.ensure(B * (1 + 2 * N));
       S->h_eps.ensure(B);
       S->h_tree.ensure(2 * N);
+      CG_CUDA(cudaEventCreateWithFlags(&S->ev_fwd, cudaEventDisableTiming));
+      S->res.d_outs.ensure((uint64_t)N * B * v);
+      S->res.d_topi.ensure((uint64_t)N * B * topk);
+      S->res.d_topv.ensure((uint64_t)N * B * topk);
+      S->res.d_diam.ensure(B);
+      S->res.d_sel.ensure(B);
+      S->res.d_mnodes.ensure(amax);
+      S->res.d_mops.ensure(amax);
+      S->res.d_kinds.ensure(amax);
+      S->res.d_count.ensure(1);
+      S->res.d_leaf.ensure(32 * (uint64_t)N * B);
+      S->res.d_rroots.ensure(32 * (uint64_t)N);
+      S->res.d_aleaf.ensure(32 * amax);
+      S->res.d_aroot.ensure(32);
+      S->res.d_sat.ensure(B);
+      S->res.d_status.ensure(B);
+      S->res.d_label.ensure(B);
+      S->res.d_single_pos.ensure((uint64_t)N * B);
       g->slots.push_back(std::move(S));
     }
     *out = g.release();
@@ -1239,6 +1295,7 @@ void cg_group_free(cg_group* g) {
   if (!g) return;
   cudaSetDevice(g->ctx->device);
   cudaStreamSynchronize(g->ctx->stream);
+  if (g->ctx->tail) cudaStreamSynchronize(g->ctx->tail);
   for (auto& s : g->slots) cudaStreamSynchronize(s->stream);
   delete g;
 }
@@ -1426,20 +1483,22 @@ int cg_group_auth_paths(cg_group* g, uint32_t tree, const uint64_t* indices, uin
   if (!g) return CG_EINVAL;
   return guarded(g->ctx, [&] {
     const uint32_t B = g->last_B, N = g->N;
-    if (B == 0) throw InvalidArgument("nothing certified yet");
+    if (B == 0 || !g->last) throw InvalidArgument("nothing certified yet");
     if (tree > N) throw InvalidArgument("tree index out of range");
     if (g->dist && tree < N && tree != g->rank)
       throw InvalidArgument("replica-parallel group: only this rank's result tree is local");
     const uint8_t* leaves;
     uint64_t n;
+    const BatchResults& R = g->last->res;
+    CG_CUDA(cudaStreamWaitEvent(g->ctx->stream, g->last->ev_done, 0));
     if (tree < N) {  // provider `tree`'s R tree: its B result leaves
-      leaves = g->d_leaf.p + 32 * (uint64_t)tree * B;
+      leaves = R.d_leaf.p + 32 * (uint64_t)tree * B;
       n = B;
     } else {  // the attestation tree, manifest order
       uint32_t cnt = 0;
-      CG_CUDA(cudaMemcpyAsync(&cnt, g->d_count.p, 4, cudaMemcpyDeviceToHost, g->ctx->stream));
+      CG_CUDA(cudaMemcpyAsync(&cnt, R.d_count.p, 4, cudaMemcpyDeviceToHost, g->ctx->stream));
       CG_CUDA(cudaStreamSynchronize(g->ctx->stream));
-      leaves = g->d_aleaf.p;
+      leaves = R.d_aleaf.p;
       n = cnt;
     }
     auth_paths_device(g->ctx, leaves, n, indices, count, siblings, sides, lens, nullptr);
@@ -1488,6 +1547,17 @@ int cg_group_fetch(cg_group* g, cg_certify_out* out) {
   if (!g || !out) return CG_EINVAL;
   return guarded(g->ctx, [&] {
     certify_fetch(g, out);
+    return CG_OK;
+  });
+}
+
+int cg_group_fetch_ticket(cg_group* g, uint64_t ticket, cg_certify_out* out) {
+  if (!g || !out) return CG_EINVAL;
+  return guarded(g->ctx, [&] {
+    const IngestSlot& S = *g->slots[ticket % g->slots.size()];
+    if (S.ticket != ticket || !S.certified)
+      throw InvalidArgument("ticket not certified or its slot already reused");
+    certify_fetch(g, out, &S);
     return CG_OK;
   });
 }

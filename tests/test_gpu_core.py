@@ -228,3 +228,19 @@ def test_ingest_ahead_and_out_of_order(ctx):
         w = want if i % 2 == 0 else want_half
         assert np.array_equal(r["a_root"], w["a_root"]) and np.array_equal(r["r_roots"], w["r_roots"])
     assert np.array_equal(want["a_root"], g["honest_a_root"])
+
+
+def test_fetch_ticket_after_next_certify(ctx):
+    """Batch i's results stay readable (fetch_ticket) while batch i+1 is
+    certified: per-batch results live in the batch's ingest slot."""
+    from paper_2205_15757_b200 import RequestBatch
+    g = golden("c1_batch.npz")
+    grp = _group(ctx, g, int(g["B"]))
+    b = RequestBatch.from_encoded(split_reqs(g))
+    t0, t1 = grp.ingest(b), grp.ingest(b)
+    grp.certify_ticket(t0, sync=False)
+    grp.certify_ticket(t1, sync=False)
+    r0 = grp.fetch_ticket(t0)
+    r1 = grp.fetch_ticket(t1)
+    assert np.array_equal(r0["a_root"], g["honest_a_root"])
+    assert np.array_equal(r1["a_root"], g["honest_a_root"])
