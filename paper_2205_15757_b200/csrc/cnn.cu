@@ -148,25 +148,36 @@ __global__ void gather_s2_1x1_kernel(const bf16* __restrict__ in, int B, int H, 
       in + (((size_t)n * H + 2 * ho) * H + 2 * wo) * C + ch * 8));
 }
 
-// Global average pool [B, HW, C] -> [B, C] (f32 sum in pixel order).
-__global__ void avgpool_kernel(const bf16* __restrict__ in, int B, int HW, int C,
-                               bf16* __restrict__ out) {
-  const int chunks = C / 8;
-  int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= B * chunks) return;
-  int n = t / chunks, ch = t - n * chunks;
+// Global average pool [B, HW, C] -> [B, C]. A CTA owns (image, 256
+// channels): 32 lanes x 8 channels, 8 warps striding the pixels, then a
+// fixed-order smem reduction over the warps (deterministic, batch-invariant).
+__global__ void __launch_bounds__(256) avgpool_kernel(const bf16* __restrict__ in, int B, int HW,
+                                                      int C, bf16* __restrict__ out) {
+  __shared__ float part[8][32][9];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int groups = C / 256, n = blockIdx.x / groups, cg = blockIdx.x - n * groups;
+  const int c0 = cg * 256 + lane * 8;
   float s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  for (int p = 0; p < HW; p++) {
-    uint4 q = __ldg(reinterpret_cast<const uint4*>(in + ((size_t)n * HW + p) * C + ch * 8));
+  for (int p = w; p < HW; p += 8) {
+    uint4 q = __ldg(reinterpret_cast<const uint4*>(in + ((size_t)n * HW + p) * C + c0));
     const bf16* e = reinterpret_cast<const bf16*>(&q);
 #pragma unroll
     for (int j = 0; j < 8; j++) s[j] += __bfloat162float(e[j]);
   }
-  __align__(16) bf16 o[8];
-  const float inv = 1.0f / (float)HW;
 #pragma unroll
-  for (int j = 0; j < 8; j++) o[j] = __float2bfloat16(s[j] * inv);
-  *reinterpret_cast<uint4*>(out + (size_t)n * C + ch * 8) = *reinterpret_cast<uint4*>(o);
+  for (int j = 0; j < 8; j++) part[w][lane][j] = s[j];
+  __syncthreads();
+  if (w == 0) {
+    float t[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int g = 0; g < 8; g++)
+#pragma unroll
+      for (int j = 0; j < 8; j++) t[j] += part[g][lane][j];
+    __align__(16) bf16 o[8];
+    const float inv = 1.0f / (float)HW;
+#pragma unroll
+    for (int j = 0; j < 8; j++) o[j] = __float2bfloat16(t[j] * inv);
+    *reinterpret_cast<uint4*>(out + (size_t)n * C + c0) = *reinterpret_cast<uint4*>(o);
+  }
 }
 
 unsigned grid_for(size_t threads, int tpb = 256) { return (unsigned)ceil_div(threads, tpb); }
@@ -534,7 +545,7 @@ class ResNet final : public CnnModel {
       bf16* out = pooled_;
       int HW = H_last_ * H_last_, C = fc_.cin;
       aux([in, out, B, HW, C](cudaStream_t st) {
-        avgpool_kernel<<<grid_for((size_t)B * C / 8), 256, 0, st>>>(in, B, HW, C, out);
+        avgpool_kernel<<<(unsigned)(B * (C / 256)), 256, 0, st>>>(in, B, HW, C, out);
         CG_CHECK_LAUNCH();
       });
     }
@@ -1272,7 +1283,7 @@ class MobileNetV2 final : public SeqNet {
       bf16* in = head_out_;
       bf16* out = pooled_;
       push_aux(L, [in, out, b, HW](cudaStream_t st) {
-        avgpool_kernel<<<grid_for((size_t)b * 1280 / 8), 256, 0, st>>>(in, b, HW, 1280, out);
+        avgpool_kernel<<<(unsigned)(b * (1280 / 256)), 256, 0, st>>>(in, b, HW, 1280, out);
         CG_CHECK_LAUNCH();
       });
     }
