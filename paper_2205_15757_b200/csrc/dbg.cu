@@ -147,8 +147,18 @@ extern "C" int cg_dbg_halo_trace(cg_ctx* ctx, int B, int H, int C, int N, int BN
 
 // Timing + CTA-0 event trace of one 1x1 conv GEMM shape on device-resident
 // random operands (no host copies in the timed launch).
+extern "C" int cg_dbg_gemm_trace_mode(cg_ctx* ctx, int M, int N, int K, int BN, int residual,
+                                      int row_mode, int H, long long* trace_host, double* us);
+
 extern "C" int cg_dbg_gemm_trace(cg_ctx* ctx, int M, int N, int K, int BN, int residual,
                                  long long* trace_host, double* us) {
+  return cg_dbg_gemm_trace_mode(ctx, M, N, K, BN, residual, 0, 0, trace_host, us);
+}
+
+// The same with a row remap (row_mode, H = W): M compact rows in, the output
+// sized for the mode (e.g. CompactToPad writes the padded grid interior).
+extern "C" int cg_dbg_gemm_trace_mode(cg_ctx* ctx, int M, int N, int K, int BN, int residual,
+                                      int row_mode, int H, long long* trace_host, double* us) {
   try {
     cudaStream_t st = (cudaStream_t)cg_ctx_stream(ctx);
     void *dA, *dB, *dbias, *dres = nullptr, *dout;
@@ -156,7 +166,10 @@ extern "C" int cg_dbg_gemm_trace(cg_ctx* ctx, int M, int N, int K, int BN, int r
     CG_CUDA(cudaMalloc(&dA, (size_t)M * K * 2));
     CG_CUDA(cudaMalloc(&dB, (size_t)N * K * 2));
     CG_CUDA(cudaMalloc(&dbias, (size_t)N * 4));
-    CG_CUDA(cudaMalloc(&dout, (size_t)M * N * 2));
+    const size_t out_rows = row_mode == kRowCompactToPad
+                                ? (size_t)(M / (H * H)) * (H + 2) * (H + 2)
+                                : (size_t)M;
+    CG_CUDA(cudaMalloc(&dout, out_rows * N * 2));
     CG_CUDA(cudaMalloc(&dtr, 8 * 64 * 8));
     CG_CUDA(cudaMemset(dA, 0x11, (size_t)M * K * 2));
     CG_CUDA(cudaMemset(dB, 0x11, (size_t)N * K * 2));
@@ -180,7 +193,10 @@ extern "C" int cg_dbg_gemm_trace(cg_ctx* ctx, int M, int N, int K, int BN, int r
     a.out = dout;
     a.ld_out = N;
     a.relu = 1;
-    a.rows_out = M;
+    a.rows_out = (int)out_rows;
+    a.row_mode = row_mode;
+    a.H = H;
+    a.W = H;
     launch_conv_gemm(oa, ob, a, BN, st);  // warm
     cudaEvent_t e0, e1;
     CG_CUDA(cudaEventCreate(&e0));

@@ -511,10 +511,23 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t stg_a = su32(s_epi + (warp - 2) * (32 * kStgLd));
     const int rr8 = lane >> 2, cg8 = lane & 3;
     constexpr int CPT = BN / 32;  // 32-column chunks per tile
+    // BN = 64 (2 chunks): the two warp groups take alternate tiles whole
+    // (both TMEM accumulators drained concurrently) instead of one chunk
+    // each of the same tile; wider tiles split chunks between the groups.
+    constexpr bool kTileSplit = BN == 64;
+    constexpr int C0S = kTileSplit ? 1 : 2;  // chunk stride of one warp
     int tile_i = 0, acc = 0;
     int stage_seq = 0;  // staging buffer sequence across all of this warp's chunks
     uint32_t acc_phase = 0;
     for (int t = blockIdx.x; t < tiles; t += gridDim.x, tile_i++) {
+      if (kTileSplit && (tile_i & 1) != h) {
+        // the other group drains this accumulator; release our share of it
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        continue;
+      }
+      const int c_first = kTileSplit ? 0 : h;
       int r_, m0, n0;
       coords(t, r_, m0, n0);
       const float* bias_r = gp.bias[r_];
@@ -529,12 +542,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       // while chunk c is biased, stored and written out.
       const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16) + acc * BN;
       uint32_t v[32];
-      if (h < CPT) tmem_ld32_issue(trow + h * 32, v);
+      if (c_first < CPT) tmem_ld32_issue(trow + c_first * 32, v);
 #pragma unroll 1
-      for (int c = h; c < CPT; c += 2) {
+      for (int c = c_first; c < CPT; c += C0S) {
         const int g = tile_i * CPT + c;
         tmem_ld_wait(v);
-        if (c + 2 >= CPT) {  // this warp's last chunk: hand TMEM back early
+        if (c + C0S >= CPT) {  // this warp's last chunk: hand TMEM back early
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -554,7 +567,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             x[4 * j + 2] = __uint_as_float(v[4 * j + 2]) + b4.z;
             x[4 * j + 3] = __uint_as_float(v[4 * j + 3]) + b4.w;
           }
-          if (c + 2 < CPT) tmem_ld32_issue(trow + (c + 2) * 32, v);
+          if (c + C0S < CPT) tmem_ld32_issue(trow + (c + C0S) * 32, v);
           const int slot = kResSlots > 0 ? g % kResSlots : 0;
           if (res_tma) {
             mbar_wait(&rfull[slot], (g / (kResSlots > 0 ? kResSlots : 1)) & 1);
@@ -603,7 +616,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           sts_v4(stg_a + 4 * (lane * kStgLd + 4 * j), v[4 * j], v[4 * j + 1], v[4 * j + 2],
                  v[4 * j + 3]);
         __syncwarp();
-        if (c + 2 < CPT) tmem_ld32_issue(trow + (c + 2) * 32, v);
+        if (c + C0S < CPT) tmem_ld32_issue(trow + (c + C0S) * 32, v);
         // phase 2: lane = (row rr8 of 8, 8-column group cg8 of 4): 16-byte
         // stores, each warp store instruction covers 8 rows x 64 B.
         const int n = n0 + c * 32 + cg8 * 8;
@@ -663,9 +676,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (warp == 2) CG_TRACE(6, tile_i);
       if (warp == 9) CG_TRACE(7, tile_i);
-      if (tma_out && lane == 0 && t + (int)gridDim.x >= tiles) bulk_wait_all();
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
+    if (tma_out && lane == 0) bulk_wait_all();  // this warp's stores read their staging
   }
   __syncthreads();
   if (warp == 1) {
