@@ -86,3 +86,52 @@ def test_label_digest_batch(ctx, oracle):
     got = ctx.label_digests(ids, labels, 11)
     for k in range(300):
         assert got[k].tobytes() == oracle.label_digest(ids[k].tobytes(), 11, int(labels[k]))
+
+
+def _adversarial(rng, R, n, v):
+    """Outputs built to hit the corner cases of select_quorum / the label
+    vote: NaN and Inf lanes, exactly duplicated replicas (zero distances and
+    diameter ties between equal-size subsets -> lexicographic tie-break),
+    distances exactly at epsilon, and argmax ties (first maximum wins)."""
+    outs = rng.uniform(0, 1, (R, n, v)).round(2)  # coarse values -> many exact ties
+    kind = rng.integers(0, 6, R)
+    for k in range(R):
+        if kind[k] == 0:    # NaN somewhere
+            outs[k, rng.integers(n), rng.integers(v)] = np.nan
+        elif kind[k] == 1:  # +/-Inf lanes
+            outs[k, rng.integers(n), rng.integers(v)] = np.inf
+            outs[k, rng.integers(n), rng.integers(v)] = -np.inf
+        elif kind[k] == 2:  # duplicated replicas
+            src = rng.integers(n)
+            outs[k, :] = outs[k, src]
+        elif kind[k] == 3:  # two clusters of equal size
+            outs[k, : n // 2] = outs[k, 0]
+            outs[k, n // 2:] = outs[k, -1]
+        elif kind[k] == 4:  # argmax ties inside a row
+            outs[k, :, :] = outs[k, 0]
+            outs[k, :, 0] = 1.0
+            if v > 1:
+                outs[k, :, 1] = 1.0
+    return outs
+
+
+@pytest.mark.parametrize("n,f,v,metric", [(4, 1, 6, 0), (8, 2, 6, 0), (5, 1, 4, 2),
+                                          (8, 3, 3, 2), (3, 1, 1, 1)])
+def test_agreement_adversarial_both_kernels(ctx, oracle, n, f, v, metric):
+    """Bit-exact against the oracle on NaN/Inf/tie cases, through both the
+    CTA-per-request kernel (small batch) and the thread-per-request kernel
+    (large batch); the oracle's select_quorum follows distance.cpp's exact
+    comparison semantics (std::max, strict '>' against epsilon)."""
+    rng = np.random.default_rng(n * 100 + v)
+    R = 5000
+    outs = _adversarial(rng, R, n, v)
+    eps = rng.choice([0.0, 0.1, 0.25, 1.0], R)
+    want = oracle.agree_batch(np.transpose(outs, (1, 0, 2)), f, metric, eps)
+    big = ctx.select_quorum_batch(outs, n, f, metric, eps)               # wide kernel
+    small = ctx.select_quorum_batch(outs[:300], n, f, metric, eps[:300])  # CTA kernel
+    for key in ("selected", "satisfied", "label"):
+        assert np.array_equal(big[key], want[key]), key
+        assert np.array_equal(small[key], want[key][:300]), key
+    assert np.array_equal(big["diameter"].view(np.uint64), want["diameter"].view(np.uint64))
+    assert np.array_equal(small["diameter"].view(np.uint64),
+                          want["diameter"][:300].view(np.uint64))
