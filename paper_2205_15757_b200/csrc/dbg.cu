@@ -353,3 +353,13 @@ extern "C" int cg_synth_outputs(cg_ctx* ctx, uint64_t seed, uint32_t R, uint32_t
     return CG_ECUDA;
   }
 }
+
+extern "C" int cg_dbg_mma_rate(cg_ctx* ctx, int N, int iters, int ctas, int two_acc,
+                               double* cycles_per_mma) {
+  try {
+    *cycles_per_mma = mma_rate_bench(N, iters, ctas, two_acc, (cudaStream_t)cg_ctx_stream(ctx));
+    return CG_OK;
+  } catch (const std::exception&) {
+    return CG_ECUDA;
+  }
+}

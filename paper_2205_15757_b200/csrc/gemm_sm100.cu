@@ -744,6 +744,158 @@ void launch_t(const PreparedGemm& p, cudaStream_t st, int max_ctas) {
 
 }  // namespace
 
+// ---------------------------------------------------- MMA rate microbench
+// One elected thread per CTA issues `iters` x 4 back-to-back kind::f16 MMAs
+// (M=128, N, K=16, both operands in shared memory) into one or two TMEM
+// accumulators; cycles per MMA = the issue/dispatch rate the conv kernels
+// can reach at best for that N (tools/mma_rate.py).
+template <int N>
+__global__ void __launch_bounds__(128, 1) mma_rate_kernel(int iters, int two_acc,
+                                                          long long* cycles) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024 - (su32(smem_raw) & 1023)) & 1023);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + A_BYTES;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sB + N * BK * 2);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     su32(tslot)), "r"(512) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  if (warp == 1 && lane == 0) {
+    const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) |
+                           ((uint32_t)(BM >> 4) << 24);
+    const uint64_t ad = smem_desc_sw128(sA), bd = smem_desc_sw128(sB);
+    long long t0 = clock64();
+    for (int i = 0; i < iters; i++) {
+      const uint32_t d = tmem + ((two_acc && (i & 1)) ? 256u : 0u);
+#pragma unroll
+      for (int k = 0; k < 4; k++) umma_bf16(d, ad + 2 * k, bd + 2 * k, idesc, (i | k) != 0);
+    }
+    umma_commit(bar);
+    mbar_wait(bar, 0);
+    long long t1 = clock64();
+    if (blockIdx.x == 0) *cycles = t1 - t0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512)
+                 : "memory");
+  }
+}
+
+// The same on an SM pair: cluster of 2 CTAs, TMEM allocated with
+// cta_group::2, the leader issues M = 256 MMAs over both CTAs' operands and
+// commits to both CTAs' barriers.
+template <int N>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
+    mma_rate_pair_kernel(int iters, long long* cycles) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024 - (su32(smem_raw) & 1023)) & 1023);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + A_BYTES;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sB + (N / 2) * BK * 2);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t rank;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     su32(tslot)), "r"(256) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;"
+               ::: "memory");
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  if (rank == 0 && warp == 1 && lane == 0) {
+    const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) |
+                           ((uint32_t)(256 >> 4) << 24);
+    const uint64_t ad = smem_desc_sw128(sA), bd = smem_desc_sw128(sB);
+    long long t0 = clock64();
+    for (int i = 0; i < iters; i++) {
+#pragma unroll
+      for (int k = 0; k < 4; k++) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem),
+            "l"(ad + 2 * k), "l"(bd + 2 * k), "r"(idesc), "r"((uint32_t)((i | k) != 0)));
+      }
+    }
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+        " [%0], %1;" ::"r"(su32(bar)), "h"((uint16_t)3) : "memory");
+    mbar_wait(bar, 0);
+    long long t1 = clock64();
+    if (blockIdx.x == 0) *cycles = t1 - t0;
+  }
+  if (rank == 1 && warp == 1 && lane == 0) mbar_wait(bar, 0);
+  tc_fence_before();
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;"
+               ::: "memory");
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256)
+                 : "memory");
+  }
+}
+
+double mma_rate_pair_bench(int N, int iters, int ctas, cudaStream_t st) {
+  long long* d = nullptr;
+  CG_CUDA(cudaMalloc(&d, 8));
+  const int smem = 1024 + A_BYTES + (N / 2) * BK * 2 + 64;
+  auto run = [&](auto kern) {
+    CG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    kern<<<ctas, 128, smem, st>>>(iters, d);
+    CG_CHECK_LAUNCH();
+  };
+  if (N == 64) run(mma_rate_pair_kernel<64>);
+  else if (N == 128) run(mma_rate_pair_kernel<128>);
+  else run(mma_rate_pair_kernel<256>);
+  long long c = 0;
+  CG_CUDA(cudaMemcpyAsync(&c, d, 8, cudaMemcpyDeviceToHost, st));
+  CG_CUDA(cudaStreamSynchronize(st));
+  cudaFree(d);
+  return (double)c / (4.0 * iters);
+}
+
+double mma_rate_bench(int N, int iters, int ctas, int two_acc, cudaStream_t st) {
+  if (two_acc == 2) return mma_rate_pair_bench(N, iters, ctas, st);
+  long long* d = nullptr;
+  CG_CUDA(cudaMalloc(&d, 8));
+  const int smem = 1024 + A_BYTES + N * BK * 2 + 64;
+  auto run = [&](auto kern) {
+    CG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    kern<<<ctas, 128, smem, st>>>(iters, two_acc, d);
+    CG_CHECK_LAUNCH();
+  };
+  if (N == 64) run(mma_rate_kernel<64>);
+  else if (N == 128) run(mma_rate_kernel<128>);
+  else run(mma_rate_kernel<256>);
+  long long c = 0;
+  CG_CUDA(cudaMemcpyAsync(&c, d, 8, cudaMemcpyDeviceToHost, st));
+  CG_CUDA(cudaStreamSynchronize(st));
+  cudaFree(d);
+  return (double)c / (4.0 * iters);
+}
+
 static std::atomic<int> g_sm_budget{kNumSMs};
 void set_gemm_sm_budget(int sms) {
   g_sm_budget = sms < 1 ? 1 : (sms > kNumSMs ? kNumSMs : sms);

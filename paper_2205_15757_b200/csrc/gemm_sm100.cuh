@@ -105,6 +105,8 @@ void launch_prepared(const PreparedGemm& p, cudaStream_t st, int max_ctas = 0);
 // pipeline lowers it while request-midstate chains run on their own SMs, so
 // no statically scheduled GEMM CTA ever shares an SM with a chain CTA.
 void set_gemm_sm_budget(int sms);
+// Cycles per M=128 x N x K=16 SS-mode MMA issued back to back (microbench).
+double mma_rate_bench(int N, int iters, int ctas, int two_acc, cudaStream_t st);
 int gemm_sm_budget();
 
 // Launches the persistent warp-specialised kernel; BN in {64, 128, 256}.
