@@ -270,12 +270,23 @@ int cg_dbg_conv_gemm(cg_ctx* ctx, const uint16_t* A, int rowsA,
                      const uint16_t* residual, int relu, int row_mode, int H,
                      int W, int M, int rows_out, int out_f32, int BN, void* out,
                      int max_ctas);
+/* The same on SM pairs (cta_group::2: 256 x 256 tiles, each CTA holding
+ * half of the weight tile; BN = 256 only). */
+int cg_dbg_conv_gemm_pair(cg_ctx* ctx, const uint16_t* A, int rowsA, const uint16_t* B, int N,
+                          int Kc, int ntaps, const int* tap_off, const float* bias,
+                          const uint16_t* residual, int relu, int row_mode, int H, int W, int M,
+                          int rows_out, int out_f32, int BN, void* out, int max_ctas);
 /* The same in halo mode (one (BM + 2*halo_lo)-row box per channel block
  * feeds all 9 taps from shared memory). */
 int cg_dbg_conv_gemm_halo(cg_ctx* ctx, const uint16_t* A, int rowsA, const uint16_t* B, int N,
                           int Kc, int ntaps, const int* tap_off, const float* bias, int relu,
                           int row_mode, int H, int W, int M, int rows_out, int BN, void* out,
                           int halo_lo);
+/* Halo mode on SM pairs (cta_group::2, 256-row tiles; BN = 128 only). */
+int cg_dbg_conv_gemm_halo_pair(cg_ctx* ctx, const uint16_t* A, int rowsA, const uint16_t* B,
+                               int N, int Kc, int ntaps, const int* tap_off, const float* bias,
+                               int relu, int row_mode, int H, int W, int M, int rows_out, int BN,
+                               void* out, int halo_lo);
 
 #ifdef __cplusplus
 }

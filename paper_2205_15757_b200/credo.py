@@ -31,7 +31,8 @@ from typing import Optional, Sequence
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libcredo_gpu.so")
+# CREDO_GPU_LIB: an alternative build of the same library (A/B experiments)
+LIB_PATH = os.environ.get("CREDO_GPU_LIB") or os.path.join(HERE, "libcredo_gpu.so")
 
 CG_OK, CG_EINVAL, CG_ECUDA, CG_ENCCL, CG_EDIGEST, CG_ECODEC, CG_ENOTSUP = range(7)
 EUCLIDEAN, MAX_MINUS_MIN, CHEBYSHEV = 0, 1, 2

@@ -85,8 +85,14 @@ extern "C" int cg_dbg_sha_bench(cg_ctx* ctx, int mode, uint64_t nblocks,
 
 // Timing + CTA-0 event trace of one halo-mode 3x3 conv (B images of H x H,
 // C -> N channels) over a padded grid of device-resident operands.
+extern "C" int cg_dbg_halo_trace2(cg_ctx* ctx, int B, int H, int C, int N, int BN, int pair,
+                                  long long* trace_host, double* us);
 extern "C" int cg_dbg_halo_trace(cg_ctx* ctx, int B, int H, int C, int N, int BN,
                                  long long* trace_host, double* us) {
+  return cg_dbg_halo_trace2(ctx, B, H, C, N, BN, 0, trace_host, us);
+}
+extern "C" int cg_dbg_halo_trace2(cg_ctx* ctx, int B, int H, int C, int N, int BN, int pair,
+                                  long long* trace_host, double* us) {
   try {
     cudaStream_t st = (cudaStream_t)cg_ctx_stream(ctx);
     const int Hp = H + 2, rows = B * Hp * Hp;
@@ -103,8 +109,9 @@ extern "C" int cg_dbg_halo_trace(cg_ctx* ctx, int B, int H, int C, int N, int BN
     CG_CUDA(cudaMemset(dtr, 0, 8 * 64 * 8));
     Operand oa, ob;
     make_operand(oa, dA, rows, C, 128 + 2 * (Hp + 1));
-    make_operand(ob, dB, N, 9 * C, BN);
+    make_operand(ob, dB, N, 9 * C, pair ? BN / 2 : BN);
     ConvGemmArgs a{};
+    a.pair = pair;
     a.M = rows;
     a.N = N;
     a.Kc = C;
@@ -180,9 +187,12 @@ extern "C" int cg_dbg_gemm_trace_mode(cg_ctx* ctx, int M, int N, int K, int BN, 
       CG_CUDA(cudaMemset(dres, 0x11, (size_t)M * N * 2));
     }
     Operand oa, ob;
+    const int pair = (residual >> 1) & 1;
+    residual &= 1;
     make_operand(oa, dA, M, K, 128);
-    make_operand(ob, dB, N, K, BN);
+    make_operand(ob, dB, N, K, pair ? BN / 2 : BN);
     ConvGemmArgs a{};
+    a.pair = pair;
     a.M = M;
     a.N = N;
     a.Kc = K;
@@ -226,7 +236,8 @@ extern "C" int cg_dbg_gemm_trace_mode(cg_ctx* ctx, int M, int N, int K, int BN, 
 static int dbg_conv_gemm(cg_ctx* ctx, const uint16_t* A, int rowsA, const uint16_t* B, int N,
                          int Kc, int ntaps, const int* tap_off, const float* bias,
                          const uint16_t* residual, int relu, int row_mode, int H, int W, int M,
-                         int rows_out, int out_f32, int BN, void* out, int max_ctas, int halo_lo);
+                         int rows_out, int out_f32, int BN, void* out, int max_ctas, int halo_lo,
+                         int pair = 0);
 
 extern "C" int cg_dbg_conv_gemm(cg_ctx* ctx, const uint16_t* A, int rowsA,
                                 const uint16_t* B, int N, int Kc, int ntaps,
@@ -247,10 +258,30 @@ extern "C" int cg_dbg_conv_gemm_halo(cg_ctx* ctx, const uint16_t* A, int rowsA,
                        W, M, rows_out, 0, BN, out, 0, halo_lo);
 }
 
+extern "C" int cg_dbg_conv_gemm_pair(cg_ctx* ctx, const uint16_t* A, int rowsA,
+                                     const uint16_t* B, int N, int Kc, int ntaps,
+                                     const int* tap_off, const float* bias,
+                                     const uint16_t* residual, int relu, int row_mode, int H,
+                                     int W, int M, int rows_out, int out_f32, int BN, void* out,
+                                     int max_ctas) {
+  return dbg_conv_gemm(ctx, A, rowsA, B, N, Kc, ntaps, tap_off, bias, residual, relu, row_mode,
+                       H, W, M, rows_out, out_f32, BN, out, max_ctas, 0, 1);
+}
+
+extern "C" int cg_dbg_conv_gemm_halo_pair(cg_ctx* ctx, const uint16_t* A, int rowsA,
+                                          const uint16_t* B, int N, int Kc, int ntaps,
+                                          const int* tap_off, const float* bias, int relu,
+                                          int row_mode, int H, int W, int M, int rows_out,
+                                          int BN, void* out, int halo_lo) {
+  return dbg_conv_gemm(ctx, A, rowsA, B, N, Kc, ntaps, tap_off, bias, nullptr, relu, row_mode, H,
+                       W, M, rows_out, 0, BN, out, 0, halo_lo, 1);
+}
+
 static int dbg_conv_gemm(cg_ctx* ctx, const uint16_t* A, int rowsA, const uint16_t* B, int N,
                          int Kc, int ntaps, const int* tap_off, const float* bias,
                          const uint16_t* residual, int relu, int row_mode, int H, int W, int M,
-                         int rows_out, int out_f32, int BN, void* out, int max_ctas, int halo_lo) {
+                         int rows_out, int out_f32, int BN, void* out, int max_ctas, int halo_lo,
+                         int pair) {
   try {
     cudaStream_t st = (cudaStream_t)cg_ctx_stream(ctx);
     void *dA, *dB, *dbias, *dres = nullptr, *dout;
@@ -269,12 +300,13 @@ static int dbg_conv_gemm(cg_ctx* ctx, const uint16_t* A, int rowsA, const uint16
     }
     Operand oa, ob;
     make_operand(oa, dA, rowsA, Kc, 128 + 2 * halo_lo);
-    make_operand(ob, dB, N, ntaps * Kc, BN);
+    make_operand(ob, dB, N, ntaps * Kc, pair ? BN / 2 : BN);
     ConvGemmArgs a{};
     a.M = M;
     a.N = N;
     a.Kc = Kc;
     a.ntaps = ntaps;
+    a.pair = pair;
     for (int t = 0; t < ntaps; t++) a.tap_off[t] = tap_off[t];
     a.bias = (const float*)dbias;
     a.residual = (const __nv_bfloat16*)dres;

@@ -21,6 +21,10 @@ constexpr int BM = 128, BK = 64, kThreads = 352;
 constexpr int kEpiWarps = 8, kStgLd = 36;        // staging row stride (floats)
 constexpr int A_BYTES = BM * BK * 2;
 constexpr int kHaloBytes = 256 * BK * 2;  // largest halo box (BM + 2*halo_lo <= 256 rows)
+#ifndef CG_DIRECT_REMAP
+#define CG_DIRECT_REMAP 1
+#endif
+constexpr bool kDirectRemap = CG_DIRECT_REMAP != 0;  // thread-per-row remapped epilogue
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -114,6 +118,50 @@ __device__ __forceinline__ void stg_f4(void* p, float4 v) {
                "f"(v.z), "f"(v.w)
                : "memory");
 }
+// ---- SM-pair (cta_group::2) helpers
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// shared::cluster address of the same smem offset in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa_cluster(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(su32(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;"
+               ::: "memory");
+}
+// TMA into this CTA's smem, completion counted on the pair leader's mbarrier
+__device__ __forceinline__ void tma_load_2d_pair(const CUtensorMap* tm, uint32_t bar_cluster,
+                                                 void* dst, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(su32(dst)),
+      "l"(tm), "r"(bar_cluster), "r"(x), "r"(y)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit_pair(uint64_t* b) {  // both CTAs' barrier
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(su32(b)), "h"((uint16_t)3)
+      : "memory");
+}
+__device__ __forceinline__ void umma_bf16_pair(uint32_t d, uint64_t a, uint64_t b,
+                                               uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accum));
+}
+
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 }
@@ -254,10 +302,19 @@ __device__ __forceinline__ int remap_row(int M, int rows_out, int mode, int H,
       a.trace[(slot) * 64 + (i)] = clock64();                         \
   } while (0)
 
-template <int BN, int STAGES, int kResSlots, int HALO, int RESB>
+// PAIR: an SM pair (cluster of 2, cta_group::2) computes 256-row tiles: each
+// CTA loads its 128 rows of A (or its 128-row halo) and half of the weight
+// tile (BN/2 rows) with cta_group::2 TMA that completes on the leader's
+// barrier; the leader issues M=256 MMAs over both CTAs' shared memory and
+// commits to both CTAs' barriers; each CTA's epilogue drains its own TMEM
+// half and the peer releases the accumulator on the leader's barrier.
+// Per SM and 128x256 output this halves the weight bytes written to and read
+// from shared memory (the bound of the BN=256 mainloop).
+template <int BN, int STAGES, int kResSlots, int HALO, int RESB, int PAIR>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_gemm_kernel(const __grid_constant__ GemmGroupParams gp, const ConvGemmArgs a) {
-  constexpr int B_BYTES = BN * BK * 2;
+  static_assert(!PAIR || (RESB == 0 && (HALO == 0 || kResSlots == 0)), "pair: streamed weights");
+  constexpr int B_BYTES = (PAIR ? BN / 2 : BN) * BK * 2;  // this CTA's weight tile
   constexpr uint32_t TMEM_COLS = 2 * BN;
   extern __shared__ uint8_t smem_raw[];
   // 1024-aligned regions first: operand ring (128B swizzle), residual ring and
@@ -286,13 +343,20 @@ __global__ void __launch_bounds__(kThreads, 1)
   // tile order t -> (m block, replica r, n block): the replicas' tiles of one
   // row block run back to back, so an operand they share (the conv1 im2col
   // of the batch) is read from HBM once and from L2 by the other replicas
-  const int tiles = num_m * num_n * gp.n;
+  // pair: a tile is 256 rows (this CTA's 128-row half at crank * 128)
+  const uint32_t crank = PAIR ? cluster_rank() : 0;
+  constexpr int BMT = PAIR ? 2 * BM : BM;
+  const int num_mt = (a.M + BMT - 1) / BMT;
+  const int tiles = num_mt * num_n * gp.n;
+  const int t_first = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int t_step = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
   const int kpt = a.Kc / BK, num_k = a.ntaps * kpt;
+  (void)num_m;
   auto coords = [&](int t, int& r, int& m0, int& n0) {
     const int per_m = gp.n * num_n;
     const int mb = t / per_m, rem = t - mb * per_m;
     r = rem / num_n;
-    m0 = mb * BM;
+    m0 = mb * BMT + (int)crank * BM;
     n0 = (rem - r * num_n) * BN;
   };
 
@@ -313,7 +377,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int s = 0; s < 2; s++) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], kEpiWarps);
+      mbar_init(&tempty[s], kEpiWarps * (PAIR ? 2 : 1));  // pair: both CTAs' epilogues
     }
     for (int s = 0; s < kResSlots; s++) {
       mbar_init(&rfull[s], 1);
@@ -326,14 +390,23 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     su32(tmem_slot)),
-                 "r"(TMEM_COLS)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if constexpr (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       su32(tmem_slot)),
+                   "r"(TMEM_COLS)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       su32(tmem_slot)),
+                   "r"(TMEM_COLS)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if (PAIR) cluster_sync_all();  // peer barriers initialised before any remote arrive
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
@@ -344,7 +417,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int ti = 0;
       int hs = 0;
       uint32_t hphase = 0;
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x, ti++) {
+      for (int t = t_first; t < tiles; t += t_step, ti++) {
         int r, m0, n0;
         coords(t, r, m0, n0);
         CG_TRACE(0, ti);
@@ -366,6 +439,26 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           continue;
         }
+        if constexpr (PAIR && HALO > 0) {
+          // both CTAs load their halves; all completions land on the
+          // leader's barriers, which expect both CTAs' bytes
+          const int hrows = BM + 2 * a.halo_lo;
+          for (int cb = 0; cb < kpt; cb++) {
+            mbar_wait(&hempty[hs], hphase ^ 1);
+            if (crank == 0) mbar_expect_tx(&hfull[hs], 2 * hrows * BK * 2);
+            tma_load_2d_pair(&gp.A[r], mapa_cluster(&hfull[hs], 0), sA + hs * kHaloBytes, cb * BK,
+                             m0 - a.halo_lo);
+            if (++hs == HALO) { hs = 0; hphase ^= 1; }
+            for (int tap = 0; tap < a.ntaps; tap++) {
+              mbar_wait(&empty[stage], phase ^ 1);
+              if (crank == 0) mbar_expect_tx(&full[stage], 2 * B_BYTES);
+              tma_load_2d_pair(&gp.B[r], mapa_cluster(&full[stage], 0), sB + stage * B_BYTES,
+                               (tap * kpt + cb) * BK, n0 + (int)crank * (BN / 2));
+              if (++stage == STAGES) { stage = 0; phase ^= 1; }
+            }
+          }
+          continue;
+        }
         if constexpr (HALO > 0) {
           // per channel block: one halo box, then the 9 taps' weight tiles
           const int hrows = BM + 2 * a.halo_lo;
@@ -384,6 +477,22 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           continue;
         }
+        if constexpr (PAIR) {
+          // this CTA's 128 rows of A and half of the weight tile, completing
+          // on the leader's barrier (which expects both CTAs' bytes)
+          for (int kb = 0; kb < num_k; kb++) {
+            const int tap = kb / kpt, cb = kb - tap * kpt;
+            mbar_wait(&empty[stage], phase ^ 1);
+            if (kb == 0) CG_TRACE(1, ti);
+            uint32_t fb = mapa_cluster(&full[stage], 0);
+            if (crank == 0) mbar_expect_tx(&full[stage], 2 * (A_BYTES + B_BYTES));
+            tma_load_2d_pair(&gp.A[r], fb, sA + stage * A_BYTES, cb * BK, m0 + s_tap[tap]);
+            tma_load_2d_pair(&gp.B[r], fb, sB + stage * B_BYTES, kb * BK,
+                             n0 + (int)crank * (BN / 2));
+            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          }
+          continue;
+        }
         for (int kb = 0; kb < num_k; kb++) {
           const int tap = kb / kpt, cb = kb - tap * kpt;
           mbar_wait(&empty[stage], phase ^ 1);
@@ -397,14 +506,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // ---------------- MMA issuer
+    if (lane == 0 && crank == 0) {  // ---------------- MMA issuer
       // kind::f16 instruction descriptor: D f32, A/B bf16, K-major, M=128, N=BN
       const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) |
                              ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
       int stage = 0, acc = 0, hs = 0;
       uint32_t phase = 0, acc_phase = 0, hphase = 0;
       int ti = 0;
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x, ti++) {
+      for (int t = t_first; t < tiles; t += t_step, ti++) {
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         CG_TRACE(2, ti);
         tc_fence_after();
@@ -436,6 +545,56 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           umma_commit(&tfull[acc]);
           CG_TRACE(4, ti);
+          if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+          continue;
+        }
+        if constexpr (PAIR && HALO == 0) {
+          // leader: both CTAs' A rows and weight halves landed; M=256 MMAs
+          const uint32_t idesc2 = (1u << 4) | (1u << 7) | (1u << 10) |
+                                  ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+          const uint64_t ad0 = smem_desc_sw128(sA), bd0 = smem_desc_sw128(sB);
+          for (int kb = 0; kb < num_k; kb++) {
+            mbar_wait(&full[stage], phase);
+            if (kb == 0) CG_TRACE(3, ti);
+            tc_fence_after();
+            const uint64_t ad = ad0 + (uint64_t)((stage * A_BYTES) >> 4);
+            const uint64_t bd = bd0 + (uint64_t)((stage * B_BYTES) >> 4);
+#pragma unroll
+            for (int k = 0; k < BK / 16; k++)
+              umma_bf16_pair(d, ad + 2 * k, bd + 2 * k, idesc2, (kb | k) != 0);
+            umma_commit_pair(&empty[stage]);
+            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          }
+          umma_commit_pair(&tfull[acc]);
+          CG_TRACE(4, ti);
+          if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+          continue;
+        }
+        if constexpr (PAIR) {
+          // leader: wait for both CTAs' halo and weight halves, M=256 MMAs
+          const uint32_t idesc2 = (1u << 4) | (1u << 7) | (1u << 10) |
+                                  ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+          const uint32_t sA_u = su32(sA), sB_u = su32(sB);
+          for (int cb = 0; cb < kpt; cb++) {
+            mbar_wait(&hfull[hs], hphase);
+            tc_fence_after();
+            const uint32_t hbase = sA_u + (uint32_t)(hs * kHaloBytes + a.halo_lo * 128);
+#pragma unroll
+            for (int tap = 0; tap < 9; tap++) {
+              mbar_wait(&full[stage], phase);
+              tc_fence_after();
+              const uint64_t ad = smem_desc_sw128_row(hbase + (uint32_t)(a.tap_off[tap] * 128), 0);
+              const uint64_t bd = smem_desc_sw128_row(sB_u + (uint32_t)(stage * B_BYTES), 0);
+#pragma unroll
+              for (int k = 0; k < BK / 16; k++)
+                umma_bf16_pair(d, ad + 2 * k, bd + 2 * k, idesc2, (cb | tap | k) != 0);
+              umma_commit_pair(&empty[stage]);
+              if (++stage == STAGES) { stage = 0; phase ^= 1; }
+            }
+            umma_commit_pair(&hempty[hs]);
+            if (++hs == HALO) { hs = 0; hphase ^= 1; }
+          }
+          umma_commit_pair(&tfull[acc]);
           if (++acc == 2) { acc = 0; acc_phase ^= 1; }
           continue;
         }
@@ -489,7 +648,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (res_tma && lane == 0) {
       constexpr int CPT = BN / 32;
       int g = 0;
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+      for (int t = t_first; t < tiles; t += t_step) {
         int r, m0, n0;
         coords(t, r, m0, n0);
         for (int c = 0; c < CPT; c++, g++) {
@@ -519,11 +678,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     int tile_i = 0, acc = 0;
     int stage_seq = 0;  // staging buffer sequence across all of this warp's chunks
     uint32_t acc_phase = 0;
-    for (int t = blockIdx.x; t < tiles; t += gridDim.x, tile_i++) {
+    for (int t = t_first; t < tiles; t += t_step, tile_i++) {
       if (kTileSplit && (tile_i & 1) != h) {
         // the other group drains this accumulator; release our share of it
         __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[acc]);
+        if (lane == 0) {
+            if (PAIR && crank == 1) mbar_arrive_cluster(mapa_cluster(&tempty[acc], 0));
+            else mbar_arrive(&tempty[acc]);
+          }
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         continue;
       }
@@ -550,7 +712,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (c + C0S >= CPT) {  // this warp's last chunk: hand TMEM back early
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty[acc]);
+          if (lane == 0) {
+            if (PAIR && crank == 1) mbar_arrive_cluster(mapa_cluster(&tempty[acc], 0));
+            else mbar_arrive(&tempty[acc]);
+          }
         }
         if (tma_out) {
           // thread = row: bias (+ residual row from the 64B-swizzled ring) +
@@ -608,6 +773,43 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (lane == 0) {
             tma_store_2d(&gp.O[r_], sb, n, m0 + q * 32);
             bulk_commit();
+          }
+          continue;
+        }
+        if (kDirectRemap && !a.out_f32 && !res_r) {
+          // remapped rows, bf16 out, no residual (the 3x3 / 1x1 grid layers):
+          // thread = row; bias + activation + pack in registers, then the
+          // row's 64 bytes go straight to its remapped output row
+          const int n = n0 + c * 32;
+          float x[32];
+#pragma unroll
+          for (int j = 0; j < 8; j++) {
+            const float4 b4 = n + 4 * j < a.N
+                                  ? __ldg(reinterpret_cast<const float4*>(bias_r + n) + j)
+                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+            x[4 * j] = __uint_as_float(v[4 * j]) + b4.x;
+            x[4 * j + 1] = __uint_as_float(v[4 * j + 1]) + b4.y;
+            x[4 * j + 2] = __uint_as_float(v[4 * j + 2]) + b4.z;
+            x[4 * j + 3] = __uint_as_float(v[4 * j + 3]) + b4.w;
+          }
+          if (c + C0S < CPT) tmem_ld32_issue(trow + (c + C0S) * 32, v);
+          if (a.relu) {
+            const float hi = a.relu == 2 ? 6.f : INFINITY;
+#pragma unroll
+            for (int j = 0; j < 32; j++) x[j] = fminf(fmaxf(x[j], 0.f), hi);
+          }
+          uint32_t o[16];
+#pragma unroll
+          for (int j = 0; j < 16; j++) {
+            __nv_bfloat162 t2 = __floats2bfloat162_rn(x[2 * j], x[2 * j + 1]);
+            o[j] = *reinterpret_cast<uint32_t*>(&t2);
+          }
+          if (my_orow >= 0 && n < a.N) {
+            __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(out_r) +
+                                 (size_t)my_orow * a.ld_out + n;
+#pragma unroll
+            for (int j = 0; j < 4; j++)
+              stg_u4(dst + 8 * j, make_uint4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]));
           }
           continue;
         }
@@ -680,12 +882,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     if (tma_out && lane == 0) bulk_wait_all();  // this warp's stores read their staging
   }
-  __syncthreads();
+  tc_fence_before();
+  if (PAIR) cluster_sync_all();  // both CTAs done with the pair's TMEM
+  else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                 "r"(TMEM_COLS)
-                 : "memory");
+    if constexpr (PAIR)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                   "r"(TMEM_COLS)
+                   : "memory");
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                   "r"(TMEM_COLS)
+                   : "memory");
   }
 }
 
@@ -708,22 +917,22 @@ EncodeFn get_encode() {
   return fn;
 }
 
-template <int BN, int STAGES, int kResSlots, int HALO, int RESB>
+template <int BN, int STAGES, int kResSlots, int HALO, int RESB, int PAIR = 0>
 constexpr int smem_bytes() {
   return 1024 + (HALO > 0 ? HALO * kHaloBytes : STAGES * A_BYTES) +
-         (RESB > STAGES ? RESB : STAGES) * BN * BK * 2 +
+         (RESB > STAGES ? RESB : STAGES) * (PAIR ? BN / 2 : BN) * BK * 2 +
          kResSlots * 8192 + kEpiWarps * 32 * kStgLd * 4 +
          8 * (2 * STAGES + 4 + 2 * (kResSlots > 0 ? kResSlots : 1) + 2 * (HALO > 0 ? HALO : 1)) +
          16 + 48;
 }
 
-template <int BN, int STAGES, int RS, int HALO = 0, int RESB = 0>
+template <int BN, int STAGES, int RS, int HALO = 0, int RESB = 0, int PAIR = 0>
 void launch_t(const PreparedGemm& p, cudaStream_t st, int max_ctas) {
   static bool attr = false;
-  constexpr int smem = smem_bytes<BN, STAGES, RS, HALO, RESB>();
+  constexpr int smem = smem_bytes<BN, STAGES, RS, HALO, RESB, PAIR>();
   static_assert(smem <= 232448, "smem budget");
   if (!attr) {
-    CG_CUDA(cudaFuncSetAttribute(conv_gemm_kernel<BN, STAGES, RS, HALO, RESB>,
+    CG_CUDA(cudaFuncSetAttribute(conv_gemm_kernel<BN, STAGES, RS, HALO, RESB, PAIR>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr = true;
   }
@@ -737,8 +946,33 @@ void launch_t(const PreparedGemm& p, cudaStream_t st, int max_ctas) {
     if (grid < p.gp.n) throw InvalidArgument("conv_gemm: grid too small for resident weights");
   }
   timer_begin(st, kTimeGemm);
-  conv_gemm_kernel<BN, STAGES, RS, HALO, RESB><<<grid, kThreads, smem, st>>>(p.gp, a);
-  CG_CHECK_LAUNCH();
+  if constexpr (PAIR) {
+    // SM pairs: a cluster of 2 CTAs per 256-row tile
+    const int pair_tiles = ((a.M + 2 * BM - 1) / (2 * BM)) * ((a.N + BN - 1) / BN) * p.gp.n;
+    // a pair needs both SMs of a TPC: each SM held back from the budget (by
+    // a concurrent chain CTA) can block one TPC
+    const int tpcs = kNumSMs / 2 - (kNumSMs - budget);
+    int g2 = std::min(2 * pair_tiles, 2 * std::max(tpcs, 1));
+    if (max_ctas > 0) g2 = std::min(g2, max_ctas - (max_ctas & 1));
+    if (g2 < 2) throw InvalidArgument("conv_gemm: an SM pair needs 2 CTAs");
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)g2);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr2[1];
+    attr2[0].id = cudaLaunchAttributeClusterDimension;
+    attr2[0].val.clusterDim.x = 2;
+    attr2[0].val.clusterDim.y = 1;
+    attr2[0].val.clusterDim.z = 1;
+    cfg.attrs = attr2;
+    cfg.numAttrs = 1;
+    CG_CUDA(cudaLaunchKernelEx(&cfg, conv_gemm_kernel<BN, STAGES, RS, HALO, RESB, PAIR>, p.gp, a));
+    launch_counter_add(1);
+  } else {
+    conv_gemm_kernel<BN, STAGES, RS, HALO, RESB, PAIR><<<grid, kThreads, smem, st>>>(p.gp, a);
+    CG_CHECK_LAUNCH();
+  }
   timer_end(st, kTimeGemm);
 }
 
@@ -950,7 +1184,7 @@ void prepare_conv_gemm(PreparedGemm& p, const ConvGemmGroup& g, const ConvGemmAr
     if (a.tap_off[t] < -a.halo_lo || a.tap_off[t] > a.halo_lo)
       throw InvalidArgument("conv_gemm: tap outside the halo");
   for (int r = 0; r < g.n; r++) {
-    if (g.A[r]->box_rows != BM + 2 * a.halo_lo || g.B[r]->box_rows != BN)
+    if (g.A[r]->box_rows != BM + 2 * a.halo_lo || g.B[r]->box_rows != (a.pair ? BN / 2 : BN))
       throw InvalidArgument("conv_gemm: box mismatch");
     if ((g.residual[r] != nullptr) != (g.residual[0] != nullptr))
       throw InvalidArgument("conv_gemm: residual on some replicas only");
@@ -978,6 +1212,18 @@ void prepare_conv_gemm(PreparedGemm& p, const ConvGemmGroup& g, const ConvGemmAr
 }
 
 void launch_prepared(const PreparedGemm& p, cudaStream_t st, int max_ctas) {
+  if (p.args.pair) {
+    if (p.args.halo_lo > 0) {
+      if (p.BN != 128 || p.res)
+        throw InvalidArgument("conv_gemm: halo SM pairs only for 128-wide tiles");
+      launch_t<128, 7, 0, 2, 0, 1>(p, st, max_ctas);
+      return;
+    }
+    if (p.BN != 256) throw InvalidArgument("conv_gemm: SM pairs only for 256-wide tiles");
+    if (p.res) launch_t<256, 3, 10, 0, 0, 1>(p, st, max_ctas);
+    else launch_t<256, 5, 0, 0, 0, 1>(p, st, max_ctas);
+    return;
+  }
   if (p.args.halo_lo > 0) {
     if (p.res) throw InvalidArgument("conv_gemm: halo mode has no residual ring");
     // small weight sets (one n block, 9 x 64-channel taps): keep B resident

@@ -55,6 +55,7 @@ struct ConvGemmArgs {
   // one BM-row box per tap. 0 = off. The A operand's box must then have
   // BM + 2*halo_lo (<= 256) rows.
   int halo_lo;
+  int pair;  // 1: SM-pair (cta_group::2) 256-row tiles, B operand box = BN/2 rows
 };
 
 // One encoded operand (tensor map over a row-major bf16 [rows, cols] matrix

@@ -18,14 +18,15 @@ def bf16_bits(x: torch.Tensor) -> np.ndarray:
 
 
 def run_gemm(ctx, A, Bw, N, Kc, ntaps, taps, bias, residual, relu, mode, H, W, M,
-             rows_out, out_f32, BN, max_ctas=0):
+             rows_out, out_f32, BN, max_ctas=0, pair=0):
     a = bf16_bits(A)
     b = bf16_bits(Bw)
     res = None if residual is None else bf16_bits(residual)
     t = np.array(list(taps) + [0] * (9 - len(taps)), np.int32)
     bias = np.ascontiguousarray(bias, np.float32)
     out = np.zeros((rows_out, N), np.float32 if out_f32 else np.uint16)
-    rc = ctx.L.cg_dbg_conv_gemm(
+    fn = ctx.L.cg_dbg_conv_gemm_pair if pair else ctx.L.cg_dbg_conv_gemm
+    rc = fn(
         ctx.h, a.ctypes.data_as(C.c_void_p), A.shape[0], b.ctypes.data_as(C.c_void_p),
         N, Kc, ntaps, t.ctypes.data_as(C.c_void_p), bias.ctypes.data_as(C.c_void_p),
         None if res is None else res.ctypes.data_as(C.c_void_p), relu, mode, H, W, M,
@@ -80,6 +81,50 @@ def test_gemm_residual_and_f32_tail(ctx):
     assert torch.allclose(got, ref, rtol=1e-4, atol=1e-3)
 
 
+@pytest.mark.parametrize("M,N,Kc,res,relu,max_ctas,out_f32", [
+    (300, 256, 256, 0, 1, 0, 0), (777, 512, 192, 1, 1, 0, 0), (2048, 1024, 512, 1, 0, 6, 0),
+    (128, 256, 64, 1, 1, 0, 0), (5000, 2048, 128, 0, 1, 0, 0), (256, 1000, 128, 0, 0, 0, 1)])
+def test_gemm_pair(ctx, M, N, Kc, res, relu, max_ctas, out_f32):
+    """SM-pair (cta_group::2) 256 x 256 tiles: ragged row tails (a peer CTA
+    with no rows), the residual ring, a capped grid, f32 logits (FC shape)."""
+    g = torch.Generator().manual_seed(M + 7 * N)
+    A = torch.rand(M, Kc, generator=g) * 2 - 1
+    Bw = torch.rand(N, Kc, generator=g) * 2 - 1
+    R = torch.rand(M, N, generator=g) * 2 - 1 if res else None
+    bias = torch.rand(N, generator=g) - 0.5
+    got = run_gemm(ctx, A, Bw, N, Kc, 1, [0], bias, R, relu, 0, 0, 0, M, M, out_f32, 256,
+                   max_ctas, pair=1)
+    ref = q(A) @ q(Bw).T + bias
+    if res:
+        ref = ref + q(R)
+    if relu:
+        ref = ref.clamp_min(0)
+    if out_f32:
+        assert torch.allclose(got, ref, rtol=1e-4, atol=1e-3)
+    else:
+        close(got, ref)
+
+
+def test_gemm_pair_taps_remap(ctx):
+    """SM pairs over 9 row-shifted taps with a row remap (PadToCompact)."""
+    NB, H, C, Cout = 2, 14, 64, 256
+    W = H
+    g = torch.Generator().manual_seed(11)
+    x = torch.rand(NB, C, H, W, generator=g) * 2 - 1
+    w = (torch.rand(Cout, C, 3, 3, generator=g) * 2 - 1) / 3
+    bias = torch.rand(Cout, generator=g) - 0.5
+    xp = torch.nn.functional.pad(q(x), (1, 1, 1, 1))
+    A = xp.permute(0, 2, 3, 1).reshape(-1, C)
+    Wp = W + 2
+    taps = [(dr - 1) * Wp + (ds - 1) for dr in range(3) for ds in range(3)]
+    Bw = q(w).permute(0, 2, 3, 1).reshape(Cout, 9 * C)
+    M = NB * (H + 2) * Wp
+    got = run_gemm(ctx, A, Bw, Cout, C, 9, taps, bias, None, 1, 1, H, W, M, NB * H * W, 0, 256,
+                   pair=1)
+    ref = torch.nn.functional.conv2d(q(x), q(w), bias, padding=1).clamp_min(0)
+    close(got, ref.permute(0, 2, 3, 1).reshape(-1, Cout))
+
+
 @pytest.mark.parametrize("NB,H,C,Cout,BN", [(3, 7, 64, 128, 128), (2, 14, 128, 64, 64),
                                             (2, 28, 64, 256, 256)])
 def test_conv3x3_padded_grid(ctx, NB, H, C, Cout, BN):
@@ -102,18 +147,63 @@ def test_conv3x3_padded_grid(ctx, NB, H, C, Cout, BN):
     close(got, ref)
 
 
-def run_halo(ctx, A, Bw, N, Kc, taps, bias, H, W, M, rows_out, BN, halo_lo):
+def run_halo(ctx, A, Bw, N, Kc, taps, bias, H, W, M, rows_out, BN, halo_lo, pair=False):
     a = bf16_bits(A)
     b = bf16_bits(Bw)
     t = np.array(list(taps), np.int32)
     bias = np.ascontiguousarray(bias, np.float32)
     out = np.zeros((rows_out, N), np.uint16)
-    rc = ctx.L.cg_dbg_conv_gemm_halo(
+    fn = ctx.L.cg_dbg_conv_gemm_halo_pair if pair else ctx.L.cg_dbg_conv_gemm_halo
+    rc = fn(
         ctx.h, a.ctypes.data_as(C.c_void_p), A.shape[0], b.ctypes.data_as(C.c_void_p), N, Kc,
         9, t.ctypes.data_as(C.c_void_p), bias.ctypes.data_as(C.c_void_p), 1, 1, H, W, M,
         rows_out, BN, out.ctypes.data_as(C.c_void_p), halo_lo)
     assert rc == 0, ctx.L.cg_last_error(ctx.h)
     return torch.from_numpy(out.view(np.int16)).view(torch.bfloat16).float()
+
+
+@pytest.mark.parametrize("M,N,Kc,res,relu,max_ctas,out_f32", [
+    (300, 256, 256, 0, 1, 0, 0), (777, 512, 192, 1, 1, 0, 0), (2048, 1024, 512, 1, 0, 6, 0),
+    (128, 256, 64, 1, 1, 0, 0), (5000, 2048, 128, 0, 1, 0, 0), (256, 1000, 128, 0, 0, 0, 1)])
+def test_gemm_pair(ctx, M, N, Kc, res, relu, max_ctas, out_f32):
+    """SM-pair (cta_group::2) 256 x 256 tiles: ragged row tails (a peer CTA
+    with no rows), the residual ring, a capped grid, f32 logits (FC shape)."""
+    g = torch.Generator().manual_seed(M + 7 * N)
+    A = torch.rand(M, Kc, generator=g) * 2 - 1
+    Bw = torch.rand(N, Kc, generator=g) * 2 - 1
+    R = torch.rand(M, N, generator=g) * 2 - 1 if res else None
+    bias = torch.rand(N, generator=g) - 0.5
+    got = run_gemm(ctx, A, Bw, N, Kc, 1, [0], bias, R, relu, 0, 0, 0, M, M, out_f32, 256,
+                   max_ctas, pair=1)
+    ref = q(A) @ q(Bw).T + bias
+    if res:
+        ref = ref + q(R)
+    if relu:
+        ref = ref.clamp_min(0)
+    if out_f32:
+        assert torch.allclose(got, ref, rtol=1e-4, atol=1e-3)
+    else:
+        close(got, ref)
+
+
+def test_gemm_pair_taps_remap(ctx):
+    """SM pairs over 9 row-shifted taps with a row remap (PadToCompact)."""
+    NB, H, C, Cout = 2, 14, 64, 256
+    W = H
+    g = torch.Generator().manual_seed(11)
+    x = torch.rand(NB, C, H, W, generator=g) * 2 - 1
+    w = (torch.rand(Cout, C, 3, 3, generator=g) * 2 - 1) / 3
+    bias = torch.rand(Cout, generator=g) - 0.5
+    xp = torch.nn.functional.pad(q(x), (1, 1, 1, 1))
+    A = xp.permute(0, 2, 3, 1).reshape(-1, C)
+    Wp = W + 2
+    taps = [(dr - 1) * Wp + (ds - 1) for dr in range(3) for ds in range(3)]
+    Bw = q(w).permute(0, 2, 3, 1).reshape(Cout, 9 * C)
+    M = NB * (H + 2) * Wp
+    got = run_gemm(ctx, A, Bw, Cout, C, 9, taps, bias, None, 1, 1, H, W, M, NB * H * W, 0, 256,
+                   pair=1)
+    ref = torch.nn.functional.conv2d(q(x), q(w), bias, padding=1).clamp_min(0)
+    close(got, ref.permute(0, 2, 3, 1).reshape(-1, Cout))
 
 
 @pytest.mark.parametrize("NB,H,C,Cout,BN", [(3, 7, 64, 128, 128), (2, 14, 128, 64, 64),
@@ -170,3 +260,24 @@ def test_gemm_many_tiles_per_cta_tma_store(ctx, BN):
         got = run_gemm(ctx, A, Bw, N, Kc, 1, [0], bias, res, 1, 0, 0, 0, M, M, 0, BN, max_ctas=2)
         ref = q(A) @ q(Bw).T + bias + (0 if res is None else q(res))
         close(got, ref.clamp_min(0))
+
+
+@pytest.mark.parametrize("NB,H,C,Cout", [(3, 7, 64, 128), (2, 28, 128, 128), (1, 14, 256, 512)])
+def test_conv3x3_halo_sm_pair(ctx, NB, H, C, Cout):
+    """SM-pair halo mode (cluster of 2, cta_group::2 M=256 MMAs over both
+    CTAs' shared memory, weights split by N across the pair) == torch."""
+    W = H
+    g = torch.Generator().manual_seed(H * C + 7)
+    x = torch.rand(NB, C, H, W, generator=g) * 2 - 1
+    w = (torch.rand(Cout, C, 3, 3, generator=g) * 2 - 1) / 3
+    bias = torch.rand(Cout, generator=g) - 0.5
+    xp = torch.nn.functional.pad(q(x), (1, 1, 1, 1))
+    A = xp.permute(0, 2, 3, 1).reshape(-1, C)
+    Wp = W + 2
+    taps = [(dr - 1) * Wp + (ds - 1) for dr in range(3) for ds in range(3)]
+    Bw = q(w).permute(0, 2, 3, 1).reshape(Cout, 9 * C)
+    M = NB * (H + 2) * Wp
+    ref = torch.nn.functional.conv2d(q(x), q(w), bias, padding=1).clamp_min(0)
+    ref = ref.permute(0, 2, 3, 1).reshape(-1, Cout)
+    got = run_halo(ctx, A, Bw, Cout, C, taps, bias, H, W, M, NB * H * W, 128, Wp + 1, pair=True)
+    close(got, ref)
