@@ -21,6 +21,9 @@ constexpr int BM = 128, BK = 64, kThreads = 352;
 constexpr int kEpiWarps = 8, kStgLd = 36;        // staging row stride (floats)
 constexpr int A_BYTES = BM * BK * 2;
 constexpr int kHaloBytes = 256 * BK * 2;  // largest halo box (BM + 2*halo_lo <= 256 rows)
+#ifndef CG_RES_COLS
+#define CG_RES_COLS 64
+#endif
 #ifndef CG_DIRECT_REMAP
 #define CG_DIRECT_REMAP 1
 #endif
@@ -316,6 +319,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   static_assert(!PAIR || (RESB == 0 && (HALO == 0 || kResSlots == 0)), "pair: streamed weights");
   constexpr int B_BYTES = (PAIR ? BN / 2 : BN) * BK * 2;  // this CTA's weight tile
   constexpr uint32_t TMEM_COLS = 2 * BN;
+  // residual ring: 128-row boxes of kResCols columns (64: 128-byte rows, SW128;
+  // half the TMA row requests of 32-column SW64 boxes) in kResSlots x 8 KB
+  constexpr int kResCols = CG_RES_COLS;
+  constexpr int kResBox = 128 * kResCols * 2;
+  constexpr int kRS = kResSlots > 0 ? kResSlots * 8192 / kResBox : 1;
   extern __shared__ uint8_t smem_raw[];
   // 1024-aligned regions first: operand ring (128B swizzle), residual ring and
   // output staging (64B swizzle), then barriers.
@@ -381,7 +389,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int s = 0; s < kResSlots; s++) {
       mbar_init(&rfull[s], 1);
-      mbar_init(&rempty[s], 4);
+      mbar_init(&rempty[s], 4 * (kResCols / 32));  // 4 warps x the box's 32-col chunks
     }
     for (int s = 0; s < HALO; s++) {
       mbar_init(&hfull[s], 1);
@@ -409,6 +417,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // Programmatic dependent launch: the setup above (barriers, TMEM, tensor
+  // map prefetch) overlapped the previous launch's tail; wait for that grid
+  // and its memory before reading activations or writing outputs, and let
+  // the next launch's CTAs take SMs as this grid's CTAs retire.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer
@@ -646,16 +660,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ---------------- residual loader: streams [128 x 32] residual chunks
     // through the ring in epilogue order, as far ahead as the slots allow.
     if (res_tma && lane == 0) {
-      constexpr int CPT = BN / 32;
       int g = 0;
       for (int t = t_first; t < tiles; t += t_step) {
         int r, m0, n0;
         coords(t, r, m0, n0);
-        for (int c = 0; c < CPT; c++, g++) {
-          const int slot = g % (kResSlots > 0 ? kResSlots : 1);
-          if (g >= kResSlots) mbar_wait(&rempty[slot], ((g / kResSlots) - 1) & 1);
-          mbar_expect_tx(&rfull[slot], 128 * 32 * 2);
-          tma_load_2d(&gp.R[r], &rfull[slot], s_res + slot * 8192, n0 + c * 32, m0);
+        for (int c = 0; c < BN / kResCols; c++, g++) {
+          const int slot = g % kRS;
+          if (g >= kRS) mbar_wait(&rempty[slot], ((g / kRS) - 1) & 1);
+          mbar_expect_tx(&rfull[slot], kResBox);
+          tma_load_2d(&gp.R[r], &rfull[slot], s_res + slot * kResBox, n0 + c * kResCols, m0);
         }
       }
     }
@@ -733,13 +746,18 @@ __global__ void __launch_bounds__(kThreads, 1)
             x[4 * j + 3] = __uint_as_float(v[4 * j + 3]) + b4.w;
           }
           if (c + C0S < CPT) tmem_ld32_issue(trow + (c + C0S) * 32, v);
-          const int slot = kResSlots > 0 ? g % kResSlots : 0;
           if (res_tma) {
-            mbar_wait(&rfull[slot], (g / (kResSlots > 0 ? kResSlots : 1)) & 1);
-            const uint32_t rb = su32(s_res + slot * 8192 + q * 32 * 64);
+            // box gq of this CTA's residual stream holds chunk c's columns
+            const int gq = tile_i * (BN / kResCols) + c / (kResCols / 32);
+            const int slot = gq % kRS;
+            mbar_wait(&rfull[slot], (gq / kRS) & 1);
+            const uint32_t rb = su32(s_res + slot * kResBox + q * 32 * kResCols * 2);
 #pragma unroll
             for (int j = 0; j < 4; j++) {
-              const uint4 rv = lds_u4(rb + sw64(lane, j));
+              const uint4 rv =
+                  lds_u4(rb + (kResCols == 64 ? (uint32_t)(lane * 128 +
+                                                           16 * ((((c & 1) * 4) + j) ^ (lane & 7)))
+                                              : sw64(lane, j)));
               const uint32_t w[4] = {rv.x, rv.y, rv.z, rv.w};
 #pragma unroll
               for (int e = 0; e < 4; e++) {
@@ -926,6 +944,9 @@ constexpr int smem_bytes() {
          16 + 48;
 }
 
+// env CREDO_NO_PDL: plain stream serialisation between GEMM launches (A/B)
+const int g_pdl = std::getenv("CREDO_NO_PDL") == nullptr ? 1 : 0;
+
 template <int BN, int STAGES, int RS, int HALO = 0, int RESB = 0, int PAIR = 0>
 void launch_t(const PreparedGemm& p, cudaStream_t st, int max_ctas) {
   static bool attr = false;
@@ -960,18 +981,31 @@ void launch_t(const PreparedGemm& p, cudaStream_t st, int max_ctas) {
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute attr2[1];
+    cudaLaunchAttribute attr2[2];
     attr2[0].id = cudaLaunchAttributeClusterDimension;
     attr2[0].val.clusterDim.x = 2;
     attr2[0].val.clusterDim.y = 1;
     attr2[0].val.clusterDim.z = 1;
+    attr2[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr2[1].val.programmaticStreamSerializationAllowed = g_pdl;
     cfg.attrs = attr2;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     CG_CUDA(cudaLaunchKernelEx(&cfg, conv_gemm_kernel<BN, STAGES, RS, HALO, RESB, PAIR>, p.gp, a));
     launch_counter_add(1);
   } else {
-    conv_gemm_kernel<BN, STAGES, RS, HALO, RESB, PAIR><<<grid, kThreads, smem, st>>>(p.gp, a);
-    CG_CHECK_LAUNCH();
+    // programmatic dependent launch (the kernel waits on griddepcontrol)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = g_pdl;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CG_CUDA(cudaLaunchKernelEx(&cfg, conv_gemm_kernel<BN, STAGES, RS, HALO, RESB, PAIR>, p.gp, a));
+    launch_counter_add(1);
   }
   timer_end(st, kTimeGemm);
 }
@@ -1169,6 +1203,20 @@ static void map64(CUtensorMap& m, const void* p, int ld, int rows, int box_rows)
   if (r != CUDA_SUCCESS) throw CudaError("epilogue tensor map failed");
 }
 
+// [rows, ld] bf16 map with a 64-column x 128-row box, 128B swizzle: the
+// residual ring's boxes.
+static void map128_res(CUtensorMap& m, const void* p, int ld, int rows) {
+  cuuint64_t dims[2] = {(cuuint64_t)ld, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+  cuuint32_t box[2] = {64, 128};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = get_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(p), dims,
+                            strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw CudaError("residual tensor map failed");
+}
+
 void prepare_conv_gemm(PreparedGemm& p, const ConvGemmGroup& g, const ConvGemmArgs& a, int BN) {
   if (a.Kc % 64 || a.ntaps < 1 || a.ntaps > 9) throw InvalidArgument("conv_gemm: bad K");
   if (!a.out_f32 && (a.N % 32)) throw InvalidArgument("conv_gemm: bf16 out needs N%32==0");
@@ -1200,7 +1248,8 @@ void prepare_conv_gemm(PreparedGemm& p, const ConvGemmGroup& g, const ConvGemmAr
       if (g.residual[r]) {
         if (a.ld_res % 8 || reinterpret_cast<uintptr_t>(g.residual[r]) % 16)
           throw InvalidArgument("conv_gemm: residual must be 16B aligned");
-        map64(p.gp.R[r], g.residual[r], a.ld_res, a.rows_out, 128);
+        if (CG_RES_COLS == 64) map128_res(p.gp.R[r], g.residual[r], a.ld_res, a.rows_out);
+        else map64(p.gp.R[r], g.residual[r], a.ld_res, a.rows_out, 128);
       }
     }
   }
@@ -1239,13 +1288,30 @@ void launch_prepared(const PreparedGemm& p, cudaStream_t st, int max_ctas) {
       default: throw InvalidArgument("conv_gemm: BN must be 64, 128 or 256");
     }
   }
+  // Residual layers share shared memory between mainloop stages and the
+  // residual ring: short K (< 8 k-blocks per tile) is epilogue-bound and
+  // wants the deep ring; long K starves a 2-stage mainloop (measured: ResNet
+  // stage-4 c3, K = 512: 60 -> 46 us with 3 stages and a 2-box ring).
+#ifndef CG_RES_DEEPK
+#define CG_RES_DEEPK 1
+#endif
+  const bool deep_k = CG_RES_DEEPK && p.args.Kc * p.args.ntaps >= 8 * BK;
   switch (p.BN * 2 + (p.res ? 1 : 0)) {
     case 128: launch_t<64, 7, 0>(p, st, max_ctas); break;  // (p.BN * 2 + residual)
-    case 129: launch_t<64, 4, 10>(p, st, max_ctas); break;
+    case 129:
+      if (deep_k) launch_t<64, 5, 6>(p, st, max_ctas);
+      else launch_t<64, 4, 10>(p, st, max_ctas);
+      break;
     case 256: launch_t<128, 5, 0>(p, st, max_ctas); break;
-    case 257: launch_t<128, 3, 10>(p, st, max_ctas); break;
+    case 257:
+      if (deep_k) launch_t<128, 4, 6>(p, st, max_ctas);
+      else launch_t<128, 3, 10>(p, st, max_ctas);
+      break;
     case 512: launch_t<256, 3, 0>(p, st, max_ctas); break;
-    case 513: launch_t<256, 2, 10>(p, st, max_ctas); break;
+    case 513:
+      if (deep_k) launch_t<256, 3, 4>(p, st, max_ctas);
+      else launch_t<256, 2, 10>(p, st, max_ctas);
+      break;
     default: throw InvalidArgument("conv_gemm: BN must be 64, 128 or 256");
   }
 }

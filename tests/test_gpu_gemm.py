@@ -81,6 +81,20 @@ def test_gemm_residual_and_f32_tail(ctx):
     assert torch.allclose(got, ref, rtol=1e-4, atol=1e-3)
 
 
+@pytest.mark.parametrize("M,N,Kc,BN", [(700, 512, 640, 256), (1500, 256, 512, 128),
+                                        (333, 128, 1024, 64), (2000, 1024, 256, 256)])
+def test_gemm_residual_ring_configs(ctx, M, N, Kc, BN):
+    """Both residual-ring layouts (deep ring for short K, more mainloop
+    stages for K >= 512) over ragged tails."""
+    g = torch.Generator().manual_seed(M * 3 + Kc)
+    A = torch.rand(M, Kc, generator=g) * 2 - 1
+    Bw = (torch.rand(N, Kc, generator=g) * 2 - 1) / 8
+    R = torch.rand(M, N, generator=g) * 2 - 1
+    bias = torch.rand(N, generator=g) - 0.5
+    got = run_gemm(ctx, A, Bw, N, Kc, 1, [0], bias, R, 1, 0, 0, 0, M, M, 0, BN)
+    close(got, (q(A) @ q(Bw).T + bias + q(R)).clamp_min(0))
+
+
 @pytest.mark.parametrize("M,N,Kc,res,relu,max_ctas,out_f32", [
     (300, 256, 256, 0, 1, 0, 0), (777, 512, 192, 1, 1, 0, 0), (2048, 1024, 512, 1, 0, 6, 0),
     (128, 256, 64, 1, 1, 0, 0), (5000, 2048, 128, 0, 1, 0, 0), (256, 1000, 128, 0, 0, 0, 1)])
@@ -160,6 +174,20 @@ def run_halo(ctx, A, Bw, N, Kc, taps, bias, H, W, M, rows_out, BN, halo_lo, pair
         rows_out, BN, out.ctypes.data_as(C.c_void_p), halo_lo)
     assert rc == 0, ctx.L.cg_last_error(ctx.h)
     return torch.from_numpy(out.view(np.int16)).view(torch.bfloat16).float()
+
+
+@pytest.mark.parametrize("M,N,Kc,BN", [(700, 512, 640, 256), (1500, 256, 512, 128),
+                                        (333, 128, 1024, 64), (2000, 1024, 256, 256)])
+def test_gemm_residual_ring_configs(ctx, M, N, Kc, BN):
+    """Both residual-ring layouts (deep ring for short K, more mainloop
+    stages for K >= 512) over ragged tails."""
+    g = torch.Generator().manual_seed(M * 3 + Kc)
+    A = torch.rand(M, Kc, generator=g) * 2 - 1
+    Bw = (torch.rand(N, Kc, generator=g) * 2 - 1) / 8
+    R = torch.rand(M, N, generator=g) * 2 - 1
+    bias = torch.rand(N, generator=g) - 0.5
+    got = run_gemm(ctx, A, Bw, N, Kc, 1, [0], bias, R, 1, 0, 0, 0, M, M, 0, BN)
+    close(got, (q(A) @ q(Bw).T + bias + q(R)).clamp_min(0))
 
 
 @pytest.mark.parametrize("M,N,Kc,res,relu,max_ctas,out_f32", [

@@ -30,7 +30,10 @@ shapes = [("square K2048", 32768, 2048, 2048, 256, 0),
           ("l3 c1", 75264, 256, 1024, 256, 0),
           ("l3 c1 BN128", 75264, 256, 1024, 128, 0),
           ("l4 c1", 18816, 512, 2048, 256, 0)]
+only = sys.argv[1] if len(sys.argv) > 1 else None  # run one shape (for ncu)
 for label, M, N, K, BN, res in shapes:
+    if only and label != only:
+        continue
     tr = np.zeros(8 * 64, np.int64)
     us = C.c_double()
     rc = f(ctx.h, M, N, K, BN, res, 0, 0, tr.ctypes.data_as(C.c_void_p), C.byref(us))
