@@ -489,20 +489,21 @@ class ResNet final : public CnnModel {
       bf16* X = act_[cur];
       bf16* Y = act_[cur ^ 1];
       const int Hi = b.H_in, Ho = b.H_out, Hp = Hi + 2;
+      const int G = Hi + 1;  // shared-border grid pitch (remap_row, gemm_sm100.cu)
       bf16* P = pads_.at({Hi, b.width});
       if (b.stride == 1) {
         // c1: 1x1 -> interior of the zero-bordered grid
         gemm(b.c1, X, B * Hi * Hi, B * Hi * Hi, b.c1.Kc, 1, &zero, nullptr, 0, P, b.width, 0, 1,
-             kRowCompactToPad, Hi, B * Hp * Hp);
+             kRowCompactToPad, Hi, B * G * G);
         // c2: 3x3 as 9 row shifts of the padded grid
         int taps[9];
         for (int dr = 0; dr < 3; dr++)
-          for (int ds = 0; ds < 3; ds++) taps[dr * 3 + ds] = (dr - 1) * Hp + (ds - 1);
-        gemm(b.c2, P, B * Hp * Hp, B * Hp * Hp, b.c2.Kc, 9, taps, nullptr, 0, t2_, b.width, 0,
+          for (int ds = 0; ds < 3; ds++) taps[dr * 3 + ds] = (dr - 1) * G + (ds - 1);
+        gemm(b.c2, P, B * G * G, B * G * G, b.c2.Kc, 9, taps, nullptr, 0, t2_, b.width, 0,
              1, kRowPadToCompact, Hi, B * Ho * Ho);
-        // halo mode: the 9 taps read one (128 + 2*(Hp+1))-row box per
+        // halo mode: the 9 taps read one (128 + 2*(G+1))-row box per
         // channel block from shared memory (4.7-7x less operand traffic)
-        if (kUseHalo && 128 + 2 * (Hp + 1) <= 256) L.back().g.halo_lo = Hp + 1;
+        if (kUseHalo && 128 + 2 * (G + 1) <= 256) L.back().g.halo_lo = G + 1;
       } else {
         // Stride 2: c1 writes the phase split of its zero-bordered grid; the
         // stride-2 3x3 is then 9 row shifts (plane base + p*Wq + q) over an
@@ -748,7 +749,8 @@ __global__ void maxpool2x2_kernel(const bf16* __restrict__ in, int B, int H, int
   __align__(16) bf16 o[8];
 #pragma unroll
   for (int j = 0; j < 8; j++) o[j] = __float2bfloat16(m[j]);
-  const size_t orow = padded_out ? ((size_t)n * (Ho + 2) + ho + 1) * (Ho + 2) + wo + 1 : pix;
+  // padded: the next conv's shared-border grid (pitch Ho + 1, remap_row)
+  const size_t orow = padded_out ? ((size_t)n * (Ho + 1) + ho + 1) * (Ho + 1) + wo : pix;
   *reinterpret_cast<uint4*>(out + orow * C + ch * 8) = *reinterpret_cast<uint4*>(o);
 }
 
@@ -1118,7 +1120,7 @@ class Vgg16 final : public SeqNet {
     const bf16* in = x0;  // conv0: im2col rows; later: a padded grid
     for (size_t i = 0; i < convs_.size(); i++) {
       ConvW& c = convs_[i];
-      const int H = Hs_[i], Hp = H + 2, rows_pad = b * Hp * Hp;
+      const int H = Hs_[i], G = H + 1, rows_pad = b * G * G;  // shared-border grid
       void* out = pool_after_[i] ? (void*)compact_[i] : (void*)pads_[i];
       if (i == 0) {
         push_gemm(L, c, in, b * H * H, b * H * H, nullptr, nullptr, 0, out, c.cout, 0, 1,
@@ -1126,10 +1128,10 @@ class Vgg16 final : public SeqNet {
       } else {
         int taps[9];
         for (int dr = 0; dr < 3; dr++)
-          for (int ds = 0; ds < 3; ds++) taps[dr * 3 + ds] = (dr - 1) * Hp + (ds - 1);
+          for (int ds = 0; ds < 3; ds++) taps[dr * 3 + ds] = (dr - 1) * G + (ds - 1);
         push_gemm(L, c, in, rows_pad, rows_pad, taps, nullptr, 0, out, c.cout, 0, 1,
                   pool_after_[i] ? kRowPadToCompact : kRowPadToPad, H, b * H * H);
-        if (kUseHalo && 128 + 2 * (Hp + 1) <= 256) L.back().g.halo_lo = Hp + 1;
+        if (kUseHalo && 128 + 2 * (G + 1) <= 256) L.back().g.halo_lo = G + 1;
       }
       if (pool_after_[i]) {
         const bf16* src = compact_[i];

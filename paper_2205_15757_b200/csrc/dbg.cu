@@ -95,7 +95,7 @@ extern "C" int cg_dbg_halo_trace2(cg_ctx* ctx, int B, int H, int C, int N, int B
                                   long long* trace_host, double* us) {
   try {
     cudaStream_t st = (cudaStream_t)cg_ctx_stream(ctx);
-    const int Hp = H + 2, rows = B * Hp * Hp;
+    const int Hp = H + 1, rows = B * Hp * Hp;  // shared-border grid pitch
     void *dA, *dB, *dbias, *dout;
     long long* dtr;
     CG_CUDA(cudaMalloc(&dA, (size_t)rows * C * 2));
@@ -174,7 +174,7 @@ extern "C" int cg_dbg_gemm_trace_mode(cg_ctx* ctx, int M, int N, int K, int BN, 
     CG_CUDA(cudaMalloc(&dB, (size_t)N * K * 2));
     CG_CUDA(cudaMalloc(&dbias, (size_t)N * 4));
     const size_t out_rows = row_mode == kRowCompactToPad
-                                ? (size_t)(M / (H * H)) * (H + 2) * (H + 2)
+                                ? (size_t)(M / (H * H)) * (H + 1) * (H + 1) + H + 2
                                 : (size_t)M;
     CG_CUDA(cudaMalloc(&dout, out_rows * N * 2));
     CG_CUDA(cudaMalloc(&dtr, 8 * 64 * 8));

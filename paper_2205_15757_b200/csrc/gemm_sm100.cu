@@ -286,17 +286,25 @@ __device__ __forceinline__ int remap_row(int M, int rows_out, int mode, int H,
     const int Hq = (H + 2) >> 1, Wq = (W + 2) >> 1;
     return ((((h & 1) * 2 + (w & 1)) * Bn + n) * Hq + (h >> 1)) * Wq + (w >> 1);
   }
-  const int Wp = W + 2, HpWp = (H + 2) * Wp;
+  // Zero-bordered pixel grid with shared borders: each grid row is W pixels
+  // plus one zero column (the right border of a row is the left border of
+  // the next), each image H + 1 grid rows of which row 0 is zero (the bottom
+  // border of the image above). Pixel (n, h, w) sits at grid row
+  // n (H+1)(W+1) + (h+1)(W+1) + w; the 3x3 taps are shifts by
+  // (dr-1)(W+1) + (ds-1); index -1 (top-left of image 0) and the rows past
+  // the last image are TMA out-of-bounds zeros. (H+1)(W+1) rows per image
+  // instead of (H+2)(W+2): 21 % fewer MMA rows at 7x7.
+  const int Wp = W + 1, HpWp = (H + 1) * Wp;
   if (mode == kRowPadToCompact || mode == kRowPadToPad) {
     int img = m / HpWp, rem = m - img * HpWp;
     int hp = rem / Wp, wp = rem - hp * Wp;
-    if (hp < 1 || hp > H || wp < 1 || wp > W) return -1;
-    return mode == kRowPadToPad ? m : (img * H + hp - 1) * W + wp - 1;
+    if (hp < 1 || wp >= W) return -1;
+    return mode == kRowPadToPad ? m : (img * H + hp - 1) * W + wp;
   }
   const int HW = H * W;
   int img = m / HW, rem = m - img * HW;
   int h = rem / W, w = rem - h * W;
-  return img * HpWp + (h + 1) * Wp + w + 1;
+  return img * HpWp + (h + 1) * Wp + w;
 }
 
 #define CG_TRACE(slot, i)                                             \

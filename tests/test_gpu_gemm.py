@@ -37,6 +37,16 @@ def run_gemm(ctx, A, Bw, N, Kc, ntaps, taps, bias, residual, relu, mode, H, W, M
     return torch.from_numpy(out.view(np.int16)).view(torch.bfloat16).float()
 
 
+def grid_rows(xq):
+    """[NB, C, H, W] -> the kernels' shared-border zero grid as NHWC rows:
+    per image H + 1 grid rows of W pixels + 1 zero column, grid row 0 zero
+    (remap_row in csrc/gemm_sm100.cu). Returns (rows, pitch W + 1)."""
+    NB, C, H, W = xq.shape
+    z = torch.zeros(NB, H + 1, W + 1, C)
+    z[:, 1:, :W, :] = xq.permute(0, 2, 3, 1)
+    return z.reshape(-1, C), W + 1
+
+
 def close(got, ref):
     err = (got - ref).abs()
     lim = 2.0 ** -7 * ref.abs() + 1e-3
@@ -127,12 +137,10 @@ def test_gemm_pair_taps_remap(ctx):
     x = torch.rand(NB, C, H, W, generator=g) * 2 - 1
     w = (torch.rand(Cout, C, 3, 3, generator=g) * 2 - 1) / 3
     bias = torch.rand(Cout, generator=g) - 0.5
-    xp = torch.nn.functional.pad(q(x), (1, 1, 1, 1))
-    A = xp.permute(0, 2, 3, 1).reshape(-1, C)
-    Wp = W + 2
+    A, Wp = grid_rows(q(x))
     taps = [(dr - 1) * Wp + (ds - 1) for dr in range(3) for ds in range(3)]
     Bw = q(w).permute(0, 2, 3, 1).reshape(Cout, 9 * C)
-    M = NB * (H + 2) * Wp
+    M = A.shape[0]
     got = run_gemm(ctx, A, Bw, Cout, C, 9, taps, bias, None, 1, 1, H, W, M, NB * H * W, 0, 256,
                    pair=1)
     ref = torch.nn.functional.conv2d(q(x), q(w), bias, padding=1).clamp_min(0)
@@ -149,12 +157,10 @@ def test_conv3x3_padded_grid(ctx, NB, H, C, Cout, BN):
     x = torch.rand(NB, C, H, W, generator=g) * 2 - 1
     w = (torch.rand(Cout, C, 3, 3, generator=g) * 2 - 1) / 3
     bias = torch.rand(Cout, generator=g) - 0.5
-    xp = torch.nn.functional.pad(q(x), (1, 1, 1, 1))            # NB,C,Hp,Wp
-    A = xp.permute(0, 2, 3, 1).reshape(-1, C)                   # padded NHWC rows
-    Wp = W + 2
+    A, Wp = grid_rows(q(x))                                     # zero-bordered NHWC rows
     taps = [(dr - 1) * Wp + (ds - 1) for dr in range(3) for ds in range(3)]
     Bw = q(w).permute(0, 2, 3, 1).reshape(Cout, 9 * C)          # [Cout, (dr,ds,c)]
-    M = NB * (H + 2) * Wp
+    M = A.shape[0]
     got = run_gemm(ctx, A, Bw, Cout, C, 9, taps, bias, None, 1, 1, H, W, M, NB * H * W, 0, BN)
     ref = torch.nn.functional.conv2d(q(x), q(w), bias, padding=1).clamp_min(0)
     ref = ref.permute(0, 2, 3, 1).reshape(-1, Cout)
@@ -222,12 +228,10 @@ def test_gemm_pair_taps_remap(ctx):
     x = torch.rand(NB, C, H, W, generator=g) * 2 - 1
     w = (torch.rand(Cout, C, 3, 3, generator=g) * 2 - 1) / 3
     bias = torch.rand(Cout, generator=g) - 0.5
-    xp = torch.nn.functional.pad(q(x), (1, 1, 1, 1))
-    A = xp.permute(0, 2, 3, 1).reshape(-1, C)
-    Wp = W + 2
+    A, Wp = grid_rows(q(x))
     taps = [(dr - 1) * Wp + (ds - 1) for dr in range(3) for ds in range(3)]
     Bw = q(w).permute(0, 2, 3, 1).reshape(Cout, 9 * C)
-    M = NB * (H + 2) * Wp
+    M = A.shape[0]
     got = run_gemm(ctx, A, Bw, Cout, C, 9, taps, bias, None, 1, 1, H, W, M, NB * H * W, 0, 256,
                    pair=1)
     ref = torch.nn.functional.conv2d(q(x), q(w), bias, padding=1).clamp_min(0)
@@ -237,7 +241,7 @@ def test_gemm_pair_taps_remap(ctx):
 @pytest.mark.parametrize("NB,H,C,Cout,BN", [(3, 7, 64, 128, 128), (2, 14, 128, 64, 64),
                                             (2, 28, 64, 256, 256), (2, 56, 64, 64, 64)])
 def test_conv3x3_halo(ctx, NB, H, C, Cout, BN):
-    """Halo mode: one (128 + 2*(W+3))-row box per channel block feeds all 9
+    """Halo mode: one (128 + 2*(W+2))-row box per channel block feeds all 9
     taps (MMA descriptors at arbitrary row offsets inside the 128B-swizzled
     halo) == torch conv2d."""
     W = H
@@ -245,12 +249,10 @@ def test_conv3x3_halo(ctx, NB, H, C, Cout, BN):
     x = torch.rand(NB, C, H, W, generator=g) * 2 - 1
     w = (torch.rand(Cout, C, 3, 3, generator=g) * 2 - 1) / 3
     bias = torch.rand(Cout, generator=g) - 0.5
-    xp = torch.nn.functional.pad(q(x), (1, 1, 1, 1))
-    A = xp.permute(0, 2, 3, 1).reshape(-1, C)
-    Wp = W + 2
+    A, Wp = grid_rows(q(x))
     taps = [(dr - 1) * Wp + (ds - 1) for dr in range(3) for ds in range(3)]
     Bw = q(w).permute(0, 2, 3, 1).reshape(Cout, 9 * C)
-    M = NB * (H + 2) * Wp
+    M = A.shape[0]
     ref = torch.nn.functional.conv2d(q(x), q(w), bias, padding=1).clamp_min(0)
     ref = ref.permute(0, 2, 3, 1).reshape(-1, Cout)
     got = run_halo(ctx, A, Bw, Cout, C, taps, bias, H, W, M, NB * H * W, BN, Wp + 1)
@@ -259,19 +261,19 @@ def test_conv3x3_halo(ctx, NB, H, C, Cout, BN):
 
 def test_compact_to_padded_interior(ctx):
     NB, H, C, Cout = 2, 7, 64, 64
-    W, Wp = H, H + 2
+    W, Wp = H, H + 1
     g = torch.Generator().manual_seed(9)
     A = torch.rand(NB * H * W, C, generator=g) * 2 - 1
     Bw = torch.rand(Cout, C, generator=g) * 2 - 1
     bias = torch.zeros(Cout)
-    rows_out = NB * (H + 2) * Wp
+    rows_out = NB * (H + 1) * Wp
     got = run_gemm(ctx, A, Bw, Cout, C, 1, [0], bias, None, 1, 2, H, W, NB * H * W,
                    rows_out, 0, 64)
     ref = (q(A) @ q(Bw).T).clamp_min(0).reshape(NB, H, W, Cout)
-    gp = got.reshape(NB, H + 2, Wp, Cout)
-    close(gp[:, 1:H + 1, 1:W + 1], ref)
-    assert gp[:, 0].abs().sum() == 0 and gp[:, H + 1].abs().sum() == 0
-    assert gp[:, :, 0].abs().sum() == 0 and gp[:, :, W + 1].abs().sum() == 0
+    gp = got.reshape(NB, H + 1, Wp, Cout)
+    close(gp[:, 1:, :W], ref)
+    # the shared zero row / column stay zero
+    assert gp[:, 0].abs().sum() == 0 and gp[:, :, W].abs().sum() == 0
 
 
 @pytest.mark.parametrize("BN", [64, 128, 256])
@@ -299,12 +301,10 @@ def test_conv3x3_halo_sm_pair(ctx, NB, H, C, Cout):
     x = torch.rand(NB, C, H, W, generator=g) * 2 - 1
     w = (torch.rand(Cout, C, 3, 3, generator=g) * 2 - 1) / 3
     bias = torch.rand(Cout, generator=g) - 0.5
-    xp = torch.nn.functional.pad(q(x), (1, 1, 1, 1))
-    A = xp.permute(0, 2, 3, 1).reshape(-1, C)
-    Wp = W + 2
+    A, Wp = grid_rows(q(x))
     taps = [(dr - 1) * Wp + (ds - 1) for dr in range(3) for ds in range(3)]
     Bw = q(w).permute(0, 2, 3, 1).reshape(Cout, 9 * C)
-    M = NB * (H + 2) * Wp
+    M = A.shape[0]
     ref = torch.nn.functional.conv2d(q(x), q(w), bias, padding=1).clamp_min(0)
     ref = ref.permute(0, 2, 3, 1).reshape(-1, Cout)
     got = run_halo(ctx, A, Bw, Cout, C, taps, bias, H, W, M, NB * H * W, 128, Wp + 1, pair=True)
