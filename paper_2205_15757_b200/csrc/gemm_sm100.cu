@@ -185,6 +185,42 @@ __device__ __forceinline__ void umma_bf16(uint32_t d, uint64_t a, uint64_t b,
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d),
       "l"(a), "l"(b), "r"(idesc), "r"(accum));
 }
+// Warp-collective forms: every lane of the warp executes them, one lane
+// (elect.sync) issues the tcgen05 instruction.
+__device__ __forceinline__ void umma_bf16_w(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
+                                            uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accum));
+}
+__device__ __forceinline__ void umma_commit_w(uint64_t* b) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}" ::"r"(
+          su32(b))
+      : "memory");
+}
+__device__ __forceinline__ void umma_bf16_pair_w(uint32_t d, uint64_t a, uint64_t b,
+                                                 uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accum));
+}
+__device__ __forceinline__ void umma_commit_pair_w(uint64_t* b) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;\n}" ::"r"(su32(b)), "h"((uint16_t)3)
+      : "memory");
+}
 // K-major, 128B-swizzled operand tile: 8-row atoms of 1024 B (SBO), version 1.
 __device__ __forceinline__ uint64_t smem_desc_sw128(const void* p) {
   uint64_t addr = su32(p);
@@ -528,7 +564,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && crank == 0) {  // ---------------- MMA issuer
+    // ---------------- MMA issuer: the whole warp runs the loop (warp-uniform
+    // control flow keeps descriptors in uniform registers); one elected lane
+    // issues each tcgen05 instruction
+    if (crank == 0) {
       // kind::f16 instruction descriptor: D f32, A/B bf16, K-major, M=128, N=BN
       const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) |
                              ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
@@ -560,12 +599,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                   smem_desc_sw128_row(sB_u + (uint32_t)((tap * kpt + cb) * B_BYTES), 0);
 #pragma unroll
               for (int k = 0; k < BK / 16; k++)
-                umma_bf16(d, ad + 2 * k, bd + 2 * k, idesc, (cb | tap | k) != 0);
+                umma_bf16_w(d, ad + 2 * k, bd + 2 * k, idesc, (cb | tap | k) != 0);
             }
-            umma_commit(&hempty[hs]);
+            umma_commit_w(&hempty[hs]);
             if (++hs == HALO) { hs = 0; hphase ^= 1; }
           }
-          umma_commit(&tfull[acc]);
+          umma_commit_w(&tfull[acc]);
           CG_TRACE(4, ti);
           if (++acc == 2) { acc = 0; acc_phase ^= 1; }
           continue;
@@ -583,11 +622,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t bd = bd0 + (uint64_t)((stage * B_BYTES) >> 4);
 #pragma unroll
             for (int k = 0; k < BK / 16; k++)
-              umma_bf16_pair(d, ad + 2 * k, bd + 2 * k, idesc2, (kb | k) != 0);
-            umma_commit_pair(&empty[stage]);
+              umma_bf16_pair_w(d, ad + 2 * k, bd + 2 * k, idesc2, (kb | k) != 0);
+            umma_commit_pair_w(&empty[stage]);
             if (++stage == STAGES) { stage = 0; phase ^= 1; }
           }
-          umma_commit_pair(&tfull[acc]);
+          umma_commit_pair_w(&tfull[acc]);
           CG_TRACE(4, ti);
           if (++acc == 2) { acc = 0; acc_phase ^= 1; }
           continue;
@@ -609,14 +648,14 @@ __global__ void __launch_bounds__(kThreads, 1)
               const uint64_t bd = smem_desc_sw128_row(sB_u + (uint32_t)(stage * B_BYTES), 0);
 #pragma unroll
               for (int k = 0; k < BK / 16; k++)
-                umma_bf16_pair(d, ad + 2 * k, bd + 2 * k, idesc2, (cb | tap | k) != 0);
-              umma_commit_pair(&empty[stage]);
+                umma_bf16_pair_w(d, ad + 2 * k, bd + 2 * k, idesc2, (cb | tap | k) != 0);
+              umma_commit_pair_w(&empty[stage]);
               if (++stage == STAGES) { stage = 0; phase ^= 1; }
             }
-            umma_commit_pair(&hempty[hs]);
+            umma_commit_pair_w(&hempty[hs]);
             if (++hs == HALO) { hs = 0; hphase ^= 1; }
           }
-          umma_commit_pair(&tfull[acc]);
+          umma_commit_pair_w(&tfull[acc]);
           if (++acc == 2) { acc = 0; acc_phase ^= 1; }
           continue;
         }
@@ -634,14 +673,14 @@ __global__ void __launch_bounds__(kThreads, 1)
               const uint64_t bd = smem_desc_sw128_row(sB_u + (uint32_t)(stage * B_BYTES), 0);
 #pragma unroll
               for (int k = 0; k < BK / 16; k++)
-                umma_bf16(d, ad + 2 * k, bd + 2 * k, idesc, (cb | tap | k) != 0);
-              umma_commit(&empty[stage]);
+                umma_bf16_w(d, ad + 2 * k, bd + 2 * k, idesc, (cb | tap | k) != 0);
+              umma_commit_w(&empty[stage]);
               if (++stage == STAGES) { stage = 0; phase ^= 1; }
             }
-            umma_commit(&hempty[hs]);
+            umma_commit_w(&hempty[hs]);
             if (++hs == HALO) { hs = 0; hphase ^= 1; }
           }
-          umma_commit(&tfull[acc]);
+          umma_commit_w(&tfull[acc]);
           if (++acc == 2) { acc = 0; acc_phase ^= 1; }
           continue;
         }
@@ -655,11 +694,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint64_t bd = bd0 + (uint64_t)((stage * B_BYTES) >> 4);
 #pragma unroll
           for (int k = 0; k < BK / 16; k++)  // UMMA_K = 16 (32 bytes)
-            umma_bf16(d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
-          umma_commit(&empty[stage]);
+            umma_bf16_w(d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+          umma_commit_w(&empty[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        umma_commit(&tfull[acc]);
+        umma_commit_w(&tfull[acc]);
         CG_TRACE(4, ti);
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
