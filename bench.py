@@ -476,8 +476,11 @@ def cpu_baseline(archs, digs, sds, batch, args, eps=0.1):
     from oracle.oracle import Reference
     from paper_2205_15757_b200.workload import encode_request
     threads = os.cpu_count() or 1
-    S = args.cpu_sample
-    encs = [encode_request(batch, k) for k in range(S)]
+    S = max(1, args.cpu_sample)
+    # the sample cycles through the batch's requests when S > batch size
+    nb = len(batch.inputs)
+    idx = [k % nb for k in range(S)]
+    encs = [encode_request(batch, k) for k in idx]
     kind = "reference" if Reference.available() else "port"
     if kind != "reference":
         return {"value": None, "unit": UNIT, "cores": threads, "kind": "port",
@@ -486,7 +489,7 @@ def cpu_baseline(archs, digs, sds, batch, args, eps=0.1):
     models = cpu_models(archs, sds)
     cpu_path(models, encs[:2], batch.inputs[:2], digs, threads, R, eps)  # warm
     t = time.perf_counter()
-    cpu_path(models, encs, batch.inputs[:S], digs, threads, R, eps)
+    cpu_path(models, encs, np.take(batch.inputs, idx, axis=0), digs, threads, R, eps)
     dt = time.perf_counter() - t
     return {"value": round(S / dt, 3), "unit": UNIT, "cores": threads, "kind": kind,
             "sample": f"{S} requests x {len(archs)} replicas ({'+'.join(sorted(set(archs)))}): "
