@@ -12,9 +12,12 @@ for r in rows:
         continue
     if hdr and len(r) == len(hdr):
         data.append(dict(zip(hdr, r)))
-start = sys.argv[2] if len(sys.argv) > 2 else "conv1_im2col"
+start = sys.argv[2] if len(sys.argv) > 2 and not sys.argv[2].startswith("-") else "conv1_im2col"
 idx = [i for i, d in enumerate(data) if start in d["Kernel Name"]]
-seg = data[idx[-1]:] if idx else data
+# -p: the last COMPLETE forward (between the last two starts) when the
+# capture ends mid-step
+seg = (data[idx[-2]:idx[-1]] if "-p" in sys.argv and len(idx) > 1
+       else data[idx[-1]:] if idx else data)
 tot = 0.0
 agg = collections.defaultdict(lambda: [0, 0.0])
 for d in seg:
