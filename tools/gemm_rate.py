@@ -27,6 +27,10 @@ shapes = [("square K2048", 32768, 2048, 2048, 256, 0),
           ("l3 c3 +res pair", 75264, 1024, 256, 256, 3),
           ("l3 c1 pair", 75264, 256, 1024, 256, 2),
           ("l4 c1 pair", 18816, 512, 2048, 256, 2),
+          ("l3 c3 +res BN128", 75264, 1024, 256, 128, 1),
+          ("l2 c3 +res", 301056, 512, 128, 256, 1),
+          ("l2 c3 +res BN128", 301056, 512, 128, 128, 1),
+          ("l2 c3 +res pair", 301056, 512, 128, 256, 3),
           ("l3 c1", 75264, 256, 1024, 256, 0),
           ("l3 c1 BN128", 75264, 256, 1024, 128, 0),
           ("l4 c1", 18816, 512, 2048, 256, 0)]
