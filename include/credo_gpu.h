@@ -18,6 +18,7 @@
  *                              include/credo/model.hpp:22-39, src/model.cpp:46-65, src/engine.cpp:67-97
  *   cg_model_load_cnn          (new) ImageNet-class model behind the same seam, keyed by weights_digest
  *   cg_exec_run                ModelExecutor::run      include/credo/model.hpp:41-51, src/model.cpp:67-73
+ *   cg_exec_run_perturbed      PerturbingExecutor::run include/credo/model.hpp:60-79, src/model.cpp:75-105
  *   cg_certify_batch           InferenceEngine::execute_batch (src/engine.cpp:269-306) +
  *                              build_result_tree (src/messages.cpp:235-258) + Coordinator::try_attest's
  *                              agreement, manifest and A tree (src/coordinator.cpp:727-849) for one batch
@@ -137,6 +138,14 @@ int cg_model_dims(const cg_model* m, uint64_t* input_dim, uint64_t* output_dim);
  * in is B × u, out is B × v, both f64 row-major. */
 int cg_exec_run(cg_ctx* ctx, cg_model* m, const double* in, uint64_t B,
                 uint64_t u, double* out, uint64_t v);
+/* PerturbingExecutor(inner = cg_exec_run, node_index, magnitude)::run: each
+ * output lane gets the node's deterministic offset in [-magnitude,
+ * +magnitude] from SHA-256(u64 node || model digest || f64_list(input) ||
+ * u64 lane). magnitude 0 = cg_exec_run; negative or NaN -> CG_EINVAL (the
+ * reference constructor's std::invalid_argument). */
+int cg_exec_run_perturbed(cg_ctx* ctx, cg_model* m, const double* in, uint64_t B,
+                          uint64_t u, double* out, uint64_t v,
+                          uint64_t node_index, double magnitude);
 
 /* ---- one batch through the whole hot path -------------------------------
  * A model group replica set: models[p] answers for node p (the

@@ -406,6 +406,39 @@ void oc_linear_run(const double* W, const double* b, uint64_t u, uint64_t v,
   if (softmax) oc_softmax(y, v);
 }
 
+/* PerturbingExecutor::run (model.cpp:82-105). The seed encoder is
+ * u64 node || hash(model_digest) || f64_list(input) (codec.hpp:32-71: u32be
+ * count, then big-endian doubles); each lane appends u64 lane and hashes. */
+void oc_perturb(uint64_t node, const uint8_t model_digest[32], const double* x,
+                uint64_t u, double* y, uint64_t v, double mag) {
+  if (mag == 0.0) return;
+  uint8_t hdr[44];
+  for (int i = 0; i < 8; i++) hdr[i] = (uint8_t)(node >> (56 - 8 * i));
+  memcpy(hdr + 8, model_digest, 32);
+  for (int i = 0; i < 4; i++) hdr[40 + i] = (uint8_t)((uint32_t)u >> (24 - 8 * i));
+  oc_sha256_ctx seed;
+  oc_sha256_init(&seed);
+  oc_sha256_update(&seed, hdr, 44);
+  for (uint64_t k = 0; k < u; k++) {
+    uint64_t bits;
+    uint8_t be[8];
+    memcpy(&bits, x + k, 8);
+    for (int i = 0; i < 8; i++) be[i] = (uint8_t)(bits >> (56 - 8 * i));
+    oc_sha256_update(&seed, be, 8);
+  }
+  for (uint64_t lane = 0; lane < v; lane++) {
+    oc_sha256_ctx c = seed;
+    uint8_t lb[8], h[32];
+    for (int i = 0; i < 8; i++) lb[i] = (uint8_t)(lane >> (56 - 8 * i));
+    oc_sha256_update(&c, lb, 8);
+    oc_sha256_final(&c, h);
+    uint64_t raw = 0;
+    for (int b = 0; b < 8; b++) raw = (raw << 8) | h[b];
+    double unit = (double)raw / 18446744073709551615.0;
+    y[lane] += (2.0 * unit - 1.0) * mag;
+  }
+}
+
 /* -------------------------------------------------------- attestation */
 uint64_t oc_attest_manifest(uint64_t B, uint64_t N, const uint64_t* sel_mask,
                             const uint8_t* satisfied, uint8_t* kinds,

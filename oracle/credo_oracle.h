@@ -72,6 +72,12 @@ void oc_linear_run(const double* W, const double* b, uint64_t u, uint64_t v,
                    int softmax, const double* x, double* y);
 /* The softmax tail of model.cpp:26-34 applied in place. */
 void oc_softmax(double* y, uint64_t v);
+/* PerturbingExecutor::run (model.cpp:82-105) for one request, in place on
+ * its v outputs: lane offset from SHA(u64 node || model_digest ||
+ * f64_list(input) || u64 lane), first 8 digest bytes -> U[-mag, +mag].
+ * mag == 0 leaves y unchanged (model.cpp:85). */
+void oc_perturb(uint64_t node, const uint8_t model_digest[32], const double* x,
+                uint64_t u, double* y, uint64_t v, double mag);
 
 /* Coordinator::try_attest manifest (coordinator.cpp:774-832) for a batch of
  * B request ops with all N providers present. kinds: 0 whole_batch,

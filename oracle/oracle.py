@@ -187,6 +187,14 @@ class Oracle:
                              _p(x), _p(y))
         return y
 
+    def perturb(self, node: int, model_digest: bytes, x, y, mag: float) -> np.ndarray:
+        """PerturbingExecutor::run's offset for one request (model.cpp:82-105)."""
+        x = np.ascontiguousarray(x, np.float64)
+        y = np.array(y, np.float64)
+        self.L.oc_perturb(u64(node), bytes(model_digest), _p(x), u64(x.size),
+                          _p(y), u64(y.size), C.c_double(mag))
+        return y
+
     def softmax(self, y) -> np.ndarray:
         y = np.array(y, np.float64)
         self.L.oc_softmax(_p(y), u64(y.size))
@@ -345,6 +353,17 @@ class Reference:
         y = np.zeros((x.shape[0], v), np.float64)
         rc = self.L.ref_linear_run(file, u64(len(file)), _p(x),
                                    u64(x.shape[0]), _p(y))
+        assert rc == 0, rc
+        return y
+
+    def perturbing_run(self, file: bytes, inputs: np.ndarray, v: int, node: int,
+                       magnitude: float) -> np.ndarray:
+        x = np.ascontiguousarray(inputs, np.float64)
+        y = np.zeros((x.shape[0], v), np.float64)
+        rc = self.L.ref_perturbing_run(file, u64(len(file)), _p(x), u64(x.shape[0]),
+                                       u64(node), C.c_double(magnitude), _p(y))
+        if rc == -2:
+            raise ValueError("negative magnitude")
         assert rc == 0, rc
         return y
 

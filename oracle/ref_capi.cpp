@@ -301,6 +301,26 @@ int ref_linear_run(const uint8_t* file, uint64_t len, const double* in,
   }
 }
 
+// PerturbingExecutor(ToyExecutor) over n inputs (src/model.cpp:75-105).
+int ref_perturbing_run(const uint8_t* file, uint64_t len, const double* in,
+                       uint64_t n, uint64_t node, double magnitude, double* out) {
+  try {
+    auto m = LinearToyModel::from_file_bytes(ByteView(file, len));
+    PerturbingExecutor ex(std::make_unique<ToyExecutor>(), node, magnitude);
+    std::vector<std::vector<double>> xs;
+    for (uint64_t i = 0; i < n; i++)
+      xs.emplace_back(in + i * m.input_dim, in + (i + 1) * m.input_dim);
+    auto ys = ex.run(m, xs);
+    for (uint64_t i = 0; i < n; i++)
+      std::memcpy(out + i * m.output_dim, ys[i].data(), 8 * m.output_dim);
+    return 0;
+  } catch (const std::invalid_argument&) {
+    return -2;
+  } catch (const std::exception&) {
+    return -1;
+  }
+}
+
 // distance::select_quorum (src/distance.cpp:138-216). outs: m×v, node ids in
 // node_idx. selected_mask: bit k set when node k is selected.
 int ref_select_quorum(const double* outs, const uint64_t* node_idx, uint64_t m,

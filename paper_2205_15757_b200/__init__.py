@@ -3,8 +3,10 @@ replica inference, per-request agreement and certificate digests behind a
 C-ABI (include/credo_gpu.h). See DESIGN.md."""
 from .credo import (AgreementOutcome, CHEBYSHEV, Context, CredoError,
                     CudaExecutor, DigestMismatch, EUCLIDEAN, InvalidArgument,
-                    MAX_MINUS_MIN, Model, ModelGroup, RequestBatch, lib)
+                    MAX_MINUS_MIN, Model, ModelGroup, PerturbingExecutor,
+                    RequestBatch, lib)
 
 __all__ = ["AgreementOutcome", "CHEBYSHEV", "Context", "CredoError",
            "CudaExecutor", "DigestMismatch", "EUCLIDEAN", "InvalidArgument",
-           "MAX_MINUS_MIN", "Model", "ModelGroup", "RequestBatch", "lib"]
+           "MAX_MINUS_MIN", "Model", "ModelGroup", "PerturbingExecutor",
+           "RequestBatch", "lib"]

@@ -384,6 +384,29 @@ class CudaExecutor:
         return y
 
 
+class PerturbingExecutor:
+    """PerturbingExecutor(inner, node_index, magnitude) (model.hpp:60-79,
+    model.cpp:75-105) around the CUDA executor: each lane gets the node's
+    deterministic offset from SHA-256(node || model digest || input || lane),
+    computed on the GPU (midstate chain jobs + one thread per lane)."""
+
+    def __init__(self, ctx: Context, node_index: int, magnitude: float):
+        if not (magnitude >= 0.0):
+            raise ValueError("negative magnitude")
+        self.ctx, self.node_index, self.magnitude = ctx, node_index, magnitude
+
+    def run(self, model: Model, inputs) -> np.ndarray:
+        x = np.ascontiguousarray(inputs, np.float64)
+        if x.ndim == 1:
+            x = x[None]
+        B, u = x.shape
+        y = np.zeros((B, model.output_dim), np.float64)
+        self.ctx._check(self.ctx.L.cg_exec_run_perturbed(
+            self.ctx.h, model.h, _p(x), u64(B), u64(u), _p(y),
+            u64(model.output_dim), u64(self.node_index), C.c_double(self.magnitude)))
+        return y
+
+
 # ------------------------------------------------------------ request batch
 @dataclass
 class RequestBatch:

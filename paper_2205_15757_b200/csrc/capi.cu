@@ -699,9 +699,13 @@ void replica_forward(cg_model* m, const double* d_in, uint32_t B,
 
 }  // namespace
 
-extern "C" int cg_exec_run(cg_ctx* ctx, cg_model* m, const double* in,
-                           uint64_t B, uint64_t u, double* out, uint64_t v) {
+namespace {
+
+// ModelExecutor::run, optionally wrapped by PerturbingExecutor (mag > 0).
+int exec_run(cg_ctx* ctx, cg_model* m, const double* in, uint64_t B, uint64_t u,
+             double* out, uint64_t v, uint64_t node, double mag) {
   return guarded(ctx, [&] {
+    if (!(mag >= 0.0)) throw InvalidArgument("negative magnitude");
     if (!m || m->ctx != ctx) throw InvalidArgument("model from another context");
     if (u != m->u) throw InvalidArgument("model input dimension mismatch");
     if (v != m->v) throw InvalidArgument("model output dimension mismatch");
@@ -724,10 +728,56 @@ extern "C" int cg_exec_run(cg_ctx* ctx, cg_model* m, const double* in,
     else
       launch_softmax_topk_f32(d_pre32.p, v, (uint32_t)B, (uint32_t)v, m->softmax,
                               d_out.p, v, 1, d_topi.p, d_topv.p, st);
+    DevBuf<uint8_t> d_hdr;
+    DevBuf<uint32_t> d_mid;
+    if (mag != 0.0) {  // model.cpp:85: magnitude 0 returns the inner outputs
+      // Seed = u64 node || model digest || u32be count (model.cpp:87-90); the
+      // model digest is the descriptor digest verified at load.
+      PerturbHdr hdr;
+      for (int i = 0; i < 8; i++) hdr.b[i] = (uint8_t)(node >> (56 - 8 * i));
+      std::memcpy(hdr.b + 8, m->digest, 32);
+      for (int i = 0; i < 4; i++) hdr.b[40 + i] = (uint8_t)((uint32_t)u >> (24 - 8 * i));
+      const uint64_t nshared = (44 + 8 * u) / 64;
+      if (nshared) {
+        d_hdr.ensure(64);
+        d_mid.ensure(8 * B);
+        CG_CUDA(cudaMemcpyAsync(d_hdr.p, hdr.b, 44, cudaMemcpyHostToDevice, st));
+        std::vector<ChainJob> jobs(B);
+        for (uint64_t k = 0; k < B; k++) {
+          ChainJob& j = jobs[k];
+          std::memset(&j, 0, sizeof j);
+          j.seg[0] = ChainSeg{(uint64_t)d_hdr.p, 0, 44, kSegRaw, 0};
+          j.seg[1] = ChainSeg{(uint64_t)(d_in.p + u * k), 44, 8 * u, kSegF64, 0};
+          j.nseg = 2;
+          j.total_len = 44 + 8 * u;
+          j.blk_end = nshared;
+          j.state_out = (uint64_t)(d_mid.p + 8 * k);
+        }
+        ctx->d_jobs.ensure(B);
+        CG_CUDA(cudaMemcpyAsync(ctx->d_jobs.p, jobs.data(), B * sizeof(ChainJob),
+                                cudaMemcpyHostToDevice, st));
+        launch_chain_jobs(ctx->d_jobs.p, (uint32_t)B, st);
+      }
+      launch_perturb_tail(d_mid.p, d_in.p, u, hdr, nshared, d_out.p, v, (uint32_t)B,
+                          (uint32_t)v, mag, st);
+    }
     CG_CUDA(cudaMemcpyAsync(out, d_out.p, 8 * B * v, cudaMemcpyDeviceToHost, st));
     CG_CUDA(cudaStreamSynchronize(st));
     return CG_OK;
   });
+}
+
+}  // namespace
+
+extern "C" int cg_exec_run(cg_ctx* ctx, cg_model* m, const double* in,
+                           uint64_t B, uint64_t u, double* out, uint64_t v) {
+  return exec_run(ctx, m, in, B, u, out, v, 0, 0.0);
+}
+
+extern "C" int cg_exec_run_perturbed(cg_ctx* ctx, cg_model* m, const double* in,
+                                     uint64_t B, uint64_t u, double* out, uint64_t v,
+                                     uint64_t node_index, double magnitude) {
+  return exec_run(ctx, m, in, B, u, out, v, node_index, magnitude);
 }
 
 // Test hook: iters forwards of one CNN replica over B device-resident random

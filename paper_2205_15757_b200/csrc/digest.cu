@@ -293,4 +293,77 @@ void launch_path_roots(const uint8_t* d_leaf_hashes, const uint8_t* d_sib, const
   CG_CHECK_LAUNCH();
 }
 
+// ---------------------------------------------------------------------------
+// PerturbingExecutor lane offsets (proj/src/model.cpp:82-105). Message per
+// (request i, lane) = hdr(44: u64 node || model_digest || u32 count) ||
+// f64_list body(8u) || u64 lane. The first nshared whole blocks are common
+// to every lane of a request and were absorbed by a chain job into mid[i];
+// each thread here finishes one (request, lane): the last P mod 64 prefix
+// bytes, the lane, FIPS padding (1-2 blocks), then applies the offset to
+// out[i][lane] with explicitly rounded f64 ops (no FMA contraction), in the
+// reference's order: unit = raw / (2^64 - 1); out += (2 unit - 1) * mag.
+__global__ void __launch_bounds__(128) perturb_tail_kernel(
+    const uint32_t* __restrict__ mid, const double* __restrict__ in, uint64_t u,
+    PerturbHdr hdr, uint64_t nshared, double* __restrict__ out, uint64_t ldo,
+    uint32_t B, uint32_t v, double mag) {
+  uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (uint64_t)B * v) return;
+  const uint32_t i = (uint32_t)(t / v);
+  const uint64_t lane = t % v;
+  uint32_t s[8];
+  if (nshared) {
+#pragma unroll
+    for (int k = 0; k < 8; k++) s[k] = mid[8ull * i + k];
+  } else {
+    sha256_iv(s);
+  }
+  const double* x = in + (uint64_t)i * u;
+  const uint64_t P = 44 + 8 * u, total = P + 8;
+  const uint64_t nblk = (total + 9 + 63) / 64;
+  for (uint64_t blk = nshared; blk < nblk; blk++) {
+    uint32_t w[16];
+    for (int q = 0; q < 16; q++) {
+      uint32_t word = 0;
+      for (int b = 0; b < 4; b++) {
+        const uint64_t pos = blk * 64 + 4 * q + b;
+        uint32_t byte;
+        if (pos < 44) {
+          byte = hdr.b[pos];
+        } else if (pos < P) {
+          const uint64_t r = pos - 44;
+          const uint64_t bits = __double_as_longlong(__ldg(x + (r >> 3)));
+          byte = (uint32_t)(bits >> (56 - 8 * (r & 7))) & 0xffu;
+        } else if (pos < total) {
+          byte = (uint32_t)(lane >> (56 - 8 * (pos - P))) & 0xffu;
+        } else if (pos == total) {
+          byte = 0x80u;
+        } else if (pos >= nblk * 64 - 8) {
+          byte = (uint32_t)((total * 8) >> (56 - 8 * (pos - (nblk * 64 - 8)))) & 0xffu;
+        } else {
+          byte = 0;
+        }
+        word = (word << 8) | byte;
+      }
+      w[q] = word;
+    }
+    sha256_compress<true>(s, w);
+  }
+  const uint64_t raw = ((uint64_t)s[0] << 32) | s[1];
+  const double unit = __ddiv_rn(__ull2double_rn(raw), 18446744073709551615.0);
+  const double off = __dmul_rn(__dsub_rn(__dmul_rn(2.0, unit), 1.0), mag);
+  double* y = out + (uint64_t)i * ldo + lane;
+  *y = __dadd_rn(*y, off);
+}
+
+void launch_perturb_tail(const uint32_t* d_mid, const double* d_in, uint64_t u,
+                         const PerturbHdr& hdr, uint64_t nshared, double* d_out,
+                         uint64_t ldo, uint32_t B, uint32_t v, double mag,
+                         cudaStream_t st) {
+  const uint64_t n = (uint64_t)B * v;
+  if (n == 0) return;
+  perturb_tail_kernel<<<(unsigned)ceil_div(n, 128), 128, 0, st>>>(d_mid, d_in, u, hdr, nshared,
+                                                                d_out, ldo, B, v, mag);
+  CG_CHECK_LAUNCH();
+}
+
 }  // namespace cg

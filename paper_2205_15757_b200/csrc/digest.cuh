@@ -41,4 +41,15 @@ void launch_path_roots(const uint8_t* d_leaf_hashes, const uint8_t* d_sib, const
                        const uint32_t* d_lens, uint32_t count, uint8_t* d_roots,
                        cudaStream_t st);
 
+// PerturbingExecutor (proj/src/model.cpp:82-105): the 44-byte seed header
+// (u64 node || model_digest || u32be input count), the B midstates over the
+// first nshared = (44 + 8u) / 64 blocks, then one thread per (request, lane).
+struct PerturbHdr {
+  uint8_t b[44];
+};
+void launch_perturb_tail(const uint32_t* d_mid, const double* d_in, uint64_t u,
+                         const PerturbHdr& hdr, uint64_t nshared, double* d_out,
+                         uint64_t ldo, uint32_t B, uint32_t v, double mag,
+                         cudaStream_t st);
+
 }  // namespace cg

@@ -17,6 +17,12 @@ them. Fixture contents:
                    hashes, and ref_certify_batch results for three fault
                    patterns (honest / one replica corrupt on some requests /
                    tight epsilon -> failures)
+* perturb.npz    — PerturbingExecutor(ToyExecutor, node, magnitude) outputs
+                   over generate_group models with u in {1, 9, 3072} (0, 1
+                   and 384 shared SHA blocks; 1- and 2-block lane tails), a
+                   softmax model, several nodes and magnitudes
+
+    python tests/golden/make_golden.py perturb   # that fixture alone
 """
 import os
 import sys
@@ -167,15 +173,41 @@ def c1_fixture(R):
     np.savez_compressed(os.path.join(OUT, "c1_batch.npz"), **save)
 
 
+# (u, v, softmax, node, magnitude, seed)
+PERTURB_CASES = [(1, 3, False, 0, 0.25, 11), (9, 5, False, 3, 1e-3, 12),
+                 (3072, 10, False, 1, 0.05, 7), (3072, 10, True, 2, 1e-4, 7),
+                 (40, 17, False, 2**40 + 5, 3.5, 13), (3072, 10, False, 0, 0.0, 7)]
+
+
+def perturb_fixture(R):
+    save = {}
+    for c, (u, v, sm, node, mag, seed) in enumerate(PERTURB_CASES):
+        files, digs = R.generate_group(b"group-0", u, v, 1, 0, 0.05, seed, softmax=sm)
+        x = np.random.default_rng(100 + c).uniform(-1, 1, (6, u))
+        save[f"c{c}_file"] = np.frombuffer(files[0], np.uint8)
+        save[f"c{c}_digest"] = np.frombuffer(digs[0], np.uint8)
+        save[f"c{c}_inputs"] = x
+        save[f"c{c}_plain"] = R.linear_run(files[0], x, v)
+        save[f"c{c}_outputs"] = R.perturbing_run(files[0], x, v, node, mag)
+        save[f"c{c}_case"] = np.array([u, v, int(sm), node], np.uint64)
+        save[f"c{c}_mag"] = np.array(mag, np.float64)
+    save["ncases"] = np.array(len(PERTURB_CASES))
+    np.savez_compressed(os.path.join(OUT, "perturb.npz"), **save)
+
+
 if __name__ == "__main__":
     if not Reference.available():
         sys.exit("oracle/_ref/libcredo_ref.so missing: run `make -C oracle ref` "
                  "where /root/reference exists")
     R = Reference()
+    if sys.argv[1:] == ["perturb"]:
+        perturb_fixture(R)
+        sys.exit(0)
     sha_fixture(R)
     merkle_fixture(R)
     quorum_fixture(R)
     c1_fixture(R)
+    perturb_fixture(R)
     for f in sorted(os.listdir(OUT)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(OUT, f)))

@@ -22,7 +22,8 @@ def declared_symbols():
 def test_header_declares_entry_points():
     syms = declared_symbols()
     for s in ("cg_sha256_batch", "cg_select_quorum_batch", "cg_exec_run",
-              "cg_certify_batch", "cg_merkle_root_batch", "cg_model_load_cnn"):
+              "cg_certify_batch", "cg_merkle_root_batch", "cg_model_load_cnn",
+              "cg_exec_run_perturbed"):
         assert s in syms
 
 

@@ -244,3 +244,48 @@ def test_fetch_ticket_after_next_certify(ctx):
     r1 = grp.fetch_ticket(t1)
     assert np.array_equal(r0["a_root"], g["honest_a_root"])
     assert np.array_equal(r1["a_root"], g["honest_a_root"])
+
+
+@pytest.mark.gpu
+def test_perturbing_executor_bit_exact(ctx, oracle):
+    """PerturbingExecutor on the GPU (midstate chain jobs + lane-tail kernel)
+    vs the compiled reference's outputs (golden) and the oracle: bit-exact
+    for the fp64 linear model; for softmax models (exp within 4 ulp of glibc)
+    the offsets applied to the GPU's own unperturbed outputs are bit-exact."""
+    from paper_2205_15757_b200 import CudaExecutor, InvalidArgument, Model, PerturbingExecutor
+    g = golden("perturb.npz")
+    for c in range(int(g["ncases"])):
+        u, v, sm, node = (int(t) for t in g[f"c{c}_case"])
+        mag = float(g[f"c{c}_mag"])
+        dig = g[f"c{c}_digest"].tobytes()
+        m = Model.load_linear(ctx, g[f"c{c}_file"].tobytes(), dig)
+        x = g[f"c{c}_inputs"]
+        y = PerturbingExecutor(ctx, node, mag).run(m, x)
+        if not sm:
+            assert np.array_equal(y, g[f"c{c}_outputs"]), c
+        plain = CudaExecutor(ctx).run(m, x)
+        want = np.stack([oracle.perturb(node, dig, x[k], plain[k], mag) for k in range(len(x))])
+        assert np.array_equal(y, want), c
+        m.free()
+    # larger batch, every tail shape (u mod 8 sweeps P mod 64), random nodes
+    from oracle.oracle import Reference  # noqa: F401  (oracle only checks)
+    rng = np.random.default_rng(9)
+    for u in (2, 3, 8, 9, 15, 16, 100, 777):
+        v = int(rng.integers(1, 40))
+        W = rng.normal(size=(v, u)) / np.sqrt(u)
+        b = rng.normal(size=v) * 0.1
+        import hashlib, struct
+        f = struct.pack(">QQ?", u, v, False) + struct.pack(">I", v * u) + \
+            W.astype(">f8").tobytes() + struct.pack(">I", v) + b.astype(">f8").tobytes()
+        dig = hashlib.sha256(f).digest()
+        m = Model.load_linear(ctx, f, dig)
+        x = rng.uniform(-1, 1, (33, u))
+        node = int(rng.integers(0, 2**63))
+        y = PerturbingExecutor(ctx, node, 0.01).run(m, x)
+        plain = CudaExecutor(ctx).run(m, x)
+        want = np.stack([oracle.perturb(node, dig, x[k], plain[k], 0.01) for k in range(33)])
+        assert np.array_equal(y, want), u
+        with pytest.raises(InvalidArgument):
+            ctx._check(ctx.L.cg_exec_run_perturbed(ctx.h, m.h, None, 0, 0, None, 0, 0,
+                                                   __import__("ctypes").c_double(-1.0)))
+        m.free()

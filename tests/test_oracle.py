@@ -210,3 +210,34 @@ def test_agree_batch_matches_per_request(oracle):
         lab = oracle.ensemble_label(outs[:, k], mask, 1) if sat else -1
         assert lab == r["label"][k]
         assert r["digest"][k].tobytes() == oracle.label_digest(ids[k].tobytes(), 2, lab)
+
+
+def test_perturb_golden(oracle):
+    """oc_perturb == PerturbingExecutor::run (model.cpp:75-105) bit-exact on
+    the compiled reference's outputs (tests/golden/perturb.npz)."""
+    g = golden("perturb.npz")
+    for c in range(int(g["ncases"])):
+        u, v, sm, node = (int(t) for t in g[f"c{c}_case"])
+        mag = float(g[f"c{c}_mag"])
+        dig = g[f"c{c}_digest"].tobytes()
+        for k, x in enumerate(g[f"c{c}_inputs"]):
+            y = oracle.perturb(node, dig, x, g[f"c{c}_plain"][k], mag)
+            assert np.array_equal(y, g[f"c{c}_outputs"][k]), (c, k)
+
+
+def test_perturb_live_reference(oracle):
+    from oracle.oracle import Reference
+    if not Reference.available():
+        pytest.skip("oracle/_ref not built here")
+    R = Reference()
+    files, digs = R.generate_group(b"group-0", 17, 4, 1, 0, 0.05, 21)
+    x = np.random.default_rng(3).uniform(-1, 1, (3, 17))
+    with pytest.raises(ValueError):
+        R.perturbing_run(files[0], x, 4, 0, -1.0)
+    with pytest.raises(ValueError):
+        R.perturbing_run(files[0], x, 4, 0, float("nan"))
+    plain = R.linear_run(files[0], x, 4)
+    for node in (0, 1, 2**63):
+        want = R.perturbing_run(files[0], x, 4, node, 0.125)
+        got = np.stack([oracle.perturb(node, digs[0], x[k], plain[k], 0.125) for k in range(3)])
+        assert np.array_equal(got, want)
