@@ -156,6 +156,13 @@ int cg_group_create(cg_ctx* ctx, cg_model* const* models, uint32_t N,
                     uint64_t version, uint32_t max_batch, uint32_t topk,
                     cg_group** out);
 void cg_group_free(cg_group* g);
+/* Wrap every local replica in PerturbingExecutor(node_index = provider
+ * index, magnitude) (src/model.cpp:75-105, harness wiring
+ * src/harness.cpp:255-258; harness default 1e-9, include/credo/harness.hpp:163)
+ * for the forwards of later certify calls. 0 (the default) = plain replicas;
+ * negative or NaN -> CG_EINVAL. cg_certify_outputs (precomputed outputs) is
+ * not affected. The reported top-k is of the unperturbed replica outputs. */
+int cg_group_set_perturbation(cg_group* g, double magnitude);
 
 /* The ExecutionBatch (include/credo/engine.hpp:29-34) in struct-of-arrays
  * form: the request fields of InferenceRequest (include/credo/domain.hpp:

@@ -545,6 +545,10 @@ class ModelGroup:
                         sigs.ctypes.data)
         return cb, keep, B
 
+    def set_perturbation(self, magnitude: float):
+        """PerturbingExecutor around every replica (harness.cpp:255-258)."""
+        self.ctx._check(self.ctx.L.cg_group_set_perturbation(self.h, C.c_double(magnitude)))
+
     def certify(self, batch: RequestBatch, want_outputs: bool = False,
                 want_leaves: bool = False, sync: bool = True):
         """One ExecutionBatch through the hot path. sync=False only enqueues

@@ -877,9 +877,58 @@ struct cg_group {
   std::vector<std::unique_ptr<IngestSlot>> slots;
   uint64_t next_ticket = 1;
   uint32_t last_B = 0;
+  // PerturbingExecutor wrapping of every local replica (harness.cpp:255-258;
+  // the harness default perturb_magnitude is 1e-9, harness.hpp:163)
+  double perturb_mag = 0;
+  DevBuf<uint8_t> d_phdr;     // 64 B per local provider: the seed header
+  DevBuf<uint32_t> d_pmid;    // 8 words per (local provider, request)
+  DevBuf<ChainJob> d_pjobs;
 };
 
 namespace {
+
+// Each local provider p's outputs += its PerturbingExecutor offsets
+// (model.cpp:82-105): per (p, request) a midstate chain over the shared
+// whole blocks of u64 p || weights digest || f64_list(input), then one thread
+// per (request, lane) for the tail. The node index is the provider index
+// (the harness builds node i's executor with node_index i).
+void perturb_group_outputs(cg_group* g, const double* d_in, uint32_t B, double* d_outs,
+                           cudaStream_t st) {
+  const uint64_t u = g->u, v = g->v;
+  const uint32_t nloc = (uint32_t)g->models.size();
+  const uint64_t nshared = (44 + 8 * u) / 64;
+  std::vector<PerturbHdr> hdr(nloc);
+  for (uint32_t li = 0; li < nloc; li++) {
+    const uint64_t p = g->dist ? g->rank : li;
+    for (int i = 0; i < 8; i++) hdr[li].b[i] = (uint8_t)(p >> (56 - 8 * i));
+    std::memcpy(hdr[li].b + 8, g->digests[p].data(), 32);
+    for (int i = 0; i < 4; i++) hdr[li].b[40 + i] = (uint8_t)((uint32_t)u >> (24 - 8 * i));
+  }
+  if (nshared) {
+    g->d_pmid.ensure(8ull * nloc * B);
+    g->d_pjobs.ensure((uint64_t)nloc * B);
+    std::vector<ChainJob> jobs((uint64_t)nloc * B);
+    for (uint32_t li = 0; li < nloc; li++)
+      for (uint32_t k = 0; k < B; k++) {
+        ChainJob& j = jobs[(uint64_t)li * B + k];
+        std::memset(&j, 0, sizeof j);
+        j.seg[0] = ChainSeg{(uint64_t)(g->d_phdr.p + 64 * li), 0, 44, kSegRaw, 0};
+        j.seg[1] = ChainSeg{(uint64_t)(d_in + u * k), 44, 8 * u, kSegF64, 0};
+        j.nseg = 2;
+        j.total_len = 44 + 8 * u;
+        j.blk_end = nshared;
+        j.state_out = (uint64_t)(g->d_pmid.p + 8 * ((uint64_t)li * B + k));
+      }
+    CG_CUDA(cudaMemcpyAsync(g->d_pjobs.p, jobs.data(), jobs.size() * sizeof(ChainJob),
+                            cudaMemcpyHostToDevice, st));
+    launch_chain_jobs(g->d_pjobs.p, nloc * B, st);
+  }
+  for (uint32_t li = 0; li < nloc; li++) {
+    const uint64_t p = g->dist ? g->rank : li;
+    launch_perturb_tail(nshared ? g->d_pmid.p + 8ull * li * B : nullptr, d_in, u, hdr[li],
+                        nshared, d_outs + p * B * v, v, B, (uint32_t)v, g->perturb_mag, st);
+  }
+}
 
 IngestSlot& slot_for(cg_group* g, uint64_t ticket) {
   IngestSlot& s = *g->slots[ticket % g->slots.size()];
@@ -1133,6 +1182,7 @@ void certify(cg_group* g, uint64_t ticket, const double* precomputed_outputs) {
     }
     set_gemm_sm_budget(kNumSMs);
   }
+  if (g->perturb_mag != 0.0 && !precomputed_outputs) perturb_group_outputs(g, S.d_in_ptr, B, R.d_outs.p, st);
   CG_CUDA(cudaEventRecord(S.ev_fwd, st));
   // ---- the tail, on the tail stream
   CG_CUDA(cudaStreamWaitEvent(tl, S.ev_fwd, 0));
@@ -1339,6 +1389,28 @@ int cg_group_create_dist(cg_ctx* ctx, cg_model* my_model, const uint8_t* all_dig
   if (!ctx || !ctx->comm) return fail(ctx, CG_EINVAL, "cg_ctx_init_nccl first");
   return create_group(ctx, &my_model, 1, (uint32_t)ctx->nranks, all_digests, true, f, metric,
                       default_eps, group_id, group_id_len, version, max_batch, topk, out);
+}
+
+int cg_group_set_perturbation(cg_group* g, double magnitude) {
+  if (!g) return CG_EINVAL;
+  return guarded(g->ctx, [&] {
+    if (!(magnitude >= 0.0)) throw InvalidArgument("negative magnitude");
+    cudaStream_t st = g->ctx->stream;
+    CG_CUDA(cudaStreamSynchronize(st));  // no certify in flight reads the header
+    const uint32_t nloc = (uint32_t)g->models.size();
+    g->d_phdr.ensure(64ull * nloc);
+    std::vector<uint8_t> h(64ull * nloc, 0);
+    for (uint32_t li = 0; li < nloc; li++) {
+      const uint64_t p = g->dist ? g->rank : li;
+      uint8_t* b = h.data() + 64ull * li;
+      for (int i = 0; i < 8; i++) b[i] = (uint8_t)(p >> (56 - 8 * i));
+      std::memcpy(b + 8, g->digests[p].data(), 32);
+      for (int i = 0; i < 4; i++) b[40 + i] = (uint8_t)((uint32_t)g->u >> (24 - 8 * i));
+    }
+    CG_CUDA(cudaMemcpy(g->d_phdr.p, h.data(), h.size(), cudaMemcpyHostToDevice));
+    g->perturb_mag = magnitude;
+    return CG_OK;
+  });
 }
 
 void cg_group_free(cg_group* g) {

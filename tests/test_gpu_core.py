@@ -289,3 +289,35 @@ def test_perturbing_executor_bit_exact(ctx, oracle):
             ctx._check(ctx.L.cg_exec_run_perturbed(ctx.h, m.h, None, 0, 0, None, 0, 0,
                                                    __import__("ctypes").c_double(-1.0)))
         m.free()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mag", [1e-9, 0.02])
+def test_certify_batch_perturbed(ctx, oracle, mag):
+    """The reference harness wraps node i's executor in
+    PerturbingExecutor(node_index=i, perturb_magnitude) (harness.cpp:255-258,
+    default 1e-9). Certified outputs == the compiled reference's outputs
+    (golden) plus the oracle's offsets for provider p, bit-exact; agreement,
+    leaves and roots == certifying those outputs as precomputed replica
+    outputs (that path is itself pinned to the reference's certify_batch)."""
+    from paper_2205_15757_b200 import InvalidArgument, RequestBatch
+    g = golden("c1_batch.npz")
+    B, N = int(g["B"]), int(g["N"])
+    grp = _group(ctx, g, B)
+    with pytest.raises(InvalidArgument):
+        grp.set_perturbation(-1.0)
+    grp.set_perturbation(mag)
+    batch = RequestBatch.from_encoded(split_reqs(g))
+    r = grp.certify(batch, want_outputs=True, want_leaves=True)
+    want = np.stack([np.stack([oracle.perturb(p, g["digests"][p].tobytes(), g["inputs"][k],
+                                              g["outputs"][p, k], mag) for k in range(B)])
+                     for p in range(N)])
+    assert not np.array_equal(want, g["outputs"])
+    assert np.array_equal(r["outputs"], want)
+    ref = _group(ctx, g, B).certify_outputs(batch, want, want_leaves=True)
+    for key in ("selected", "diameter", "satisfied", "label", "r_roots", "a_root",
+                "manifest_len", "leaf_hashes"):
+        assert np.array_equal(r[key], ref[key]), key
+    grp.set_perturbation(0.0)
+    r0 = grp.certify(batch, want_outputs=True)
+    assert np.array_equal(r0["outputs"], g["outputs"])
