@@ -228,10 +228,9 @@ int guarded(cg_ctx* ctx, Fn&& fn) {
 
 // SHA-256 of count host messages on the device (one chain job each).
 // prefix_byte >= 0 prepends that byte (merkle leaf domain 0x00).
-void device_sha256_many(cg_ctx* ctx, const uint8_t* buf, const uint64_t* off,
-                        const uint64_t* len, uint64_t count, int prefix_byte,
-                        uint8_t* out_host) {
-  if (count == 0) return;
+// Enqueue only (results land in ctx->d_out); device_sha256_many waits.
+void device_sha256_start(cg_ctx* ctx, const uint8_t* buf, const uint64_t* off,
+                         const uint64_t* len, uint64_t count, int prefix_byte) {
   Arena ar;
   std::vector<size_t> pos(count), pre(count);
   const uint8_t pb = (uint8_t)prefix_byte;
@@ -267,10 +266,21 @@ void device_sha256_many(cg_ctx* ctx, const uint8_t* buf, const uint64_t* off,
                           cudaMemcpyHostToDevice, ctx->stream));
   CG_CUDA(cudaMemcpyAsync(ctx->d_jobs.p, jobs.data(), count * sizeof(ChainJob),
                           cudaMemcpyHostToDevice, ctx->stream));
-  launch_chain_jobs(ctx->d_jobs.p, (uint32_t)count, ctx->stream);
+  launch_chain_jobs_raw(ctx->d_jobs.p, (uint32_t)count, ctx->stream);
+}
+
+void device_sha256_finish(cg_ctx* ctx, uint64_t count, uint8_t* out_host) {
   CG_CUDA(cudaMemcpyAsync(out_host, ctx->d_out.p, 32 * count,
                           cudaMemcpyDeviceToHost, ctx->stream));
   CG_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+void device_sha256_many(cg_ctx* ctx, const uint8_t* buf, const uint64_t* off,
+                        const uint64_t* len, uint64_t count, int prefix_byte,
+                        uint8_t* out_host) {
+  if (count == 0) return;
+  device_sha256_start(ctx, buf, off, len, count, prefix_byte);
+  device_sha256_finish(ctx, count, out_host);
 }
 
 void check_model_digest(cg_ctx* ctx, const uint8_t* file, uint64_t len,
@@ -278,6 +288,19 @@ void check_model_digest(cg_ctx* ctx, const uint8_t* file, uint64_t len,
   uint8_t got[32];
   uint64_t off = 0;
   device_sha256_many(ctx, file, &off, &len, 1, -1, got);
+  if (std::memcmp(got, digest, 32) != 0)
+    throw DigestError("model file does not match its weights digest");
+}
+
+// The model-file digest chain (one ~100 MB SHA-256 chain for an ImageNet
+// CNN) runs on the GPU while the host parses and folds the weights.
+void start_model_digest(cg_ctx* ctx, const uint8_t* file, uint64_t len) {
+  uint64_t off = 0;
+  device_sha256_start(ctx, file, &off, &len, 1, -1);
+}
+void finish_model_digest(cg_ctx* ctx, const uint8_t digest[32]) {
+  uint8_t got[32];
+  device_sha256_finish(ctx, 1, got);
   if (std::memcmp(got, digest, 32) != 0)
     throw DigestError("model file does not match its weights digest");
 }
@@ -647,12 +670,14 @@ int cg_model_load_cnn(cg_ctx* ctx, const uint8_t* file, uint64_t len,
   return guarded(ctx, [&] {
     *out = nullptr;
     std::unique_ptr<CnnModel> cnn;
+    start_model_digest(ctx, file, len);
     try {
       cnn = CnnModel::from_file(file, len);
     } catch (const std::invalid_argument& e) {
+      CG_CUDA(cudaStreamSynchronize(ctx->stream));
       throw CodecError(e.what());
     }
-    check_model_digest(ctx, file, len, digest);
+    finish_model_digest(ctx, digest);
     cnn->upload(ctx->stream);
     CG_CUDA(cudaStreamSynchronize(ctx->stream));
     auto m = std::make_unique<cg_model>();

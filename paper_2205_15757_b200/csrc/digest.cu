@@ -29,6 +29,19 @@ __global__ void __launch_bounds__(128) chain_jobs_kernel(const ChainJob* jobs,
   run_chain_job(j, digest_out);
 }
 
+// Flat byte messages (no f64 segment): the raw-segment fast run.
+__global__ void __launch_bounds__(64) chain_jobs_raw_kernel(const ChainJob* jobs, uint32_t n) {
+  uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  run_chain_job<CG_CHAIN_LOOP, true>(jobs[t], jobs[t].digest_out);
+}
+
+void launch_chain_jobs_raw(const ChainJob* d_jobs, uint32_t n, cudaStream_t st) {
+  if (n == 0) return;
+  chain_jobs_raw_kernel<<<(unsigned)ceil_div(n, 64), 64, 0, st>>>(d_jobs, n);
+  CG_CHECK_LAUNCH();
+}
+
 void launch_chain_jobs(const ChainJob* d_jobs, uint32_t n, cudaStream_t st,
                        bool exclusive_sm) {
   if (n == 0) return;

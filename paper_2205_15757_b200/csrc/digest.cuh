@@ -13,6 +13,8 @@ constexpr int kChainExclusiveSmem = 120 * 1024;
 constexpr int kChainExclusiveThreads = 128;
 void launch_chain_jobs(const ChainJob* d_jobs, uint32_t n, cudaStream_t st,
                        bool exclusive_sm = false);
+// Jobs whose messages are plain bytes (no f64 segment, no skip flag).
+void launch_chain_jobs_raw(const ChainJob* d_jobs, uint32_t n, cudaStream_t st);
 // ntrees trees; tree t = leaves [off[t], off[t]+len[t]) or count_dev[t].
 void launch_merkle_trees(const uint8_t* d_leaves, const uint64_t* d_off,
                          const uint64_t* d_len, const uint32_t* d_count,

@@ -280,7 +280,7 @@ __device__ __forceinline__ void f64_window_words(const F64Window& win,
 #ifndef CG_CHAIN_LOOP
 #define CG_CHAIN_LOOP 1
 #endif
-template <int kLoop = CG_CHAIN_LOOP>
+template <int kLoop = CG_CHAIN_LOOP, bool kRawFast = false>
 __device__ __forceinline__ void run_chain_job(const ChainJob& j,
                                               uint64_t digest_out) {
   constexpr bool kRolled = kLoop == 1;
@@ -311,6 +311,26 @@ __device__ __forceinline__ void run_chain_job(const ChainJob& j,
       run_e = b1;
     }
   }
+  // kRawFast (flat byte messages: cg_sha256_batch, model-file digests): with
+  // no f64 segment, the raw segment covering the most whole blocks runs with
+  // 16 word loads per block (word-aligned: Arena places a segment at an
+  // address congruent to its message offset mod 4), issued one block ahead.
+  int rs = -1;
+  if (kRawFast && fs < 0) {
+    for (uint32_t t = 0; t < j.nseg; t++) {
+      const ChainSeg& g = j.seg[t];
+      if (g.kind != kSegRaw || ((g.ptr - g.msg_off) & 3)) continue;
+      uint64_t b0 = (g.msg_off + 63) / 64;
+      uint64_t b1 = (g.msg_off + g.len) / 64;
+      b0 = b0 > j.blk_begin ? b0 : j.blk_begin;
+      b1 = b1 < j.blk_end ? b1 : j.blk_end;
+      if (b1 > b0 && (rs < 0 || b1 - b0 > run_e - run_b)) {
+        rs = (int)t;
+        run_b = b0;
+        run_e = b1;
+      }
+    }
+  }
   uint32_t w[16];
   uint64_t blk = j.blk_begin;
 #pragma unroll 1
@@ -318,7 +338,25 @@ __device__ __forceinline__ void run_chain_job(const ChainJob& j,
     load_block_slow(j, blk, nblk_total, w);
     sha256_compress<kRolled>(s, w);
   }
-  if (run_e > run_b) {
+  if (kRawFast && rs >= 0) {
+    const ChainSeg& g = j.seg[rs];
+    const uint32_t* p = reinterpret_cast<const uint32_t*>(g.ptr + run_b * 64 - g.msg_off);
+    const uint64_t n = run_e - run_b;
+    uint32_t nx[16];
+#pragma unroll
+    for (int q = 0; q < 16; q++) nx[q] = __ldg(p + q);
+#pragma unroll 1
+    for (uint64_t i = 0; i < n; i++) {
+#pragma unroll
+      for (int q = 0; q < 16; q++) w[q] = bswap32(nx[q]);
+      if (i + 1 < n) {
+#pragma unroll
+        for (int q = 0; q < 16; q++) nx[q] = __ldg(p + 16 * (i + 1) + q);
+      }
+      sha256_compress<kRolled>(s, w);
+    }
+    blk = run_e;
+  } else if (run_e > run_b) {
     const ChainSeg& g = j.seg[fs];
     const double* base = reinterpret_cast<const double*>(g.ptr);
     const uint64_t dmax = g.len / 8 - 1;
