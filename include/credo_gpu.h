@@ -163,6 +163,14 @@ void cg_group_free(cg_group* g);
  * negative or NaN -> CG_EINVAL. cg_certify_outputs (precomputed outputs) is
  * not affected. The reported top-k is of the unperturbed replica outputs. */
 int cg_group_set_perturbation(cg_group* g, double magnitude);
+/* The wire payload of provider `provider`'s results for the last certified
+ * batch, as PREPARE / PRE-PREPARE carry them: encode_results
+ * (src/messages.cpp:48-50, used at :376 and :406) = u32be count || B ×
+ * InferenceResult::encode (src/domain.cpp:218-225), encoded on the device
+ * from the resident f64 outputs. *len = 4 + B·(88 + |group_id| + 8v); with
+ * out == NULL only *len is set; cap < *len -> CG_EINVAL. */
+int cg_group_encode_results(cg_group* g, uint32_t provider, uint8_t* out, uint64_t cap,
+                            uint64_t* len);
 
 /* The ExecutionBatch (include/credo/engine.hpp:29-34) in struct-of-arrays
  * form: the request fields of InferenceRequest (include/credo/domain.hpp:

@@ -545,6 +545,17 @@ class ModelGroup:
                         sigs.ctypes.data)
         return cb, keep, B
 
+    def encode_results(self, provider: int) -> bytes:
+        """encode_results (messages.cpp:48-50) of one provider's results for
+        the last certified batch: the PREPARE / PRE-PREPARE result payload."""
+        L, n = self.ctx.L, u64()
+        self.ctx._check(L.cg_group_encode_results(self.h, C.c_uint32(provider), None, u64(0),
+                                                  C.byref(n)))
+        buf = C.create_string_buffer(max(n.value, 1))
+        self.ctx._check(L.cg_group_encode_results(self.h, C.c_uint32(provider), buf,
+                                                  u64(n.value), C.byref(n)))
+        return buf.raw[:n.value]
+
     def set_perturbation(self, magnitude: float):
         """PerturbingExecutor around every replica (harness.cpp:255-258)."""
         self.ctx._check(self.ctx.L.cg_group_set_perturbation(self.h, C.c_double(magnitude)))

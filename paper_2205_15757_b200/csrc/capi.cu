@@ -1416,6 +1416,33 @@ int cg_group_create_dist(cg_ctx* ctx, cg_model* my_model, const uint8_t* all_dig
                       default_eps, group_id, group_id_len, version, max_batch, topk, out);
 }
 
+int cg_group_encode_results(cg_group* g, uint32_t provider, uint8_t* out, uint64_t cap,
+                            uint64_t* len) {
+  if (!g || !len) return CG_EINVAL;
+  return guarded(g->ctx, [&] {
+    const IngestSlot* S = g->last;
+    if (!S || !S->certified) throw InvalidArgument("nothing certified yet");
+    if (provider >= g->N) throw InvalidArgument("provider index >= N");
+    const uint32_t B = S->B, gl = (uint32_t)g->gid.size();
+    const uint64_t v = g->v;
+    const uint64_t need = 4 + (uint64_t)B * (88 + gl + 8 * v);
+    *len = need;
+    if (!out) return CG_OK;  // size query
+    if (cap < need) throw InvalidArgument("output buffer too small");
+    cudaStream_t st = g->ctx->stream;
+    CG_CUDA(cudaStreamWaitEvent(st, S->ev_done, 0));
+    g->ctx->d_bytes.ensure(need);
+    Digest32 dg;
+    std::memcpy(dg.b, g->digests[provider].data(), 32);
+    launch_encode_results(S->d_reqids.p, S->res.d_outs.p + (uint64_t)provider * B * v, B,
+                          (uint32_t)v, provider, g->d_gid.p, gl, g->version, dg,
+                          g->ctx->d_bytes.p, st);
+    CG_CUDA(cudaMemcpyAsync(out, g->ctx->d_bytes.p, need, cudaMemcpyDeviceToHost, st));
+    CG_CUDA(cudaStreamSynchronize(st));
+    return CG_OK;
+  });
+}
+
 int cg_group_set_perturbation(cg_group* g, double magnitude) {
   if (!g) return CG_EINVAL;
   return guarded(g->ctx, [&] {

@@ -379,4 +379,49 @@ void launch_perturb_tail(const uint32_t* d_mid, const double* d_in, uint64_t u,
   CG_CHECK_LAUNCH();
 }
 
+// ---------------------------------------------------------------------------
+// encode_results (proj/src/messages.cpp:48-50): u32be count || per result
+// InferenceResult::encode (proj/src/domain.cpp:218-225) = request_id[32] ||
+// u64 node || str(group) || u64 version || f64_list(output) || digest[32],
+// all big-endian. Fixed stride 88 + gl + 8v per result; one CTA per result,
+// threads stride the output doubles (byte stores: the f64 list starts at an
+// arbitrary offset).
+__global__ void __launch_bounds__(128) encode_results_kernel(
+    const uint8_t* __restrict__ reqids, const double* __restrict__ outs, uint32_t B, uint32_t v,
+    uint64_t node, const uint8_t* __restrict__ gid, uint32_t gl, uint64_t version,
+    Digest32 model_digest, uint8_t* __restrict__ dst) {
+  const uint32_t k = blockIdx.x;
+  const uint64_t stride = 88ull + gl + 8ull * v;
+  uint8_t* o = dst + 4 + stride * k;
+  if (k == 0 && threadIdx.x < 4) dst[threadIdx.x] = (uint8_t)(B >> (24 - 8 * threadIdx.x));
+  const uint32_t hdr = 32 + 8 + 4 + gl + 8 + 4;  // bytes before the doubles
+  for (uint32_t t = threadIdx.x; t < hdr; t += blockDim.x) {
+    uint8_t b;
+    if (t < 32) b = reqids[32ull * k + t];
+    else if (t < 40) b = (uint8_t)(node >> (56 - 8 * (t - 32)));
+    else if (t < 44) b = (uint8_t)(gl >> (24 - 8 * (t - 40)));
+    else if (t < 44 + gl) b = gid[t - 44];
+    else if (t < 52 + gl) b = (uint8_t)(version >> (56 - 8 * (t - 44 - gl)));
+    else b = (uint8_t)(v >> (24 - 8 * (t - 52 - gl)));
+    o[t] = b;
+  }
+  const double* y = outs + (uint64_t)k * v;
+  uint8_t* od = o + hdr;
+  for (uint32_t i = threadIdx.x; i < v; i += blockDim.x) {
+    const uint64_t bits = __double_as_longlong(y[i]);
+#pragma unroll
+    for (int q = 0; q < 8; q++) od[8ull * i + q] = (uint8_t)(bits >> (56 - 8 * q));
+  }
+  if (threadIdx.x < 32) od[8ull * v + threadIdx.x] = model_digest.b[threadIdx.x];
+}
+
+void launch_encode_results(const uint8_t* d_reqids, const double* d_outs, uint32_t B, uint32_t v,
+                           uint64_t node, const uint8_t* d_gid, uint32_t gl, uint64_t version,
+                           const Digest32& model_digest, uint8_t* d_dst, cudaStream_t st) {
+  if (B == 0) return;
+  encode_results_kernel<<<B, 128, 0, st>>>(d_reqids, d_outs, B, v, node, d_gid, gl, version,
+                                           model_digest, d_dst);
+  CG_CHECK_LAUNCH();
+}
+
 }  // namespace cg

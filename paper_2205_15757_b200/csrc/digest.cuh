@@ -43,6 +43,15 @@ void launch_path_roots(const uint8_t* d_leaf_hashes, const uint8_t* d_sib, const
                        const uint32_t* d_lens, uint32_t count, uint8_t* d_roots,
                        cudaStream_t st);
 
+// encode_results (proj/src/messages.cpp:48-50) of one provider's B results
+// into d_dst (4 + B * (88 + gl + 8v) bytes).
+struct Digest32 {
+  uint8_t b[32];
+};
+void launch_encode_results(const uint8_t* d_reqids, const double* d_outs, uint32_t B, uint32_t v,
+                           uint64_t node, const uint8_t* d_gid, uint32_t gl, uint64_t version,
+                           const Digest32& model_digest, uint8_t* d_dst, cudaStream_t st);
+
 // PerturbingExecutor (proj/src/model.cpp:82-105): the 44-byte seed header
 // (u64 node || model_digest || u32be input count), the B midstates over the
 // first nshared = (44 + 8u) / 64 blocks, then one thread per (request, lane).

@@ -321,3 +321,28 @@ def test_certify_batch_perturbed(ctx, oracle, mag):
     grp.set_perturbation(0.0)
     r0 = grp.certify(batch, want_outputs=True)
     assert np.array_equal(r0["outputs"], g["outputs"])
+
+
+@pytest.mark.gpu
+def test_encode_results_payload(ctx, oracle):
+    """encode_results (messages.cpp:48-50): the device-encoded PREPARE
+    result payload == u32be count || the oracle's InferenceResult encodings
+    (pinned by the golden R-leaf hashes) of the golden outputs, per provider."""
+    from oracle.oracle import parse_request
+    from paper_2205_15757_b200 import InvalidArgument, RequestBatch
+    g = golden("c1_batch.npz")
+    B, N = int(g["B"]), int(g["N"])
+    grp = _group(ctx, g, B)
+    with pytest.raises(InvalidArgument):
+        grp.encode_results(0)  # nothing certified yet
+    reqs = split_reqs(g)
+    grp.certify(RequestBatch.from_encoded(reqs))
+    gid = g["gid"].tobytes()
+    for p in range(N):
+        want = B.to_bytes(4, "big") + b"".join(
+            oracle.result_encode(parse_request(reqs[k])["request_id"], p, gid, 1,
+                                 g["outputs"][p, k], g["digests"][p].tobytes())
+            for k in range(B))
+        assert grp.encode_results(p) == want
+    with pytest.raises(InvalidArgument):
+        grp.encode_results(N)
