@@ -1156,7 +1156,10 @@ void certify(cg_group* g, uint64_t ticket, const double* precomputed_outputs) {
       else if (o->certified && cudaEventQuery(o->ev_done) == cudaErrorNotReady)
         chain_ctas += (int)ceil_div((uint64_t)o->B * (g->dist ? 1 : N), kChainExclusiveThreads);
     }
-    set_gemm_sm_budget(kNumSMs - chain_ctas);
+    // never below half the GPU: with many large batches in flight (C4 on one
+    // GPU: 8 replicas x 512, 12 slots ahead) the chain CTAs would otherwise
+    // starve the persistent GEMM down to one SM; excess chain CTAs just queue
+    set_gemm_sm_budget(std::max(kNumSMs - chain_ctas, kNumSMs / 2));
     const void* prepped = nullptr;
     if (g->same_prep) {  // replica-independent input stage, once per batch
       g->models[0]->cnn->prepare_input(S.d_in_ptr, B, g->d_prep.p, st);
