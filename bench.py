@@ -747,7 +747,7 @@ def main():
                     help="requests in the bounded CPU-baseline sample (~10-30 s of CPU work)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--depth", type=int, default=12,
-                    help="batches ingested ahead of certification (ring holds 16)")
+                    help="batches ingested ahead of certification (ring holds 24)")
     ap.add_argument("--mode", default="group", choices=["group", "replica"],
                     help="group: a whole 3-replica group per GPU (weak scaling); "
                          "replica: one replica per GPU, NCCL all-gather (N>1)")

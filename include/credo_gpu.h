@@ -58,8 +58,10 @@ const char* cg_last_error(const cg_ctx* ctx);
 int cg_ctx_set_stream(cg_ctx* ctx, void* stream);
 void* cg_ctx_stream(cg_ctx* ctx);
 int cg_ctx_synchronize(cg_ctx* ctx);
-/* Makes the context stream wait for every certification tail enqueued so
- * far (tails run on an internal stream, overlapping the next forwards). */
+/* Makes the context stream wait for all work enqueued so far on the
+ * context's internal streams: every certification tail (internal tail
+ * stream), every certified batch's single-attestation leaves and A root (its
+ * ingest slot's stream) and every ingested batch's request-midstate chains. */
 int cg_ctx_join(cg_ctx* ctx);
 
 /* Number of kernels this library has launched on the context so far. */
@@ -163,6 +165,12 @@ void cg_group_free(cg_group* g);
  * negative or NaN -> CG_EINVAL. cg_certify_outputs (precomputed outputs) is
  * not affected. The reported top-k is of the unperturbed replica outputs. */
 int cg_group_set_perturbation(cg_group* g, double magnitude);
+/* Fault injection: wrap provider `provider` in OffsetExecutor(offset) (the
+ * corrupt_result fault, src/harness.cpp:167-186, wrapping the perturbing
+ * executor as at :255-261) for the requests whose first request-id byte is
+ * below round(256 * fraction); fraction 1 = every request (the reference's
+ * executor exactly), offset 0 = no fault. Applies to later certify calls. */
+int cg_group_set_fault(cg_group* g, uint32_t provider, double offset, double fraction);
 /* The wire payload of provider `provider`'s results for the last certified
  * batch, as PREPARE / PRE-PREPARE carry them: encode_results
  * (src/messages.cpp:48-50, used at :376 and :406) = u32be count || B ×
@@ -171,10 +179,16 @@ int cg_group_set_perturbation(cg_group* g, double magnitude);
  * out == NULL only *len is set; cap < *len -> CG_EINVAL. */
 int cg_group_encode_results(cg_group* g, uint32_t provider, uint8_t* out, uint64_t cap,
                             uint64_t* len);
+/* The same for a named certified ticket (CG_EINVAL when the ticket is not
+ * certified or its ingest slot was reused). */
+int cg_group_encode_results_ticket(cg_group* g, uint64_t ticket, uint32_t provider,
+                                   uint8_t* out, uint64_t cap, uint64_t* len);
 
 /* The ExecutionBatch (include/credo/engine.hpp:29-34) in struct-of-arrays
  * form: the request fields of InferenceRequest (include/credo/domain.hpp:
  * 99-115). inputs is B × u f64; host memory unless inputs_on_device. */
+#define CG_INGEST_RING 24
+
 typedef struct {
   uint32_t B;
   uint64_t u;
@@ -216,14 +230,16 @@ int cg_certify_batch(cg_group* g, const cg_request_batch* batch,
                      cg_certify_out* out);
 int cg_group_fetch(cg_group* g, cg_certify_out* out);
 /* Results of a certified ticket whose ingest slot has not been reused yet
- * (the ring holds 16 batches), e.g. to read batch i back while batch i+1's
- * forwards run. */
+ * (the ring holds CG_INGEST_RING batches), e.g. to read batch i back while
+ * batch i+1's forwards run. */
 int cg_group_fetch_ticket(cg_group* g, uint64_t ticket, cg_certify_out* out);
 /* The same path split at the reference's own seam: ingest = the hot part of
  * InferenceEngine::submit (src/engine.cpp:182-209) — framing bytes, upload,
  * and the request-midstate SHA-256 chains started on a per-batch stream —
  * and certify = execute_batch + R trees + try_attest for that ticket. Up to
- * 16 batches may be ingested ahead; tickets are certified in any order. */
+ * CG_INGEST_RING batches may be ingested ahead; tickets are certified in any
+ * order. A slot is reused by the CG_INGEST_RING-th ingest after its own, so a
+ * certified ticket's results stay fetchable until then. */
 int cg_ingest_batch(cg_group* g, const cg_request_batch* batch, uint64_t* ticket);
 int cg_certify_ticket(cg_group* g, uint64_t ticket, cg_certify_out* out);
 /* Agreement + digest path over precomputed replica outputs (host memory,
@@ -250,6 +266,10 @@ int cg_request_digests(cg_ctx* ctx, const cg_request_batch* batch, const char* g
  * cg_merkle_auth_paths. */
 int cg_group_auth_paths(cg_group* g, uint32_t tree, const uint64_t* indices, uint32_t count,
                         uint8_t* siblings, uint8_t* sides, uint32_t* lens);
+/* The same for a named certified ticket. */
+int cg_group_auth_paths_ticket(cg_group* g, uint64_t ticket, uint32_t tree,
+                               const uint64_t* indices, uint32_t count, uint8_t* siblings,
+                               uint8_t* sides, uint32_t* lens);
 
 /* ---- replica-parallel groups (one model owner's replica per GPU) ---------
  * The SURVEY §8(e) / north-star mapping: rank r of an NCCL communicator is

@@ -275,7 +275,9 @@ int oc_select_quorum(const double* outs, const uint64_t* node_idx, uint64_t m,
   for (uint64_t i = 0; i < m; i++)
     if (node_idx[i] >= n || v == 0) return -1;
   if (m > 20) return -1;
-  if (metric == 1 && v != 1) return -1; /* max_minus_min throws on vectors */
+  /* max_minus_min throws on vectors, but only when delta runs (m >= 2,
+   * distance.cpp:87-91 inside the pair loop at :170-175) */
+  if (metric == 1 && v != 1 && m >= 2) return -1;
   double* dist = (double*)calloc(m * m, sizeof(double));
   for (uint64_t i = 0; i < m; i++)
     for (uint64_t j = i + 1; j < m; j++)

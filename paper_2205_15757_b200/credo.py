@@ -502,16 +502,23 @@ class ModelGroup:
         self._keep = None
         return self
 
-    def auth_paths(self, tree: int, indices):
+    def auth_paths(self, tree: int, indices, ticket: Optional[int] = None):
         """Paths in provider `tree`'s result tree (tree < N) or the
-        attestation tree (tree == N) of the last certified batch."""
+        attestation tree (tree == N) of the last certified batch (or of the
+        certified `ticket`)."""
         idx = np.ascontiguousarray(indices, np.uint64)
         c = len(idx)
         sib = np.zeros((max(c, 1), 64, 32), np.uint8)
         sides = np.zeros((max(c, 1), 64), np.uint8)
         lens = np.zeros(max(c, 1), np.uint32)
-        self.ctx._check(self.ctx.L.cg_group_auth_paths(self.h, u32(tree), _p(idx), u32(c),
-                                                       _p(sib), _p(sides), _p(lens)))
+        L = self.ctx.L
+        if ticket is None:
+            rc = L.cg_group_auth_paths(self.h, u32(tree), _p(idx), u32(c), _p(sib), _p(sides),
+                                       _p(lens))
+        else:
+            rc = L.cg_group_auth_paths_ticket(self.h, u64(ticket), u32(tree), _p(idx), u32(c),
+                                              _p(sib), _p(sides), _p(lens))
+        self.ctx._check(rc)
         return _unpack_paths(sib, sides, lens, c)
 
     def free(self):
@@ -545,16 +552,28 @@ class ModelGroup:
                         sigs.ctypes.data)
         return cb, keep, B
 
-    def encode_results(self, provider: int) -> bytes:
+    def encode_results(self, provider: int, ticket: Optional[int] = None) -> bytes:
         """encode_results (messages.cpp:48-50) of one provider's results for
-        the last certified batch: the PREPARE / PRE-PREPARE result payload."""
+        the last certified batch (or the certified `ticket`): the PREPARE /
+        PRE-PREPARE result payload."""
         L, n = self.ctx.L, u64()
-        self.ctx._check(L.cg_group_encode_results(self.h, C.c_uint32(provider), None, u64(0),
-                                                  C.byref(n)))
+        if ticket is None:
+            call = lambda buf, cap: L.cg_group_encode_results(  # noqa: E731
+                self.h, C.c_uint32(provider), buf, u64(cap), C.byref(n))
+        else:
+            call = lambda buf, cap: L.cg_group_encode_results_ticket(  # noqa: E731
+                self.h, u64(ticket), C.c_uint32(provider), buf, u64(cap), C.byref(n))
+        self.ctx._check(call(None, 0))
         buf = C.create_string_buffer(max(n.value, 1))
-        self.ctx._check(L.cg_group_encode_results(self.h, C.c_uint32(provider), buf,
-                                                  u64(n.value), C.byref(n)))
+        self.ctx._check(call(buf, n.value))
         return buf.raw[:n.value]
+
+    def set_fault(self, provider: int, offset: float, fraction: float = 1.0):
+        """OffsetExecutor(offset) around provider `provider` (the
+        corrupt_result fault, harness.cpp:167-186) for the requests whose
+        first id byte is < round(256 * fraction)."""
+        self.ctx._check(self.ctx.L.cg_group_set_fault(self.h, C.c_uint32(provider),
+                                                      C.c_double(offset), C.c_double(fraction)))
 
     def set_perturbation(self, magnitude: float):
         """PerturbingExecutor around every replica (harness.cpp:255-258)."""

@@ -547,8 +547,8 @@ __global__ void __launch_bounds__(kManThreads) attest_manifest_kernel(
     const uint8_t* __restrict__ sat, const uint8_t* __restrict__ r_roots,
     const uint8_t* __restrict__ req_ids, const uint8_t* __restrict__ gid,
     uint32_t gid_len, uint64_t version, uint8_t* __restrict__ a_leaves,
-    int32_t* __restrict__ single_pos, uint8_t* __restrict__ kinds,
-    uint32_t* __restrict__ m_nodes, uint32_t* __restrict__ m_ops,
+    int32_t* __restrict__ single_pos, int32_t* __restrict__ need53,
+    uint8_t* __restrict__ kinds, uint32_t* __restrict__ m_nodes, uint32_t* __restrict__ m_ops,
     uint32_t* __restrict__ count) {
   __shared__ uint32_t s_whole;
   __shared__ uint32_t s_scan[kManThreads];
@@ -607,6 +607,9 @@ __global__ void __launch_bounds__(kManThreads) attest_manifest_kernel(
     uint32_t fpos = nwhole + nsingle + s_carry_fail - nsingle + (ex >> 16);
     if (k < B) {
       for (uint32_t p = 0; p < N; p++) single_pos[k * N + p] = -1;
+      // request k's single leaves H(0x00||0x53||req||res) share one request
+      // midstate, computed only when k has at least one single leaf
+      if (need53) need53[k] = (sat[k] && (sel[k] & ~whole)) ? 0 : -1;
       if (sat[k]) {
         uint32_t sm = sel[k] & ~whole;
         for (uint32_t p = 0; p < N; p++)
@@ -652,13 +655,13 @@ void launch_attest_manifest(uint32_t B, uint32_t N, const uint32_t* sel,
                             const uint8_t* sat, const uint8_t* r_roots,
                             const uint8_t* req_ids, const uint8_t* gid,
                             uint32_t gid_len, uint64_t version,
-                            uint8_t* a_leaves, int32_t* single_pos,
+                            uint8_t* a_leaves, int32_t* single_pos, int32_t* need53,
                             uint8_t* kinds, uint32_t* m_nodes, uint32_t* m_ops,
                             uint32_t* count, cudaStream_t st) {
   if (gid_len > 100) throw InvalidArgument("group id too long for failure leaf");
   attest_manifest_kernel<<<1, kManThreads, 0, st>>>(
       B, N, sel, sat, r_roots, req_ids, gid, gid_len, version, a_leaves,
-      single_pos, kinds, m_nodes, m_ops, count);
+      single_pos, need53, kinds, m_nodes, m_ops, count);
   CG_CHECK_LAUNCH();
 }
 

@@ -27,7 +27,7 @@ void launch_attest_manifest(uint32_t B, uint32_t N, const uint32_t* sel,
                             const uint8_t* sat, const uint8_t* r_roots,
                             const uint8_t* req_ids, const uint8_t* gid,
                             uint32_t gid_len, uint64_t version,
-                            uint8_t* a_leaves, int32_t* single_pos,
+                            uint8_t* a_leaves, int32_t* single_pos, int32_t* need53,
                             uint8_t* kinds, uint32_t* m_nodes, uint32_t* m_ops,
                             uint32_t* count, cudaStream_t st);
 void launch_softmax_topk_f32(const float* in, uint64_t in_ld, uint32_t rows,

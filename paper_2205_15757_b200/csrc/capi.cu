@@ -158,6 +158,8 @@ struct Arena {
 
 using namespace cg;
 
+constexpr int kIngestRing = CG_INGEST_RING;
+
 // ------------------------------------------------------------------ ctx
 struct cg_ctx {
   int device = 0;
@@ -184,7 +186,13 @@ struct cg_ctx {
   // this context, in issue order: they overlap the next batch's forwards,
   // and one stream keeps the NCCL exchanges in the same order on all ranks
   cudaStream_t tail = nullptr;
+  // groups created on this context (cg_ctx_join drains their slot streams)
+  std::vector<cg_group*> groups;
 };
+
+namespace {
+void join_group_slots(cg_ctx* ctx);
+}
 
 struct cg_model {
   cg_ctx* ctx = nullptr;
@@ -373,6 +381,7 @@ int cg_ctx_join(cg_ctx* ctx) {
       CG_CUDA(cudaEventRecord(ctx->ev_a, ctx->tail));
       CG_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_a, 0));
     }
+    join_group_slots(ctx);
     return CG_OK;
   });
 }
@@ -849,7 +858,7 @@ struct BatchResults {
   DevBuf<uint8_t> d_leaf, d_rroots, d_aleaf, d_aroot, d_sat, d_kinds;
   DevBuf<int8_t> d_status;
   DevBuf<int64_t> d_label;
-  DevBuf<int32_t> d_single_pos;
+  DevBuf<int32_t> d_single_pos, d_need53;
 };
 
 struct IngestSlot {
@@ -859,23 +868,31 @@ struct IngestSlot {
   BatchResults res;
   cudaEvent_t ev_fwd = nullptr;  // replica outputs written (main stream)
   const double* d_in_ptr = nullptr;
-  DevBuf<double> d_in, d_eps;
+  DevBuf<double> d_in, d_eps;  // d_in: device copy of host inputs (allocated on first use)
   DevBuf<uint8_t> d_arena, d_reqids;
+  // chain jobs: [0, B) request midstates H(0x00||0x52||req), [B, off_leaf)
+  // PerturbingExecutor seed midstates, [off_leaf, +N*B) result leaves,
+  // [off_mid53, +B) single-attestation request midstates H(0x00||0x53||req)
+  // (run only for requests with a single leaf), [off_single, +N*B) the
+  // single leaves' tails
   DevBuf<ChainJob> d_jobs;
-  DevBuf<uint32_t> d_mid;
+  uint64_t off_leaf = 0, off_mid53 = 0, off_single = 0;
+  bool perturbed = false;
+  DevBuf<uint32_t> d_mid, d_mid53, d_pmid;
   DevBuf<uint64_t> d_tree;  // per-provider tree offsets then lengths
   PinBuf<uint8_t> h_arena, h_reqids;
   PinBuf<ChainJob> h_jobs;
   PinBuf<double> h_eps;
   PinBuf<uint64_t> h_tree;
   cudaStream_t stream = nullptr;
-  cudaEvent_t ev_staged = nullptr, ev_prefix = nullptr, ev_done = nullptr;
+  cudaEvent_t ev_staged = nullptr, ev_prefix = nullptr, ev_done = nullptr, ev_man = nullptr;
   ~IngestSlot() {
     if (stream) cudaStreamDestroy(stream);
     if (ev_staged) cudaEventDestroy(ev_staged);
     if (ev_prefix) cudaEventDestroy(ev_prefix);
     if (ev_done) cudaEventDestroy(ev_done);
     if (ev_fwd) cudaEventDestroy(ev_fwd);
+    if (ev_man) cudaEventDestroy(ev_man);
   }
 };
 
@@ -906,53 +923,53 @@ struct cg_group {
   // the harness default perturb_magnitude is 1e-9, harness.hpp:163)
   double perturb_mag = 0;
   DevBuf<uint8_t> d_phdr;     // 64 B per local provider: the seed header
-  DevBuf<uint32_t> d_pmid;    // 8 words per (local provider, request)
-  DevBuf<ChainJob> d_pjobs;
+  // OffsetExecutor fault injection (harness.cpp:167-186): provider
+  // fault_provider's outputs += fault_offset for requests whose first id
+  // byte is < fault_thr (0: no fault)
+  uint32_t fault_provider = 0, fault_thr = 0;
+  double fault_offset = 0;
 };
 
 namespace {
 
 // Each local provider p's outputs += its PerturbingExecutor offsets
-// (model.cpp:82-105): per (p, request) a midstate chain over the shared
-// whole blocks of u64 p || weights digest || f64_list(input), then one thread
-// per (request, lane) for the tail. The node index is the provider index
-// (the harness builds node i's executor with node_index i).
-void perturb_group_outputs(cg_group* g, const double* d_in, uint32_t B, double* d_outs,
-                           cudaStream_t st) {
+// (model.cpp:82-105). The per (p, request) midstates over the shared whole
+// blocks of u64 p || weights digest || f64_list(input) were chained at ingest
+// on the slot's stream (they depend on the input only); here one thread per
+// (request, lane) runs the 1-2 tail blocks. The node index is the provider
+// index (the harness builds node i's executor with node_index i).
+void perturb_group_outputs(cg_group* g, const IngestSlot& S, double* d_outs, cudaStream_t st) {
   const uint64_t u = g->u, v = g->v;
-  const uint32_t nloc = (uint32_t)g->models.size();
+  const uint32_t nloc = (uint32_t)g->models.size(), B = S.B;
   const uint64_t nshared = (44 + 8 * u) / 64;
-  std::vector<PerturbHdr> hdr(nloc);
   for (uint32_t li = 0; li < nloc; li++) {
     const uint64_t p = g->dist ? g->rank : li;
-    for (int i = 0; i < 8; i++) hdr[li].b[i] = (uint8_t)(p >> (56 - 8 * i));
-    std::memcpy(hdr[li].b + 8, g->digests[p].data(), 32);
-    for (int i = 0; i < 4; i++) hdr[li].b[40 + i] = (uint8_t)((uint32_t)u >> (24 - 8 * i));
-  }
-  if (nshared) {
-    g->d_pmid.ensure(8ull * nloc * B);
-    g->d_pjobs.ensure((uint64_t)nloc * B);
-    std::vector<ChainJob> jobs((uint64_t)nloc * B);
-    for (uint32_t li = 0; li < nloc; li++)
-      for (uint32_t k = 0; k < B; k++) {
-        ChainJob& j = jobs[(uint64_t)li * B + k];
-        std::memset(&j, 0, sizeof j);
-        j.seg[0] = ChainSeg{(uint64_t)(g->d_phdr.p + 64 * li), 0, 44, kSegRaw, 0};
-        j.seg[1] = ChainSeg{(uint64_t)(d_in + u * k), 44, 8 * u, kSegF64, 0};
-        j.nseg = 2;
-        j.total_len = 44 + 8 * u;
-        j.blk_end = nshared;
-        j.state_out = (uint64_t)(g->d_pmid.p + 8 * ((uint64_t)li * B + k));
-      }
-    CG_CUDA(cudaMemcpyAsync(g->d_pjobs.p, jobs.data(), jobs.size() * sizeof(ChainJob),
-                            cudaMemcpyHostToDevice, st));
-    launch_chain_jobs(g->d_pjobs.p, nloc * B, st);
-  }
-  for (uint32_t li = 0; li < nloc; li++) {
-    const uint64_t p = g->dist ? g->rank : li;
-    launch_perturb_tail(nshared ? g->d_pmid.p + 8ull * li * B : nullptr, d_in, u, hdr[li],
+    PerturbHdr hdr;
+    for (int i = 0; i < 8; i++) hdr.b[i] = (uint8_t)(p >> (56 - 8 * i));
+    std::memcpy(hdr.b + 8, g->digests[p].data(), 32);
+    for (int i = 0; i < 4; i++) hdr.b[40 + i] = (uint8_t)((uint32_t)u >> (24 - 8 * i));
+    launch_perturb_tail(nshared ? S.d_pmid.p + 8ull * li * B : nullptr, S.d_in_ptr, u, hdr,
                         nshared, d_outs + p * B * v, v, B, (uint32_t)v, g->perturb_mag, st);
   }
+}
+
+// cg_ctx_join: the context stream waits for every slot's outstanding work
+// (ingest prefix chains of uncertified batches, single leaves + A root of
+// certified ones).
+void join_group_slots(cg_ctx* ctx) {
+  for (cg_group* g : ctx->groups)
+    for (auto& sl : g->slots) {
+      if (!sl->ever) continue;
+      if (sl->used) CG_CUDA(cudaStreamWaitEvent(ctx->stream, sl->ev_prefix, 0));
+      if (sl->certified) CG_CUDA(cudaStreamWaitEvent(ctx->stream, sl->ev_done, 0));
+    }
+}
+
+const IngestSlot& certified_slot(const cg_group* g, uint64_t ticket) {
+  const IngestSlot& S = *g->slots[ticket % g->slots.size()];
+  if (S.ticket != ticket || !S.certified)
+    throw InvalidArgument("ticket not certified or its slot already reused");
+  return S;
 }
 
 IngestSlot& slot_for(cg_group* g, uint64_t ticket) {
@@ -980,7 +997,7 @@ uint64_t ingest(cg_group* g, const cg_request_batch* bt) {
   }
   Arena ar;
   std::vector<ChainJob> jobs;
-  jobs.reserve((size_t)B * (1 + 2 * N));
+  jobs.reserve((size_t)B * (2 + 2 * N + g->models.size()));
   const uint8_t* gid = (const uint8_t*)g->gid.data();
   const uint32_t gl = (uint32_t)g->gid.size();
   struct ReqLayout {
@@ -1030,6 +1047,7 @@ uint64_t ingest(cg_group* g, const cg_request_batch* bt) {
   S.h_arena.ensure(ar.b.size() + 64);
   std::memcpy(S.h_arena.p, ar.b.data(), ar.b.size());
   const uint64_t A = (uint64_t)S.d_arena.p;
+  if (!bt->inputs_on_device) S.d_in.ensure((uint64_t)g->maxB * u);
   S.d_in_ptr = bt->inputs_on_device ? bt->inputs : S.d_in.p;
   const uint64_t IN = (uint64_t)S.d_in_ptr;
   const uint64_t OUT = (uint64_t)S.res.d_outs.p;
@@ -1069,7 +1087,30 @@ uint64_t ingest(cg_group* g, const cg_request_batch* bt) {
     j.state_out = (uint64_t)(S.d_mid.p + 8 * k);
     jobs.push_back(j);
   }
-  // [B, B + N*B): result leaves H(0x00||0x52||req||res) from the midstate
+  // PerturbingExecutor seeds: per (local provider, request) the midstate
+  // over the whole blocks of u64 p || weights digest || f64_list(input)
+  // (model.cpp:87-90), chained here with the request midstates (same launch)
+  const uint32_t nloc = (uint32_t)g->models.size();
+  const uint64_t pshared = (44 + 8 * u) / 64;
+  S.perturbed = g->perturb_mag != 0.0;
+  if (S.perturbed && pshared) {
+    S.d_pmid.ensure(8ull * nloc * g->maxB);
+    for (uint32_t li = 0; li < nloc; li++)
+      for (uint32_t k = 0; k < B; k++) {
+        ChainJob j;
+        std::memset(&j, 0, sizeof j);
+        j.seg[0] = seg_raw((uint64_t)(g->d_phdr.p + 64 * li), 0, 44);
+        j.seg[1] = seg_f64(IN + 8 * u * k, 44, 8 * u);
+        j.nseg = 2;
+        j.total_len = 44 + 8 * u;
+        j.blk_end = pshared;
+        j.state_out = (uint64_t)(S.d_pmid.p + 8 * ((uint64_t)li * B + k));
+        jobs.push_back(j);
+      }
+  }
+  const uint64_t n_prefix = jobs.size();
+  // result leaves H(0x00||0x52||req||res) from the request midstate
+  S.off_leaf = jobs.size();
   for (uint32_t p = 0; p < N; p++)
     for (uint32_t k = 0; k < B; k++) {
       ChainJob j = leaf_job(k, p, rl[k].h);
@@ -1078,11 +1119,31 @@ uint64_t ingest(cg_group* g, const cg_request_batch* bt) {
       j.digest_out = (uint64_t)(S.res.d_leaf.p + 32 * ((uint64_t)p * B + k));
       jobs.push_back(j);
     }
-  // [B + N*B, B + 2*N*B): single attestation leaves H(0x00||0x53||req||res);
-  // the manifest kernel decides on device which run and where they land
+  // single attestation leaves H(0x00||0x53||req||res) (messages.cpp:283-290):
+  // the manifest kernel decides on device which (request, provider) pairs
+  // need one and where it lands; the request part H(0x00||0x53||req) is one
+  // midstate per request, chained only for requests that have a single leaf
+  S.off_mid53 = jobs.size();
+  for (uint32_t k = 0; k < B; k++) {
+    const ReqLayout& L = rl[k];
+    ChainJob j;
+    std::memset(&j, 0, sizeof j);
+    j.seg[0] = seg_raw(A + L.h53, 0, L.lenH);
+    j.seg[1] = seg_f64(IN + 8 * u * k, L.lenH, 8 * u);
+    j.seg[2] = seg_raw(A + L.t, L.lenH + 8 * u, L.lenT);
+    j.nseg = 3;
+    j.total_len = L.P;
+    j.blk_end = L.P / 64;
+    j.state_out = (uint64_t)(S.d_mid53.p + 8 * k);
+    j.skip_flag = (uint64_t)(S.res.d_need53.p + k);
+    jobs.push_back(j);
+  }
+  S.off_single = jobs.size();
   for (uint32_t k = 0; k < B; k++)
     for (uint32_t p = 0; p < N; p++) {
       ChainJob j = leaf_job(k, p, rl[k].h53);
+      j.blk_begin = rl[k].P / 64;
+      j.state_in = j.blk_begin ? (uint64_t)(S.d_mid53.p + 8 * k) : 0;
       j.digest_out = (uint64_t)S.res.d_aleaf.p;
       j.skip_flag = (uint64_t)(S.res.d_single_pos.p + (uint64_t)k * N + p);
       jobs.push_back(j);
@@ -1106,7 +1167,7 @@ uint64_t ingest(cg_group* g, const cg_request_batch* bt) {
   if (!bt->inputs_on_device)
     CG_CUDA(cudaMemcpyAsync(S.d_in.p, bt->inputs, 8 * u * B, cudaMemcpyHostToDevice, st));
   CG_CUDA(cudaEventRecord(S.ev_staged, st));
-  launch_chain_jobs(S.d_jobs.p, B, st, /*exclusive_sm=*/true);
+  launch_chain_jobs(S.d_jobs.p, (uint32_t)n_prefix, st, /*exclusive_sm=*/true);
   CG_CUDA(cudaEventRecord(S.ev_prefix, st));
   S.used = true;
   S.ever = true;
@@ -1146,20 +1207,9 @@ void certify(cg_group* g, uint64_t ticket, const double* precomputed_outputs) {
     CG_CUDA(cudaMemcpyAsync(R.d_outs.p, precomputed_outputs, 8 * (size_t)N * B * v,
                             cudaMemcpyHostToDevice, st));
   } else {
-    // leave one SM per in-flight chain CTA (request midstates of batches
-    // ingested ahead, result leaves of tails still running) to the chains
-    int chain_ctas = 0;
-    for (auto& o : g->slots) {
-      if (o.get() == &S || !o->ever) continue;
-      if (o->used && cudaEventQuery(o->ev_prefix) == cudaErrorNotReady)
-        chain_ctas += (int)ceil_div(o->B, kChainExclusiveThreads);
-      else if (o->certified && cudaEventQuery(o->ev_done) == cudaErrorNotReady)
-        chain_ctas += (int)ceil_div((uint64_t)o->B * (g->dist ? 1 : N), kChainExclusiveThreads);
-    }
-    // never below half the GPU: with many large batches in flight (C4 on one
-    // GPU: 8 replicas x 512, 12 slots ahead) the chain CTAs would otherwise
-    // starve the persistent GEMM down to one SM; excess chain CTAs just queue
-    set_gemm_sm_budget(std::max(kNumSMs - chain_ctas, kNumSMs / 2));
+    // No SM budget: the GEMM launches hand out tiles by cluster launch
+    // control, so SMs held by the chain CTAs of other streams are simply
+    // not used by the GEMM (gemm_sm100.cu, TileSched).
     const void* prepped = nullptr;
     if (g->same_prep) {  // replica-independent input stage, once per batch
       g->models[0]->cnn->prepare_input(S.d_in_ptr, B, g->d_prep.p, st);
@@ -1208,9 +1258,18 @@ void certify(cg_group* g, uint64_t ticket, const double* precomputed_outputs) {
                                 g->topk, ti, tv, st);
       }
     }
-    set_gemm_sm_budget(kNumSMs);
   }
-  if (g->perturb_mag != 0.0 && !precomputed_outputs) perturb_group_outputs(g, S.d_in_ptr, B, R.d_outs.p, st);
+  if (S.perturbed && !precomputed_outputs) {
+    CG_CUDA(cudaStreamWaitEvent(st, S.ev_prefix, 0));  // seed midstates chained at ingest
+    perturb_group_outputs(g, S, R.d_outs.p, st);
+  }
+  if (g->fault_thr && !precomputed_outputs) {  // OffsetExecutor wraps the perturbing one
+    const uint32_t p = g->fault_provider;
+    const bool local = g->dist ? p == g->rank : p < (uint32_t)g->models.size();
+    if (local)
+      launch_offset_outputs(R.d_outs.p + (uint64_t)p * B * v, S.d_reqids.p, B, (uint32_t)v,
+                            g->fault_offset, g->fault_thr, st);
+  }
   CG_CUDA(cudaEventRecord(S.ev_fwd, st));
   // ---- the tail, on the tail stream
   CG_CUDA(cudaStreamWaitEvent(tl, S.ev_fwd, 0));
@@ -1221,7 +1280,7 @@ void certify(cg_group* g, uint64_t ticket, const double* precomputed_outputs) {
     // and R root over NVLink; agreement and the attestation are then
     // computed on every rank, as every reference node attests.
     const uint32_t r = g->rank;
-    launch_chain_jobs(S.d_jobs.p + B + (uint64_t)r * B, B, tl, /*exclusive_sm=*/true);
+    launch_chain_jobs(S.d_jobs.p + S.off_leaf + (uint64_t)r * B, B, tl, /*exclusive_sm=*/true);
     launch_merkle_trees(R.d_leaf.p + 32 * (uint64_t)r * B, nullptr, S.d_tree.p + N, nullptr, 1,
                         B, R.d_rroots.p + 32 * r, tl);
     timer_begin(tl, kTimeComm);
@@ -1235,7 +1294,7 @@ void certify(cg_group* g, uint64_t ticket, const double* precomputed_outputs) {
     if (e1 != ncclSuccess || e2 != ncclSuccess || e3 != ncclSuccess || e4 != ncclSuccess)
       throw CudaError(std::string("ncclAllGather: ") + ncclGetErrorString(e4));
   } else {
-    launch_chain_jobs(S.d_jobs.p + B, N * B, tl, /*exclusive_sm=*/true);  // result leaves
+    launch_chain_jobs(S.d_jobs.p + S.off_leaf, N * B, tl, /*exclusive_sm=*/true);  // result leaves
     launch_merkle_trees(R.d_leaf.p, S.d_tree.p, S.d_tree.p + N, nullptr, N, B, R.d_rroots.p, tl);
   }
   timer_begin(tl, kTimeAgree);
@@ -1243,13 +1302,20 @@ void certify(cg_group* g, uint64_t ticket, const double* precomputed_outputs) {
                        (uint32_t)v, g->metric, R.d_sel.p, R.d_diam.p, R.d_sat.p, R.d_status.p,
                        R.d_label.p, tl);
   launch_attest_manifest(B, N, R.d_sel.p, R.d_sat.p, R.d_rroots.p, S.d_reqids.p, g->d_gid.p, gl,
-                         g->version, R.d_aleaf.p, R.d_single_pos.p, R.d_kinds.p, R.d_mnodes.p,
-                         R.d_mops.p, R.d_count.p, tl);
-  launch_chain_jobs(S.d_jobs.p + B + (uint64_t)N * B, N * B, tl);  // single A leaves
-  launch_merkle_trees(R.d_aleaf.p, nullptr, nullptr, R.d_count.p, 1, (uint64_t)N * B + B + N,
-                      R.d_aroot.p, tl);
+                         g->version, R.d_aleaf.p, R.d_single_pos.p, R.d_need53.p, R.d_kinds.p,
+                         R.d_mnodes.p, R.d_mops.p, R.d_count.p, tl);
   timer_end(tl, kTimeAgree);
-  CG_CUDA(cudaEventRecord(S.ev_done, tl));
+  // Single attestation leaves re-hash their request (a 1.2 MB chain at
+  // ImageNet shape): they run on the slot's own stream, off the shared tail,
+  // so a faulty batch delays only its own A root, not the next batches'
+  // tails; requests without a single leaf skip their 0x53 midstate chain.
+  CG_CUDA(cudaEventRecord(S.ev_man, tl));
+  CG_CUDA(cudaStreamWaitEvent(S.stream, S.ev_man, 0));
+  launch_chain_jobs(S.d_jobs.p + S.off_mid53, B, S.stream, /*exclusive_sm=*/true);
+  launch_chain_jobs(S.d_jobs.p + S.off_single, N * B, S.stream);
+  launch_merkle_trees(R.d_aleaf.p, nullptr, nullptr, R.d_count.p, 1, (uint64_t)N * B + B + N,
+                      R.d_aroot.p, S.stream);
+  CG_CUDA(cudaEventRecord(S.ev_done, S.stream));
   S.used = false;
   S.certified = true;
   g->last = &S;
@@ -1352,7 +1418,7 @@ int create_group(cg_ctx* ctx, cg_model* const* models, uint32_t nlocal, uint32_t
     // ingest ring: enough batches in flight to hide the request-midstate
     // chains (latency ~ request bytes / 64 compressions, ~30 ms for a C2
     // request) behind the forwards of the batches certified meanwhile
-    const int depth = 16;
+    const int depth = kIngestRing;
     const size_t arena_max = (size_t)B * (512 + 160 * N) + 1024;
     for (int i = 0; i < depth; i++) {
       auto S = std::make_unique<IngestSlot>();
@@ -1360,19 +1426,20 @@ int create_group(cg_ctx* ctx, cg_model* const* models, uint32_t nlocal, uint32_t
       CG_CUDA(cudaEventCreateWithFlags(&S->ev_staged, cudaEventDisableTiming));
       CG_CUDA(cudaEventCreateWithFlags(&S->ev_prefix, cudaEventDisableTiming));
       CG_CUDA(cudaEventCreateWithFlags(&S->ev_done, cudaEventDisableTiming));
-      S->d_in.ensure(B * g->u);
       S->d_eps.ensure(B);
       S->d_arena.ensure(arena_max);
       S->d_reqids.ensure(32 * B);
-      S->d_jobs.ensure(B * (1 + 2 * N));
+      S->d_jobs.ensure(B * (2 + 2 * N + nlocal));
       S->d_mid.ensure(8 * B);
+      S->d_mid53.ensure(8 * B);
       S->d_tree.ensure(2 * N);
       S->h_arena.ensure(arena_max);
       S->h_reqids.ensure(32 * B);
-      S->h_jobs.ensure(B * (1 + 2 * N));
+      S->h_jobs.ensure(B * (2 + 2 * N + nlocal));
       S->h_eps.ensure(B);
       S->h_tree.ensure(2 * N);
       CG_CUDA(cudaEventCreateWithFlags(&S->ev_fwd, cudaEventDisableTiming));
+      CG_CUDA(cudaEventCreateWithFlags(&S->ev_man, cudaEventDisableTiming));
       S->res.d_outs.ensure((uint64_t)N * B * v);
       S->res.d_topi.ensure((uint64_t)N * B * topk);
       S->res.d_topv.ensure((uint64_t)N * B * topk);
@@ -1390,8 +1457,10 @@ int create_group(cg_ctx* ctx, cg_model* const* models, uint32_t nlocal, uint32_t
       S->res.d_status.ensure(B);
       S->res.d_label.ensure(B);
       S->res.d_single_pos.ensure((uint64_t)N * B);
+      S->res.d_need53.ensure(B);
       g->slots.push_back(std::move(S));
     }
+    ctx->groups.push_back(g.get());
     *out = g.release();
     return CG_OK;
   });
@@ -1419,29 +1488,48 @@ int cg_group_create_dist(cg_ctx* ctx, cg_model* my_model, const uint8_t* all_dig
                       default_eps, group_id, group_id_len, version, max_batch, topk, out);
 }
 
+}  // extern "C"
+
+namespace {
+void encode_results_slot(cg_group* g, const IngestSlot* S, uint32_t provider, uint8_t* out,
+                         uint64_t cap, uint64_t* len) {
+  if (!S || !S->certified) throw InvalidArgument("nothing certified yet");
+  if (provider >= g->N) throw InvalidArgument("provider index >= N");
+  const uint32_t B = S->B, gl = (uint32_t)g->gid.size();
+  const uint64_t v = g->v;
+  const uint64_t need = 4 + (uint64_t)B * (88 + gl + 8 * v);
+  *len = need;
+  if (!out) return;  // size query
+  if (cap < need) throw InvalidArgument("output buffer too small");
+  cudaStream_t st = g->ctx->stream;
+  CG_CUDA(cudaStreamWaitEvent(st, S->ev_done, 0));
+  g->ctx->d_bytes.ensure(need);
+  Digest32 dg;
+  std::memcpy(dg.b, g->digests[provider].data(), 32);
+  launch_encode_results(S->d_reqids.p, S->res.d_outs.p + (uint64_t)provider * B * v, B,
+                        (uint32_t)v, provider, g->d_gid.p, gl, g->version, dg, g->ctx->d_bytes.p,
+                        st);
+  CG_CUDA(cudaMemcpyAsync(out, g->ctx->d_bytes.p, need, cudaMemcpyDeviceToHost, st));
+  CG_CUDA(cudaStreamSynchronize(st));
+}
+}  // namespace
+
+extern "C" {
+
 int cg_group_encode_results(cg_group* g, uint32_t provider, uint8_t* out, uint64_t cap,
                             uint64_t* len) {
   if (!g || !len) return CG_EINVAL;
   return guarded(g->ctx, [&] {
-    const IngestSlot* S = g->last;
-    if (!S || !S->certified) throw InvalidArgument("nothing certified yet");
-    if (provider >= g->N) throw InvalidArgument("provider index >= N");
-    const uint32_t B = S->B, gl = (uint32_t)g->gid.size();
-    const uint64_t v = g->v;
-    const uint64_t need = 4 + (uint64_t)B * (88 + gl + 8 * v);
-    *len = need;
-    if (!out) return CG_OK;  // size query
-    if (cap < need) throw InvalidArgument("output buffer too small");
-    cudaStream_t st = g->ctx->stream;
-    CG_CUDA(cudaStreamWaitEvent(st, S->ev_done, 0));
-    g->ctx->d_bytes.ensure(need);
-    Digest32 dg;
-    std::memcpy(dg.b, g->digests[provider].data(), 32);
-    launch_encode_results(S->d_reqids.p, S->res.d_outs.p + (uint64_t)provider * B * v, B,
-                          (uint32_t)v, provider, g->d_gid.p, gl, g->version, dg,
-                          g->ctx->d_bytes.p, st);
-    CG_CUDA(cudaMemcpyAsync(out, g->ctx->d_bytes.p, need, cudaMemcpyDeviceToHost, st));
-    CG_CUDA(cudaStreamSynchronize(st));
+    encode_results_slot(g, g->last, provider, out, cap, len);
+    return CG_OK;
+  });
+}
+
+int cg_group_encode_results_ticket(cg_group* g, uint64_t ticket, uint32_t provider,
+                                   uint8_t* out, uint64_t cap, uint64_t* len) {
+  if (!g || !len) return CG_EINVAL;
+  return guarded(g->ctx, [&] {
+    encode_results_slot(g, &certified_slot(g, ticket), provider, out, cap, len);
     return CG_OK;
   });
 }
@@ -1450,8 +1538,11 @@ int cg_group_set_perturbation(cg_group* g, double magnitude) {
   if (!g) return CG_EINVAL;
   return guarded(g->ctx, [&] {
     if (!(magnitude >= 0.0)) throw InvalidArgument("negative magnitude");
+    for (auto& sl : g->slots)
+      if (sl->used) throw InvalidArgument("set the perturbation with no batch ingested ahead");
     cudaStream_t st = g->ctx->stream;
     CG_CUDA(cudaStreamSynchronize(st));  // no certify in flight reads the header
+    for (auto& sl : g->slots) CG_CUDA(cudaStreamSynchronize(sl->stream));
     const uint32_t nloc = (uint32_t)g->models.size();
     g->d_phdr.ensure(64ull * nloc);
     std::vector<uint8_t> h(64ull * nloc, 0);
@@ -1468,8 +1559,26 @@ int cg_group_set_perturbation(cg_group* g, double magnitude) {
   });
 }
 
+int cg_group_set_fault(cg_group* g, uint32_t provider, double offset, double fraction) {
+  if (!g) return CG_EINVAL;
+  return guarded(g->ctx, [&] {
+    if (provider >= g->N) throw InvalidArgument("provider index >= N");
+    if (!(fraction >= 0.0 && fraction <= 1.0)) throw InvalidArgument("fraction outside [0, 1]");
+    if (!std::isfinite(offset)) throw InvalidArgument("offset must be finite");
+    g->fault_provider = provider;
+    g->fault_offset = offset;
+    g->fault_thr = offset == 0.0 ? 0u : (uint32_t)std::lround(256.0 * fraction);
+    return CG_OK;
+  });
+}
+
 void cg_group_free(cg_group* g) {
   if (!g) return;
+  {
+    std::lock_guard<std::mutex> lk(g->ctx->mu);
+    auto& v = g->ctx->groups;
+    v.erase(std::remove(v.begin(), v.end(), g), v.end());
+  }
   cudaSetDevice(g->ctx->device);
   cudaStreamSynchronize(g->ctx->stream);
   if (g->ctx->tail) cudaStreamSynchronize(g->ctx->tail);
@@ -1655,30 +1764,51 @@ int cg_merkle_path_roots(cg_ctx* ctx, const uint8_t* leaf_hashes, const uint8_t*
   });
 }
 
+}  // extern "C"
+
+namespace {
+void group_auth_paths(cg_group* g, const IngestSlot* S, uint32_t tree, const uint64_t* indices,
+                      uint32_t count, uint8_t* siblings, uint8_t* sides, uint32_t* lens) {
+  if (!S || !S->certified) throw InvalidArgument("nothing certified yet");
+  const uint32_t B = S->B, N = g->N;
+  if (tree > N) throw InvalidArgument("tree index out of range");
+  if (g->dist && tree < N && tree != g->rank)
+    throw InvalidArgument("replica-parallel group: only this rank's result tree is local");
+  const uint8_t* leaves;
+  uint64_t n;
+  const BatchResults& R = S->res;
+  CG_CUDA(cudaStreamWaitEvent(g->ctx->stream, S->ev_done, 0));
+  if (tree < N) {  // provider `tree`'s R tree: its B result leaves
+    leaves = R.d_leaf.p + 32 * (uint64_t)tree * B;
+    n = B;
+  } else {  // the attestation tree, manifest order
+    uint32_t cnt = 0;
+    CG_CUDA(cudaMemcpyAsync(&cnt, R.d_count.p, 4, cudaMemcpyDeviceToHost, g->ctx->stream));
+    CG_CUDA(cudaStreamSynchronize(g->ctx->stream));
+    leaves = R.d_aleaf.p;
+    n = cnt;
+  }
+  auth_paths_device(g->ctx, leaves, n, indices, count, siblings, sides, lens, nullptr);
+}
+}  // namespace
+
+extern "C" {
+
 int cg_group_auth_paths(cg_group* g, uint32_t tree, const uint64_t* indices, uint32_t count,
                         uint8_t* siblings, uint8_t* sides, uint32_t* lens) {
   if (!g) return CG_EINVAL;
   return guarded(g->ctx, [&] {
-    const uint32_t B = g->last_B, N = g->N;
-    if (B == 0 || !g->last) throw InvalidArgument("nothing certified yet");
-    if (tree > N) throw InvalidArgument("tree index out of range");
-    if (g->dist && tree < N && tree != g->rank)
-      throw InvalidArgument("replica-parallel group: only this rank's result tree is local");
-    const uint8_t* leaves;
-    uint64_t n;
-    const BatchResults& R = g->last->res;
-    CG_CUDA(cudaStreamWaitEvent(g->ctx->stream, g->last->ev_done, 0));
-    if (tree < N) {  // provider `tree`'s R tree: its B result leaves
-      leaves = R.d_leaf.p + 32 * (uint64_t)tree * B;
-      n = B;
-    } else {  // the attestation tree, manifest order
-      uint32_t cnt = 0;
-      CG_CUDA(cudaMemcpyAsync(&cnt, R.d_count.p, 4, cudaMemcpyDeviceToHost, g->ctx->stream));
-      CG_CUDA(cudaStreamSynchronize(g->ctx->stream));
-      leaves = R.d_aleaf.p;
-      n = cnt;
-    }
-    auth_paths_device(g->ctx, leaves, n, indices, count, siblings, sides, lens, nullptr);
+    group_auth_paths(g, g->last, tree, indices, count, siblings, sides, lens);
+    return CG_OK;
+  });
+}
+
+int cg_group_auth_paths_ticket(cg_group* g, uint64_t ticket, uint32_t tree,
+                               const uint64_t* indices, uint32_t count, uint8_t* siblings,
+                               uint8_t* sides, uint32_t* lens) {
+  if (!g) return CG_EINVAL;
+  return guarded(g->ctx, [&] {
+    group_auth_paths(g, &certified_slot(g, ticket), tree, indices, count, siblings, sides, lens);
     return CG_OK;
   });
 }
@@ -1731,10 +1861,7 @@ int cg_group_fetch(cg_group* g, cg_certify_out* out) {
 int cg_group_fetch_ticket(cg_group* g, uint64_t ticket, cg_certify_out* out) {
   if (!g || !out) return CG_EINVAL;
   return guarded(g->ctx, [&] {
-    const IngestSlot& S = *g->slots[ticket % g->slots.size()];
-    if (S.ticket != ticket || !S.certified)
-      throw InvalidArgument("ticket not certified or its slot already reused");
-    certify_fetch(g, out, &S);
+    certify_fetch(g, out, &certified_slot(g, ticket));
     return CG_OK;
   });
 }

@@ -4,6 +4,7 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 
@@ -48,6 +49,22 @@ void timer_begin(cudaStream_t st, int cls);
 void timer_end(cudaStream_t st, int cls);
 
 constexpr int kNumSMs = 148;
+
+// Runs f() once per device: cudaFuncSetAttribute opt-ins (dynamic shared
+// memory above 48 KB) apply to the current device only, so a process that
+// drives several GPUs must set them on each.
+template <typename F>
+void once_per_device(std::atomic<uint64_t>& done, F&& f) {
+  int d = 0;
+  CG_CUDA(cudaGetDevice(&d));
+  const uint64_t bit = 1ull << (d & 63);
+  if (done.load(std::memory_order_acquire) & bit) return;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.load(std::memory_order_acquire) & bit) return;
+  f();
+  done.fetch_or(bit, std::memory_order_release);
+}
 
 __host__ __device__ inline uint64_t ceil_div(uint64_t a, uint64_t b) {
   return (a + b - 1) / b;

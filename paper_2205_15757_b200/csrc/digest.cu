@@ -50,12 +50,11 @@ void launch_chain_jobs(const ChainJob* d_jobs, uint32_t n, cudaStream_t st,
   // exclusive_sm: claim (unused) shared memory so the CTA can never share an
   // SM with a persistent GEMM CTA (~200 KB); long chains then run on their
   // own SMs instead of slowing one statically scheduled GEMM CTA.
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<uint64_t> attr{0};
+  once_per_device(attr, [] {
     CG_CUDA(cudaFuncSetAttribute(chain_jobs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  kChainExclusiveSmem));
-    attr = true;
-  }
+  });
   timer_begin(st, kTimeChain);
   chain_jobs_kernel<<<(unsigned)ceil_div(n, tpb), tpb, exclusive_sm ? kChainExclusiveSmem : 0,
                       st>>>(d_jobs, n);
@@ -163,13 +162,12 @@ void launch_merkle_trees(const uint8_t* d_leaves, const uint64_t* d_off,
   if (max_leaves > kMerkleSmemLeaves)
     throw InvalidArgument("merkle_tree: too many leaves for one CTA");
   size_t smem = 32 * ((max_leaves + 1) / 2 + 1);
-  static bool attr_set = false;
-  if (!attr_set) {
+  static std::atomic<uint64_t> attr{0};
+  once_per_device(attr, [] {
     CG_CUDA(cudaFuncSetAttribute(merkle_tree_kernel,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  32 * (kMerkleSmemLeaves / 2 + 1)));
-    attr_set = true;
-  }
+  });
   merkle_tree_kernel<<<ntrees, 256, smem, st>>>(d_leaves, d_off, d_len,
                                                 d_count, n_const, d_roots);
   CG_CHECK_LAUNCH();
@@ -376,6 +374,28 @@ void launch_perturb_tail(const uint32_t* d_mid, const double* d_in, uint64_t u,
   if (n == 0) return;
   perturb_tail_kernel<<<(unsigned)ceil_div(n, 128), 128, 0, st>>>(d_mid, d_in, u, hdr, nshared,
                                                                 d_out, ldo, B, v, mag);
+  CG_CHECK_LAUNCH();
+}
+
+// OffsetExecutor (proj/src/harness.cpp:167-186, the corrupt_result fault):
+// every output lane of the faulty node += offset, applied after the
+// PerturbingExecutor it wraps (harness.cpp:255-261). Fault injection for a
+// fraction of requests: request k is hit when its first request-id byte is
+// below `thr` (thr = 256: every request, exactly the reference's executor).
+__global__ void offset_outputs_kernel(double* __restrict__ out, const uint8_t* __restrict__ reqids,
+                                      uint32_t B, uint32_t v, double offset, uint32_t thr) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (uint64_t)B * v) return;
+  const uint32_t k = (uint32_t)(i / v);
+  if ((uint32_t)reqids[32ull * k] < thr) out[i] = __dadd_rn(out[i], offset);
+}
+
+void launch_offset_outputs(double* d_out, const uint8_t* d_reqids, uint32_t B, uint32_t v,
+                           double offset, uint32_t thr, cudaStream_t st) {
+  const uint64_t n = (uint64_t)B * v;
+  if (n == 0 || thr == 0) return;
+  offset_outputs_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(d_out, d_reqids, B, v, offset,
+                                                                    thr);
   CG_CHECK_LAUNCH();
 }
 

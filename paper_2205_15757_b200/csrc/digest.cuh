@@ -63,4 +63,9 @@ void launch_perturb_tail(const uint32_t* d_mid, const double* d_in, uint64_t u,
                          uint64_t ldo, uint32_t B, uint32_t v, double mag,
                          cudaStream_t st);
 
+// OffsetExecutor (harness.cpp:167-186) on one provider's B x v outputs for
+// the requests whose first id byte is < thr (256 = all).
+void launch_offset_outputs(double* d_out, const uint8_t* d_reqids, uint32_t B, uint32_t v,
+                           double offset, uint32_t thr, cudaStream_t st);
+
 }  // namespace cg

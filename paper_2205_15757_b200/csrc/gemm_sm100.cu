@@ -10,6 +10,8 @@
 #include "common.cuh"
 #include "gemm_sm100.cuh"
 
+#include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 
@@ -343,6 +345,103 @@ __device__ __forceinline__ int remap_row(int M, int rows_out, int mode, int H,
   return img * HpWp + (h + 1) * Wp + w;
 }
 
+// ------------------------------------------------------------ tile scheduler
+// The work of a launch is `units` runs of T consecutive tiles.
+//  * static (a.sched == 0: SM-pair launches, tests that force a small grid):
+//    a persistent grid, CTA (pair) b takes units b, b + G, b + 2G, ...
+//  * CLC (a.sched == 1, the default): one CTA per unit. A running CTA takes
+//    its own unit, then keeps cancelling not-yet-launched CTAs of its grid
+//    with Blackwell cluster launch control (clusterlaunchcontrol.try_cancel)
+//    and runs their units instead. A CTA that cannot get an SM -- because the
+//    SHA-256 chain kernels of the ingest streams hold it -- never runs: the
+//    resident CTAs take its work, so no tile ever waits behind another
+//    kernel, and the grid needs no SM budget guessed on the host.
+// One cancel request is in flight per CTA (issued by the TMA producer when it
+// starts a unit); its 16-byte response lands in a ring slot whose mbarrier
+// every consumer warp waits on, and every warp that walks the tile sequence
+// releases the slot (cempty counts those warps).
+constexpr int kClcSlots = 8;
+struct TileSched {
+  int tiles, T, step;
+  bool clc;
+  uint32_t resp, cfull, cempty;  // shared::cta addresses of slot 0
+  int unit = 0, k = 0, nu = 0, t = 0;
+  __device__ __forceinline__ void issue(int q) const {
+    const int slot = q % kClcSlots, use = q / kClcSlots;
+    const uint32_t e = cempty + 8 * slot, f = cfull + 8 * slot;
+    if (use >= 1) {
+      asm volatile(
+          "{\n\t.reg .pred p;\n"
+          "CLCE_%=:\n\t"
+          "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+          "@!p bra CLCE_%=;\n}" ::"r"(e), "r"((uint32_t)((use - 1) & 1))
+          : "memory");
+    }
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], 16;" ::"r"(f) : "memory");
+    asm volatile(
+        "clusterlaunchcontrol.try_cancel.async.shared::cta.mbarrier::complete_tx::bytes.b128"
+        " [%0], [%1];" ::"r"(resp + 16 * slot), "r"(f)
+        : "memory");
+  }
+  // Response q: true and the cancelled CTA's unit, or false (grid exhausted).
+  __device__ __forceinline__ bool take(int q, int& u, bool arrive) const {
+    const int slot = q % kClcSlots, use = q / kClcSlots;
+    const uint32_t f = cfull + 8 * slot;
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "CLCF_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra CLCF_%=;\n}" ::"r"(f), "r"((uint32_t)(use & 1))
+        : "memory");
+    uint32_t ok, x;
+    asm volatile(
+        "{\n\t.reg .b128 rr;\n\t.reg .pred p;\n\t"
+        "ld.shared.b128 rr, [%2];\n\t"
+        "clusterlaunchcontrol.query_cancel.is_canceled.pred.b128 p, rr;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t"
+        "clusterlaunchcontrol.query_cancel.get_first_ctaid::x.b32.b128 %1, rr;\n}"
+        : "=r"(ok), "=r"(x)
+        : "r"(resp + 16 * slot)
+        : "memory");
+    __syncwarp(__activemask());
+    if (arrive)
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(cempty + 8 * slot) : "memory");
+    u = (int)x;
+    return ok != 0;
+  }
+  __device__ __forceinline__ bool first(int first_unit, bool issuer) {
+    unit = first_unit;
+    k = 0;
+    nu = 1;
+    t = unit * T;
+    if (t >= tiles) return false;
+    if (clc && issuer) issue(0);
+    return true;
+  }
+  // arrive: this thread releases response slots for its warp (lane 0)
+  __device__ __forceinline__ bool next(bool issuer, bool arrive) {
+    if (++k < T && t + 1 < tiles) {
+      t++;
+      return true;
+    }
+    if (!clc) {
+      unit += step;
+      k = 0;
+      t = unit * T;
+      return t < tiles;
+    }
+    const int q = nu - 1;
+    int u;
+    if (!take(q, u, arrive)) return false;
+    unit = u;
+    nu++;
+    k = 0;
+    t = unit * T;
+    if (issuer) issue(q + 1);
+    return true;
+  }
+};
+
 #define CG_TRACE(slot, i)                                             \
   do {                                                                \
     if (a.trace && blockIdx.x == 0 && (i) < 64 && (lane == 0))        \
@@ -386,6 +485,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* hempty = hfull + (HALO > 0 ? HALO : 1);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(hempty + (HALO > 0 ? HALO : 1));
   int* s_tap = reinterpret_cast<int*>(tmem_slot + 4);
+  // CLC response ring (16 B aligned) and its full/empty barriers
+  uint8_t* clc_base = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(s_tap + 9) + 15) & ~uintptr_t(15));
+  uint64_t* cfull = reinterpret_cast<uint64_t*>(clc_base + 16 * kClcSlots);
+  uint64_t* cempty = cfull + kClcSlots;
   // identity rows + bf16 out: thread-per-row epilogue, TMA bulk stores
   const bool tma_out = a.row_mode == kRowIdentity && !a.out_f32;
   const bool res_tma = kResSlots > 0 && gp.residual[0] != nullptr && tma_out;
@@ -400,16 +504,25 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int BMT = PAIR ? 2 * BM : BM;
   const int num_mt = (a.M + BMT - 1) / BMT;
   const int tiles = num_mt * num_n * gp.n;
-  const int t_first = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
-  const int t_step = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+  const int first_unit = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
   const int kpt = a.Kc / BK, num_k = a.ntaps * kpt;
   (void)num_m;
   auto coords = [&](int t, int& r, int& m0, int& n0) {
-    const int per_m = gp.n * num_n;
-    const int mb = t / per_m, rem = t - mb * per_m;
-    r = rem / num_n;
-    m0 = mb * BMT + (int)crank * BM;
-    n0 = (rem - r * num_n) * BN;
+    if constexpr (RESB > 0) {
+      // resident weights: replica-major, so a CTA's consecutive tiles (and
+      // the units it steals, which follow launch order) rarely switch replica
+      const int per_r = num_mt * num_n;
+      r = t / per_r;
+      const int rem = t - r * per_r, mb = rem / num_n;
+      m0 = mb * BMT + (int)crank * BM;
+      n0 = (rem - mb * num_n) * BN;
+    } else {
+      const int per_m = gp.n * num_n;
+      const int mb = t / per_m, rem = t - mb * per_m;
+      r = rem / num_n;
+      m0 = mb * BMT + (int)crank * BM;
+      n0 = (rem - r * num_n) * BN;
+    }
   };
 
   if (warp == 0 && lane == 0) {
@@ -439,6 +552,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&hfull[s], 1);
       mbar_init(&hempty[s], 1);
     }
+    // CLC slots are released by the producer, the MMA warp, the 8 epilogue
+    // warps and (when it streams a residual) the residual loader
+    for (int s = 0; s < kClcSlots; s++) {
+      mbar_init(&cfull[s], 1);
+      mbar_init(&cempty[s], 2 + kEpiWarps + (res_tma ? 1 : 0));
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -461,6 +580,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  TileSched sched;
+  sched.tiles = tiles;
+  sched.T = a.sched ? a.tile_unit : 1;
+  sched.step = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+  sched.clc = !PAIR && a.sched != 0;
+  sched.resp = su32(clc_base);
+  sched.cfull = su32(cfull);
+  sched.cempty = su32(cempty);
   // Programmatic dependent launch: the setup above (barriers, TMEM, tensor
   // map prefetch) overlapped the previous launch's tail; wait for that grid
   // and its memory before reading activations or writing outputs, and let
@@ -475,18 +602,24 @@ __global__ void __launch_bounds__(kThreads, 1)
       int ti = 0;
       int hs = 0;
       uint32_t hphase = 0;
-      for (int t = t_first; t < tiles; t += t_step, ti++) {
+      int wr = -1, wl = 0;  // RESB: replica whose weights are resident, loads so far
+      for (bool ok = sched.first(first_unit, true); ok; ok = sched.next(true, true), ti++) {
+        const int t = sched.t;
         int r, m0, n0;
         coords(t, r, m0, n0);
         CG_TRACE(0, ti);
         if constexpr (RESB > 0) {
-          // resident weights: this CTA's (replica, n block) never changes
-          // (grid % replicas == 0, one n block), so all RESB tiles of B are
-          // loaded once; per tile only the halo boxes stream
-          if (ti == 0) {
+          // resident weights (one n block): all RESB tiles of B are loaded
+          // when the replica changes (full[0] / empty[0] are the weight
+          // barriers: the MMA warp releases the old set before a reload);
+          // per tile only the halo boxes stream
+          if (r != wr) {
+            if (wl > 0) mbar_wait(&empty[0], (uint32_t)((wl - 1) & 1));
             mbar_expect_tx(&full[0], RESB * B_BYTES);
             for (int j = 0; j < RESB; j++)
               tma_load_2d(&gp.B[r], &full[0], sB + j * B_BYTES, j * BK, n0);
+            wr = r;
+            wl++;
           }
           const int hrows = BM + 2 * a.halo_lo;
           for (int cb = 0; cb < kpt; cb++) {
@@ -574,15 +707,22 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0, acc = 0, hs = 0;
       uint32_t phase = 0, acc_phase = 0, hphase = 0;
       int ti = 0;
-      for (int t = t_first; t < tiles; t += t_step, ti++) {
+      int mr = -1, ml = 0;  // RESB: replica of the resident weights, sets consumed
+      for (bool ok = sched.first(first_unit, false); ok;
+           ok = sched.next(false, lane == 0), ti++) {
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         CG_TRACE(2, ti);
         tc_fence_after();
         const uint32_t d = tmem + acc * BN;
         if constexpr (RESB > 0) {
-          if (ti == 0) {
-            mbar_wait(&full[0], 0);
+          int r_, m0_, n0_;
+          coords(sched.t, r_, m0_, n0_);
+          if (r_ != mr) {
+            if (ml > 0) umma_commit_w(&empty[0]);  // old weights free once the MMAs drain
+            mbar_wait(&full[0], (uint32_t)(ml & 1));
             tc_fence_after();
+            mr = r_;
+            ml++;
           }
           // 9 taps unrolled: tap offsets come from the kernel parameters and
           // every descriptor is uniform arithmetic (no per-MMA register moves)
@@ -708,9 +848,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     // through the ring in epilogue order, as far ahead as the slots allow.
     if (res_tma && lane == 0) {
       int g = 0;
-      for (int t = t_first; t < tiles; t += t_step) {
+      for (bool ok = sched.first(first_unit, false); ok; ok = sched.next(false, true)) {
         int r, m0, n0;
-        coords(t, r, m0, n0);
+        coords(sched.t, r, m0, n0);
         for (int c = 0; c < BN / kResCols; c++, g++) {
           const int slot = g % kRS;
           if (g >= kRS) mbar_wait(&rempty[slot], ((g / kRS) - 1) & 1);
@@ -738,7 +878,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     int tile_i = 0, acc = 0;
     int stage_seq = 0;  // staging buffer sequence across all of this warp's chunks
     uint32_t acc_phase = 0;
-    for (int t = t_first; t < tiles; t += t_step, tile_i++) {
+    for (bool ok = sched.first(first_unit, false); ok;
+         ok = sched.next(false, lane == 0), tile_i++) {
+      const int t = sched.t;
       if (kTileSplit && (tile_i & 1) != h) {
         // the other group drains this accumulator; release our share of it
         __syncwarp();
@@ -988,39 +1130,54 @@ constexpr int smem_bytes() {
          (RESB > STAGES ? RESB : STAGES) * (PAIR ? BN / 2 : BN) * BK * 2 +
          kResSlots * 8192 + kEpiWarps * 32 * kStgLd * 4 +
          8 * (2 * STAGES + 4 + 2 * (kResSlots > 0 ? kResSlots : 1) + 2 * (HALO > 0 ? HALO : 1)) +
-         16 + 48;
+         16 + 48 + 16 + 32 * kClcSlots;
 }
 
 // env CREDO_NO_PDL: plain stream serialisation between GEMM launches (A/B)
 const int g_pdl = std::getenv("CREDO_NO_PDL") == nullptr ? 1 : 0;
+// env CREDO_NO_CLC: static persistent grids (A/B); CREDO_CLC_UNIT_NS: target
+// work per scheduling unit
+const bool g_clc = std::getenv("CREDO_NO_CLC") == nullptr;
+const double g_unit_ns = std::getenv("CREDO_CLC_UNIT_NS") ? std::atof(std::getenv("CREDO_CLC_UNIT_NS"))
+                                                          : 1500.0;
+
+// Tiles per CLC unit: enough work per unit (~g_unit_ns at ~8 TFLOP/s per SM)
+// to hide one cancel round trip, while leaving >= 3 units per SM so CTAs that
+// start late (SMs freed by other kernels) still balance the load.
+int tiles_per_unit(const ConvGemmArgs& a, int BN, int tiles) {
+  const double tile_flops = 2.0 * BM * BN * (double)a.Kc * a.ntaps;
+  const double tile_ns = tile_flops / 8.0e3;  // 8 TFLOP/s per SM = 8e3 FLOP/ns
+  int T = (int)std::ceil(g_unit_ns / std::max(tile_ns, 1.0));
+  T = std::min(T, std::max(1, tiles / (3 * kNumSMs)));
+  return std::max(T, 1);
+}
 
 template <int BN, int STAGES, int RS, int HALO = 0, int RESB = 0, int PAIR = 0>
 void launch_t(const PreparedGemm& p, cudaStream_t st, int max_ctas) {
-  static bool attr = false;
   constexpr int smem = smem_bytes<BN, STAGES, RS, HALO, RESB, PAIR>();
   static_assert(smem <= 232448, "smem budget");
-  if (!attr) {
+  static std::atomic<uint64_t> attr{0};
+  once_per_device(attr, [] {
     CG_CUDA(cudaFuncSetAttribute(conv_gemm_kernel<BN, STAGES, RS, HALO, RESB, PAIR>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr = true;
-  }
-  const ConvGemmArgs& a = p.args;
-  int tiles = ((a.M + BM - 1) / BM) * ((a.N + BN - 1) / BN) * p.gp.n;
-  const int budget = gemm_sm_budget();
-  int grid = tiles < budget ? tiles : budget;
-  if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
-  if (RESB > 0) {  // each CTA keeps one replica's weights: grid % replicas == 0
-    grid -= grid % p.gp.n;
-    if (grid < p.gp.n) throw InvalidArgument("conv_gemm: grid too small for resident weights");
+  });
+  ConvGemmArgs a = p.args;
+  const int tiles = ((a.M + BM - 1) / BM) * ((a.N + BN - 1) / BN) * p.gp.n;
+  int grid;
+  if (!PAIR && g_clc && max_ctas <= 0) {
+    a.sched = 1;
+    a.tile_unit = tiles_per_unit(a, BN, tiles);
+    grid = (tiles + a.tile_unit - 1) / a.tile_unit;
+  } else {
+    a.sched = 0;
+    a.tile_unit = 1;
+    grid = std::min(tiles, max_ctas > 0 ? max_ctas : kNumSMs);
   }
   timer_begin(st, kTimeGemm);
   if constexpr (PAIR) {
-    // SM pairs: a cluster of 2 CTAs per 256-row tile
+    // SM pairs (static scheduler): a cluster of 2 CTAs per 256-row tile
     const int pair_tiles = ((a.M + 2 * BM - 1) / (2 * BM)) * ((a.N + BN - 1) / BN) * p.gp.n;
-    // a pair needs both SMs of a TPC: each SM held back from the budget (by
-    // a concurrent chain CTA) can block one TPC
-    const int tpcs = kNumSMs / 2 - (kNumSMs - budget);
-    int g2 = std::min(2 * pair_tiles, 2 * std::max(tpcs, 1));
+    int g2 = std::min(2 * pair_tiles, kNumSMs);
     if (max_ctas > 0) g2 = std::min(g2, max_ctas - (max_ctas & 1));
     if (g2 < 2) throw InvalidArgument("conv_gemm: an SM pair needs 2 CTAs");
     cudaLaunchConfig_t cfg = {};
@@ -1211,11 +1368,6 @@ double mma_rate_bench(int N, int iters, int ctas, int two_acc, cudaStream_t st) 
   return (double)c / (4.0 * iters);
 }
 
-static std::atomic<int> g_sm_budget{kNumSMs};
-void set_gemm_sm_budget(int sms) {
-  g_sm_budget = sms < 1 ? 1 : (sms > kNumSMs ? kNumSMs : sms);
-}
-int gemm_sm_budget() { return g_sm_budget.load(); }
 
 void make_operand(Operand& op, const void* ptr, int rows, int cols, int box_rows) {
   if (cols % 64 != 0) throw InvalidArgument("operand K must be a multiple of 64");

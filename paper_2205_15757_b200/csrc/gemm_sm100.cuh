@@ -56,6 +56,11 @@ struct ConvGemmArgs {
   // BM + 2*halo_lo (<= 256) rows.
   int halo_lo;
   int pair;  // 1: SM-pair (cta_group::2) 256-row tiles, B operand box = BN/2 rows
+  // Tile scheduler, set by the launcher: 0 = static persistent stride, 1 =
+  // cluster launch control (one CTA per unit of tile_unit tiles; resident
+  // CTAs cancel pending ones and take their units).
+  int sched;
+  int tile_unit;
 };
 
 // One encoded operand (tensor map over a row-major bf16 [rows, cols] matrix
@@ -102,15 +107,12 @@ struct PreparedGemm {
 void prepare_conv_gemm(PreparedGemm& p, const ConvGemmGroup& g, const ConvGemmArgs& a, int BN);
 void launch_prepared(const PreparedGemm& p, cudaStream_t st, int max_ctas = 0);
 
-// SMs the persistent GEMM grid may occupy (default all 148). The certify
-// pipeline lowers it while request-midstate chains run on their own SMs, so
-// no statically scheduled GEMM CTA ever shares an SM with a chain CTA.
-void set_gemm_sm_budget(int sms);
 // Cycles per M=128 x N x K=16 SS-mode MMA issued back to back (microbench).
 double mma_rate_bench(int N, int iters, int ctas, int two_acc, cudaStream_t st);
-int gemm_sm_budget();
 
-// Launches the persistent warp-specialised kernel; BN in {64, 128, 256}.
+// Launches the warp-specialised kernel; BN in {64, 128, 256}. max_ctas > 0
+// forces the static persistent scheduler on at most that many CTAs (tests);
+// otherwise tiles are handed out by cluster launch control.
 void launch_conv_gemm(const Operand& A, const Operand& B, const ConvGemmArgs& a,
                       int BN, cudaStream_t st, int max_ctas = 0);
 

@@ -17,12 +17,15 @@ them. Fixture contents:
                    hashes, and ref_certify_batch results for three fault
                    patterns (honest / one replica corrupt on some requests /
                    tight epsilon -> failures)
+* c1_full.npz    — the same at SURVEY §8(d)'s C1 shape (3072 -> 10 softmax,
+                   3 models, batch 64, seed 7), every-5th-request fault
 * perturb.npz    — PerturbingExecutor(ToyExecutor, node, magnitude) outputs
                    over generate_group models with u in {1, 9, 3072} (0, 1
                    and 384 shared SHA blocks; 1- and 2-block lane tails), a
                    softmax model, several nodes and magnitudes
 
     python tests/golden/make_golden.py perturb   # that fixture alone
+    python tests/golden/make_golden.py c1_full   # that fixture alone
 """
 import os
 import sys
@@ -173,6 +176,48 @@ def c1_fixture(R):
     np.savez_compressed(os.path.join(OUT, "c1_batch.npz"), **save)
 
 
+def c1_full_fixture(R):
+    """C1 at SURVEY §8(d)'s shape: generate_group("group-0", u=3072, v=10,
+    3 models, euclidean, eps=0.05, seed=7) with softmax, requests from
+    make_requests(1, 7, 64, 3072) (harness.cpp:346-395, :449-458), batch 64.
+    The inputs travel inside the request encodings."""
+    u, v, N, B, eps = 3072, 10, 3, 64, 0.05
+    gid = b"group-0"
+    files, digs = R.generate_group(gid, u, v, N, 0, eps, seed=7, softmax=True)
+    inputs, encs = R.make_requests(1, 7, B, u, gid)
+    outs = np.stack([R.linear_run(files[p], inputs, v) for p in range(N)])  # N,B,v
+    leaf = np.zeros((N, B, 32), np.uint8)
+    for p in range(N):
+        for k in range(B):
+            leaf[p, k] = np.frombuffer(
+                R.result_leaf_hash(encs[k], p, gid, 1, outs[p, k], digs[p]), np.uint8)
+    variants = {"honest": outs.copy()}
+    bad = outs.copy()  # corrupt_result (+1.0 every lane) on replica 2, every 5th request
+    bad[2, ::5] += 1.0
+    variants["partial_fault"] = bad
+    fail = bad.copy()  # replica 1 also off on request 10 -> unsatisfied -> failure leaf
+    fail[1, 10] -= 2.0
+    variants["failure"] = fail
+    h = R.batch_new(encs, 1)
+    save = dict(u=u, v=v, N=N, B=B, eps=eps, gid=np.frombuffer(gid, np.uint8),
+                files=np.stack([np.frombuffer(f_, np.uint8) for f_ in files]),
+                digests=np.stack([np.frombuffer(d, np.uint8) for d in digs]),
+                req_lens=np.array([len(e) for e in encs], np.uint64),
+                reqs=np.frombuffer(b"".join(encs), np.uint8), outputs=outs, leaf_hashes=leaf)
+    for name, o in variants.items():
+        r = R.certify_batch(h, N, 1, 0, eps, o, 1, digs, threads=4)
+        save[f"{name}_outputs"] = o
+        save[f"{name}_sel"] = r["sel_mask"]
+        save[f"{name}_diam"] = r["diameter"]
+        save[f"{name}_sat"] = r["satisfied"]
+        save[f"{name}_label"] = r["label"]
+        save[f"{name}_r_roots"] = np.frombuffer(b"".join(r["r_roots"]), np.uint8).reshape(N, 32)
+        save[f"{name}_a_root"] = np.frombuffer(r["a_root"], np.uint8)
+        save[f"{name}_mlen"] = np.array(r["manifest_len"], np.uint64)
+    R.batch_free(h)
+    np.savez_compressed(os.path.join(OUT, "c1_full.npz"), **save)
+
+
 # (u, v, softmax, node, magnitude, seed)
 PERTURB_CASES = [(1, 3, False, 0, 0.25, 11), (9, 5, False, 3, 1e-3, 12),
                  (3072, 10, False, 1, 0.05, 7), (3072, 10, True, 2, 1e-4, 7),
@@ -203,10 +248,14 @@ if __name__ == "__main__":
     if sys.argv[1:] == ["perturb"]:
         perturb_fixture(R)
         sys.exit(0)
+    if sys.argv[1:] == ["c1_full"]:
+        c1_full_fixture(R)
+        sys.exit(0)
     sha_fixture(R)
     merkle_fixture(R)
     quorum_fixture(R)
     c1_fixture(R)
+    c1_full_fixture(R)
     perturb_fixture(R)
     for f in sorted(os.listdir(OUT)):
         if f.endswith(".npz"):

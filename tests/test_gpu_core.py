@@ -177,6 +177,37 @@ def test_certify_batch_c1_bit_exact(ctx):
     assert np.array_equal(r["topk_idx"][..., 0], np.argmax(g["outputs"], axis=-1))
 
 
+def test_certify_c1_full_shape(ctx, oracle):
+    """C1 at SURVEY §8(d)'s shape (c1_full.npz: generate_group 3072 -> 10
+    with softmax, 3 replicas, f=1, batch 64, seed 7, from the compiled
+    reference): the GPU's softmax outputs within the stated 4 ulp of the
+    reference's (CUDA exp vs glibc exp), every digest and decision recomputed
+    by the oracle from the GPU's own outputs, and the reference's own
+    certificates (roots, manifests) reproduced bit-exact from its outputs for
+    the honest / fault / failure variants."""
+    from conftest import check_certificate
+    from paper_2205_15757_b200 import RequestBatch
+    g = golden("c1_full.npz")
+    B, N = int(g["B"]), int(g["N"])
+    grp = _group(ctx, g, B)
+    batch = RequestBatch.from_encoded(split_reqs(g))
+    r = grp.certify(batch, want_outputs=True, want_leaves=True)
+    want = g["outputs"]
+    assert np.all(np.abs(r["outputs"] - want) <= 4 * np.spacing(want))
+    digs = [g["digests"][p].tobytes() for p in range(N)]
+    check_certificate(r, batch, digs, 1, float(g["eps"]), g["gid"].tobytes(), oracle, topk=3)
+    for variant in ("honest", "partial_fault", "failure"):
+        r = grp.certify_outputs(batch, g[f"{variant}_outputs"])
+        assert np.array_equal(r["selected"], g[f"{variant}_sel"].astype(np.uint32))
+        assert np.array_equal(r["diameter"].view(np.uint64), g[f"{variant}_diam"].view(np.uint64))
+        assert np.array_equal(r["satisfied"], g[f"{variant}_sat"].astype(bool))
+        assert np.array_equal(r["label"], g[f"{variant}_label"])
+        assert np.array_equal(r["r_roots"], g[f"{variant}_r_roots"])
+        assert int(r["manifest_len"][0]) == int(g[f"{variant}_mlen"])
+        assert np.array_equal(r["a_root"], g[f"{variant}_a_root"]), variant
+    grp.free()
+
+
 @pytest.mark.parametrize("variant", ["honest", "partial_fault", "failure"])
 def test_certify_outputs_fault_variants(ctx, variant):
     from paper_2205_15757_b200 import RequestBatch
@@ -218,7 +249,7 @@ def test_ingest_ahead_and_out_of_order(ctx):
     half = RequestBatch.from_encoded(reqs[:6])
     want = grp.certify(b)
     want_half = grp.certify(half)
-    ring = 16  # cg_group ingest ring depth
+    ring = 24  # cg_group ingest ring depth (CG_INGEST_RING)
     t = [grp.ingest(b if i % 2 == 0 else half) for i in range(ring)]
     with pytest.raises(InvalidArgument):
         grp.ingest(b)

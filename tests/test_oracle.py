@@ -96,19 +96,26 @@ def test_select_quorum_errors(oracle):
         oracle.select_quorum(np.ones((3, 1)), [0, 1, 2], 3, 3, 0, 1.0)
 
 
-def test_c1_golden_linear_and_leaves(oracle):
+@pytest.mark.parametrize("fixture", ["c1_batch.npz", "c1_full.npz"])
+def test_c1_golden_linear_and_leaves(oracle, fixture):
+    """c1_full.npz is C1 at SURVEY §8(d)'s shape (3072 -> 10 softmax, batch
+    64, seed 7); c1_batch.npz the small variant (512 -> 10, batch 12)."""
     from oracle.oracle import parse_linear_model_file, parse_request
-    g = golden("c1_batch.npz")
+    g = golden(fixture)
     N, B, v = int(g["N"]), int(g["B"]), int(g["v"])
     reqs = split_reqs(g)
     gid = g["gid"].tobytes()
+    inputs = [parse_request(r)["input"] for r in reqs]
     for p in range(N):
         u, v_, sm, W, b = parse_linear_model_file(g["files"][p].tobytes())
-        assert not sm and v_ == v
+        assert sm == (fixture == "c1_full.npz") and v_ == v and u == int(g["u"])
         assert hashlib.sha256(g["files"][p].tobytes()).digest() == g["digests"][p].tobytes()
         for k in range(B):
-            y = oracle.linear_run(W, b, g["inputs"][k], False)
-            assert np.array_equal(y, g["outputs"][p, k])  # bit-exact fp64
+            y = oracle.linear_run(W, b, inputs[k], sm)
+            if sm:  # exp: the restatement uses the same libm as the reference build
+                assert np.array_equal(y, g["outputs"][p, k]), (p, k)
+            else:
+                assert np.array_equal(y, g["outputs"][p, k])  # bit-exact fp64
     for k in range(B):
         f = parse_request(reqs[k])
         enc = oracle.request_encode(f["request_id"], f["group_id"], f["input"],
@@ -121,10 +128,11 @@ def test_c1_golden_linear_and_leaves(oracle):
 
 
 @pytest.mark.parametrize("variant", ["honest", "partial_fault", "failure"])
-def test_c1_golden_certify(oracle, variant):
+@pytest.mark.parametrize("fixture", ["c1_batch.npz", "c1_full.npz"])
+def test_c1_golden_certify(oracle, variant, fixture):
     """Oracle restatement of the whole batch certification == reference."""
     from oracle.oracle import parse_request
-    g = golden("c1_batch.npz")
+    g = golden(fixture)
     N, B, eps = int(g["N"]), int(g["B"]), float(g["eps"])
     gid = g["gid"].tobytes()
     reqs = split_reqs(g)
@@ -182,6 +190,42 @@ def test_live_reference_cross_check(oracle):
     for n in (0, 1, 63, 64, 65, 1000):
         m = rng.integers(0, 256, n, dtype=np.uint8).tobytes()
         assert oracle.sha256(m) == R.sha256(m)
+
+
+@pytest.mark.parametrize("n,f,v,metric", [(4, 1, 6, 0), (8, 2, 6, 0), (5, 1, 4, 2),
+                                          (8, 3, 3, 2), (3, 1, 1, 1), (3, 1, 4, 1),
+                                          (2, 1, 4, 1)])
+def test_adversarial_oracle_vs_reference(oracle, n, f, v, metric):
+    """The C restatement against the compiled reference (select_quorum +
+    ensemble_label) on the NaN/Inf/tie generator the GPU sweeps use, so the
+    GPU-vs-oracle adversarial sweep is pinned to the reference itself;
+    includes max_minus_min on vectors (throws only when delta runs, m >= 2,
+    distance.cpp:87-91) and on single present results."""
+    from adversarial import adversarial
+    from oracle.oracle import Reference
+    if not Reference.available():
+        pytest.skip("oracle/_ref not built here")
+    R = Reference()
+    rng = np.random.default_rng(n * 1000 + v * 10 + metric)
+    outs = adversarial(rng, 400, n, v)
+    eps = rng.choice([0.0, 0.1, 0.25, 1.0], 400)
+    for k in range(400):
+        for idx in (list(range(n)), [0], list(range(1, n))):
+            want = got = None
+            try:
+                want = R.select_quorum(outs[k][idx], idx, n, f, metric, eps[k])
+            except ValueError:
+                want = "throws"
+            try:
+                got = oracle.select_quorum(outs[k][idx], idx, n, f, metric, eps[k])
+            except ValueError:
+                got = "throws"
+            assert got == want or (isinstance(got, tuple) and got[:1] + got[2:] == want[:1] + want[2:]
+                                   and np.array_equal(np.float64(got[1]).view(np.uint64),
+                                                      np.float64(want[1]).view(np.uint64))), (k, idx)
+            if isinstance(want, tuple) and want[2]:
+                assert oracle.ensemble_label(outs[k][idx], want[0], f) == \
+                    R.ensemble_label(outs[k][idx], want[0], f)
 
 
 def test_label_digest_layout(oracle):
