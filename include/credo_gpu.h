@@ -259,6 +259,33 @@ int cg_request_digests(cg_ctx* ctx, const cg_request_batch* batch, const char* g
                        uint64_t group_id_len, uint8_t* signing_digests,
                        uint8_t* canonical_ids, int8_t* status);
 
+/* ---- host digests (no device involved) -----------------------------------
+ * SHA-256 on the host, x86 SHA extensions when present (the model-file check
+ * of load_group, src/engine.cpp:79, runs here: one ~100 MB chain). */
+int cg_host_sha256(const uint8_t* data, uint64_t len, uint8_t out[32]);
+int cg_host_sha_accelerated(void);
+
+/* One PRE-PREPARE's op list of inference requests for hash_ops
+ * (src/messages.cpp:197-202): OpEntry{request_inf, requests[k], version
+ * versions[k] (NULL: `version` for all), status statuses[k] (NULL: ok),
+ * reason = reasons bytes of reason_lens[k] (NULL: "")}. */
+typedef struct {
+  const cg_request_batch* requests; /* host inputs */
+  const char* group_id;
+  uint64_t group_id_len;
+  uint64_t version;
+  const uint64_t* versions;
+  const uint8_t* statuses;
+  const char* reasons;
+  const uint64_t* reason_lens;
+} cg_ops_batch;
+/* hash_ops of nslots op lists on up to `threads` host threads (one op list
+ * per thread at a time; each is one sequential SHA-256 chain over every
+ * request encoding, 1.2 MB per ImageNet request, streamed from the f64
+ * inputs without re-serialising). out: nslots x 32. */
+int cg_hash_ops_batches(const cg_ops_batch* batches, uint32_t nslots, int threads,
+                        uint8_t* out);
+
 /* Certificate assembly for the last certified batch (ProxyCore::
  * assemble_response, proxy.cpp:80-186): auth paths in provider `tree`'s
  * result tree (tree < N; leaf k = request k) or, tree == N, in the

@@ -14,6 +14,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import struct
 import subprocess
 
 import numpy as np
@@ -96,6 +97,18 @@ class Oracle:
         out = C.create_string_buffer(n)
         self.L.oc_request_encode(*args, out)
         return out.raw
+
+    def hash_ops(self, encs: list[bytes], versions, statuses, reasons=None) -> bytes:
+        """hash_ops (messages.cpp:197-202): H(0x4F || u32be n || per op
+        OpEntry::encode (messages.cpp:161-169) = u8 kind 0 || bool 1 ||
+        request encoding || bool 0 || u64be version || u8 status || str
+        reason)."""
+        parts = [b"\x4f", struct.pack(">I", len(encs))]
+        for i, e in enumerate(encs):
+            r = (reasons[i] if reasons is not None else "").encode()
+            parts += [b"\x00\x01", e, b"\x00", struct.pack(">QB", int(versions[i]), int(statuses[i])),
+                      struct.pack(">I", len(r)), r]
+        return self.sha256(b"".join(parts))
 
     def result_encode(self, req_id, node, gid: bytes, version, out_vec,
                       model_digest) -> bytes:
@@ -341,6 +354,19 @@ class Reference:
         out = C.create_string_buffer(32)
         assert self.L.ref_path_root(leaf, u64(len(leaf)), sib, sides, C.c_uint32(len(path)),
                                     out) == 0
+        return out.raw
+
+    def hash_ops(self, encs: list[bytes], versions, statuses, reasons=None) -> bytes:
+        """messages.cpp:197-202 over request ops."""
+        lens = np.array([len(e) for e in encs], np.uint64)
+        ver = np.ascontiguousarray(versions, np.uint64)
+        st = np.ascontiguousarray(statuses, np.uint8)
+        rs = None
+        if reasons is not None:
+            rs = (C.c_char_p * len(reasons))(*[r.encode() for r in reasons])
+        out = C.create_string_buffer(32)
+        assert self.L.ref_hash_ops(b"".join(encs), _p(lens), u64(len(encs)), _p(ver), _p(st),
+                                   rs, out) == 0
         return out.raw
 
     def signing_digest(self, enc: bytes) -> bytes:

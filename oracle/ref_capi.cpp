@@ -572,4 +572,31 @@ int ref_certify_batch(void* h, uint64_t N, uint64_t f, uint32_t metric,
   }
 }
 
+// hash_ops (src/messages.cpp:197-202) over n request ops (encodings back to
+// back), OpEntry{request_inf, request, no group op, versions[i], statuses[i],
+// reasons[i]} (reasons NULL: "").
+int ref_hash_ops(const uint8_t* encs, const uint64_t* lens, uint64_t n, const uint64_t* versions,
+                 const uint8_t* statuses, const char* const* reasons, uint8_t* out) {
+  try {
+    std::vector<OpEntry> ops;
+    uint64_t off = 0;
+    for (uint64_t i = 0; i < n; i++) {
+      Decoder d(ByteView(encs + off, lens[i]));
+      OpEntry op;
+      op.kind = OpKind::request_inf;
+      op.request = InferenceRequest::decode(d);
+      op.version = versions[i];
+      op.status = static_cast<OpStatus>(statuses[i]);
+      op.reason = reasons ? std::string(reasons[i]) : std::string();
+      ops.push_back(std::move(op));
+      off += lens[i];
+    }
+    Hash32 h = hash_ops(ops);
+    std::memcpy(out, h.data.data(), 32);
+    return 0;
+  } catch (const std::exception&) {
+    return -1;
+  }
+}
+
 }  // extern "C"

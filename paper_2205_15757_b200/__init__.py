@@ -4,9 +4,9 @@ C-ABI (include/credo_gpu.h). See DESIGN.md."""
 from .credo import (AgreementOutcome, CHEBYSHEV, Context, CredoError,
                     CudaExecutor, DigestMismatch, EUCLIDEAN, InvalidArgument,
                     MAX_MINUS_MIN, Model, ModelGroup, PerturbingExecutor,
-                    RequestBatch, lib)
+                    RequestBatch, hash_ops_batches, host_sha256, lib)
 
 __all__ = ["AgreementOutcome", "CHEBYSHEV", "Context", "CredoError",
            "CudaExecutor", "DigestMismatch", "EUCLIDEAN", "InvalidArgument",
            "MAX_MINUS_MIN", "Model", "ModelGroup", "PerturbingExecutor",
-           "RequestBatch", "lib"]
+           "RequestBatch", "hash_ops_batches", "host_sha256", "lib"]

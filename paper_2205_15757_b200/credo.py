@@ -326,6 +326,49 @@ class Context:
             diameter=float(r["diameter"][0]), satisfied=bool(r["satisfied"][0]))
 
 
+class _COpsBatch(C.Structure):
+    _fields_ = [("requests", vp), ("group_id", C.c_char_p), ("group_id_len", u64),
+                ("version", u64), ("versions", vp), ("statuses", vp), ("reasons", C.c_char_p),
+                ("reason_lens", vp)]
+
+
+def host_sha256(data: bytes) -> bytes:
+    """SHA-256 on the host (SHA-NI when present): the model-file check."""
+    out = C.create_string_buffer(32)
+    rc = lib().cg_host_sha256(data, u64(len(data)), out)
+    if rc != CG_OK:
+        raise CredoError(rc, "cg_host_sha256 failed")
+    return out.raw
+
+
+def hash_ops_batches(batches: Sequence["RequestBatch"], group_id: bytes, versions,
+                     statuses=None, reasons=None, threads: int = 1) -> list[bytes]:
+    """hash_ops (messages.cpp:197-202) of one PRE-PREPARE op list per batch
+    (every op an inference request), host SHA-NI, one op list per thread.
+    versions[i]: an int or a per-request sequence; statuses / reasons the
+    same (None: ok / "")."""
+    keep, arr = [], (_COpsBatch * max(1, len(batches)))()
+    for i, b in enumerate(batches):
+        cb, k, B = ModelGroup._cbatch(b)
+        keep += [cb, k]
+        v = versions[i]
+        vs = None if np.isscalar(v) else np.ascontiguousarray(v, np.uint64)
+        st = None if statuses is None else np.ascontiguousarray(statuses[i], np.uint8)
+        rs = rl = None
+        if reasons is not None:
+            enc = [r.encode() for r in reasons[i]]
+            rs = b"".join(enc) or b"\0"
+            rl = np.array([len(r) for r in enc], np.uint64)
+        keep += [vs, st, rs, rl]
+        arr[i] = _COpsBatch(C.cast(C.pointer(cb), vp), group_id, len(group_id),
+                            int(v) if vs is None else 0, _p(vs), _p(st), rs, _p(rl))
+    out = C.create_string_buffer(32 * max(1, len(batches)))
+    rc = lib().cg_hash_ops_batches(arr, u32(len(batches)), C.c_int(threads), out)
+    if rc != CG_OK:
+        raise CredoError(rc, "cg_hash_ops_batches: bad arguments")
+    return [out.raw[32 * i:32 * i + 32] for i in range(len(batches))]
+
+
 @dataclass
 class AgreementOutcome:
     """distance::AgreementOutcome (distance.hpp:55-59)."""

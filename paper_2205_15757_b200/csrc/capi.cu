@@ -30,6 +30,7 @@
 #include "common.cuh"
 #include "digest.cuh"
 #include "gemm_sm100.cuh"
+#include "host_sha256.h"
 
 namespace cg {
 
@@ -291,24 +292,14 @@ void device_sha256_many(cg_ctx* ctx, const uint8_t* buf, const uint64_t* off,
   device_sha256_finish(ctx, count, out_host);
 }
 
-void check_model_digest(cg_ctx* ctx, const uint8_t* file, uint64_t len,
-                        const uint8_t digest[32]) {
+// load_group's model check (engine.cpp:79-81): SHA-256(file) must equal the
+// descriptor's weights digest, checked BEFORE the file is parsed (a tampered
+// and malformed file is a digest error, as in the reference). One ~100 MB
+// sequential chain for an ImageNet CNN: host SHA-NI (~1.2 GB/s), where the
+// reference computes it too.
+void check_model_digest(const uint8_t* file, uint64_t len, const uint8_t digest[32]) {
   uint8_t got[32];
-  uint64_t off = 0;
-  device_sha256_many(ctx, file, &off, &len, 1, -1, got);
-  if (std::memcmp(got, digest, 32) != 0)
-    throw DigestError("model file does not match its weights digest");
-}
-
-// The model-file digest chain (one ~100 MB SHA-256 chain for an ImageNet
-// CNN) runs on the GPU while the host parses and folds the weights.
-void start_model_digest(cg_ctx* ctx, const uint8_t* file, uint64_t len) {
-  uint64_t off = 0;
-  device_sha256_start(ctx, file, &off, &len, 1, -1);
-}
-void finish_model_digest(cg_ctx* ctx, const uint8_t digest[32]) {
-  uint8_t got[32];
-  device_sha256_finish(ctx, 1, got);
+  host_sha256(file, len, got);
   if (std::memcmp(got, digest, 32) != 0)
     throw DigestError("model file does not match its weights digest");
 }
@@ -637,6 +628,7 @@ int cg_model_load_linear(cg_ctx* ctx, const uint8_t* file, uint64_t len,
       for (int i = 0; i < 4; i++) v = (v << 8) | file[pos++];
       return v;
     };
+    check_model_digest(file, len, digest);
     uint64_t pos = 0;
     uint64_t in = rd_u64(pos), outd = rd_u64(pos);
     if (pos + 1 > len) throw CodecError("unexpected end of input");
@@ -657,7 +649,6 @@ int cg_model_load_linear(cg_ctx* ctx, const uint8_t* file, uint64_t len,
     if (pos != len) throw CodecError("trailing bytes after value");
     if (in < 1 || outd < 1 || W.size() != in * outd || b.size() != outd)
       throw CodecError("model file shape mismatch");
-    check_model_digest(ctx, file, len, digest);
     auto m = std::make_unique<cg_model>();
     m->ctx = ctx;
     m->kind = 0;
@@ -679,14 +670,12 @@ int cg_model_load_cnn(cg_ctx* ctx, const uint8_t* file, uint64_t len,
   return guarded(ctx, [&] {
     *out = nullptr;
     std::unique_ptr<CnnModel> cnn;
-    start_model_digest(ctx, file, len);
+    check_model_digest(file, len, digest);
     try {
       cnn = CnnModel::from_file(file, len);
     } catch (const std::invalid_argument& e) {
-      CG_CUDA(cudaStreamSynchronize(ctx->stream));
       throw CodecError(e.what());
     }
-    finish_model_digest(ctx, digest);
     cnn->upload(ctx->stream);
     CG_CUDA(cudaStreamSynchronize(ctx->stream));
     auto m = std::make_unique<cg_model>();

@@ -1391,10 +1391,14 @@ std::unique_ptr<CnnModel> CnnModel::from_file(const uint8_t* file, uint64_t len)
     if (c != count) throw std::invalid_argument("cnn file: count/shape mismatch");
     r.need(4ull * c);
     t.v.resize(c);
+    const uint8_t* src = file + r.pos;  // f32 big-endian, bounds checked above
     for (uint32_t k = 0; k < c; k++) {
-      uint32_t b = r.u32();
+      uint32_t b;
+      std::memcpy(&b, src + 4ull * k, 4);
+      b = __builtin_bswap32(b);
       std::memcpy(&t.v[k], &b, 4);
     }
+    r.pos += 4ull * c;
     T[name] = std::move(t);
   }
   if (r.pos != len) throw std::invalid_argument("cnn file: trailing bytes after value");
