@@ -176,6 +176,64 @@ def make_dist_group(ctx, B, rank, world, seed=0, eps=0.1):
     return grp, [m], files, digs, sds
 
 
+def pipeline(grp, ctx, batches, K, D, lag, stream=None):
+    """K batches through the pipelined hot path, cold start and full drain:
+    ingest D batches ahead of certification (their request-midstate chains
+    overlap the forwards), certify each, read its decisions back `lag` steps
+    behind, and join every stream at the end. With `stream`, returns the
+    device time of the whole region (CUDA events on the context stream)."""
+    import torch
+    from collections import deque
+    nb = len(batches)
+    if stream is not None:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+    h0 = time.perf_counter()
+    pend = deque(grp.ingest(batches[j % nb]) for j in range(min(D, K)))
+    done, sats, labs = deque(), [], []
+
+    def fetch():
+        r = grp.fetch_ticket(done.popleft())
+        sats.append(r["satisfied"])
+        labs.append(r["label"])
+    for i in range(K):
+        t = pend.popleft()
+        grp.certify_ticket(t, sync=False)
+        done.append(t)
+        if i + D < K:
+            pend.append(grp.ingest(batches[(i + D) % nb]))
+        while len(done) > lag:
+            fetch()
+    while done:
+        fetch()
+    ctx.join()  # every ingest, tail and single-leaf chain of the region
+    host_ms = 1e3 * (time.perf_counter() - h0) / K
+    ms = None
+    if stream is not None:
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+    torch.cuda.synchronize()
+    return ms, host_ms, sats, labs
+
+
+def host_hash_ops(batches, threads, slots):
+    """hash_ops (messages.cpp:197-202) of `slots` PRE-PREPARE op lists of B
+    ImageNet requests each on the host (SHA-NI, one op list per thread)."""
+    from paper_2205_15757_b200 import hash_ops_batches
+    from paper_2205_15757_b200.credo import lib
+    bs = [batches[i % len(batches)] for i in range(slots)]
+    hash_ops_batches(bs[:1], b"group-0", [1], threads=1)  # warm
+    t = time.perf_counter()
+    hash_ops_batches(bs, b"group-0", [1] * slots, threads=threads)
+    dt = time.perf_counter() - t
+    B = len(bs[0].nonces)
+    return {"value": round(slots * B / dt, 1), "unit": "req/s", "threads": threads,
+            "sha_ni": bool(lib().cg_host_sha_accelerated()),
+            "bytes_per_request": int(bs[0].inputs[0].size * 8 + 200),
+            "sample": f"{slots} op lists x {B} requests, {dt:.2f} s"}
+
+
 def bench_gpu(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -205,18 +263,16 @@ def bench_gpu(args, rank, world, local_rank):
                                  __import__("ctypes").POINTER(__import__("ctypes").c_uint64)]
     flops_img = sum(L.cg_model_flops_per_input(m.h) for m in models)  # this rank's replicas
 
-    # Two rotating batches of 154 MB f64 inputs each (> 126 MB L2): pinned
-    # host copies for e2e, device copies for the device-resident value.
+    # Two rotating batches of 154 MB f64 inputs each (> 126 MB L2): plain
+    # (pageable) host arrays -- one vector<double> per request, as the
+    # reference holds them -- for e2e, device copies for the device-resident
+    # value.
     nb = 2
     batches = [signed_requests(B, U, seed=seed_base + i) for i in range(nb)]
-    host_in = [torch.from_numpy(b.inputs).pin_memory() for b in batches]
-    dev_in = [h.to(f"cuda:{local_rank}") for h in host_in]
+    dev_in = [torch.from_numpy(b.inputs).to(f"cuda:{local_rank}") for b in batches]
     from copy import copy
-    dev_batches, host_batches = [], []
-    for b, h, d in zip(batches, host_in, dev_in):
-        hb = copy(b)
-        hb.inputs = h.numpy()
-        host_batches.append(hb)
+    dev_batches = []
+    for b, d in zip(batches, dev_in):
         db = copy(b)
         db.inputs, db.B, db.u = d.data_ptr(), B, U
         dev_batches.append(db)
@@ -234,7 +290,7 @@ def bench_gpu(args, rank, world, local_rank):
 
     # ---- warmup (also validates: every request must be certified) ----
     for i in range(args.warmup):
-        r = grp.certify(host_batches[i % nb])
+        r = grp.certify(batches[i % nb])
     sat = float(np.mean(r["satisfied"]))
     torch.cuda.synchronize()
     if args.profile:  # ncu mode: a few plain steps, nothing else
@@ -242,106 +298,105 @@ def bench_gpu(args, rank, world, local_rank):
             grp.certify(dev_batches[i % nb], sync=False)
         torch.cuda.synchronize()
         return {"profile": True, "satisfied": sat}
+    D, LAG = args.depth, args.fetch_lag
     if args.trace:  # kineto/CUPTI timeline of the pipelined loop (all streams)
-        from collections import deque
-
         from torch.profiler import ProfilerActivity, profile
-        pend = deque(grp.ingest(dev_batches[j % nb]) for j in range(args.depth))
-        torch.cuda.synchronize()
         with profile(activities=[ProfilerActivity.CUDA]) as prof:
-            for i in range(args.steps):
-                grp.certify_ticket(pend.popleft(), sync=False)
-                pend.append(grp.ingest(dev_batches[(i + args.depth) % nb]))
-            torch.cuda.synchronize()
-        while pend:
-            grp.certify_ticket(pend.popleft(), sync=False)
-        torch.cuda.synchronize()
+            pipeline(grp, ctx, dev_batches, args.steps, D, LAG)
         if rank == 0:
             prof.export_chrome_trace(args.trace)
         return {"trace": args.trace}
 
     # ---- device-resident throughput (value) ----
-    # Pipelined like the reference's own engine: a batch is ingested (framing
-    # + request-midstate SHA chains, InferenceEngine::submit) D steps before
-    # it is certified (execute_batch + R/A trees), so the latency-bound chains
-    # of D batches overlap the replica forwards. Each timed step certifies one
-    # batch and ingests one future batch.
-    from collections import deque
-    D = args.depth
-    pend = deque(grp.ingest(dev_batches[j % nb]) for j in range(D))
+    # Cold start, full drain: the timed region issues every ingest (framing +
+    # request-midstate SHA chains, InferenceEngine::submit's device part, D
+    # batches ahead of certification) and every certify of its K batches, and
+    # ends when all of their work -- forwards, chains, agreement, trees, the
+    # lazily chained single-attestation leaves -- has finished
+    # (cg_ctx_join). Decisions are read back LAG steps behind, inside it.
     barrier()
     torch.cuda.synchronize()
     l0 = ctx.launch_count()  # kernels launched inside the timed region only
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local_rank) as clk:
-        e0.record(stream)
-        h0 = time.perf_counter()
-        # the host reads each batch's decisions back one step behind (as the
-        # e2e loop does), which also keeps it from running far ahead of the GPU
-        sats, labs, prev = [], [], None
-        for i in range(args.steps):
-            t = pend.popleft()
-            grp.certify_ticket(t, sync=False)
-            if prev is not None:
-                r = grp.fetch_ticket(prev)
-                sats.append(r["satisfied"])
-                labs.append(r["label"])
-            pend.append(grp.ingest(dev_batches[(i + D) % nb]))
-            prev = t
-        r = grp.fetch_ticket(prev)
-        sats.append(r["satisfied"])
-        labs.append(r["label"])
-        host_ms = 1e3 * (time.perf_counter() - h0) / args.steps
-        ctx.join()  # the last batches' certification tails are inside the region
-        e1.record(stream)
-        torch.cuda.synchronize()
+        ms, host_ms, sats, labs = pipeline(grp, ctx, dev_batches, args.steps, D, LAG, stream)
     launches = round((ctx.launch_count() - l0) / args.steps)
-    ms = max_over_ranks(e0.elapsed_time(e1))
+    ms = max_over_ranks(ms)
     sat_dev = float(np.mean(np.concatenate(sats)))
     label_frac = float(np.mean(np.concatenate(labs) >= 0))
-    while pend:
-        grp.certify_ticket(pend.popleft(), sync=False)
-    torch.cuda.synchronize()
     value = jobs * args.steps * B * sat_dev / (ms / 1e3)
 
-    # ---- end to end through the public API from pinned host memory ----
-    pend = deque(grp.ingest(host_batches[j % nb]) for j in range(D))
+    # ---- fault path: corrupt_result on provider 2 for 30 % of the requests
+    # (10 % of the (request, replica) pairs): single-attestation leaves --
+    # a 0x53 request midstate per request where provider 2 is in the quorum
+    fault = None
+    if not replica and args.workload == "c2" and not args.no_fault:
+        grp.set_fault(2, 1.0, 0.3)
+        barrier()
+        torch.cuda.synchronize()
+        fms, _, fsats, _ = pipeline(grp, ctx, dev_batches, args.steps, D, LAG, stream)
+        grp.set_fault(2, 0.0, 0.0)
+        fms = max_over_ranks(fms)
+        fsat = float(np.mean(np.concatenate(fsats)))
+        hit = float(np.mean([np.mean(b.request_ids[:, 0] < round(256 * 0.3)) for b in batches]))
+        fault = {"value": round(jobs * args.steps * B * fsat / (fms / 1e3), 1), "unit": UNIT,
+                 "ms_per_step": round(fms / args.steps, 3),
+                 "faulty_pair_fraction": round(hit / 3, 4),
+                 "fault": "OffsetExecutor(+1.0) on provider 2 for requests with id[0] < 77 "
+                          "(harness.cpp:167-186 corrupt_result)",
+                 "satisfied_fraction": fsat,
+                 "ratio_to_honest": round((fsat / max(sat_dev, 1e-9)) * (ms / fms), 4)}
+
+    # ---- end to end through the public API: the batch former ----
+    # Every step submits B requests (InferenceEngine::submit: structural
+    # checks, seen-dedup, packing each request's pageable f64 input into
+    # pinned staging on pack threads), the released batch is ingested
+    # (framing, H2D of 154 MB, chains), certified, and its decisions + roots
+    # are read back LAG steps behind -- all inside the region.
+    from paper_2205_15757_b200 import InferenceEngine
+    eng = InferenceEngine(ctx, B, 10**12, pack_threads=args.pack_threads)
+    eng.load_group(grp)
+    prepared = [eng.prepare(b, b"group-0") for b in batches]
     barrier()
     torch.cuda.synchronize()
     e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e2.record(stream)
-    # each step's result (decisions + roots) is read back to the host inside
-    # the region, one step behind so its certification tail overlaps the
-    # next batch's forwards
+    h2 = time.perf_counter()
     certified = 0
-    prev = None
+    from collections import deque
+    ready_q, inflight = deque(), deque()
+
+    def certify_oldest():
+        grp_, _, t, Bt = ready_q.popleft()
+        grp_.certify_ticket(t, sync=False, B=Bt)
+        inflight.append(t)
+
+    def fetch_oldest():
+        return int(np.sum(grp.fetch_ticket(inflight.popleft())["satisfied"]))
     for i in range(args.steps):
-        t = pend.popleft()
-        grp.certify_ticket(t, sync=False)
-        if prev is not None:
-            certified += int(np.sum(grp.fetch_ticket(prev)["satisfied"]))
-        pend.append(grp.ingest(host_batches[(i + D) % nb]))
-        prev = t
-    certified += int(np.sum(grp.fetch_ticket(prev)["satisfied"]))
+        eng.submit_prepared(prepared[i % nb], now_us=i)  # one full batch of B per step
+        ready_q.extend(eng.ready())
+        while len(ready_q) > D:
+            certify_oldest()
+        while len(inflight) > LAG:
+            certified += fetch_oldest()
+    while ready_q:
+        certify_oldest()
+    while inflight:
+        certified += fetch_oldest()
+    ctx.join()
     e3.record(stream)
     torch.cuda.synchronize()
+    host_e2e = time.perf_counter() - h2
     ms_e2e = max_over_ranks(e2.elapsed_time(e3))
     e2e = jobs * certified / (ms_e2e / 1e3)
-    while pend:
-        grp.certify_ticket(pend.popleft(), sync=False)
-    torch.cuda.synchronize()
+    eng.free()
     h2d = B * U * 8
     d2h = B * (4 + 8 + 1 + 8) + grp.N * 32 + 32 + 8
 
     # ---- attribution pass: per-kernel-class device time (same pipeline) ----
     import ctypes
-    pend = deque(grp.ingest(dev_batches[j % nb]) for j in range(D))
-    torch.cuda.synchronize()
     L.cg_timing_enable(1)
-    for i in range(args.steps):
-        grp.certify_ticket(pend.popleft(), sync=False)
-        pend.append(grp.ingest(dev_batches[(i + D) % nb]))
-    torch.cuda.synchronize()
+    pipeline(grp, ctx, dev_batches, args.steps, D, LAG, stream)
     tg, ng = ctypes.c_double(), ctypes.c_uint64()
     L.cg_timing_read(0, ctypes.byref(tg), ctypes.byref(ng))
     tc, nc = ctypes.c_double(), ctypes.c_uint64()
@@ -370,9 +425,6 @@ def bench_gpu(args, rank, world, local_rank):
         L.cg_timing_read(cls, ctypes.byref(t), ctypes.byref(n))
         breakdown[name] = round(t.value / args.steps, 3)
     L.cg_timing_enable(0)
-    while pend:
-        grp.certify_ticket(pend.popleft(), sync=False)
-    torch.cuda.synchronize()
     gemm_ms_step = tg.value / args.steps
     chain_ms_step = tc.value / args.steps
     pk, pk_src = peaks()
@@ -403,7 +455,7 @@ def bench_gpu(args, rank, world, local_rank):
 
     out = {"metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup,
-           "ms_per_step": round(ms / args.steps, 3), "host_enqueue_ms_per_step": round(host_ms, 3),
+           "ms_per_step": round(ms / args.steps, 3), "host_ms_per_step": round(host_ms, 3),
            "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
            "data": "synthetic (random-init jittered ResNet-50 replicas, U(-1,1) f64 "
@@ -416,13 +468,22 @@ def bench_gpu(args, rank, world, local_rank):
                       "l2": "inputs larger than L2: 2 rotating 154 MB f64 batches",
                       "arith": "bf16 forward / f64 agreement / u32 SHA-256",
                       "satisfied_fraction": sat_dev,
-                      "pipeline": f"ingest {D} batches ahead (request-midstate SHA chains "
-                                  "overlap the forwards)"},
+                      "pipeline": f"cold start + full drain inside the region: ingest {D} "
+                                  f"batches ahead (request-midstate SHA chains overlap the "
+                                  f"forwards), decisions read back {LAG} steps behind"},
            "e2e": {"value": round(e2e, 1), "unit": UNIT, "h2d_bytes_per_step": h2d,
-                   "d2h_bytes_per_step": d2h, "ms_per_step": round(ms_e2e / args.steps, 3)},
+                   "d2h_bytes_per_step": d2h, "ms_per_step": round(ms_e2e / args.steps, 3),
+                   "host_s": round(host_e2e, 3),
+                   "path": "InferenceEngine.submit of B requests per step (structural checks, "
+                           "dedup, pack of pageable per-request f64 inputs into pinned staging "
+                           f"on {args.pack_threads} threads) -> ingest (154 MB H2D) -> certify "
+                           "-> decisions + roots read back, all in the region"},
+           "fault_path": fault,
            "gpu_launches": int(launches),
            "roofline": roofline,
            "clocks": clk.summary()}
+    if rank == 0 and not replica and args.workload == "c2":
+        out["host_hash_ops"] = host_hash_ops(batches, os.cpu_count() or 1, 16)
     if args.workload == "c3":
         from paper_2205_15757_b200.workload import HETERO_GROUP
         out["metric"] = METRIC.replace("(ResNet-50 group)", "(heterogeneous group)")
@@ -457,19 +518,52 @@ def cpu_path(models, encs, inputs, digs, threads, R, eps=0.1):
     """The reference's CPU path for a sample: torchvision fp32 forward per
     replica (restatement: the reference has no CNN), then the compiled
     reference's select_quorum, ensemble_label, result leaves, R trees,
-    manifest and A tree (oracle/_ref ref_certify_batch)."""
+    manifest and A tree (oracle/_ref ref_certify_batch). Returns (result,
+    forward seconds, agreement + digest seconds)."""
     import torch
 
     from oracle import cnn_oracle
     torch.set_num_threads(threads)
+    t0 = time.perf_counter()
     outs = []
     for m in models:
         outs.append(cnn_oracle.softmax_f64(cnn_oracle.logits(m, inputs)))
     outs = np.stack(outs)
+    t1 = time.perf_counter()
     h = R.batch_new(encs, 1)
     r = R.certify_batch(h, len(models), 1, 0, eps, outs, 1, digs, threads=threads)
     R.batch_free(h)
-    return r
+    return r, t1 - t0, time.perf_counter() - t1
+
+
+def cpu_digest_seconds(backend: str, threads: int, S: int, N: int = 3) -> float:
+    """Agreement + digest part of the reference's CPU path (select_quorum,
+    labels, result leaves, R trees, manifest, A tree) for S ImageNet-shaped
+    requests with the given SHA-256 backend. Runs in its own process (the two
+    reference builds export the same libsodium symbols)."""
+    from oracle.oracle import Reference
+    from paper_2205_15757_b200.workload import encode_request, signed_requests
+    batch = signed_requests(S, U, seed=0)
+    encs = [encode_request(batch, k) for k in range(S)]
+    rng = np.random.default_rng(1)
+    base = rng.dirichlet(np.ones(1000), S)
+    outs = np.stack([base + rng.uniform(-1e-6, 1e-6, base.shape) for _ in range(N)])
+    digs = [bytes([p]) * 32 for p in range(N)]
+    R = Reference(backend)
+    h = R.batch_new(encs, 1)
+    t = time.perf_counter()
+    R.certify_batch(h, N, 1, 0, 0.1, outs, 1, digs, threads=threads)
+    dt = time.perf_counter() - t
+    R.batch_free(h)
+    return dt
+
+
+def _digest_seconds_subprocess(backend, threads, S):
+    code = (f"import sys; sys.path.insert(0, {ROOT!r}); import bench; "
+            f"print(bench.cpu_digest_seconds({backend!r}, {threads}, {S}))")
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
+                         timeout=600)
+    return float(out.stdout.strip().splitlines()[-1])
 
 
 def cpu_baseline(archs, digs, sds, batch, args, eps=0.1):
@@ -488,14 +582,38 @@ def cpu_baseline(archs, digs, sds, batch, args, eps=0.1):
     R = Reference()
     models = cpu_models(archs, sds)
     cpu_path(models, encs[:2], batch.inputs[:2], digs, threads, R, eps)  # warm
-    t = time.perf_counter()
-    cpu_path(models, encs, np.take(batch.inputs, idx, axis=0), digs, threads, R, eps)
-    dt = time.perf_counter() - t
-    return {"value": round(S / dt, 3), "unit": UNIT, "cores": threads, "kind": kind,
-            "sample": f"{S} requests x {len(archs)} replicas ({'+'.join(sorted(set(archs)))}): "
-                      f"torchvision fp32 forward (restated; "
-                      f"the reference has no CNN) + compiled reference select_quorum/"
-                      f"ensemble_label/result leaves/R+A trees, {dt:.1f} s"}
+    _, t_fwd, t_dig = cpu_path(models, encs, np.take(batch.inputs, idx, axis=0), digs,
+                               threads, R, eps)
+    dt = t_fwd + t_dig
+    out = {"value": round(S / dt, 3), "unit": UNIT, "cores": threads, "kind": kind,
+           "sample": f"{S} requests x {len(archs)} replicas ({'+'.join(sorted(set(archs)))}): "
+                     f"torchvision fp32 forward (restated; "
+                     f"the reference has no CNN) + compiled reference select_quorum/"
+                     f"ensemble_label/result leaves/R+A trees, {dt:.1f} s "
+                     f"(forward {t_fwd:.1f} s, agreement + digests {t_dig:.2f} s), "
+                     "SHA-256 via OpenSSL (SHA-NI)"}
+    # the same with the SHA-256 the reference ships (libsodium), and on one
+    # core (a smaller sample, scaled)
+    try:
+        Sd = min(S, 64)
+        t_sod = _digest_seconds_subprocess("libsodium", threads, Sd) * S / Sd
+        S1 = 4
+        _, f1, _ = cpu_path(models, encs[:S1], np.take(batch.inputs, idx[:S1], axis=0), digs, 1,
+                            R, eps)
+        d1 = _digest_seconds_subprocess("openssl", 1, 16) / 16
+        d1s = _digest_seconds_subprocess("libsodium", 1, 8) / 8
+        out["backends"] = {
+            "openssl_all_cores": round(S / dt, 3),
+            "libsodium_all_cores": round(S / (t_fwd + t_sod), 3),
+            "openssl_1_core": round(1.0 / (f1 / S1 + d1), 3),
+            "libsodium_1_core": round(1.0 / (f1 / S1 + d1s), 3),
+            "digest_only_req_per_s": {"openssl_all_cores": round(S / t_dig, 1),
+                                      "libsodium_all_cores": round(S / t_sod, 1),
+                                      "openssl_1_core": round(1 / d1, 1),
+                                      "libsodium_1_core": round(1 / d1s, 1)}}
+    except Exception as e:  # noqa: BLE001
+        out["backends"] = {"error": str(e)[:200]}
+    return out
 
 
 # ------------------------------------------------------------ C4 update
@@ -748,6 +866,12 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--depth", type=int, default=12,
                     help="batches ingested ahead of certification (ring holds 24)")
+    ap.add_argument("--fetch-lag", type=int, default=8,
+                    help="steps between certifying a batch and reading its results back")
+    ap.add_argument("--pack-threads", type=int, default=8,
+                    help="host threads packing request inputs into pinned staging (e2e)")
+    ap.add_argument("--no-fault", action="store_true",
+                    help="skip the corrupt_result fault-path measurement")
     ap.add_argument("--mode", default="group", choices=["group", "replica"],
                     help="group: a whole 3-replica group per GPU (weak scaling); "
                          "replica: one replica per GPU, NCCL all-gather (N>1)")

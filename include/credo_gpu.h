@@ -201,6 +201,14 @@ typedef struct {
   const uint8_t* nonces;      /* concatenated nonce bytes */
   const uint64_t* nonce_lens; /* B */
   const uint8_t* client_sigs; /* B × 64 */
+  /* Optional (NULL: every request has u inputs). Request k with
+   * input_dims[k] != u is a misfit: execute_batch skips it (src/engine.cpp:
+   * 286-291), so no provider has a result for it — its R leaf is
+   * missing_result_leaf 0x4D (src/messages.cpp:213-218, :246-252), its
+   * outcome unsatisfied, its A leaf a failure. Its input_dims[k] doubles are
+   * read from misfit_inputs[k] (host); row k of `inputs` is ignored. */
+  const uint64_t* input_dims;
+  const double* const* misfit_inputs;
 } cg_request_batch;
 
 /* Host-memory results. Optional arrays may be NULL. */
@@ -258,6 +266,68 @@ int cg_certify_outputs(cg_group* g, const cg_request_batch* batch,
 int cg_request_digests(cg_ctx* ctx, const cg_request_batch* batch, const char* group_id,
                        uint64_t group_id_len, uint8_t* signing_digests,
                        uint8_t* canonical_ids, int8_t* status);
+
+/* ---- the batch former (InferenceEngine, src/engine.cpp:166-267) ----------
+ * Per live (group, version): FIFO queue with `seen` dedup; a batch is released
+ * when the queue reaches exec_batch_max (submit) or its oldest request has
+ * waited flush_interval_us (flush_due), or on demand (flush_version /
+ * flush_all); every submission is queued for EVERY live version (one batch
+ * per live version, engine.cpp:196-206). Requests are packed into pinned
+ * staging as they are submitted; a released batch is ingested into its
+ * group (cg_ingest_batch) and reported by cg_engine_ready as a ticket, in
+ * release order, for cg_certify_ticket. verify_request's structural checks
+ * run in submit; the Ed25519 check is the optional verifier callback's
+ * (NULL: the caller verified). */
+typedef struct cg_engine cg_engine;
+typedef struct { /* one InferenceRequest (include/credo/domain.hpp:99-115) */
+  const uint8_t* request_id; /* 32 */
+  const char* group_id;
+  uint64_t group_id_len;
+  const double* input; /* host */
+  uint64_t input_dim;
+  int has_eps;
+  double eps;
+  const uint8_t* client_pub; /* 32 */
+  const uint8_t* nonce;
+  uint64_t nonce_len;
+  const uint8_t* client_sig; /* 64 */
+} cg_request;
+typedef struct {
+  cg_group* group;
+  uint64_t version;
+  uint64_t ticket;
+  uint32_t B;
+} cg_ready_batch;
+/* SubmitOutcome::error (engine.cpp:182-209) */
+enum { CG_SUBMIT_OK = 0, CG_SUBMIT_INVALID = 1, CG_SUBMIT_UNKNOWN_GROUP = 2, CG_SUBMIT_RETIRED = 3 };
+/* GroupStatus (include/credo/domain.hpp) */
+enum { CG_GROUP_DEFINED = 0, CG_GROUP_ACTIVE = 1, CG_GROUP_RETIRED = 2 };
+/* Ed25519 verify(pub, signing_digest, sig): nonzero = valid. */
+typedef int (*cg_sig_verify_fn)(void* user, const uint8_t pub[32], const uint8_t digest[32],
+                                const uint8_t sig[64]);
+int cg_engine_create(cg_ctx* ctx, uint64_t exec_batch_max, uint64_t flush_interval_us,
+                     int pack_threads, cg_engine** out);
+void cg_engine_free(cg_engine* e);
+int cg_engine_set_verifier(cg_engine* e, cg_sig_verify_fn fn, void* user);
+/* load_group for a version whose replicas are resident as group g
+ * (group id and version are g's); status CG_GROUP_*. A second load of the
+ * same (group, version) -> CG_EINVAL ("version already loaded"). */
+int cg_engine_load_group(cg_engine* e, cg_group* g, int status);
+int cg_engine_set_status(cg_engine* e, const char* group_id, uint64_t group_id_len,
+                         uint64_t version, int status);
+/* n submissions in order at time now_us; errors[i] = CG_SUBMIT_* (may be NULL). */
+int cg_engine_submit(cg_engine* e, const cg_request* reqs, uint32_t n, uint64_t now_us,
+                     int* errors);
+int cg_engine_flush_due(cg_engine* e, uint64_t now_us);
+int cg_engine_flush_version(cg_engine* e, const char* group_id, uint64_t group_id_len,
+                            uint64_t version);
+int cg_engine_flush_all(cg_engine* e);
+int cg_engine_next_flush_deadline(cg_engine* e, uint64_t* deadline, int* has);
+/* Released, ingested batches in release order (up to cap; *n_out written). A
+ * released batch whose group ring is full waits here until tickets of that
+ * group are certified. */
+int cg_engine_ready(cg_engine* e, cg_ready_batch* out, uint32_t cap, uint32_t* n_out);
+int cg_engine_pending(cg_engine* e, uint64_t* queued, uint64_t* waiting_batches);
 
 /* ---- host digests (no device involved) -----------------------------------
  * SHA-256 on the host, x86 SHA extensions when present (the model-file check

@@ -95,6 +95,27 @@ int main() {
       if (!(hs[k] == merkle::leaf_hash(result_leaf(reqs[k], g[k])))) mismatches++;
     }
   }
+  // PerturbingExecutor(ToyExecutor, node, magnitude) (the harness wiring,
+  // harness.cpp:255-258) == CudaExecutor(ctx, node, magnitude), and a model
+  // is serialised + hashed once, not on every run
+  {
+    std::vector<std::vector<double>> xs;
+    for (auto& r : reqs) xs.push_back(r.input);
+    for (const auto& [url, bytes] : files) {
+      LinearToyModel model = LinearToyModel::from_file_bytes(ByteView(bytes.data(), bytes.size()));
+      for (uint64_t node : {0ull, 3ull}) {
+        PerturbingExecutor cpu(std::make_unique<ToyExecutor>(), node, 1e-9);
+        gpu::CudaExecutor g(ctx, node, 1e-9);
+        auto want = cpu.run(model, xs);
+        for (int rep = 0; rep < 3; rep++) {
+          checked++;
+          if (g.run(model, xs) != want) mismatches++;
+        }
+        checked++;
+        if (g.files_hashed() != 1) mismatches++;
+      }
+    }
+  }
   for (auto& [k, m] : outs) {
     auto want = distance::select_quorum(m, N, 1, distance::Metric::euclidean, 0.05);
     auto got = gpu::gpu_select_quorum(ctx, m, N, 1, distance::Metric::euclidean, 0.05);

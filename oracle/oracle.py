@@ -22,6 +22,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 ORACLE_SO = os.path.join(HERE, "liboracle.so")
 REF_SO = os.path.join(HERE, "_ref", "libcredo_ref.so")
+REF_SODIUM_SO = os.path.join(HERE, "_ref", "libcredo_ref_sodium.so")
 
 u64 = C.c_uint64
 u32 = C.c_uint32
@@ -262,24 +263,27 @@ def parse_request(buf: bytes):
 
 
 class Reference:
-    """The compiled reference (oracle/_ref). Raises OSError when absent."""
-    _lib = None
+    """The compiled reference (oracle/_ref). Raises OSError when absent.
+    backend "openssl": SHA-256 through the OpenSSL shim (SHA-NI);
+    "libsodium": the reference's own shipped libsodium crypto_hash_sha256
+    (identical digests, ~50x slower)."""
+    _libs = {}
 
     @staticmethod
-    def available() -> bool:
-        return os.path.exists(REF_SO)
+    def available(backend: str = "openssl") -> bool:
+        return os.path.exists(REF_SO if backend == "openssl" else REF_SODIUM_SO)
 
-    def __init__(self):
-        if Reference._lib is None:
-            L = C.CDLL(REF_SO)
+    def __init__(self, backend: str = "openssl"):
+        if backend not in Reference._libs:
+            L = C.CDLL(REF_SO if backend == "openssl" else REF_SODIUM_SO)
             L.ref_model_file_len.restype = u64
             L.ref_request_len.restype = u64
             L.ref_ensemble_label.restype = C.c_int64
             L.ref_batch_new.restype = vp
             L.ref_batch_new.argtypes = [vp, vp, u64, u64]
             L.ref_batch_free.argtypes = [vp]
-            Reference._lib = L
-        self.L = Reference._lib
+            Reference._libs[backend] = L
+        self.L = Reference._libs[backend]
 
     def sha256(self, data: bytes) -> bytes:
         out = C.create_string_buffer(32)
@@ -433,8 +437,9 @@ class Reference:
         self.L.ref_batch_free(h)
 
     def certify_batch(self, h, N, f, metric, eps, outputs, version,
-                      model_digests: list[bytes], threads=1, view=0, seq=1):
-        """outputs: (N, B, v) float64."""
+                      model_digests: list[bytes], threads=1, view=0, seq=1, missing=None):
+        """outputs: (N, B, v) float64; missing: optional B flags (request has
+        no result from any provider: a misfit)."""
         outputs = np.ascontiguousarray(outputs, np.float64)
         N_, B, v = outputs.shape
         sel = np.zeros(B, np.uint64)
@@ -444,11 +449,12 @@ class Reference:
         r_roots = C.create_string_buffer(32 * N)
         a_root = C.create_string_buffer(32)
         mlen = u64()
-        rc = self.L.ref_certify_batch(
+        miss = None if missing is None else np.ascontiguousarray(missing, np.uint8)
+        rc = self.L.ref_certify_batch_ex(
             vp(h), u64(N), u64(f), u32(metric), dbl(eps), _p(outputs), u64(v),
             u64(version), b"".join(model_digests), u64(view), u64(seq),
             C.c_int(threads), _p(sel), _p(diam), _p(sat), _p(label), r_roots,
-            a_root, C.byref(mlen))
+            a_root, C.byref(mlen), _p(miss))
         assert rc == 0, rc
         return dict(sel_mask=sel, diameter=diam, satisfied=sat, label=label,
                     r_roots=[r_roots.raw[32 * i:32 * i + 32] for i in range(N)],

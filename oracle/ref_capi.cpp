@@ -419,20 +419,26 @@ void ref_batch_free(void* h) { delete static_cast<RefBatch*>(h); }
 // and manifest length. threads<=1 runs the reference's Tree::build verbatim;
 // threads>1 shards leaf hashing across std::threads and folds with the same
 // H(0x01||L||R) rule (src/merkle.cpp:14-19), giving identical roots.
-int ref_certify_batch(void* h, uint64_t N, uint64_t f, uint32_t metric,
-                      double eps_default, const double* outputs, uint64_t v,
-                      uint64_t version, const uint8_t* model_digests,
-                      uint64_t view, uint64_t seq, int threads,
-                      uint64_t* sel_mask, double* diam, uint8_t* satisfied,
-                      int64_t* label, uint8_t* r_roots, uint8_t* a_root,
-                      uint64_t* manifest_len) {
+// missing (optional, B flags): request k has no result from any provider
+// (execute_batch skipped it as a misfit, engine.cpp:286-291): its R leaves are
+// missing_result_leaf and try_attest leaves it unsatisfied without running
+// select_quorum (coordinator.cpp:748-771).
+int ref_certify_batch_ex(void* h, uint64_t N, uint64_t f, uint32_t metric,
+                         double eps_default, const double* outputs, uint64_t v,
+                         uint64_t version, const uint8_t* model_digests,
+                         uint64_t view, uint64_t seq, int threads,
+                         uint64_t* sel_mask, double* diam, uint8_t* satisfied,
+                         int64_t* label, uint8_t* r_roots, uint8_t* a_root,
+                         uint64_t* manifest_len, const uint8_t* missing) {
   try {
     auto* b = static_cast<RefBatch*>(h);
     const uint64_t B = b->reqs.size();
+    auto miss = [&](uint64_t k) { return missing && missing[k]; };
     // results[p][k]
     std::vector<std::map<uint64_t, InferenceResult>> results(N);
     for (uint64_t p = 0; p < N; p++) {
       for (uint64_t k = 0; k < B; k++) {
+        if (miss(k)) continue;
         InferenceResult r;
         r.request_id = b->reqs[k].request_id;
         r.node_index = p;
@@ -462,6 +468,13 @@ int ref_certify_batch(void* h, uint64_t N, uint64_t f, uint32_t metric,
     // Agreement: select_quorum over all N outputs + label vote.
     std::vector<distance::AgreementOutcome> outc(B);
     parallel_for(B, [&](uint64_t k) {
+      if (miss(k)) {  // fewer than N-f outputs: unsatisfied, select_quorum not run
+        sel_mask[k] = 0;
+        diam[k] = 0;
+        satisfied[k] = 0;
+        label[k] = -1;
+        return;
+      }
       std::map<uint64_t, std::vector<double>> outs;
       for (uint64_t p = 0; p < N; p++) outs[p] = results[p][k].output;
       double eps = b->reqs[k].epsilon_override ? *b->reqs[k].epsilon_override
@@ -488,8 +501,8 @@ int ref_certify_batch(void* h, uint64_t N, uint64_t f, uint32_t metric,
       std::vector<Hash32> leaves(N * B);
       parallel_for(N * B, [&](uint64_t i) {
         uint64_t p = i / B, k = i % B;
-        leaves[i] =
-            merkle::leaf_hash(result_leaf(*b->ops[k].request, results[p][k]));
+        leaves[i] = miss(k) ? merkle::leaf_hash(missing_result_leaf(*b->ops[k].request))
+                            : merkle::leaf_hash(result_leaf(*b->ops[k].request, results[p][k]));
       });
       for (uint64_t p = 0; p < N; p++) {
         std::vector<Hash32> lvl(leaves.begin() + p * B,
@@ -554,7 +567,8 @@ int ref_certify_batch(void* h, uint64_t N, uint64_t f, uint32_t metric,
     }
     std::map<uint64_t, std::map<uint64_t, InferenceResult>> by_op;
     for (uint64_t k = 0; k < B; k++)
-      for (uint64_t p = 0; p < N; p++) by_op[k][p] = results[p][k];
+      if (!miss(k))
+        for (uint64_t p = 0; p < N; p++) by_op[k][p] = results[p][k];
     std::vector<Bytes> a_leaves(manifest.size());
     parallel_for(manifest.size(), [&](uint64_t i) {
       a_leaves[i] = *attest_leaf_bytes(manifest[i], b->ops, r_root_map, by_op);
@@ -597,6 +611,16 @@ int ref_hash_ops(const uint8_t* encs, const uint64_t* lens, uint64_t n, const ui
   } catch (const std::exception&) {
     return -1;
   }
+}
+
+int ref_certify_batch(void* h, uint64_t N, uint64_t f, uint32_t metric, double eps_default,
+                      const double* outputs, uint64_t v, uint64_t version,
+                      const uint8_t* model_digests, uint64_t view, uint64_t seq, int threads,
+                      uint64_t* sel_mask, double* diam, uint8_t* satisfied, int64_t* label,
+                      uint8_t* r_roots, uint8_t* a_root, uint64_t* manifest_len) {
+  return ref_certify_batch_ex(h, N, f, metric, eps_default, outputs, v, version, model_digests,
+                              view, seq, threads, sel_mask, diam, satisfied, label, r_roots,
+                              a_root, manifest_len, nullptr);
 }
 
 }  // extern "C"

@@ -369,6 +369,114 @@ def hash_ops_batches(batches: Sequence["RequestBatch"], group_id: bytes, version
     return [out.raw[32 * i:32 * i + 32] for i in range(len(batches))]
 
 
+class _CRequest(C.Structure):
+    _fields_ = [("request_id", vp), ("group_id", C.c_char_p), ("group_id_len", u64),
+                ("input", vp), ("input_dim", u64), ("has_eps", C.c_int), ("eps", dbl),
+                ("client_pub", vp), ("nonce", C.c_char_p), ("nonce_len", u64),
+                ("client_sig", vp)]
+
+
+class _CReady(C.Structure):
+    _fields_ = [("group", vp), ("version", u64), ("ticket", u64), ("B", u32)]
+
+
+SUBMIT_OK, SUBMIT_INVALID, SUBMIT_UNKNOWN_GROUP, SUBMIT_RETIRED = range(4)
+GROUP_DEFINED, GROUP_ACTIVE, GROUP_RETIRED = range(3)
+
+
+class InferenceEngine:
+    """The batch former (InferenceEngine::submit / flush_due / flush_version /
+    flush_all / next_flush_deadline, engine.cpp:166-267) over GPU groups:
+    per live (group, version) FIFO with seen-dedup, batches of
+    exec_batch_max or flushed partial ones, packed into pinned staging as
+    requests arrive and ingested into the group; ready() returns
+    (group, version, ticket, B) in release order for certify_ticket."""
+
+    def __init__(self, ctx: Context, exec_batch_max: int, flush_interval_us: int,
+                 pack_threads: int = 1):
+        self.ctx = ctx
+        h = vp()
+        ctx._check(ctx.L.cg_engine_create(ctx.h, u64(exec_batch_max), u64(flush_interval_us),
+                                          C.c_int(pack_threads), C.byref(h)))
+        self.h = h
+        self._groups = {}
+
+    def free(self):
+        if self.h:
+            self.ctx.L.cg_engine_free(self.h)
+            self.h = None
+
+    def load_group(self, group: "ModelGroup", status: int = GROUP_ACTIVE):
+        self.ctx._check(self.ctx.L.cg_engine_load_group(self.h, group.h, C.c_int(status)))
+        self._groups[group.h.value] = group
+
+    def set_status(self, group_id: bytes, version: int, status: int):
+        self.ctx._check(self.ctx.L.cg_engine_set_status(self.h, group_id, u64(len(group_id)),
+                                                        u64(version), C.c_int(status)))
+
+    def submit(self, batch: RequestBatch, now_us: int, group_id: bytes = b"group-0"):
+        """Submits the batch's requests in order; returns the per-request
+        SubmitOutcome error codes (SUBMIT_*)."""
+        return self.submit_prepared(self.prepare(batch, group_id), now_us)
+
+    def prepare(self, batch: RequestBatch, group_id: bytes = b"group-0"):
+        """The cg_request array of a batch (pointers into its arrays; keep
+        the batch alive), reusable across submit_prepared calls."""
+        n = len(batch.nonces)
+        rows = batch.inputs if isinstance(batch.inputs, (list, tuple)) else \
+            np.ascontiguousarray(batch.inputs, np.float64)
+        rows = [np.ascontiguousarray(rows[k], np.float64).ravel() for k in range(n)]
+        ids = np.ascontiguousarray(batch.request_ids, np.uint8)
+        pubs = np.ascontiguousarray(batch.client_pubs, np.uint8)
+        sigs = np.ascontiguousarray(batch.client_sigs, np.uint8)
+        arr = (_CRequest * max(n, 1))()
+        for k in range(n):
+            e = None if batch.eps is None else batch.eps[k]
+            arr[k] = _CRequest(ids[k].ctypes.data, group_id, len(group_id), rows[k].ctypes.data,
+                               len(rows[k]), int(e is not None), e or 0.0, pubs[k].ctypes.data,
+                               batch.nonces[k], len(batch.nonces[k]), sigs[k].ctypes.data)
+        return (arr, n, [rows, ids, pubs, sigs, batch])
+
+    def submit_prepared(self, prepared, now_us: int):
+        arr, n, _keep = prepared
+        err = np.zeros(max(n, 1), np.int32)
+        self.ctx._check(self.ctx.L.cg_engine_submit(self.h, arr, u32(n), u64(now_us), _p(err)))
+        return err[:n].tolist()
+
+    def flush_due(self, now_us: int):
+        self.ctx._check(self.ctx.L.cg_engine_flush_due(self.h, u64(now_us)))
+
+    def flush_version(self, group_id: bytes, version: int):
+        self.ctx._check(self.ctx.L.cg_engine_flush_version(self.h, group_id, u64(len(group_id)),
+                                                           u64(version)))
+
+    def flush_all(self):
+        self.ctx._check(self.ctx.L.cg_engine_flush_all(self.h))
+
+    def next_flush_deadline(self) -> Optional[int]:
+        d, has = u64(), C.c_int()
+        self.ctx._check(self.ctx.L.cg_engine_next_flush_deadline(self.h, C.byref(d), C.byref(has)))
+        return d.value if has.value else None
+
+    def ready(self):
+        """[(ModelGroup, version, ticket, B)] released since the last call."""
+        out = []
+        while True:
+            buf = (_CReady * 64)()
+            n = u32()
+            self.ctx._check(self.ctx.L.cg_engine_ready(self.h, buf, u32(64), C.byref(n)))
+            for i in range(n.value):
+                r = buf[i]
+                out.append((self._groups[r.group], r.version, r.ticket, r.B))
+            if n.value < 64:
+                return out
+
+    def pending(self):
+        q, w = u64(), u64()
+        self.ctx._check(self.ctx.L.cg_engine_pending(self.h, C.byref(q), C.byref(w)))
+        return q.value, w.value
+
+
 @dataclass
 class AgreementOutcome:
     """distance::AgreementOutcome (distance.hpp:55-59)."""
@@ -484,7 +592,8 @@ class RequestBatch:
             sigs.append(np.frombuffer(buf[off:off + 64], np.uint8)); off += 64
             if off != len(buf):
                 raise CodecError(CG_ECODEC, "trailing bytes after value")
-        return cls(np.stack(ids), np.stack(inputs), np.stack(pubs), nonces,
+        ragged = len({len(x) for x in inputs}) > 1  # misfit requests: keep rows
+        return cls(np.stack(ids), inputs if ragged else np.stack(inputs), np.stack(pubs), nonces,
                    np.stack(sigs), eps if any(e is not None for e in eps) else None)
 
 
@@ -492,7 +601,7 @@ class _CReqBatch(C.Structure):
     _fields_ = [("B", u32), ("u", u64), ("request_ids", vp), ("inputs", vp),
                 ("inputs_on_device", C.c_int), ("has_eps", vp), ("eps", vp),
                 ("client_pubs", vp), ("nonces", vp), ("nonce_lens", vp),
-                ("client_sigs", vp)]
+                ("client_sigs", vp), ("input_dims", vp), ("misfit_inputs", vp)]
 
 
 class _COut(C.Structure):
@@ -570,7 +679,24 @@ class ModelGroup:
             self.h = None
 
     @staticmethod
-    def _cbatch(b: RequestBatch):
+    def _cbatch(b: RequestBatch, group_u: Optional[int] = None):
+        """RequestBatch -> cg_request_batch. b.inputs: (B, u) array, a device
+        pointer, or (ragged) a list of 1-D arrays: rows whose length is not
+        group_u are misfits (execute_batch skips them)."""
+        dims = mis = None
+        if isinstance(b.inputs, (list, tuple)):
+            assert group_u is not None
+            rows = [np.ascontiguousarray(r, np.float64).ravel() for r in b.inputs]
+            x = np.zeros((len(rows), group_u), np.float64)
+            dims = np.array([len(r) for r in rows], np.uint64)
+            mis = (vp * len(rows))(*[r.ctypes.data if len(r) else None for r in rows])
+            for k, r in enumerate(rows):
+                if len(r) == group_u:
+                    x[k] = r
+            b = RequestBatch(b.request_ids, x, b.client_pubs, b.nonces, b.client_sigs, b.eps)
+            misfit_keep = (rows, dims, mis)
+        else:
+            misfit_keep = None
         on_dev = not isinstance(b.inputs, np.ndarray)
         if on_dev:
             inputs_ptr, B, u = int(b.inputs), int(b.B), int(b.u)
@@ -587,12 +713,14 @@ class ModelGroup:
             has = np.array([e is not None for e in b.eps], np.uint8)
             eps = np.array([e or 0.0 for e in b.eps], np.float64)
         keep = [ids, pubs, sigs, nl, nb, has, eps,
-                None if on_dev else x]
+                None if on_dev else x, misfit_keep]
         cb = _CReqBatch(B, u, ids.ctypes.data, inputs_ptr, int(on_dev),
                         None if has is None else has.ctypes.data,
                         None if eps is None else eps.ctypes.data,
                         pubs.ctypes.data, nb.ctypes.data, nl.ctypes.data,
-                        sigs.ctypes.data)
+                        sigs.ctypes.data,
+                        None if dims is None else dims.ctypes.data,
+                        None if mis is None else C.cast(mis, vp))
         return cb, keep, B
 
     def encode_results(self, provider: int, ticket: Optional[int] = None) -> bytes:
@@ -626,7 +754,7 @@ class ModelGroup:
                 want_leaves: bool = False, sync: bool = True):
         """One ExecutionBatch through the hot path. sync=False only enqueues
         (results stay on the device; call :meth:`fetch`)."""
-        cb, keep, B = self._cbatch(batch)
+        cb, keep, B = self._cbatch(batch, self.u)
         self._keep = keep
         if not sync:
             self.ctx._check(self.ctx.L.cg_certify_batch(self.h, C.byref(cb), None))
@@ -638,7 +766,7 @@ class ModelGroup:
     def ingest(self, batch: RequestBatch) -> int:
         """InferenceEngine::submit's hot part: frame, upload and start the
         request-midstate chains. Returns a ticket for :meth:`certify_ticket`."""
-        cb, keep, B = self._cbatch(batch)
+        cb, keep, B = self._cbatch(batch, self.u)
         t = C.c_uint64()
         self.ctx._check(self.ctx.L.cg_ingest_batch(self.h, C.byref(cb), C.byref(t)))
         self._inflight = getattr(self, "_inflight", {})
@@ -646,8 +774,10 @@ class ModelGroup:
         return t.value
 
     def certify_ticket(self, ticket: int, sync: bool = True, want_outputs=False,
-                       want_leaves=False):
-        keep, B = self._inflight.pop(ticket)
+                       want_leaves=False, B: Optional[int] = None):
+        """B: the batch size, for tickets ingested by an InferenceEngine."""
+        self._inflight = getattr(self, "_inflight", {})
+        keep, B = self._inflight.pop(ticket, (None, B))
         self._lastB = B
         self._doneB = getattr(self, "_doneB", {})
         self._doneB[ticket] = B
@@ -663,7 +793,7 @@ class ModelGroup:
                         want_leaves: bool = False):
         """Agreement + digests over precomputed (N, B, v) replica outputs
         (C5 sweep / fault injection: a corrupt replica is a shifted row)."""
-        cb, keep, B = self._cbatch(batch)
+        cb, keep, B = self._cbatch(batch, self.u)
         o = np.ascontiguousarray(outputs, np.float64)
         assert o.shape == (self.N, B, self.v)
         self._keep = keep + [o]

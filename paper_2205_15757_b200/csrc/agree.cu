@@ -665,6 +665,29 @@ void launch_attest_manifest(uint32_t B, uint32_t N, const uint32_t* sel,
   CG_CHECK_LAUNCH();
 }
 
+// Requests without any provider output (misfits): outcome unsatisfied with
+// an empty quorum, no label (coordinator.cpp:759-773: select_quorum only
+// runs with >= N-f outputs).
+__global__ void mark_missing_kernel(const uint8_t* __restrict__ miss, uint32_t B,
+                                    uint32_t* sel, double* diam, uint8_t* sat, int8_t* status,
+                                    int64_t* label) {
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= B || !miss[k]) return;
+  sel[k] = 0;
+  diam[k] = 0.0;
+  sat[k] = 0;
+  status[k] = 0;
+  if (label) label[k] = -1;
+}
+
+void launch_mark_missing(const uint8_t* miss, uint32_t B, uint32_t* sel, double* diam,
+                         uint8_t* sat, int8_t* status, int64_t* label, cudaStream_t st) {
+  if (B == 0) return;
+  mark_missing_kernel<<<(unsigned)ceil_div(B, 128), 128, 0, st>>>(miss, B, sel, diam, sat, status,
+                                                                 label);
+  CG_CHECK_LAUNCH();
+}
+
 // ---------------------------------------------------------- softmax/top-k
 // One warp per row: peak = first max, exp(x - peak) lane-parallel, the sum
 // taken sequentially by lane 0 in lane order (model.cpp:26-34 sums in index

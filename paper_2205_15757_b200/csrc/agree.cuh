@@ -30,6 +30,8 @@ void launch_attest_manifest(uint32_t B, uint32_t N, const uint32_t* sel,
                             uint8_t* a_leaves, int32_t* single_pos, int32_t* need53,
                             uint8_t* kinds, uint32_t* m_nodes, uint32_t* m_ops,
                             uint32_t* count, cudaStream_t st);
+void launch_mark_missing(const uint8_t* miss, uint32_t B, uint32_t* sel, double* diam,
+                         uint8_t* sat, int8_t* status, int64_t* label, cudaStream_t st);
 void launch_softmax_topk_f32(const float* in, uint64_t in_ld, uint32_t rows,
                              uint32_t v, int do_softmax, double* out,
                              uint64_t out_ld, uint32_t k, uint32_t* topi,

@@ -31,6 +31,7 @@
 #include "digest.cuh"
 #include "gemm_sm100.cuh"
 #include "host_sha256.h"
+#include "runtime.cuh"
 
 namespace cg {
 
@@ -74,166 +75,12 @@ void timer_end(cudaStream_t st, int cls) {
   g_timers.spans[cls].push_back({b, i});
 }
 
-struct CodecError : std::runtime_error {
-  using std::runtime_error::runtime_error;
-};
-struct DigestError : std::runtime_error {
-  using std::runtime_error::runtime_error;
-};
-
-// ------------------------------------------------------------- buffers
-template <typename T>
-struct DevBuf {
-  T* p = nullptr;
-  size_t n = 0;
-  DevBuf() = default;
-  DevBuf(const DevBuf&) = delete;
-  DevBuf& operator=(const DevBuf&) = delete;
-  ~DevBuf() { release(); }
-  void release() {
-    if (p) cudaFree(p);
-    p = nullptr;
-    n = 0;
-  }
-  void ensure(size_t count) {
-    if (count <= n) return;
-    release();
-    CG_CUDA(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)));
-    n = count;
-  }
-};
-
-template <typename T>
-struct PinBuf {
-  T* p = nullptr;
-  size_t n = 0;
-  ~PinBuf() {
-    if (p) cudaFreeHost(p);
-  }
-  void ensure(size_t count) {
-    if (count <= n) return;
-    if (p) cudaFreeHost(p);
-    p = nullptr;
-    CG_CUDA(cudaMallocHost(&p, std::max<size_t>(count, 1) * sizeof(T)));
-    n = count;
-  }
-};
-
-// ------------------------------------------------------ canonical bytes
-// codec.hpp:28-84: u64 BE, u32 BE length prefixes, bool byte, raw fixed.
-struct Enc {
-  std::vector<uint8_t> b;
-  void u8(uint8_t v) { b.push_back(v); }
-  void u32(uint32_t v) {
-    for (int s = 24; s >= 0; s -= 8) b.push_back((uint8_t)(v >> s));
-  }
-  void u64(uint64_t v) {
-    for (int s = 56; s >= 0; s -= 8) b.push_back((uint8_t)(v >> s));
-  }
-  void f64(double d) {
-    uint64_t v;
-    std::memcpy(&v, &d, 8);
-    u64(v);
-  }
-  void raw(const uint8_t* p, size_t n) { b.insert(b.end(), p, p + n); }
-  void bytes(const uint8_t* p, size_t n) {
-    u32((uint32_t)n);
-    raw(p, n);
-  }
-};
-
-// Host arena for the framing bytes of chain jobs. A raw segment is placed
-// at an arena offset congruent to its message offset mod 4 so that every
-// whole message word inside it is one aligned 32-bit load on the device.
-struct Arena {
-  std::vector<uint8_t> b;
-  size_t add(const uint8_t* p, size_t n, uint64_t msg_off) {
-    while ((b.size() & 3) != (msg_off & 3)) b.push_back(0);
-    size_t o = b.size();
-    b.insert(b.end(), p, p + n);
-    return o;
-  }
-};
-
 }  // namespace cg
 
 using namespace cg;
 
-constexpr int kIngestRing = CG_INGEST_RING;
-
-// ------------------------------------------------------------------ ctx
-struct cg_ctx {
-  int device = 0;
-  cudaStream_t stream = nullptr;
-  bool own_stream = true;
-  cudaStream_t side = nullptr;
-  cudaEvent_t ev_a = nullptr, ev_b = nullptr;
-  std::string err;
-  std::mutex mu;
-  // scratch for the standalone digest / agreement entry points
-  DevBuf<uint8_t> d_bytes, d_out;
-  DevBuf<ChainJob> d_jobs;
-  DevBuf<double> d_f64;
-  DevBuf<uint32_t> d_u32a, d_u32b;
-  DevBuf<uint64_t> d_u64a, d_u64b;
-  DevBuf<uint8_t> d_u8;
-  DevBuf<int8_t> d_i8;
-  DevBuf<int64_t> d_i64;
-  DevBuf<double> d_f64b;
-  // replica-parallel groups: one NCCL communicator over the ranks (one per GPU)
-  ncclComm_t comm = nullptr;
-  int rank = 0, nranks = 1;
-  // certification tails (result leaves, agreement, trees) of every group of
-  // this context, in issue order: they overlap the next batch's forwards,
-  // and one stream keeps the NCCL exchanges in the same order on all ranks
-  cudaStream_t tail = nullptr;
-  // groups created on this context (cg_ctx_join drains their slot streams)
-  std::vector<cg_group*> groups;
-};
 
 namespace {
-void join_group_slots(cg_ctx* ctx);
-}
-
-struct cg_model {
-  cg_ctx* ctx = nullptr;
-  int kind = 0;  // 0 linear, 1 cnn
-  uint64_t u = 0, v = 0;
-  bool softmax = false;
-  uint8_t digest[32];
-  DevBuf<double> W, b;          // linear
-  std::unique_ptr<CnnModel> cnn;  // cnn
-};
-
-namespace {
-
-int fail(cg_ctx* ctx, int code, const std::string& msg) {
-  if (ctx) ctx->err = msg;
-  return code;
-}
-
-template <typename Fn>
-int guarded(cg_ctx* ctx, Fn&& fn) {
-  if (!ctx) return CG_EINVAL;
-  try {
-    std::lock_guard<std::mutex> lk(ctx->mu);
-    ctx->err.clear();
-    CG_CUDA(cudaSetDevice(ctx->device));
-    return fn();
-  } catch (const InvalidArgument& e) {
-    return fail(ctx, CG_EINVAL, e.what());
-  } catch (const std::invalid_argument& e) {
-    return fail(ctx, CG_EINVAL, e.what());
-  } catch (const CodecError& e) {
-    return fail(ctx, CG_ECODEC, e.what());
-  } catch (const DigestError& e) {
-    return fail(ctx, CG_EDIGEST, e.what());
-  } catch (const CudaError& e) {
-    return fail(ctx, CG_ECUDA, e.what());
-  } catch (const std::exception& e) {
-    return fail(ctx, CG_ECUDA, e.what());
-  }
-}
 
 // SHA-256 of count host messages on the device (one chain job each).
 // prefix_byte >= 0 prepends that byte (merkle leaf domain 0x00).
@@ -667,17 +514,43 @@ int cg_model_load_linear(cg_ctx* ctx, const uint8_t* file, uint64_t len,
 
 int cg_model_load_cnn(cg_ctx* ctx, const uint8_t* file, uint64_t len,
                       const uint8_t digest[32], cg_model** out) {
-  return guarded(ctx, [&] {
-    *out = nullptr;
-    std::unique_ptr<CnnModel> cnn;
+  if (!ctx || !out) return CG_EINVAL;
+  *out = nullptr;
+  // Host phase -- the ~100 MB digest check (engine.cpp:79, before parsing),
+  // the parse and the BN fold -- runs without the context lock, so a model
+  // version loaded in the background does not stall certification on this
+  // context (C4's mid-stream update).
+  std::unique_ptr<CnnModel> cnn;
+  int code = CG_OK;
+  std::string msg;
+  try {
     check_model_digest(file, len, digest);
+    cnn = CnnModel::from_file(file, len);
+  } catch (const DigestError& e) {
+    code = CG_EDIGEST;
+    msg = e.what();
+  } catch (const std::invalid_argument& e) {
+    code = CG_ECODEC;
+    msg = e.what();
+  } catch (const std::exception& e) {
+    code = CG_ECUDA;
+    msg = e.what();
+  }
+  return guarded(ctx, [&] {
+    if (code == CG_EDIGEST) throw DigestError(msg);
+    if (code == CG_ECODEC) throw CodecError(msg);
+    if (code != CG_OK) throw std::runtime_error(msg);
+    // weights go up on a private stream: the context's streams keep running
+    cudaStream_t up = nullptr;
+    CG_CUDA(cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking));
     try {
-      cnn = CnnModel::from_file(file, len);
-    } catch (const std::invalid_argument& e) {
-      throw CodecError(e.what());
+      cnn->upload(up);
+    } catch (...) {
+      cudaStreamDestroy(up);
+      throw;
     }
-    cnn->upload(ctx->stream);
-    CG_CUDA(cudaStreamSynchronize(ctx->stream));
+    CG_CUDA(cudaStreamSynchronize(up));
+    CG_CUDA(cudaStreamDestroy(up));
     auto m = std::make_unique<cg_model>();
     m->ctx = ctx;
     m->kind = 1;
@@ -833,93 +706,7 @@ extern "C" int cg_dbg_forward_bench(cg_ctx* ctx, cg_model* m, uint32_t B, int it
   });
 }
 
-// ------------------------------------------------------------------ group
-// One in-flight ExecutionBatch: its framing bytes, chain jobs, request
-// midstates and (for host inputs) its device copy of the inputs. Ingest runs
-// on the slot's own stream so the prefix chains of several batches proceed
-// concurrently with each other and with the replica forwards.
-// A certified batch's device results; they live in the batch's ingest slot
-// until the slot is reused (ring depth later), so the tail of batch i can
-// run while batch i+1's forwards write their own slot.
-struct BatchResults {
-  DevBuf<double> d_outs, d_topv, d_diam;
-  DevBuf<uint32_t> d_topi, d_sel, d_mnodes, d_mops, d_count;
-  DevBuf<uint8_t> d_leaf, d_rroots, d_aleaf, d_aroot, d_sat, d_kinds;
-  DevBuf<int8_t> d_status;
-  DevBuf<int64_t> d_label;
-  DevBuf<int32_t> d_single_pos, d_need53;
-};
-
-struct IngestSlot {
-  bool used = false, ever = false, certified = false;
-  uint64_t ticket = 0;
-  uint32_t B = 0;
-  BatchResults res;
-  cudaEvent_t ev_fwd = nullptr;  // replica outputs written (main stream)
-  const double* d_in_ptr = nullptr;
-  DevBuf<double> d_in, d_eps;  // d_in: device copy of host inputs (allocated on first use)
-  DevBuf<uint8_t> d_arena, d_reqids;
-  // chain jobs: [0, B) request midstates H(0x00||0x52||req), [B, off_leaf)
-  // PerturbingExecutor seed midstates, [off_leaf, +N*B) result leaves,
-  // [off_mid53, +B) single-attestation request midstates H(0x00||0x53||req)
-  // (run only for requests with a single leaf), [off_single, +N*B) the
-  // single leaves' tails
-  DevBuf<ChainJob> d_jobs;
-  uint64_t off_leaf = 0, off_mid53 = 0, off_single = 0;
-  bool perturbed = false;
-  DevBuf<uint32_t> d_mid, d_mid53, d_pmid;
-  DevBuf<uint64_t> d_tree;  // per-provider tree offsets then lengths
-  PinBuf<uint8_t> h_arena, h_reqids;
-  PinBuf<ChainJob> h_jobs;
-  PinBuf<double> h_eps;
-  PinBuf<uint64_t> h_tree;
-  cudaStream_t stream = nullptr;
-  cudaEvent_t ev_staged = nullptr, ev_prefix = nullptr, ev_done = nullptr, ev_man = nullptr;
-  ~IngestSlot() {
-    if (stream) cudaStreamDestroy(stream);
-    if (ev_staged) cudaEventDestroy(ev_staged);
-    if (ev_prefix) cudaEventDestroy(ev_prefix);
-    if (ev_done) cudaEventDestroy(ev_done);
-    if (ev_fwd) cudaEventDestroy(ev_fwd);
-    if (ev_man) cudaEventDestroy(ev_man);
-  }
-};
-
-struct cg_group {
-  cg_ctx* ctx = nullptr;
-  std::vector<cg_model*> models;          // local replicas (dist: just this rank's)
-  std::vector<std::array<uint8_t, 32>> digests;  // weights digest of every provider
-  bool dist = false;                      // replica-parallel over the ctx's NCCL ranks
-  uint32_t rank = 0;                      // this rank's provider index (dist)
-  uint32_t N = 0, f = 0, metric = 0, maxB = 0, topk = 1;
-  double eps_default = 0;
-  std::string gid;
-  uint64_t version = 0;
-  uint64_t u = 0, v = 0;
-  // forward scratch (main stream); per-batch results live in the slots
-  DevBuf<double> d_pre64;
-  DevBuf<float> d_pre32;
-  DevBuf<uint8_t> d_gid;
-  DevBuf<uint8_t> d_prep;  // shared CNN input operand
-  IngestSlot* last = nullptr;  // the last certified batch (fetch, paths)
-  bool all_cnn = false, same_prep = false;
-  bool group_plan_ok = std::getenv("CREDO_NO_GROUP") == nullptr;  // false: per replica
-  std::unique_ptr<CnnGroupPlan> gplan;   // grouped per-layer launches
-  std::vector<std::unique_ptr<IngestSlot>> slots;
-  uint64_t next_ticket = 1;
-  uint32_t last_B = 0;
-  // PerturbingExecutor wrapping of every local replica (harness.cpp:255-258;
-  // the harness default perturb_magnitude is 1e-9, harness.hpp:163)
-  double perturb_mag = 0;
-  DevBuf<uint8_t> d_phdr;     // 64 B per local provider: the seed header
-  // OffsetExecutor fault injection (harness.cpp:167-186): provider
-  // fault_provider's outputs += fault_offset for requests whose first id
-  // byte is < fault_thr (0: no fault)
-  uint32_t fault_provider = 0, fault_thr = 0;
-  double fault_offset = 0;
-};
-
-namespace {
+namespace cg {
 
 // Each local provider p's outputs += its PerturbingExecutor offsets
 // (model.cpp:82-105). The per (p, request) midstates over the shared whole
@@ -986,24 +773,36 @@ uint64_t ingest(cg_group* g, const cg_request_batch* bt) {
   }
   Arena ar;
   std::vector<ChainJob> jobs;
-  jobs.reserve((size_t)B * (2 + 2 * N + g->models.size()));
+  jobs.reserve((size_t)B * (3 + 2 * N + g->models.size()));
   const uint8_t* gid = (const uint8_t*)g->gid.data();
   const uint32_t gl = (uint32_t)g->gid.size();
   struct ReqLayout {
-    size_t h, h53, t;
-    uint64_t lenH, lenT, P;
+    size_t h, h53, h4d, t;
+    uint64_t lenH, lenT, P, uk, moff;  // uk: this request's input count; moff: misfit input offset
+    bool miss;
   };
   std::vector<ReqLayout> rl(B);
   std::vector<size_t> res_off((size_t)B * N), dig_off((size_t)B * N);
-  uint64_t lenRes = 0, nonce_pos = 0;
+  uint64_t lenRes = 0, nonce_pos = 0, misfit_total = 0;
+  bool any_miss = false;
   for (uint32_t k = 0; k < B; k++) {
     const uint8_t* rid = bt->request_ids + 32 * k;
+    ReqLayout& L = rl[k];
+    L.uk = bt->input_dims ? bt->input_dims[k] : u;
+    L.miss = L.uk != u;
+    L.moff = misfit_total;
+    if (L.miss) {
+      if (!bt->misfit_inputs || (L.uk && !bt->misfit_inputs[k]))
+        throw InvalidArgument("misfit request without its input");
+      misfit_total += L.uk;
+      any_miss = true;
+    }
     Enc H;  // 0x00 (leaf domain) || 0x52 (result leaf) || request body head
     H.u8(0x00);
     H.u8(0x52);
     H.raw(rid, 32);
     H.bytes(gid, gl);
-    H.u32((uint32_t)u);
+    H.u32((uint32_t)L.uk);
     Enc T;  // request tail after the f64 input list (domain.cpp:144-158)
     bool he = bt->has_eps && bt->has_eps[k];
     T.u8(he ? 1 : 0);
@@ -1012,14 +811,15 @@ uint64_t ingest(cg_group* g, const cg_request_batch* bt) {
     T.bytes(bt->nonces + nonce_pos, bt->nonce_lens[k]);
     nonce_pos += bt->nonce_lens[k];
     T.raw(bt->client_sigs + 64 * k, 64);
-    ReqLayout& L = rl[k];
     L.lenH = H.b.size();
     L.lenT = T.b.size();
-    L.P = L.lenH + 8 * u + L.lenT;
+    L.P = L.lenH + 8 * L.uk + L.lenT;
     L.h = ar.add(H.b.data(), H.b.size(), 0);
     H.b[1] = 0x53;  // single_attest_leaf tag (messages.cpp:283-290)
     L.h53 = ar.add(H.b.data(), H.b.size(), 0);
-    L.t = ar.add(T.b.data(), T.b.size(), L.lenH + 8 * u);
+    H.b[1] = 0x4D;  // missing_result_leaf tag (messages.cpp:213-218)
+    L.h4d = L.miss ? ar.add(H.b.data(), H.b.size(), 0) : 0;
+    L.t = ar.add(T.b.data(), T.b.size(), L.lenH + 8 * L.uk);
     for (uint32_t p = 0; p < N; p++) {
       Enc R;  // InferenceResult::encode up to the output list (domain.cpp:218-225)
       R.raw(rid, 32);
@@ -1038,6 +838,24 @@ uint64_t ingest(cg_group* g, const cg_request_batch* bt) {
   const uint64_t A = (uint64_t)S.d_arena.p;
   if (!bt->inputs_on_device) S.d_in.ensure((uint64_t)g->maxB * u);
   S.d_in_ptr = bt->inputs_on_device ? bt->inputs : S.d_in.p;
+  S.any_miss = any_miss;
+  if (any_miss) {
+    S.d_misfit.ensure(std::max<uint64_t>(misfit_total, 1));
+    S.d_miss.ensure(g->maxB);
+    S.h_miss.ensure(g->maxB);
+    if (!S.d_neg1.p) {
+      const int32_t neg1 = -1;
+      S.d_neg1.ensure(1);
+      CG_CUDA(cudaMemcpy(S.d_neg1.p, &neg1, 4, cudaMemcpyHostToDevice));
+    }
+    for (uint32_t k = 0; k < B; k++) {
+      S.h_miss.p[k] = rl[k].miss ? 1 : 0;
+      if (rl[k].miss && rl[k].uk)  // pageable host source: synchronous, rare
+        CG_CUDA(cudaMemcpyAsync(S.d_misfit.p + rl[k].moff, bt->misfit_inputs[k], 8 * rl[k].uk,
+                                cudaMemcpyHostToDevice, st));
+    }
+  }
+  const uint64_t MIS = (uint64_t)S.d_misfit.p;
   const uint64_t IN = (uint64_t)S.d_in_ptr;
   const uint64_t OUT = (uint64_t)S.res.d_outs.p;
   auto seg_raw = [](uint64_t ptr, uint64_t off, uint64_t len) {
@@ -1051,8 +869,8 @@ uint64_t ingest(cg_group* g, const cg_request_batch* bt) {
     ChainJob j;
     std::memset(&j, 0, sizeof j);
     j.seg[0] = seg_raw(A + head, 0, L.lenH);
-    j.seg[1] = seg_f64(IN + 8 * u * k, L.lenH, 8 * u);
-    j.seg[2] = seg_raw(A + L.t, L.lenH + 8 * u, L.lenT);
+    j.seg[1] = seg_f64(L.miss ? MIS + 8 * L.moff : IN + 8 * u * k, L.lenH, 8 * L.uk);
+    j.seg[2] = seg_raw(A + L.t, L.lenH + 8 * L.uk, L.lenT);
     j.seg[3] = seg_raw(A + res_off[(size_t)k * N + p], L.P, lenRes);
     j.seg[4] = seg_f64(OUT + 8 * v * ((uint64_t)p * B + k), L.P + lenRes, 8 * v);
     j.seg[5] = seg_raw(A + dig_off[(size_t)k * N + p], L.P + lenRes + 8 * v, 32);
@@ -1062,7 +880,8 @@ uint64_t ingest(cg_group* g, const cg_request_batch* bt) {
     j.blk_end = (j.total_len + 9 + 63) / 64;
     return j;
   };
-  // [0, B): request midstates
+  // [0, B): request midstates (a misfit's slot is a no-op: its R leaves are
+  // whole missing_result_leaf chains, below)
   for (uint32_t k = 0; k < B; k++) {
     const ReqLayout& L = rl[k];
     ChainJob j;
@@ -1074,8 +893,30 @@ uint64_t ingest(cg_group* g, const cg_request_batch* bt) {
     j.total_len = L.P;
     j.blk_end = L.P / 64;
     j.state_out = (uint64_t)(S.d_mid.p + 8 * k);
+    if (L.miss) j.skip_flag = (uint64_t)S.d_neg1.p;
     jobs.push_back(j);
   }
+  // missing_result_leaf H(0x00||0x4D||request) of each misfit request: every
+  // local provider's R tree holds it at the request's position
+  if (any_miss)
+    for (uint32_t k = 0; k < B; k++) {
+      const ReqLayout& L = rl[k];
+      if (!L.miss) continue;
+      for (uint32_t li = 0; li < (uint32_t)g->models.size(); li++) {
+        const uint32_t p = g->dist ? g->rank : li;
+        ChainJob j;
+        std::memset(&j, 0, sizeof j);
+        j.seg[0] = seg_raw(A + L.h4d, 0, L.lenH);
+        j.seg[1] = seg_f64(MIS + 8 * L.moff, L.lenH, 8 * L.uk);
+        j.seg[2] = seg_raw(A + L.t, L.lenH + 8 * L.uk, L.lenT);
+        j.nseg = 3;
+        j.final_ = 1;
+        j.total_len = L.P;
+        j.blk_end = (L.P + 9 + 63) / 64;
+        j.digest_out = (uint64_t)(S.res.d_leaf.p + 32 * ((uint64_t)p * B + k));
+        jobs.push_back(j);
+      }
+    }
   // PerturbingExecutor seeds: per (local provider, request) the midstate
   // over the whole blocks of u64 p || weights digest || f64_list(input)
   // (model.cpp:87-90), chained here with the request midstates (same launch)
@@ -1106,6 +947,7 @@ uint64_t ingest(cg_group* g, const cg_request_batch* bt) {
       j.blk_begin = rl[k].P / 64;
       j.state_in = j.blk_begin ? (uint64_t)(S.d_mid.p + 8 * k) : 0;
       j.digest_out = (uint64_t)(S.res.d_leaf.p + 32 * ((uint64_t)p * B + k));
+      if (rl[k].miss) j.skip_flag = (uint64_t)S.d_neg1.p;  // written at ingest (0x4D)
       jobs.push_back(j);
     }
   // single attestation leaves H(0x00||0x53||req||res) (messages.cpp:283-290):
@@ -1118,8 +960,8 @@ uint64_t ingest(cg_group* g, const cg_request_batch* bt) {
     ChainJob j;
     std::memset(&j, 0, sizeof j);
     j.seg[0] = seg_raw(A + L.h53, 0, L.lenH);
-    j.seg[1] = seg_f64(IN + 8 * u * k, L.lenH, 8 * u);
-    j.seg[2] = seg_raw(A + L.t, L.lenH + 8 * u, L.lenT);
+    j.seg[1] = seg_f64(L.miss ? MIS + 8 * L.moff : IN + 8 * u * k, L.lenH, 8 * L.uk);
+    j.seg[2] = seg_raw(A + L.t, L.lenH + 8 * L.uk, L.lenT);
     j.nseg = 3;
     j.total_len = L.P;
     j.blk_end = L.P / 64;
@@ -1153,6 +995,8 @@ uint64_t ingest(cg_group* g, const cg_request_batch* bt) {
   CG_CUDA(cudaMemcpyAsync(S.d_eps.p, S.h_eps.p, 8 * (size_t)B, cudaMemcpyHostToDevice, st));
   CG_CUDA(cudaMemcpyAsync(S.d_reqids.p, S.h_reqids.p, 32 * (size_t)B, cudaMemcpyHostToDevice, st));
   CG_CUDA(cudaMemcpyAsync(S.d_tree.p, S.h_tree.p, 16 * (size_t)N, cudaMemcpyHostToDevice, st));
+  if (any_miss)
+    CG_CUDA(cudaMemcpyAsync(S.d_miss.p, S.h_miss.p, B, cudaMemcpyHostToDevice, st));
   if (!bt->inputs_on_device)
     CG_CUDA(cudaMemcpyAsync(S.d_in.p, bt->inputs, 8 * u * B, cudaMemcpyHostToDevice, st));
   CG_CUDA(cudaEventRecord(S.ev_staged, st));
@@ -1290,6 +1134,11 @@ void certify(cg_group* g, uint64_t ticket, const double* precomputed_outputs) {
   launch_select_quorum(R.d_outs.p, (uint64_t)B * v, v, nullptr, S.d_eps.p, B, N, g->f,
                        (uint32_t)v, g->metric, R.d_sel.p, R.d_diam.p, R.d_sat.p, R.d_status.p,
                        R.d_label.p, tl);
+  // misfits: no provider has an output, so try_attest never runs
+  // select_quorum for them (fewer than N-f outputs, coordinator.cpp:759-768)
+  if (S.any_miss)
+    launch_mark_missing(S.d_miss.p, B, R.d_sel.p, R.d_diam.p, R.d_sat.p, R.d_status.p,
+                        R.d_label.p, tl);
   launch_attest_manifest(B, N, R.d_sel.p, R.d_sat.p, R.d_rroots.p, S.d_reqids.p, g->d_gid.p, gl,
                          g->version, R.d_aleaf.p, R.d_single_pos.p, R.d_need53.p, R.d_kinds.p,
                          R.d_mnodes.p, R.d_mops.p, R.d_count.p, tl);
@@ -1311,7 +1160,7 @@ void certify(cg_group* g, uint64_t ticket, const double* precomputed_outputs) {
   g->last_B = B;
 }
 
-void certify_fetch(cg_group* g, cg_certify_out* o, const IngestSlot* slot = nullptr) {
+void certify_fetch(cg_group* g, cg_certify_out* o, const IngestSlot* slot) {
   cudaStream_t st = g->ctx->stream;
   if (!slot) slot = g->last;
   if (!slot || !slot->certified) throw InvalidArgument("nothing certified yet");
@@ -1455,7 +1304,7 @@ int create_group(cg_ctx* ctx, cg_model* const* models, uint32_t nlocal, uint32_t
   });
 }
 
-}  // namespace
+}  // namespace cg
 
 extern "C" {
 

@@ -19,6 +19,8 @@ them. Fixture contents:
                    tight epsilon -> failures)
 * c1_full.npz    — the same at SURVEY §8(d)'s C1 shape (3072 -> 10 softmax,
                    3 models, batch 64, seed 7), every-5th-request fault
+* c1_misfit.npz  — a batch with two wrong-input-dimension requests
+                   (missing_result_leaf, unsatisfied, failure leaves)
 * perturb.npz    — PerturbingExecutor(ToyExecutor, node, magnitude) outputs
                    over generate_group models with u in {1, 9, 3072} (0, 1
                    and 384 shared SHA blocks; 1- and 2-block lane tails), a
@@ -218,6 +220,44 @@ def c1_full_fixture(R):
     np.savez_compressed(os.path.join(OUT, "c1_full.npz"), **save)
 
 
+def c1_misfit_fixture(R):
+    """A C1-model batch (u=512) with two misfit requests (input dims 500 and
+    513): execute_batch skips them (engine.cpp:286-291), so every R tree has
+    missing_result_leaf there and try_attest leaves them unsatisfied."""
+    u, v, N, B, eps = 512, 10, 3, 12, 0.05
+    gid = b"group-0"
+    files, digs = R.generate_group(gid, u, v, N, 0, eps, seed=7, softmax=False)
+    inputs, encs = R.make_requests(1, 9, B, u, gid)
+    rng = np.random.default_rng(13)
+    misfit = {4: 500, 9: 513}
+    dims = np.full(B, u, np.uint64)
+    rows = [inputs[k] for k in range(B)]
+    for k, d in misfit.items():
+        rows[k] = rng.uniform(-1, 1, d)
+        dims[k] = d
+        encs[k] = R.make_request(1, bytes(rng.integers(0, 256, 16, dtype=np.uint8)), gid, rows[k])
+    outs = np.zeros((N, B, v))
+    fit = [k for k in range(B) if k not in misfit]
+    for p in range(N):
+        outs[p, fit] = R.linear_run(files[p], np.stack([rows[k] for k in fit]), v)
+    miss = np.array([k in misfit for k in range(B)], np.uint8)
+    h = R.batch_new(encs, 1)
+    r = R.certify_batch(h, N, 1, 0, eps, outs, 1, digs, threads=1, missing=miss)
+    r4 = R.certify_batch(h, N, 1, 0, eps, outs, 1, digs, threads=4, missing=miss)
+    assert r["a_root"] == r4["a_root"] and r["r_roots"] == r4["r_roots"]
+    R.batch_free(h)
+    save = dict(u=u, v=v, N=N, B=B, eps=eps, gid=np.frombuffer(gid, np.uint8), dims=dims,
+                missing=miss, files=np.stack([np.frombuffer(f_, np.uint8) for f_ in files]),
+                digests=np.stack([np.frombuffer(d, np.uint8) for d in digs]),
+                req_lens=np.array([len(e) for e in encs], np.uint64),
+                reqs=np.frombuffer(b"".join(encs), np.uint8), outputs=outs,
+                sel=r["sel_mask"], diam=r["diameter"], sat=r["satisfied"], label=r["label"],
+                r_roots=np.frombuffer(b"".join(r["r_roots"]), np.uint8).reshape(N, 32),
+                a_root=np.frombuffer(r["a_root"], np.uint8),
+                mlen=np.array(r["manifest_len"], np.uint64))
+    np.savez_compressed(os.path.join(OUT, "c1_misfit.npz"), **save)
+
+
 # (u, v, softmax, node, magnitude, seed)
 PERTURB_CASES = [(1, 3, False, 0, 0.25, 11), (9, 5, False, 3, 1e-3, 12),
                  (3072, 10, False, 1, 0.05, 7), (3072, 10, True, 2, 1e-4, 7),
@@ -251,11 +291,15 @@ if __name__ == "__main__":
     if sys.argv[1:] == ["c1_full"]:
         c1_full_fixture(R)
         sys.exit(0)
+    if sys.argv[1:] == ["c1_misfit"]:
+        c1_misfit_fixture(R)
+        sys.exit(0)
     sha_fixture(R)
     merkle_fixture(R)
     quorum_fixture(R)
     c1_fixture(R)
     c1_full_fixture(R)
+    c1_misfit_fixture(R)
     perturb_fixture(R)
     for f in sorted(os.listdir(OUT)):
         if f.endswith(".npz"):

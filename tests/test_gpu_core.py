@@ -208,6 +208,29 @@ def test_certify_c1_full_shape(ctx, oracle):
     grp.free()
 
 
+def test_certify_misfit_requests(ctx):
+    """Requests whose input dimension differs from the group's: skipped by
+    execute_batch (engine.cpp:286-291), so missing_result_leaf (0x4D) in every
+    R tree, unsatisfied, failure leaves -- bit-exact against the compiled
+    reference (c1_misfit.npz), through the whole GPU certify path."""
+    from paper_2205_15757_b200 import RequestBatch
+    g = golden("c1_misfit.npz")
+    B = int(g["B"])
+    grp = _group(ctx, g, B)
+    batch = RequestBatch.from_encoded(split_reqs(g))
+    assert isinstance(batch.inputs, list)
+    r = grp.certify(batch, want_outputs=True)
+    fit = ~g["missing"].astype(bool)
+    assert np.array_equal(r["outputs"][:, fit], g["outputs"][:, fit])
+    assert np.array_equal(r["selected"], g["sel"].astype(np.uint32))
+    assert np.array_equal(r["satisfied"], g["sat"].astype(bool))
+    assert np.array_equal(r["label"][~fit], [-1, -1])
+    assert np.array_equal(r["r_roots"], g["r_roots"])
+    assert int(r["manifest_len"][0]) == int(g["mlen"])
+    assert np.array_equal(r["a_root"], g["a_root"])
+    grp.free()
+
+
 @pytest.mark.parametrize("variant", ["honest", "partial_fault", "failure"])
 def test_certify_outputs_fault_variants(ctx, variant):
     from paper_2205_15757_b200 import RequestBatch

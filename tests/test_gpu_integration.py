@@ -21,3 +21,30 @@ def test_reference_engine_with_cuda_executor():
     print(out.stdout, out.stderr)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "0 mismatches" in out.stdout
+
+
+CNN_DEMO = os.path.join(ROOT, "oracle", "_ref", "integration_cnn")
+
+
+def test_reference_requests_certified_on_every_gpu(tmp_path):
+    """The headline path as a drop-in: a C++ program linking the UNMODIFIED
+    reference builds a ModelGroup of 3 ResNet-50 descriptors (params["arch"],
+    files fetched by the reference's filesystem_fetcher), signs requests with
+    make_signed_request, checks them with verify_request, and certifies them
+    through GroupServer (load_group -> batch former -> dispatch) on every
+    visible GPU from ONE process; the certificates must be identical across
+    GPUs and equal to the reference's own recomputation from the GPU outputs."""
+    import torch
+    if not os.path.exists(CNN_DEMO):
+        pytest.skip("oracle/_ref/integration_cnn not built (needs /root/reference at build time)")
+    from paper_2205_15757_b200.workload import resnet_group
+    files, digs, _ = resnet_group("resnet50", replicas=3, seed=0, jitter=5e-3)
+    for p, f in enumerate(files):
+        (tmp_path / f"m{p}.bin").write_bytes(f)
+        (tmp_path / f"m{p}.arch").write_text("resnet50\n")
+    ndev = min(2, torch.cuda.device_count())
+    out = subprocess.run([CNN_DEMO, str(tmp_path), "3", "8"] + [str(d) for d in range(ndev)],
+                         capture_output=True, text=True, timeout=900)
+    print(out.stdout, out.stderr)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert f"{ndev} device(s)" in out.stdout and " 0 mismatches" in out.stdout

@@ -228,6 +228,51 @@ def test_adversarial_oracle_vs_reference(oracle, n, f, v, metric):
                     R.ensemble_label(outs[k][idx], want[0], f)
 
 
+def test_c1_misfit_golden(oracle):
+    """Misfit requests (wrong input dimension): missing_result_leaf in every
+    R tree, unsatisfied, a failure leaf -- the oracle restatement against the
+    reference's answers (c1_misfit.npz)."""
+    from oracle.oracle import parse_request
+    g = golden("c1_misfit.npz")
+    N, B, eps = int(g["N"]), int(g["B"]), float(g["eps"])
+    gid = g["gid"].tobytes()
+    reqs = split_reqs(g)
+    miss = g["missing"].astype(bool)
+    sels, sats, leaves = [], [], {}
+    for k in range(B):
+        if miss[k]:
+            m, d, sat = 0, 0.0, False
+        else:
+            m, d, sat = oracle.select_quorum(g["outputs"][:, k], list(range(N)), N, 1, 0, eps)
+        assert (m, sat) == (int(g["sel"][k]), bool(g["sat"][k]))
+        sels.append(m)
+        sats.append(sat)
+    for p in range(N):
+        hs = []
+        for k in range(B):
+            f = parse_request(reqs[k])
+            assert len(f["input"]) == int(g["dims"][k])
+            if miss[k]:
+                hs.append(oracle.tagged_leaf_hash(0x4D, reqs[k], b""))
+            else:
+                res = oracle.result_encode(f["request_id"], p, gid, 1, g["outputs"][p, k],
+                                           g["digests"][p].tobytes())
+                leaves[(k, p)] = res
+                hs.append(oracle.tagged_leaf_hash(0x52, reqs[k], res))
+        assert oracle.merkle_root(hs) == g["r_roots"][p].tobytes()
+    man = oracle.attest_manifest(sels, sats, N)
+    assert len(man) == int(g["mlen"])
+    a = []
+    for kind, node, op in man:
+        if kind == 1:
+            a.append(oracle.tagged_leaf_hash(0x53, reqs[op], leaves[(op, node)]))
+        else:
+            assert kind == 2
+            rid = parse_request(reqs[op])["request_id"]
+            a.append(oracle.leaf_hash(oracle.failure_leaf(rid, gid, 1)))
+    assert oracle.merkle_root(a) == g["a_root"].tobytes()
+
+
 def test_label_digest_layout(oracle):
     """The compact agreed-label digest (new, C5 'D2') is plain SHA-256 over
     0x4C || id || u64be version || u64be label; pinned by the SHA KATs."""

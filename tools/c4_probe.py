@@ -4,8 +4,11 @@ for one version and then both live versions. Memory after each phase.
 
     python tools/c4_probe.py [replicas] [batch] [steps]
 """
+import faulthandler
 import sys
 import time
+
+faulthandler.dump_traceback_later(600, exit=True)
 
 sys.path.insert(0, ".")
 import numpy as np  # noqa: E402
