@@ -24,6 +24,7 @@ are exchanged with one NCCL all-gather per batch (cg_group_create_dist).
 from __future__ import annotations
 
 import argparse
+import copy
 import json
 import os
 import subprocess
@@ -160,20 +161,22 @@ def replica_f(world):
     return (world - 1) // 2  # quorum of a strict majority
 
 
-def make_dist_group(ctx, B, rank, world, seed=0, eps=0.1):
-    """Replica-parallel group: rank serves one replica of a world-replica
-    group; NCCL communicator from rank 0's unique id."""
+def make_dist_group(ctx, B, rank, world, seed=0, eps=0.1, N=None):
+    """Replica-parallel group of N (default: world) replicas: rank serves
+    assigned_models(world, N, rank) (domain.cpp:247-268: one replica per GPU
+    when N == world, contiguous chunks otherwise); NCCL communicator from
+    rank 0's unique id."""
     from paper_2205_15757_b200 import EUCLIDEAN, Context, Model, ModelGroup
     from paper_2205_15757_b200.dist import assigned_models, share_bytes
     from paper_2205_15757_b200.workload import resnet_group
-    files, digs, sds = resnet_group("resnet50", replicas=world, seed=seed, jitter=5e-3)
+    N = N or world
+    files, digs, sds = resnet_group("resnet50", replicas=N, seed=seed, jitter=5e-3)
     uid = share_bytes(Context.nccl_unique_id() if rank == 0 else None)
     ctx.init_nccl(uid, world, rank)
-    (p,) = assigned_models(world, world, rank)
-    m = Model.load_cnn(ctx, files[p], digs[p])
-    grp = ModelGroup.create_dist(ctx, m, digs, replica_f(world), EUCLIDEAN, eps, b"group-0",
+    ms = [Model.load_cnn(ctx, files[p], digs[p]) for p in assigned_models(world, N, rank)]
+    grp = ModelGroup.create_dist(ctx, ms, digs, replica_f(N), EUCLIDEAN, eps, b"group-0",
                                  1, max_batch=B, topk=5)
-    return grp, [m], files, digs, sds
+    return grp, ms, files, digs, sds
 
 
 def pipeline(grp, ctx, batches, K, D, lag, stream=None):
@@ -248,7 +251,8 @@ def bench_gpu(args, rank, world, local_rank):
     B = args.batch
     replica = args.mode == "replica"
     if replica:
-        grp, models, files, digs, sds = make_dist_group(ctx, B, rank, world)
+        grp, models, files, digs, sds = make_dist_group(ctx, B, rank, world,
+                                                        N=max(world, args.replicas_dist))
     elif args.workload == "c3":
         grp, models, files, digs, sds = make_hetero_group(ctx, B)
     else:
@@ -495,10 +499,11 @@ def bench_gpu(args, rank, world, local_rank):
     if replica:
         out["scaling"] = "strong"
         out["config"].update(
-            workload=f"{world}-replica ResNet-50 group, one replica per GPU, f={replica_f(world)}, "
-                     f"batch {B}, 224x224; outputs + R roots all-gathered over NCCL",
-            replicas=world, f=replica_f(world), global_batch=B,
-            parallelism=f"replica-parallel x{world} (rank = provider)")
+            workload=f"{grp.N}-replica ResNet-50 group, {grp.N // world} replica(s) per GPU, "
+                     f"f={replica_f(grp.N)}, batch {B}, 224x224; outputs + R roots "
+                     "all-gathered over NCCL",
+            replicas=grp.N, f=replica_f(grp.N), global_batch=B,
+            parallelism=f"replica-parallel x{world} (rank = provider chunk, assigned_models)")
     if world == 1 and not args.no_cpu_baseline:  # the CPU baseline is timed at N=1 only
         archs = [m.arch for m in models] if args.workload == "c3" else ["resnet50"] * 3
         out["cpu_baseline"] = cpu_baseline(archs, digs, sds, batches[0], args,
@@ -618,14 +623,25 @@ def cpu_baseline(archs, digs, sds, batch, args, eps=0.1):
 
 # ------------------------------------------------------------ C4 update
 def bench_c4(args, rank, world, local_rank):
-    """C4 (BASELINE.json configs[3]): an N-replica ResNet-50 group, one model
-    owner per GPU (rank = provider, replica outputs + R roots all-gathered
-    over NCCL; on one GPU the N replicas are time-sliced), f = (N-1)//3,
-    batch 512, with a model-version update mid-stream: in the middle third
-    of the timed steps both versions are live, so every batch is certified
-    under v1 and v2 (engine.cpp:196-206: one batch per live version); the
-    host-side version fold (state.cpp:23-45) keeps one certificate per
-    request, so a request counts once."""
+    """C4 (BASELINE.json configs[3]): an N-replica ResNet-50 group, f =
+    (N-1)//3, batch 512, with a concurrent model-version update mid-stream.
+    One GPU: the N (default 8) replicas time-sliced on it; N GPUs: one model
+    owner per GPU (rank = provider, outputs + R roots all-gathered over NCCL).
+
+    Inside the timed region:
+      * v1 serves alone;
+      * at step K//3 a background thread loads v2 -- every replica file's
+        SHA-256 check (load_group, engine.cpp:79), parse + BN fold, upload --
+        and creates its group while v1 keeps certifying (v2 = a new jitter
+        salt, harness.cpp:601-602);
+      * once v2 is resident (the same step on every rank) each batch is
+        ingested and certified under BOTH live versions (engine.cpp:196-206);
+      * v1 retires at step 2K//3 (or D+1 steps after v2 went live, if later);
+    a request counts once if satisfied under at least one version (the
+    host-side version fold, state.cpp:23-45). Every batch's decisions are
+    read back inside the region; the region ends when all work is drained."""
+    import threading
+
     import torch
     import torch.distributed as dist
     from collections import deque
@@ -640,47 +656,65 @@ def bench_c4(args, rank, world, local_rank):
     B, N = args.batch, (world if world > 1 else args.replicas)
     f = (N - 1) // 3
     eps = 0.1
+    gloo = None
     if world > 1:
         uid = share_bytes(Context.nccl_unique_id() if rank == 0 else None)
         ctx.init_nccl(uid, world, rank)
-    groups, keep = [], []
-    for version, salt in ((1, 0), (2, 1000)):  # v2: a new jitter salt (harness.cpp:601-602)
-        files, digs, _ = resnet_group("resnet50", replicas=N, seed=0, jitter=5e-3, salt=salt)
+        gloo = dist.new_group(backend="gloo")
+    files = {}
+    for version, salt in ((1, 0), (2, 1000)):  # model files on disk: setup, untimed
+        fl, dg, _ = resnet_group("resnet50", replicas=N, seed=0, jitter=5e-3, salt=salt)
+        files[version] = (fl, dg)
+
+    def load(version):
+        fl, dg = files[version]
         if world > 1:
             (p,) = assigned_models(world, N, rank)
-            ms = [Model.load_cnn(ctx, files[p], digs[p])]
-            g = ModelGroup.create_dist(ctx, ms[0], digs, f, EUCLIDEAN, eps, b"group-0", version,
+            ms = [Model.load_cnn(ctx, fl[p], dg[p])]
+            g = ModelGroup.create_dist(ctx, ms[0], dg, f, EUCLIDEAN, eps, b"group-0", version,
                                        max_batch=B, topk=5)
         else:
-            ms = [Model.load_cnn(ctx, fl, d) for fl, d in zip(files, digs)]
+            ms = [Model.load_cnn(ctx, x, d) for x, d in zip(fl, dg)]
             g = ModelGroup(ctx, ms, f, EUCLIDEAN, eps, b"group-0", version, max_batch=B, topk=5)
-        groups.append(g)
-        keep.append(ms)
+        return g, ms
+
+    t_load0 = time.perf_counter()
+    g1, ms1 = load(1)
+    v1_load_s = time.perf_counter() - t_load0
     nb = 2
     batches = [signed_requests(B, U, seed=7 + i) for i in range(nb)]
-    from copy import copy
     dev = []
     for b in batches:
         d = torch.from_numpy(b.inputs).to(f"cuda:{local_rank}")
-        db = copy(b)
+        db = copy.copy(b)
         db.inputs, db.B, db.u = d.data_ptr(), B, U
         db._keep = d
         dev.append(db)
-    K, D = args.steps, min(args.depth, 6)
-
-    def live(i):  # versions live for timed step i (warm-up steps: v1 only)
-        if i < K // 3:
-            return [0]
-        return [0, 1] if i < 2 * K // 3 else [1]
-
-    for i in range(args.warmup):  # untimed, both versions
-        for g in groups:
-            g.certify(dev[i % nb])
+    for i in range(args.warmup):
+        g1.certify(dev[i % nb])
     torch.cuda.synchronize()
-    pend = [deque(), deque()]
-    for j in range(min(D, K)):
-        for v in live(j):
-            pend[v].append(groups[v].ingest(dev[j % nb]))
+    K, D, LAG = args.steps, min(args.depth, 6), min(args.fetch_lag, 6)
+    groups = {1: g1}
+    loaded, loader = {}, None
+    v2_live_at, v1_retired_at = None, None
+
+    def agreed(flag):  # the same decision on every rank (gloo: no GPU sync)
+        if world == 1:
+            return flag
+        t = torch.tensor([1 if flag else 0])
+        dist.all_reduce(t, op=dist.ReduceOp.MIN, group=gloo)
+        return bool(t.item())
+
+    tickets = {}  # batch -> [(version, ticket)]
+    done, sat_by_batch = deque(), {}
+
+    def ingest(j, live):
+        tickets[j] = [(v, groups[v].ingest(dev[j % nb])) for v in live]
+
+    def fetch_one():
+        j, v, t = done.popleft()
+        s_ = groups[v].fetch_ticket(t)["satisfied"].astype(bool)
+        sat_by_batch[j] = s_ if j not in sat_by_batch else (sat_by_batch[j] | s_)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -688,41 +722,214 @@ def bench_c4(args, rank, world, local_rank):
     certs = 0
     with ClockSampler(local_rank) as clk:
         e0.record(stream)
+        h0 = time.perf_counter()
+        live = [1]
+        for j in range(min(D, K)):
+            ingest(j, live)
         for i in range(K):
-            for v in live(i):
-                groups[v].certify_ticket(pend[v].popleft(), sync=False)
-            certs += len(live(i))
-            j = i + D
-            if j < K:
-                for v in live(j):
-                    pend[v].append(groups[v].ingest(dev[j % nb]))
-        ctx.join()  # the last batches' certification tails are inside the region
+            if i == K // 3:
+                def bg():
+                    t = time.perf_counter()
+                    loaded["g"] = load(2)
+                    loaded["s"] = time.perf_counter() - t
+                loader = threading.Thread(target=bg)
+                loader.start()
+            if v2_live_at is None and i > K // 3 and agreed("g" in loaded):
+                loader.join()
+                groups[2] = loaded["g"][0]
+                v2_live_at = i
+                live = [1, 2]
+            if (v2_live_at is not None and v1_retired_at is None
+                    and i >= max(2 * K // 3, v2_live_at + D + 1)):
+                v1_retired_at = i
+                live = [2]
+            for v, t in tickets.pop(i):
+                groups[v].certify_ticket(t, sync=False)
+                done.append((i, v, t))
+                certs += 1
+            if i + D < K:
+                ingest(i + D, live)
+            while len(done) > LAG * len(live):
+                fetch_one()
+        while done:
+            fetch_one()
+        ctx.join()
         e1.record(stream)
         torch.cuda.synchronize()
+        host_s = time.perf_counter() - h0
+    if loader is not None and loader.is_alive():
+        loader.join()
     ms = e0.elapsed_time(e1)
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local_rank}")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    sat = float(np.mean(groups[1].fetch()["satisfied"]))
-    value = K * B * sat / (ms / 1e3)
+    certified = int(sum(int(np.sum(s_)) for s_ in sat_by_batch.values()))
+    value = certified / (ms / 1e3)
     out = {"metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
            "steps": K, "warmup": args.warmup, "ms_per_step": round(ms / K, 3),
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
            "data": "synthetic (random-init jittered ResNet-50 replicas, v2 = new jitter salt)",
            "config": {"workload": f"C4: {N}-replica ResNet-50 group, f={f}, batch {B}, "
                                   f"{'one model owner per GPU' if world > 1 else 'time-sliced on 1 GPU'}"
-                                  ", v1 -> v2 update mid-stream (BASELINE.json configs[3])",
+                                  ", v1 -> v2 update mid-stream, v2 loaded inside the timed "
+                                  "region (BASELINE.json configs[3])",
                       "model": "resnet50", "replicas": N, "f": f, "global_batch": B,
-                      "update_window_steps": [K // 3, 2 * K // 3],
+                      "v2_load_started_step": K // 3, "v2_live_step": v2_live_at,
+                      "v1_retired_step": v1_retired_at,
+                      "v2_load_s": round(loaded.get("s", float("nan")), 2),
+                      "v1_load_s_untimed": round(v1_load_s, 2),
                       "certifications_per_request": round(certs / K, 3),
-                      "satisfied_fraction": sat,
+                      "certified_requests": certified, "requests": K * B,
+                      "host_s": round(host_s, 2),
                       "parallelism": f"replica-parallel x{world}" if world > 1 else "1 GPU",
-                      "l2": "inputs larger than L2: 2 rotating 617 MB f64 batches"},
+                      "l2": f"inputs larger than L2: 2 rotating {B * U * 8 >> 20} MB f64 batches"},
            "clocks": clk.summary()}
-    for g in groups:
+    for g in groups.values():
         g.free()
     return out
+
+
+# ------------------------------------------------------------- C1
+def bench_c1(args, rank, world, local_rank):
+    """C1 (BASELINE.json configs[0]): the reference's default group at SURVEY
+    §8(d)'s shape -- three generate_group LinearToyModels 3072 -> 10 with
+    softmax (the compiled reference's own model files, tests/golden/
+    c1_full.npz), f=1, batch 64, euclidean eps 0.05 -- through the same
+    pipelined path as C2: fp64 LinearToyModel kernel (bit-exact), softmax /
+    top-k, agreement + label, result leaves (~26 KB hashed per request), R
+    and A trees. 100 rotating batches (157 MB of inputs > L2)."""
+    import torch
+
+    from paper_2205_15757_b200 import EUCLIDEAN, Context, Model, ModelGroup
+    from paper_2205_15757_b200.workload import signed_requests
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    g = np.load(os.path.join(ROOT, "tests", "golden", "c1_full.npz"))
+    torch.cuda.set_device(local_rank)
+    ctx = Context(local_rank)
+    stream = torch.cuda.current_stream()
+    ctx.set_stream(stream.cuda_stream)
+    N, B, u = int(g["N"]), int(g["B"]), int(g["u"])
+    models = [Model.load_linear(ctx, g["files"][p].tobytes(), g["digests"][p].tobytes())
+              for p in range(N)]
+    grp = ModelGroup(ctx, models, 1, EUCLIDEAN, float(g["eps"]), g["gid"].tobytes(), 1,
+                     max_batch=B, topk=5)
+    nb = 100
+    batches = [signed_requests(B, u, seed=1000 + rank * nb + i) for i in range(nb)]
+    dev = []
+    for b in batches:
+        d = torch.from_numpy(b.inputs).to(f"cuda:{local_rank}")
+        db = copy.copy(b)
+        db.inputs, db.B, db.u = d.data_ptr(), B, u
+        db._keep = d
+        dev.append(db)
+    for i in range(args.warmup):
+        grp.certify(batches[i % nb])
+    torch.cuda.synchronize()
+    D, LAG = args.depth, args.fetch_lag
+    l0 = ctx.launch_count()
+    with ClockSampler(local_rank) as clk:
+        ms, host_ms, sats, _ = pipeline(grp, ctx, dev, args.steps, D, LAG, stream)
+    launches = round((ctx.launch_count() - l0) / args.steps)
+    sat = float(np.mean(np.concatenate(sats)))
+    value = world * args.steps * B * sat / (ms / 1e3)
+    # e2e: the batch former from pageable host inputs
+    from paper_2205_15757_b200 import InferenceEngine
+    eng = InferenceEngine(ctx, B, 10**12, pack_threads=2)
+    eng.load_group(grp)
+    prepared = [eng.prepare(b, g["gid"].tobytes()) for b in batches]
+    torch.cuda.synchronize()
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2.record(stream)
+    from collections import deque
+    ready_q, inflight, certified = deque(), deque(), 0
+    for i in range(args.steps):
+        eng.submit_prepared(prepared[i % nb], now_us=i)
+        ready_q.extend(eng.ready())
+        while len(ready_q) > D:
+            gq, _, t, Bt = ready_q.popleft()
+            gq.certify_ticket(t, sync=False, B=Bt)
+            inflight.append(t)
+        while len(inflight) > LAG:
+            certified += int(np.sum(grp.fetch_ticket(inflight.popleft())["satisfied"]))
+    while ready_q:
+        gq, _, t, Bt = ready_q.popleft()
+        gq.certify_ticket(t, sync=False, B=Bt)
+        inflight.append(t)
+    while inflight:
+        certified += int(np.sum(grp.fetch_ticket(inflight.popleft())["satisfied"]))
+    ctx.join()
+    e3.record(stream)
+    torch.cuda.synchronize()
+    e2e = world * certified / (e2.elapsed_time(e3) / 1e3)
+    eng.free()
+    # digest work per request: the shared request midstate (386 blocks) + N
+    # result-leaf tails + the A/R tree nodes, in SHA-256 blocks of 64 B
+    req_len = len(bytes(g["reqs"].tobytes())) // B
+    blocks = (req_len + 2) // 64 + N * 4 + 2 * N + 4
+    hashed = blocks * 64 * B * args.steps * sat
+    pk, pk_src = peaks()
+    out = {"metric": METRIC.replace("(ResNet-50 group)", "(C1 LinearToyModel group)"),
+           "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3),
+           "host_ms_per_step": round(host_ms, 3), "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64 (LinearToyModel, bit-exact)",
+           "data": "the compiled reference's generate_group models (seed 7, softmax); "
+                   "synthetic signed U(-1,1) requests",
+           "config": {"workload": "C1: 3 x LinearToyModel 3072->10 softmax, f=1, batch 64, "
+                                  "eps 0.05 (BASELINE.json configs[0], SURVEY §8(d))",
+                      "replicas": N, "f": 1, "batch_per_gpu": B, "satisfied_fraction": sat,
+                      "l2": "100 rotating batches, 157 MB of inputs > L2",
+                      "pipeline": f"cold start + full drain, ingest {D} ahead, read back "
+                                  f"{LAG} behind"},
+           "e2e": {"value": round(e2e, 1), "unit": UNIT, "h2d_bytes_per_step": B * u * 8,
+                   "d2h_bytes_per_step": B * 21 + N * 32 + 40,
+                   "path": "InferenceEngine.submit -> ingest -> certify -> read back"},
+           "gpu_launches": int(launches),
+           "roofline": {"bound": "latency (SHA-256 chains, one thread per chain)",
+                        "achieved": round(hashed / (ms / 1e3) / 1e9, 2),
+                        "peak": pk.get("hbm_gbs", 6650.0), "unit": "GB/s",
+                        "frac": round(hashed / (ms / 1e3) / 1e9 / pk.get("hbm_gbs", 6650.0), 5),
+                        "traffic": None,
+                        "note": "bytes hashed per second against HBM bandwidth: C1 is bound "
+                                "by the per-request SHA chain latency and launch overheads, "
+                                "not by a roofline"},
+           "clocks": clk.summary()}
+    if world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = c1_cpu_baseline(g, batches[0], args)
+    grp.free()
+    for m in models:
+        m.free()
+    return out
+
+
+def c1_cpu_baseline(g, batch, args):
+    """The compiled reference's C1 path on the host cores: LinearToyModel::run
+    per replica (ref_linear_run) + select_quorum / ensemble_label / leaves /
+    trees (ref_certify_batch); all cores, a bounded sample."""
+    from oracle.oracle import Reference
+    from paper_2205_15757_b200.workload import encode_request
+    if not Reference.available():
+        return {"value": None, "kind": "port", "sample": "oracle/_ref not built"}
+    R = Reference()
+    threads = os.cpu_count() or 1
+    N, v = int(g["N"]), int(g["v"])
+    gid = g["gid"].tobytes()
+    encs = [encode_request(batch, k, gid) for k in range(len(batch.nonces))]
+    digs = [g["digests"][p].tobytes() for p in range(N)]
+    h = R.batch_new(encs, 1)
+    reps = 0
+    t = time.perf_counter()
+    while time.perf_counter() - t < 5.0:
+        outs = np.stack([R.linear_run(g["files"][p].tobytes(), batch.inputs, v) for p in range(N)])
+        R.certify_batch(h, N, 1, 0, float(g["eps"]), outs, 1, digs, threads=threads)
+        reps += 1
+    dt = time.perf_counter() - t
+    R.batch_free(h)
+    return {"value": round(reps * len(encs) / dt, 1), "unit": UNIT, "cores": threads,
+            "kind": "reference",
+            "sample": f"{reps} batches x {len(encs)} requests, LinearToyModel::run x {N} "
+                      f"(single thread) + certify_batch ({threads} threads), {dt:.1f} s"}
 
 
 # ------------------------------------------------------------- C5 sweep
@@ -866,6 +1073,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--depth", type=int, default=12,
                     help="batches ingested ahead of certification (ring holds 24)")
+    ap.add_argument("--replicas-dist", type=int, default=0,
+                    help="--mode replica: group size (default = number of GPUs; a multiple "
+                         "of it gives several replicas per rank)")
     ap.add_argument("--fetch-lag", type=int, default=8,
                     help="steps between certifying a batch and reading its results back")
     ap.add_argument("--pack-threads", type=int, default=8,
@@ -875,7 +1085,7 @@ def main():
     ap.add_argument("--mode", default="group", choices=["group", "replica"],
                     help="group: a whole 3-replica group per GPU (weak scaling); "
                          "replica: one replica per GPU, NCCL all-gather (N>1)")
-    ap.add_argument("--workload", default="c2", choices=["c2", "c3", "c4", "c5"],
+    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5"],
                     help="c2: the headline certified-request pipeline (3x ResNet-50); "
                          "c3: the heterogeneous 4-replica group; c5: agreement + "
                          "label-digest sweep (one line per --c5 spec)")
@@ -892,7 +1102,7 @@ def main():
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.batch is None:
-        args.batch = 512 if args.workload == "c4" else 128
+        args.batch = {"c4": 512, "c1": 64}.get(args.workload, 128)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
@@ -918,6 +1128,8 @@ def main():
         out = bench_reference(args, rank, world)
     elif args.workload == "c4":
         out = bench_c4(args, rank, world, local_rank)
+    elif args.workload == "c1":
+        out = bench_c1(args, rank, world, local_rank)
     elif args.workload == "c5":
         for line in bench_c5(args, local_rank):
             emit(line)

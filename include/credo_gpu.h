@@ -209,7 +209,25 @@ typedef struct {
    * read from misfit_inputs[k] (host); row k of `inputs` is ignored. */
   const uint64_t* input_dims;
   const double* const* misfit_inputs;
+  /* Optional slot structure: the batch as a PRE-PREPARE's op list
+   * (include/credo/messages.hpp:106-118). op_kinds[k] (NULL: every op an ok
+   * request) = CG_OP_REQUEST, CG_OP_REQUEST_REJECTED (status rejected: no
+   * result, R leaf missing_result_leaf, no outcome, A leaf = its failure
+   * record) or CG_OP_GROUP (a define/activate/retire op: R leaf
+   * group_op_leaf 0x47 || op_entries[k], no outcome, an A leaf only if
+   * rejected). op_entries: the group ops' OpEntry::encode bytes back to back
+   * (op_entry_lens[k], 0 for requests); fail_records: FailureRecord::encode
+   * of failure_record_for(op) (messages.cpp:299-312) for every rejected op
+   * (fail_record_lens[k], 0 otherwise). A group op's request fields are
+   * ignored (zeros, nonce length 0). */
+  const uint8_t* op_kinds;
+  const uint8_t* op_entries;
+  const uint64_t* op_entry_lens;
+  const uint8_t* fail_records;
+  const uint64_t* fail_record_lens;
 } cg_request_batch;
+
+enum { CG_OP_REQUEST = 0, CG_OP_REQUEST_REJECTED = 1, CG_OP_GROUP = 2 };
 
 /* Host-memory results. Optional arrays may be NULL. */
 typedef struct {
@@ -255,6 +273,12 @@ int cg_certify_ticket(cg_group* g, uint64_t ticket, cg_certify_out* out);
  * point (a corrupt replica is just a shifted output row). */
 int cg_certify_outputs(cg_group* g, const cg_request_batch* batch,
                        const double* outputs, cg_certify_out* out);
+/* An empty filler slot (build_result_tree with no ops, messages.cpp:240-243):
+ * every provider's R tree is the single noop_leaf H(0x00||0x4E||u64 view||
+ * u64 seq); with no outcomes every provider is whole-batch attested
+ * (coordinator.cpp:776-787), so the A tree is N whole-batch leaves. Fills
+ * out->r_roots, a_root, manifest_len / kind / node / op, a_leaf_hashes. */
+int cg_certify_empty_slot(cg_group* g, uint64_t view, uint64_t seq, cg_certify_out* out);
 
 /* verify_request's digests for a batch (domain.cpp:177-216, :238-241):
  * signing_digests[k] = InferenceRequest::signing_digest() = SHA-256(0x01 ||
@@ -384,6 +408,15 @@ int cg_group_create_dist(cg_ctx* ctx, cg_model* my_model, const uint8_t* all_dig
                          uint32_t f, uint32_t metric, double default_eps,
                          const char* group_id, uint64_t group_id_len, uint64_t version,
                          uint32_t max_batch, uint32_t topk, cg_group** out);
+/* k = nlocal replicas per rank (assigned_models chunking): rank r serves
+ * providers [r k, (r + 1) k), my_models in that order; N = k x nranks. The
+ * local replicas of one architecture run as grouped launches; the
+ * all-gather moves k providers' outputs and R roots per rank. */
+int cg_group_create_dist_multi(cg_ctx* ctx, cg_model* const* my_models, uint32_t nlocal,
+                               const uint8_t* all_digests, uint32_t f, uint32_t metric,
+                               double default_eps, const char* group_id, uint64_t group_id_len,
+                               uint64_t version, uint32_t max_batch, uint32_t topk,
+                               cg_group** out);
 
 /* ---- measurement hooks ----------------------------------------------------
  * Per-kernel-class device time from CUDA events recorded on each launching

@@ -373,6 +373,35 @@ class Reference:
                                    rs, out) == 0
         return out.raw
 
+    def certify_slot(self, encs, kinds, reasons, N, f, eps, outputs, version, digests):
+        """A mixed PRE-PREPARE op list (ok / rejected requests, activate_group
+        ops) through build_result_tree + the try_attest manifest; returns the
+        roots, manifest length, satisfied flags, every op's OpEntry encoding
+        and the rejected ops' FailureRecord encodings."""
+        B = len(kinds)
+        lens = np.array([len(e) for e in encs], np.uint64)
+        k8 = np.ascontiguousarray(kinds, np.uint8)
+        rs = (C.c_char_p * B)(*[r.encode() for r in reasons])
+        o = np.ascontiguousarray(outputs, np.float64)
+        cap = 1 << 21
+        ent = np.zeros(B * cap, np.uint8)
+        rec = np.zeros(B * cap, np.uint8)
+        el = np.zeros(B, np.uint64)
+        rl = np.zeros(B, np.uint64)
+        rr = C.create_string_buffer(32 * N)
+        ar = C.create_string_buffer(32)
+        ml = u64()
+        sat = np.zeros(B, np.uint8)
+        rc = self.L.ref_certify_slot(b"".join(encs) or b"\0", _p(lens), u64(B), _p(k8), rs, u64(N),
+                                     u64(f), dbl(eps), _p(o), u64(o.shape[2]), u64(version),
+                                     b"".join(digests), rr, ar, C.byref(ml), _p(sat), _p(ent),
+                                     _p(el), _p(rec), _p(rl), u64(cap))
+        assert rc == 0, rc
+        return dict(r_roots=[rr.raw[32 * i:32 * i + 32] for i in range(N)], a_root=ar.raw,
+                    manifest_len=ml.value, satisfied=sat,
+                    entries=[ent[k * cap:k * cap + int(el[k])].tobytes() for k in range(B)],
+                    records=[rec[k * cap:k * cap + int(rl[k])].tobytes() for k in range(B)])
+
     def signing_digest(self, enc: bytes) -> bytes:
         out = C.create_string_buffer(32)
         assert self.L.ref_signing_digest(enc, u64(len(enc)), out) == 0

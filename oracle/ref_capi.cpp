@@ -623,4 +623,145 @@ int ref_certify_batch(void* h, uint64_t N, uint64_t f, uint32_t metric, double e
                               a_root, manifest_len, nullptr);
 }
 
+// A mixed PRE-PREPARE op list through the reference: build_result_tree
+// (messages.cpp:235-258) per provider and the try_attest manifest
+// (coordinator.cpp:735-849, restated above in ref_certify_batch_ex with
+// outcomes only for ok request ops) + attest_leaf_bytes. ops: kinds[k] 0 ok
+// request (the next encoding), 1 rejected request (next encoding, status
+// rejected, reasons[k]), 2 group op (an activate_group op signed here,
+// status ok, or rejected when reasons[k] is non-empty). outputs: N x B x v
+// provider-major; rows of non-ok ops are ignored. Writes every op's
+// OpEntry::encode (entries, entry_lens) and, for rejected ops, the
+// FailureRecord::encode (recs, rec_lens), so the GPU path can be fed the
+// same bytes; caps are per-op byte capacities.
+int ref_certify_slot(const uint8_t* enc, const uint64_t* lens, uint64_t B, const uint8_t* kinds,
+                     const char* const* reasons, uint64_t N, uint64_t f, double eps_default,
+                     const double* outputs, uint64_t v, uint64_t version,
+                     const uint8_t* model_digests, uint8_t* r_roots, uint8_t* a_root,
+                     uint64_t* manifest_len, uint8_t* sat_out, uint8_t* entries,
+                     uint64_t* entry_lens, uint8_t* recs, uint64_t* rec_lens, uint64_t cap) {
+  try {
+    std::vector<OpEntry> ops(B);
+    KeyPair owner = KeyPair::from_seed(std::array<uint8_t, 32>{42});
+    uint64_t off = 0;
+    std::string gid;
+    for (uint64_t k = 0; k < B; k++) {
+      OpEntry& op = ops[k];
+      op.version = version;
+      if (kinds[k] <= 1) {
+        Decoder d(ByteView(enc + off, lens[k]));
+        op.kind = OpKind::request_inf;
+        op.request = InferenceRequest::decode(d);
+        gid = op.request->group_id;
+        op.status = kinds[k] == 1 ? OpStatus::rejected : OpStatus::ok;
+        if (kinds[k] == 1) op.reason = reasons[k];
+      } else {
+        Encoder ne;
+        ne.u64(k);
+        op.kind = OpKind::activate_group;
+        op.group_op = make_signed_group_op(owner, ne.take(), OpKind::activate_group, "group-1",
+                                           std::nullopt);
+        if (reasons[k][0]) {
+          op.status = OpStatus::rejected;
+          op.reason = reasons[k];
+        }
+      }
+      off += lens[k];
+    }
+    // per provider results for the ok request ops
+    std::vector<std::map<uint64_t, InferenceResult>> results(N);
+    std::map<uint64_t, std::map<uint64_t, InferenceResult>> by_op;
+    std::map<uint64_t, distance::AgreementOutcome> outc;
+    for (uint64_t k = 0; k < B; k++) {
+      if (ops[k].kind != OpKind::request_inf || ops[k].status != OpStatus::ok) continue;
+      std::map<uint64_t, std::vector<double>> outs;
+      for (uint64_t p = 0; p < N; p++) {
+        InferenceResult r;
+        r.request_id = ops[k].request->request_id;
+        r.node_index = p;
+        r.group_id = ops[k].request->group_id;
+        r.group_version = version;
+        const double* o = outputs + (p * B + k) * v;
+        r.output.assign(o, o + v);
+        r.model_digest = to_h32(model_digests + 32 * p);
+        results[p][k] = r;
+        by_op[k][p] = r;
+        outs[p] = r.output;
+      }
+      double eps = ops[k].request->epsilon_override ? *ops[k].request->epsilon_override
+                                                    : eps_default;
+      outc[k] = distance::select_quorum(outs, N, f, distance::Metric::euclidean, eps);
+    }
+    std::map<uint64_t, Hash32> r_root_map;
+    for (uint64_t p = 0; p < N; p++) {
+      r_root_map[p] = build_result_tree(0, 1, ops, results[p]).root();
+      std::memcpy(r_roots + 32 * p, r_root_map[p].data.data(), 32);
+    }
+    std::vector<AttestLeafRef> manifest;
+    std::set<uint64_t> whole;
+    for (uint64_t p = 0; p < N; p++) {
+      bool all = true;
+      for (const auto& [k, o] : outc)
+        if (!o.satisfied || !o.selected.count(p)) {
+          all = false;
+          break;
+        }
+      if (all) whole.insert(p);
+    }
+    for (uint64_t p : whole) {
+      AttestLeafRef ref;
+      ref.kind = AttestLeafRef::Kind::whole_batch;
+      ref.node = p;
+      manifest.push_back(ref);
+    }
+    for (const auto& [k, o] : outc) {
+      if (!o.satisfied) continue;
+      for (uint64_t p : o.selected) {
+        if (whole.count(p)) continue;
+        AttestLeafRef ref;
+        ref.kind = AttestLeafRef::Kind::single;
+        ref.node = p;
+        ref.op_index = k;
+        manifest.push_back(ref);
+      }
+    }
+    for (uint64_t k = 0; k < B; k++) {
+      bool failed = ops[k].status == OpStatus::rejected;
+      if (ops[k].kind == OpKind::request_inf && ops[k].status == OpStatus::ok)
+        failed = !outc.at(k).satisfied;
+      if (!failed) continue;
+      AttestLeafRef ref;
+      ref.kind = AttestLeafRef::Kind::failure;
+      ref.op_index = k;
+      manifest.push_back(ref);
+    }
+    std::vector<Bytes> leaves;
+    for (const auto& ref : manifest) leaves.push_back(*attest_leaf_bytes(ref, ops, r_root_map, by_op));
+    Hash32 a = merkle::Tree::build(leaves).root();
+    std::memcpy(a_root, a.data.data(), 32);
+    *manifest_len = manifest.size();
+    for (uint64_t k = 0; k < B; k++) {
+      sat_out[k] = outc.count(k) && outc.at(k).satisfied ? 1 : 0;
+      Encoder e;
+      ops[k].encode(e);
+      Bytes b = e.take();
+      entry_lens[k] = b.size();
+      if (b.size() > cap) return -2;
+      std::memcpy(entries + k * cap, b.data(), b.size());
+      rec_lens[k] = 0;
+      if (ops[k].status == OpStatus::rejected) {
+        Encoder r;
+        failure_record_for(ops[k]).encode(r);
+        Bytes rb = r.take();
+        if (rb.size() > cap) return -2;
+        rec_lens[k] = rb.size();
+        std::memcpy(recs + k * cap, rb.data(), rb.size());
+      }
+    }
+    return 0;
+  } catch (const std::exception&) {
+    return -1;
+  }
+}
+
 }  // extern "C"

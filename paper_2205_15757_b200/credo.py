@@ -35,6 +35,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("CREDO_GPU_LIB") or os.path.join(HERE, "libcredo_gpu.so")
 
 CG_OK, CG_EINVAL, CG_ECUDA, CG_ENCCL, CG_EDIGEST, CG_ECODEC, CG_ENOTSUP = range(7)
+OP_REQUEST, OP_REQUEST_REJECTED, OP_GROUP = range(3)
 EUCLIDEAN, MAX_MINUS_MIN, CHEBYSHEV = 0, 1, 2
 
 u64, u32, dbl, vp = C.c_uint64, C.c_uint32, C.c_double, C.c_void_p
@@ -570,6 +571,12 @@ class RequestBatch:
     eps: Optional[list] = None       # B × (float | None)
     u: Optional[int] = None
     B: Optional[int] = None
+    # optional PRE-PREPARE op-list structure (cg_request_batch.op_kinds):
+    # per op OP_REQUEST / OP_REQUEST_REJECTED / OP_GROUP, the group ops'
+    # OpEntry encodings and the rejected ops' FailureRecord encodings
+    op_kinds: Optional[list] = None
+    op_entries: Optional[list] = None    # B x bytes (b"" for requests)
+    fail_records: Optional[list] = None  # B x bytes (b"" when not rejected)
 
     @classmethod
     def from_encoded(cls, encs: Sequence[bytes]) -> "RequestBatch":
@@ -601,7 +608,9 @@ class _CReqBatch(C.Structure):
     _fields_ = [("B", u32), ("u", u64), ("request_ids", vp), ("inputs", vp),
                 ("inputs_on_device", C.c_int), ("has_eps", vp), ("eps", vp),
                 ("client_pubs", vp), ("nonces", vp), ("nonce_lens", vp),
-                ("client_sigs", vp), ("input_dims", vp), ("misfit_inputs", vp)]
+                ("client_sigs", vp), ("input_dims", vp), ("misfit_inputs", vp),
+                ("op_kinds", vp), ("op_entries", vp), ("op_entry_lens", vp),
+                ("fail_records", vp), ("fail_record_lens", vp)]
 
 
 class _COut(C.Structure):
@@ -634,22 +643,26 @@ class ModelGroup:
         self._keep = None
 
     @classmethod
-    def create_dist(cls, ctx: Context, my_model: Model, digests: Sequence[bytes],
+    def create_dist(cls, ctx: Context, my_model, digests: Sequence[bytes],
                     f: int, metric: int, default_eps: float, group_id: bytes,
                     version: int, max_batch: int, topk: int = 5) -> "ModelGroup":
-        """Replica-parallel group: this rank (ctx.init_nccl) is provider
-        `rank` and runs only my_model; digests lists every provider's."""
+        """Replica-parallel group: this rank (ctx.init_nccl) serves provider
+        `rank` (my_model), or with a list of k models providers
+        [rank k, (rank + 1) k); digests lists every provider's."""
+        mine = list(my_model) if isinstance(my_model, (list, tuple)) else [my_model]
         self = cls.__new__(cls)
-        self.ctx, self.models = ctx, [my_model]
+        self.ctx, self.models = ctx, mine
         self.N, self.f, self.topk = len(digests), f, topk
-        self.v, self.u = my_model.output_dim, my_model.input_dim
+        self.v, self.u = mine[0].output_dim, mine[0].input_dim
         self.group_id, self.version = group_id, version
         self.default_eps = default_eps
         h = vp()
-        ctx._check(ctx.L.cg_group_create_dist(ctx.h, my_model.h, b"".join(digests), u32(f),
-                                              u32(metric), dbl(default_eps), group_id,
-                                              u64(len(group_id)), u64(version),
-                                              u32(max_batch), u32(topk), C.byref(h)))
+        arr = (vp * len(mine))(*[m.h for m in mine])
+        ctx._check(ctx.L.cg_group_create_dist_multi(ctx.h, arr, u32(len(mine)),
+                                                    b"".join(digests), u32(f), u32(metric),
+                                                    dbl(default_eps), group_id,
+                                                    u64(len(group_id)), u64(version),
+                                                    u32(max_batch), u32(topk), C.byref(h)))
         self.h = h
         self._keep = None
         return self
@@ -693,7 +706,8 @@ class ModelGroup:
             for k, r in enumerate(rows):
                 if len(r) == group_u:
                     x[k] = r
-            b = RequestBatch(b.request_ids, x, b.client_pubs, b.nonces, b.client_sigs, b.eps)
+            import dataclasses
+            b = dataclasses.replace(b, inputs=x)
             misfit_keep = (rows, dims, mis)
         else:
             misfit_keep = None
@@ -712,15 +726,25 @@ class ModelGroup:
         if b.eps is not None:
             has = np.array([e is not None for e in b.eps], np.uint8)
             eps = np.array([e or 0.0 for e in b.eps], np.float64)
+        kinds = ents = el = recs = rl = None
+        if b.op_kinds is not None:
+            kinds = np.ascontiguousarray(b.op_kinds, np.uint8)
+            e = b.op_entries or [b""] * B
+            r = b.fail_records or [b""] * B
+            el = np.array([len(x) for x in e], np.uint64)
+            rl = np.array([len(x) for x in r], np.uint64)
+            ents = np.frombuffer(b"".join(e) or b"\0", np.uint8).copy()
+            recs = np.frombuffer(b"".join(r) or b"\0", np.uint8).copy()
         keep = [ids, pubs, sigs, nl, nb, has, eps,
-                None if on_dev else x, misfit_keep]
+                None if on_dev else x, misfit_keep, kinds, ents, el, recs, rl]
         cb = _CReqBatch(B, u, ids.ctypes.data, inputs_ptr, int(on_dev),
                         None if has is None else has.ctypes.data,
                         None if eps is None else eps.ctypes.data,
                         pubs.ctypes.data, nb.ctypes.data, nl.ctypes.data,
                         sigs.ctypes.data,
                         None if dims is None else dims.ctypes.data,
-                        None if mis is None else C.cast(mis, vp))
+                        None if mis is None else C.cast(mis, vp),
+                        *[None if z is None else z.ctypes.data for z in (kinds, ents, el, recs, rl)])
         return cb, keep, B
 
     def encode_results(self, provider: int, ticket: Optional[int] = None) -> bytes:
@@ -799,6 +823,17 @@ class ModelGroup:
         self._keep = keep + [o]
         self._lastB = B
         return self.fetch(False, want_leaves, _enqueue=(cb,), _outputs=o)
+
+    def certify_empty_slot(self, view: int, seq: int):
+        """An empty filler slot: noop_leaf R trees, N whole-batch A leaves."""
+        N = self.N
+        r = dict(r_roots=np.zeros((N, 32), np.uint8), a_root=np.zeros(32, np.uint8),
+                 manifest_len=np.zeros(1, np.uint64), manifest_kind=np.zeros(N, np.uint8),
+                 manifest_node=np.zeros(N, np.uint32), manifest_op=np.zeros(N, np.uint32),
+                 a_leaf_hashes=np.zeros((N, 32), np.uint8))
+        o = _COut(*[r[n].ctypes.data if n in r else None for n, _ in _COut._fields_])
+        self.ctx._check(self.ctx.L.cg_certify_empty_slot(self.h, u64(view), u64(seq), C.byref(o)))
+        return r
 
     def fetch_ticket(self, ticket: int, want_outputs=False, want_leaves=False):
         """Results of an already certified ticket (its slot not yet reused),

@@ -549,7 +549,14 @@ __global__ void __launch_bounds__(kManThreads) attest_manifest_kernel(
     uint32_t gid_len, uint64_t version, uint8_t* __restrict__ a_leaves,
     int32_t* __restrict__ single_pos, int32_t* __restrict__ need53,
     uint8_t* __restrict__ kinds, uint32_t* __restrict__ m_nodes, uint32_t* __restrict__ m_ops,
-    uint32_t* __restrict__ count) {
+    uint32_t* __restrict__ count, const uint8_t* __restrict__ has_outcome,
+    const uint8_t* __restrict__ explicit_fail, int32_t* __restrict__ fail_pos) {
+  // has_outcome == NULL: every op is an ok inference request (an outcome,
+  // coordinator.cpp:738-771); ops without one (rejected requests, group
+  // ops) neither restrict whole-batch attestation nor get single leaves,
+  // and fail only with their explicit record (messages.cpp:299-312).
+  auto outcome = [&](uint32_t k) { return has_outcome ? has_outcome[k] != 0 : true; };
+  auto explicit_f = [&](uint32_t k) { return explicit_fail ? explicit_fail[k] != 0 : false; };
   __shared__ uint32_t s_whole;
   __shared__ uint32_t s_scan[kManThreads];
   __shared__ uint32_t s_carry_single, s_carry_fail;
@@ -557,7 +564,8 @@ __global__ void __launch_bounds__(kManThreads) attest_manifest_kernel(
   if (tid == 0) { s_whole = 0xffffffffu; s_carry_single = 0; s_carry_fail = 0; }
   __syncthreads();
   uint32_t acc = 0xffffffffu;
-  for (uint32_t k = tid; k < B; k += kManThreads) acc &= sat[k] ? sel[k] : 0u;
+  for (uint32_t k = tid; k < B; k += kManThreads)
+    if (outcome(k)) acc &= sat[k] ? sel[k] : 0u;
   atomicAnd(&s_whole, acc);
   __syncthreads();
   const uint32_t all_nodes = (N >= 32) ? 0xffffffffu : ((1u << N) - 1);
@@ -574,7 +582,7 @@ __global__ void __launch_bounds__(kManThreads) attest_manifest_kernel(
   // total singles for the failure offset
   uint32_t local = 0;
   for (uint32_t k = tid; k < B; k += kManThreads)
-    if (sat[k]) local += __popc(sel[k] & ~whole);
+    if (outcome(k) && sat[k]) local += __popc(sel[k] & ~whole);
   s_scan[tid] = local;
   __syncthreads();
   if (tid == 0) {
@@ -589,8 +597,12 @@ __global__ void __launch_bounds__(kManThreads) attest_manifest_kernel(
     uint32_t k = base + tid;
     uint32_t ns = 0, nf = 0;
     if (k < B) {
-      if (sat[k]) ns = __popc(sel[k] & ~whole);
-      else nf = 1;
+      if (outcome(k)) {
+        if (sat[k]) ns = __popc(sel[k] & ~whole);
+        else nf = 1;
+      } else if (explicit_f(k)) {
+        nf = 1;
+      }
     }
     // exclusive scan of (ns | nf<<16) — B and N small enough for 16 bits
     s_scan[tid] = ns | (nf << 16);
@@ -609,8 +621,16 @@ __global__ void __launch_bounds__(kManThreads) attest_manifest_kernel(
       for (uint32_t p = 0; p < N; p++) single_pos[k * N + p] = -1;
       // request k's single leaves H(0x00||0x53||req||res) share one request
       // midstate, computed only when k has at least one single leaf
-      if (need53) need53[k] = (sat[k] && (sel[k] & ~whole)) ? 0 : -1;
-      if (sat[k]) {
+      if (need53) need53[k] = (outcome(k) && sat[k] && (sel[k] & ~whole)) ? 0 : -1;
+      if (fail_pos) fail_pos[k] = -1;
+      if (!outcome(k)) {
+        if (explicit_f(k)) {  // the op's own FailureRecord: a chain job hashes it there
+          fail_pos[k] = (int32_t)fpos;
+          kinds[fpos] = 2;
+          m_nodes[fpos] = 0;
+          m_ops[fpos] = k;
+        }
+      } else if (sat[k]) {
         uint32_t sm = sel[k] & ~whole;
         for (uint32_t p = 0; p < N; p++)
           if (sm >> p & 1) {
@@ -657,11 +677,12 @@ void launch_attest_manifest(uint32_t B, uint32_t N, const uint32_t* sel,
                             uint32_t gid_len, uint64_t version,
                             uint8_t* a_leaves, int32_t* single_pos, int32_t* need53,
                             uint8_t* kinds, uint32_t* m_nodes, uint32_t* m_ops,
-                            uint32_t* count, cudaStream_t st) {
+                            uint32_t* count, const uint8_t* has_outcome,
+                            const uint8_t* explicit_fail, int32_t* fail_pos, cudaStream_t st) {
   if (gid_len > 100) throw InvalidArgument("group id too long for failure leaf");
   attest_manifest_kernel<<<1, kManThreads, 0, st>>>(
       B, N, sel, sat, r_roots, req_ids, gid, gid_len, version, a_leaves,
-      single_pos, need53, kinds, m_nodes, m_ops, count);
+      single_pos, need53, kinds, m_nodes, m_ops, count, has_outcome, explicit_fail, fail_pos);
   CG_CHECK_LAUNCH();
 }
 

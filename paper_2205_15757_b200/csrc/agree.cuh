@@ -29,7 +29,8 @@ void launch_attest_manifest(uint32_t B, uint32_t N, const uint32_t* sel,
                             uint32_t gid_len, uint64_t version,
                             uint8_t* a_leaves, int32_t* single_pos, int32_t* need53,
                             uint8_t* kinds, uint32_t* m_nodes, uint32_t* m_ops,
-                            uint32_t* count, cudaStream_t st);
+                            uint32_t* count, const uint8_t* has_outcome,
+                            const uint8_t* explicit_fail, int32_t* fail_pos, cudaStream_t st);
 void launch_mark_missing(const uint8_t* miss, uint32_t B, uint32_t* sel, double* diam,
                          uint8_t* sat, int8_t* status, int64_t* label, cudaStream_t st);
 void launch_softmax_topk_f32(const float* in, uint64_t in_ld, uint32_t rows,

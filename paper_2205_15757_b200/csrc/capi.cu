@@ -719,7 +719,7 @@ void perturb_group_outputs(cg_group* g, const IngestSlot& S, double* d_outs, cud
   const uint32_t nloc = (uint32_t)g->models.size(), B = S.B;
   const uint64_t nshared = (44 + 8 * u) / 64;
   for (uint32_t li = 0; li < nloc; li++) {
-    const uint64_t p = g->dist ? g->rank : li;
+    const uint64_t p = g->first + li;
     PerturbHdr hdr;
     for (int i = 0; i < 8; i++) hdr.b[i] = (uint8_t)(p >> (56 - 8 * i));
     std::memcpy(hdr.b + 8, g->digests[p].data(), 32);
@@ -773,29 +773,67 @@ uint64_t ingest(cg_group* g, const cg_request_batch* bt) {
   }
   Arena ar;
   std::vector<ChainJob> jobs;
-  jobs.reserve((size_t)B * (3 + 2 * N + g->models.size()));
+  jobs.reserve((size_t)B * (4 + 2 * N + 2 * g->models.size()));
   const uint8_t* gid = (const uint8_t*)g->gid.data();
   const uint32_t gl = (uint32_t)g->gid.size();
+  // Per op: an ok inference request (the common case), a request the
+  // primary rejected, or a group operation (PRE-PREPARE op list,
+  // messages.hpp:106-118). Requests without provider results -- misfits
+  // (input dimension != u), rejected requests -- get missing_result_leaf;
+  // group ops get group_op_leaf; neither kind has an agreement outcome.
   struct ReqLayout {
-    size_t h, h53, h4d, t;
+    size_t h, h53, h4d, t, h47, f46;
     uint64_t lenH, lenT, P, uk, moff;  // uk: this request's input count; moff: misfit input offset
-    bool miss;
+    uint64_t len47, len46;
+    uint8_t kind;
+    bool in_mis;   // input read from the misfit buffer (its dimension != u)
+    bool noresult; // no provider output: R leaf 0x4D (requests) / 0x47 (group ops)
   };
   std::vector<ReqLayout> rl(B);
   std::vector<size_t> res_off((size_t)B * N), dig_off((size_t)B * N);
-  uint64_t lenRes = 0, nonce_pos = 0, misfit_total = 0;
-  bool any_miss = false;
+  uint64_t lenRes = 0, nonce_pos = 0, misfit_total = 0, entry_pos = 0, rec_pos = 0;
+  bool any_miss = false, any_kind = false;
   for (uint32_t k = 0; k < B; k++) {
     const uint8_t* rid = bt->request_ids + 32 * k;
     ReqLayout& L = rl[k];
-    L.uk = bt->input_dims ? bt->input_dims[k] : u;
-    L.miss = L.uk != u;
+    L.kind = bt->op_kinds ? bt->op_kinds[k] : CG_OP_REQUEST;
+    if (L.kind > CG_OP_GROUP) throw InvalidArgument("unknown op kind");
+    any_kind |= L.kind != CG_OP_REQUEST;
+    L.uk = L.kind == CG_OP_GROUP ? u : (bt->input_dims ? bt->input_dims[k] : u);
+    L.in_mis = L.uk != u;
+    L.noresult = L.in_mis || L.kind != CG_OP_REQUEST;
     L.moff = misfit_total;
-    if (L.miss) {
+    if (L.in_mis) {
       if (!bt->misfit_inputs || (L.uk && !bt->misfit_inputs[k]))
         throw InvalidArgument("misfit request without its input");
       misfit_total += L.uk;
-      any_miss = true;
+    }
+    any_miss |= L.noresult;
+    L.len47 = L.kind == CG_OP_GROUP ? (bt->op_entry_lens ? bt->op_entry_lens[k] : 0) : 0;
+    L.len46 = bt->fail_record_lens ? bt->fail_record_lens[k] : 0;
+    if (L.kind == CG_OP_REQUEST && L.len46)
+      throw InvalidArgument("a failure record is for rejected ops only");
+    if (L.kind == CG_OP_REQUEST_REJECTED && !L.len46)
+      throw InvalidArgument("a rejected op needs its failure record");
+    if (L.len47) {  // group_op_leaf: 0x00 || 0x47 || OpEntry::encode (messages.cpp:220-225)
+      Enc E;
+      E.u8(0x00);
+      E.u8(0x47);
+      E.raw(bt->op_entries + entry_pos, L.len47);
+      entry_pos += L.len47;
+      L.h47 = ar.add(E.b.data(), E.b.size(), 0);
+      L.len47 = E.b.size();
+    } else if (L.kind == CG_OP_GROUP) {
+      throw InvalidArgument("a group op needs its OpEntry encoding");
+    }
+    if (L.len46) {  // failure_leaf: 0x00 || 0x46 || FailureRecord::encode (messages.cpp:260-297)
+      Enc E;
+      E.u8(0x00);
+      E.u8(0x46);
+      E.raw(bt->fail_records + rec_pos, L.len46);
+      rec_pos += L.len46;
+      L.f46 = ar.add(E.b.data(), E.b.size(), 0);
+      L.len46 = E.b.size();
     }
     Enc H;  // 0x00 (leaf domain) || 0x52 (result leaf) || request body head
     H.u8(0x00);
@@ -818,7 +856,7 @@ uint64_t ingest(cg_group* g, const cg_request_batch* bt) {
     H.b[1] = 0x53;  // single_attest_leaf tag (messages.cpp:283-290)
     L.h53 = ar.add(H.b.data(), H.b.size(), 0);
     H.b[1] = 0x4D;  // missing_result_leaf tag (messages.cpp:213-218)
-    L.h4d = L.miss ? ar.add(H.b.data(), H.b.size(), 0) : 0;
+    L.h4d = (L.noresult && L.kind != CG_OP_GROUP) ? ar.add(H.b.data(), H.b.size(), 0) : 0;
     L.t = ar.add(T.b.data(), T.b.size(), L.lenH + 8 * L.uk);
     for (uint32_t p = 0; p < N; p++) {
       Enc R;  // InferenceResult::encode up to the output list (domain.cpp:218-225)
@@ -839,18 +877,22 @@ uint64_t ingest(cg_group* g, const cg_request_batch* bt) {
   if (!bt->inputs_on_device) S.d_in.ensure((uint64_t)g->maxB * u);
   S.d_in_ptr = bt->inputs_on_device ? bt->inputs : S.d_in.p;
   S.any_miss = any_miss;
+  S.any_kind = any_kind;
   if (any_miss) {
     S.d_misfit.ensure(std::max<uint64_t>(misfit_total, 1));
-    S.d_miss.ensure(g->maxB);
-    S.h_miss.ensure(g->maxB);
+    S.d_miss.ensure(3 * (uint64_t)g->maxB);  // missing, has-outcome, explicit-failure flags
+    S.h_miss.ensure(3 * (uint64_t)g->maxB);
+    S.d_fail_pos.ensure(g->maxB);
     if (!S.d_neg1.p) {
       const int32_t neg1 = -1;
       S.d_neg1.ensure(1);
       CG_CUDA(cudaMemcpy(S.d_neg1.p, &neg1, 4, cudaMemcpyHostToDevice));
     }
     for (uint32_t k = 0; k < B; k++) {
-      S.h_miss.p[k] = rl[k].miss ? 1 : 0;
-      if (rl[k].miss && rl[k].uk)  // pageable host source: synchronous, rare
+      S.h_miss.p[k] = rl[k].noresult ? 1 : 0;
+      S.h_miss.p[B + k] = rl[k].kind == CG_OP_REQUEST ? 1 : 0;
+      S.h_miss.p[2 * B + k] = rl[k].len46 ? 1 : 0;
+      if (rl[k].in_mis && rl[k].uk)  // pageable host source: synchronous, rare
         CG_CUDA(cudaMemcpyAsync(S.d_misfit.p + rl[k].moff, bt->misfit_inputs[k], 8 * rl[k].uk,
                                 cudaMemcpyHostToDevice, st));
     }
@@ -869,7 +911,7 @@ uint64_t ingest(cg_group* g, const cg_request_batch* bt) {
     ChainJob j;
     std::memset(&j, 0, sizeof j);
     j.seg[0] = seg_raw(A + head, 0, L.lenH);
-    j.seg[1] = seg_f64(L.miss ? MIS + 8 * L.moff : IN + 8 * u * k, L.lenH, 8 * L.uk);
+    j.seg[1] = seg_f64(L.in_mis ? MIS + 8 * L.moff : IN + 8 * u * k, L.lenH, 8 * L.uk);
     j.seg[2] = seg_raw(A + L.t, L.lenH + 8 * L.uk, L.lenT);
     j.seg[3] = seg_raw(A + res_off[(size_t)k * N + p], L.P, lenRes);
     j.seg[4] = seg_f64(OUT + 8 * v * ((uint64_t)p * B + k), L.P + lenRes, 8 * v);
@@ -893,26 +935,34 @@ uint64_t ingest(cg_group* g, const cg_request_batch* bt) {
     j.total_len = L.P;
     j.blk_end = L.P / 64;
     j.state_out = (uint64_t)(S.d_mid.p + 8 * k);
-    if (L.miss) j.skip_flag = (uint64_t)S.d_neg1.p;
+    if (L.noresult) j.skip_flag = (uint64_t)S.d_neg1.p;
     jobs.push_back(j);
   }
-  // missing_result_leaf H(0x00||0x4D||request) of each misfit request: every
-  // local provider's R tree holds it at the request's position
+  // ops without provider results: every local provider's R tree holds
+  // missing_result_leaf H(0x00||0x4D||request) (misfit / rejected requests)
+  // or group_op_leaf H(0x00||0x47||OpEntry) at the op's position
+  // (build_result_tree, messages.cpp:235-258)
   if (any_miss)
     for (uint32_t k = 0; k < B; k++) {
       const ReqLayout& L = rl[k];
-      if (!L.miss) continue;
+      if (!L.noresult) continue;
       for (uint32_t li = 0; li < (uint32_t)g->models.size(); li++) {
-        const uint32_t p = g->dist ? g->rank : li;
+        const uint32_t p = g->first + li;
         ChainJob j;
         std::memset(&j, 0, sizeof j);
-        j.seg[0] = seg_raw(A + L.h4d, 0, L.lenH);
-        j.seg[1] = seg_f64(MIS + 8 * L.moff, L.lenH, 8 * L.uk);
-        j.seg[2] = seg_raw(A + L.t, L.lenH + 8 * L.uk, L.lenT);
-        j.nseg = 3;
+        if (L.kind == CG_OP_GROUP) {
+          j.seg[0] = seg_raw(A + L.h47, 0, L.len47);
+          j.nseg = 1;
+          j.total_len = L.len47;
+        } else {
+          j.seg[0] = seg_raw(A + L.h4d, 0, L.lenH);
+          j.seg[1] = seg_f64(L.in_mis ? MIS + 8 * L.moff : IN + 8 * u * k, L.lenH, 8 * L.uk);
+          j.seg[2] = seg_raw(A + L.t, L.lenH + 8 * L.uk, L.lenT);
+          j.nseg = 3;
+          j.total_len = L.P;
+        }
         j.final_ = 1;
-        j.total_len = L.P;
-        j.blk_end = (L.P + 9 + 63) / 64;
+        j.blk_end = (j.total_len + 9 + 63) / 64;
         j.digest_out = (uint64_t)(S.res.d_leaf.p + 32 * ((uint64_t)p * B + k));
         jobs.push_back(j);
       }
@@ -947,7 +997,7 @@ uint64_t ingest(cg_group* g, const cg_request_batch* bt) {
       j.blk_begin = rl[k].P / 64;
       j.state_in = j.blk_begin ? (uint64_t)(S.d_mid.p + 8 * k) : 0;
       j.digest_out = (uint64_t)(S.res.d_leaf.p + 32 * ((uint64_t)p * B + k));
-      if (rl[k].miss) j.skip_flag = (uint64_t)S.d_neg1.p;  // written at ingest (0x4D)
+      if (rl[k].noresult) j.skip_flag = (uint64_t)S.d_neg1.p;  // written at ingest (0x4D / 0x47)
       jobs.push_back(j);
     }
   // single attestation leaves H(0x00||0x53||req||res) (messages.cpp:283-290):
@@ -960,7 +1010,7 @@ uint64_t ingest(cg_group* g, const cg_request_batch* bt) {
     ChainJob j;
     std::memset(&j, 0, sizeof j);
     j.seg[0] = seg_raw(A + L.h53, 0, L.lenH);
-    j.seg[1] = seg_f64(L.miss ? MIS + 8 * L.moff : IN + 8 * u * k, L.lenH, 8 * L.uk);
+    j.seg[1] = seg_f64(L.in_mis ? MIS + 8 * L.moff : IN + 8 * u * k, L.lenH, 8 * L.uk);
     j.seg[2] = seg_raw(A + L.t, L.lenH + 8 * L.uk, L.lenT);
     j.nseg = 3;
     j.total_len = L.P;
@@ -979,6 +1029,25 @@ uint64_t ingest(cg_group* g, const cg_request_batch* bt) {
       j.skip_flag = (uint64_t)(S.res.d_single_pos.p + (uint64_t)k * N + p);
       jobs.push_back(j);
     }
+  // explicit failure leaves of rejected ops (failure_record_for with the
+  // op's reason, messages.cpp:299-312): the manifest decides where they land
+  S.n_fail_jobs = 0;
+  if (any_miss)
+    for (uint32_t k = 0; k < B; k++) {
+      const ReqLayout& L = rl[k];
+      if (!L.len46) continue;
+      ChainJob j;
+      std::memset(&j, 0, sizeof j);
+      j.seg[0] = seg_raw(A + L.f46, 0, L.len46);
+      j.nseg = 1;
+      j.final_ = 1;
+      j.total_len = L.len46;
+      j.blk_end = (L.len46 + 9 + 63) / 64;
+      j.digest_out = (uint64_t)S.res.d_aleaf.p;
+      j.skip_flag = (uint64_t)(S.d_fail_pos.p + k);
+      jobs.push_back(j);
+      S.n_fail_jobs++;
+    }
   S.h_jobs.ensure(jobs.size());
   S.d_jobs.ensure(jobs.size());
   std::memcpy(S.h_jobs.p, jobs.data(), jobs.size() * sizeof(ChainJob));
@@ -996,7 +1065,7 @@ uint64_t ingest(cg_group* g, const cg_request_batch* bt) {
   CG_CUDA(cudaMemcpyAsync(S.d_reqids.p, S.h_reqids.p, 32 * (size_t)B, cudaMemcpyHostToDevice, st));
   CG_CUDA(cudaMemcpyAsync(S.d_tree.p, S.h_tree.p, 16 * (size_t)N, cudaMemcpyHostToDevice, st));
   if (any_miss)
-    CG_CUDA(cudaMemcpyAsync(S.d_miss.p, S.h_miss.p, B, cudaMemcpyHostToDevice, st));
+    CG_CUDA(cudaMemcpyAsync(S.d_miss.p, S.h_miss.p, 3 * (size_t)B, cudaMemcpyHostToDevice, st));
   if (!bt->inputs_on_device)
     CG_CUDA(cudaMemcpyAsync(S.d_in.p, bt->inputs, 8 * u * B, cudaMemcpyHostToDevice, st));
   CG_CUDA(cudaEventRecord(S.ev_staged, st));
@@ -1049,34 +1118,40 @@ void certify(cg_group* g, uint64_t ticket, const double* precomputed_outputs) {
       prepped = g->d_prep.p;
     }
     // Same-architecture CNN replicas: one grouped GEMM launch per layer.
-    if (!g->dist && g->same_prep && g->group_plan_ok && (!g->gplan || g->gplan->batch() != B)) {
+    // (replica-parallel groups: this rank's replicas)
+    const uint32_t nloc = (uint32_t)g->models.size(), first = g->first;
+    if (g->same_prep && g->group_plan_ok && (!g->gplan || g->gplan->batch() != B)) {
       std::vector<CnnModel*> ms;
       std::vector<float*> lg;
-      for (uint32_t p = 0; p < N; p++) {
-        ms.push_back(g->models[p]->cnn.get());
-        lg.push_back(g->d_pre32.p + (uint64_t)p * B * v);
+      for (uint32_t li = 0; li < nloc; li++) {
+        ms.push_back(g->models[li]->cnn.get());
+        lg.push_back(g->d_pre32.p + (uint64_t)li * B * v);
       }
       g->gplan = CnnGroupPlan::build(ms, B, g->d_prep.p, lg);
       g->group_plan_ok = g->gplan != nullptr;
     }
-    const bool grouped = !g->dist && g->same_prep && g->gplan && g->gplan->batch() == B;
+    const bool grouped = g->same_prep && g->gplan && g->gplan->batch() == B;
     if (grouped) {
       g->gplan->run(st);
       bool same_sm = true;
-      for (uint32_t p = 1; p < N; p++) same_sm &= g->models[p]->softmax == g->models[0]->softmax;
-      if (same_sm) {  // softmax/top-k of all N x B rows in one launch
-        launch_softmax_topk_f32(g->d_pre32.p, v, N * B, (uint32_t)v, g->models[0]->softmax,
-                                R.d_outs.p, v, g->topk, R.d_topi.p, R.d_topv.p, st);
+      for (uint32_t li = 1; li < nloc; li++)
+        same_sm &= g->models[li]->softmax == g->models[0]->softmax;
+      if (same_sm) {  // softmax/top-k of all local rows in one launch
+        launch_softmax_topk_f32(g->d_pre32.p, v, nloc * B, (uint32_t)v, g->models[0]->softmax,
+                                R.d_outs.p + (uint64_t)first * B * v, v, g->topk,
+                                R.d_topi.p + (uint64_t)first * B * g->topk,
+                                R.d_topv.p + (uint64_t)first * B * g->topk, st);
       } else {
-        for (uint32_t p = 0; p < N; p++)
-          launch_softmax_topk_f32(g->d_pre32.p + (uint64_t)p * B * v, v, B, (uint32_t)v,
-                                  g->models[p]->softmax, R.d_outs.p + (uint64_t)p * B * v, v,
-                                  g->topk, R.d_topi.p + (uint64_t)p * B * g->topk,
-                                  R.d_topv.p + (uint64_t)p * B * g->topk, st);
+        for (uint32_t li = 0; li < nloc; li++) {
+          const uint64_t p = first + li;
+          launch_softmax_topk_f32(g->d_pre32.p + (uint64_t)li * B * v, v, B, (uint32_t)v,
+                                  g->models[li]->softmax, R.d_outs.p + p * B * v, v, g->topk,
+                                  R.d_topi.p + p * B * g->topk, R.d_topv.p + p * B * g->topk, st);
+        }
       }
     }
-    for (uint32_t li = 0; li < (uint32_t)g->models.size() && !grouped; li++) {
-      const uint32_t p = g->dist ? g->rank : li;  // provider index of local replica li
+    for (uint32_t li = 0; li < nloc && !grouped; li++) {
+      const uint32_t p = first + li;  // provider index of local replica li
       cg_model* m = g->models[li];
       double* outs = R.d_outs.p + (uint64_t)p * B * v;
       uint32_t* ti = R.d_topi.p + (uint64_t)p * B * g->topk;
@@ -1098,7 +1173,7 @@ void certify(cg_group* g, uint64_t ticket, const double* precomputed_outputs) {
   }
   if (g->fault_thr && !precomputed_outputs) {  // OffsetExecutor wraps the perturbing one
     const uint32_t p = g->fault_provider;
-    const bool local = g->dist ? p == g->rank : p < (uint32_t)g->models.size();
+    const bool local = p >= g->first && p < g->first + (uint32_t)g->models.size();
     if (local)
       launch_offset_outputs(R.d_outs.p + (uint64_t)p * B * v, S.d_reqids.p, B, (uint32_t)v,
                             g->fault_offset, g->fault_thr, st);
@@ -1108,20 +1183,23 @@ void certify(cg_group* g, uint64_t ticket, const double* precomputed_outputs) {
   CG_CUDA(cudaStreamWaitEvent(tl, S.ev_fwd, 0));
   CG_CUDA(cudaStreamWaitEvent(tl, S.ev_prefix, 0));
   if (g->dist) {
-    // This rank is provider `rank`: its own result leaves and R root
-    // (try_prepare), then one NCCL all-gather of every provider's outputs
-    // and R root over NVLink; agreement and the attestation are then
-    // computed on every rank, as every reference node attests.
-    const uint32_t r = g->rank;
-    launch_chain_jobs(S.d_jobs.p + S.off_leaf + (uint64_t)r * B, B, tl, /*exclusive_sm=*/true);
-    launch_merkle_trees(R.d_leaf.p + 32 * (uint64_t)r * B, nullptr, S.d_tree.p + N, nullptr, 1,
-                        B, R.d_rroots.p + 32 * r, tl);
+    // This rank serves providers [first, first + nloc) (assigned_models
+    // chunking): their result leaves and R roots (try_prepare), then one
+    // NCCL all-gather of every provider's outputs and R root over NVLink;
+    // agreement and the attestation are then computed on every rank, as
+    // every reference node attests.
+    const uint32_t first = g->first, nloc = (uint32_t)g->models.size();
+    launch_chain_jobs(S.d_jobs.p + S.off_leaf + (uint64_t)first * B, nloc * B, tl,
+                      /*exclusive_sm=*/true);
+    launch_merkle_trees(R.d_leaf.p, S.d_tree.p + first, S.d_tree.p + N + first, nullptr, nloc, B,
+                        R.d_rroots.p + 32 * first, tl);
     timer_begin(tl, kTimeComm);
     ncclResult_t e1, e2, e3;
     e1 = ncclGroupStart();
-    e2 = ncclAllGather(R.d_outs.p + (uint64_t)r * B * v, R.d_outs.p, (size_t)B * v, ncclDouble,
+    e2 = ncclAllGather(R.d_outs.p + (uint64_t)first * B * v, R.d_outs.p, (size_t)nloc * B * v,
+                       ncclDouble, ctx->comm, tl);
+    e3 = ncclAllGather(R.d_rroots.p + 32 * first, R.d_rroots.p, 32 * (size_t)nloc, ncclUint8,
                        ctx->comm, tl);
-    e3 = ncclAllGather(R.d_rroots.p + 32 * r, R.d_rroots.p, 32, ncclUint8, ctx->comm, tl);
     ncclResult_t e4 = ncclGroupEnd();
     timer_end(tl, kTimeComm);
     if (e1 != ncclSuccess || e2 != ncclSuccess || e3 != ncclSuccess || e4 != ncclSuccess)
@@ -1141,7 +1219,10 @@ void certify(cg_group* g, uint64_t ticket, const double* precomputed_outputs) {
                         R.d_label.p, tl);
   launch_attest_manifest(B, N, R.d_sel.p, R.d_sat.p, R.d_rroots.p, S.d_reqids.p, g->d_gid.p, gl,
                          g->version, R.d_aleaf.p, R.d_single_pos.p, R.d_need53.p, R.d_kinds.p,
-                         R.d_mnodes.p, R.d_mops.p, R.d_count.p, tl);
+                         R.d_mnodes.p, R.d_mops.p, R.d_count.p,
+                         S.any_kind ? S.d_miss.p + B : nullptr,
+                         S.any_kind ? S.d_miss.p + 2 * (size_t)B : nullptr,
+                         S.any_kind ? S.d_fail_pos.p : nullptr, tl);
   timer_end(tl, kTimeAgree);
   // Single attestation leaves re-hash their request (a 1.2 MB chain at
   // ImageNet shape): they run on the slot's own stream, off the shared tail,
@@ -1150,7 +1231,7 @@ void certify(cg_group* g, uint64_t ticket, const double* precomputed_outputs) {
   CG_CUDA(cudaEventRecord(S.ev_man, tl));
   CG_CUDA(cudaStreamWaitEvent(S.stream, S.ev_man, 0));
   launch_chain_jobs(S.d_jobs.p + S.off_mid53, B, S.stream, /*exclusive_sm=*/true);
-  launch_chain_jobs(S.d_jobs.p + S.off_single, N * B, S.stream);
+  launch_chain_jobs(S.d_jobs.p + S.off_single, N * B + S.n_fail_jobs, S.stream);
   launch_merkle_trees(R.d_aleaf.p, nullptr, nullptr, R.d_count.p, 1, (uint64_t)N * B + B + N,
                       R.d_aroot.p, S.stream);
   CG_CUDA(cudaEventRecord(S.ev_done, S.stream));
@@ -1220,6 +1301,9 @@ int create_group(cg_ctx* ctx, cg_model* const* models, uint32_t nlocal, uint32_t
     g->topk = topk;
     g->dist = dist;
     g->rank = dist ? (uint32_t)ctx->rank : 0;
+    g->first = dist ? g->rank * nlocal : 0;
+    if (dist && nlocal * (uint32_t)ctx->nranks != N)
+      throw InvalidArgument("replica-parallel group: N must be (replicas per rank) x ranks");
     for (uint32_t p = 0; p < nlocal; p++) {
       if (!models[p] || models[p]->ctx != ctx) throw InvalidArgument("bad model");
       g->models.push_back(models[p]);
@@ -1229,8 +1313,9 @@ int create_group(cg_ctx* ctx, cg_model* const* models, uint32_t nlocal, uint32_t
       std::memcpy(d.data(), dist ? all_digests + 32 * p : models[p]->digest, 32);
       g->digests.push_back(d);
     }
-    if (dist && std::memcmp(g->digests[g->rank].data(), models[0]->digest, 32) != 0)
-      throw InvalidArgument("this rank's model is not provider `rank` of the group");
+    for (uint32_t li = 0; dist && li < nlocal; li++)
+      if (std::memcmp(g->digests[g->first + li].data(), models[li]->digest, 32) != 0)
+        throw InvalidArgument("this rank's models are not providers [rank x k, (rank + 1) x k)");
     g->u = models[0]->u;
     g->v = models[0]->v;
     for (auto* m : g->models)
@@ -1267,13 +1352,13 @@ int create_group(cg_ctx* ctx, cg_model* const* models, uint32_t nlocal, uint32_t
       S->d_eps.ensure(B);
       S->d_arena.ensure(arena_max);
       S->d_reqids.ensure(32 * B);
-      S->d_jobs.ensure(B * (2 + 2 * N + nlocal));
+      S->d_jobs.ensure(B * (4 + 2 * N + 2 * nlocal));
       S->d_mid.ensure(8 * B);
       S->d_mid53.ensure(8 * B);
       S->d_tree.ensure(2 * N);
       S->h_arena.ensure(arena_max);
       S->h_reqids.ensure(32 * B);
-      S->h_jobs.ensure(B * (2 + 2 * N + nlocal));
+      S->h_jobs.ensure(B * (4 + 2 * N + 2 * nlocal));
       S->h_eps.ensure(B);
       S->h_tree.ensure(2 * N);
       CG_CUDA(cudaEventCreateWithFlags(&S->ev_fwd, cudaEventDisableTiming));
@@ -1324,6 +1409,18 @@ int cg_group_create_dist(cg_ctx* ctx, cg_model* my_model, const uint8_t* all_dig
   if (!ctx || !ctx->comm) return fail(ctx, CG_EINVAL, "cg_ctx_init_nccl first");
   return create_group(ctx, &my_model, 1, (uint32_t)ctx->nranks, all_digests, true, f, metric,
                       default_eps, group_id, group_id_len, version, max_batch, topk, out);
+}
+
+int cg_group_create_dist_multi(cg_ctx* ctx, cg_model* const* my_models, uint32_t nlocal,
+                               const uint8_t* all_digests, uint32_t f, uint32_t metric,
+                               double default_eps, const char* group_id, uint64_t group_id_len,
+                               uint64_t version, uint32_t max_batch, uint32_t topk,
+                               cg_group** out) {
+  if (!ctx || !ctx->comm) return fail(ctx, CG_EINVAL, "cg_ctx_init_nccl first");
+  if (nlocal == 0 || !my_models) return fail(ctx, CG_EINVAL, "no local models");
+  return create_group(ctx, my_models, nlocal, nlocal * (uint32_t)ctx->nranks, all_digests, true,
+                      f, metric, default_eps, group_id, group_id_len, version, max_batch, topk,
+                      out);
 }
 
 }  // extern "C"
@@ -1385,7 +1482,7 @@ int cg_group_set_perturbation(cg_group* g, double magnitude) {
     g->d_phdr.ensure(64ull * nloc);
     std::vector<uint8_t> h(64ull * nloc, 0);
     for (uint32_t li = 0; li < nloc; li++) {
-      const uint64_t p = g->dist ? g->rank : li;
+      const uint64_t p = g->first + li;
       uint8_t* b = h.data() + 64ull * li;
       for (int i = 0; i < 8; i++) b[i] = (uint8_t)(p >> (56 - 8 * i));
       std::memcpy(b + 8, g->digests[p].data(), 32);
@@ -1610,7 +1707,7 @@ void group_auth_paths(cg_group* g, const IngestSlot* S, uint32_t tree, const uin
   if (!S || !S->certified) throw InvalidArgument("nothing certified yet");
   const uint32_t B = S->B, N = g->N;
   if (tree > N) throw InvalidArgument("tree index out of range");
-  if (g->dist && tree < N && tree != g->rank)
+  if (g->dist && tree < N && (tree < g->first || tree >= g->first + g->models.size()))
     throw InvalidArgument("replica-parallel group: only this rank's result tree is local");
   const uint8_t* leaves;
   uint64_t n;
@@ -1692,6 +1789,53 @@ int cg_group_fetch(cg_group* g, cg_certify_out* out) {
   if (!g || !out) return CG_EINVAL;
   return guarded(g->ctx, [&] {
     certify_fetch(g, out);
+    return CG_OK;
+  });
+}
+
+// An empty filler slot (messages.cpp:240-243, coordinator.cpp:776-787):
+// R tree = [noop_leaf(view, seq)] for every provider; no outcomes, so every
+// provider is whole-batch attested. The four SHA-256 messages run on the
+// device like every other digest.
+int cg_certify_empty_slot(cg_group* g, uint64_t view, uint64_t seq, cg_certify_out* o) {
+  if (!g || !o) return CG_EINVAL;
+  return guarded(g->ctx, [&] {
+    cg_ctx* ctx = g->ctx;
+    const uint32_t N = g->N;
+    uint8_t noop[17];
+    noop[0] = 0x4E;  // kLeafNoop || u64be view || u64be seq (messages.cpp:227-233)
+    for (int i = 0; i < 8; i++) {
+      noop[1 + i] = (uint8_t)(view >> (56 - 8 * i));
+      noop[9 + i] = (uint8_t)(seq >> (56 - 8 * i));
+    }
+    uint64_t off = 0, len = 17;
+    uint8_t rroot[32], whole[33], aleaf[32];
+    device_sha256_many(ctx, noop, &off, &len, 1, 0x00, rroot);  // one-leaf tree: root = leaf hash
+    whole[0] = 0x57;  // whole_batch_leaf(R root) (messages.cpp:276-280)
+    std::memcpy(whole + 1, rroot, 32);
+    len = 33;
+    device_sha256_many(ctx, whole, &off, &len, 1, 0x00, aleaf);
+    std::vector<uint8_t> leaves(32 * (size_t)N);
+    for (uint32_t p = 0; p < N; p++) std::memcpy(leaves.data() + 32 * p, aleaf, 32);
+    ctx->d_bytes.ensure(leaves.size());
+    ctx->d_out.ensure(32);
+    CG_CUDA(cudaMemcpyAsync(ctx->d_bytes.p, leaves.data(), leaves.size(), cudaMemcpyHostToDevice,
+                            ctx->stream));
+    launch_merkle_trees(ctx->d_bytes.p, nullptr, nullptr, nullptr, 1, N, ctx->d_out.p, ctx->stream,
+                        N);
+    uint8_t aroot[32];
+    CG_CUDA(cudaMemcpyAsync(aroot, ctx->d_out.p, 32, cudaMemcpyDeviceToHost, ctx->stream));
+    CG_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (o->r_roots)
+      for (uint32_t p = 0; p < N; p++) std::memcpy(o->r_roots + 32 * p, rroot, 32);
+    if (o->a_root) std::memcpy(o->a_root, aroot, 32);
+    if (o->manifest_len) *o->manifest_len = N;
+    for (uint32_t p = 0; p < N; p++) {
+      if (o->manifest_kind) o->manifest_kind[p] = 0;
+      if (o->manifest_node) o->manifest_node[p] = p;
+      if (o->manifest_op) o->manifest_op[p] = 0;
+      if (o->a_leaf_hashes) std::memcpy(o->a_leaf_hashes + 32 * p, aleaf, 32);
+    }
     return CG_OK;
   });
 }

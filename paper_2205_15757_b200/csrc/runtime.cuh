@@ -219,10 +219,11 @@ struct IngestSlot {
   // misfit requests (input dimension != the group's; execute_batch skips
   // them, engine.cpp:286-291): their inputs, flags, and an int32 -1 that the
   // skipped result-leaf jobs point their skip flag at
-  bool any_miss = false;
+  bool any_miss = false, any_kind = false;
   DevBuf<double> d_misfit;
-  DevBuf<uint8_t> d_miss;
-  DevBuf<int32_t> d_neg1;
+  DevBuf<uint8_t> d_miss;        // [B] no result, [B] has outcome, [B] explicit failure
+  DevBuf<int32_t> d_neg1, d_fail_pos;
+  uint32_t n_fail_jobs = 0;      // explicit failure-leaf jobs after the single leaves
   PinBuf<uint8_t> h_miss;
   PinBuf<uint8_t> h_arena, h_reqids;
   PinBuf<ChainJob> h_jobs;
@@ -245,7 +246,8 @@ struct cg_group {
   std::vector<cg_model*> models;          // local replicas (dist: just this rank's)
   std::vector<std::array<uint8_t, 32>> digests;  // weights digest of every provider
   bool dist = false;                      // replica-parallel over the ctx's NCCL ranks
-  uint32_t rank = 0;                      // this rank's provider index (dist)
+  uint32_t rank = 0;                      // this rank (dist)
+  uint32_t first = 0;                     // provider index of local replica 0 (dist: rank x local)
   uint32_t N = 0, f = 0, metric = 0, maxB = 0, topk = 1;
   double eps_default = 0;
   std::string gid;

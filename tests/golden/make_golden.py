@@ -21,6 +21,8 @@ them. Fixture contents:
                    3 models, batch 64, seed 7), every-5th-request fault
 * c1_misfit.npz  — a batch with two wrong-input-dimension requests
                    (missing_result_leaf, unsatisfied, failure leaves)
+* c1_slot.npz    — a mixed op list: ok / rejected requests, activate_group
+                   ops (0x52 / 0x4D / 0x47 R leaves, explicit failure leaves)
 * perturb.npz    — PerturbingExecutor(ToyExecutor, node, magnitude) outputs
                    over generate_group models with u in {1, 9, 3072} (0, 1
                    and 384 shared SHA blocks; 1- and 2-block lane tails), a
@@ -258,6 +260,47 @@ def c1_misfit_fixture(R):
     np.savez_compressed(os.path.join(OUT, "c1_misfit.npz"), **save)
 
 
+SLOT_KINDS = [0, 0, 1, 0, 2, 0, 0, 2, 0, 1, 0, 0]
+SLOT_REASONS = ["", "", "unknown group version", "", "", "", "", "group op rejected: retired",
+                "", "malformed request", "", ""]
+
+
+def c1_slot_fixture(R):
+    """A mixed PRE-PREPARE op list on the C1 models (u=512): ok requests,
+    two requests the primary rejected (no result: missing_result_leaf; A leaf
+    = their failure record with the reason) and two activate_group ops (R leaf
+    group_op_leaf; one rejected, with a failure leaf) -- build_result_tree
+    (messages.cpp:235-258) and the try_attest manifest with outcomes only for
+    the ok request ops. Also an empty slot's roots (noop leaf)."""
+    u, v, N, eps = 512, 10, 3, 0.05
+    gid = b"group-0"
+    files, digs = R.generate_group(gid, u, v, N, 0, eps, seed=7, softmax=False)
+    B = len(SLOT_KINDS)
+    inputs, encs_all = R.make_requests(1, 11, B, u, gid)
+    encs = [encs_all[k] if SLOT_KINDS[k] <= 1 else b"" for k in range(B)]
+    outs = np.zeros((N, B, v))
+    req = [k for k in range(B) if SLOT_KINDS[k] <= 1]
+    for p in range(N):
+        outs[p, req] = R.linear_run(files[p], inputs[req], v)
+    outs[2, 5] += 1.0  # one faulty provider on one op: no whole-batch leaf for 2
+    r = R.certify_slot(encs, SLOT_KINDS, SLOT_REASONS, N, 1, eps, outs, 1, digs)
+    save = dict(u=u, v=v, N=N, B=B, eps=eps, gid=np.frombuffer(gid, np.uint8),
+                kinds=np.array(SLOT_KINDS, np.uint8), inputs=inputs,
+                files=np.stack([np.frombuffer(f_, np.uint8) for f_ in files]),
+                digests=np.stack([np.frombuffer(d, np.uint8) for d in digs]),
+                req_lens=np.array([len(e) for e in encs], np.uint64),
+                reqs=np.frombuffer(b"".join(encs), np.uint8), outputs=outs,
+                entry_lens=np.array([len(e) for e in r["entries"]], np.uint64),
+                entries=np.frombuffer(b"".join(r["entries"]), np.uint8),
+                rec_lens=np.array([len(e) for e in r["records"]], np.uint64),
+                recs=np.frombuffer(b"".join(r["records"]) or b"\0", np.uint8),
+                sat=r["satisfied"],
+                r_roots=np.frombuffer(b"".join(r["r_roots"]), np.uint8).reshape(N, 32),
+                a_root=np.frombuffer(r["a_root"], np.uint8),
+                mlen=np.array(r["manifest_len"], np.uint64))
+    np.savez_compressed(os.path.join(OUT, "c1_slot.npz"), **save)
+
+
 # (u, v, softmax, node, magnitude, seed)
 PERTURB_CASES = [(1, 3, False, 0, 0.25, 11), (9, 5, False, 3, 1e-3, 12),
                  (3072, 10, False, 1, 0.05, 7), (3072, 10, True, 2, 1e-4, 7),
@@ -294,12 +337,16 @@ if __name__ == "__main__":
     if sys.argv[1:] == ["c1_misfit"]:
         c1_misfit_fixture(R)
         sys.exit(0)
+    if sys.argv[1:] == ["c1_slot"]:
+        c1_slot_fixture(R)
+        sys.exit(0)
     sha_fixture(R)
     merkle_fixture(R)
     quorum_fixture(R)
     c1_fixture(R)
     c1_full_fixture(R)
     c1_misfit_fixture(R)
+    c1_slot_fixture(R)
     perturb_fixture(R)
     for f in sorted(os.listdir(OUT)):
         if f.endswith(".npz"):

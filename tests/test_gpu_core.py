@@ -231,6 +231,86 @@ def test_certify_misfit_requests(ctx):
     grp.free()
 
 
+def _slot_batch(g):
+    """c1_slot.npz as a RequestBatch with its op-list structure: request ops
+    carry their request fields, group ops zeros (ignored)."""
+    from oracle.oracle import parse_request
+    from paper_2205_15757_b200 import RequestBatch
+    B, u = int(g["B"]), int(g["u"])
+    lens, buf = g["req_lens"], g["reqs"].tobytes()
+    ids, ins, pubs, nonces, sigs, eps, off = [], [], [], [], [], [], 0
+    for k in range(B):
+        n = int(lens[k])
+        if n:
+            f = parse_request(buf[off:off + n])
+            ids.append(np.frombuffer(f["request_id"], np.uint8))
+            ins.append(f["input"])
+            pubs.append(np.frombuffer(f["pub"], np.uint8))
+            nonces.append(f["nonce"])
+            sigs.append(np.frombuffer(f["sig"], np.uint8))
+            eps.append(f["eps"])
+        else:
+            ids.append(np.zeros(32, np.uint8))
+            ins.append(np.zeros(u))
+            pubs.append(np.zeros(32, np.uint8))
+            nonces.append(b"")
+            sigs.append(np.zeros(64, np.uint8))
+            eps.append(None)
+        off += n
+    def split(data, ls):
+        out, o = [], 0
+        for n in ls:
+            out.append(data[o:o + int(n)])
+            o += int(n)
+        return out
+    kinds = g["kinds"].tolist()
+    entries = split(g["entries"].tobytes(), g["entry_lens"])
+    return RequestBatch(np.stack(ids), np.stack(ins), np.stack(pubs), nonces, np.stack(sigs),
+                        eps if any(e is not None for e in eps) else None,
+                        op_kinds=kinds,
+                        op_entries=[e if kd == 2 else b"" for e, kd in zip(entries, kinds)],
+                        fail_records=split(g["recs"].tobytes(), g["rec_lens"]))
+
+
+def test_certify_mixed_slot(ctx):
+    """A PRE-PREPARE op list mixing ok requests, rejected requests and
+    activate_group ops (c1_slot.npz, from the compiled reference's
+    build_result_tree + try_attest manifest): R leaves 0x52 / 0x4D / 0x47,
+    outcomes only for ok request ops, explicit failure leaves -- bit-exact."""
+    g = golden("c1_slot.npz")
+    B = int(g["B"])
+    grp = _group(ctx, g, B)
+    batch = _slot_batch(g)
+    r = grp.certify_outputs(batch, g["outputs"])
+    assert np.array_equal(r["r_roots"], g["r_roots"])
+    assert int(r["manifest_len"][0]) == int(g["mlen"])
+    assert np.array_equal(r["a_root"], g["a_root"])
+    assert np.array_equal(r["satisfied"], g["sat"].astype(bool))
+    # and with the replicas' own forwards (the ok rows equal the fixture's
+    # honest outputs except the injected fault on provider 2, op 5)
+    r2 = grp.certify(batch, want_outputs=True)
+    ok = g["kinds"] == 0
+    want = g["outputs"].copy()
+    want[2, 5] -= 1.0
+    assert np.array_equal(r2["outputs"][:, ok], want[:, ok])
+    grp.free()
+
+
+def test_certify_empty_slot(ctx, oracle):
+    """An empty filler slot (messages.cpp:240-243): noop R leaves, N
+    whole-batch A leaves."""
+    import struct
+    g = golden("c1_slot.npz")
+    grp = _group(ctx, g, 4)
+    r = grp.certify_empty_slot(7, 42)
+    leaf = oracle.leaf_hash(b"\x4e" + struct.pack(">QQ", 7, 42))
+    assert all(x.tobytes() == leaf for x in r["r_roots"])
+    a = oracle.leaf_hash(b"\x57" + leaf)
+    assert r["a_root"].tobytes() == oracle.merkle_root([a] * int(g["N"]))
+    assert int(r["manifest_len"][0]) == int(g["N"])
+    grp.free()
+
+
 @pytest.mark.parametrize("variant", ["honest", "partial_fault", "failure"])
 def test_certify_outputs_fault_variants(ctx, variant):
     from paper_2205_15757_b200 import RequestBatch

@@ -45,22 +45,24 @@ def _worker(rank, world, port, N, f, q):
         ctx = Context(rank)
         uid = share_bytes(Context.nccl_unique_id() if rank == 0 else None)
         ctx.init_nccl(uid, world, rank)
-        (p,) = assigned_models(world, N, rank)  # bijection: |G| == d
-        m = Model.load_linear(ctx, g["files"][p].tobytes(), g["digests"][p].tobytes())
-        digests = [g["digests"][i].tobytes() for i in range(N)]
-        grp = ModelGroup.create_dist(ctx, m, digests, f, EUCLIDEAN, float(g["eps"]),
-                                     g["gid"].tobytes(), 1, max_batch=B, topk=3)
+        mine = assigned_models(world, N, rank)  # |G| == d: the bijection; else chunks
+        ms = [Model.load_linear(ctx, g["files"][p % 3].tobytes(), g["digests"][p % 3].tobytes())
+              for p in mine]
+        digests = [g["digests"][i % 3].tobytes() for i in range(N)]
+        grp = ModelGroup.create_dist(ctx, ms if len(ms) > 1 else ms[0], digests, f, EUCLIDEAN,
+                                     float(g["eps"]), g["gid"].tobytes(), 1, max_batch=B, topk=3)
         batch = RequestBatch.from_encoded(split_reqs(g))
         r1 = grp.certify(batch, want_outputs=True)
         # pipelined path: ingest ahead, certify later
         t0, t1 = grp.ingest(batch), grp.ingest(batch)
         grp.certify_ticket(t0)
         r2 = grp.certify_ticket(t1)
-        r3 = grp.certify_outputs(batch, g["partial_fault_outputs"][:N])
+        r3 = grp.certify_outputs(batch, g["partial_fault_outputs"][[i % 3 for i in range(N)]])
         out = {k: (r1[k], r2[k], r3[k]) for k in KEYS}
         out["outputs"] = r1["outputs"]
         grp.free()
-        m.free()
+        for m in ms:
+            m.free()
         ctx.close()
         dist.destroy_process_group()
         q.put((rank, out, None))
@@ -90,13 +92,13 @@ def _single(N, f):
     g = golden("c1_batch.npz")
     B = int(g["B"])
     ctx = Context(0)
-    ms = [Model.load_linear(ctx, g["files"][p].tobytes(), g["digests"][p].tobytes())
+    ms = [Model.load_linear(ctx, g["files"][p % 3].tobytes(), g["digests"][p % 3].tobytes())
           for p in range(N)]
     grp = ModelGroup(ctx, ms, f, EUCLIDEAN, float(g["eps"]), g["gid"].tobytes(), 1,
                      max_batch=B, topk=3)
     batch = RequestBatch.from_encoded(split_reqs(g))
     r1 = grp.certify(batch, want_outputs=True)
-    r3 = grp.certify_outputs(batch, g["partial_fault_outputs"][:N])
+    r3 = grp.certify_outputs(batch, g["partial_fault_outputs"][[i % 3 for i in range(N)]])
     out = {k: (r1[k], r3[k]) for k in KEYS}
     out["outputs"] = r1["outputs"]
     grp.free()
@@ -134,3 +136,20 @@ def test_dist_three_ranks_reference_golden():
         assert np.array_equal(out["label"][0], g["honest_label"]), rank
         assert np.array_equal(out["r_roots"][2], g["partial_fault_r_roots"]), rank
         assert out["a_root"][2].tobytes() == g["partial_fault_a_root"].tobytes(), rank
+
+
+@pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
+def test_dist_two_replicas_per_rank_equals_single_gpu_group():
+    """assigned_models chunking with |G| > d (domain.cpp:247-268): 4 providers
+    on 2 ranks, 2 local replicas per rank (cg_group_create_dist_multi), one
+    all-gather of 2 providers' outputs and R roots per rank."""
+    N, f = 4, 1
+    res = _run(2, N, f)
+    want = _single(N, f)
+    for rank, out in res.items():
+        assert np.array_equal(out["outputs"], want["outputs"]), rank
+        for k in KEYS:
+            r1, r2, r3 = out[k]
+            assert np.array_equal(r1, want[k][0]), (rank, k)
+            assert np.array_equal(r2, want[k][0]), (rank, k, "pipelined")
+            assert np.array_equal(r3, want[k][1]), (rank, k, "outputs")

@@ -48,3 +48,23 @@ def test_reference_requests_certified_on_every_gpu(tmp_path):
     print(out.stdout, out.stderr)
     assert out.returncode == 0, out.stdout + out.stderr
     assert f"{ndev} device(s)" in out.stdout and " 0 mismatches" in out.stdout
+
+
+SCENARIO = os.path.join(ROOT, "oracle", "_ref", "integration_scenario")
+
+
+def test_run_scenario_with_gpu_executor():
+    """§8(f)3 live integration: the reference's own simulated cluster
+    (run_scenario, N=4, f=1, PBFT ordering, proxies, clients) with every
+    node's ToyExecutor running on the GPU (CudaExecutor, wired at link time
+    where harness.cpp:255 builds executors): no deadlock, every request
+    certified, check_invariants() empty, and the rendered trace byte-identical
+    to the stock CPU run -- for the honest, agree_then_execute, corrupt-beyond
+    and corrupt-within-epsilon scenarios of tests/test_harness.cpp and a
+    C1-shaped (3072 -> 10) workload."""
+    if not os.path.exists(SCENARIO):
+        pytest.skip("oracle/_ref/integration_scenario not built (needs /root/reference at build time)")
+    out = subprocess.run([SCENARIO], capture_output=True, text=True, timeout=900)
+    print(out.stdout, out.stderr)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "0 failures" in out.stdout

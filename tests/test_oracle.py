@@ -273,6 +273,62 @@ def test_c1_misfit_golden(oracle):
     assert oracle.merkle_root(a) == g["a_root"].tobytes()
 
 
+def test_c1_slot_golden(oracle):
+    """The mixed op list (c1_slot.npz): the oracle's leaf constructions and
+    fold reproduce the reference's R roots, manifest and A root --
+    0x52 / 0x4D / 0x47 R leaves, outcomes only for ok request ops, failure
+    leaves from the ops' own FailureRecord bytes."""
+    from oracle.oracle import parse_request
+    g = golden("c1_slot.npz")
+    N, B, eps = int(g["N"]), int(g["B"]), float(g["eps"])
+    gid = g["gid"].tobytes()
+    kinds = g["kinds"]
+    lens, buf = g["req_lens"], g["reqs"].tobytes()
+    reqs, off = [], 0
+    for n in lens:
+        reqs.append(buf[off:off + int(n)])
+        off += int(n)
+    ents, recs, o1, o2 = [], [], 0, 0
+    for a, b in zip(g["entry_lens"], g["rec_lens"]):
+        ents.append(g["entries"].tobytes()[o1:o1 + int(a)])
+        recs.append(g["recs"].tobytes()[o2:o2 + int(b)])
+        o1 += int(a)
+        o2 += int(b)
+    sels, sats, res = {}, {}, {}
+    for k in range(B):
+        if kinds[k] == 0:
+            m, d, s_ = oracle.select_quorum(g["outputs"][:, k], list(range(N)), N, 1, 0, eps)
+            sels[k], sats[k] = m, s_
+    for p in range(N):
+        hs = []
+        for k in range(B):
+            if kinds[k] == 0:
+                f = parse_request(reqs[k])
+                res[(k, p)] = oracle.result_encode(f["request_id"], p, gid, 1,
+                                                   g["outputs"][p, k], g["digests"][p].tobytes())
+                hs.append(oracle.tagged_leaf_hash(0x52, reqs[k], res[(k, p)]))
+            elif kinds[k] == 1:
+                hs.append(oracle.tagged_leaf_hash(0x4D, reqs[k], b""))
+            else:
+                hs.append(oracle.leaf_hash(b"\x47" + ents[k]))
+        assert oracle.merkle_root(hs) == g["r_roots"][p].tobytes(), p
+    whole = [p for p in range(N) if all(sats[k] and sels[k] >> p & 1 for k in sats)]
+    a = [oracle.leaf_hash(b"\x57" + g["r_roots"][p].tobytes()) for p in whole]
+    for k in sorted(sats):
+        if sats[k]:
+            for p in range(N):
+                if sels[k] >> p & 1 and p not in whole:
+                    a.append(oracle.tagged_leaf_hash(0x53, reqs[k], res[(k, p)]))
+    for k in range(B):
+        if kinds[k] == 0 and not sats[k]:
+            rid = parse_request(reqs[k])["request_id"]
+            a.append(oracle.leaf_hash(oracle.failure_leaf(rid, gid, 1)))
+        elif recs[k]:
+            a.append(oracle.leaf_hash(b"\x46" + recs[k]))
+    assert len(a) == int(g["mlen"])
+    assert oracle.merkle_root(a) == g["a_root"].tobytes()
+
+
 def test_label_digest_layout(oracle):
     """The compact agreed-label digest (new, C5 'D2') is plain SHA-256 over
     0x4C || id || u64be version || u64be label; pinned by the SHA KATs."""
