@@ -462,6 +462,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   static_assert(!PAIR || (RESB == 0 && (HALO == 0 || kResSlots == 0)), "pair: streamed weights");
   constexpr int B_BYTES = (PAIR ? BN / 2 : BN) * BK * 2;  // this CTA's weight tile
   constexpr uint32_t TMEM_COLS = 2 * BN;
+  // BN = 64 (2 chunks of 32 columns): the two epilogue warp groups take
+  // alternate tiles whole; wider tiles split their chunks between the groups.
+  // An accumulator is released (tempty) by exactly the warps that drained it.
+  constexpr bool kTileSplit = BN == 64;
+  constexpr int kDrainWarps = kTileSplit ? kEpiWarps / 2 : kEpiWarps;
   // residual ring: 128-row boxes of kResCols columns (64: 128-byte rows, SW128;
   // half the TMA row requests of 32-column SW64 boxes) in kResSlots x 8 KB
   constexpr int kResCols = CG_RES_COLS;
@@ -542,7 +547,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int s = 0; s < 2; s++) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], kEpiWarps * (PAIR ? 2 : 1));  // pair: both CTAs' epilogues
+      mbar_init(&tempty[s], kDrainWarps * (PAIR ? 2 : 1));  // pair: both CTAs' epilogues
     }
     for (int s = 0; s < kResSlots; s++) {
       mbar_init(&rfull[s], 1);
@@ -873,7 +878,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     // BN = 64 (2 chunks): the two warp groups take alternate tiles whole
     // (both TMEM accumulators drained concurrently) instead of one chunk
     // each of the same tile; wider tiles split chunks between the groups.
-    constexpr bool kTileSplit = BN == 64;
     constexpr int C0S = kTileSplit ? 1 : 2;  // chunk stride of one warp
     int tile_i = 0, acc = 0;
     int stage_seq = 0;  // staging buffer sequence across all of this warp's chunks
@@ -882,12 +886,10 @@ __global__ void __launch_bounds__(kThreads, 1)
          ok = sched.next(false, lane == 0), tile_i++) {
       const int t = sched.t;
       if (kTileSplit && (tile_i & 1) != h) {
-        // the other group drains this accumulator; release our share of it
-        __syncwarp();
-        if (lane == 0) {
-            if (PAIR && crank == 1) mbar_arrive_cluster(mapa_cluster(&tempty[acc], 0));
-            else mbar_arrive(&tempty[acc]);
-          }
+        // the other group drains (and releases) this accumulator. Arriving
+        // here as well would let this group, running ahead on its own odd
+        // tiles, complete the NEXT phase of tempty[acc] while the other
+        // group still reads the accumulator.
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         continue;
       }
