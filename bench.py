@@ -359,7 +359,12 @@ def bench_gpu(args, rank, world, local_rank):
     from paper_2205_15757_b200 import InferenceEngine
     eng = InferenceEngine(ctx, B, 10**12, pack_threads=args.pack_threads)
     eng.load_group(grp)
-    prepared = [eng.prepare(b, b"group-0") for b in batches]
+    # K distinct signed batches (the engine's seen-dedup absorbs repeats);
+    # their inputs share the two 154 MB arrays' rows, the pack still copies
+    # every request's 1.2 MB into pinned staging
+    e2e_batches = [signed_requests(B, U, seed=10_000 + 100 * rank + i,
+                                   inputs=batches[i % nb].inputs) for i in range(args.steps)]
+    prepared = [eng.prepare(b, b"group-0") for b in e2e_batches]
     barrier()
     torch.cuda.synchronize()
     e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -377,7 +382,7 @@ def bench_gpu(args, rank, world, local_rank):
     def fetch_oldest():
         return int(np.sum(grp.fetch_ticket(inflight.popleft())["satisfied"]))
     for i in range(args.steps):
-        eng.submit_prepared(prepared[i % nb], now_us=i)  # one full batch of B per step
+        eng.submit_prepared(prepared[i], now_us=i)  # one full batch of B per step
         ready_q.extend(eng.ready())
         while len(ready_q) > D:
             certify_oldest()
@@ -814,7 +819,7 @@ def bench_c1(args, rank, world, local_rank):
               for p in range(N)]
     grp = ModelGroup(ctx, models, 1, EUCLIDEAN, float(g["eps"]), g["gid"].tobytes(), 1,
                      max_batch=B, topk=5)
-    nb = 100
+    nb = max(100, args.steps)  # distinct batches: the batch former dedups repeats
     batches = [signed_requests(B, u, seed=1000 + rank * nb + i) for i in range(nb)]
     dev = []
     for b in batches:
@@ -844,7 +849,7 @@ def bench_c1(args, rank, world, local_rank):
     from collections import deque
     ready_q, inflight, certified = deque(), deque(), 0
     for i in range(args.steps):
-        eng.submit_prepared(prepared[i % nb], now_us=i)
+        eng.submit_prepared(prepared[i % nb], now_us=i)  # nb = 100 distinct batches
         ready_q.extend(eng.ready())
         while len(ready_q) > D:
             gq, _, t, Bt = ready_q.popleft()

@@ -668,7 +668,10 @@ __global__ void __launch_bounds__(kManThreads) attest_manifest_kernel(
     }
     __syncthreads();
   }
-  if (tid == 0) *count = nwhole + nsingle + (s_carry_fail - nsingle);
+  if (tid == 0) {
+    count[0] = nwhole + nsingle + (s_carry_fail - nsingle);
+    count[1] = nsingle;
+  }
 }
 
 void launch_attest_manifest(uint32_t B, uint32_t N, const uint32_t* sel,

@@ -878,16 +878,16 @@ uint64_t ingest(cg_group* g, const cg_request_batch* bt) {
   S.d_in_ptr = bt->inputs_on_device ? bt->inputs : S.d_in.p;
   S.any_miss = any_miss;
   S.any_kind = any_kind;
+  if (!S.d_neg1.p) {
+    const int32_t neg1 = -1;
+    S.d_neg1.ensure(1);
+    CG_CUDA(cudaMemcpy(S.d_neg1.p, &neg1, 4, cudaMemcpyHostToDevice));
+  }
   if (any_miss) {
     S.d_misfit.ensure(std::max<uint64_t>(misfit_total, 1));
     S.d_miss.ensure(3 * (uint64_t)g->maxB);  // missing, has-outcome, explicit-failure flags
     S.h_miss.ensure(3 * (uint64_t)g->maxB);
     S.d_fail_pos.ensure(g->maxB);
-    if (!S.d_neg1.p) {
-      const int32_t neg1 = -1;
-      S.d_neg1.ensure(1);
-      CG_CUDA(cudaMemcpy(S.d_neg1.p, &neg1, 4, cudaMemcpyHostToDevice));
-    }
     for (uint32_t k = 0; k < B; k++) {
       S.h_miss.p[k] = rl[k].noresult ? 1 : 0;
       S.h_miss.p[B + k] = rl[k].kind == CG_OP_REQUEST ? 1 : 0;
@@ -988,6 +988,33 @@ uint64_t ingest(cg_group* g, const cg_request_batch* bt) {
         jobs.push_back(j);
       }
   }
+  // single attestation leaves H(0x00||0x53||req||res) (messages.cpp:283-290):
+  // the manifest kernel decides on device which (request, provider) pairs
+  // need one and where it lands; the request part H(0x00||0x53||req) is one
+  // midstate per request. Lazy (default): chained after the manifest only for
+  // requests that have a single leaf. Speculative (after recent batches had
+  // single leaves, g->spec53): chained at ingest with the request midstates,
+  // so a faulty stream's 1.2 MB chains are off the certification path.
+  S.spec53 = g->spec53 > 0;
+  auto push_mid53 = [&] {
+    S.off_mid53 = jobs.size();
+    for (uint32_t k = 0; k < B; k++) {
+      const ReqLayout& L = rl[k];
+      ChainJob j;
+      std::memset(&j, 0, sizeof j);
+      j.seg[0] = seg_raw(A + L.h53, 0, L.lenH);
+      j.seg[1] = seg_f64(L.in_mis ? MIS + 8 * L.moff : IN + 8 * u * k, L.lenH, 8 * L.uk);
+      j.seg[2] = seg_raw(A + L.t, L.lenH + 8 * L.uk, L.lenT);
+      j.nseg = 3;
+      j.total_len = L.P;
+      j.blk_end = L.P / 64;
+      j.state_out = (uint64_t)(S.d_mid53.p + 8 * k);
+      if (!S.spec53 || L.noresult) j.skip_flag = (uint64_t)(S.res.d_need53.p + k);
+      if (S.spec53 && L.noresult) j.skip_flag = (uint64_t)S.d_neg1.p;
+      jobs.push_back(j);
+    }
+  };
+  if (S.spec53) push_mid53();
   const uint64_t n_prefix = jobs.size();
   // result leaves H(0x00||0x52||req||res) from the request midstate
   S.off_leaf = jobs.size();
@@ -1000,25 +1027,7 @@ uint64_t ingest(cg_group* g, const cg_request_batch* bt) {
       if (rl[k].noresult) j.skip_flag = (uint64_t)S.d_neg1.p;  // written at ingest (0x4D / 0x47)
       jobs.push_back(j);
     }
-  // single attestation leaves H(0x00||0x53||req||res) (messages.cpp:283-290):
-  // the manifest kernel decides on device which (request, provider) pairs
-  // need one and where it lands; the request part H(0x00||0x53||req) is one
-  // midstate per request, chained only for requests that have a single leaf
-  S.off_mid53 = jobs.size();
-  for (uint32_t k = 0; k < B; k++) {
-    const ReqLayout& L = rl[k];
-    ChainJob j;
-    std::memset(&j, 0, sizeof j);
-    j.seg[0] = seg_raw(A + L.h53, 0, L.lenH);
-    j.seg[1] = seg_f64(L.in_mis ? MIS + 8 * L.moff : IN + 8 * u * k, L.lenH, 8 * L.uk);
-    j.seg[2] = seg_raw(A + L.t, L.lenH + 8 * L.uk, L.lenT);
-    j.nseg = 3;
-    j.total_len = L.P;
-    j.blk_end = L.P / 64;
-    j.state_out = (uint64_t)(S.d_mid53.p + 8 * k);
-    j.skip_flag = (uint64_t)(S.res.d_need53.p + k);
-    jobs.push_back(j);
-  }
+  if (!S.spec53) push_mid53();
   S.off_single = jobs.size();
   for (uint32_t k = 0; k < B; k++)
     for (uint32_t p = 0; p < N; p++) {
@@ -1230,7 +1239,7 @@ void certify(cg_group* g, uint64_t ticket, const double* precomputed_outputs) {
   // tails; requests without a single leaf skip their 0x53 midstate chain.
   CG_CUDA(cudaEventRecord(S.ev_man, tl));
   CG_CUDA(cudaStreamWaitEvent(S.stream, S.ev_man, 0));
-  launch_chain_jobs(S.d_jobs.p + S.off_mid53, B, S.stream, /*exclusive_sm=*/true);
+  if (!S.spec53) launch_chain_jobs(S.d_jobs.p + S.off_mid53, B, S.stream, /*exclusive_sm=*/true);
   launch_chain_jobs(S.d_jobs.p + S.off_single, N * B + S.n_fail_jobs, S.stream);
   launch_merkle_trees(R.d_aleaf.p, nullptr, nullptr, R.d_count.p, 1, (uint64_t)N * B + B + N,
                       R.d_aroot.p, S.stream);
@@ -1253,9 +1262,9 @@ void certify_fetch(cg_group* g, cg_certify_out* o, const IngestSlot* slot) {
     if (dst) CG_CUDA(cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToHost, st));
   };
   std::vector<int8_t> status(B);
-  uint32_t count = 0;
+  uint32_t count[2] = {0, 0};  // manifest entries, single leaves
   d2h(status.data(), R.d_status.p, B);
-  d2h(&count, R.d_count.p, 4);
+  d2h(count, R.d_count.p, 8);
   d2h(o->selected, R.d_sel.p, 4 * (size_t)B);
   d2h(o->diameter, R.d_diam.p, 8 * (size_t)B);
   d2h(o->satisfied, R.d_sat.p, B);
@@ -1267,11 +1276,15 @@ void certify_fetch(cg_group* g, cg_certify_out* o, const IngestSlot* slot) {
   d2h(o->topk_idx, R.d_topi.p, 4 * (size_t)N * B * g->topk);
   d2h(o->topk_val, R.d_topv.p, 8 * (size_t)N * B * g->topk);
   CG_CUDA(cudaStreamSynchronize(st));
-  if (o->manifest_len) *o->manifest_len = count;
-  d2h(o->manifest_kind, R.d_kinds.p, count);
-  d2h(o->manifest_node, R.d_mnodes.p, 4 * (size_t)count);
-  d2h(o->manifest_op, R.d_mops.p, 4 * (size_t)count);
-  d2h(o->a_leaf_hashes, R.d_aleaf.p, 32 * (size_t)count);
+  if (o->manifest_len) *o->manifest_len = count[0];
+  d2h(o->manifest_kind, R.d_kinds.p, count[0]);
+  d2h(o->manifest_node, R.d_mnodes.p, 4 * (size_t)count[0]);
+  d2h(o->manifest_op, R.d_mops.p, 4 * (size_t)count[0]);
+  d2h(o->a_leaf_hashes, R.d_aleaf.p, 32 * (size_t)count[0]);
+  // a stream that produces single leaves gets its 0x53 request midstates
+  // chained speculatively at ingest for the next ring's worth of batches
+  if (count[1]) g->spec53 = 2 * (uint32_t)g->slots.size();
+  else if (g->spec53) g->spec53--;
   CG_CUDA(cudaStreamSynchronize(st));
   for (uint32_t k = 0; k < B; k++)
     if (status[k] != 0) throw InvalidArgument("select_quorum: invalid argument");
@@ -1371,7 +1384,7 @@ int create_group(cg_ctx* ctx, cg_model* const* models, uint32_t nlocal, uint32_t
       S->res.d_mnodes.ensure(amax);
       S->res.d_mops.ensure(amax);
       S->res.d_kinds.ensure(amax);
-      S->res.d_count.ensure(1);
+      S->res.d_count.ensure(2);
       S->res.d_leaf.ensure(32 * (uint64_t)N * B);
       S->res.d_rroots.ensure(32 * (uint64_t)N);
       S->res.d_aleaf.ensure(32 * amax);

@@ -224,6 +224,7 @@ struct IngestSlot {
   DevBuf<uint8_t> d_miss;        // [B] no result, [B] has outcome, [B] explicit failure
   DevBuf<int32_t> d_neg1, d_fail_pos;
   uint32_t n_fail_jobs = 0;      // explicit failure-leaf jobs after the single leaves
+  bool spec53 = false;           // 0x53 request midstates chained at ingest
   PinBuf<uint8_t> h_miss;
   PinBuf<uint8_t> h_arena, h_reqids;
   PinBuf<ChainJob> h_jobs;
@@ -274,6 +275,9 @@ struct cg_group {
   // byte is < fault_thr (0: no fault)
   uint32_t fault_provider = 0, fault_thr = 0;
   double fault_offset = 0;
+  // batches left to ingest with speculative 0x53 midstates (set when a
+  // fetched batch had single-attestation leaves)
+  uint32_t spec53 = 0;
 };
 
 namespace cg {
