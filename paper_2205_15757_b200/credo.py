@@ -642,6 +642,8 @@ class ModelGroup:
         self.h = h
         self._keep = None
 
+    ring = 24  # CG_INGEST_RING: batches in flight per group
+
     @classmethod
     def create_dist(cls, ctx: Context, my_model, digests: Sequence[bytes],
                     f: int, metric: int, default_eps: float, group_id: bytes,
