@@ -1251,7 +1251,11 @@ void certify(cg_group* g, uint64_t ticket, const double* precomputed_outputs) {
 }
 
 void certify_fetch(cg_group* g, cg_certify_out* o, const IngestSlot* slot) {
-  cudaStream_t st = g->ctx->stream;
+  // The readback waits for this batch's own completion only (ev_done), on
+  // the context's side stream: on the launch stream it would queue behind
+  // every forward enqueued since, and the host would drain the pipeline on
+  // each fetch.
+  cudaStream_t st = g->ctx->side;
   if (!slot) slot = g->last;
   if (!slot || !slot->certified) throw InvalidArgument("nothing certified yet");
   const uint32_t B = slot->B, N = g->N;

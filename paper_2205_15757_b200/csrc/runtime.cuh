@@ -113,7 +113,7 @@ struct cg_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = true;
-  cudaStream_t side = nullptr;
+  cudaStream_t side = nullptr;  // result readback (certify_fetch): waits on one batch only
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;
   std::string err;
   std::mutex mu;
