@@ -333,7 +333,7 @@ def bench_gpu(args, rank, world, local_rank):
     # (10 % of the (request, replica) pairs): single-attestation leaves --
     # a 0x53 request midstate per request where provider 2 is in the quorum
     fault = None
-    if not replica and args.workload == "c2" and not args.no_fault:
+    if not replica and args.workload == "c2" and not args.no_fault and not args.quick:
         grp.set_fault(2, 1.0, 0.3)
         # untimed: the stream's first single leaves switch the group to
         # speculative 0x53 midstates (chained at ingest), its steady state
@@ -353,6 +353,7 @@ def bench_gpu(args, rank, world, local_rank):
                  "satisfied_fraction": fsat,
                  "ratio_to_honest": round((fsat / max(sat_dev, 1e-9)) * (ms / fms), 4)}
 
+    e2e, ms_e2e, host_e2e = None, 0.0, 0.0
     # ---- end to end through the public API: the batch former ----
     # Every step submits B requests (InferenceEngine::submit: structural
     # checks, seen-dedup, packing each request's pageable f64 input into
@@ -362,63 +363,10 @@ def bench_gpu(args, rank, world, local_rank):
     from collections import deque
 
     from paper_2205_15757_b200 import InferenceEngine
-    eng = InferenceEngine(ctx, B, 10**12, pack_threads=args.pack_threads)
-    eng.load_group(grp)
-    # K distinct signed batches (the engine's seen-dedup absorbs repeats);
-    # their inputs share the two 154 MB arrays' rows, the pack still copies
-    # every request's 1.2 MB into pinned staging
-    e2e_batches = [signed_requests(B, U, seed=10_000 + 100 * rank + i,
-                                   inputs=batches[i % nb].inputs) for i in range(args.steps)]
-    prepared = [eng.prepare(b, b"group-0") for b in e2e_batches]
-    # untimed warm-up with other requests: the engine's pinned staging and
-    # every ingest slot's device input buffer get allocated here
-    warm = [eng.prepare(signed_requests(B, U, seed=20_000 + 100 * rank + i,
-                                        inputs=batches[i % nb].inputs), b"group-0")
-            for i in range(min(grp.ring, D + LAG + 4))]
-    wq = deque()
-    for i, w in enumerate(warm):
-        eng.submit_prepared(w, now_us=i)
-        for gq, _, t, Bt in eng.ready():
-            gq.certify_ticket(t, sync=False, B=Bt)
-            wq.append(t)
-        while len(wq) > LAG:
-            grp.fetch_ticket(wq.popleft())
-    while wq:
-        grp.fetch_ticket(wq.popleft())
-    ctx.join()
-    barrier()
-    torch.cuda.synchronize()
-    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e2.record(stream)
-    h2 = time.perf_counter()
-    certified = 0
-    ready_q, inflight = deque(), deque()
+    if not args.quick:
+        e2e, ms_e2e, host_e2e = e2e_leg(args, ctx, grp, batches, B, D, LAG, rank, jobs, stream,
+                                        barrier, max_over_ranks)
 
-    def certify_oldest():
-        grp_, _, t, Bt = ready_q.popleft()
-        grp_.certify_ticket(t, sync=False, B=Bt)
-        inflight.append(t)
-
-    def fetch_oldest():
-        return int(np.sum(grp.fetch_ticket(inflight.popleft())["satisfied"]))
-    for i in range(args.steps):
-        eng.submit_prepared(prepared[i], now_us=i)  # one full batch of B per step
-        ready_q.extend(eng.ready())
-        while len(ready_q) > D:
-            certify_oldest()
-        while len(inflight) > LAG:
-            certified += fetch_oldest()
-    while ready_q:
-        certify_oldest()
-    while inflight:
-        certified += fetch_oldest()
-    ctx.join()
-    e3.record(stream)
-    torch.cuda.synchronize()
-    host_e2e = time.perf_counter() - h2
-    ms_e2e = max_over_ranks(e2.elapsed_time(e3))
-    e2e = jobs * certified / (ms_e2e / 1e3)
-    eng.free()
     h2d = B * U * 8
     d2h = B * (4 + 8 + 1 + 8) + grp.N * 32 + 32 + 8
 
@@ -500,7 +448,7 @@ def bench_gpu(args, rank, world, local_rank):
                       "pipeline": f"cold start + full drain inside the region: ingest {D} "
                                   f"batches ahead (request-midstate SHA chains overlap the "
                                   f"forwards), decisions read back {LAG} steps behind"},
-           "e2e": {"value": round(e2e, 1), "unit": UNIT, "h2d_bytes_per_step": h2d,
+           "e2e": None if e2e is None else {"value": round(e2e, 1), "unit": UNIT, "h2d_bytes_per_step": h2d,
                    "d2h_bytes_per_step": d2h, "ms_per_step": round(ms_e2e / args.steps, 3),
                    "host_s": round(host_e2e, 3),
                    "path": "InferenceEngine.submit of B requests per step (structural checks, "
@@ -511,7 +459,7 @@ def bench_gpu(args, rank, world, local_rank):
            "gpu_launches": int(launches),
            "roofline": roofline,
            "clocks": clk.summary()}
-    if rank == 0 and not replica and args.workload == "c2":
+    if rank == 0 and not replica and args.workload == "c2" and not args.quick:
         out["host_hash_ops"] = host_hash_ops(batches, os.cpu_count() or 1, 16)
     if args.workload == "c3":
         from paper_2205_15757_b200.workload import HETERO_GROUP
@@ -529,11 +477,79 @@ def bench_gpu(args, rank, world, local_rank):
                      "all-gathered over NCCL",
             replicas=grp.N, f=replica_f(grp.N), global_batch=B,
             parallelism=f"replica-parallel x{world} (rank = provider chunk, assigned_models)")
-    if world == 1 and not args.no_cpu_baseline:  # the CPU baseline is timed at N=1 only
+    if world == 1 and not args.no_cpu_baseline and not args.quick:  # timed at N=1 only
         archs = [m.arch for m in models] if args.workload == "c3" else ["resnet50"] * 3
         out["cpu_baseline"] = cpu_baseline(archs, digs, sds, batches[0], args,
                                            grp.default_eps)
     return out
+
+
+def e2e_leg(args, ctx, grp, batches, B, D, LAG, rank, jobs, stream, barrier, max_over_ranks):
+    import torch
+    from collections import deque
+
+    from paper_2205_15757_b200 import InferenceEngine
+    from paper_2205_15757_b200.workload import signed_requests
+    nb = len(batches)
+    eng = InferenceEngine(ctx, B, 10**12, pack_threads=args.pack_threads)
+    eng.load_group(grp)
+    # K distinct signed batches (the engine's seen-dedup absorbs repeats);
+    # their inputs share the two 154 MB arrays' rows, the pack still copies
+    # every request's 1.2 MB into pinned staging
+    e2e_batches = [signed_requests(B, U, seed=10_000 + 100 * rank + i,
+                                   inputs=batches[i % nb].inputs) for i in range(args.steps)]
+    prepared = [eng.prepare(b, b"group-0") for b in e2e_batches]
+    # untimed warm-up with other requests: the engine's pinned staging and
+    # every ingest slot's device input buffer get allocated here
+    warm = [eng.prepare(signed_requests(B, U, seed=20_000 + 100 * rank + i,
+                                        inputs=batches[i % nb].inputs), b"group-0")
+            for i in range(min(grp.ring, D + LAG + 4))]
+    wq = deque()
+    for i, w in enumerate(warm):
+        eng.submit_prepared(w, now_us=i)
+        for gq, _, t, Bt in eng.ready():
+            gq.certify_ticket(t, sync=False, B=Bt)
+            wq.append(t)
+        while len(wq) > LAG:
+            grp.fetch_ticket(wq.popleft())
+    while wq:
+        grp.fetch_ticket(wq.popleft())
+    ctx.join()
+    barrier()
+    torch.cuda.synchronize()
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2.record(stream)
+    h2 = time.perf_counter()
+    certified = 0
+    ready_q, inflight = deque(), deque()
+
+    def certify_oldest():
+        grp_, _, t, Bt = ready_q.popleft()
+        grp_.certify_ticket(t, sync=False, B=Bt)
+        inflight.append(t)
+
+    def fetch_oldest():
+        return int(np.sum(grp.fetch_ticket(inflight.popleft())["satisfied"]))
+    for i in range(args.steps):
+        eng.submit_prepared(prepared[i], now_us=i)  # one full batch of B per step
+        ready_q.extend(eng.ready())
+        while len(ready_q) > D:
+            certify_oldest()
+        while len(inflight) > LAG:
+            certified += fetch_oldest()
+    while ready_q:
+        certify_oldest()
+    while inflight:
+        certified += fetch_oldest()
+    ctx.join()
+    e3.record(stream)
+    torch.cuda.synchronize()
+    host_e2e = time.perf_counter() - h2
+    ms_e2e = max_over_ranks(e2.elapsed_time(e3))
+    e2e = jobs * certified / (ms_e2e / 1e3)
+    eng.free()
+    return e2e, ms_e2e, host_e2e
+
 
 
 # ------------------------------------------------------------ CPU baseline
@@ -1107,6 +1123,9 @@ def main():
                     help="host threads packing request inputs into pinned staging (e2e)")
     ap.add_argument("--no-fault", action="store_true",
                     help="skip the corrupt_result fault-path measurement")
+    ap.add_argument("--quick", action="store_true",
+                    help="A/B mode: value + GEMM attribution only (no e2e, fault, "
+                         "hash_ops or CPU baseline legs)")
     ap.add_argument("--mode", default="group", choices=["group", "replica"],
                     help="group: a whole 3-replica group per GPU (weak scaling); "
                          "replica: one replica per GPU, NCCL all-gather (N>1)")
