@@ -757,7 +757,7 @@ IngestSlot& slot_for(cg_group* g, uint64_t ticket) {
 // InferenceEngine::submit's hot part (engine.cpp:182-209): take the batch,
 // build the canonical framing bytes of every leaf it will need, upload, and
 // start the request-midstate chains H(0x00||0x52||request)[whole blocks].
-uint64_t ingest(cg_group* g, const cg_request_batch* bt) {
+uint64_t ingest(cg_group* g, const cg_request_batch* bt, cudaEvent_t staged) {
   const uint32_t B = bt->B, N = g->N;
   const uint64_t u = bt->u, v = g->v;
   if (B == 0) throw InvalidArgument("empty batch");
@@ -1078,6 +1078,7 @@ uint64_t ingest(cg_group* g, const cg_request_batch* bt) {
   if (!bt->inputs_on_device)
     CG_CUDA(cudaMemcpyAsync(S.d_in.p, bt->inputs, 8 * u * B, cudaMemcpyHostToDevice, st));
   CG_CUDA(cudaEventRecord(S.ev_staged, st));
+  if (staged) CG_CUDA(cudaEventRecord(staged, st));  // the caller's staging is free again
   launch_chain_jobs(S.d_jobs.p, (uint32_t)n_prefix, st, /*exclusive_sm=*/true);
   CG_CUDA(cudaEventRecord(S.ev_prefix, st));
   S.used = true;

@@ -15,7 +15,10 @@
 // nonce and input, finite non-negative epsilon override, request id ==
 // canonical id) run here; the Ed25519 signature check is the caller's (an
 // optional host callback), it needs the caller's signature library.
+#include <chrono>
 #include <condition_variable>
+#include <cstdio>
+#include <cstdlib>
 #include <functional>
 #include <map>
 #include <set>
@@ -128,6 +131,10 @@ struct cg_engine {
   std::unique_ptr<PackPool> pack;
   cg_sig_verify_fn verify = nullptr;
   void* verify_user = nullptr;
+  // CREDO_ENGINE_PROFILE=1: host seconds per submit phase, printed at free
+  bool prof = std::getenv("CREDO_ENGINE_PROFILE") != nullptr;
+  double t_stage = 0, t_pack = 0, t_ingest = 0;
+  uint64_t n_submits = 0;
 };
 
 namespace {
@@ -188,8 +195,9 @@ void drain_released(cg_engine* e) {
           b.input_dims = f->dims.p;
           b.misfit_inputs = f->misfit_ptr.data();
         }
-        const uint64_t t = ingest(g, &b);
-        CG_CUDA(cudaEventRecord(f->ev, g->slots[t % g->slots.size()]->stream));
+        // f->ev fires when the H2D copies out of this staging are done (not
+        // after the 35 ms request-midstate chains queued behind them)
+        const uint64_t t = ingest(g, &b, f->ev);
         e->ready.push_back(cg_ready_batch{g, ver, t, f->n});
         f->n = 0;
         f->nonce_bytes = 0;
@@ -244,6 +252,10 @@ int cg_engine_create(cg_ctx* ctx, uint64_t exec_batch_max, uint64_t flush_interv
 
 void cg_engine_free(cg_engine* e) {
   if (!e) return;
+  if (e->prof && e->n_submits)
+    std::fprintf(stderr, "cg_engine: %lu submits, ms per submit: stage %.3f pack %.3f ingest %.3f\n",
+                 (unsigned long)e->n_submits, 1e3 * e->t_stage / e->n_submits,
+                 1e3 * e->t_pack / e->n_submits, 1e3 * e->t_ingest / e->n_submits);
   cudaSetDevice(e->ctx->device);
   for (auto& [gid, versions] : e->groups)
     for (auto& [ver, V] : versions)
@@ -299,6 +311,8 @@ int cg_engine_submit(cg_engine* e, const cg_request* reqs, uint32_t n, uint64_t 
                      int* errors) {
   if (!e || (n && !reqs)) return CG_EINVAL;
   return guarded(e->ctx, [&] {
+    using clk = std::chrono::steady_clock;
+    const auto t0 = clk::now();
     struct Copy {
       const double* src;
       double* dst;
@@ -377,9 +391,11 @@ int cg_engine_submit(cg_engine* e, const cg_request* reqs, uint32_t n, uint64_t 
     }
     // the packing copies (1.2 MB per ImageNet request) on the pack threads,
     // before any of these batches is ingested
+    const auto t1 = clk::now();
     e->pack->run(copies.size(), [&](size_t i) {
       std::memcpy(copies[i].dst, copies[i].src, 8 * copies[i].count);
     });
+    const auto t2 = clk::now();
     for (auto& [gid, versions] : e->groups)
       for (auto& [ver, V] : versions)
         for (auto& f : V.released)
@@ -388,6 +404,13 @@ int cg_engine_submit(cg_engine* e, const cg_request* reqs, uint32_t n, uint64_t 
             for (uint32_t k = 0; k < f->n; k++) f->misfit_ptr[k] = f->misfit[k].data();
           }
     drain_released(e);
+    if (e->prof) {
+      const auto t3 = clk::now();
+      e->t_stage += std::chrono::duration<double>(t1 - t0).count();
+      e->t_pack += std::chrono::duration<double>(t2 - t1).count();
+      e->t_ingest += std::chrono::duration<double>(t3 - t2).count();
+      e->n_submits++;
+    }
     return CG_OK;
   });
 }

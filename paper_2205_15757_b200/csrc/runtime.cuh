@@ -282,7 +282,9 @@ struct cg_group {
 
 namespace cg {
 // capi.cu: the per-batch pipeline
-uint64_t ingest(cg_group* g, const cg_request_batch* bt);
+// staged (optional): recorded once the batch's host buffers have been copied
+// (before the request-midstate chains), so the caller may reuse them
+uint64_t ingest(cg_group* g, const cg_request_batch* bt, cudaEvent_t staged = nullptr);
 void certify(cg_group* g, uint64_t ticket, const double* precomputed_outputs);
 void certify_fetch(cg_group* g, cg_certify_out* o, const IngestSlot* slot = nullptr);
 // the context stream waits for every group slot's outstanding work
