@@ -36,7 +36,11 @@
 namespace cg {
 
 static std::atomic<uint64_t> g_launches{0};
-uint64_t launch_counter_add(uint64_t n) { return g_launches += n; }
+thread_local std::atomic<uint64_t>* tl_ctx_launches = nullptr;
+uint64_t launch_counter_add(uint64_t n) {
+  if (tl_ctx_launches) *tl_ctx_launches += n;
+  return g_launches += n;
+}
 
 // ------------------------------------------------------------ kernel timers
 struct Timers {
@@ -224,7 +228,9 @@ int cg_ctx_join(cg_ctx* ctx) {
   });
 }
 
-uint64_t cg_ctx_launch_count(const cg_ctx*) { return g_launches.load(); }
+uint64_t cg_ctx_launch_count(const cg_ctx* ctx) {
+  return ctx ? ctx->launches.load() : g_launches.load();
+}
 
 int cg_nccl_unique_id(uint8_t out[128]) {
   ncclUniqueId id;

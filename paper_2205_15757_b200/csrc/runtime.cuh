@@ -136,6 +136,7 @@ struct cg_ctx {
   cudaStream_t tail = nullptr;
   // groups created on this context (cg_ctx_join drains their slot streams)
   std::vector<cg_group*> groups;
+  std::atomic<uint64_t> launches{0};  // kernels launched by this context's calls
 };
 
 struct cg_model {
@@ -155,11 +156,21 @@ inline int fail(cg_ctx* ctx, int code, const std::string& msg) {
   return code;
 }
 
+// The launch counter of the context whose entry point runs on this thread
+// (launch_counter_add credits it); set for the duration of a guarded call.
+extern thread_local std::atomic<uint64_t>* tl_ctx_launches;
+struct LaunchScope {
+  std::atomic<uint64_t>* prev;
+  explicit LaunchScope(std::atomic<uint64_t>* c) : prev(tl_ctx_launches) { tl_ctx_launches = c; }
+  ~LaunchScope() { tl_ctx_launches = prev; }
+};
+
 template <typename Fn>
 int guarded(cg_ctx* ctx, Fn&& fn) {
   if (!ctx) return CG_EINVAL;
   try {
     std::lock_guard<std::mutex> lk(ctx->mu);
+    LaunchScope scope(&ctx->launches);
     ctx->err.clear();
     CG_CUDA(cudaSetDevice(ctx->device));
     return fn();
