@@ -15,6 +15,7 @@ from paper_2205_15757_b200.workload import signed_requests  # noqa: E402
 
 PT = int(sys.argv[1]) if len(sys.argv) > 1 else 8
 K = int(sys.argv[2]) if len(sys.argv) > 2 else 30
+DEPTH = int(sys.argv[3]) if len(sys.argv) > 3 else 12
 B, U = 128, 3 * 224 * 224
 ctx = Context(0)
 grp, ms, _, _, _ = bench.make_group(ctx, B)
@@ -24,7 +25,7 @@ eng.load_group(grp)
 t = time.perf_counter()
 reqs = [eng.prepare(signed_requests(B, U, seed=100 + i, inputs=base[i % 2].inputs), b"group-0")
         for i in range(2 * K)]
-print(f"pack threads {PT}: signing {2 * K} batches: {time.perf_counter() - t:.1f}s", flush=True)
+print(f"pack threads {PT}, depth {DEPTH}: signing {2 * K} batches: {time.perf_counter() - t:.1f}s", flush=True)
 for rnd, lo in (("warm", 0), ("timed", K)):
     ph = dict(submit=0.0, ready=0.0, certify=0.0, fetch=0.0)
     rq, inf = deque(), deque()
@@ -35,7 +36,7 @@ for rnd, lo in (("warm", 0), ("timed", K)):
         b = time.perf_counter()
         rq.extend(eng.ready())
         c = time.perf_counter()
-        while len(rq) > 12:
+        while len(rq) > DEPTH:
             g, _, tk, Bt = rq.popleft()
             g.certify_ticket(tk, sync=False, B=Bt)
             inf.append(tk)
