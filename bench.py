@@ -139,8 +139,7 @@ def resnet50_gemm_plan(B, R, S=224):
     L = []
     px = lambda h: B * h * h  # noqa: E731
     H1, H = S // 2, S // 4
-    # conv1 reads the zero-padded NHWC4 image (gathered on chip), writes 64 ch
-    L.append(("conv1", 2 * px(H1) * 64 * 147 * R, B * (S + 6) ** 2 * 8 + R * px(H1) * 64 * 2))
+    L.append(("conv1", 2 * px(H1) * 64 * 147 * R, px(H1) * 192 * 2 + R * px(H1) * 64 * 2))
     cin = 64
     for stage, (w, n) in enumerate(((64, 3), (128, 4), (256, 6), (512, 3))):
         for i in range(n):
@@ -703,7 +702,11 @@ def bench_c4(args, rank, world, local_rank):
     ctx = Context(local_rank)
     stream = torch.cuda.current_stream()
     ctx.set_stream(stream.cuda_stream)
-    B, N = args.batch, (world if world > 1 else args.replicas)
+    # N replicas (default 8): on N GPUs one per GPU; on fewer GPUs that
+    # divide N, assigned_models chunks of N / world per rank; on one GPU
+    # all N time-sliced
+    B = args.batch
+    N = args.replicas if args.replicas % max(world, 1) == 0 and args.replicas >= world else world
     f = (N - 1) // 3
     eps = 0.1
     gloo = None
@@ -719,9 +722,8 @@ def bench_c4(args, rank, world, local_rank):
     def load(version):
         fl, dg = files[version]
         if world > 1:
-            (p,) = assigned_models(world, N, rank)
-            ms = [Model.load_cnn(ctx, fl[p], dg[p])]
-            g = ModelGroup.create_dist(ctx, ms[0], dg, f, EUCLIDEAN, eps, b"group-0", version,
+            ms = [Model.load_cnn(ctx, fl[p], dg[p]) for p in assigned_models(world, N, rank)]
+            g = ModelGroup.create_dist(ctx, ms, dg, f, EUCLIDEAN, eps, b"group-0", version,
                                        max_batch=B, topk=5)
         else:
             ms = [Model.load_cnn(ctx, x, d) for x, d in zip(fl, dg)]
@@ -821,7 +823,7 @@ def bench_c4(args, rank, world, local_rank):
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
            "data": "synthetic (random-init jittered ResNet-50 replicas, v2 = new jitter salt)",
            "config": {"workload": f"C4: {N}-replica ResNet-50 group, f={f}, batch {B}, "
-                                  f"{'one model owner per GPU' if world > 1 else 'time-sliced on 1 GPU'}"
+                                  f"{f'{N // world} replica(s) per GPU over NCCL' if world > 1 else 'time-sliced on 1 GPU'}"
                                   ", v1 -> v2 update mid-stream, v2 loaded inside the timed "
                                   "region (BASELINE.json configs[3])",
                       "model": "resnet50", "replicas": N, "f": f, "global_batch": B,

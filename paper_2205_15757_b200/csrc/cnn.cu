@@ -8,8 +8,7 @@
 //   3x3, stride 2      -> c1 writes its zero-bordered grid phase split (4
 //                         parity planes), so the 3x3 is 9 row shifts over
 //                         the planes (no im2col); 1x1/2 downsample: gather
-//   conv1 7x7/2        -> f64 -> bf16 NHWC4 padded image; the GEMM gathers the
-//                         7x7/2 windows on chip (no im2col in HBM)
+//   conv1 7x7/2        -> fused f64->bf16 im2col of the request input
 //   fc                 -> GEMM with f32 logits out
 #include <cuda_bf16.h>
 
@@ -30,10 +29,9 @@ namespace {
 using bf16 = __nv_bfloat16;
 
 // ------------------------------------------------------------------ kernels
-// The conv1 operand: f64 CHW -> bf16 NHWC4 on a grid padded by 3 (channel 3
-// and the border are zero). Coalesced on both sides: adjacent threads read
-// adjacent doubles of each channel plane and write 8 B each. The 7x7/2
-// windows are gathered from it on chip by the conv1 GEMM (GATHER mode).
+// Pass 1 of the conv1 operand: f64 CHW -> bf16 NHWC4 on a grid padded by 3
+// (channel 3 and the border are zero). Coalesced on both sides: adjacent
+// threads read adjacent doubles of each channel plane and write 8 B each.
 __global__ void chw_to_nhwc4_pad3_kernel(const double* __restrict__ in, int B, int S,
                                          uint2* __restrict__ out) {
   const int Sp = S + 6;
@@ -49,6 +47,60 @@ __global__ void chw_to_nhwc4_pad3_kernel(const double* __restrict__ in, int B, i
     b[k] = __double2bfloat16(inside ? __ldg(in + (((size_t)n * 3 + k) * S + h) * S + w) : 0.0);
   b[3] = __float2bfloat16(0.f);
   out[t] = *reinterpret_cast<uint2*>(b);
+}
+
+// Pass 2: [B*Ho*Wo, 192] im2col from the padded NHWC4 grid (K = (dr*7+ds)*3+c,
+// zero beyond 147). A warp builds 32 consecutive output rows: lane = row,
+// taps loaded as 8-byte pixels (adjacent lanes read pixels 16 B apart), the
+// row assembled 16 B at a time in a padded smem tile (row stride 25 x 16 B,
+// conflict-free), then written out as one contiguous 12 KB block.
+constexpr int kIm2colWarps = 3;
+__global__ void __launch_bounds__(32 * kIm2colWarps) conv1_im2col_nhwc4_kernel(
+    const uint2* __restrict__ px, int B, int S, int Ho, bf16* __restrict__ out) {
+  __shared__ uint4 tile[kIm2colWarps][32 * 25];
+  const int Sp = S + 6, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const size_t rows = (size_t)B * Ho * Ho;
+  const size_t row0 = ((size_t)blockIdx.x * kIm2colWarps + w) * 32;
+  if (row0 >= rows) return;
+  const size_t row = row0 + lane;
+  const bool valid = row < rows;
+  int n = 0, ho = 0, wo = 0;
+  if (valid) {
+    n = (int)(row / (Ho * Ho));
+    int rem = (int)(row - (size_t)n * Ho * Ho);
+    ho = rem / Ho;
+    wo = rem - ho * Ho;
+  }
+  const uint2* base = px + ((size_t)n * Sp + 2 * ho) * Sp + 2 * wo;
+  uint4* my = &tile[w][lane * 25];
+  uint32_t buf[4] = {0, 0, 0, 0};  // 8 bf16 = one 16-byte chunk
+  int fill = 0, chunk = 0;
+  auto put = [&](uint32_t bf16_bits) {  // append one bf16
+    if (fill & 1) buf[fill >> 1] |= bf16_bits << 16;
+    else buf[fill >> 1] = bf16_bits;
+    if (++fill == 8) {
+      my[chunk++] = make_uint4(buf[0], buf[1], buf[2], buf[3]);
+      fill = 0;
+    }
+  };
+  // fully unrolled: every put() position is a compile-time constant, so the
+  // 8-value staging buffer stays in registers
+#pragma unroll
+  for (int dr = 0; dr < 7; dr++) {
+#pragma unroll
+    for (int ds = 0; ds < 7; ds++) {
+      uint2 p = valid ? __ldg(base + dr * Sp + ds) : make_uint2(0, 0);
+      put(p.x & 0xffffu);
+      put(p.x >> 16);
+      put(p.y & 0xffffu);
+    }
+  }
+#pragma unroll
+  for (int k = 147; k < 192; k++) put(0);  // K 147 -> 192
+  __syncwarp();
+  const size_t nrow = rows - row0 < 32 ? rows - row0 : 32;
+  uint4* dst = reinterpret_cast<uint4*>(out + row0 * 192);
+  for (int i = lane; i < (int)nrow * 24; i += 32) dst[i] = tile[w][(i / 24) * 25 + i % 24];
 }
 
 // 3x3/2 max pool, pad 1 (torch pads with -inf). A thread owns two
@@ -228,10 +280,8 @@ class ResNet final : public CnnModel {
     S_ = (int)std::lround(std::sqrt((double)in_dim / 3.0));
     if ((uint64_t)3 * S_ * S_ != in_dim || S_ % 32 != 0)
       throw std::invalid_argument("cnn file: input_dim must be 3*S*S with S % 32 == 0");
-    // conv1 + bn1 in the gather layout: K = tap x 4 + c, 64 tap slots (49
-    // used) = 256 = 4 k-blocks; the GEMM builds A on chip from the padded
-    // NHWC4 image (gemm_sm100.cu, GATHER)
-    fold(conv1_, T, "conv1.weight", "bn1", 7, 2, 256, 4);
+    // conv1 + bn1: K = 147 padded to 192 (3 k-blocks of 64)
+    fold(conv1_, T, "conv1.weight", "bn1", 7, 2, 192);
     flops_ = 2.0 * (S_ / 2) * (S_ / 2) * 64 * 147;
     int H = S_ / 4, cin = 64;
     const int widths[4] = {64, 128, 256, 512};
@@ -309,6 +359,7 @@ class ResNet final : public CnnModel {
       bufs_.push_back(p);
       return reinterpret_cast<bf16*>(p);
     };
+    xcol_ = alloc(B * H1 * H1 * 192);
     nhwc4_ = alloc(B * (S_ + 6) * (S_ + 6) * 4);
     c1out_ = alloc(B * H1 * H1 * 64);
     size_t act = 0, t2 = 0, dsz = 0, g1 = 0;
@@ -333,20 +384,23 @@ class ResNet final : public CnnModel {
     pooled_ = alloc(B * fc_.cin);
   }
 
-  // the shared input stage: the zero-padded NHWC4 bf16 image (conv1 gathers
-  // its 7x7/2 windows on chip)
   size_t prepared_bytes(uint32_t B) const override {
-    return (size_t)B * (S_ + 6) * (S_ + 6) * 4 * 2;
+    return (size_t)B * (S_ / 2) * (S_ / 2) * 192 * 2;
   }
-  std::string prep_kind() const override { return "nhwc4pad3/" + std::to_string(S_); }
+  std::string prep_kind() const override { return "im2col7x7s2k192/" + std::to_string(S_); }
 
   void prepare_input(const double* d_in, uint32_t B, void* prepped, cudaStream_t st) override {
-    const int Sp = S_ + 6;
+    const int H1 = S_ / 2, Sp = S_ + 6;
     if (B > maxB_) reserve(B);
     timer_begin(st, kTimeAux);
-    // one coalesced pass: f64 CHW -> bf16 NHWC4 on a grid padded by 3
+    // two coalesced passes: f64 CHW -> bf16 NHWC4 (pad 3), then im2col
     chw_to_nhwc4_pad3_kernel<<<grid_for((size_t)B * Sp * Sp), 256, 0, st>>>(
-        d_in, B, S_, reinterpret_cast<uint2*>(prepped));
+        d_in, B, S_, reinterpret_cast<uint2*>(nhwc4_));
+    CG_CHECK_LAUNCH();
+    size_t rows = (size_t)B * H1 * H1;
+    conv1_im2col_nhwc4_kernel<<<(unsigned)ceil_div(rows, 32 * kIm2colWarps), 32 * kIm2colWarps,
+                                0, st>>>(reinterpret_cast<const uint2*>(nhwc4_), B, S_, H1,
+                                         reinterpret_cast<bf16*>(prepped));
     CG_CHECK_LAUNCH();
     timer_end(st, kTimeAux);
   }
@@ -356,8 +410,8 @@ class ResNet final : public CnnModel {
     if (B > maxB_) reserve(B);
     const bf16* x0 = reinterpret_cast<const bf16*>(prepped);
     if (!x0) {
-      prepare_input(d_in, B, nhwc4_, st);
-      x0 = nhwc4_;
+      prepare_input(d_in, B, xcol_, st);
+      x0 = xcol_;
     }
     Plan& p = plan_for(B, x0, logits);
     for (auto& s : p.steps) s(st);
@@ -382,7 +436,6 @@ class ResNet final : public CnnModel {
     void* out = nullptr;
     int ldout = 0, out_f32 = 0, relu = 0, mode = 0, H = 0, rows_out = 0;
     int halo_lo = 0;  // > 0: 3x3 taps fed from one halo box per channel block
-    int gather_Sp = 0;  // > 0: conv1 gather mode (A built from the padded image)
   };
   struct Op {
     bool gemm = false;
@@ -428,11 +481,9 @@ class ResNet final : public CnnModel {
     };
     const int H1 = S_ / 2;
     const int zero = 0;
-    // conv1 (A gathered on chip from the padded NHWC4 image) -> c1out, then
-    // maxpool -> act_[0]
+    // conv1 (im2col operand) -> c1out, then maxpool -> act_[0]
     gemm(conv1_, reinterpret_cast<const bf16*>(x0), B * H1 * H1, B * H1 * H1, conv1_.Kc, 1,
-         &zero, nullptr, 0, c1out_, 64, 0, 1, kRowIdentity, H1, B * H1 * H1);
-    L.back().g.gather_Sp = S_ + 6;
+         &zero, nullptr, 0, c1out_, 64, 0, 1, kRowIdentity, 0, B * H1 * H1);
     {
       bf16* in = c1out_;
       bf16* out = act_[0];
@@ -533,10 +584,8 @@ class ResNet final : public CnnModel {
   // Folds eval-mode BatchNorm into the preceding conv (torch BN eps 1e-5):
   // w' = w * g / sqrt(var + eps), b' = beta - mean * g / sqrt(var + eps).
   // Weight layout [cout][(dr*k + ds)*cin + c], zero-padded to Kpad.
-  // cslot > 0: each tap takes cslot K columns (channels zero-padded), the
-  // conv1 gather layout K = tap x 4 + c.
   void fold(ConvW& c, std::map<std::string, HostTensor>& T, const std::string& wname,
-            const std::string& bn, int k, int stride, int Kpad, int cslot = 0) {
+            const std::string& bn, int k, int stride, int Kpad) {
     auto it = T.find(wname);
     if (it == T.end()) throw std::invalid_argument("cnn file: missing tensor " + wname);
     const HostTensor& W = it->second;
@@ -565,8 +614,7 @@ class ResNet final : public CnnModel {
         for (int dr = 0; dr < k; dr++)
           for (int ds = 0; ds < k; ds++) {
             float w = W.v[(((size_t)o * c.cin + ci) * k + dr) * k + ds];
-            c.hw[(size_t)o * Ktot + (dr * k + ds) * (cslot ? cslot : c.cin) + ci] =
-                f2bf_bits((float)(w * s));
+            c.hw[(size_t)o * Ktot + (dr * k + ds) * c.cin + ci] = f2bf_bits((float)(w * s));
           }
     }
   }
@@ -611,8 +659,7 @@ class ResNet final : public CnnModel {
     g.n = R;
     for (int r = 0; r < R; r++) {
       const GemmDesc& d = *ds[r];
-      if (!d.gather_Sp) make_operand(A[r], d.A, d.rowsA, d.Kc, 128 + 2 * d.halo_lo);
-      else if (d.A != d0.A) throw InvalidArgument("gather conv1: replicas must share the image");
+      make_operand(A[r], d.A, d.rowsA, d.Kc, 128 + 2 * d.halo_lo);
       make_operand(Bm[r], d.c->w, d.c->cout, d.Kc * d.ntaps, BN);
       g.A[r] = &A[r];
       g.B[r] = &Bm[r];
@@ -635,10 +682,6 @@ class ResNet final : public CnnModel {
     a.W = d0.H;
     a.rows_out = d0.rows_out;
     a.halo_lo = d0.halo_lo;
-    if (d0.gather_Sp) {
-      a.gather_src = d0.A;
-      a.gather_Sp = d0.gather_Sp;
-    }
     auto p = std::make_shared<PreparedGemm>();
     prepare_conv_gemm(*p, g, a, BN);
     return [p](cudaStream_t st) { launch_prepared(*p, st); };
@@ -654,7 +697,7 @@ class ResNet final : public CnnModel {
   std::vector<Block> blocks_;
   uint32_t maxB_ = 0;
   std::vector<void*> bufs_;
-  bf16 *nhwc4_ = nullptr, *c1out_ = nullptr, *act_[2] = {nullptr, nullptr}, *t2_ = nullptr,
+  bf16 *xcol_ = nullptr, *nhwc4_ = nullptr, *c1out_ = nullptr, *act_[2] = {nullptr, nullptr}, *t2_ = nullptr,
        *ds_ = nullptr, *g1_ = nullptr, *pooled_ = nullptr;
   std::map<std::pair<int, int>, bf16*> pads_;
   std::map<uint32_t, Plan> plans_;

@@ -20,8 +20,6 @@ namespace {
 
 // warps: 0 TMA producer, 1 MMA issuer, 2-9 epilogue, 10 residual loader
 constexpr int BM = 128, BK = 64, kThreads = 352;
-// GATHER launches add 4 warps (11-14) that build the A operand in shared memory
-constexpr int kGatherWarps = 4, kThreadsGather = kThreads + 32 * kGatherWarps;
 constexpr int kEpiWarps = 8, kStgLd = 36;        // staging row stride (floats)
 constexpr int A_BYTES = BM * BK * 2;
 constexpr int kHaloBytes = 256 * BK * 2;  // largest halo box (BM + 2*halo_lo <= 256 rows)
@@ -458,20 +456,10 @@ struct TileSched {
 // half and the peer releases the accumulator on the leader's barrier.
 // Per SM and 128x256 output this halves the weight bytes written to and read
 // from shared memory (the bound of the BN=256 mainloop).
-//
-// GATHER (conv1 7x7/2 of the ResNets): the A operand is not a tensor in HBM
-// but built in shared memory by warps 11-14 straight from the zero-padded
-// NHWC4 image (a.gather_src, 8 bytes per pixel): row r of a 128-row tile is
-// output pixel m0 + r, k-block kb holds taps 16 kb .. 16 kb + 15 (4 channels
-// each; taps >= 49 are zero), i.e. one 128-byte swizzled smem row of 16
-// 8-byte pixel loads. This replaces a 617 MB im2col operand (C2) written and
-// read back through HBM by ~54 MB of image read mostly from L2.
-template <int BN, int STAGES, int kResSlots, int HALO, int RESB, int PAIR, int GATHER = 0>
-__global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
+template <int BN, int STAGES, int kResSlots, int HALO, int RESB, int PAIR>
+__global__ void __launch_bounds__(kThreads, 1)
     conv_gemm_kernel(const __grid_constant__ GemmGroupParams gp, const ConvGemmArgs a) {
   static_assert(!PAIR || (RESB == 0 && (HALO == 0 || kResSlots == 0)), "pair: streamed weights");
-  static_assert(!GATHER || (HALO == 0 && RESB == 0 && PAIR == 0 && kResSlots == 0),
-                "gather: plain streamed weights only");
   constexpr int B_BYTES = (PAIR ? BN / 2 : BN) * BK * 2;  // this CTA's weight tile
   constexpr uint32_t TMEM_COLS = 2 * BN;
   // BN = 64 (2 chunks of 32 columns): the two epilogue warp groups take
@@ -548,13 +536,13 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
   }
   if (warp == 0 && lane == 0) {
     for (int r = 0; r < gp.n; r++) {
-      if (!GATHER) asm volatile("prefetch.tensormap [%0];" ::"l"(&gp.A[r]) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&gp.A[r]) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(&gp.B[r]) : "memory");
       if (tma_out) asm volatile("prefetch.tensormap [%0];" ::"l"(&gp.O[r]) : "memory");
       if (res_tma) asm volatile("prefetch.tensormap [%0];" ::"l"(&gp.R[r]) : "memory");
     }
     for (int s = 0; s < STAGES; s++) {
-      mbar_init(&full[s], 1 + (GATHER ? kGatherWarps : 0));  // TMA (+ gather warps)
+      mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
     for (int s = 0; s < 2; s++) {
@@ -573,7 +561,7 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
     // warps and (when it streams a residual) the residual loader
     for (int s = 0; s < kClcSlots; s++) {
       mbar_init(&cfull[s], 1);
-      mbar_init(&cempty[s], 2 + kEpiWarps + (res_tma ? 1 : 0) + (GATHER ? kGatherWarps : 0));
+      mbar_init(&cempty[s], 2 + kEpiWarps + (res_tma ? 1 : 0));
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -705,13 +693,9 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
           const int tap = kb / kpt, cb = kb - tap * kpt;
           mbar_wait(&empty[stage], phase ^ 1);
           if (kb == 0) CG_TRACE(1, ti);
-          if constexpr (GATHER) {  // A comes from the gather warps
-            mbar_expect_tx(&full[stage], B_BYTES);
-          } else {
-            mbar_expect_tx(&full[stage], A_BYTES + B_BYTES);
-            tma_load_2d(&gp.A[r], &full[stage], sA + stage * A_BYTES, cb * BK,
-                        m0 + s_tap[tap]);
-          }
+          mbar_expect_tx(&full[stage], A_BYTES + B_BYTES);
+          tma_load_2d(&gp.A[r], &full[stage], sA + stage * A_BYTES, cb * BK,
+                      m0 + s_tap[tap]);
           tma_load_2d(&gp.B[r], &full[stage], sB + stage * B_BYTES, kb * BK, n0);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
@@ -862,44 +846,6 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
         umma_commit_w(&tfull[acc]);
         CG_TRACE(4, ti);
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-      }
-    }
-  } else if (GATHER && warp > 10) {
-    // ---------------- A-operand gather (warps 11-14): thread = tile row
-    const int row = (warp - 11) * 32 + lane;
-    const uint2* __restrict__ src = reinterpret_cast<const uint2*>(a.gather_src);
-    const int Sp = a.gather_Sp, Ho = a.H, HoHo = Ho * Ho;
-    int stage = 0;
-    uint32_t phase = 0;
-    for (bool ok = sched.first(first_unit, false); ok; ok = sched.next(false, lane == 0)) {
-      int r_, m0, n0;
-      coords(sched.t, r_, m0, n0);
-      const int m = m0 + row;
-      const bool valid = m < a.M;
-      long long base = 0;
-      if (valid) {
-        const int n = m / HoHo, rem = m - n * HoHo, ho = rem / Ho, wo = rem - ho * Ho;
-        base = ((long long)n * Sp + 2 * ho) * Sp + 2 * wo;
-      }
-      for (int kb = 0; kb < num_k; kb++) {
-        // the 16 taps of this k-block: 8-byte pixels of the padded image
-        uint2 px[16];
-#pragma unroll
-        for (int j = 0; j < 16; j++) {
-          const int t = 16 * kb + j;
-          const int dr = t / 7, ds = t - dr * 7;
-          px[j] = (valid && t < 49) ? __ldg(src + base + (long long)dr * Sp + ds) : make_uint2(0, 0);
-        }
-        mbar_wait(&empty[stage], phase ^ 1);
-        const uint32_t rb = su32(sA + stage * A_BYTES) + (uint32_t)row * 128;
-#pragma unroll
-        for (int c = 0; c < 8; c++)  // 16-byte chunk c of the row, 128B swizzle
-          sts_v4(rb + 16 * (uint32_t)(c ^ (row & 7)), px[2 * c].x, px[2 * c].y, px[2 * c + 1].x,
-                 px[2 * c + 1].y);
-        fence_async_smem();  // generic-proxy stores -> the tensor core's async reads
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&full[stage]);
-        if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
     }
   } else if (warp == 10) {
@@ -1208,15 +1154,14 @@ int tiles_per_unit(const ConvGemmArgs& a, int BN, int tiles) {
   return std::max(T, 1);
 }
 
-template <int BN, int STAGES, int RS, int HALO = 0, int RESB = 0, int PAIR = 0, int GATHER = 0>
+template <int BN, int STAGES, int RS, int HALO = 0, int RESB = 0, int PAIR = 0>
 void launch_t(const PreparedGemm& p, cudaStream_t st, int max_ctas) {
   constexpr int smem = smem_bytes<BN, STAGES, RS, HALO, RESB, PAIR>();
   static_assert(smem <= 232448, "smem budget");
-  constexpr int threads = GATHER ? kThreadsGather : kThreads;
-  auto kern = conv_gemm_kernel<BN, STAGES, RS, HALO, RESB, PAIR, GATHER>;
   static std::atomic<uint64_t> attr{0};
-  once_per_device(attr, [&] {
-    CG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  once_per_device(attr, [] {
+    CG_CUDA(cudaFuncSetAttribute(conv_gemm_kernel<BN, STAGES, RS, HALO, RESB, PAIR>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   });
   ConvGemmArgs a = p.args;
   const int tiles = ((a.M + BM - 1) / BM) * ((a.N + BN - 1) / BN) * p.gp.n;
@@ -1239,7 +1184,7 @@ void launch_t(const PreparedGemm& p, cudaStream_t st, int max_ctas) {
     if (g2 < 2) throw InvalidArgument("conv_gemm: an SM pair needs 2 CTAs");
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)g2);
-    cfg.blockDim = dim3(threads);
+    cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr2[2];
@@ -1251,13 +1196,13 @@ void launch_t(const PreparedGemm& p, cudaStream_t st, int max_ctas) {
     attr2[1].val.programmaticStreamSerializationAllowed = g_pdl;
     cfg.attrs = attr2;
     cfg.numAttrs = 2;
-    CG_CUDA(cudaLaunchKernelEx(&cfg, kern, p.gp, a));
+    CG_CUDA(cudaLaunchKernelEx(&cfg, conv_gemm_kernel<BN, STAGES, RS, HALO, RESB, PAIR>, p.gp, a));
     launch_counter_add(1);
   } else {
     // programmatic dependent launch (the kernel waits on griddepcontrol)
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
-    cfg.blockDim = dim3(threads);
+    cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute at[1];
@@ -1265,7 +1210,7 @@ void launch_t(const PreparedGemm& p, cudaStream_t st, int max_ctas) {
     at[0].val.programmaticStreamSerializationAllowed = g_pdl;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    CG_CUDA(cudaLaunchKernelEx(&cfg, kern, p.gp, a));
+    CG_CUDA(cudaLaunchKernelEx(&cfg, conv_gemm_kernel<BN, STAGES, RS, HALO, RESB, PAIR>, p.gp, a));
     launch_counter_add(1);
   }
   timer_end(st, kTimeGemm);
@@ -1487,15 +1432,12 @@ void prepare_conv_gemm(PreparedGemm& p, const ConvGemmGroup& g, const ConvGemmAr
   for (int t = 0; a.halo_lo > 0 && t < a.ntaps; t++)
     if (a.tap_off[t] < -a.halo_lo || a.tap_off[t] > a.halo_lo)
       throw InvalidArgument("conv_gemm: tap outside the halo");
-  if (a.gather_src && (a.Kc != 256 || a.ntaps != 1 || a.gather_Sp < 7 || a.H < 1))
-    throw InvalidArgument("conv_gemm: gather mode needs K = 256 (64 taps x 4 channels)");
   for (int r = 0; r < g.n; r++) {
-    if ((!a.gather_src && g.A[r]->box_rows != BM + 2 * a.halo_lo) ||
-        g.B[r]->box_rows != (a.pair ? BN / 2 : BN))
+    if (g.A[r]->box_rows != BM + 2 * a.halo_lo || g.B[r]->box_rows != (a.pair ? BN / 2 : BN))
       throw InvalidArgument("conv_gemm: box mismatch");
     if ((g.residual[r] != nullptr) != (g.residual[0] != nullptr))
       throw InvalidArgument("conv_gemm: residual on some replicas only");
-    if (!a.gather_src) p.gp.A[r] = g.A[r]->map;
+    p.gp.A[r] = g.A[r]->map;
     p.gp.B[r] = g.B[r]->map;
     p.gp.bias[r] = g.bias[r];
     p.gp.residual[r] = g.residual[r];
@@ -1520,12 +1462,6 @@ void prepare_conv_gemm(PreparedGemm& p, const ConvGemmGroup& g, const ConvGemmAr
 }
 
 void launch_prepared(const PreparedGemm& p, cudaStream_t st, int max_ctas) {
-  if (p.args.gather_src) {
-    if (p.BN != 64 || p.res || p.args.halo_lo || p.args.pair)
-      throw InvalidArgument("conv_gemm: gather mode is BN = 64, no residual / halo / pair");
-    launch_t<64, 6, 0, 0, 0, 0, 1>(p, st, max_ctas);
-    return;
-  }
   if (p.args.pair) {
     if (p.args.halo_lo > 0) {
       if (p.BN != 128 || p.res)

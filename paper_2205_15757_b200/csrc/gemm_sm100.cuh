@@ -61,12 +61,6 @@ struct ConvGemmArgs {
   // CTAs cancel pending ones and take their units).
   int sched;
   int tile_unit;
-  // Gather mode (ResNet conv1 7x7/2): A rows built on chip from the
-  // zero-padded NHWC4 image at gather_src ([B][Sp][Sp][4] bf16, Sp = S + 6),
-  // output pixel m = (n, ho, wo) with Ho = H; K = 256 = 64 taps x 4 channels
-  // (taps >= 49 zero). nullptr: A is a tensor map.
-  const void* gather_src;
-  int gather_Sp;
 };
 
 // One encoded operand (tensor map over a row-major bf16 [rows, cols] matrix

@@ -22,7 +22,7 @@ def plan(B, R, S=224):
     L = []
     px = lambda h: B * h * h  # noqa: E731
     H1, H = S // 2, S // 4
-    L.append(("conv1 7x7/2", 2 * px(H1) * 64 * 147 * R, B * (S + 6) ** 2 * 8 + R * px(H1) * 64 * 2))
+    L.append(("conv1 7x7/2", 2 * px(H1) * 64 * 147 * R, px(H1) * 192 * 2 + R * px(H1) * 64 * 2))
     cin = 64
     for stage, (w, n) in enumerate(((64, 3), (128, 4), (256, 6), (512, 3))):
         for i in range(n):
