@@ -437,11 +437,7 @@ def bench_gpu(args, rank, world, local_rank):
            "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
            "data": "synthetic (random-init jittered ResNet-50 replicas, U(-1,1) f64 "
                    "requests, Ed25519-signed)",
-           "config": {"workload": "C2: 3-replica ResNet-50 group, f=1, batch 128, "
-                                  "224x224 (BASELINE.json configs[1])",
-                      "model": "resnet50", "replicas": 3, "f": 1, "global_batch": B * world,
-                      "batch_per_gpu": B, "epsilon": 0.1, "distance": "euclidean",
-                      "seq_len": None, "parallelism": f"group-per-GPU x{world}",
+           "config": {**c2_config(B, world),
                       "l2": "inputs larger than L2: 2 rotating 154 MB f64 batches",
                       "arith": "bf16 forward / f64 agreement / u32 SHA-256",
                       "satisfied_fraction": sat_dev,
@@ -1062,6 +1058,15 @@ def bench_c5(args, local_rank):
     return lines
 
 
+def c2_config(B, world):
+    """The C2 workload keys both arms report (BASELINE.json configs[1])."""
+    return {"workload": "C2: 3-replica ResNet-50 group, f=1, batch 128, "
+                        "224x224 (BASELINE.json configs[1])",
+            "model": "resnet50", "replicas": 3, "f": 1, "global_batch": B * world,
+            "batch_per_gpu": B, "epsilon": 0.1, "distance": "euclidean",
+            "seq_len": None, "parallelism": f"group-per-GPU x{world}"}
+
+
 def bench_reference(args, rank, world):
     """--impl reference: the reference's CPU path on the host cores."""
     if rank != 0:
@@ -1093,8 +1098,8 @@ def bench_reference(args, rank, world):
             "n_gpus": world, "steps": K, "warmup": 1,
             "ms_per_step": round(1e3 * dt / K, 1), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32 forward / f64 agreement",
-            "data": "synthetic", "config": {"workload": "C2 sample", "batch_per_step": S,
-                                            "model": "resnet50", "replicas": 3, "f": 1},
+            "data": "synthetic", "config": {**c2_config(args.batch, world),
+                                            "sample_per_step": S},
             "cpu_baseline": {"value": round(v, 3), "unit": UNIT, "cores": threads,
                              "kind": "reference",
                              "sample": f"{S} requests per step, torchvision fp32 forward "

@@ -22,6 +22,10 @@
  *   cg_certify_batch           InferenceEngine::execute_batch (src/engine.cpp:269-306) +
  *                              build_result_tree (src/messages.cpp:235-258) + Coordinator::try_attest's
  *                              agreement, manifest and A tree (src/coordinator.cpp:727-849) for one batch
+ *   cg_cert_leaf_hashes        the leaf re-hashing inside verify_cert / verify_failure
+ *                              (src/certificate.cpp:215-316) and rebuild_committer_trees /
+ *                              assemble_response (src/proxy.cpp:28-186): result_leaf,
+ *                              single_attest_leaf, missing_result_leaf (src/messages.cpp:204-218,283-290)
  */
 #ifndef CREDO_GPU_H
 #define CREDO_GPU_H
@@ -290,6 +294,25 @@ int cg_certify_empty_slot(cg_group* g, uint64_t view, uint64_t seq, cg_certify_o
 int cg_request_digests(cg_ctx* ctx, const cg_request_batch* batch, const char* group_id,
                        uint64_t group_id_len, uint8_t* signing_digests,
                        uint8_t* canonical_ids, int8_t* status);
+
+/* ---- certificate verification / assembly at batch scale ------------------
+ * For M (request, result) pairs over one request batch (uniform input length,
+ * request ops only; group_id as in cg_request_digests): want[m] is a mask of
+ *   1: leaf_hash(result_leaf(req, res))        -> leaf52 + 32m  (0x52)
+ *   2: leaf_hash(single_attest_leaf(req, res)) -> leaf53 + 32m  (0x53)
+ *   4: leaf_hash(missing_result_leaf(req))     -> leaf4d + 32m  (0x4D; result unused)
+ * with req = request req_index[m] and res = InferenceResult::encode bytes
+ * (src/domain.cpp:218-225), result_lens[m] of them, back to back in
+ * result_enc (an entry with only bit 4 may have length 0). Each request's
+ * 1.2 MB prefix (ImageNet shape) is hashed once per tag as a midstate shared
+ * by all of its results. The C++ adapters credo::gpu::verify_responses and
+ * credo::gpu::assemble_responses (include/credo_gpu_adapters.hpp) build the
+ * reference's verify_response / assemble_response on it. */
+int cg_cert_leaf_hashes(cg_ctx* ctx, const cg_request_batch* batch, const char* group_id,
+                        uint64_t group_id_len, uint32_t M, const uint32_t* req_index,
+                        const uint8_t* want, const uint8_t* result_enc,
+                        const uint64_t* result_lens, uint8_t* leaf52, uint8_t* leaf53,
+                        uint8_t* leaf4d);
 
 /* ---- the batch former (InferenceEngine, src/engine.cpp:166-267) ----------
  * Per live (group, version): FIFO queue with `seen` dedup; a batch is released

@@ -7,6 +7,9 @@
 //   GroupServer       : InferenceEngine::load_group / submit / flush_* /
 //                       execute_batch + try_attest's digests for any model
 //                       family (src/engine.cpp:67-306, coordinator.cpp:727-865)
+//                       execute_batches: dispatch_batches for adjacency_batches
+//                       of an ordered slot, results into PendingResultStore
+//                       (coordinator.cpp:26-43,1030-1048; engine.cpp:11-34)
 //   gpu_select_quorum : distance::select_quorum (include/credo/distance.hpp:65-67)
 //   gpu_hash_many     : crypto::hash, batched   (include/credo/crypto.hpp:26-30)
 #pragma once
@@ -218,7 +221,10 @@ class GroupServer {
                    : group.status == GroupStatus::active ? CG_GROUP_ACTIVE
                                                          : CG_GROUP_DEFINED;
     check(ctx_.get(), cg_engine_load_group(eng_, g, st));
-    groups_[{group.group_id, group.version}] = Group{g, (uint32_t)ms.size(), group.models.front().output_dim};
+    Group G{g, (uint32_t)ms.size(), group.models.front().output_dim,
+            group.models.front().input_dim, {}};
+    for (const auto& desc : group.models) G.digests.push_back(desc.weights_digest);
+    groups_[{group.group_id, group.version}] = std::move(G);
     return std::nullopt;
   }
 
@@ -268,6 +274,84 @@ class GroupServer {
     return has ? std::optional<uint64_t>(d) : std::nullopt;
   }
 
+  // Coordinator::dispatch_batches (coordinator.cpp:1030-1048) for batches
+  // formed outside the batch former -- adjacency_batches of an ordered slot
+  // under agree_then_execute (coordinator.cpp:26-43, :588-624): each batch is
+  // ingested and certified as it is (a request whose input does not fit the
+  // group is skipped by execute_batch, engine.cpp:286-291: missing results).
+  // With stores[p], provider p's results go into that PendingResultStore as
+  // InferenceEngine::execute_batch puts them (engine.cpp:293-303): node p,
+  // the batch's version, the output, p's weights_digest.
+  std::vector<Certified> execute_batches(const std::vector<ExecutionBatch>& batches,
+                                         const std::map<uint64_t, PendingResultStore*>& stores = {},
+                                         bool keep_outputs = false) {
+    std::vector<Certified> out;
+    for (const ExecutionBatch& b : batches) {
+      if (b.requests.empty()) continue;
+      auto git = groups_.find({b.group_id, b.group_version});
+      if (git == groups_.end()) throw std::invalid_argument("execute_batches: version not loaded");
+      const Group& G = git->second;
+      const uint32_t B = (uint32_t)b.requests.size();
+      const uint64_t u = G.u;
+      std::vector<uint8_t> ids(32 * (size_t)B), has_eps(B), pubs(32 * (size_t)B),
+          sigs(64 * (size_t)B), nonces;
+      std::vector<double> eps(B), in((size_t)B * u, 0.0);
+      std::vector<uint64_t> nonce_lens(B), dims(B);
+      std::vector<const double*> mis(B, nullptr);
+      bool any_mis = false;
+      for (uint32_t k = 0; k < B; k++) {
+        const InferenceRequest& r = b.requests[k];
+        std::memcpy(&ids[32 * (size_t)k], r.request_id.data.data(), 32);
+        dims[k] = r.input.size();
+        if (dims[k] == u) std::copy(r.input.begin(), r.input.end(), in.begin() + (size_t)k * u);
+        else mis[k] = r.input.data(), any_mis = true;
+        has_eps[k] = r.epsilon_override.has_value();
+        eps[k] = r.epsilon_override.value_or(0.0);
+        std::memcpy(&pubs[32 * (size_t)k], r.client_pub.data(), 32);
+        nonces.insert(nonces.end(), r.client_nonce.begin(), r.client_nonce.end());
+        nonce_lens[k] = r.client_nonce.size();
+        std::memcpy(&sigs[64 * (size_t)k], r.client_sig.data(), 64);
+      }
+      cg_request_batch bt{};
+      bt.B = B;
+      bt.u = u;
+      bt.request_ids = ids.data();
+      bt.inputs = in.data();
+      bt.has_eps = has_eps.data();
+      bt.eps = eps.data();
+      bt.client_pubs = pubs.data();
+      bt.nonces = nonces.data();
+      bt.nonce_lens = nonce_lens.data();
+      bt.client_sigs = sigs.data();
+      if (any_mis) {
+        bt.input_dims = dims.data();
+        bt.misfit_inputs = mis.data();
+      }
+      uint64_t ticket = 0;
+      check(ctx_.get(), cg_ingest_batch(G.h, &bt, &ticket));
+      auto [c, Gp] = certify_group(cg_ready_batch{G.h, b.group_version, ticket, B},
+                                   keep_outputs || !stores.empty());
+      for (const auto& [p, store] : stores) {
+        if (p >= G.N || !store) continue;
+        for (uint32_t k = 0; k < B; k++) {
+          if (dims[k] != u) continue;
+          InferenceResult r;
+          r.request_id = b.requests[k].request_id;
+          r.node_index = p;
+          r.group_id = b.group_id;
+          r.group_version = b.group_version;
+          const double* o = c.outputs.data() + ((size_t)p * B + k) * G.v;
+          r.output.assign(o, o + G.v);
+          r.model_digest = G.digests[p];
+          store->put(r);
+        }
+      }
+      if (!keep_outputs) c.outputs.clear();
+      out.push_back(std::move(c));
+    }
+    return out;
+  }
+
   // dispatch_batches + execute_batch + try_prepare/try_attest digests for
   // every released batch, in release order.
   std::vector<Certified> dispatch(bool keep_outputs = false) {
@@ -286,9 +370,13 @@ class GroupServer {
   struct Group {
     cg_group* h;
     uint32_t N;
-    uint64_t v;
+    uint64_t v, u;
+    std::vector<Hash32> digests;  // provider p's weights_digest
   };
   Certified certify(const cg_ready_batch& rb, bool keep_outputs) {
+    return certify_group(rb, keep_outputs).first;
+  }
+  std::pair<Certified, const Group*> certify_group(const cg_ready_batch& rb, bool keep_outputs) {
     const Group* G = nullptr;
     Certified c;
     for (auto& [key, g] : groups_)
@@ -317,7 +405,7 @@ class GroupServer {
     if (keep_outputs) o.outputs = c.outputs.data();
     check(ctx_.get(), cg_certify_ticket(rb.group, rb.ticket, &o));
     for (uint32_t p = 0; p < N; p++) std::memcpy(c.r_roots[p].data.data(), &rr[32 * p], 32);
-    return c;
+    return {std::move(c), G};
   }
 
   Context& ctx_;
@@ -326,6 +414,26 @@ class GroupServer {
   std::map<Hash32, cg_model*> models_;
   std::map<std::pair<std::string, uint64_t>, Group> groups_;
 };
+
+// adjacency_batches (coordinator.cpp:24-43, file-local there): consecutive
+// ok request ops sharing a (group, version), chunked to batch_max, batch
+// order kept -- how an ordered slot becomes execution batches under
+// agree_then_execute.
+inline std::vector<ExecutionBatch> adjacency_batches(
+    const std::vector<const InferenceRequest*>& reqs, const std::vector<uint64_t>& versions,
+    uint64_t batch_max) {
+  std::vector<ExecutionBatch> out;
+  for (size_t i = 0; i < reqs.size(); i++) {
+    if (out.empty() || out.back().group_id != reqs[i]->group_id ||
+        out.back().group_version != versions[i] || out.back().requests.size() >= batch_max) {
+      out.emplace_back();
+      out.back().group_id = reqs[i]->group_id;
+      out.back().group_version = versions[i];
+    }
+    out.back().requests.push_back(*reqs[i]);
+  }
+  return out;
+}
 
 // distance::select_quorum with the reference's signature and exceptions.
 inline distance::AgreementOutcome gpu_select_quorum(

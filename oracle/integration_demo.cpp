@@ -4,7 +4,9 @@
 // ToyExecutor on the same generated group and signed requests, and checks:
 //   * execute_batch results bit-identical (LinearToyModel fp64 path),
 //   * distance::select_quorum == gpu_select_quorum on every request,
-//   * crypto::hash == gpu_hash_many on the result leaves.
+//   * crypto::hash == gpu_hash_many on the result leaves,
+//   * adjacency_batches + GroupServer::execute_batches filling per-node
+//     PendingResultStores == the reference engines' execute_batch results.
 // Built by `make -C oracle integration`; run by tests/test_gpu_integration.py.
 #include <cstdio>
 #include <map>
@@ -114,6 +116,53 @@ int main() {
         checked++;
         if (g.files_hashed() != 1) mismatches++;
       }
+    }
+  }
+  // agree_then_execute's execution path: an ordered slot's ok request ops
+  // (two live versions interleaved, one misfit input) chunked by
+  // adjacency_batches (coordinator.cpp:26-43), dispatched through
+  // GroupServer::execute_batches, every provider's results in its own
+  // PendingResultStore == each node's InferenceEngine::execute_batch results
+  // (engine.cpp:269-306, stored in results()), bit for bit
+  {
+    ModelGroup g2 = group;
+    g2.version = 2;
+    gpu::GroupServer srv(ctx, B, 2000);
+    if (srv.load_group(group, fetch, 1) || srv.load_group(g2, fetch, 1)) {
+      std::fprintf(stderr, "GroupServer load_group failed\n");
+      return 2;
+    }
+    std::vector<InferenceRequest> slot_reqs(reqs.begin(), reqs.begin() + 11);
+    slot_reqs[6].input.resize(5);  // does not fit: skipped by execute_batch
+    std::vector<const InferenceRequest*> ptrs;
+    std::vector<uint64_t> versions;
+    const uint64_t pattern[11] = {1, 1, 1, 1, 1, 2, 2, 1, 2, 2, 2};
+    for (size_t i = 0; i < slot_reqs.size(); i++) {
+      ptrs.push_back(&slot_reqs[i]);
+      versions.push_back(pattern[i]);
+    }
+    auto batches = gpu::adjacency_batches(ptrs, versions, 4);
+    checked++;
+    if (batches.size() != 5) mismatches++;  // [1x4] [1] [2x2] [1] [2x3]
+    std::vector<PendingResultStore> stores(N);
+    std::map<uint64_t, PendingResultStore*> sp;
+    for (uint64_t p = 0; p < N; p++) sp[p] = &stores[p];
+    srv.execute_batches(batches, sp);
+    for (uint64_t node = 0; node < N; node++) {
+      NodeIdentity self;
+      self.index = node;
+      InferenceEngine cpu_engine(self, N, B, 2000, std::make_unique<ToyExecutor>(), fetch);
+      if (cpu_engine.load_group(group) || cpu_engine.load_group(g2)) return 2;
+      for (const auto& b : batches) cpu_engine.execute_batch(b);
+      for (size_t i = 0; i < slot_reqs.size(); i++)
+        for (uint64_t ver : {1ull, 2ull}) {
+          checked++;
+          auto want = cpu_engine.results().get(slot_reqs[i].request_id, ver);
+          auto got = stores[node].get(slot_reqs[i].request_id, ver);
+          if (want != got) mismatches++;
+        }
+      checked++;
+      if (stores[node].request_count() != cpu_engine.results().request_count()) mismatches++;
     }
   }
   for (auto& [k, m] : outs) {

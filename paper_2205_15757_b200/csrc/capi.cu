@@ -1651,6 +1651,157 @@ int cg_request_digests(cg_ctx* ctx, const cg_request_batch* bt, const char* grou
   });
 }
 
+// ------------------------------------------- certificate leaf hashes (verify)
+// The leaves a verifier re-hashes (verify_cert, certificate.cpp:235-275) and a
+// proxy re-hashes when it rebuilds committer and result trees (proxy.cpp:
+// 28-48, :134-141): result_leaf 0x52 / single_attest_leaf 0x53 =
+// 0x00 || tag || request || result and missing_result_leaf 0x4D =
+// 0x00 || 0x4D || request (messages.cpp:204-218, :283-290). The request part
+// is streamed from the f64 input tensor; its whole blocks are hashed once
+// per (request, tag) into a midstate that every result of the request
+// continues from.
+int cg_cert_leaf_hashes(cg_ctx* ctx, const cg_request_batch* bt, const char* group_id,
+                        uint64_t group_id_len, uint32_t M, const uint32_t* req_index,
+                        const uint8_t* want, const uint8_t* result_enc,
+                        const uint64_t* result_lens, uint8_t* leaf52, uint8_t* leaf53,
+                        uint8_t* leaf4d) {
+  if (!ctx || !bt || (M && (!req_index || !want))) return CG_EINVAL;
+  return guarded(ctx, [&] {
+    const uint32_t B = bt->B;
+    const uint64_t u = bt->u;
+    if (M == 0) return CG_OK;
+    if (bt->input_dims || bt->op_kinds)
+      throw InvalidArgument("cg_cert_leaf_hashes: one input length per batch, request ops only");
+    // which (request, tag) prefixes are needed; result byte offsets
+    std::vector<uint8_t> need(3 * (size_t)B, 0);  // [tag 0x52 | 0x53 | 0x4D][k]
+    std::vector<uint64_t> roff(M);
+    uint64_t rpos = 0;
+    for (uint32_t m = 0; m < M; m++) {
+      const uint32_t k = req_index[m], w = want[m];
+      if (k >= B) throw InvalidArgument("cg_cert_leaf_hashes: request index out of range");
+      if (w & ~7u) throw InvalidArgument("cg_cert_leaf_hashes: want is a mask of 1 | 2 | 4");
+      if (((w & 1) && !leaf52) || ((w & 2) && !leaf53) || ((w & 4) && !leaf4d))
+        throw InvalidArgument("cg_cert_leaf_hashes: output for a requested leaf kind is NULL");
+      if ((w & 3) && (!result_enc || !result_lens))
+        throw InvalidArgument("cg_cert_leaf_hashes: result leaves need result encodings");
+      for (int t = 0; t < 3; t++)
+        if (w & (1u << t)) need[(size_t)t * B + k] = 1;
+      roff[m] = rpos;
+      if (result_lens) rpos += result_lens[m];
+    }
+    cudaStream_t st = ctx->stream;
+    const double* d_in = bt->inputs;
+    if (!bt->inputs_on_device) {
+      ctx->d_f64.ensure((size_t)B * u);
+      CG_CUDA(cudaMemcpyAsync(ctx->d_f64.p, bt->inputs, 8 * (size_t)B * u,
+                              cudaMemcpyHostToDevice, st));
+      d_in = ctx->d_f64.p;
+    }
+    static const uint8_t kTag[3] = {0x52, 0x53, 0x4D};
+    Arena ar;
+    std::vector<size_t> h(3 * (size_t)B), t(B);
+    std::vector<uint64_t> P(B);
+    uint64_t lenH = 0, nonce_pos = 0;
+    for (uint32_t k = 0; k < B; k++) {
+      Enc H;  // 0x00 || tag || request body up to the input list (domain.cpp:144-158)
+      H.u8(0x00);
+      H.u8(0x52);
+      H.raw(bt->request_ids + 32 * k, 32);
+      H.bytes((const uint8_t*)group_id, group_id_len);
+      H.u32((uint32_t)u);
+      Enc T;
+      const bool he = bt->has_eps && bt->has_eps[k];
+      T.u8(he ? 1 : 0);
+      if (he) T.f64(bt->eps[k]);
+      T.raw(bt->client_pubs + 32 * k, 32);
+      T.bytes(bt->nonces + nonce_pos, bt->nonce_lens[k]);
+      nonce_pos += bt->nonce_lens[k];
+      T.raw(bt->client_sigs + 64 * k, 64);
+      lenH = H.b.size();
+      P[k] = lenH + 8 * u + T.b.size();
+      for (int tg = 0; tg < 3; tg++)
+        if (need[(size_t)tg * B + k]) {
+          H.b[1] = kTag[tg];
+          h[(size_t)tg * B + k] = ar.add(H.b.data(), lenH, 0);
+        }
+      t[k] = ar.add(T.b.data(), T.b.size(), lenH + 8 * u);
+    }
+    std::vector<size_t> rar(M, 0);
+    for (uint32_t m = 0; m < M; m++)
+      if ((want[m] & 3) && result_lens[m])
+        rar[m] = ar.add(result_enc + roff[m], result_lens[m], P[req_index[m]]);
+    // device scratch: digests [0x52: M][0x53: M][0x4D: B], midstates [2][B]
+    const size_t dig_bytes = 32 * (2 * (size_t)M + B);
+    ctx->d_out.ensure(dig_bytes + 64 * (size_t)B);
+    ctx->d_bytes.ensure(ar.b.size() + 16);
+    uint8_t* d_dig = ctx->d_out.p;
+    uint32_t* d_mid = (uint32_t*)(ctx->d_out.p + dig_bytes);
+    const uint64_t A = (uint64_t)ctx->d_bytes.p;
+    auto prefix = [&](ChainJob& j, int tg, uint32_t k) {
+      std::memset(&j, 0, sizeof j);
+      j.seg[0] = ChainSeg{A + h[(size_t)tg * B + k], 0, lenH, kSegRaw, 0};
+      j.seg[1] = ChainSeg{(uint64_t)(d_in + u * k), lenH, 8 * u, kSegF64, 0};
+      j.seg[2] = ChainSeg{A + t[k], lenH + 8 * u, P[k] - lenH - 8 * u, kSegRaw, 0};
+      j.nseg = 3;
+      j.total_len = P[k];
+    };
+    std::vector<ChainJob> mids, fins;
+    for (uint32_t k = 0; k < B; k++) {
+      for (int tg = 0; tg < 2; tg++)
+        if (need[(size_t)tg * B + k] && P[k] >= 64) {
+          ChainJob j;
+          prefix(j, tg, k);
+          j.blk_end = P[k] / 64;
+          j.state_out = (uint64_t)(d_mid + 8 * ((size_t)tg * B + k));
+          mids.push_back(j);
+        }
+      if (need[2 * (size_t)B + k]) {  // missing_result_leaf: the request alone
+        ChainJob j;
+        prefix(j, 2, k);
+        j.final_ = 1;
+        j.blk_end = (P[k] + 9 + 63) / 64;
+        j.digest_out = (uint64_t)(d_dig + 32 * (2 * (size_t)M + k));
+        fins.push_back(j);
+      }
+    }
+    for (uint32_t m = 0; m < M; m++)
+      for (int tg = 0; tg < 2; tg++) {
+        if (!(want[m] & (1u << tg))) continue;
+        const uint32_t k = req_index[m];
+        ChainJob j;
+        prefix(j, tg, k);
+        j.seg[3] = ChainSeg{A + rar[m], P[k], result_lens[m], kSegRaw, 0};
+        j.nseg = 4;
+        j.final_ = 1;
+        j.total_len = P[k] + result_lens[m];
+        j.blk_begin = P[k] / 64;
+        j.blk_end = (j.total_len + 9 + 63) / 64;
+        j.state_in = j.blk_begin ? (uint64_t)(d_mid + 8 * ((size_t)tg * B + k)) : 0;
+        j.digest_out = (uint64_t)(d_dig + 32 * ((size_t)tg * M + m));
+        fins.push_back(j);
+      }
+    ctx->d_jobs.ensure(mids.size() + fins.size());
+    CG_CUDA(cudaMemcpyAsync(ctx->d_bytes.p, ar.b.data(), ar.b.size(), cudaMemcpyHostToDevice, st));
+    if (!mids.empty())
+      CG_CUDA(cudaMemcpyAsync(ctx->d_jobs.p, mids.data(), mids.size() * sizeof(ChainJob),
+                              cudaMemcpyHostToDevice, st));
+    CG_CUDA(cudaMemcpyAsync(ctx->d_jobs.p + mids.size(), fins.data(),
+                            fins.size() * sizeof(ChainJob), cudaMemcpyHostToDevice, st));
+    if (!mids.empty()) launch_chain_jobs(ctx->d_jobs.p, (uint32_t)mids.size(), st);
+    launch_chain_jobs(ctx->d_jobs.p + mids.size(), (uint32_t)fins.size(), st);
+    std::vector<uint8_t> dig(dig_bytes);
+    CG_CUDA(cudaMemcpyAsync(dig.data(), d_dig, dig_bytes, cudaMemcpyDeviceToHost, st));
+    CG_CUDA(cudaStreamSynchronize(st));
+    for (uint32_t m = 0; m < M; m++) {
+      if (want[m] & 1) std::memcpy(leaf52 + 32 * (size_t)m, &dig[32 * (size_t)m], 32);
+      if (want[m] & 2) std::memcpy(leaf53 + 32 * (size_t)m, &dig[32 * ((size_t)M + m)], 32);
+      if (want[m] & 4)
+        std::memcpy(leaf4d + 32 * (size_t)m, &dig[32 * (2 * (size_t)M + req_index[m])], 32);
+    }
+    return CG_OK;
+  });
+}
+
 // ---------------------------------------------------- authentication paths
 namespace {
 void auth_paths_device(cg_ctx* ctx, const uint8_t* d_leaves, uint64_t n, const uint64_t* indices,

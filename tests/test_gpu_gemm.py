@@ -182,62 +182,6 @@ def run_halo(ctx, A, Bw, N, Kc, taps, bias, H, W, M, rows_out, BN, halo_lo, pair
     return torch.from_numpy(out.view(np.int16)).view(torch.bfloat16).float()
 
 
-@pytest.mark.parametrize("M,N,Kc,BN", [(700, 512, 640, 256), (1500, 256, 512, 128),
-                                        (333, 128, 1024, 64), (2000, 1024, 256, 256)])
-def test_gemm_residual_ring_configs(ctx, M, N, Kc, BN):
-    """Both residual-ring layouts (deep ring for short K, more mainloop
-    stages for K >= 512) over ragged tails."""
-    g = torch.Generator().manual_seed(M * 3 + Kc)
-    A = torch.rand(M, Kc, generator=g) * 2 - 1
-    Bw = (torch.rand(N, Kc, generator=g) * 2 - 1) / 8
-    R = torch.rand(M, N, generator=g) * 2 - 1
-    bias = torch.rand(N, generator=g) - 0.5
-    got = run_gemm(ctx, A, Bw, N, Kc, 1, [0], bias, R, 1, 0, 0, 0, M, M, 0, BN)
-    close(got, (q(A) @ q(Bw).T + bias + q(R)).clamp_min(0))
-
-
-@pytest.mark.parametrize("M,N,Kc,res,relu,max_ctas,out_f32", [
-    (300, 256, 256, 0, 1, 0, 0), (777, 512, 192, 1, 1, 0, 0), (2048, 1024, 512, 1, 0, 6, 0),
-    (128, 256, 64, 1, 1, 0, 0), (5000, 2048, 128, 0, 1, 0, 0), (256, 1000, 128, 0, 0, 0, 1)])
-def test_gemm_pair(ctx, M, N, Kc, res, relu, max_ctas, out_f32):
-    """SM-pair (cta_group::2) 256 x 256 tiles: ragged row tails (a peer CTA
-    with no rows), the residual ring, a capped grid, f32 logits (FC shape)."""
-    g = torch.Generator().manual_seed(M + 7 * N)
-    A = torch.rand(M, Kc, generator=g) * 2 - 1
-    Bw = torch.rand(N, Kc, generator=g) * 2 - 1
-    R = torch.rand(M, N, generator=g) * 2 - 1 if res else None
-    bias = torch.rand(N, generator=g) - 0.5
-    got = run_gemm(ctx, A, Bw, N, Kc, 1, [0], bias, R, relu, 0, 0, 0, M, M, out_f32, 256,
-                   max_ctas, pair=1)
-    ref = q(A) @ q(Bw).T + bias
-    if res:
-        ref = ref + q(R)
-    if relu:
-        ref = ref.clamp_min(0)
-    if out_f32:
-        assert torch.allclose(got, ref, rtol=1e-4, atol=1e-3)
-    else:
-        close(got, ref)
-
-
-def test_gemm_pair_taps_remap(ctx):
-    """SM pairs over 9 row-shifted taps with a row remap (PadToCompact)."""
-    NB, H, C, Cout = 2, 14, 64, 256
-    W = H
-    g = torch.Generator().manual_seed(11)
-    x = torch.rand(NB, C, H, W, generator=g) * 2 - 1
-    w = (torch.rand(Cout, C, 3, 3, generator=g) * 2 - 1) / 3
-    bias = torch.rand(Cout, generator=g) - 0.5
-    A, Wp = grid_rows(q(x))
-    taps = [(dr - 1) * Wp + (ds - 1) for dr in range(3) for ds in range(3)]
-    Bw = q(w).permute(0, 2, 3, 1).reshape(Cout, 9 * C)
-    M = A.shape[0]
-    got = run_gemm(ctx, A, Bw, Cout, C, 9, taps, bias, None, 1, 1, H, W, M, NB * H * W, 0, 256,
-                   pair=1)
-    ref = torch.nn.functional.conv2d(q(x), q(w), bias, padding=1).clamp_min(0)
-    close(got, ref.permute(0, 2, 3, 1).reshape(-1, Cout))
-
-
 @pytest.mark.parametrize("NB,H,C,Cout,BN", [(3, 7, 64, 128, 128), (2, 14, 128, 64, 64),
                                             (2, 28, 64, 256, 256), (2, 56, 64, 64, 64)])
 def test_conv3x3_halo(ctx, NB, H, C, Cout, BN):

@@ -68,3 +68,25 @@ def test_run_scenario_with_gpu_executor():
     print(out.stdout, out.stderr)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "0 failures" in out.stdout
+
+
+VERIFY = os.path.join(ROOT, "oracle", "_ref", "integration_verify")
+
+
+def test_certificate_assembly_and_verification_batched():
+    """§8(f)1: certificate assembly and verification at batch scale
+    (include/credo_gpu_certs.hpp over cg_cert_leaf_hashes). On every node's
+    ordered slots of run_scenario (honest, agree_then_execute, corrupt
+    beyond / within epsilon, C1 and ImageNet shapes), assemble_responses
+    must equal the reference's assemble_response (proxy.cpp:80-186) for
+    every op, and verify_responses must equal verify_response
+    (certificate.cpp:325-347) on every certified response and on forged
+    variants of each (flipped output, path sibling/side, attestation kind,
+    signatures, duplicate attestor, dropped result, failure reason, primary
+    root, altered request) -- genuine ones accepted, every forgery rejected."""
+    if not os.path.exists(VERIFY):
+        pytest.skip("oracle/_ref/integration_verify not built (needs /root/reference at build time)")
+    out = subprocess.run([VERIFY], capture_output=True, text=True, timeout=1200)
+    print(out.stdout, out.stderr)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "0 failures" in out.stdout
