@@ -157,8 +157,8 @@ def resnet50_gemm_plan(B, R, S=224):
     return L
 
 
-def replica_f(world):
-    return (world - 1) // 2  # quorum of a strict majority
+def replica_f(n):
+    return (n - 1) // 3  # the largest f with n >= 3f + 1 (ClusterConfig::validate)
 
 
 def make_dist_group(ctx, B, rank, world, seed=0, eps=0.1, N=None):

@@ -21,10 +21,12 @@
 #pragma once
 
 #include <algorithm>
+#include <atomic>
 #include <map>
 #include <optional>
 #include <set>
 #include <string>
+#include <thread>
 #include <tuple>
 #include <vector>
 
@@ -179,14 +181,38 @@ inline std::vector<Hash32> fold_paths(Context& ctx, const std::vector<Hash32>& l
 }
 
 // merkle::Tree over precomputed leaf hashes: root and every leaf's path.
+// Small trees (a slot's few committers / providers) are folded on the host
+// with SHA-NI (65-byte internal nodes); large ones on the GPU.
 struct HashTree {
   Hash32 root{};
   std::vector<merkle::AuthPath> paths;
 };
 inline HashTree build_hash_tree(Context& ctx, const std::vector<Hash32>& leaves) {
-  constexpr size_t kSteps = 64;
+  constexpr size_t kSteps = 64, kHostMax = 4096;
   const size_t n = leaves.size();
   HashTree t;
+  t.paths.resize(n);
+  if (n <= kHostMax) {  // Tree::build + auth_path (merkle.cpp:47-84)
+    std::vector<std::vector<Hash32>> lv{leaves};
+    while (lv.back().size() > 1) {
+      const auto& prev = lv.back();
+      std::vector<Hash32> next;
+      for (size_t i = 0; i < prev.size(); i += 2)
+        next.push_back(i + 1 < prev.size() ? internal_hash_host(prev[i], prev[i + 1]) : prev[i]);
+      lv.push_back(std::move(next));
+    }
+    t.root = lv.back().back();
+    for (size_t i = 0; i < n; i++) {
+      size_t idx = i;
+      for (size_t l = 0; l + 1 < lv.size(); l++) {
+        if (idx % 2 == 1) t.paths[i].siblings.push_back({lv[l][idx - 1], merkle::Side::left});
+        else if (idx + 1 < lv[l].size())
+          t.paths[i].siblings.push_back({lv[l][idx + 1], merkle::Side::right});
+        idx /= 2;
+      }
+    }
+    return t;
+  }
   std::vector<uint8_t> lh(32 * n), sib(32 * kSteps * n), sides(kSteps * n);
   std::vector<uint64_t> idx(n);
   std::vector<uint32_t> lens(n);
@@ -197,7 +223,6 @@ inline HashTree build_hash_tree(Context& ctx, const std::vector<Hash32>& leaves)
   check(ctx.get(), cg_merkle_auth_paths(ctx.get(), lh.data(), n, idx.data(), (uint32_t)n,
                                         sib.data(), sides.data(), lens.data(),
                                         t.root.data.data()));
-  t.paths.resize(n);
   for (size_t i = 0; i < n; i++)
     for (uint32_t s = 0; s < lens[i]; s++) {
       merkle::PathStep st;
@@ -210,102 +235,99 @@ inline HashTree build_hash_tree(Context& ctx, const std::vector<Hash32>& leaves)
 
 // ---------------------------------------------------------------- assembly
 
-// assemble_response(slot, k, config) for every op k of the slot
-// (proxy.cpp:80-186), the committer trees rebuilt once for the whole slot.
-inline std::vector<std::optional<InferenceResponse>> assemble_responses(
-    Context& ctx, const OrderedSlot& slot, const ClusterConfig& config) {
-  const uint64_t n = config.n(), f = config.f;
-  const size_t nops = slot.ops.size();
-  std::vector<std::optional<InferenceResponse>> out(nops);
-  LeafHasher lh;
-  // rebuild_committer_trees (proxy.cpp:28-48): attest_leaf_bytes per
-  // manifest entry (messages.cpp:315-343); an unresolvable entry drops the
-  // committer
+namespace detail {
+// One slot's trees: rebuild_committer_trees (proxy.cpp:28-48) and every
+// provider's result tree (build_result_tree, messages.cpp:235-258), leaves
+// registered with a LeafHasher shared by all slots of the call.
+struct SlotTrees {
+  using Ref = std::pair<bool, size_t>;  // (GPU leaf, LeafHasher index) / host leaf index
   struct Committer {
     uint64_t node;
     const CommitMsg* commit;
-    std::vector<std::pair<bool, size_t>> leaf;  // (on device, index) / host hash below
-    std::vector<Hash32> host;
+    std::vector<Ref> leaf;
     HashTree tree;
   };
   std::vector<Committer> cts;
-  for (const auto& [c, commit] : slot.commits) {
-    Committer ct{c, &commit, {}, {}, {}};
-    bool complete = true;
-    for (const AttestLeafRef& ref : commit.manifest) {
-      if (ref.kind == AttestLeafRef::Kind::whole_batch) {
-        auto it = slot.r_roots.find(ref.node);
-        if (it == slot.r_roots.end()) { complete = false; break; }
-        ct.leaf.push_back({false, ct.host.size()});
-        ct.host.push_back(merkle::leaf_hash(whole_batch_leaf(it->second)));
-      } else if (ref.kind == AttestLeafRef::Kind::single) {
-        if (ref.op_index >= nops) { complete = false; break; }
-        const OpEntry& op = slot.ops[ref.op_index];
-        if (op.kind != OpKind::request_inf) { complete = false; break; }
-        auto oit = slot.results_by_op.find(ref.op_index);
-        if (oit == slot.results_by_op.end()) { complete = false; break; }
-        auto rit = oit->second.find(ref.node);
-        if (rit == oit->second.end()) { complete = false; break; }
-        ct.leaf.push_back({true, lh.add(*op.request, &rit->second, LeafHasher::single)});
-      } else {
-        if (ref.op_index >= nops) { complete = false; break; }
-        ct.leaf.push_back({false, ct.host.size()});
-        ct.host.push_back(merkle::leaf_hash(failure_leaf(failure_record_for(slot.ops[ref.op_index]))));
-      }
-    }
-    if (!complete || ct.leaf.empty()) continue;
-    cts.push_back(std::move(ct));
-  }
-  // provider result trees (build_result_tree, messages.cpp:235-258) for
-  // every provider with a result in the slot
-  std::set<uint64_t> providers;
-  for (const auto& [k, per] : slot.results_by_op)
-    for (const auto& [p, r] : per) providers.insert(p);
-  std::map<uint64_t, std::vector<std::pair<bool, size_t>>> rleaf;
-  std::vector<Hash32> rhost;
-  for (uint64_t p : providers) {
-    auto& L = rleaf[p];
-    if (slot.ops.empty()) {
-      L.push_back({false, rhost.size()});
-      rhost.push_back(merkle::leaf_hash(noop_leaf(slot.view, slot.seq)));
-    }
-    for (size_t k = 0; k < nops; k++) {
-      const OpEntry& op = slot.ops[k];
-      if (op.kind == OpKind::request_inf) {
-        const InferenceResult* mine = nullptr;
-        if (auto it = slot.results_by_op.find(k); it != slot.results_by_op.end())
-          if (auto jt = it->second.find(p); jt != it->second.end()) mine = &jt->second;
-        L.push_back({true, lh.add(*op.request, mine, mine ? LeafHasher::result : LeafHasher::missing)});
-      } else {
-        L.push_back({false, rhost.size()});
-        rhost.push_back(merkle::leaf_hash(group_op_leaf(op)));
-      }
-    }
-  }
-  lh.run(ctx);
-  for (Committer& ct : cts) {
-    std::vector<Hash32> leaves;
-    for (auto [dev, i] : ct.leaf) leaves.push_back(dev ? lh[i] : ct.host[i]);
-    ct.tree = build_hash_tree(ctx, leaves);
-  }
+  std::map<uint64_t, std::vector<Ref>> rleaf;
   std::map<uint64_t, HashTree> rtree;
-  for (auto& [p, L] : rleaf) {
-    std::vector<Hash32> leaves;
-    for (auto [dev, i] : L) leaves.push_back(dev ? lh[i] : rhost[i]);
-    rtree[p] = build_hash_tree(ctx, leaves);
+  std::vector<Hash32> host;
+
+  void plan(const OrderedSlot& slot, LeafHasher& lh) {
+    const size_t nops = slot.ops.size();
+    for (const auto& [c, commit] : slot.commits) {
+      Committer ct{c, &commit, {}, {}};
+      bool complete = true;
+      for (const AttestLeafRef& ref : commit.manifest) {  // attest_leaf_bytes, messages.cpp:315-343
+        if (ref.kind == AttestLeafRef::Kind::whole_batch) {
+          auto it = slot.r_roots.find(ref.node);
+          if (it == slot.r_roots.end()) { complete = false; break; }
+          ct.leaf.push_back({false, host.size()});
+          host.push_back(merkle::leaf_hash(whole_batch_leaf(it->second)));
+        } else if (ref.kind == AttestLeafRef::Kind::single) {
+          if (ref.op_index >= nops) { complete = false; break; }
+          const OpEntry& op = slot.ops[ref.op_index];
+          if (op.kind != OpKind::request_inf) { complete = false; break; }
+          auto oit = slot.results_by_op.find(ref.op_index);
+          if (oit == slot.results_by_op.end()) { complete = false; break; }
+          auto rit = oit->second.find(ref.node);
+          if (rit == oit->second.end()) { complete = false; break; }
+          ct.leaf.push_back({true, lh.add(*op.request, &rit->second, LeafHasher::single)});
+        } else {
+          if (ref.op_index >= nops) { complete = false; break; }
+          ct.leaf.push_back({false, host.size()});
+          host.push_back(merkle::leaf_hash(failure_leaf(failure_record_for(slot.ops[ref.op_index]))));
+        }
+      }
+      if (complete && !ct.leaf.empty()) cts.push_back(std::move(ct));
+    }
+    std::set<uint64_t> providers;
+    for (const auto& [k, per] : slot.results_by_op)
+      for (const auto& [p, r] : per) providers.insert(p);
+    for (uint64_t p : providers) {
+      auto& L = rleaf[p];
+      if (slot.ops.empty()) {
+        L.push_back({false, host.size()});
+        host.push_back(merkle::leaf_hash(noop_leaf(slot.view, slot.seq)));
+      }
+      for (size_t k = 0; k < nops; k++) {
+        const OpEntry& op = slot.ops[k];
+        if (op.kind == OpKind::request_inf) {
+          const InferenceResult* mine = nullptr;
+          if (auto it = slot.results_by_op.find(k); it != slot.results_by_op.end())
+            if (auto jt = it->second.find(p); jt != it->second.end()) mine = &jt->second;
+          L.push_back({true, lh.add(*op.request, mine,
+                                    mine ? LeafHasher::result : LeafHasher::missing)});
+        } else {
+          L.push_back({false, host.size()});
+          host.push_back(merkle::leaf_hash(group_op_leaf(op)));
+        }
+      }
+    }
   }
 
-  for (size_t op_index = 0; op_index < nops; op_index++) {
+  void build(Context& ctx, const LeafHasher& lh) {
+    auto leaves_of = [&](const std::vector<Ref>& refs) {
+      std::vector<Hash32> v;
+      for (auto [dev, i] : refs) v.push_back(dev ? lh[i] : host[i]);
+      return v;
+    };
+    for (Committer& ct : cts) ct.tree = build_hash_tree(ctx, leaves_of(ct.leaf));
+    for (auto& [p, L] : rleaf) rtree[p] = build_hash_tree(ctx, leaves_of(L));
+  }
+
+  // assemble_response's body (proxy.cpp:80-186) with the trees prebuilt
+  std::optional<InferenceResponse> respond(const OrderedSlot& slot, size_t op_index,
+                                           const ClusterConfig& config) const {
+    const uint64_t n = config.n(), f = config.f;
+    if (op_index >= slot.ops.size()) return std::nullopt;
     const OpEntry& op = slot.ops[op_index];
-    if (op.kind != OpKind::request_inf || !op.request) continue;
-    const InferenceRequest& req = *op.request;
+    if (op.kind != OpKind::request_inf || !op.request) return std::nullopt;
     InferenceResponse resp;
-    resp.request_id = req.request_id;
+    resp.request_id = op.request->request_id;
     if (auto oc = slot.outcomes.find(op_index); oc != slot.outcomes.end()) {
       resp.distance = oc->second.descriptor;
       resp.effective_epsilon = oc->second.epsilon;
     }
-    bool done = false;
     if (op.status == OpStatus::ok) {
       auto results_it = slot.results_by_op.find(op_index);
       if (results_it != slot.results_by_op.end()) {
@@ -361,14 +383,11 @@ inline std::vector<std::optional<InferenceResponse>> assemble_responses(
           resp.kind = InferenceResponse::Kind::success;
           resp.results = std::move(covered);
           resp.certificate = std::move(cert);
-          out[op_index] = std::move(resp);
-          done = true;
+          return resp;
         }
       }
     }
-    if (done) continue;
-    // certified failure (proxy.cpp:163-184)
-    FailureCertificate fc;
+    FailureCertificate fc;  // certified failure (proxy.cpp:163-184)
     fc.view = slot.view;
     fc.seq = slot.seq;
     fc.h_ops = slot.h_ops;
@@ -387,12 +406,35 @@ inline std::vector<std::optional<InferenceResponse>> assemble_responses(
           break;
         }
     }
-    if (fc.attests.size() <= f) continue;
+    if (fc.attests.size() <= f) return std::nullopt;
     resp.kind = InferenceResponse::Kind::failure;
     resp.failure = std::move(fc);
-    out[op_index] = std::move(resp);
+    return resp;
+  }
+};
+}  // namespace detail
+
+// assemble_response(slot, k, config) for every op k of every slot
+// (proxy.cpp:80-186): the request-streaming leaves of all slots hashed on the
+// GPU in one pass, each slot's committer and result trees rebuilt once.
+inline std::vector<std::vector<std::optional<InferenceResponse>>> assemble_responses(
+    Context& ctx, const std::vector<const OrderedSlot*>& slots, const ClusterConfig& config) {
+  LeafHasher lh;
+  std::vector<detail::SlotTrees> trees(slots.size());
+  for (size_t s = 0; s < slots.size(); s++) trees[s].plan(*slots[s], lh);
+  lh.run(ctx);
+  std::vector<std::vector<std::optional<InferenceResponse>>> out(slots.size());
+  for (size_t s = 0; s < slots.size(); s++) {
+    trees[s].build(ctx, lh);
+    for (size_t k = 0; k < slots[s]->ops.size(); k++)
+      out[s].push_back(trees[s].respond(*slots[s], k, config));
   }
   return out;
+}
+
+inline std::vector<std::optional<InferenceResponse>> assemble_responses(
+    Context& ctx, const OrderedSlot& slot, const ClusterConfig& config) {
+  return assemble_responses(ctx, std::vector<const OrderedSlot*>{&slot}, config)[0];
 }
 
 // ------------------------------------------------------------ verification
@@ -509,8 +551,8 @@ inline std::vector<bool> verify_responses(Context& ctx,
     h_pp = pre_prepare_hash_of(view, seq, h_ops, r_root, sig);
     return true;
   };
-  for (size_t i = 0; i < R; i++) {
-    if (!live[i]) continue;
+  auto check_one = [&](size_t i) -> bool {
+    if (!live[i]) return false;
     const InferenceRequest& request = requests[i];
     const InferenceResponse& resp = responses[i];
     try {
@@ -519,7 +561,7 @@ inline std::vector<bool> verify_responses(Context& ctx,
         Hash32 h_pp;
         if (!binding(cert.view, cert.seq, cert.h_ops, cert.primary_r_root, cert.pre_prepare_sig,
                      h_pp))
-          continue;
+          return false;
         const uint64_t primary = cert.view % n;
         std::set<uint64_t> providers;
         const uint64_t version = resp.results.front().group_version;
@@ -563,14 +605,14 @@ inline std::vector<bool> verify_responses(Context& ctx,
           }
           if (good && attestors.size() <= f) good = false;
         }
-        ok[i] = good;
+        return good;
       } else {  // verify_failure
         const auto& fc = *resp.failure;
         if (fc.record.request_id != request.request_id || fc.record.group_id != request.group_id)
-          continue;
+          return false;
         Hash32 h_pp;
         if (!binding(fc.view, fc.seq, fc.h_ops, fc.primary_r_root, fc.pre_prepare_sig, h_pp))
-          continue;
+          return false;
         std::set<uint64_t> attestors;
         bool good = true;
         for (size_t a = 0; a < fc.attests.size(); a++) {
@@ -584,12 +626,24 @@ inline std::vector<bool> verify_responses(Context& ctx,
             break;
           }
         }
-        ok[i] = good && attestors.size() > f;
+        return good && attestors.size() > f;
       }
     } catch (...) {
-      ok[i] = false;
+      return false;
     }
-  }
+  };
+  // the signature checks (libsodium Ed25519, thread-safe) across host threads
+  std::vector<uint8_t> okb(R, 0);
+  std::atomic<size_t> next{0};
+  auto worker = [&] {
+    for (size_t i; (i = next.fetch_add(1)) < R;) okb[i] = check_one(i) ? 1 : 0;
+  };
+  const size_t nt = std::min<size_t>(std::max(1u, std::thread::hardware_concurrency()), (R + 7) / 8);
+  std::vector<std::thread> pool;
+  for (size_t t = 1; t < nt; t++) pool.emplace_back(worker);
+  worker();
+  for (auto& t : pool) t.join();
+  for (size_t i = 0; i < R; i++) ok[i] = okb[i] != 0;
   return ok;
 }
 

@@ -33,7 +33,10 @@ shapes = [("square K2048", 32768, 2048, 2048, 256, 0),
           ("l2 c3 +res pair", 301056, 512, 128, 256, 3),
           ("l3 c1", 75264, 256, 1024, 256, 0),
           ("l3 c1 BN128", 75264, 256, 1024, 128, 0),
-          ("l4 c1", 18816, 512, 2048, 256, 0)]
+          ("l4 c1", 18816, 512, 2048, 256, 0),
+          ("l1 c1 K64", 1204224, 64, 64, 64, 0),
+          ("l1 c1 K256", 1204224, 64, 256, 64, 0),
+          ("l1 c3 +res", 1204224, 256, 64, 256, 1)]
 only = sys.argv[1] if len(sys.argv) > 1 else None  # run one shape (for ncu)
 for label, M, N, K, BN, res in shapes:
     if only and label != only:
@@ -61,7 +64,7 @@ for label, M, N, K, BN, res in shapes:
     print(f"{label}: ours {us.value:.1f} us {fl / us.value / 1e6:.0f} TF/s | cublas {tus:.1f} us "
           f"{fl / tus / 1e6:.0f} TF/s | tiles/CTA {n}, commit-to-commit {per:.0f} cyc "
           f"(MMA floor {K // 16 * BN // 2} cyc)")
-    if "l4 c3" in label or "l3 c3" in label:
+    if "l4 c3" in label or "l3 c3" in label or label.startswith("l1"):
         t0 = t[t > 0].min()
         print("tile " + " ".join(f"{x:>8s}" for x in names))
         for i in range(min(n, 6)):
