@@ -48,9 +48,21 @@ class LeafHasher {
   // leaf_hash(missing_result_leaf(req)) (res unused); returns its index.
   size_t add(const InferenceRequest& req, const InferenceResult* res, Kind kind) {
     Batch& b = batches_[{req.group_id, req.input.size()}];
-    auto [it, fresh] = b.index.emplace(&req, (uint32_t)b.reqs.size());
-    if (fresh) b.reqs.push_back(&req);
-    Entry e{it->second, kind, {}, out_.size()};
+    // one prefix per distinct request: the same object, or an equal copy
+    // (a response set usually carries its request once per response)
+    uint32_t k = UINT32_MAX;
+    if (auto it = b.index.find(&req); it != b.index.end()) k = it->second;
+    else {
+      for (uint32_t c : b.by_id[req.request_id])
+        if (*b.reqs[c] == req) { k = c; break; }
+      if (k == UINT32_MAX) {
+        k = (uint32_t)b.reqs.size();
+        b.reqs.push_back(&req);
+        b.by_id[req.request_id].push_back(k);
+      }
+      b.index.emplace(&req, k);
+    }
+    Entry e{k, kind, {}, out_.size()};
     if (kind != missing) {
       Encoder enc;
       res->encode(enc);
@@ -127,6 +139,7 @@ class LeafHasher {
   struct Batch {
     std::vector<const InferenceRequest*> reqs;
     std::map<const InferenceRequest*, uint32_t> index;
+    std::map<Hash32, std::vector<uint32_t>> by_id;
     std::vector<Entry> entries;
   };
   std::map<std::pair<std::string, size_t>, Batch> batches_;

@@ -227,7 +227,11 @@ int main() {
       }
       // dropping one of N results still leaves >= N - f valid ones: not a
       // forgery; every other variant must be rejected
-      if (what[i] != "drop_result") accepted += ref_ok[i];
+      // (nor is an altered request input under a failure certificate:
+      // verify_failure binds only the request id and group, certificate.cpp:290-316)
+      const bool forgery = what[i] != "drop_result" &&
+                           !(what[i] == "request" && resps[i].kind == InferenceResponse::Kind::failure);
+      if (forgery || what[i] == "genuine") accepted += ref_ok[i];
       if (what[i] == "genuine") {
         genuine++;
         genuine_ok += ref_ok[i];
@@ -236,7 +240,7 @@ int main() {
     const bool ok = mism == 0 && vmism == 0 && ops > 0 && genuine > 0 && genuine_ok == genuine &&
                     accepted == genuine_ok;
     std::printf("%-20s slots %3lu ops %4lu (success %lu, failure %lu, none %lu) assembly "
-                "mismatches %lu | responses %lu (%lu genuine) accepted %lu (excl. drop_result) verify "
+                "mismatches %lu | responses %lu (%lu genuine) accepted %lu (genuine + forgeries) verify "
                 "mismatches %lu  %s\n",
                 c.name, (unsigned long)slots, (unsigned long)ops, (unsigned long)succ,
                 (unsigned long)fail, (unsigned long)none, (unsigned long)mism,
