@@ -139,7 +139,10 @@ def resnet50_gemm_plan(B, R, S=224):
     L = []
     px = lambda h: B * h * h  # noqa: E731
     H1, H = S // 2, S // 4
-    L.append(("conv1", 2 * px(H1) * 64 * 147 * R, px(H1) * 192 * 2 + R * px(H1) * 64 * 2))
+    # conv1: the s2d stem reads the 2-plane space-to-depth image (16 B per
+    # plane and grid pixel, ((S + 6) / 2)^2 grid pixels per image)
+    G = (S + 6) // 2
+    L.append(("conv1", 2 * px(H1) * 64 * 147 * R, B * G * G * 32 + R * px(H1) * 64 * 2))
     cin = 64
     for stage, (w, n) in enumerate(((64, 3), (128, 4), (256, 6), (512, 3))):
         for i in range(n):

@@ -49,6 +49,36 @@ __global__ void chw_to_nhwc4_pad3_kernel(const double* __restrict__ in, int B, i
   out[t] = *reinterpret_cast<uint2*>(b);
 }
 
+// The s2d stem operand (default): f64 CHW -> the 2x2 space-to-depth image
+// of the input padded by 3 (S + 6 = 2 Gs), channel (py*2 + px)*3 + c holding
+// padded pixel (2Y + py, 2X + px) channel c, 12 channels padded to 16:
+// [B * Gs * Gs][16] bf16, one 32-byte K = 16 row per pixel
+// (ConvGemmArgs::s2d). One thread per s2d pixel; one f64 -> bf16 rounding,
+// as the im2col path.
+__global__ void chw_to_s2d16_kernel(const double* __restrict__ in, int B, int S,
+                                    uint4* __restrict__ out) {
+  const int Gs = (S + 6) / 2;
+  const size_t npix = (size_t)B * Gs * Gs;
+  const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= npix) return;
+  const int n = (int)(t / ((size_t)Gs * Gs)), rem = (int)(t - (size_t)n * Gs * Gs);
+  const int Y = rem / Gs, X = rem - Y * Gs;
+  __align__(16) bf16 v[16];
+#pragma unroll
+  for (int q = 0; q < 4; q++) {
+    const int h = 2 * Y + (q >> 1) - 3, w = 2 * X + (q & 1) - 3;
+    const bool inside = h >= 0 && h < S && w >= 0 && w < S;
+#pragma unroll
+    for (int c = 0; c < 3; c++)
+      v[q * 3 + c] =
+          __double2bfloat16(inside ? __ldg(in + (((size_t)n * 3 + c) * S + h) * S + w) : 0.0);
+  }
+#pragma unroll
+  for (int k = 12; k < 16; k++) v[k] = __float2bfloat16(0.f);
+  out[2 * t] = *reinterpret_cast<const uint4*>(v);
+  out[2 * t + 1] = *reinterpret_cast<const uint4*>(v + 8);
+}
+
 // Pass 2: [B*Ho*Wo, 192] im2col from the padded NHWC4 grid (K = (dr*7+ds)*3+c,
 // zero beyond 147). A warp builds 32 consecutive output rows: lane = row,
 // taps loaded as 8-byte pixels (adjacent lanes read pixels 16 B apart), the
@@ -107,8 +137,10 @@ __global__ void __launch_bounds__(32 * kIm2colWarps) conv1_im2col_nhwc4_kernel(
 // horizontally adjacent outputs x 8 channels: their windows share a column,
 // so 15 loads instead of 18; packed bf16x2 max (exact, like fmaxf on the
 // widened values).
-__global__ void maxpool3s2_kernel(const bf16* __restrict__ in, int B, int H, int C,
-                                  bf16* __restrict__ out) {
+// The input is H x H pixels stored with a row pitch of P pixels and Gh rows
+// per image (P = Gh = H: compact; the s2d stem's output grid: Gs x Gs).
+__global__ void maxpool3s2_kernel(const bf16* __restrict__ in, int B, int H, int C, int P,
+                                  int Gh, bf16* __restrict__ out) {
   const int Ho = (H + 1) / 2, chunks = C / 8, Wq = (Ho + 1) / 2;
   size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   size_t pq = t / chunks;
@@ -123,7 +155,7 @@ __global__ void maxpool3s2_kernel(const bf16* __restrict__ in, int B, int H, int
   for (int dr = 0; dr < 3; dr++) {
     const int h = 2 * ho - 1 + dr;
     if (h < 0 || h >= H) continue;
-    const bf16* row = in + ((size_t)n * H + h) * H * C + ch * 8;
+    const bf16* row = in + ((size_t)n * Gh + h) * P * C + ch * 8;
 #pragma unroll
     for (int dc = 0; dc < 5; dc++) {
       const int w = 4 * j - 1 + dc;
@@ -256,6 +288,9 @@ struct Block {
 // 128 x 64 tile is shared-memory-bandwidth bound (A is re-read per 64
 // columns) while 128 x 256 streams A once per 256 columns. Ties -> wider.
 int kSmallKMaxBN = 256;  // env CREDO_SMALLK_BN overrides (tuning)
+// ResNet stem: the s2d conv (default) or CREDO_NO_S2D=1, the im2col (K = 192)
+const bool kUseS2D = std::getenv("CREDO_NO_S2D") == nullptr;
+constexpr int kS2DMaxS = 2 * (256 - 128 - 3) - 6;  // a dy-pair box (128 + Gs + 3 rows) fits 256
 const bool kUseHalo = std::getenv("CREDO_NO_HALO") == nullptr;  // A/B switch for measurements
 
 int pick_bn(int rows, int N, int replicas = 1) {
@@ -280,8 +315,10 @@ class ResNet final : public CnnModel {
     S_ = (int)std::lround(std::sqrt((double)in_dim / 3.0));
     if ((uint64_t)3 * S_ * S_ != in_dim || S_ % 32 != 0)
       throw std::invalid_argument("cnn file: input_dim must be 3*S*S with S % 32 == 0");
-    // conv1 + bn1: K = 147 padded to 192 (3 k-blocks of 64)
-    fold(conv1_, T, "conv1.weight", "bn1", 7, 2, 192);
+    // conv1 + bn1: the s2d stem (16 taps of K = 16) or K = 147 padded to 192
+    s2d_ = kUseS2D && S_ <= kS2DMaxS;
+    if (s2d_) fold_s2d(conv1_, T, "conv1.weight", "bn1");
+    else fold(conv1_, T, "conv1.weight", "bn1", 7, 2, 192);
     flops_ = 2.0 * (S_ / 2) * (S_ / 2) * 64 * 147;
     int H = S_ / 4, cin = 64;
     const int widths[4] = {64, 128, 256, 512};
@@ -361,7 +398,7 @@ class ResNet final : public CnnModel {
     };
     xcol_ = alloc(B * H1 * H1 * 192);
     nhwc4_ = alloc(B * (S_ + 6) * (S_ + 6) * 4);
-    c1out_ = alloc(B * H1 * H1 * 64);
+    c1out_ = alloc(B * (size_t)((S_ + 6) / 2) * ((S_ + 6) / 2) * 64);  // s2d grid >= H1 x H1
     size_t act = 0, t2 = 0, dsz = 0, g1 = 0;
     for (auto& b : blocks_) {
       act = std::max(act, B * b.H_out * b.H_out * b.cout);
@@ -385,14 +422,24 @@ class ResNet final : public CnnModel {
   }
 
   size_t prepared_bytes(uint32_t B) const override {
-    return (size_t)B * (S_ / 2) * (S_ / 2) * 192 * 2;
+    const size_t Gs = (S_ + 6) / 2;
+    return s2d_ ? (size_t)B * Gs * Gs * 32 : (size_t)B * (S_ / 2) * (S_ / 2) * 192 * 2;
   }
-  std::string prep_kind() const override { return "im2col7x7s2k192/" + std::to_string(S_); }
+  std::string prep_kind() const override {
+    return (s2d_ ? "s2d16/" : "im2col7x7s2k192/") + std::to_string(S_);
+  }
 
   void prepare_input(const double* d_in, uint32_t B, void* prepped, cudaStream_t st) override {
     const int H1 = S_ / 2, Sp = S_ + 6;
     if (B > maxB_) reserve(B);
     timer_begin(st, kTimeAux);
+    if (s2d_) {  // one pass: f64 CHW -> the padded s2d image
+      chw_to_s2d16_kernel<<<grid_for((size_t)B * (Sp / 2) * (Sp / 2)), 256, 0, st>>>(
+          d_in, B, S_, reinterpret_cast<uint4*>(prepped));
+      CG_CHECK_LAUNCH();
+      timer_end(st, kTimeAux);
+      return;
+    }
     // two coalesced passes: f64 CHW -> bf16 NHWC4 (pad 3), then im2col
     chw_to_nhwc4_pad3_kernel<<<grid_for((size_t)B * Sp * Sp), 256, 0, st>>>(
         d_in, B, S_, reinterpret_cast<uint2*>(nhwc4_));
@@ -436,6 +483,7 @@ class ResNet final : public CnnModel {
     void* out = nullptr;
     int ldout = 0, out_f32 = 0, relu = 0, mode = 0, H = 0, rows_out = 0;
     int halo_lo = 0;  // > 0: 3x3 taps fed from one halo box per channel block
+    int s2d = 0, gh = 0, gw = 0;  // the s2d stem (ConvGemmArgs::s2d)
   };
   struct Op {
     bool gemm = false;
@@ -481,16 +529,28 @@ class ResNet final : public CnnModel {
     };
     const int H1 = S_ / 2;
     const int zero = 0;
-    // conv1 (im2col operand) -> c1out, then maxpool -> act_[0]
-    gemm(conv1_, reinterpret_cast<const bf16*>(x0), B * H1 * H1, B * H1 * H1, conv1_.Kc, 1,
-         &zero, nullptr, 0, c1out_, 64, 0, 1, kRowIdentity, 0, B * H1 * H1);
+    // conv1 (s2d stem or im2col operand) -> c1out, then maxpool -> act_[0]
+    if (s2d_) {
+      const int Gs = (S_ + 6) / 2;
+      // output stays on the Gs x Gs grid (identity rows: TMA-store epilogue;
+      // the max pool reads the H1 x H1 interior of each image's grid)
+      gemm(conv1_, reinterpret_cast<const bf16*>(x0), B * Gs * Gs, B * Gs * Gs, 16, 1, &zero,
+           nullptr, 0, c1out_, 64, 0, 1, kRowIdentity, H1, B * Gs * Gs);
+      L.back().g.ntaps = 16;  // taps (dy, dx) are implicit in the s2d mode
+      L.back().g.s2d = 1;
+      L.back().g.gh = L.back().g.gw = Gs;
+    } else {
+      gemm(conv1_, reinterpret_cast<const bf16*>(x0), B * H1 * H1, B * H1 * H1, conv1_.Kc, 1,
+           &zero, nullptr, 0, c1out_, 64, 0, 1, kRowIdentity, 0, B * H1 * H1);
+    }
     {
       bf16* in = c1out_;
       bf16* out = act_[0];
-      aux([in, out, B, H1](cudaStream_t st) {
+      const int P = s2d_ ? (S_ + 6) / 2 : H1;  // conv1 output pitch / rows per image
+      aux([in, out, B, H1, P](cudaStream_t st) {
         const size_t Ho = (H1 + 1) / 2;
         size_t th = (size_t)B * Ho * ((Ho + 1) / 2) * (64 / 8);
-        maxpool3s2_kernel<<<grid_for(th), 256, 0, st>>>(in, B, H1, 64, out);
+        maxpool3s2_kernel<<<grid_for(th), 256, 0, st>>>(in, B, H1, 64, P, P, out);
         CG_CHECK_LAUNCH();
       });
     }
@@ -619,6 +679,30 @@ class ResNet final : public CnnModel {
     }
   }
 
+  // conv1 (7x7/2, pad 3) as a 4x4 stride-1 conv over the 2x2 space-to-depth
+  // image: tap (dy, dx), s2d channel (py*2 + px)*3 + c is kernel position
+  // (2 dy + py, 2 dx + px) channel c (zero at kernel row / column 7). Layout
+  // [tap][cout][16] (K = 16 per tap), the resident weight tile of the s2d
+  // GEMM mode.
+  void fold_s2d(ConvW& c, std::map<std::string, HostTensor>& T, const std::string& wname,
+                const std::string& bn) {
+    fold(c, T, wname, bn, 7, 2, 147);  // [cout][(dr*7 + ds)*3 + ci]
+    if (c.cin != 3 || c.cout != 64) throw std::invalid_argument("cnn file: stem must be 3 -> 64");
+    std::vector<uint16_t> w((size_t)16 * 64 * 16, 0);
+    for (int o = 0; o < 64; o++)
+      for (int tap = 0; tap < 16; tap++)
+        for (int ch = 0; ch < 12; ch++) {
+          const int dy = tap / 4, dx = tap % 4, q = ch / 3, ci = ch % 3;
+          const int dr = 2 * dy + (q >> 1), ds = 2 * dx + (q & 1);
+          if (dr > 6 || ds > 6) continue;
+          w[((size_t)tap * 64 + o) * 16 + ch] =
+              c.hw[(size_t)o * 147 + (dr * 7 + ds) * 3 + ci];
+        }
+    c.hw.swap(w);
+    c.Kc = 16;
+    c.ntaps = 16;
+  }
+
   std::vector<ConvW*> all_convs() {
     std::vector<ConvW*> v{&conv1_, &fc_};
     for (auto& b : blocks_) {
@@ -657,10 +741,16 @@ class ResNet final : public CnnModel {
     std::vector<Operand> A(R), Bm(R);
     ConvGemmGroup g;
     g.n = R;
+    if (d0.s2d) BN = 64;
     for (int r = 0; r < R; r++) {
       const GemmDesc& d = *ds[r];
-      make_operand(A[r], d.A, d.rowsA, d.Kc, 128 + 2 * d.halo_lo);
-      make_operand(Bm[r], d.c->w, d.c->cout, d.Kc * d.ntaps, BN);
+      if (d.s2d) {
+        make_operand_s2d_a(A[r], d.A, d.rowsA, 128 + d.gw + 3);
+        make_operand_s2d_b(Bm[r], d.c->w, 16 * d.c->cout);
+      } else {
+        make_operand(A[r], d.A, d.rowsA, d.Kc, 128 + 2 * d.halo_lo);
+        make_operand(Bm[r], d.c->w, d.c->cout, d.Kc * d.ntaps, BN);
+      }
       g.A[r] = &A[r];
       g.B[r] = &Bm[r];
       g.bias[r] = d.c->b;
@@ -672,7 +762,7 @@ class ResNet final : public CnnModel {
     a.N = d0.c->cout;
     a.Kc = d0.Kc;
     a.ntaps = d0.ntaps;
-    for (int t = 0; t < d0.ntaps; t++) a.tap_off[t] = d0.taps[t];
+    for (int t = 0; t < d0.ntaps && t < 9; t++) a.tap_off[t] = d0.taps[t];
     a.ld_res = d0.ldres;
     a.ld_out = d0.ldout;
     a.out_f32 = d0.out_f32;
@@ -682,6 +772,9 @@ class ResNet final : public CnnModel {
     a.W = d0.H;
     a.rows_out = d0.rows_out;
     a.halo_lo = d0.halo_lo;
+    a.s2d = d0.s2d;
+    a.gh = d0.gh;
+    a.gw = d0.gw;
     auto p = std::make_shared<PreparedGemm>();
     prepare_conv_gemm(*p, g, a, BN);
     return [p](cudaStream_t st) { launch_prepared(*p, st); };
@@ -697,6 +790,7 @@ class ResNet final : public CnnModel {
   std::vector<Block> blocks_;
   uint32_t maxB_ = 0;
   std::vector<void*> bufs_;
+  bool s2d_ = false;  // the s2d stem (kUseS2D, image size within kS2DMaxS)
   bf16 *xcol_ = nullptr, *nhwc4_ = nullptr, *c1out_ = nullptr, *act_[2] = {nullptr, nullptr}, *t2_ = nullptr,
        *ds_ = nullptr, *g1_ = nullptr, *pooled_ = nullptr;
   std::map<std::pair<int, int>, bf16*> pads_;

@@ -23,6 +23,8 @@ constexpr int BM = 128, BK = 64, kThreads = 352;
 constexpr int kEpiWarps = 8, kStgLd = 36;        // staging row stride (floats)
 constexpr int A_BYTES = BM * BK * 2;
 constexpr int kHaloBytes = 256 * BK * 2;  // largest halo box (BM + 2*halo_lo <= 256 rows)
+// s2d stem: one box per dy pair, BM + gw + 3 <= 256 rows of 32 bytes (16 channels)
+constexpr int kS2DSlot = 256 * 32;
 #ifndef CG_RES_COLS
 #define CG_RES_COLS 64
 #endif
@@ -198,6 +200,24 @@ __device__ __forceinline__ void umma_bf16_w(uint32_t d, uint64_t a, uint64_t b, 
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d),
       "l"(a), "l"(b), "r"(idesc), "r"(accum));
 }
+// Four MMAs under one elect: descriptors a + 2j, b + bstep * j (j = 0..3),
+// the first accumulating when accum != 0, the rest always (the s2d stem's
+// 4 dx taps of one dy box: +32 B rows of A, +2 KB tap tiles of B).
+template <int BSTEP>
+__device__ __forceinline__ void umma_bf16_x4_w(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
+                                               uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t.reg .b64 a1, a2, a3, b1, b2, b3;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "add.s64 a1, %1, 2;\n\tadd.s64 a2, %1, 4;\n\tadd.s64 a3, %1, 6;\n\t"
+      "add.s64 b1, %2, %5;\n\tadd.s64 b2, %2, %6;\n\tadd.s64 b3, %2, %7;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %3, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b2, %3, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b3, %3, 1;\n}" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accum), "n"(BSTEP), "n"(2 * BSTEP), "n"(3 * BSTEP));
+}
 __device__ __forceinline__ void umma_commit_w(uint64_t* b) {
   asm volatile(
       "{\n\t.reg .pred e;\n\t"
@@ -237,6 +257,14 @@ __device__ __forceinline__ uint64_t smem_desc_sw128(const void* p) {
 __device__ __forceinline__ uint64_t smem_desc_sw128_row(uint32_t addr, int) {
   return (((uint64_t)addr >> 4) & 0x3FFFull) | (1ull << 16) | (64ull << 32) | (1ull << 46) |
          (2ull << 61);
+}
+// K-major operand with 32-byte rows (K = 16 bf16) under the 32B swizzle (the
+// s2d stem): 8-row atoms of 256 B (SBO), layout type 6. Like the 128B halo
+// mode, the start address may sit at any 32-byte row of a TMA-written box:
+// the swizzle follows absolute smem address bits.
+__device__ __forceinline__ uint64_t smem_desc_sw32_row(uint32_t addr) {
+  return (((uint64_t)addr >> 4) & 0x3FFFull) | (1ull << 16) | ((uint64_t)(256 >> 4) << 32) |
+         (1ull << 46) | (6ull << 61);
 }
 // tcgen05.ld without the wait (the registers are valid after tmem_ld_wait).
 __device__ __forceinline__ void tmem_ld32_issue(uint32_t taddr, uint32_t (&v)[32]) {
@@ -307,9 +335,13 @@ __device__ __forceinline__ uint32_t sw64(int r, int j) {
 }
 
 __device__ __forceinline__ int remap_row(int M, int rows_out, int mode, int H,
-                                         int W, int m) {
+                                         int W, int m, int gh = 0, int gw = 0) {
   if (m >= M) return -1;
   if (mode == kRowIdentity) return m < rows_out ? m : -1;
+  if (mode == kRowGridToCompact) {  // per-image gh x gw grid, output H x W
+    const int G = gh * gw, n = m / G, rem = m - n * G, i = rem / gw, j = rem - i * gw;
+    return (i < H && j < W) ? (n * H + i) * W + j : -1;
+  }
   if (mode == kRowPhaseGridToCompact) {  // H, W = output dims, grid (H+1)(W+1)
     const int Wq = W + 1, HqWq = (H + 1) * Wq;
     const int n = m / HqWq, rem = m - n * HqWq, i = rem / Wq, j = rem - i * Wq;
@@ -456,10 +488,13 @@ struct TileSched {
 // half and the peer releases the accumulator on the leader's barrier.
 // Per SM and 128x256 output this halves the weight bytes written to and read
 // from shared memory (the bound of the BN=256 mainloop).
-template <int BN, int STAGES, int kResSlots, int HALO, int RESB, int PAIR>
+template <int BN, int STAGES, int kResSlots, int HALO, int RESB, int PAIR, int S2D = 0>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_gemm_kernel(const __grid_constant__ GemmGroupParams gp, const ConvGemmArgs a) {
   static_assert(!PAIR || (RESB == 0 && (HALO == 0 || kResSlots == 0)), "pair: streamed weights");
+  static_assert(!S2D || (BN == 64 && RESB == 4 && HALO > 0 && !PAIR), "s2d stem layout");
+  // s2d stem: a ring slot holds one dy box (2 planes x (BM + 3) rows x 16 B)
+  constexpr int kHaloSlot = S2D ? kS2DSlot : kHaloBytes;
   constexpr int B_BYTES = (PAIR ? BN / 2 : BN) * BK * 2;  // this CTA's weight tile
   constexpr uint32_t TMEM_COLS = 2 * BN;
   // BN = 64 (2 chunks of 32 columns): the two epilogue warp groups take
@@ -477,7 +512,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // output staging (64B swizzle), then barriers.
   uint8_t* smem = smem_raw + ((1024 - (su32(smem_raw) & 1023)) & 1023);
   uint8_t* sA = smem;
-  uint8_t* sB = smem + (HALO > 0 ? HALO * kHaloBytes : STAGES * A_BYTES);
+  uint8_t* sB = smem + (HALO > 0 ? HALO * kHaloSlot : STAGES * A_BYTES);
   uint8_t* s_res = sB + (RESB > STAGES ? RESB : STAGES) * B_BYTES;  // residual ring (SW64)
   float* s_epi = reinterpret_cast<float*>(s_res + kResSlots * 8192);  // 36 KB
   uint64_t* full = reinterpret_cast<uint64_t*>(s_epi + kEpiWarps * 32 * kStgLd);
@@ -510,7 +545,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int num_mt = (a.M + BMT - 1) / BMT;
   const int tiles = num_mt * num_n * gp.n;
   const int first_unit = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
-  const int kpt = a.Kc / BK, num_k = a.ntaps * kpt;
+  const int kpt = S2D ? 4 : a.Kc / BK, num_k = a.ntaps * kpt;  // s2d: kpt = the 4 dy boxes
   (void)num_m;
   auto coords = [&](int t, int& r, int& m0, int& n0) {
     if constexpr (RESB > 0) {
@@ -621,10 +656,24 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (r != wr) {
             if (wl > 0) mbar_wait(&empty[0], (uint32_t)((wl - 1) & 1));
             mbar_expect_tx(&full[0], RESB * B_BYTES);
-            for (int j = 0; j < RESB; j++)
-              tma_load_2d(&gp.B[r], &full[0], sB + j * B_BYTES, j * BK, n0);
+            if constexpr (S2D) {  // 16 taps x 64 rows x 32 B, 256-row boxes
+              for (int j = 0; j < RESB * B_BYTES / 8192; j++)
+                tma_load_2d(&gp.B[r], &full[0], sB + j * 8192, 0, j * 256);
+            } else {
+              for (int j = 0; j < RESB; j++)
+                tma_load_2d(&gp.B[r], &full[0], sB + j * B_BYTES, j * BK, n0);
+            }
             wr = r;
             wl++;
+          }
+          if constexpr (S2D) {  // one box per dy pair: BM + gw + 3 rows of 16 channels
+            for (int h = 0; h < 2; h++) {
+              mbar_wait(&hempty[hs], hphase ^ 1);
+              mbar_expect_tx(&hfull[hs], (BM + a.gw + 3) * 32);
+              tma_load_2d(&gp.A[r], &hfull[hs], sA + hs * kHaloSlot, 0, m0 + 2 * h * a.gw);
+              if (++hs == HALO) { hs = 0; hphase ^= 1; }
+            }
+            continue;
           }
           const int hrows = BM + 2 * a.halo_lo;
           for (int cb = 0; cb < kpt; cb++) {
@@ -728,6 +777,29 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_fence_after();
             mr = r_;
             ml++;
+          }
+          if constexpr (S2D) {
+            // 16 taps (dy, dx): A = the dy box from row dx, B = the tap's [64][16]
+            const uint32_t sA_u = su32(sA), sB_u = su32(sB);
+            for (int h = 0; h < 2; h++) {
+              mbar_wait(&hfull[hs], hphase);
+              if (h == 0) CG_TRACE(3, ti);
+              tc_fence_after();
+              const uint32_t hbase = sA_u + (uint32_t)(hs * kHaloSlot);
+#pragma unroll
+              for (int j = 0; j < 2; j++) {  // dy = 2h + j: rows j * gw on of the box
+                const int dy = 2 * h + j;
+                umma_bf16_x4_w<2048 / 16>(
+                    d, smem_desc_sw32_row(hbase + (uint32_t)(j * a.gw * 32)),
+                    smem_desc_sw32_row(sB_u + (uint32_t)(dy * 4 * 2048)), idesc, dy != 0);
+              }
+              umma_commit_w(&hempty[hs]);
+              if (++hs == HALO) { hs = 0; hphase ^= 1; }
+            }
+            umma_commit_w(&tfull[acc]);
+            CG_TRACE(4, ti);
+            if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+            continue;
           }
           // 9 taps unrolled: tap offsets come from the kernel parameters and
           // every descriptor is uniform arithmetic (no per-MMA register moves)
@@ -899,7 +971,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float* bias_r = gp.bias[r_];
       const __nv_bfloat16* res_r = gp.residual[r_];
       void* out_r = gp.out[r_];
-      const int my_orow = remap_row(a.M, a.rows_out, a.row_mode, a.H, a.W, m0 + q * 32 + lane);
+      const int my_orow =
+          remap_row(a.M, a.rows_out, a.row_mode, a.H, a.W, m0 + q * 32 + lane, a.gh, a.gw);
 
       mbar_wait(&tfull[acc], acc_phase);
       if (warp == 2) CG_TRACE(5, tile_i);
@@ -1126,9 +1199,9 @@ EncodeFn get_encode() {
   return fn;
 }
 
-template <int BN, int STAGES, int kResSlots, int HALO, int RESB, int PAIR = 0>
+template <int BN, int STAGES, int kResSlots, int HALO, int RESB, int PAIR = 0, int S2D = 0>
 constexpr int smem_bytes() {
-  return 1024 + (HALO > 0 ? HALO * kHaloBytes : STAGES * A_BYTES) +
+  return 1024 + (HALO > 0 ? HALO * (S2D ? kS2DSlot : kHaloBytes) : STAGES * A_BYTES) +
          (RESB > STAGES ? RESB : STAGES) * (PAIR ? BN / 2 : BN) * BK * 2 +
          kResSlots * 8192 + kEpiWarps * 32 * kStgLd * 4 +
          8 * (2 * STAGES + 4 + 2 * (kResSlots > 0 ? kResSlots : 1) + 2 * (HALO > 0 ? HALO : 1)) +
@@ -1154,13 +1227,13 @@ int tiles_per_unit(const ConvGemmArgs& a, int BN, int tiles) {
   return std::max(T, 1);
 }
 
-template <int BN, int STAGES, int RS, int HALO = 0, int RESB = 0, int PAIR = 0>
+template <int BN, int STAGES, int RS, int HALO = 0, int RESB = 0, int PAIR = 0, int S2D = 0>
 void launch_t(const PreparedGemm& p, cudaStream_t st, int max_ctas) {
-  constexpr int smem = smem_bytes<BN, STAGES, RS, HALO, RESB, PAIR>();
+  constexpr int smem = smem_bytes<BN, STAGES, RS, HALO, RESB, PAIR, S2D>();
   static_assert(smem <= 232448, "smem budget");
   static std::atomic<uint64_t> attr{0};
   once_per_device(attr, [] {
-    CG_CUDA(cudaFuncSetAttribute(conv_gemm_kernel<BN, STAGES, RS, HALO, RESB, PAIR>,
+    CG_CUDA(cudaFuncSetAttribute(conv_gemm_kernel<BN, STAGES, RS, HALO, RESB, PAIR, S2D>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   });
   ConvGemmArgs a = p.args;
@@ -1210,7 +1283,8 @@ void launch_t(const PreparedGemm& p, cudaStream_t st, int max_ctas) {
     at[0].val.programmaticStreamSerializationAllowed = g_pdl;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    CG_CUDA(cudaLaunchKernelEx(&cfg, conv_gemm_kernel<BN, STAGES, RS, HALO, RESB, PAIR>, p.gp, a));
+    CG_CUDA(cudaLaunchKernelEx(&cfg, conv_gemm_kernel<BN, STAGES, RS, HALO, RESB, PAIR, S2D>,
+                               p.gp, a));
     launch_counter_add(1);
   }
   timer_end(st, kTimeGemm);
@@ -1390,6 +1464,32 @@ void make_operand(Operand& op, const void* ptr, int rows, int cols, int box_rows
   op.box_rows = box_rows;
 }
 
+// [rows, 16] bf16 (32-byte rows) with the 32B swizzle: the s2d stem's
+// image (box_rows-row boxes) and weights (256-row boxes).
+static void make_operand_k16(Operand& op, const void* ptr, int rows, int box_rows) {
+  if (reinterpret_cast<uintptr_t>(ptr) % 16) throw InvalidArgument("operand misaligned");
+  cuuint64_t dims[2] = {16, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {32};
+  cuuint32_t box[2] = {16, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = get_encode()(&op.map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                            const_cast<void*>(ptr), dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw CudaError("s2d tensor map failed: " + std::to_string((int)r));
+  op.ptr = ptr;
+  op.rows = rows;
+  op.cols = 16;
+  op.box_rows = box_rows;
+}
+void make_operand_s2d_a(Operand& op, const void* ptr, int rows, int box_rows) {
+  make_operand_k16(op, ptr, rows, box_rows);
+}
+void make_operand_s2d_b(Operand& op, const void* ptr, int rows) {
+  make_operand_k16(op, ptr, rows, 256);
+}
+
 // [rows, ld] bf16 map with a 32-column box and the 64B swizzle (64-byte box
 // rows): the residual ring (128-row box) and the output stage (32-row box).
 static void map64(CUtensorMap& m, const void* p, int ld, int rows, int box_rows) {
@@ -1419,7 +1519,18 @@ static void map128_res(CUtensorMap& m, const void* p, int ld, int rows) {
 }
 
 void prepare_conv_gemm(PreparedGemm& p, const ConvGemmGroup& g, const ConvGemmArgs& a, int BN) {
-  if (a.Kc % 64 || a.ntaps < 1 || a.ntaps > 9) throw InvalidArgument("conv_gemm: bad K");
+  if (a.s2d) {
+    if (BN != 64 || a.N != 64 || a.Kc != 16 || a.ntaps != 16 || a.halo_lo || a.pair ||
+        (a.row_mode != kRowGridToCompact && a.row_mode != kRowIdentity) || a.out_f32 ||
+        a.gw < 4 || a.gh < 4)
+      throw InvalidArgument("conv_gemm: s2d stem is 64 outputs, 16 taps of K = 16, grid rows");
+    for (int r = 0; r < g.n; r++)
+      if (g.A[r]->box_rows != BM + a.gw + 3 || BM + a.gw + 3 > 256 || g.B[r]->box_rows != 256 ||
+          g.residual[r])
+        throw InvalidArgument("conv_gemm: s2d stem operand mismatch");
+  } else if (a.Kc % 64 || a.ntaps < 1 || a.ntaps > 9) {
+    throw InvalidArgument("conv_gemm: bad K");
+  }
   if (!a.out_f32 && (a.N % 32)) throw InvalidArgument("conv_gemm: bf16 out needs N%32==0");
   if (a.out_f32 && (a.N % 8)) throw InvalidArgument("conv_gemm: f32 out needs N%8==0");
   if (g.n < 1 || g.n > kMaxGroup) throw InvalidArgument("conv_gemm: group size 1..4");
@@ -1433,7 +1544,8 @@ void prepare_conv_gemm(PreparedGemm& p, const ConvGemmGroup& g, const ConvGemmAr
     if (a.tap_off[t] < -a.halo_lo || a.tap_off[t] > a.halo_lo)
       throw InvalidArgument("conv_gemm: tap outside the halo");
   for (int r = 0; r < g.n; r++) {
-    if (g.A[r]->box_rows != BM + 2 * a.halo_lo || g.B[r]->box_rows != (a.pair ? BN / 2 : BN))
+    if (!a.s2d &&
+        (g.A[r]->box_rows != BM + 2 * a.halo_lo || g.B[r]->box_rows != (a.pair ? BN / 2 : BN)))
       throw InvalidArgument("conv_gemm: box mismatch");
     if ((g.residual[r] != nullptr) != (g.residual[0] != nullptr))
       throw InvalidArgument("conv_gemm: residual on some replicas only");
@@ -1462,6 +1574,10 @@ void prepare_conv_gemm(PreparedGemm& p, const ConvGemmGroup& g, const ConvGemmAr
 }
 
 void launch_prepared(const PreparedGemm& p, cudaStream_t st, int max_ctas) {
+  if (p.args.s2d) {  // 12 dy-pair boxes (6 tiles) in flight, 16 taps' weights resident
+    launch_t<64, 1, 0, 12, 4, 0, 1>(p, st, max_ctas);
+    return;
+  }
   if (p.args.pair) {
     if (p.args.halo_lo > 0) {
       if (p.BN != 128 || p.res)

@@ -30,6 +30,8 @@ enum RowMode : int {
   kRowCompactToPhasePad = 4,  // m compact (H x W) -> phase-split padded grid
   kRowPhaseGridToCompact = 5, // m on an (H+1) x (W+1) plane-00 grid -> compact
                               // H x W (H, W = output dims)
+  kRowGridToCompact = 6,      // m on a per-image gh x gw grid -> compact H x W
+                              // (rows with i >= H or j >= W are not stored)
 };
 
 struct ConvGemmArgs {
@@ -61,6 +63,14 @@ struct ConvGemmArgs {
   // CTAs cancel pending ones and take their units).
   int sched;
   int tile_unit;
+  // Space-to-depth stem (s2d = 1): the 7x7/2 conv1 as a 4x4 stride-1 conv
+  // over the 2x2 space-to-depth image (12 channels padded to 16: 32-byte
+  // rows, 32B swizzle): per tile 2 row boxes (dy pairs) of BM + gw + 3 <=
+  // 256 rows, 16 taps (dy, dx) of one K = 16 MMA each at row shift
+  // dy * gw + dx, the 16 taps' weights resident ([tap][N][16]).
+  // Rows live on a per-image gh x gw grid (row_mode kRowGridToCompact).
+  int s2d;
+  int gh, gw;
 };
 
 // One encoded operand (tensor map over a row-major bf16 [rows, cols] matrix
@@ -72,6 +82,10 @@ struct Operand {
 };
 
 void make_operand(Operand& op, const void* ptr, int rows, int cols, int box_rows);
+// s2d stem operands: A = [rows, 16] bf16 image, box 16 x box_rows; B =
+// [16 * N, 16] bf16 weights in [tap][N][16] order, box 16 x 256; 32B swizzle.
+void make_operand_s2d_a(Operand& op, const void* ptr, int rows, int box_rows);
+void make_operand_s2d_b(Operand& op, const void* ptr, int rows);
 
 // One launch over up to kMaxGroup replicas: the same GEMM shape on each
 // replica's own activations/weights (tiles are replica-major), so small

@@ -1,5 +1,5 @@
 """Summarise an ncu --metrics gpu__time_duration.sum CSV: the last forward
-(from the last conv1_im2col launch) with per-launch times. Dev tool."""
+(from the last conv1 operand launch: chw_to_s2d16 / conv1_im2col) with per-launch times. Dev tool."""
 import collections
 import csv
 import sys
@@ -12,8 +12,9 @@ for r in rows:
         continue
     if hdr and len(r) == len(hdr):
         data.append(dict(zip(hdr, r)))
-start = sys.argv[2] if len(sys.argv) > 2 and not sys.argv[2].startswith("-") else "conv1_im2col"
-idx = [i for i, d in enumerate(data) if start in d["Kernel Name"]]
+start = sys.argv[2] if len(sys.argv) > 2 and not sys.argv[2].startswith("-") else None
+starts = [start] if start else ["chw_to_s2d16", "conv1_im2col"]
+idx = [i for i, d in enumerate(data) if any(x in d["Kernel Name"] for x in starts)]
 # -p: the last COMPLETE forward (between the last two starts) when the
 # capture ends mid-step
 seg = (data[idx[-2]:idx[-1]] if "-p" in sys.argv and len(idx) > 1

@@ -61,7 +61,8 @@ def main():
     rows = list(csv.reader(open(path)))
     hdr = next(r for r in rows if "Kernel Name" in r)
     data = [dict(zip(hdr, r)) for r in rows if len(r) == len(hdr) and r != hdr]
-    idx = [i for i, d in enumerate(data) if "conv1_im2col" in d["Kernel Name"]]
+    idx = [i for i, d in enumerate(data)
+           if "conv1_im2col" in d["Kernel Name"] or "chw_to_s2d16" in d["Kernel Name"]]
     seg = [d for d in data[idx[-1] + 1:]]
     P = plan(B)
     if len(seg) != len(P):

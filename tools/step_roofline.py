@@ -22,7 +22,8 @@ def plan(B, R, S=224):
     L = []
     px = lambda h: B * h * h  # noqa: E731
     H1, H = S // 2, S // 4
-    L.append(("conv1 7x7/2", 2 * px(H1) * 64 * 147 * R, px(H1) * 192 * 2 + R * px(H1) * 64 * 2))
+    G = (S + 6) // 2  # s2d stem: 2 planes x 16 B per grid pixel
+    L.append(("conv1 7x7/2", 2 * px(H1) * 64 * 147 * R, B * G * G * 32 + R * px(H1) * 64 * 2))
     cin = 64
     for stage, (w, n) in enumerate(((64, 3), (128, 4), (256, 6), (512, 3))):
         for i in range(n):
@@ -62,7 +63,7 @@ def main():
     seq = list(per.values())
     gem = None
     for i in range(len(seq) - 1, -1, -1):
-        if "conv1_im2col" in seq[i]["name"]:
+        if "conv1_im2col" in seq[i]["name"] or "chw_to_s2d16" in seq[i]["name"]:
             g = [d for d in seq[i + 1:] if "conv_gemm" in d["name"]][:len(P)]
             if len(g) == len(P):
                 gem = g
