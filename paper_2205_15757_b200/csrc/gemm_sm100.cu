@@ -191,18 +191,12 @@ __device__ __forceinline__ void umma_bf16(uint32_t d, uint64_t a, uint64_t b,
 }
 // Warp-collective forms: every lane of the warp executes them, one lane
 // (elect.sync) issues the tcgen05 instruction.
-__device__ __forceinline__ void umma_bf16_w(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
-                                            uint32_t accum) {
-  asm volatile(
-      "{\n\t.reg .pred p, e;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "elect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d),
-      "l"(a), "l"(b), "r"(idesc), "r"(accum));
-}
 // Four MMAs under one elect: descriptors a + 2j, b + bstep * j (j = 0..3),
-// the first accumulating when accum != 0, the rest always (the s2d stem's
-// 4 dx taps of one dy box: +32 B rows of A, +2 KB tap tiles of B).
+// the first accumulating when accum != 0, the rest always. One elect and
+// one set of uniform-register moves per 4 MMAs instead of per MMA (the MMA
+// warp's issue overhead bounds the N = 64 layers): a k-block's 4 K = 16
+// slices (bstep 2) or the s2d stem's 4 dx taps (+32 B rows of A, +2 KB tap
+// tiles of B).
 template <int BSTEP>
 __device__ __forceinline__ void umma_bf16_x4_w(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
                                                uint32_t accum) {
@@ -218,6 +212,7 @@ __device__ __forceinline__ void umma_bf16_x4_w(uint32_t d, uint64_t a, uint64_t 
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b3, %3, 1;\n}" ::"r"(d),
       "l"(a), "l"(b), "r"(idesc), "r"(accum), "n"(BSTEP), "n"(2 * BSTEP), "n"(3 * BSTEP));
 }
+
 __device__ __forceinline__ void umma_commit_w(uint64_t* b) {
   asm volatile(
       "{\n\t.reg .pred e;\n\t"
@@ -814,9 +809,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               const uint64_t ad = smem_desc_sw128_row(hbase + (uint32_t)(a.tap_off[tap] * 128), 0);
               const uint64_t bd =
                   smem_desc_sw128_row(sB_u + (uint32_t)((tap * kpt + cb) * B_BYTES), 0);
-#pragma unroll
-              for (int k = 0; k < BK / 16; k++)
-                umma_bf16_w(d, ad + 2 * k, bd + 2 * k, idesc, (cb | tap | k) != 0);
+              umma_bf16_x4_w<2>(d, ad, bd, idesc, (cb | tap) != 0);
             }
             umma_commit_w(&hempty[hs]);
             if (++hs == HALO) { hs = 0; hphase ^= 1; }
@@ -888,9 +881,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               tc_fence_after();
               const uint64_t ad = smem_desc_sw128_row(hbase + (uint32_t)(a.tap_off[tap] * 128), 0);
               const uint64_t bd = smem_desc_sw128_row(sB_u + (uint32_t)(stage * B_BYTES), 0);
-#pragma unroll
-              for (int k = 0; k < BK / 16; k++)
-                umma_bf16_w(d, ad + 2 * k, bd + 2 * k, idesc, (cb | tap | k) != 0);
+              umma_bf16_x4_w<2>(d, ad, bd, idesc, (cb | tap) != 0);
               umma_commit_w(&empty[stage]);
               if (++stage == STAGES) { stage = 0; phase ^= 1; }
             }
@@ -909,9 +900,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           // stage offsets added to the 14-bit start-address field (uniform adds)
           const uint64_t ad = ad0 + (uint64_t)((stage * A_BYTES) >> 4);
           const uint64_t bd = bd0 + (uint64_t)((stage * B_BYTES) >> 4);
-#pragma unroll
-          for (int k = 0; k < BK / 16; k++)  // UMMA_K = 16 (32 bytes)
-            umma_bf16_w(d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+          umma_bf16_x4_w<2>(d, ad, bd, idesc, kb != 0);  // 4 x UMMA_K = 16
           umma_commit_w(&empty[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
