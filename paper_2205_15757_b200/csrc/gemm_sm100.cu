@@ -213,6 +213,32 @@ __device__ __forceinline__ void umma_bf16_x4_w(uint32_t d, uint64_t a, uint64_t 
       "l"(a), "l"(b), "r"(idesc), "r"(accum), "n"(BSTEP), "n"(2 * BSTEP), "n"(3 * BSTEP));
 }
 
+// The same 4 taps for two accumulators (d0 with A a0, d1 with A a1, shared
+// B), interleaved so that no MMA waits on the previous one's accumulation:
+// a K = 16, N = 64 MMA is shorter than the accumulate latency, so back-to-
+// back MMAs into one accumulator run at the latency, not the tensor rate.
+template <int BSTEP>
+__device__ __forceinline__ void umma_bf16_x4x2_w(uint32_t d0, uint32_t d1, uint64_t a0,
+                                                 uint64_t a1, uint64_t b, uint32_t idesc,
+                                                 uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t.reg .b64 x1, x2, x3, y1, y2, y3, b1, b2, b3;\n\t"
+      "setp.ne.b32 p, %6, 0;\n\t"
+      "add.s64 x1, %2, 2;\n\tadd.s64 x2, %2, 4;\n\tadd.s64 x3, %2, 6;\n\t"
+      "add.s64 y1, %3, 2;\n\tadd.s64 y2, %3, 4;\n\tadd.s64 y3, %3, 6;\n\t"
+      "add.s64 b1, %4, %7;\n\tadd.s64 b2, %4, %8;\n\tadd.s64 b3, %4, %9;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %2, %4, %5, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], %3, %4, %5, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], x1, b1, %5, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], y1, b1, %5, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], x2, b2, %5, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], y2, b2, %5, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], x3, b3, %5, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], y3, b3, %5, 1;\n}" ::"r"(d0),
+      "r"(d1), "l"(a0), "l"(a1), "l"(b), "r"(idesc), "r"(accum), "n"(BSTEP), "n"(2 * BSTEP),
+      "n"(3 * BSTEP));
+}
 __device__ __forceinline__ void umma_commit_w(uint64_t* b) {
   asm volatile(
       "{\n\t.reg .pred e;\n\t"
@@ -491,11 +517,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   // s2d stem: a ring slot holds one dy box (2 planes x (BM + 3) rows x 16 B)
   constexpr int kHaloSlot = S2D ? kS2DSlot : kHaloBytes;
   constexpr int B_BYTES = (PAIR ? BN / 2 : BN) * BK * 2;  // this CTA's weight tile
-  constexpr uint32_t TMEM_COLS = 2 * BN;
+  // s2d stem: 256-row tiles of two 128-row sub-tiles (2 accumulators each)
+  constexpr int kSubTiles = S2D ? 2 : 1;
+  constexpr uint32_t TMEM_COLS = 2 * BN * kSubTiles;
   // BN = 64 (2 chunks of 32 columns): the two epilogue warp groups take
   // alternate tiles whole; wider tiles split their chunks between the groups.
   // An accumulator is released (tempty) by exactly the warps that drained it.
-  constexpr bool kTileSplit = BN == 64;
+  constexpr bool kTileSplit = BN == 64 && !S2D;  // s2d: group h drains sub-tile h
   constexpr int kDrainWarps = kTileSplit ? kEpiWarps / 2 : kEpiWarps;
   // residual ring: 128-row boxes of kResCols columns (64: 128-byte rows, SW128;
   // half the TMA row requests of 32-column SW64 boxes) in kResSlots x 8 KB
@@ -536,7 +564,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // of the batch) is read from HBM once and from L2 by the other replicas
   // pair: a tile is 256 rows (this CTA's 128-row half at crank * 128)
   const uint32_t crank = PAIR ? cluster_rank() : 0;
-  constexpr int BMT = PAIR ? 2 * BM : BM;
+  constexpr int BMT = (PAIR || S2D) ? 2 * BM : BM;
   const int num_mt = (a.M + BMT - 1) / BMT;
   const int tiles = num_mt * num_n * gp.n;
   const int first_unit = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
@@ -661,13 +689,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             wr = r;
             wl++;
           }
-          if constexpr (S2D) {  // one box per dy pair: BM + gw + 3 rows of 16 channels
-            for (int h = 0; h < 2; h++) {
-              mbar_wait(&hempty[hs], hphase ^ 1);
-              mbar_expect_tx(&hfull[hs], (BM + a.gw + 3) * 32);
-              tma_load_2d(&gp.A[r], &hfull[hs], sA + hs * kHaloSlot, 0, m0 + 2 * h * a.gw);
-              if (++hs == HALO) { hs = 0; hphase ^= 1; }
-            }
+          if constexpr (S2D) {  // per dy pair, one box per sub-tile: BM + gw + 3 rows
+            for (int h = 0; h < 2; h++)
+              for (int sub = 0; sub < kSubTiles; sub++) {
+                mbar_wait(&hempty[hs], hphase ^ 1);
+                mbar_expect_tx(&hfull[hs], (BM + a.gw + 3) * 32);
+                tma_load_2d(&gp.A[r], &hfull[hs], sA + hs * kHaloSlot, 0,
+                            m0 + sub * BM + 2 * h * a.gw);
+                if (++hs == HALO) { hs = 0; hphase ^= 1; }
+              }
             continue;
           }
           const int hrows = BM + 2 * a.halo_lo;
@@ -762,7 +792,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         CG_TRACE(2, ti);
         tc_fence_after();
-        const uint32_t d = tmem + acc * BN;
+        const uint32_t d = tmem + acc * BN * kSubTiles;
         if constexpr (RESB > 0) {
           int r_, m0_, n0_;
           coords(sched.t, r_, m0_, n0_);
@@ -776,20 +806,28 @@ __global__ void __launch_bounds__(kThreads, 1)
           if constexpr (S2D) {
             // 16 taps (dy, dx): A = the dy box from row dx, B = the tap's [64][16]
             const uint32_t sA_u = su32(sA), sB_u = su32(sB);
+            // per dy pair: both sub-tiles' boxes (ring slots hs, hs + 1), the
+            // two accumulators' MMAs interleaved
+            static_assert(kSubTiles == 2 && HALO % 2 == 0, "s2d: sub-tile box pairs");
             for (int h = 0; h < 2; h++) {
               mbar_wait(&hfull[hs], hphase);
+              mbar_wait(&hfull[hs + 1], hphase);
               if (h == 0) CG_TRACE(3, ti);
               tc_fence_after();
-              const uint32_t hbase = sA_u + (uint32_t)(hs * kHaloSlot);
+              const uint32_t hb0 = sA_u + (uint32_t)(hs * kHaloSlot), hb1 = hb0 + kHaloSlot;
 #pragma unroll
-              for (int j = 0; j < 2; j++) {  // dy = 2h + j: rows j * gw on of the box
+              for (int j = 0; j < 2; j++) {  // dy = 2h + j: rows j * gw on of each box
                 const int dy = 2 * h + j;
-                umma_bf16_x4_w<2048 / 16>(
-                    d, smem_desc_sw32_row(hbase + (uint32_t)(j * a.gw * 32)),
-                    smem_desc_sw32_row(sB_u + (uint32_t)(dy * 4 * 2048)), idesc, dy != 0);
+                const uint32_t ro = (uint32_t)(j * a.gw * 32);
+                umma_bf16_x4x2_w<2048 / 16>(d, d + BN, smem_desc_sw32_row(hb0 + ro),
+                                            smem_desc_sw32_row(hb1 + ro),
+                                            smem_desc_sw32_row(sB_u + (uint32_t)(dy * 4 * 2048)),
+                                            idesc, dy != 0);
               }
               umma_commit_w(&hempty[hs]);
-              if (++hs == HALO) { hs = 0; hphase ^= 1; }
+              umma_commit_w(&hempty[hs + 1]);
+              hs += 2;
+              if (hs == HALO) { hs = 0; hphase ^= 1; }
             }
             umma_commit_w(&tfull[acc]);
             CG_TRACE(4, ti);
@@ -939,7 +977,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     // BN = 64 (2 chunks): the two warp groups take alternate tiles whole
     // (both TMEM accumulators drained concurrently) instead of one chunk
     // each of the same tile; wider tiles split chunks between the groups.
-    constexpr int C0S = kTileSplit ? 1 : 2;  // chunk stride of one warp
+    // s2d stem (256-row tiles): group h drains sub-tile h, both chunks.
+    constexpr int C0S = (kTileSplit || S2D) ? 1 : 2;  // chunk stride of one warp
     int tile_i = 0, acc = 0;
     int stage_seq = 0;  // staging buffer sequence across all of this warp's chunks
     uint32_t acc_phase = 0;
@@ -954,9 +993,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         continue;
       }
-      const int c_first = kTileSplit ? 0 : h;
+      const int c_first = (kTileSplit || S2D) ? 0 : h;
       int r_, m0, n0;
       coords(t, r_, m0, n0);
+      if (S2D) m0 += h * BM;  // this group's sub-tile
       const float* bias_r = gp.bias[r_];
       const __nv_bfloat16* res_r = gp.residual[r_];
       void* out_r = gp.out[r_];
@@ -968,7 +1008,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       // TMEM reads are software-pipelined: chunk c+2's tcgen05.ld is in flight
       // while chunk c is biased, stored and written out.
-      const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16) + acc * BN;
+      const uint32_t trow =
+          tmem + ((uint32_t)(q * 32) << 16) + acc * BN * kSubTiles + (S2D ? h * BN : 0);
       uint32_t v[32];
       if (c_first < CPT) tmem_ld32_issue(trow + c_first * 32, v);
 #pragma unroll 1
@@ -1226,7 +1267,8 @@ void launch_t(const PreparedGemm& p, cudaStream_t st, int max_ctas) {
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   });
   ConvGemmArgs a = p.args;
-  const int tiles = ((a.M + BM - 1) / BM) * ((a.N + BN - 1) / BN) * p.gp.n;
+  constexpr int kTileRows = S2D ? 2 * BM : BM;  // the s2d stem's 256-row tiles
+  const int tiles = ((a.M + kTileRows - 1) / kTileRows) * ((a.N + BN - 1) / BN) * p.gp.n;
   int grid;
   if (!PAIR && g_clc && max_ctas <= 0) {
     a.sched = 1;
