@@ -1333,9 +1333,11 @@ __global__ void __launch_bounds__(128, 1) mma_rate_kernel(int iters, int two_acc
                                                           long long* cycles) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (su32(smem_raw) & 1023)) & 1023);
+  // two_acc 3 / 4: rotate over nbuf distinct A and B tiles (1 / 2 accumulators)
+  const int nbuf = two_acc >= 3 ? (N == 64 ? 8 : 4) : 1;
   uint8_t* sA = smem;
-  uint8_t* sB = smem + A_BYTES;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sB + N * BK * 2);
+  uint8_t* sB = smem + nbuf * A_BYTES;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sB + nbuf * N * BK * 2);
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -1357,9 +1359,13 @@ __global__ void __launch_bounds__(128, 1) mma_rate_kernel(int iters, int two_acc
     const uint64_t ad = smem_desc_sw128(sA), bd = smem_desc_sw128(sB);
     long long t0 = clock64();
     for (int i = 0; i < iters; i++) {
-      const uint32_t d = tmem + ((two_acc && (i & 1)) ? 256u : 0u);
+      const bool alt = (two_acc == 1 || two_acc == 4) && (i & 1);
+      const uint32_t d = tmem + (alt ? 256u : 0u);
+      const int bi = (i >> (two_acc == 4 ? 1 : 0)) % nbuf;
+      const uint64_t a_i = ad + (uint64_t)((bi * A_BYTES) >> 4);
+      const uint64_t b_i = bd + (uint64_t)((bi * N * BK * 2) >> 4);
 #pragma unroll
-      for (int k = 0; k < 4; k++) umma_bf16(d, ad + 2 * k, bd + 2 * k, idesc, (i | k) != 0);
+      for (int k = 0; k < 4; k++) umma_bf16(d, a_i + 2 * k, b_i + 2 * k, idesc, (i | k) != 0);
     }
     umma_commit(bar);
     mbar_wait(bar, 0);
@@ -1459,7 +1465,9 @@ double mma_rate_bench(int N, int iters, int ctas, int two_acc, cudaStream_t st) 
   if (two_acc == 2) return mma_rate_pair_bench(N, iters, ctas, st);
   long long* d = nullptr;
   CG_CUDA(cudaMalloc(&d, 8));
-  const int smem = 1024 + A_BYTES + N * BK * 2 + 64;
+  const int nbuf = two_acc >= 3 ? (N == 64 ? 8 : 4) : 1;
+  if (N == 256 && nbuf > 1) throw InvalidArgument("mma_rate: rotating buffers for N <= 128");
+  const int smem = 1024 + nbuf * (A_BYTES + N * BK * 2) + 64;
   auto run = [&](auto kern) {
     CG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     kern<<<ctas, 128, smem, st>>>(iters, two_acc, d);
