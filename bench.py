@@ -414,7 +414,7 @@ def bench_gpu(args, rank, world, local_rank):
     traffic, traffic_src = None, None
     if args.workload == "c2" and not replica:
         try:  # DRAM bytes of one step's GEMM launches, from the committed ncu capture
-            with open(os.path.join(ROOT, "profiles", "r01_gemm_step_traffic.json")) as f:
+            with open(os.path.join(ROOT, "profiles", "r02_gemm_step_traffic.json")) as f:
                 tj = json.load(f)
             traffic, traffic_src = tj["traffic_bytes_per_step"], tj["source"]
         except Exception:
