@@ -860,41 +860,91 @@ __global__ void maxpool2x2_kernel(const bf16* __restrict__ in, int B, int H, int
 
 // Depthwise 3x3 (pad 1, stride 1/2) + folded-BN bias + ReLU6, NHWC bf16,
 // f32 weights [9][C] tap-major; thread = (output pixel, 8 channels).
-__global__ void dw3x3_kernel(const bf16* __restrict__ in, int B, int H, int C, int stride,
-                             const float* __restrict__ w, const float* __restrict__ bias,
-                             bf16* __restrict__ out) {
-  const int Ho = (H - 1) / stride + 1, chunks = C / 8;
+// Depthwise 3x3 (pad 1) + bias + ReLU6 on NHWC bf16. A thread owns 8
+// channels of P horizontally adjacent outputs: each input column is loaded
+// once for all the outputs whose windows cover it, and a kernel row's 3 x 8
+// weights are loaded once for all P outputs (per output: 9 x 16 B input +
+// 9 x 32 B weight loads at P = 1, about a third of that at P = 4). The tap
+// order of every output's FMA chain is unchanged (rows, then columns).
+template <int STRIDE, int P>
+__global__ void __launch_bounds__(256) dw3x3_kernel(const bf16* __restrict__ in, int B, int H,
+                                                    int C, const float* __restrict__ w,
+                                                    const float* __restrict__ bias,
+                                                    bf16* __restrict__ out) {
+  const int Ho = (H - 1) / STRIDE + 1, chunks = C / 8, Wg = (Ho + P - 1) / P;
   const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const size_t pix = t / chunks;
-  const int ch = (int)(t - pix * chunks);
-  if (pix >= (size_t)B * Ho * Ho) return;
-  const int n = (int)(pix / (Ho * Ho)), rem = (int)(pix - (size_t)n * Ho * Ho);
-  const int ho = rem / Ho, wo = rem - ho * Ho;
+  const size_t grp = t / chunks;
+  const int ch = (int)(t - grp * chunks);
+  if (grp >= (size_t)B * Ho * Wg) return;
+  const int n = (int)(grp / ((size_t)Ho * Wg)), rem = (int)(grp - (size_t)n * Ho * Wg);
+  const int ho = rem / Wg, wo0 = (rem - ho * Wg) * P;
   const int c0 = ch * 8;
-  float acc[8];
+  float acc[P][8];
   {
     const float4 b0 = __ldg(reinterpret_cast<const float4*>(bias + c0));
     const float4 b1 = __ldg(reinterpret_cast<const float4*>(bias + c0 + 4));
-    acc[0] = b0.x; acc[1] = b0.y; acc[2] = b0.z; acc[3] = b0.w;
-    acc[4] = b1.x; acc[5] = b1.y; acc[6] = b1.z; acc[7] = b1.w;
+    const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+    for (int p = 0; p < P; p++)
+#pragma unroll
+      for (int j = 0; j < 8; j++) acc[p][j] = bv[j];
+  }
+  constexpr int NCOL = (P - 1) * STRIDE + 3;  // input columns covering the P windows
+  const int x0 = wo0 * STRIDE - 1;
+#pragma unroll
+  for (int dr = 0; dr < 3; dr++) {
+    const int h = ho * STRIDE - 1 + dr;
+    if (h < 0 || h >= H) continue;
+    float wr[3][8];
+#pragma unroll
+    for (int ds = 0; ds < 3; ds++) {
+      const float4 w0 = __ldg(reinterpret_cast<const float4*>(w + (dr * 3 + ds) * C + c0));
+      const float4 w1 = __ldg(reinterpret_cast<const float4*>(w + (dr * 3 + ds) * C + c0 + 4));
+      wr[ds][0] = w0.x; wr[ds][1] = w0.y; wr[ds][2] = w0.z; wr[ds][3] = w0.w;
+      wr[ds][4] = w1.x; wr[ds][5] = w1.y; wr[ds][6] = w1.z; wr[ds][7] = w1.w;
+    }
+    const bf16* row = in + ((size_t)n * H + h) * H * C + c0;
+#pragma unroll
+    for (int col = 0; col < NCOL; col++) {
+      const int x = x0 + col;
+      if (x < 0 || x >= H) continue;
+      const uint4 q = __ldg(reinterpret_cast<const uint4*>(row + (size_t)x * C));
+      const bf16* e = reinterpret_cast<const bf16*>(&q);
+      float v[8];
+#pragma unroll
+      for (int j = 0; j < 8; j++) v[j] = __bfloat162float(e[j]);
+#pragma unroll
+      for (int p = 0; p < P; p++) {
+        const int ds = col - p * STRIDE;  // this column's tap in output p's window
+        if (ds < 0 || ds > 2) continue;
+#pragma unroll
+        for (int j = 0; j < 8; j++) acc[p][j] = fmaf(v[j], wr[ds][j], acc[p][j]);
+      }
+    }
   }
 #pragma unroll
-  for (int tap = 0; tap < 9; tap++) {
-    const int h = ho * stride - 1 + tap / 3, x = wo * stride - 1 + tap % 3;
-    if (h < 0 || h >= H || x < 0 || x >= H) continue;
-    const uint4 q =
-        __ldg(reinterpret_cast<const uint4*>(in + (((size_t)n * H + h) * H + x) * C + c0));
-    const bf16* e = reinterpret_cast<const bf16*>(&q);
-    const float4 w0 = __ldg(reinterpret_cast<const float4*>(w + tap * C + c0));
-    const float4 w1 = __ldg(reinterpret_cast<const float4*>(w + tap * C + c0 + 4));
-    const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+  for (int p = 0; p < P; p++) {
+    if (wo0 + p >= Ho) break;
+    __align__(16) bf16 o[8];
 #pragma unroll
-    for (int j = 0; j < 8; j++) acc[j] = fmaf(__bfloat162float(e[j]), wv[j], acc[j]);
+    for (int j = 0; j < 8; j++) o[j] = __float2bfloat16(fminf(fmaxf(acc[p][j], 0.f), 6.f));
+    *reinterpret_cast<uint4*>(out + (((size_t)n * Ho + ho) * Ho + wo0 + p) * C + c0) =
+        *reinterpret_cast<uint4*>(o);
   }
-  __align__(16) bf16 o[8];
-#pragma unroll
-  for (int j = 0; j < 8; j++) o[j] = __float2bfloat16(fminf(fmaxf(acc[j], 0.f), 6.f));
-  *reinterpret_cast<uint4*>(out + pix * C + c0) = *reinterpret_cast<uint4*>(o);
+}
+// outputs per thread (A/B: CREDO_DW_P = 1, 2 or 4)
+const int kDwP = std::getenv("CREDO_DW_P") ? std::atoi(std::getenv("CREDO_DW_P")) : 4;
+template <int STRIDE>
+void launch_dw3x3(const bf16* in, int B, int H, int C, const float* w, const float* b, bf16* out,
+                  cudaStream_t st) {
+  const int Ho = (H - 1) / STRIDE + 1;
+  auto go = [&](auto kern, int P) {
+    const size_t th = (size_t)B * Ho * ((Ho + P - 1) / P) * (C / 8);
+    kern<<<grid_for(th), 256, 0, st>>>(in, B, H, C, w, b, out);
+  };
+  if (kDwP == 1) go(dw3x3_kernel<STRIDE, 1>, 1);
+  else if (kDwP == 4) go(dw3x3_kernel<STRIDE, 4>, 4);
+  else go(dw3x3_kernel<STRIDE, 2>, 2);
 }
 
 int pad64(int c) { return (c + 63) / 64 * 64; }
@@ -1371,9 +1421,9 @@ class MobileNetV2 final : public SeqNet {
         const DwW* dw = &k.dw;
         bf16* D = d_;
         const int H = k.H, C = k.hidden, s = k.dw.stride, Ho = k.Ho;
-        push_aux(L, [dwin, dw, D, b, H, C, s, Ho](cudaStream_t st) {
-          size_t th = (size_t)b * Ho * Ho * (C / 8);
-          dw3x3_kernel<<<grid_for(th), 256, 0, st>>>(dwin, b, H, C, s, dw->w, dw->b, D);
+        push_aux(L, [dwin, dw, D, b, H, C, s](cudaStream_t st) {
+          if (s == 1) launch_dw3x3<1>(dwin, b, H, C, dw->w, dw->b, D, st);
+          else launch_dw3x3<2>(dwin, b, H, C, dw->w, dw->b, D, st);
           CG_CHECK_LAUNCH();
         });
       }
