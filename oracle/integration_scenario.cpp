@@ -16,8 +16,20 @@
 // certified, check_invariants() empty, and the two rendered traces
 // byte-identical (the fp64 GPU path is bit-exact, so every digest, vote and
 // certificate in the run is the same).
+//
+// Then the reference's own strategy benchmark (bench_strategies,
+// src/experiments.cpp:60-80: execute-then-agree vs agree-then-execute over
+// the same workload) with the GPU executor, under three device-time models
+// for a batch (ExecCost, include/credo/engine.hpp:38-45): the reference's
+// default, the measured wall time of CudaExecutor::run on the harness's
+// LinearToyModel, and (argv[1], argv[2] = fixed_us, per_item_us) the
+// measured device time of one ResNet-50 replica's forward on the B200.
+#include <chrono>
 #include <cstdio>
+#include <cstdlib>
 #include <memory>
+#include <optional>
+#include <random>
 #include <string>
 
 #include "credo/harness.hpp"
@@ -49,7 +61,39 @@ std::vector<std::vector<double>> ToyExecutor::run(const LinearToyModel& model,
 using namespace credo;
 using namespace credo::harness;
 
-int main() {
+// ExecCost of CudaExecutor::run on the harness's default model shape
+// (WorkloadSpec defaults): wall time per call, H2D + kernel + D2H + sync,
+// fitted as fixed + per_item * n over batches of 1 and 4 requests.
+static ExecCost measure_linear_cost() {
+  WorkloadSpec w;
+  auto gen = generate_group("bench", w, 0);
+  const LinearToyModel model = LinearToyModel::from_file_bytes(
+      ByteView(gen.model_files.begin()->second.data(), gen.model_files.begin()->second.size()));
+  std::mt19937_64 rng(3);
+  std::uniform_real_distribution<double> uni(-1.0, 1.0);
+  auto batch = [&](size_t n) {
+    std::vector<std::vector<double>> xs(n, std::vector<double>(model.input_dim));
+    for (auto& x : xs)
+      for (double& v : x) v = uni(rng);
+    return xs;
+  };
+  auto time_us = [&](size_t n) {
+    auto xs = batch(n);
+    for (int i = 0; i < 20; i++) g_exec->run(model, xs);  // warm: residency, plans
+    const int reps = 200;
+    auto t0 = std::chrono::steady_clock::now();
+    for (int i = 0; i < reps; i++) g_exec->run(model, xs);
+    return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0)
+               .count() / reps;
+  };
+  const double t1 = time_us(1), t4 = time_us(4);
+  ExecCost c;
+  c.per_item_us = (uint64_t)std::llround(std::max(0.0, (t4 - t1) / 3.0));
+  c.fixed_us = (uint64_t)std::llround(std::max(1.0, t1 - (double)c.per_item_us));
+  return c;
+}
+
+int main(int argc, char** argv) {
   g_ctx = std::make_unique<gpu::Context>(0);
   g_exec = std::make_unique<gpu::CudaExecutor>(*g_ctx);
   auto small_spec = [] {  // tests/test_harness.cpp:19-28
@@ -111,6 +155,37 @@ int main() {
                 ok ? "ok" : "FAIL");
     for (auto& v : violations) std::printf("  violation: %s\n", v.c_str());
     if (!ok) failures++;
+  }
+  // the reference's strategy benchmark with real device-time models
+  {
+    struct Model {
+      const char* name;
+      std::optional<ExecCost> cost;
+    };
+    std::vector<Model> models{{"reference default ExecCost", std::nullopt},
+                              {"B200 LinearToyModel (measured)", measure_linear_cost()}};
+    if (argc > 2) {
+      ExecCost rn;
+      rn.fixed_us = std::strtoull(argv[1], nullptr, 10);
+      rn.per_item_us = std::strtoull(argv[2], nullptr, 10);
+      models.push_back({"B200 ResNet-50 replica (measured)", rn});
+    }
+    g_gpu = true;
+    for (uint64_t gap : {1000ull, 100ull})  // BenchSpec default arrival gap, and 10x the rate
+      for (const auto& m : models) {
+        BenchSpec bs;
+        bs.exec_cost = m.cost;
+        bs.arrival_gap_us = gap;
+        const ExecCost c = m.cost.value_or(ExecCost{});
+        BenchReport rep = bench_strategies(bs);
+        std::printf("strategies [%s: %lu + %lu*n us, arrival gap %lu us]: execute-agree-attest "
+                    "%.1f req/s, agree-execute %.1f req/s (%lu requests, all certified %d)\n",
+                    m.name, (unsigned long)c.fixed_us, (unsigned long)c.per_item_us,
+                    (unsigned long)gap, rep.execute_agree_attest_tps, rep.agree_execute_tps,
+                    (unsigned long)rep.n_requests, (int)rep.all_certified);
+        if (!rep.all_certified) failures++;
+      }
+    g_gpu = false;
   }
   std::printf("integration_scenario: %zu scenarios, %lu GPU executor calls (%lu inputs), "
               "%d failures\n",

@@ -61,13 +61,35 @@ def test_run_scenario_with_gpu_executor():
     certified, check_invariants() empty, and the rendered trace byte-identical
     to the stock CPU run -- for the honest, agree_then_execute, corrupt-beyond
     and corrupt-within-epsilon scenarios of tests/test_harness.cpp and a
-    C1-shaped (3072 -> 10) workload."""
+    C1-shaped (3072 -> 10) workload. Then the reference's strategy benchmark
+    (bench_strategies, experiments.cpp:60-80) with the GPU executor under the
+    default, the measured LinearToyModel and the measured ResNet-50 batch
+    cost: every request certified under both strategies."""
     if not os.path.exists(SCENARIO):
         pytest.skip("oracle/_ref/integration_scenario not built (needs /root/reference at build time)")
-    out = subprocess.run([SCENARIO], capture_output=True, text=True, timeout=900)
+    # device time of one ResNet-50 replica's forward at batch 1 and 4 (the
+    # harness's exec_batch_max) -> the ExecCost the strategy benchmark uses
+    import ctypes as C
+    from paper_2205_15757_b200 import Context, Model
+    from paper_2205_15757_b200.workload import resnet_group
+    ctx = Context(0)
+    files, digs, _ = resnet_group("resnet50", replicas=1, seed=0)
+    m = Model.load_cnn(ctx, files[0], digs[0])
+    ms = {}
+    for b in (1, 4):
+        v = C.c_double()
+        assert ctx.L.cg_dbg_forward_bench(ctx.h, m.h, b, 20, C.byref(v)) == 0
+        ms[b] = v.value
+    per_item = max(0.0, (ms[4] - ms[1]) / 3.0) * 1e3
+    fixed = max(1.0, ms[1] * 1e3 - per_item)
+    m.free()
+    ctx.close()
+    out = subprocess.run([SCENARIO, str(round(fixed)), str(round(per_item))], capture_output=True,
+                         text=True, timeout=1200)
     print(out.stdout, out.stderr)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "0 failures" in out.stdout
+    assert out.stdout.count("all certified 1") == 6
 
 
 VERIFY = os.path.join(ROOT, "oracle", "_ref", "integration_verify")
