@@ -304,6 +304,25 @@ class Context:
                                               _p(sig), _p(ids), _p(st)))
         return sig, ids, st
 
+    def cert_leaf_hashes(self, batch: "RequestBatch", group_id: bytes, req_index, want,
+                         results):
+        """cg_cert_leaf_hashes: per entry m, leaf_hash of result_leaf (want
+        bit 1), single_attest_leaf (bit 2) of (request req_index[m],
+        results[m] = InferenceResult::encode bytes) or missing_result_leaf
+        (bit 4) -- the leaves verify_cert / assemble_response re-hash.
+        Returns (leaf52, leaf53, leaf4d), each M x 32 (zeros where not wanted)."""
+        cb, keep, B = ModelGroup._cbatch(batch)
+        M = len(req_index)
+        ridx = np.ascontiguousarray(req_index, np.uint32)
+        w = np.ascontiguousarray(want, np.uint8)
+        lens = np.array([len(r) for r in results], np.uint64)
+        enc = np.frombuffer(b"".join(results) or b"\0", np.uint8)
+        out = [np.zeros((M, 32), np.uint8) for _ in range(3)]
+        self._check(self.L.cg_cert_leaf_hashes(
+            self.h, C.byref(cb), group_id, u64(len(group_id)), C.c_uint32(M), _p(ridx), _p(w),
+            _p(enc), _p(lens), _p(out[0]), _p(out[1]), _p(out[2])))
+        return tuple(out)
+
     def select_quorum(self, results: dict, n: int, f: int, metric: int,
                       epsilon: float):
         """distance::select_quorum(map<node, vector<double>>, n, f, m, eps)."""
