@@ -134,7 +134,8 @@ def make_hetero_group(ctx, B, seed=0, eps=C3_EPS):
 def resnet50_gemm_plan(B, R, S=224):
     """(name, FLOPs, compulsory HBM bytes) of each conv GEMM launch of one
     grouped ResNet-50 forward over R replicas, in csrc/cnn.cu ResNet::ops
-    order (conv1, per block c1, c2, [ds], c3, fc); same model as
+    order (conv1, per block c1, c2, c3 -- with the projection shortcut fused
+    into c3 in the first block of each stage -- fc); same model as
     tools/step_roofline.py."""
     L = []
     px = lambda h: B * h * h  # noqa: E731
@@ -150,11 +151,12 @@ def resnet50_gemm_plan(B, R, S=224):
             Ho, cout = H // s, 4 * w
             L.append(("c1", 2 * px(H) * cin * w * R, R * (px(H) * cin * 2 + px(H) * w * 2)))
             L.append(("c2", 2 * px(Ho) * 9 * w * w * R, R * (px(H) * w * 2 + px(Ho) * w * 2)))
-            if i == 0:
-                L.append(("ds", 2 * px(Ho) * cin * cout * R,
-                          R * (px(Ho) * cin * 2 + px(Ho) * cout * 2)))
-            L.append(("c3", 2 * px(Ho) * w * cout * R,
-                      R * (px(Ho) * w * 2 + 2 * px(Ho) * cout * 2)))
+            if i == 0:  # c3 + projection shortcut, one GEMM over K = w + cin
+                L.append(("c3+ds", 2 * px(Ho) * (w + cin) * cout * R,
+                          R * (px(Ho) * (w + cin) * 2 + px(Ho) * cout * 2)))
+            else:
+                L.append(("c3", 2 * px(Ho) * w * cout * R,
+                          R * (px(Ho) * w * 2 + 2 * px(Ho) * cout * 2)))
             H, cin = Ho, cout
     L.append(("fc", 2 * B * cin * 1000 * R, R * (B * cin * 2 + B * 1000 * 4)))
     return L

@@ -280,6 +280,7 @@ struct ConvW {
 
 struct Block {
   ConvW c1, c2, c3, ds;
+  ConvW c3ds;  // has_ds: [W3 | Wds] with b3 + bds, c3 + shortcut as one GEMM
   bool has_ds = false;
   int width = 0, stride = 1, H_in = 0, H_out = 0, cin = 0, cout = 0;
 };
@@ -290,6 +291,9 @@ struct Block {
 int kSmallKMaxBN = 256;  // env CREDO_SMALLK_BN overrides (tuning)
 // ResNet stem: the s2d conv (default) or CREDO_NO_S2D=1, the im2col (K = 192)
 const bool kUseS2D = std::getenv("CREDO_NO_S2D") == nullptr;
+// c3 + projection shortcut as one GEMM over concatenated K (or
+// CREDO_NO_FUSE_DS=1: the shortcut GEMM's output read back as a residual)
+const bool kFuseDs = std::getenv("CREDO_NO_FUSE_DS") == nullptr;
 constexpr int kS2DMaxS = 2 * (256 - 128 - 3) - 6;  // a dy-pair box (128 + Gs + 3 rows) fits 256
 const bool kUseHalo = std::getenv("CREDO_NO_HALO") == nullptr;  // A/B switch for measurements
 
@@ -336,7 +340,10 @@ class ResNet final : public CnnModel {
         fold(b.c2, T, pre + "conv2.weight", pre + "bn2", 3, b.stride, 0);
         fold(b.c3, T, pre + "conv3.weight", pre + "bn3", 1, 1, 0);
         b.has_ds = T.count(pre + "downsample.0.weight") > 0;
-        if (b.has_ds) fold(b.ds, T, pre + "downsample.0.weight", pre + "downsample.1", 1, b.stride, 0);
+        if (b.has_ds) {
+          fold(b.ds, T, pre + "downsample.0.weight", pre + "downsample.1", 1, b.stride, 0);
+          fuse_shortcut(b);
+        }
         if (b.c1.cin != cin || b.c3.cout != b.cout || b.c2.cin != b.width)
           throw std::invalid_argument("cnn file: unexpected block shapes at " + pre);
         double ho2 = (double)b.H_out * b.H_out;
@@ -484,6 +491,8 @@ class ResNet final : public CnnModel {
     int ldout = 0, out_f32 = 0, relu = 0, mode = 0, H = 0, rows_out = 0;
     int halo_lo = 0;  // > 0: 3x3 taps fed from one halo box per channel block
     int s2d = 0, gh = 0, gw = 0;  // the s2d stem (ConvGemmArgs::s2d)
+    const bf16* A2 = nullptr;     // second K segment operand (ConvGemmArgs::kc2)
+    int kc2 = 0;
   };
   struct Op {
     bool gemm = false;
@@ -590,6 +599,26 @@ class ResNet final : public CnnModel {
       }
       // identity / downsample (stride 2: the decimated input X[2h, 2w])
       const bf16* ident = X;
+      if (b.has_ds && kFuseDs) {
+        // c3 + shortcut: K over t2's width channels, then the (decimated) x
+        const bf16* dsin = X;
+        if (b.stride == 2) {
+          bf16* G1 = g1_;
+          const int C = b.cin;
+          aux([X, G1, B, Hi, C](cudaStream_t st) {
+            size_t th = (size_t)B * (Hi / 2) * (Hi / 2) * (C / 8);
+            gather_s2_1x1_kernel<<<grid_for(th), 256, 0, st>>>(X, B, Hi, C, G1);
+            CG_CHECK_LAUNCH();
+          });
+          dsin = G1;
+        }
+        gemm(b.c3ds, t2_, B * Ho * Ho, B * Ho * Ho, b.c3ds.Kc, 1, &zero, nullptr, 0, Y, b.cout,
+             0, 1, kRowIdentity, 0, B * Ho * Ho);
+        L.back().g.A2 = dsin;
+        L.back().g.kc2 = b.ds.Kc;
+        cur ^= 1;
+        continue;
+      }
       if (b.has_ds) {
         const bf16* dsin = X;
         if (b.stride == 2) {
@@ -703,13 +732,44 @@ class ResNet final : public CnnModel {
     c.ntaps = 16;
   }
 
+  // relu(bn3(conv3(t2)) + bn_ds(conv_ds(x))) = relu([t2 | x] [W3 | Wds]^T +
+  // b3 + bds): the bottleneck's last conv and its projection shortcut as
+  // one GEMM whose K runs over t2's channels, then x's (ConvGemmArgs::kc2),
+  // both folded with their BatchNorms; one fp32 accumulation instead of a
+  // bf16 shortcut tensor written and read back.
+  static void fuse_shortcut(Block& b) {
+    const ConvW &c3 = b.c3, &ds = b.ds;
+    if (c3.cout != ds.cout || c3.ntaps != 1 || ds.ntaps != 1)
+      throw std::invalid_argument("cnn file: shortcut does not match conv3");
+    ConvW& f = b.c3ds;
+    f.cin = c3.Kc + ds.Kc;
+    f.cout = c3.cout;
+    f.k = 1;
+    f.stride = 1;
+    f.Kc = c3.Kc;  // first segment; the second (ds.Kc) goes in GemmDesc::kc2
+    f.ntaps = 1;
+    const int K = c3.Kc + ds.Kc;
+    f.hw.assign((size_t)f.cout * K, 0);
+    f.hb.resize(f.cout);
+    for (int o = 0; o < f.cout; o++) {
+      std::copy(c3.hw.begin() + (size_t)o * c3.Kc, c3.hw.begin() + (size_t)(o + 1) * c3.Kc,
+                f.hw.begin() + (size_t)o * K);
+      std::copy(ds.hw.begin() + (size_t)o * ds.Kc, ds.hw.begin() + (size_t)(o + 1) * ds.Kc,
+                f.hw.begin() + (size_t)o * K + c3.Kc);
+      f.hb[o] = c3.hb[o] + ds.hb[o];
+    }
+  }
+
   std::vector<ConvW*> all_convs() {
     std::vector<ConvW*> v{&conv1_, &fc_};
     for (auto& b : blocks_) {
       v.push_back(&b.c1);
       v.push_back(&b.c2);
       v.push_back(&b.c3);
-      if (b.has_ds) v.push_back(&b.ds);
+      if (b.has_ds) {
+        v.push_back(&b.ds);
+        v.push_back(&b.c3ds);
+      }
     }
     return v;
   }
@@ -738,7 +798,7 @@ class ResNet final : public CnnModel {
     int BN = pick_bn(d0.M, d0.c->cout, R);
     if (const char* e = std::getenv("CREDO_SMALLK_BN")) kSmallKMaxBN = std::atoi(e);
     if (d0.Kc * d0.ntaps <= 128 && BN > kSmallKMaxBN) BN = kSmallKMaxBN;
-    std::vector<Operand> A(R), Bm(R);
+    std::vector<Operand> A(R), Bm(R), A2(R);
     ConvGemmGroup g;
     g.n = R;
     if (d0.s2d) BN = 64;
@@ -749,7 +809,11 @@ class ResNet final : public CnnModel {
         make_operand_s2d_b(Bm[r], d.c->w, 16 * d.c->cout);
       } else {
         make_operand(A[r], d.A, d.rowsA, d.Kc, 128 + 2 * d.halo_lo);
-        make_operand(Bm[r], d.c->w, d.c->cout, d.Kc * d.ntaps, BN);
+        make_operand(Bm[r], d.c->w, d.c->cout, d.Kc * d.ntaps + d.kc2, BN);
+        if (d.kc2) {
+          make_operand(A2[r], d.A2, d.rowsA, d.kc2, 128);
+          g.A2[r] = &A2[r];
+        }
       }
       g.A[r] = &A[r];
       g.B[r] = &Bm[r];
@@ -773,6 +837,7 @@ class ResNet final : public CnnModel {
     a.rows_out = d0.rows_out;
     a.halo_lo = d0.halo_lo;
     a.s2d = d0.s2d;
+    a.kc2 = d0.kc2;
     a.gh = d0.gh;
     a.gw = d0.gw;
     auto p = std::make_shared<PreparedGemm>();

@@ -568,7 +568,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int num_mt = (a.M + BMT - 1) / BMT;
   const int tiles = num_mt * num_n * gp.n;
   const int first_unit = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
-  const int kpt = S2D ? 4 : a.Kc / BK, num_k = a.ntaps * kpt;  // s2d: kpt = the 4 dy boxes
+  const int kpt = S2D ? 4 : a.Kc / BK;  // s2d: kpt = the 4 dy boxes
+  const int num_k1 = a.ntaps * kpt, num_k = num_k1 + a.kc2 / BK;  // + second K segment
   (void)num_m;
   auto coords = [&](int t, int& r, int& m0, int& n0) {
     if constexpr (RESB > 0) {
@@ -596,6 +597,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int r = 0; r < gp.n; r++) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(&gp.A[r]) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(&gp.B[r]) : "memory");
+      if (a.kc2) asm volatile("prefetch.tensormap [%0];" ::"l"(&gp.A2[r]) : "memory");
       if (tma_out) asm volatile("prefetch.tensormap [%0];" ::"l"(&gp.O[r]) : "memory");
       if (res_tma) asm volatile("prefetch.tensormap [%0];" ::"l"(&gp.R[r]) : "memory");
     }
@@ -768,8 +770,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&empty[stage], phase ^ 1);
           if (kb == 0) CG_TRACE(1, ti);
           mbar_expect_tx(&full[stage], A_BYTES + B_BYTES);
-          tma_load_2d(&gp.A[r], &full[stage], sA + stage * A_BYTES, cb * BK,
-                      m0 + s_tap[tap]);
+          if (kb < num_k1)
+            tma_load_2d(&gp.A[r], &full[stage], sA + stage * A_BYTES, cb * BK,
+                        m0 + s_tap[tap]);
+          else  // second K segment: the same rows of the A2 operand
+            tma_load_2d(&gp.A2[r], &full[stage], sA + stage * A_BYTES, (kb - num_k1) * BK, m0);
           tma_load_2d(&gp.B[r], &full[stage], sB + stage * B_BYTES, kb * BK, n0);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
@@ -1250,7 +1255,7 @@ const double g_unit_ns = std::getenv("CREDO_CLC_UNIT_NS") ? std::atof(std::geten
 // to hide one cancel round trip, while leaving >= 3 units per SM so CTAs that
 // start late (SMs freed by other kernels) still balance the load.
 int tiles_per_unit(const ConvGemmArgs& a, int BN, int tiles) {
-  const double tile_flops = 2.0 * BM * BN * (double)a.Kc * a.ntaps;
+  const double tile_flops = 2.0 * BM * BN * ((double)a.Kc * a.ntaps + a.kc2);
   const double tile_ns = tile_flops / 8.0e3;  // 8 TFLOP/s per SM = 8e3 FLOP/ns
   int T = (int)std::ceil(g_unit_ns / std::max(tile_ns, 1.0));
   T = std::min(T, std::max(1, tiles / (3 * kNumSMs)));
@@ -1570,6 +1575,8 @@ void prepare_conv_gemm(PreparedGemm& p, const ConvGemmGroup& g, const ConvGemmAr
   } else if (a.Kc % 64 || a.ntaps < 1 || a.ntaps > 9) {
     throw InvalidArgument("conv_gemm: bad K");
   }
+  if (a.kc2 && (a.kc2 % 64 || a.ntaps != 1 || a.halo_lo || a.pair || a.s2d))
+    throw InvalidArgument("conv_gemm: a second K segment is for 1x1 streamed GEMMs");
   if (!a.out_f32 && (a.N % 32)) throw InvalidArgument("conv_gemm: bf16 out needs N%32==0");
   if (a.out_f32 && (a.N % 8)) throw InvalidArgument("conv_gemm: f32 out needs N%8==0");
   if (g.n < 1 || g.n > kMaxGroup) throw InvalidArgument("conv_gemm: group size 1..4");
@@ -1589,6 +1596,11 @@ void prepare_conv_gemm(PreparedGemm& p, const ConvGemmGroup& g, const ConvGemmAr
     if ((g.residual[r] != nullptr) != (g.residual[0] != nullptr))
       throw InvalidArgument("conv_gemm: residual on some replicas only");
     p.gp.A[r] = g.A[r]->map;
+    if (a.kc2) {
+      if (!g.A2[r] || g.A2[r]->box_rows != BM || g.A2[r]->cols != a.kc2)
+        throw InvalidArgument("conv_gemm: second K segment operand mismatch");
+      p.gp.A2[r] = g.A2[r]->map;
+    }
     p.gp.B[r] = g.B[r]->map;
     p.gp.bias[r] = g.bias[r];
     p.gp.residual[r] = g.residual[r];

@@ -71,6 +71,11 @@ struct ConvGemmArgs {
   // Rows live on a per-image gh x gw grid (row_mode kRowGridToCompact).
   int s2d;
   int gh, gw;
+  // Second K segment (1x1 convs only): k-blocks Kc/64 .. Kc/64 + kc2/64 - 1
+  // read A from the A2 operand (same rows) against weight columns Kc ..
+  // Kc + kc2 - 1 -- a bottleneck's c3 and its projection shortcut (ds) as one
+  // GEMM over [t2 | x] x [W3 | Wds]^T, no shortcut tensor in HBM. 0 = off.
+  int kc2;
 };
 
 // One encoded operand (tensor map over a row-major bf16 [rows, cols] matrix
@@ -94,6 +99,7 @@ constexpr int kMaxGroup = 4;
 struct ConvGemmGroup {
   int n = 0;
   const Operand* A[kMaxGroup];
+  const Operand* A2[kMaxGroup] = {};  // second K segment (ConvGemmArgs::kc2)
   const Operand* B[kMaxGroup];
   const float* bias[kMaxGroup];
   const __nv_bfloat16* residual[kMaxGroup];
@@ -102,7 +108,7 @@ struct ConvGemmGroup {
 
 // Kernel parameters of a grouped launch (all tensor maps pre-encoded).
 struct GemmGroupParams {
-  CUtensorMap A[kMaxGroup], B[kMaxGroup], R[kMaxGroup], O[kMaxGroup];
+  CUtensorMap A[kMaxGroup], B[kMaxGroup], R[kMaxGroup], O[kMaxGroup], A2[kMaxGroup];
   const float* bias[kMaxGroup];
   const __nv_bfloat16* residual[kMaxGroup];
   void* out[kMaxGroup];

@@ -3,7 +3,8 @@ grouped per launch, batch B), from an ncu CSV of `-k regex:conv_gemm`
 launches with gpu__time_duration.sum, dram__bytes_read.sum and
 dram__bytes_write.sum. floor = max(FLOPs / peak, compulsory bytes / peak BW)
 with the measured peaks (MEASURED_PEAKS.json); launch order = csrc/cnn.cu
-ResNet::ops (conv1, per block c1, c2, [ds], c3, fc).
+ResNet::ops (conv1, per block c1, c2, c3 (+ the projection shortcut in each
+stage's first block), fc).
 
   python tools/step_roofline.py <ncu.csv> [B] [replicas]
 """
@@ -33,11 +34,13 @@ def plan(B, R, S=224):
                       R * (px(H) * cin * 2 + px(H) * w * 2)))
             L.append((f"l{stage + 1}.{i} c2 3x3{'/2' if s == 2 else ''} {w}",
                       2 * px(Ho) * 9 * w * w * R, R * (px(H) * w * 2 + px(Ho) * w * 2)))
-            if i == 0:
-                L.append((f"l{stage + 1}.{i} ds 1x1 {cin}->{cout}", 2 * px(Ho) * cin * cout * R,
-                          R * (px(Ho) * cin * 2 + px(Ho) * cout * 2)))
-            L.append((f"l{stage + 1}.{i} c3 1x1 {w}->{cout} +res", 2 * px(Ho) * w * cout * R,
-                      R * (px(Ho) * w * 2 + 2 * px(Ho) * cout * 2)))
+            if i == 0:  # c3 + projection shortcut fused (K = w + cin)
+                L.append((f"l{stage + 1}.{i} c3+ds 1x1 {w}+{cin}->{cout}",
+                          2 * px(Ho) * (w + cin) * cout * R,
+                          R * (px(Ho) * (w + cin) * 2 + px(Ho) * cout * 2)))
+            else:
+                L.append((f"l{stage + 1}.{i} c3 1x1 {w}->{cout} +res", 2 * px(Ho) * w * cout * R,
+                          R * (px(Ho) * w * 2 + 2 * px(Ho) * cout * 2)))
             H, cin = Ho, cout
     L.append(("fc", 2 * B * cin * 1000 * R, R * (B * cin * 2 + B * 1000 * 4)))
     return L
