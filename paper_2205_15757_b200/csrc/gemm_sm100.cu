@@ -1363,6 +1363,17 @@ __global__ void __launch_bounds__(128, 1) mma_rate_kernel(int iters, int two_acc
                            ((uint32_t)(BM >> 4) << 24);
     const uint64_t ad = smem_desc_sw128(sA), bd = smem_desc_sw128(sB);
     long long t0 = clock64();
+    if (two_acc == 5) {
+      // the s2d stem's pattern: SW32 K = 16 rows, A at 4 row shifts (+32 B),
+      // 16 B tap tiles of 64 x 32 B, one accumulator
+      const uint64_t a32 = smem_desc_sw32_row(su32(sA)), b32 = smem_desc_sw32_row(su32(sB));
+      for (int i = 0; i < iters; i++)
+#pragma unroll
+        for (int k = 0; k < 4; k++)
+          umma_bf16(tmem, a32 + 2 * k + 2 * 4 * (i & 1), b32 + 128 * (4 * (i & 3) + k), idesc,
+                    (i | k) != 0);
+      iters *= 1;  // 4 MMAs per iteration, as the other modes
+    } else
     for (int i = 0; i < iters; i++) {
       const bool alt = (two_acc == 1 || two_acc == 4) && (i & 1);
       const uint32_t d = tmem + (alt ? 256u : 0u);
@@ -1471,6 +1482,7 @@ double mma_rate_bench(int N, int iters, int ctas, int two_acc, cudaStream_t st) 
   long long* d = nullptr;
   CG_CUDA(cudaMalloc(&d, 8));
   const int nbuf = two_acc >= 3 ? (N == 64 ? 8 : 4) : 1;
+  if (two_acc == 5 && N != 64) throw InvalidArgument("mma_rate: the s2d pattern is N = 64");
   if (N == 256 && nbuf > 1) throw InvalidArgument("mma_rate: rotating buffers for N <= 128");
   const int smem = 1024 + nbuf * (A_BYTES + N * BK * 2) + 64;
   auto run = [&](auto kern) {

@@ -16,3 +16,6 @@ for N in (64, 128):
         rc = ctx.L.cg_dbg_mma_rate(ctx.h, N, 4096, 148, mode, C.byref(c))
         assert rc == 0, ctx.L.cg_last_error(ctx.h)
         print(f"N={N:3d} {label}: {c.value:6.1f} cycles/MMA")
+c = C.c_double()
+assert ctx.L.cg_dbg_mma_rate(ctx.h, 64, 4096, 148, 5, C.byref(c)) == 0, ctx.L.cg_last_error(ctx.h)
+print(f"N= 64 s2d stem pattern (SW32, K = 16 rows, row-shifted A, 16 tap tiles): {c.value:6.1f} cycles/MMA")
