@@ -294,6 +294,9 @@ const bool kUseS2D = std::getenv("CREDO_NO_S2D") == nullptr;
 // c3 + projection shortcut as one GEMM over concatenated K (or
 // CREDO_NO_FUSE_DS=1: the shortcut GEMM's output read back as a residual)
 const bool kFuseDs = std::getenv("CREDO_NO_FUSE_DS") == nullptr;
+// the fused stride-2 shortcut reads x[2h, 2w] in place through a strided
+// tensor map (or CREDO_NO_A2VIEW=1: a gather pass first)
+const bool kA2View = std::getenv("CREDO_NO_A2VIEW") == nullptr;
 constexpr int kS2DMaxS = 2 * (256 - 128 - 3) - 6;  // a dy-pair box (128 + Gs + 3 rows) fits 256
 const bool kUseHalo = std::getenv("CREDO_NO_HALO") == nullptr;  // A/B switch for measurements
 
@@ -493,6 +496,7 @@ class ResNet final : public CnnModel {
     int s2d = 0, gh = 0, gw = 0;  // the s2d stem (ConvGemmArgs::s2d)
     const bf16* A2 = nullptr;     // second K segment operand (ConvGemmArgs::kc2)
     int kc2 = 0;
+    int a2_b = 0, a2_h = 0, a2_rpb = 0;  // A2 = x[2h, 2w] of [a2_b, a2_h, a2_h, kc2] in place
   };
   struct Op {
     bool gemm = false;
@@ -602,7 +606,8 @@ class ResNet final : public CnnModel {
       if (b.has_ds && kFuseDs) {
         // c3 + shortcut: K over t2's width channels, then the (decimated) x
         const bf16* dsin = X;
-        if (b.stride == 2) {
+        const bool view = b.stride == 2 && kA2View && Ho <= 56 && 56 % Ho == 0;
+        if (b.stride == 2 && !view) {
           bf16* G1 = g1_;
           const int C = b.cin;
           aux([X, G1, B, Hi, C](cudaStream_t st) {
@@ -616,6 +621,11 @@ class ResNet final : public CnnModel {
              0, 1, kRowIdentity, 0, B * Ho * Ho);
         L.back().g.A2 = dsin;
         L.back().g.kc2 = b.ds.Kc;
+        if (view) {
+          L.back().g.a2_b = (int)B;
+          L.back().g.a2_h = Hi;
+          L.back().g.a2_rpb = 56 / Ho;
+        }
         cur ^= 1;
         continue;
       }
@@ -802,6 +812,7 @@ class ResNet final : public CnnModel {
     ConvGemmGroup g;
     g.n = R;
     if (d0.s2d) BN = 64;
+    if (d0.a2_rpb) BN = 256;  // the strided-A2 kernel variant is BN = 256
     for (int r = 0; r < R; r++) {
       const GemmDesc& d = *ds[r];
       if (d.s2d) {
@@ -811,7 +822,8 @@ class ResNet final : public CnnModel {
         make_operand(A[r], d.A, d.rowsA, d.Kc, 128 + 2 * d.halo_lo);
         make_operand(Bm[r], d.c->w, d.c->cout, d.Kc * d.ntaps + d.kc2, BN);
         if (d.kc2) {
-          make_operand(A2[r], d.A2, d.rowsA, d.kc2, 128);
+          if (d.a2_rpb) make_operand_s2_view(A2[r], d.A2, d.a2_b, d.a2_h, d.kc2, d.a2_rpb);
+          else make_operand(A2[r], d.A2, d.rowsA, d.kc2, 128);
           g.A2[r] = &A2[r];
         }
       }
@@ -838,6 +850,8 @@ class ResNet final : public CnnModel {
     a.halo_lo = d0.halo_lo;
     a.s2d = d0.s2d;
     a.kc2 = d0.kc2;
+    a.a2_wo = d0.a2_rpb ? d0.a2_h / 2 : 0;
+    a.a2_rpb = d0.a2_rpb;
     a.gh = d0.gh;
     a.gw = d0.gw;
     auto p = std::make_shared<PreparedGemm>();

@@ -77,6 +77,14 @@ __device__ __forceinline__ void tma_load_2d(const CUtensorMap* tm, uint64_t* bar
       "l"(tm), "r"(su32(bar)), "r"(x), "r"(y)
       : "memory");
 }
+__device__ __forceinline__ void tma_load_3d(const CUtensorMap* tm, uint64_t* bar, void* dst, int x,
+                                            int y, int z) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(su32(dst)),
+      "l"(tm), "r"(su32(bar)), "r"(x), "r"(y), "r"(z)
+      : "memory");
+}
 __device__ __forceinline__ void sts_f32(uint32_t addr, float v) {
   asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
 }
@@ -509,9 +517,13 @@ struct TileSched {
 // half and the peer releases the accumulator on the leader's barrier.
 // Per SM and 128x256 output this halves the weight bytes written to and read
 // from shared memory (the bound of the BN=256 mainloop).
-template <int BN, int STAGES, int kResSlots, int HALO, int RESB, int PAIR, int S2D = 0>
+template <int BN, int STAGES, int kResSlots, int HALO, int RESB, int PAIR, int S2D = 0,
+          int A2S = 0>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_gemm_kernel(const __grid_constant__ GemmGroupParams gp, const ConvGemmArgs a) {
+  // A2S (strided second segment): A slots hold up to 4 boxes of 56 rows
+  constexpr int kASlot = A2S ? 4 * 56 * 128 : A_BYTES;
+  static_assert(!A2S || (HALO == 0 && RESB == 0 && !PAIR && !S2D), "strided A2: plain GEMMs");
   static_assert(!PAIR || (RESB == 0 && (HALO == 0 || kResSlots == 0)), "pair: streamed weights");
   static_assert(!S2D || (BN == 64 && RESB == 4 && HALO > 0 && !PAIR), "s2d stem layout");
   // s2d stem: a ring slot holds one dy box (2 planes x (BM + 3) rows x 16 B)
@@ -535,7 +547,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // output staging (64B swizzle), then barriers.
   uint8_t* smem = smem_raw + ((1024 - (su32(smem_raw) & 1023)) & 1023);
   uint8_t* sA = smem;
-  uint8_t* sB = smem + (HALO > 0 ? HALO * kHaloSlot : STAGES * A_BYTES);
+  uint8_t* sB = smem + (HALO > 0 ? HALO * kHaloSlot : STAGES * kASlot);
   uint8_t* s_res = sB + (RESB > STAGES ? RESB : STAGES) * B_BYTES;  // residual ring (SW64)
   float* s_epi = reinterpret_cast<float*>(s_res + kResSlots * 8192);  // 36 KB
   uint64_t* full = reinterpret_cast<uint64_t*>(s_epi + kEpiWarps * 32 * kStgLd);
@@ -769,12 +781,22 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int tap = kb / kpt, cb = kb - tap * kpt;
           mbar_wait(&empty[stage], phase ^ 1);
           if (kb == 0) CG_TRACE(1, ti);
-          mbar_expect_tx(&full[stage], A_BYTES + B_BYTES);
-          if (kb < num_k1)
-            tma_load_2d(&gp.A[r], &full[stage], sA + stage * A_BYTES, cb * BK,
-                        m0 + s_tap[tap]);
-          else  // second K segment: the same rows of the A2 operand
-            tma_load_2d(&gp.A2[r], &full[stage], sA + stage * A_BYTES, (kb - num_k1) * BK, m0);
+          if (A2S && kb >= num_k1) {
+            // strided second segment: the output rows covering [m0, m0 + 128)
+            const int rows_box = a.a2_rpb * a.a2_wo, r0 = m0 / a.a2_wo;
+            const int nbox = (m0 - r0 * a.a2_wo + BM + rows_box - 1) / rows_box;
+            mbar_expect_tx(&full[stage], nbox * rows_box * 128 + B_BYTES);
+            for (int j = 0; j < nbox; j++)
+              tma_load_3d(&gp.A2[r], &full[stage], sA + stage * kASlot + j * rows_box * 128,
+                          (kb - num_k1) * BK, 0, r0 + j * a.a2_rpb);
+          } else {
+            mbar_expect_tx(&full[stage], A_BYTES + B_BYTES);
+            if (kb < num_k1)
+              tma_load_2d(&gp.A[r], &full[stage], sA + stage * kASlot, cb * BK,
+                          m0 + s_tap[tap]);
+            else  // second K segment: the same rows of the A2 operand
+              tma_load_2d(&gp.A2[r], &full[stage], sA + stage * kASlot, (kb - num_k1) * BK, m0);
+          }
           tma_load_2d(&gp.B[r], &full[stage], sB + stage * B_BYTES, kb * BK, n0);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
@@ -936,12 +958,19 @@ __global__ void __launch_bounds__(kThreads, 1)
           continue;
         }
         const uint64_t ad0 = smem_desc_sw128(sA), bd0 = smem_desc_sw128(sB);
+        uint32_t a2_off = 0;  // strided second segment: the tile's row in its first box
+        if constexpr (A2S) {
+          int r_, m0_, n0_;
+          coords(sched.t, r_, m0_, n0_);
+          a2_off = (uint32_t)(m0_ % a.a2_wo) * (128 >> 4);
+        }
         for (int kb = 0; kb < num_k; kb++) {
           mbar_wait(&full[stage], phase);
           if (kb == 0) CG_TRACE(3, ti);
           tc_fence_after();
           // stage offsets added to the 14-bit start-address field (uniform adds)
-          const uint64_t ad = ad0 + (uint64_t)((stage * A_BYTES) >> 4);
+          const uint64_t ad = ad0 + (uint64_t)((stage * kASlot) >> 4) +
+                              (A2S && kb >= num_k1 ? a2_off : 0u);
           const uint64_t bd = bd0 + (uint64_t)((stage * B_BYTES) >> 4);
           umma_bf16_x4_w<2>(d, ad, bd, idesc, kb != 0);  // 4 x UMMA_K = 16
           umma_commit_w(&empty[stage]);
@@ -1234,9 +1263,12 @@ EncodeFn get_encode() {
   return fn;
 }
 
-template <int BN, int STAGES, int kResSlots, int HALO, int RESB, int PAIR = 0, int S2D = 0>
+template <int BN, int STAGES, int kResSlots, int HALO, int RESB, int PAIR = 0, int S2D = 0,
+          int A2S = 0>
 constexpr int smem_bytes() {
-  return 1024 + (HALO > 0 ? HALO * (S2D ? kS2DSlot : kHaloBytes) : STAGES * A_BYTES) +
+  return 1024 +
+         (HALO > 0 ? HALO * (S2D ? kS2DSlot : kHaloBytes)
+                   : STAGES * (A2S ? 4 * 56 * 128 : A_BYTES)) +
          (RESB > STAGES ? RESB : STAGES) * (PAIR ? BN / 2 : BN) * BK * 2 +
          kResSlots * 8192 + kEpiWarps * 32 * kStgLd * 4 +
          8 * (2 * STAGES + 4 + 2 * (kResSlots > 0 ? kResSlots : 1) + 2 * (HALO > 0 ? HALO : 1)) +
@@ -1262,13 +1294,14 @@ int tiles_per_unit(const ConvGemmArgs& a, int BN, int tiles) {
   return std::max(T, 1);
 }
 
-template <int BN, int STAGES, int RS, int HALO = 0, int RESB = 0, int PAIR = 0, int S2D = 0>
+template <int BN, int STAGES, int RS, int HALO = 0, int RESB = 0, int PAIR = 0, int S2D = 0,
+          int A2S = 0>
 void launch_t(const PreparedGemm& p, cudaStream_t st, int max_ctas) {
-  constexpr int smem = smem_bytes<BN, STAGES, RS, HALO, RESB, PAIR, S2D>();
+  constexpr int smem = smem_bytes<BN, STAGES, RS, HALO, RESB, PAIR, S2D, A2S>();
   static_assert(smem <= 232448, "smem budget");
   static std::atomic<uint64_t> attr{0};
   once_per_device(attr, [] {
-    CG_CUDA(cudaFuncSetAttribute(conv_gemm_kernel<BN, STAGES, RS, HALO, RESB, PAIR, S2D>,
+    CG_CUDA(cudaFuncSetAttribute(conv_gemm_kernel<BN, STAGES, RS, HALO, RESB, PAIR, S2D, A2S>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   });
   ConvGemmArgs a = p.args;
@@ -1319,7 +1352,7 @@ void launch_t(const PreparedGemm& p, cudaStream_t st, int max_ctas) {
     at[0].val.programmaticStreamSerializationAllowed = g_pdl;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    CG_CUDA(cudaLaunchKernelEx(&cfg, conv_gemm_kernel<BN, STAGES, RS, HALO, RESB, PAIR, S2D>,
+    CG_CUDA(cudaLaunchKernelEx(&cfg, conv_gemm_kernel<BN, STAGES, RS, HALO, RESB, PAIR, S2D, A2S>,
                                p.gp, a));
     launch_counter_add(1);
   }
@@ -1520,6 +1553,25 @@ void make_operand(Operand& op, const void* ptr, int rows, int cols, int box_rows
   op.box_rows = box_rows;
 }
 
+void make_operand_s2_view(Operand& op, const void* x, int B, int H, int C, int rpb) {
+  if (reinterpret_cast<uintptr_t>(x) % 16 || C % 64 || H % 2)
+    throw InvalidArgument("strided view: misaligned or odd shape");
+  const int Wo = H / 2;
+  cuuint64_t dims[3] = {(cuuint64_t)C, (cuuint64_t)Wo, (cuuint64_t)B * Wo};
+  cuuint64_t strides[2] = {(cuuint64_t)2 * C * 2, (cuuint64_t)2 * H * C * 2};
+  cuuint32_t box[3] = {64, (cuuint32_t)Wo, (cuuint32_t)rpb};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = get_encode()(&op.map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(x),
+                            dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw CudaError("strided view tensor map failed: " + std::to_string((int)r));
+  op.ptr = x;
+  op.rows = B * Wo * Wo;
+  op.cols = C;
+  op.box_rows = Wo * rpb;
+}
+
 // [rows, 16] bf16 (32-byte rows) with the 32B swizzle: the s2d stem's
 // image (box_rows-row boxes) and weights (256-row boxes).
 static void make_operand_k16(Operand& op, const void* ptr, int rows, int box_rows) {
@@ -1609,8 +1661,11 @@ void prepare_conv_gemm(PreparedGemm& p, const ConvGemmGroup& g, const ConvGemmAr
       throw InvalidArgument("conv_gemm: residual on some replicas only");
     p.gp.A[r] = g.A[r]->map;
     if (a.kc2) {
-      if (!g.A2[r] || g.A2[r]->box_rows != BM || g.A2[r]->cols != a.kc2)
+      if (!g.A2[r] || g.A2[r]->cols != a.kc2 ||
+          g.A2[r]->box_rows != (a.a2_wo ? a.a2_wo * a.a2_rpb : BM))
         throw InvalidArgument("conv_gemm: second K segment operand mismatch");
+      if (a.a2_wo && (a.a2_wo * a.a2_rpb != 56 || a.kc2 % 64))
+        throw InvalidArgument("conv_gemm: strided A2 boxes are 56 rows");
       p.gp.A2[r] = g.A2[r]->map;
     }
     p.gp.B[r] = g.B[r]->map;
@@ -1637,6 +1692,11 @@ void prepare_conv_gemm(PreparedGemm& p, const ConvGemmGroup& g, const ConvGemmAr
 }
 
 void launch_prepared(const PreparedGemm& p, cudaStream_t st, int max_ctas) {
+  if (p.args.a2_wo) {  // strided second segment (the stride-2 shortcut, no gather)
+    if (p.BN != 256 || p.res) throw InvalidArgument("conv_gemm: strided A2 is for BN = 256");
+    launch_t<256, 3, 0, 0, 0, 0, 0, 1>(p, st, max_ctas);
+    return;
+  }
   if (p.args.s2d) {  // 12 dy-pair boxes (6 tiles) in flight, 16 taps' weights resident
     launch_t<64, 1, 0, 12, 4, 0, 1>(p, st, max_ctas);
     return;

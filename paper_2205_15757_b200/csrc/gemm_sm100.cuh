@@ -76,6 +76,13 @@ struct ConvGemmArgs {
   // Kc + kc2 - 1 -- a bottleneck's c3 and its projection shortcut (ds) as one
   // GEMM over [t2 | x] x [W3 | Wds]^T, no shortcut tensor in HBM. 0 = off.
   int kc2;
+  // Strided second segment (a2_wo > 0): the A2 operand is x[2h, 2w] read in
+  // place through a 3-D tensor map (channels, w' stepping 2 pixels, output
+  // rows stepping 2 input rows) in boxes of a2_rpb output rows of a2_wo
+  // pixels (a2_rpb * a2_wo = 56 rows, 7 KB, 1024-aligned in the stage), the
+  // MMA reading the tile's 128 rows from its offset in the first box -- the
+  // stride-2 shortcut without a gather pass. 0 = A2 is a compact operand.
+  int a2_wo, a2_rpb;
 };
 
 // One encoded operand (tensor map over a row-major bf16 [rows, cols] matrix
@@ -87,6 +94,9 @@ struct Operand {
 };
 
 void make_operand(Operand& op, const void* ptr, int rows, int cols, int box_rows);
+// x[2h, 2w] of an NHWC [B, H, H, C] bf16 tensor as a 3-D map (C, H/2 w',
+// B*H/2 output rows), box 64 x (H/2) x rpb, 128B swizzle (ConvGemmArgs::a2_wo)
+void make_operand_s2_view(Operand& op, const void* x, int B, int H, int C, int rpb);
 // s2d stem operands: A = [rows, 16] bf16 image, box 16 x box_rows; B =
 // [16 * N, 16] bf16 weights in [tap][N][16] order, box 16 x 256; 32B swizzle.
 void make_operand_s2d_a(Operand& op, const void* ptr, int rows, int box_rows);
