@@ -524,6 +524,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   // A2S (strided second segment): A slots hold up to 4 boxes of 56 rows
   constexpr int kASlot = A2S ? 4 * 56 * 128 : A_BYTES;
   static_assert(!A2S || (HALO == 0 && RESB == 0 && !PAIR && !S2D), "strided A2: plain GEMMs");
+  // 4-stage 256-wide streamed GEMMs: epilogue staging sized for the
+  // TMA-store path only (2 x 2 KB per warp; the launcher picks them for
+  // identity bf16 rows), which frees the fourth stage
+  constexpr bool kSmallStg = STAGES == 4 && BN == 256 && kResSlots == 0 && HALO == 0 && !PAIR;
+  constexpr int kStgWarp = kSmallStg ? 1024 : 32 * kStgLd;  // floats per epilogue warp
   static_assert(!PAIR || (RESB == 0 && (HALO == 0 || kResSlots == 0)), "pair: streamed weights");
   static_assert(!S2D || (BN == 64 && RESB == 4 && HALO > 0 && !PAIR), "s2d stem layout");
   // s2d stem: a ring slot holds one dy box (2 planes x (BM + 3) rows x 16 B)
@@ -550,7 +555,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sB = smem + (HALO > 0 ? HALO * kHaloSlot : STAGES * kASlot);
   uint8_t* s_res = sB + (RESB > STAGES ? RESB : STAGES) * B_BYTES;  // residual ring (SW64)
   float* s_epi = reinterpret_cast<float*>(s_res + kResSlots * 8192);  // 36 KB
-  uint64_t* full = reinterpret_cast<uint64_t*>(s_epi + kEpiWarps * 32 * kStgLd);
+  uint64_t* full = reinterpret_cast<uint64_t*>(s_epi + kEpiWarps * kStgWarp);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
@@ -1005,7 +1010,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     //    32x36 fp32 smem tile; (2) lane = (row group, 8-column group): bias,
     //    ReLU, pack, 16-byte stores covering 8 rows x 64 B per instruction.
     const int q = warp & 3, h = (warp - 2) >> 2;
-    const uint32_t stg_a = su32(s_epi + (warp - 2) * (32 * kStgLd));
+    const uint32_t stg_a = su32(s_epi + (warp - 2) * kStgWarp);
     const int rr8 = lane >> 2, cg8 = lane & 3;
     constexpr int CPT = BN / 32;  // 32-column chunks per tile
     // BN = 64 (2 chunks): the two warp groups take alternate tiles whole
@@ -1270,7 +1275,10 @@ constexpr int smem_bytes() {
          (HALO > 0 ? HALO * (S2D ? kS2DSlot : kHaloBytes)
                    : STAGES * (A2S ? 4 * 56 * 128 : A_BYTES)) +
          (RESB > STAGES ? RESB : STAGES) * (PAIR ? BN / 2 : BN) * BK * 2 +
-         kResSlots * 8192 + kEpiWarps * 32 * kStgLd * 4 +
+         kResSlots * 8192 +
+         kEpiWarps * 4 *
+             ((STAGES == 4 && BN == 256 && kResSlots == 0 && HALO == 0 && !PAIR) ? 1024
+                                                                                  : 32 * kStgLd) +
          8 * (2 * STAGES + 4 + 2 * (kResSlots > 0 ? kResSlots : 1) + 2 * (HALO > 0 ? HALO : 1)) +
          16 + 48 + 16 + 32 * kClcSlots;
 }
@@ -1280,6 +1288,8 @@ const int g_pdl = std::getenv("CREDO_NO_PDL") == nullptr ? 1 : 0;
 // env CREDO_NO_CLC: static persistent grids (A/B); CREDO_CLC_UNIT_NS: target
 // work per scheduling unit
 const bool g_clc = std::getenv("CREDO_NO_CLC") == nullptr;
+// env CREDO_NO_STG4=1: 3 stages for every streamed 256-wide GEMM (A/B)
+const bool g_stg4 = std::getenv("CREDO_NO_STG4") == nullptr;
 const double g_unit_ns = std::getenv("CREDO_CLC_UNIT_NS") ? std::atof(std::getenv("CREDO_CLC_UNIT_NS"))
                                                           : 1500.0;
 
@@ -1747,7 +1757,12 @@ void launch_prepared(const PreparedGemm& p, cudaStream_t st, int max_ctas) {
       if (deep_k) launch_t<128, 4, 6>(p, st, max_ctas);
       else launch_t<128, 3, 10>(p, st, max_ctas);
       break;
-    case 512: launch_t<256, 3, 0>(p, st, max_ctas); break;
+    case 512:  // identity bf16 rows: the TMA-store epilogue leaves room for 4 stages
+      if (p.args.row_mode == kRowIdentity && !p.args.out_f32 && g_stg4)
+        launch_t<256, 4, 0>(p, st, max_ctas);
+      else
+        launch_t<256, 3, 0>(p, st, max_ctas);
+      break;
     case 513:
       if (deep_k) launch_t<256, 3, 4>(p, st, max_ctas);
       else launch_t<256, 2, 10>(p, st, max_ctas);
