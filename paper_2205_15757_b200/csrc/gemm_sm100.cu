@@ -525,8 +525,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int kASlot = A2S ? 4 * 56 * 128 : A_BYTES;
   static_assert(!A2S || (HALO == 0 && RESB == 0 && !PAIR && !S2D), "strided A2: plain GEMMs");
   // 4-stage 256-wide streamed GEMMs: epilogue staging sized for the
-  // TMA-store path only (2 x 2 KB per warp; the launcher picks them for
-  // identity bf16 rows), which frees the fourth stage
+  // TMA-store path only (2 x 2 KB per warp; the launcher picks them for bf16
+  // outputs, which take the TMA-store or the staging-free direct-store
+  // epilogue), which frees the fourth stage
   constexpr bool kSmallStg = STAGES == 4 && BN == 256 && kResSlots == 0 && HALO == 0 && !PAIR;
   constexpr int kStgWarp = kSmallStg ? 1024 : 32 * kStgLd;  // floats per epilogue warp
   static_assert(!PAIR || (RESB == 0 && (HALO == 0 || kResSlots == 0)), "pair: streamed weights");
@@ -1757,8 +1758,8 @@ void launch_prepared(const PreparedGemm& p, cudaStream_t st, int max_ctas) {
       if (deep_k) launch_t<128, 4, 6>(p, st, max_ctas);
       else launch_t<128, 3, 10>(p, st, max_ctas);
       break;
-    case 512:  // identity bf16 rows: the TMA-store epilogue leaves room for 4 stages
-      if (p.args.row_mode == kRowIdentity && !p.args.out_f32 && g_stg4)
+    case 512:  // bf16 out through the TMA-store or direct-store epilogue: room for 4 stages
+      if (!p.args.out_f32 && (p.args.row_mode == kRowIdentity || kDirectRemap) && g_stg4)
         launch_t<256, 4, 0>(p, st, max_ctas);
       else
         launch_t<256, 3, 0>(p, st, max_ctas);
