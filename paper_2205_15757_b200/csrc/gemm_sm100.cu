@@ -528,7 +528,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   // TMA-store path only (2 x 2 KB per warp; the launcher picks them for bf16
   // outputs, which take the TMA-store or the staging-free direct-store
   // epilogue), which frees the fourth stage
-  constexpr bool kSmallStg = STAGES == 4 && BN == 256 && kResSlots == 0 && HALO == 0 && !PAIR;
+  constexpr bool kSmallStg = ((BN == 256 && STAGES == 4) || (BN == 128 && STAGES == 6) ||
+                              (BN == 64 && STAGES == 8)) &&
+                             kResSlots == 0 && HALO == 0 && !PAIR;
   constexpr int kStgWarp = kSmallStg ? 1024 : 32 * kStgLd;  // floats per epilogue warp
   static_assert(!PAIR || (RESB == 0 && (HALO == 0 || kResSlots == 0)), "pair: streamed weights");
   static_assert(!S2D || (BN == 64 && RESB == 4 && HALO > 0 && !PAIR), "s2d stem layout");
@@ -1278,8 +1280,11 @@ constexpr int smem_bytes() {
          (RESB > STAGES ? RESB : STAGES) * (PAIR ? BN / 2 : BN) * BK * 2 +
          kResSlots * 8192 +
          kEpiWarps * 4 *
-             ((STAGES == 4 && BN == 256 && kResSlots == 0 && HALO == 0 && !PAIR) ? 1024
-                                                                                  : 32 * kStgLd) +
+             ((((BN == 256 && STAGES == 4) || (BN == 128 && STAGES == 6) ||
+                (BN == 64 && STAGES == 8)) &&
+               kResSlots == 0 && HALO == 0 && !PAIR)
+                  ? 1024
+                  : 32 * kStgLd) +
          8 * (2 * STAGES + 4 + 2 * (kResSlots > 0 ? kResSlots : 1) + 2 * (HALO > 0 ? HALO : 1)) +
          16 + 48 + 16 + 32 * kClcSlots;
 }
@@ -1748,12 +1753,22 @@ void launch_prepared(const PreparedGemm& p, cudaStream_t st, int max_ctas) {
 #endif
   const bool deep_k = CG_RES_DEEPK && p.args.Kc * p.args.ntaps >= 8 * BK;
   switch (p.BN * 2 + (p.res ? 1 : 0)) {
-    case 128: launch_t<64, 7, 0>(p, st, max_ctas); break;  // (p.BN * 2 + residual)
+    case 128:  // (p.BN * 2 + residual); bf16 out: one more stage in the freed staging
+      if (!p.args.out_f32 && (p.args.row_mode == kRowIdentity || kDirectRemap) && g_stg4)
+        launch_t<64, 8, 0>(p, st, max_ctas);
+      else
+        launch_t<64, 7, 0>(p, st, max_ctas);
+      break;
     case 129:
       if (deep_k) launch_t<64, 5, 6>(p, st, max_ctas);
       else launch_t<64, 4, 10>(p, st, max_ctas);
       break;
-    case 256: launch_t<128, 5, 0>(p, st, max_ctas); break;
+    case 256:
+      if (!p.args.out_f32 && (p.args.row_mode == kRowIdentity || kDirectRemap) && g_stg4)
+        launch_t<128, 6, 0>(p, st, max_ctas);
+      else
+        launch_t<128, 5, 0>(p, st, max_ctas);
+      break;
     case 257:
       if (deep_k) launch_t<128, 4, 6>(p, st, max_ctas);
       else launch_t<128, 3, 10>(p, st, max_ctas);
