@@ -517,6 +517,23 @@ struct TileSched {
 // half and the peer releases the accumulator on the leader's barrier.
 // Per SM and 128x256 output this halves the weight bytes written to and read
 // from shared memory (the bound of the BN=256 mainloop).
+// Floats of epilogue staging per epilogue warp: 32 x kStgLd for the f32 /
+// remapped-row staging paths, 1024 (2 x 2 KB) for the TMA-store path only,
+// 0 for halo variants whose remapped bf16 rows go out by direct stores. The
+// launcher picks the reduced variants only for outputs that fit them; the
+// freed shared memory buys mainloop stages / halo slots.
+template <int BN, int STAGES, int kResSlots, int HALO, int RESB, int PAIR>
+constexpr int stg_floats() {
+  if (PAIR || kResSlots) return 32 * kStgLd;
+  if (HALO == 0 && ((BN == 256 && STAGES == 4) || (BN == 128 && STAGES == 6) ||
+                    (BN == 64 && STAGES == 8)))
+    return 1024;
+  if ((BN == 256 && STAGES == 4 && HALO == 2) || (BN == 128 && STAGES == 8 && HALO == 2) ||
+      (BN == 64 && STAGES == 8 && HALO == 4) || (BN == 64 && RESB == 9 && HALO == 4))
+    return 0;
+  return 32 * kStgLd;
+}
+
 template <int BN, int STAGES, int kResSlots, int HALO, int RESB, int PAIR, int S2D = 0,
           int A2S = 0>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -528,10 +545,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // TMA-store path only (2 x 2 KB per warp; the launcher picks them for bf16
   // outputs, which take the TMA-store or the staging-free direct-store
   // epilogue), which frees the fourth stage
-  constexpr bool kSmallStg = ((BN == 256 && STAGES == 4) || (BN == 128 && STAGES == 6) ||
-                              (BN == 64 && STAGES == 8)) &&
-                             kResSlots == 0 && HALO == 0 && !PAIR;
-  constexpr int kStgWarp = kSmallStg ? 1024 : 32 * kStgLd;  // floats per epilogue warp
+  constexpr int kStgWarp = stg_floats<BN, STAGES, kResSlots, HALO, RESB, PAIR>();
   static_assert(!PAIR || (RESB == 0 && (HALO == 0 || kResSlots == 0)), "pair: streamed weights");
   static_assert(!S2D || (BN == 64 && RESB == 4 && HALO > 0 && !PAIR), "s2d stem layout");
   // s2d stem: a ring slot holds one dy box (2 planes x (BM + 3) rows x 16 B)
@@ -1279,12 +1293,7 @@ constexpr int smem_bytes() {
                    : STAGES * (A2S ? 4 * 56 * 128 : A_BYTES)) +
          (RESB > STAGES ? RESB : STAGES) * (PAIR ? BN / 2 : BN) * BK * 2 +
          kResSlots * 8192 +
-         kEpiWarps * 4 *
-             ((((BN == 256 && STAGES == 4) || (BN == 128 && STAGES == 6) ||
-                (BN == 64 && STAGES == 8)) &&
-               kResSlots == 0 && HALO == 0 && !PAIR)
-                  ? 1024
-                  : 32 * kStgLd) +
+         kEpiWarps * 4 * stg_floats<BN, STAGES, kResSlots, HALO, RESB, PAIR>() +
          8 * (2 * STAGES + 4 + 2 * (kResSlots > 0 ? kResSlots : 1) + 2 * (HALO > 0 ? HALO : 1)) +
          16 + 48 + 16 + 32 * kClcSlots;
 }
@@ -1734,13 +1743,28 @@ void launch_prepared(const PreparedGemm& p, cudaStream_t st, int max_ctas) {
     // small weight sets (one n block, 9 x 64-channel taps): keep B resident
     if (p.BN == 64 && p.args.N <= 64 && p.args.Kc == 64 && p.args.ntaps == 9 &&
         std::getenv("CREDO_NO_RESB") == nullptr) {
-      launch_t<64, 1, 0, 3, 9>(p, st, max_ctas);
+      if (!p.args.out_f32 && p.args.row_mode != kRowIdentity && kDirectRemap && g_stg4)
+        launch_t<64, 1, 0, 4, 9>(p, st, max_ctas);  // no staging: a 4th halo slot
+      else
+        launch_t<64, 1, 0, 3, 9>(p, st, max_ctas);
       return;
     }
+    // remapped bf16 rows leave the epilogue staging unused: deeper halo rings
+    const bool deep_halo =
+        !p.args.out_f32 && p.args.row_mode != kRowIdentity && kDirectRemap && g_stg4;
     switch (p.BN) {
-      case 64: launch_t<64, 8, 0, 3>(p, st, max_ctas); return;
-      case 128: launch_t<128, 6, 0, 2>(p, st, max_ctas); return;
-      case 256: launch_t<256, 3, 0, 2>(p, st, max_ctas); return;
+      case 64:
+        if (deep_halo) launch_t<64, 8, 0, 4>(p, st, max_ctas);
+        else launch_t<64, 8, 0, 3>(p, st, max_ctas);
+        return;
+      case 128:
+        if (deep_halo) launch_t<128, 8, 0, 2>(p, st, max_ctas);
+        else launch_t<128, 6, 0, 2>(p, st, max_ctas);
+        return;
+      case 256:
+        if (deep_halo) launch_t<256, 4, 0, 2>(p, st, max_ctas);
+        else launch_t<256, 3, 0, 2>(p, st, max_ctas);
+        return;
       default: throw InvalidArgument("conv_gemm: BN must be 64, 128 or 256");
     }
   }
