@@ -524,6 +524,7 @@ struct TileSched {
 // freed shared memory buys mainloop stages / halo slots.
 template <int BN, int STAGES, int kResSlots, int HALO, int RESB, int PAIR>
 constexpr int stg_floats() {
+  if (!PAIR && BN == 256 && STAGES == 2 && kResSlots == 12) return 1024;  // residual: 6 boxes
   if (PAIR || kResSlots) return 32 * kStgLd;
   if (HALO == 0 && ((BN == 256 && STAGES == 4) || (BN == 128 && STAGES == 6) ||
                     (BN == 64 && STAGES == 8)))
@@ -1805,6 +1806,8 @@ void launch_prepared(const PreparedGemm& p, cudaStream_t st, int max_ctas) {
       break;
     case 513:
       if (deep_k) launch_t<256, 3, 4>(p, st, max_ctas);
+      else if (p.args.row_mode == kRowIdentity && !p.args.out_f32 && g_stg4)
+        launch_t<256, 2, 12>(p, st, max_ctas);  // TMA-store staging only: a deeper ring
       else launch_t<256, 2, 10>(p, st, max_ctas);
       break;
     default: throw InvalidArgument("conv_gemm: BN must be 64, 128 or 256");
