@@ -983,12 +983,19 @@ __global__ void __launch_bounds__(256) dw3x3_kernel(const bf16* __restrict__ in,
       wr[ds][4] = w1.x; wr[ds][5] = w1.y; wr[ds][6] = w1.z; wr[ds][7] = w1.w;
     }
     const bf16* row = in + ((size_t)n * H + h) * H * C + c0;
+    // all of the row's column loads first (clamped addresses, zero outside):
+    // NCOL independent 16-byte loads in flight per thread
+    uint4 qs[NCOL];
+#pragma unroll
+    for (int col = 0; col < NCOL; col++) {
+      const int x = min(max(x0 + col, 0), H - 1);
+      qs[col] = __ldg(reinterpret_cast<const uint4*>(row + (size_t)x * C));
+    }
 #pragma unroll
     for (int col = 0; col < NCOL; col++) {
       const int x = x0 + col;
       if (x < 0 || x >= H) continue;
-      const uint4 q = __ldg(reinterpret_cast<const uint4*>(row + (size_t)x * C));
-      const bf16* e = reinterpret_cast<const bf16*>(&q);
+      const bf16* e = reinterpret_cast<const bf16*>(&qs[col]);
       float v[8];
 #pragma unroll
       for (int j = 0; j < 8; j++) v[j] = __bfloat162float(e[j]);
