@@ -156,11 +156,16 @@ __global__ void maxpool3s2_kernel(const bf16* __restrict__ in, int B, int H, int
     const int h = 2 * ho - 1 + dr;
     if (h < 0 || h >= H) continue;
     const bf16* row = in + ((size_t)n * Gh + h) * P * C + ch * 8;
+    uint4 qs[5];  // the row's 5 column loads in flight together (clamped addresses)
+#pragma unroll
+    for (int dc = 0; dc < 5; dc++)
+      qs[dc] = __ldg(reinterpret_cast<const uint4*>(
+          row + (size_t)min(max(4 * j - 1 + dc, 0), H - 1) * C));
 #pragma unroll
     for (int dc = 0; dc < 5; dc++) {
       const int w = 4 * j - 1 + dc;
       if (w < 0 || w >= H) continue;
-      uint4 q = __ldg(reinterpret_cast<const uint4*>(row + (size_t)w * C));
+      const uint4 q = qs[dc];
       const __nv_bfloat162* e = reinterpret_cast<const __nv_bfloat162*>(&q);
 #pragma unroll
       for (int k = 0; k < 4; k++) {
