@@ -395,3 +395,77 @@ extern "C" int cg_dbg_mma_rate(cg_ctx* ctx, int N, int iters, int ctas, int two_
     return CG_ECUDA;
   }
 }
+
+// Timing + CTA-0 event trace of the s2d stem GEMM (conv1 of a ResNet at
+// S x S input: 16 taps of K = 16 over the Gs x Gs space-to-depth grid, 64
+// outputs on the same grid) for `reps` grouped replicas of B images.
+extern "C" int cg_dbg_s2d_trace(cg_ctx* ctx, int B, int S, int reps, long long* trace_host,
+                                double* us) {
+  try {
+    cudaStream_t st = (cudaStream_t)cg_ctx_stream(ctx);
+    const int Gs = (S + 6) / 2, rows = B * Gs * Gs;
+    if (reps < 1 || reps > kMaxGroup) return CG_EINVAL;
+    void *dA[kMaxGroup], *dB, *dbias, *dout[kMaxGroup];
+    long long* dtr;
+    CG_CUDA(cudaMalloc(&dB, (size_t)16 * 64 * 16 * 2));
+    CG_CUDA(cudaMalloc(&dbias, 64 * 4));
+    CG_CUDA(cudaMalloc(&dtr, 16 * 64 * 8));
+    CG_CUDA(cudaMemset(dB, 0x11, (size_t)16 * 64 * 16 * 2));
+    CG_CUDA(cudaMemset(dbias, 0, 64 * 4));
+    CG_CUDA(cudaMemset(dtr, 0, 16 * 64 * 8));
+    Operand oa[kMaxGroup], ob;
+    make_operand_s2d_b(ob, dB, 16 * 64);
+    ConvGemmGroup g;
+    g.n = reps;
+    for (int r = 0; r < reps; r++) {
+      CG_CUDA(cudaMalloc(&dA[r], (size_t)rows * 32));
+      CG_CUDA(cudaMalloc(&dout[r], (size_t)rows * 64 * 2));
+      CG_CUDA(cudaMemset(dA[r], 0x11, (size_t)rows * 32));
+      make_operand_s2d_a(oa[r], dA[r], rows, 128 + Gs + 3);
+      g.A[r] = &oa[r];
+      g.B[r] = &ob;
+      g.bias[r] = (const float*)dbias;
+      g.residual[r] = nullptr;
+      g.out[r] = dout[r];
+    }
+    ConvGemmArgs a{};
+    a.M = rows;
+    a.N = 64;
+    a.Kc = 16;
+    a.ntaps = 16;
+    a.ld_out = 64;
+    a.relu = 1;
+    a.row_mode = kRowIdentity;
+    a.H = a.W = S / 2;
+    a.rows_out = rows;
+    a.s2d = 1;
+    a.gh = a.gw = Gs;
+    PreparedGemm p;
+    prepare_conv_gemm(p, g, a, 64);
+    launch_prepared(p, st);  // warm
+    cudaEvent_t e0, e1;
+    CG_CUDA(cudaEventCreate(&e0));
+    CG_CUDA(cudaEventCreate(&e1));
+    CG_CUDA(cudaEventRecord(e0, st));
+    for (int i = 0; i < 5; i++) launch_prepared(p, st);
+    CG_CUDA(cudaEventRecord(e1, st));
+    PreparedGemm pt = p;
+    pt.args.trace = dtr;
+    launch_prepared(pt, st);
+    CG_CUDA(cudaStreamSynchronize(st));
+    float ms = 0;
+    CG_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    *us = 1000.0 * ms / 5;
+    CG_CUDA(cudaMemcpy(trace_host, dtr, 16 * 64 * 8, cudaMemcpyDeviceToHost));
+    for (int r = 0; r < reps; r++) {
+      cudaFree(dA[r]);
+      cudaFree(dout[r]);
+    }
+    cudaFree(dB);
+    cudaFree(dbias);
+    cudaFree(dtr);
+    return CG_OK;
+  } catch (const std::exception&) {
+    return CG_ECUDA;
+  }
+}

@@ -247,6 +247,33 @@ __device__ __forceinline__ void umma_bf16_x4x2_w(uint32_t d0, uint32_t d1, uint6
       "r"(d1), "l"(a0), "l"(a1), "l"(b), "r"(idesc), "r"(accum), "n"(BSTEP), "n"(2 * BSTEP),
       "n"(3 * BSTEP));
 }
+// bf16x2 pack of (lo, hi) with the ReLU folded into the conversion
+// (cvt.rn.relu: negative -> 0 in the same instruction; lo in the low half)
+__device__ __forceinline__ uint32_t pack_bf16x2_relu(float lo, float hi) {
+  uint32_t d;
+  asm("cvt.rn.relu.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi), "f"(lo));
+  return d;
+}
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  uint32_t d;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi), "f"(lo));
+  return d;
+}
+// ReLU / ReLU6 / none + bf16 pack of 2n floats
+template <int N2>
+__device__ __forceinline__ void act_pack(const float* x, uint32_t* o, int relu) {
+  if (relu == 1) {
+#pragma unroll
+    for (int j = 0; j < N2; j++) o[j] = pack_bf16x2_relu(x[2 * j], x[2 * j + 1]);
+  } else if (relu == 2) {
+#pragma unroll
+    for (int j = 0; j < N2; j++)
+      o[j] = pack_bf16x2_relu(fminf(x[2 * j], 6.f), fminf(x[2 * j + 1], 6.f));
+  } else {
+#pragma unroll
+    for (int j = 0; j < N2; j++) o[j] = pack_bf16x2(x[2 * j], x[2 * j + 1]);
+  }
+}
 __device__ __forceinline__ void umma_commit_w(uint64_t* b) {
   asm volatile(
       "{\n\t.reg .pred e;\n\t"
@@ -1119,17 +1146,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&rempty[slot]);
           }
-          if (a.relu) {
-            const float hi = a.relu == 2 ? 6.f : INFINITY;  // ReLU / ReLU6
-#pragma unroll
-            for (int j = 0; j < 32; j++) x[j] = fminf(fmaxf(x[j], 0.f), hi);
-          }
           uint32_t o[16];
-#pragma unroll
-          for (int j = 0; j < 16; j++) {
-            __nv_bfloat162 t2 = __floats2bfloat162_rn(x[2 * j], x[2 * j + 1]);
-            o[j] = *reinterpret_cast<uint32_t*>(&t2);
-          }
+          act_pack<16>(x, o, a.relu);  // ReLU / ReLU6 + bf16 pack
           const int buf = stage_seq++ & 1;  // this warp's chunks alternate buffers
           const uint32_t sb = stg_a + buf * 2048;
           if (lane == 0) bulk_wait_read<1>();
@@ -1162,17 +1180,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             x[4 * j + 3] = __uint_as_float(v[4 * j + 3]) + b4.w;
           }
           if (c + C0S < CPT) tmem_ld32_issue(trow + (c + C0S) * 32, v);
-          if (a.relu) {
-            const float hi = a.relu == 2 ? 6.f : INFINITY;
-#pragma unroll
-            for (int j = 0; j < 32; j++) x[j] = fminf(fmaxf(x[j], 0.f), hi);
-          }
           uint32_t o[16];
-#pragma unroll
-          for (int j = 0; j < 16; j++) {
-            __nv_bfloat162 t2 = __floats2bfloat162_rn(x[2 * j], x[2 * j + 1]);
-            o[j] = *reinterpret_cast<uint32_t*>(&t2);
-          }
+          act_pack<16>(x, o, a.relu);  // ReLU / ReLU6 + bf16 pack
           if (my_orow >= 0 && n < a.N) {
             __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(out_r) +
                                  (size_t)my_orow * a.ld_out + n;
@@ -1247,6 +1256,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (warp == 2) CG_TRACE(6, tile_i);
       if (warp == 9) CG_TRACE(7, tile_i);
+      if (S2D) CG_TRACE(8 + warp - 2, tile_i);  // dbg: every epilogue warp's end
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
     if (tma_out && lane == 0) bulk_wait_all();  // this warp's stores read their staging
