@@ -69,6 +69,32 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
       : "memory");
 #endif
 }
+// The same wait with a suspend-time hint: the warp sleeps in the barrier
+// until the phase completes (or the hint elapses) instead of re-polling, so
+// an epilogue warp waiting for its next accumulator takes no issue slots
+// from the warps of its SM sub-partition that are still draining theirs.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(su32(b)),
+      "r"(parity), "r"(100000)
+      : "memory");
+}
+// n / d for a kernel-uniform divisor by multiply-high (n, d < 2^31): the
+// tile -> (replica, row block, column block) split runs once per tile in
+// every warp role, and a generic integer division is ~20 instructions.
+struct FastDiv {
+  uint32_t d, m, l;
+  __device__ __forceinline__ void init(uint32_t d_) {
+    d = d_;
+    l = 0;
+    while ((1u << l) < d && l < 31) l++;
+    m = (uint32_t)((((1ull << l) - d) << 32) / d + 1);
+  }
+  __device__ __forceinline__ uint32_t div(uint32_t n) const { return (__umulhi(n, m) + n) >> l; }
+};
 __device__ __forceinline__ void tma_load_2d(const CUtensorMap* tm, uint64_t* bar,
                                             void* dst, int x, int y) {
   asm volatile(
@@ -633,19 +659,20 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int kpt = S2D ? 4 : a.Kc / BK;  // s2d: kpt = the 4 dy boxes
   const int num_k1 = a.ntaps * kpt, num_k = num_k1 + a.kc2 / BK;  // + second K segment
   (void)num_m;
+  FastDiv div_outer, div_n;  // per_r (RESB) or per_m, and num_n
+  div_outer.init(RESB > 0 ? num_mt * num_n : gp.n * num_n);
+  div_n.init(num_n);
   auto coords = [&](int t, int& r, int& m0, int& n0) {
     if constexpr (RESB > 0) {
       // resident weights: replica-major, so a CTA's consecutive tiles (and
       // the units it steals, which follow launch order) rarely switch replica
-      const int per_r = num_mt * num_n;
-      r = t / per_r;
-      const int rem = t - r * per_r, mb = rem / num_n;
+      r = (int)div_outer.div(t);
+      const int rem = t - r * (int)div_outer.d, mb = (int)div_n.div(rem);
       m0 = mb * BMT + (int)crank * BM;
       n0 = (rem - mb * num_n) * BN;
     } else {
-      const int per_m = gp.n * num_n;
-      const int mb = t / per_m, rem = t - mb * per_m;
-      r = rem / num_n;
+      const int mb = (int)div_outer.div(t), rem = t - mb * (int)div_outer.d;
+      r = (int)div_n.div(rem);
       m0 = mb * BMT + (int)crank * BM;
       n0 = (rem - r * num_n) * BN;
     }
@@ -1087,7 +1114,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int my_orow =
           remap_row(a.M, a.rows_out, a.row_mode, a.H, a.W, m0 + q * 32 + lane, a.gh, a.gw);
 
-      mbar_wait(&tfull[acc], acc_phase);
+      mbar_wait_sleep(&tfull[acc], acc_phase);
       if (warp == 2) CG_TRACE(5, tile_i);
       tc_fence_after();
       // TMEM reads are software-pipelined: chunk c+2's tcgen05.ld is in flight
