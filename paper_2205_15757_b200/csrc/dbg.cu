@@ -102,11 +102,11 @@ extern "C" int cg_dbg_halo_trace2(cg_ctx* ctx, int B, int H, int C, int N, int B
     CG_CUDA(cudaMalloc(&dB, (size_t)N * 9 * C * 2));
     CG_CUDA(cudaMalloc(&dbias, (size_t)N * 4));
     CG_CUDA(cudaMalloc(&dout, (size_t)B * H * H * N * 2));
-    CG_CUDA(cudaMalloc(&dtr, 8 * 64 * 8));
+    CG_CUDA(cudaMalloc(&dtr, 16 * 64 * 8));
     CG_CUDA(cudaMemset(dA, 0x11, (size_t)rows * C * 2));
     CG_CUDA(cudaMemset(dB, 0x11, (size_t)N * 9 * C * 2));
     CG_CUDA(cudaMemset(dbias, 0, (size_t)N * 4));
-    CG_CUDA(cudaMemset(dtr, 0, 8 * 64 * 8));
+    CG_CUDA(cudaMemset(dtr, 0, 16 * 64 * 8));
     Operand oa, ob;
     make_operand(oa, dA, rows, C, 128 + 2 * (Hp + 1));
     make_operand(ob, dB, N, 9 * C, pair ? BN / 2 : BN);
@@ -140,7 +140,7 @@ extern "C" int cg_dbg_halo_trace2(cg_ctx* ctx, int B, int H, int C, int N, int B
     float ms = 0;
     CG_CUDA(cudaEventElapsedTime(&ms, e0, e1));
     *us = 1000.0 * ms / 5;
-    CG_CUDA(cudaMemcpy(trace_host, dtr, 8 * 64 * 8, cudaMemcpyDeviceToHost));
+    CG_CUDA(cudaMemcpy(trace_host, dtr, 16 * 64 * 8, cudaMemcpyDeviceToHost));
     cudaFree(dA);
     cudaFree(dB);
     cudaFree(dbias);
@@ -177,11 +177,11 @@ extern "C" int cg_dbg_gemm_trace_mode(cg_ctx* ctx, int M, int N, int K, int BN, 
                                 ? (size_t)(M / (H * H)) * (H + 1) * (H + 1) + H + 2
                                 : (size_t)M;
     CG_CUDA(cudaMalloc(&dout, out_rows * N * 2));
-    CG_CUDA(cudaMalloc(&dtr, 8 * 64 * 8));
+    CG_CUDA(cudaMalloc(&dtr, 16 * 64 * 8));
     CG_CUDA(cudaMemset(dA, 0x11, (size_t)M * K * 2));
     CG_CUDA(cudaMemset(dB, 0x11, (size_t)N * K * 2));
     CG_CUDA(cudaMemset(dbias, 0, (size_t)N * 4));
-    CG_CUDA(cudaMemset(dtr, 0, 8 * 64 * 8));
+    CG_CUDA(cudaMemset(dtr, 0, 16 * 64 * 8));
     if (residual) {
       CG_CUDA(cudaMalloc(&dres, (size_t)M * N * 2));
       CG_CUDA(cudaMemset(dres, 0x11, (size_t)M * N * 2));
@@ -220,7 +220,7 @@ extern "C" int cg_dbg_gemm_trace_mode(cg_ctx* ctx, int M, int N, int K, int BN, 
     float ms = 0;
     CG_CUDA(cudaEventElapsedTime(&ms, e0, e1));
     *us = 1000.0 * ms / 5;
-    CG_CUDA(cudaMemcpy(trace_host, dtr, 8 * 64 * 8, cudaMemcpyDeviceToHost));
+    CG_CUDA(cudaMemcpy(trace_host, dtr, 16 * 64 * 8, cudaMemcpyDeviceToHost));
     cudaFree(dA);
     cudaFree(dB);
     cudaFree(dbias);

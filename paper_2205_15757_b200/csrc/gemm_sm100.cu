@@ -1283,7 +1283,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (warp == 2) CG_TRACE(6, tile_i);
       if (warp == 9) CG_TRACE(7, tile_i);
-      if (S2D) CG_TRACE(8 + warp - 2, tile_i);  // dbg: every epilogue warp's end
+      CG_TRACE(8 + warp - 2, tile_i);  // every epilogue warp's end (trace buffers: 16 x 64)
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
     if (tma_out && lane == 0) bulk_wait_all();  // this warp's stores read their staging

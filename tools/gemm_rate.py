@@ -41,7 +41,7 @@ only = sys.argv[1] if len(sys.argv) > 1 else None  # run one shape (for ncu)
 for label, M, N, K, BN, res in shapes:
     if only and label != only:
         continue
-    tr = np.zeros(8 * 64, np.int64)
+    tr = np.zeros(16 * 64, np.int64)
     us = C.c_double()
     rc = f(ctx.h, M, N, K, BN, res, 0, 0, tr.ctypes.data_as(C.c_void_p), C.byref(us))
     assert rc == 0, rc
@@ -57,7 +57,7 @@ for label, M, N, K, BN, res in shapes:
     torch.cuda.synchronize()
     tus = e0.elapsed_time(e1) * 100
     fl = 2.0 * M * N * K
-    t = tr.reshape(8, 64)
+    t = tr.reshape(16, 64)
     n = int((t[0] > 0).sum())
     c = t[4, :n]
     per = np.diff(c).mean() if n > 2 else 0
@@ -66,7 +66,8 @@ for label, M, N, K, BN, res in shapes:
           f"(MMA floor {K // 16 * BN // 2} cyc)")
     if "l4 c3" in label or "l3 c3" in label or label.startswith("l1"):
         t0 = t[t > 0].min()
-        print("tile " + " ".join(f"{x:>8s}" for x in names))
-        for i in range(min(n, 6)):
-            print(f"{i:4d} " + " ".join(f"{(t[j, i] - t0) if t[j, i] else -1:8d}" for j in range(8)))
+        print("tile " + " ".join(f"{x:>8s}" for x in names) + "  | end of epilogue warps 2..9 - t0")
+        for i in range(min(n, 8)):
+            print(f"{i:4d} " + " ".join(f"{(t[j, i] - t0) if t[j, i] else -1:8d}" for j in range(8))
+                  + " | " + " ".join(f"{(t[8 + w, i] - t0) if t[8 + w, i] else -1:6d}" for w in range(8)))
     del a, b

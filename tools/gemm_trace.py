@@ -21,12 +21,12 @@ for name, M, N, K, res in shapes:
     for BN in (64, 128, 256):
         if BN > N:
             continue
-        tr = np.zeros(8 * 64, np.int64)
+        tr = np.zeros(16 * 64, np.int64)
         us = C.c_double()
         rc = f(ctx.h, M, N, K, BN, res, tr.ctypes.data_as(C.c_void_p), C.byref(us))
         assert rc == 0
         byts = M * K * 2 + M * N * 2 * (2 if res else 1)
-        t = tr.reshape(8, 64)
+        t = tr.reshape(16, 64)
         n = int((t[0] > 0).sum())
         t = t[:, :n] - t[0, 0]
         per_tile = np.diff(t[6]).mean() if n > 2 else 0

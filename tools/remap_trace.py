@@ -17,11 +17,11 @@ H = 56
 for label, M, N, K, BN, mode in (("l1.0 c1 K64 N64 identity", 128 * H * H, 64, 64, 64, 0),
                                  ("l1.0 c1 K64 N64 CompactToPad", 128 * H * H, 64, 64, 64, 2),
                                  ("l1.1 c1 K256 N64 CompactToPad", 128 * H * H, 64, 256, 64, 2)):
-    tr = np.zeros(8 * 64, np.int64)
+    tr = np.zeros(16 * 64, np.int64)
     us = C.c_double()
     rc = f(ctx.h, M, N, K, BN, 0, mode, H, tr.ctypes.data_as(C.c_void_p), C.byref(us))
     assert rc == 0, rc
-    t = tr.reshape(8, 64)
+    t = tr.reshape(16, 64)
     n = int((t[0] > 0).sum())
     t0 = t[t > 0].min()
     byts = M * K * 2 + M * N * 2
