@@ -578,6 +578,7 @@ struct TileSched {
 template <int BN, int STAGES, int kResSlots, int HALO, int RESB, int PAIR>
 constexpr int stg_floats() {
   if (!PAIR && BN == 256 && STAGES == 2 && kResSlots == 12) return 1024;  // residual: 6 boxes
+  if (!PAIR && BN == 64 && kResSlots) return 1280;  // 1024-aligned (see below)
   if (PAIR || kResSlots) return 32 * kStgLd;
   if (HALO == 0 && ((BN == 256 && STAGES == 4) || (BN == 128 && STAGES == 6) ||
                     (BN == 64 && STAGES == 8)))
@@ -585,6 +586,10 @@ constexpr int stg_floats() {
   if ((BN == 256 && STAGES == 4 && HALO == 2) || (BN == 128 && STAGES == 8 && HALO == 2) ||
       (BN == 64 && STAGES == 8 && HALO == 4) || (BN == 64 && RESB == 9 && HALO == 4))
     return 0;
+  // 64-wide tiles: one 32 x 128 B staging block per warp, 1024-aligned for
+  // the 128B-swizzled bulk store (the s2d stem: 4 KB exactly)
+  if (BN == 64 && RESB == 4 && HALO == 12) return 1024;
+  if (BN == 64) return 1280;
   return 32 * kStgLd;
 }
 
@@ -1122,11 +1127,67 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t trow =
           tmem + ((uint32_t)(q * 32) << 16) + acc * BN * kSubTiles + (S2D ? h * BN : 0);
       uint32_t v[32];
+      // (the staging-free halo variants never take the identity-row path)
+      if constexpr (C0S == 1 && CPT == 2 && !PAIR && kStgWarp > 0) {
+        static_assert((kStgWarp * 4) % 1024 == 0, "64-wide tiles: 1024-aligned staging");
+        if (tma_out && !res_tma) {
+          // 64-wide tiles drained whole by one warp (identity rows): both
+          // chunks' TMEM loads in flight together, one staging buffer of
+          // 32 rows x 128 B (128B swizzle), one fence and ONE bulk store
+          uint32_t w[32];
+          tmem_ld32_issue(trow, v);
+          tmem_ld32_issue(trow + 32, w);
+          tmem_ld_wait(v);
+          tmem_ld_wait(w);
+          if (S2D && warp == 2) CG_TRACE(1, tile_i);  // dbg: TMEM loads landed
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[acc]);
+          uint32_t o[32];
+          float x[32];
+#pragma unroll
+          for (int j = 0; j < 8; j++) {
+            const float4 b4 = __ldg(reinterpret_cast<const float4*>(bias_r + n0) + j);
+            x[4 * j] = __uint_as_float(v[4 * j]) + b4.x;
+            x[4 * j + 1] = __uint_as_float(v[4 * j + 1]) + b4.y;
+            x[4 * j + 2] = __uint_as_float(v[4 * j + 2]) + b4.z;
+            x[4 * j + 3] = __uint_as_float(v[4 * j + 3]) + b4.w;
+          }
+          act_pack<16>(x, o, a.relu);
+#pragma unroll
+          for (int j = 0; j < 8; j++) {
+            const float4 b4 = __ldg(reinterpret_cast<const float4*>(bias_r + n0 + 32) + j);
+            x[4 * j] = __uint_as_float(w[4 * j]) + b4.x;
+            x[4 * j + 1] = __uint_as_float(w[4 * j + 1]) + b4.y;
+            x[4 * j + 2] = __uint_as_float(w[4 * j + 2]) + b4.z;
+            x[4 * j + 3] = __uint_as_float(w[4 * j + 3]) + b4.w;
+          }
+          act_pack<16>(x, o + 16, a.relu);
+          if (lane == 0) bulk_wait_read<0>();  // the previous tile's store read its buffer
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 8; j++)
+            sts_v4(stg_a + (uint32_t)(lane * 128 + ((j ^ (lane & 7)) << 4)), o[4 * j],
+                   o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
+          fence_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&gp.O[r_], stg_a, n0, m0 + q * 32);
+            bulk_commit();
+          }
+          if (warp == 2) CG_TRACE(6, tile_i);
+          if (warp == 9) CG_TRACE(7, tile_i);
+          CG_TRACE(8 + warp - 2, tile_i);
+          if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+          continue;
+        }
+      }
       if (c_first < CPT) tmem_ld32_issue(trow + c_first * 32, v);
 #pragma unroll 1
       for (int c = c_first; c < CPT; c += C0S) {
         const int g = tile_i * CPT + c;
         tmem_ld_wait(v);
+        if (S2D && warp == 2 && c == c_first) CG_TRACE(1, tile_i);  // dbg: first TMEM load landed
         if (c + C0S >= CPT) {  // this warp's last chunk: hand TMEM back early
           tc_fence_before();
           __syncwarp();
@@ -1675,6 +1736,20 @@ static void map64(CUtensorMap& m, const void* p, int ld, int rows, int box_rows)
   if (r != CUDA_SUCCESS) throw CudaError("epilogue tensor map failed");
 }
 
+// [rows, ld] bf16 map with a 64-column x 32-row box, 128B swizzle: a warp's
+// whole 32 x 64 output block of a 64-wide tile in one bulk store.
+static void map_out128(CUtensorMap& m, const void* p, int ld, int rows) {
+  cuuint64_t dims[2] = {(cuuint64_t)ld, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+  cuuint32_t box[2] = {64, 32};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = get_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(p), dims,
+                            strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw CudaError("epilogue tensor map failed");
+}
+
 // [rows, ld] bf16 map with a 64-column x 128-row box, 128B swizzle: the
 // residual ring's boxes.
 static void map128_res(CUtensorMap& m, const void* p, int ld, int rows) {
@@ -1738,7 +1813,10 @@ void prepare_conv_gemm(PreparedGemm& p, const ConvGemmGroup& g, const ConvGemmAr
     if (tma_out) {
       if (a.ld_out % 8 || reinterpret_cast<uintptr_t>(g.out[r]) % 16)
         throw InvalidArgument("conv_gemm: output must be 16B aligned");
-      map64(p.gp.O[r], g.out[r], a.ld_out, a.rows_out, 32);
+      // 64-wide tiles without a residual: the kernel's one-store-per-warp path
+      if (BN == 64 && !a.pair && !g.residual[r])
+        map_out128(p.gp.O[r], g.out[r], a.ld_out, a.rows_out);
+      else map64(p.gp.O[r], g.out[r], a.ld_out, a.rows_out, 32);
       if (g.residual[r]) {
         if (a.ld_res % 8 || reinterpret_cast<uintptr_t>(g.residual[r]) % 16)
           throw InvalidArgument("conv_gemm: residual must be 16B aligned");

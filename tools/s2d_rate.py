@@ -13,7 +13,7 @@ from paper_2205_15757_b200 import Context  # noqa: E402
 ctx = Context(0)
 B = int(sys.argv[1]) if len(sys.argv) > 1 else 128
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
-names = ["prod", "p_stage", "mma_go", "data", "commit", "epi_go", "epi_end2", "epi_end9"]
+names = ["prod", "ld0_w2", "mma_go", "data", "commit", "epi_go", "epi_end2", "epi_end9"]
 tr = np.zeros(16 * 64, np.int64)
 us = C.c_double()
 rc = ctx.L.cg_dbg_s2d_trace(ctx.h, B, 224, reps, tr.ctypes.data_as(C.c_void_p), C.byref(us))
