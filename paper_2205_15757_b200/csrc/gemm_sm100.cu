@@ -1130,10 +1130,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       // (the staging-free halo variants never take the identity-row path)
       if constexpr (C0S == 1 && CPT == 2 && !PAIR && kStgWarp > 0) {
         static_assert((kStgWarp * 4) % 1024 == 0, "64-wide tiles: 1024-aligned staging");
-        if (tma_out && !res_tma) {
-          // 64-wide tiles drained whole by one warp (identity rows): both
-          // chunks' TMEM loads in flight together, one staging buffer of
-          // 32 rows x 128 B (128B swizzle), one fence and ONE bulk store
+        const bool remap_fast = !tma_out && kDirectRemap && !a.out_f32 && !res_r;
+        if ((tma_out && !res_tma) || remap_fast) {
+          // 64-wide tiles drained whole by one warp: both chunks' TMEM loads
+          // in flight together, one staging buffer of 32 rows x 128 B (128B
+          // swizzle). Identity rows: one fence and ONE bulk store. Remapped
+          // rows: read back 4 rows x 128 B per instruction (8 lanes a row),
+          // so every 16-byte store instruction writes 4 whole 128-byte lines
+          // instead of 32 rows' 16-byte pieces.
           uint32_t w[32];
           tmem_ld32_issue(trow, v);
           tmem_ld32_issue(trow + 32, w);
@@ -1156,7 +1160,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           act_pack<16>(x, o, a.relu);
 #pragma unroll
           for (int j = 0; j < 8; j++) {
-            const float4 b4 = __ldg(reinterpret_cast<const float4*>(bias_r + n0 + 32) + j);
+            const float4 b4 = n0 + 32 < a.N
+                                  ? __ldg(reinterpret_cast<const float4*>(bias_r + n0 + 32) + j)
+                                  : make_float4(0.f, 0.f, 0.f, 0.f);
             x[4 * j] = __uint_as_float(w[4 * j]) + b4.x;
             x[4 * j + 1] = __uint_as_float(w[4 * j + 1]) + b4.y;
             x[4 * j + 2] = __uint_as_float(w[4 * j + 2]) + b4.z;
@@ -1169,11 +1175,24 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int j = 0; j < 8; j++)
             sts_v4(stg_a + (uint32_t)(lane * 128 + ((j ^ (lane & 7)) << 4)), o[4 * j],
                    o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
-          fence_async_smem();
-          __syncwarp();
-          if (lane == 0) {
-            tma_store_2d(&gp.O[r_], stg_a, n0, m0 + q * 32);
-            bulk_commit();
+          if (remap_fast) {
+            __syncwarp();
+            const int ch = lane & 7, n = n0 + ch * 8;
+#pragma unroll
+            for (int it = 0; it < 8; it++) {
+              const int row = it * 4 + (lane >> 3);
+              const uint4 val = lds_u4(stg_a + (uint32_t)(row * 128 + ((ch ^ (row & 7)) << 4)));
+              const int orow = __shfl_sync(0xffffffffu, my_orow, row);
+              if (orow >= 0 && n < a.N)
+                stg_u4(reinterpret_cast<__nv_bfloat16*>(out_r) + (size_t)orow * a.ld_out + n, val);
+            }
+          } else {
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(&gp.O[r_], stg_a, n0, m0 + q * 32);
+              bulk_commit();
+            }
           }
           if (warp == 2) CG_TRACE(6, tile_i);
           if (warp == 9) CG_TRACE(7, tile_i);
