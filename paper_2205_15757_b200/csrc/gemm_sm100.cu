@@ -1127,71 +1127,88 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t trow =
           tmem + ((uint32_t)(q * 32) << 16) + acc * BN * kSubTiles + (S2D ? h * BN : 0);
       uint32_t v[32];
-      // (the staging-free halo variants never take the identity-row path)
-      if constexpr (C0S == 1 && CPT == 2 && !PAIR && kStgWarp > 0) {
-        static_assert((kStgWarp * 4) % 1024 == 0, "64-wide tiles: 1024-aligned staging");
+      // 64-column blocks drained whole by one warp (the staging-free halo
+      // variants never take these paths): both 32-column TMEM loads of a
+      // block in flight together, one 32 x 128 B staging buffer (rows
+      // XOR-swizzled in 16-byte units, the TMA 128B pattern).
+      //  * identity rows, 64-wide tiles: one fence and ONE bulk store;
+      //  * remapped rows (any width; group h takes blocks h, h + 2, ...):
+      //    read back 4 rows x 128 B per instruction (8 lanes a row), so each
+      //    16-byte store instruction writes 4 whole 128-byte row segments
+      //    instead of 32 rows' 16-byte pieces.
+      constexpr bool kWhole = C0S == 1 && CPT == 2;
+      if constexpr (!PAIR && kStgWarp >= 1024 && (kWhole || C0S == 2)) {
+        if constexpr (kWhole)
+          static_assert((kStgWarp * 4) % 1024 == 0, "64-wide tiles: 1024-aligned staging");
         const bool remap_fast = !tma_out && kDirectRemap && !a.out_f32 && !res_r;
-        if ((tma_out && !res_tma) || remap_fast) {
-          // 64-wide tiles drained whole by one warp: both chunks' TMEM loads
-          // in flight together, one staging buffer of 32 rows x 128 B (128B
-          // swizzle). Identity rows: one fence and ONE bulk store. Remapped
-          // rows: read back 4 rows x 128 B per instruction (8 lanes a row),
-          // so every 16-byte store instruction writes 4 whole 128-byte lines
-          // instead of 32 rows' 16-byte pieces.
-          uint32_t w[32];
-          tmem_ld32_issue(trow, v);
-          tmem_ld32_issue(trow + 32, w);
-          tmem_ld_wait(v);
-          tmem_ld_wait(w);
-          if (S2D && warp == 2) CG_TRACE(1, tile_i);  // dbg: TMEM loads landed
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty[acc]);
-          uint32_t o[32];
-          float x[32];
-#pragma unroll
-          for (int j = 0; j < 8; j++) {
-            const float4 b4 = __ldg(reinterpret_cast<const float4*>(bias_r + n0) + j);
-            x[4 * j] = __uint_as_float(v[4 * j]) + b4.x;
-            x[4 * j + 1] = __uint_as_float(v[4 * j + 1]) + b4.y;
-            x[4 * j + 2] = __uint_as_float(v[4 * j + 2]) + b4.z;
-            x[4 * j + 3] = __uint_as_float(v[4 * j + 3]) + b4.w;
-          }
-          act_pack<16>(x, o, a.relu);
-#pragma unroll
-          for (int j = 0; j < 8; j++) {
-            const float4 b4 = n0 + 32 < a.N
-                                  ? __ldg(reinterpret_cast<const float4*>(bias_r + n0 + 32) + j)
-                                  : make_float4(0.f, 0.f, 0.f, 0.f);
-            x[4 * j] = __uint_as_float(w[4 * j]) + b4.x;
-            x[4 * j + 1] = __uint_as_float(w[4 * j + 1]) + b4.y;
-            x[4 * j + 2] = __uint_as_float(w[4 * j + 2]) + b4.z;
-            x[4 * j + 3] = __uint_as_float(w[4 * j + 3]) + b4.w;
-          }
-          act_pack<16>(x, o + 16, a.relu);
-          if (lane == 0) bulk_wait_read<0>();  // the previous tile's store read its buffer
-          __syncwarp();
-#pragma unroll
-          for (int j = 0; j < 8; j++)
-            sts_v4(stg_a + (uint32_t)(lane * 128 + ((j ^ (lane & 7)) << 4)), o[4 * j],
-                   o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
-          if (remap_fast) {
-            __syncwarp();
-            const int ch = lane & 7, n = n0 + ch * 8;
-#pragma unroll
-            for (int it = 0; it < 8; it++) {
-              const int row = it * 4 + (lane >> 3);
-              const uint4 val = lds_u4(stg_a + (uint32_t)(row * 128 + ((ch ^ (row & 7)) << 4)));
-              const int orow = __shfl_sync(0xffffffffu, my_orow, row);
-              if (orow >= 0 && n < a.N)
-                stg_u4(reinterpret_cast<__nv_bfloat16*>(out_r) + (size_t)orow * a.ld_out + n, val);
+        if ((kWhole && tma_out && !res_tma) || remap_fast) {
+          constexpr int kBlk = BN / 64, kBStep = kWhole ? 1 : 2;
+#pragma unroll 1
+          for (int b = kWhole ? 0 : h; b < kBlk; b += kBStep) {
+            const uint32_t tb = trow + (uint32_t)(b * 64);
+            const int nb = n0 + b * 64;
+            uint32_t w[32];
+            tmem_ld32_issue(tb, v);
+            tmem_ld32_issue(tb + 32, w);
+            tmem_ld_wait(v);
+            tmem_ld_wait(w);
+            if (S2D && warp == 2) CG_TRACE(1, tile_i);  // dbg: TMEM loads landed
+            if (b + kBStep >= kBlk) {  // this warp's last block: hand TMEM back early
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&tempty[acc]);
             }
-          } else {
-            fence_async_smem();
+            uint32_t o[32];
+            float x[32];
+#pragma unroll
+            for (int j = 0; j < 8; j++) {
+              const float4 b4 = nb < a.N
+                                    ? __ldg(reinterpret_cast<const float4*>(bias_r + nb) + j)
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+              x[4 * j] = __uint_as_float(v[4 * j]) + b4.x;
+              x[4 * j + 1] = __uint_as_float(v[4 * j + 1]) + b4.y;
+              x[4 * j + 2] = __uint_as_float(v[4 * j + 2]) + b4.z;
+              x[4 * j + 3] = __uint_as_float(v[4 * j + 3]) + b4.w;
+            }
+            act_pack<16>(x, o, a.relu);
+#pragma unroll
+            for (int j = 0; j < 8; j++) {
+              const float4 b4 = nb + 32 < a.N
+                                    ? __ldg(reinterpret_cast<const float4*>(bias_r + nb + 32) + j)
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+              x[4 * j] = __uint_as_float(w[4 * j]) + b4.x;
+              x[4 * j + 1] = __uint_as_float(w[4 * j + 1]) + b4.y;
+              x[4 * j + 2] = __uint_as_float(w[4 * j + 2]) + b4.z;
+              x[4 * j + 3] = __uint_as_float(w[4 * j + 3]) + b4.w;
+            }
+            act_pack<16>(x, o + 16, a.relu);
+            if (!remap_fast && lane == 0) bulk_wait_read<0>();  // last store read its buffer
             __syncwarp();
-            if (lane == 0) {
-              tma_store_2d(&gp.O[r_], stg_a, n0, m0 + q * 32);
-              bulk_commit();
+#pragma unroll
+            for (int j = 0; j < 8; j++)
+              sts_v4(stg_a + (uint32_t)(lane * 128 + ((j ^ (lane & 7)) << 4)), o[4 * j],
+                     o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
+            if (remap_fast) {
+              __syncwarp();
+              const int ch = lane & 7, n = nb + ch * 8;
+#pragma unroll
+              for (int it = 0; it < 8; it++) {
+                const int row = it * 4 + (lane >> 3);
+                const uint4 val =
+                    lds_u4(stg_a + (uint32_t)(row * 128 + ((ch ^ (row & 7)) << 4)));
+                const int orow = __shfl_sync(0xffffffffu, my_orow, row);
+                if (orow >= 0 && n < a.N)
+                  stg_u4(reinterpret_cast<__nv_bfloat16*>(out_r) + (size_t)orow * a.ld_out + n,
+                         val);
+              }
+              __syncwarp();  // staging read back before the next block rewrites it
+            } else {
+              fence_async_smem();
+              __syncwarp();
+              if (lane == 0) {
+                tma_store_2d(&gp.O[r_], stg_a, nb, m0 + q * 32);
+                bulk_commit();
+              }
             }
           }
           if (warp == 2) CG_TRACE(6, tile_i);
