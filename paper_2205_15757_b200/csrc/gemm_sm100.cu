@@ -416,48 +416,61 @@ __device__ __forceinline__ uint32_t sw64(int r, int j) {
   return (uint32_t)(r * 64 + 16 * (j ^ ((r >> 1) & 3)));
 }
 
-__device__ __forceinline__ int remap_row(int M, int rows_out, int mode, int H,
-                                         int W, int m, int gh = 0, int gw = 0) {
-  if (m >= M) return -1;
-  if (mode == kRowIdentity) return m < rows_out ? m : -1;
-  if (mode == kRowGridToCompact) {  // per-image gh x gw grid, output H x W
-    const int G = gh * gw, n = m / G, rem = m - n * G, i = rem / gw, j = rem - i * gw;
-    return (i < H && j < W) ? (n * H + i) * W + j : -1;
+// Output row of GEMM row m under ConvGemmArgs::row_mode (-1: not stored),
+// the mode's two divisors as multiply-high divisions set up once per thread
+// (the epilogue maps one row per thread per tile).
+// Zero-bordered pixel grid with shared borders: each grid row is W pixels
+// plus one zero column (the right border of a row is the left border of the
+// next), each image H + 1 grid rows of which row 0 is zero (the bottom
+// border of the image above). Pixel (n, h, w) sits at grid row
+// n (H+1)(W+1) + (h+1)(W+1) + w; the 3x3 taps are shifts by
+// (dr-1)(W+1) + (ds-1); index -1 (top-left of image 0) and the rows past the
+// last image are TMA out-of-bounds zeros. (H+1)(W+1) rows per image instead
+// of (H+2)(W+2): 21 % fewer MMA rows at 7x7.
+struct RowRemap {
+  FastDiv d1, d2;
+  int mode, M, rows_out, H, W, Bn;
+  __device__ __forceinline__ void init(const ConvGemmArgs& a) {
+    mode = a.row_mode;
+    M = a.M;
+    rows_out = a.rows_out;
+    H = a.H;
+    W = a.W;
+    Bn = 0;
+    switch (mode) {
+      case kRowGridToCompact: d1.init(a.gh * a.gw); d2.init(a.gw); break;
+      case kRowPhaseGridToCompact:
+      case kRowPadToCompact:
+      case kRowPadToPad: d1.init((H + 1) * (W + 1)); d2.init(W + 1); break;
+      case kRowCompactToPhasePad:
+      case kRowCompactToPad:
+        d1.init(H * W);
+        d2.init(W);
+        Bn = M / (H * W);
+        break;
+      default: d1.init(1); d2.init(1);
+    }
   }
-  if (mode == kRowPhaseGridToCompact) {  // H, W = output dims, grid (H+1)(W+1)
-    const int Wq = W + 1, HqWq = (H + 1) * Wq;
-    const int n = m / HqWq, rem = m - n * HqWq, i = rem / Wq, j = rem - i * Wq;
-    return (i < H && j < W) ? (n * H + i) * W + j : -1;
+  __device__ __forceinline__ int map(int m) const {
+    if (m >= M) return -1;
+    if (mode == kRowIdentity) return m < rows_out ? m : -1;
+    const int n = (int)d1.div(m), rem = m - n * (int)d1.d;
+    const int i = (int)d2.div(rem), j = rem - i * (int)d2.d;
+    switch (mode) {
+      case kRowGridToCompact:
+      case kRowPhaseGridToCompact: return (i < H && j < W) ? (n * H + i) * W + j : -1;
+      case kRowCompactToPhasePad: {
+        const int h = i + 1, w = j + 1, Hq = (H + 2) >> 1, Wq = (W + 2) >> 1;
+        return ((((h & 1) * 2 + (w & 1)) * Bn + n) * Hq + (h >> 1)) * Wq + (w >> 1);
+      }
+      case kRowPadToCompact:
+      case kRowPadToPad:
+        if (i < 1 || j >= W) return -1;
+        return mode == kRowPadToPad ? m : (n * H + i - 1) * W + j;
+      default: return (n * (H + 1) + i + 1) * (W + 1) + j;  // compact -> shared-border grid
+    }
   }
-  if (mode == kRowCompactToPhasePad) {
-    // compact (n, h, w) -> padded (h+1, w+1) -> plane (row & 1, col & 1) of
-    // the phase-split zero-bordered grid; planes stacked ab-major, image next
-    const int HW = H * W, Bn = M / HW;
-    const int n = m / HW, rem = m - n * HW;
-    const int h = rem / W + 1, w = rem - (rem / W) * W + 1;
-    const int Hq = (H + 2) >> 1, Wq = (W + 2) >> 1;
-    return ((((h & 1) * 2 + (w & 1)) * Bn + n) * Hq + (h >> 1)) * Wq + (w >> 1);
-  }
-  // Zero-bordered pixel grid with shared borders: each grid row is W pixels
-  // plus one zero column (the right border of a row is the left border of
-  // the next), each image H + 1 grid rows of which row 0 is zero (the bottom
-  // border of the image above). Pixel (n, h, w) sits at grid row
-  // n (H+1)(W+1) + (h+1)(W+1) + w; the 3x3 taps are shifts by
-  // (dr-1)(W+1) + (ds-1); index -1 (top-left of image 0) and the rows past
-  // the last image are TMA out-of-bounds zeros. (H+1)(W+1) rows per image
-  // instead of (H+2)(W+2): 21 % fewer MMA rows at 7x7.
-  const int Wp = W + 1, HpWp = (H + 1) * Wp;
-  if (mode == kRowPadToCompact || mode == kRowPadToPad) {
-    int img = m / HpWp, rem = m - img * HpWp;
-    int hp = rem / Wp, wp = rem - hp * Wp;
-    if (hp < 1 || wp >= W) return -1;
-    return mode == kRowPadToPad ? m : (img * H + hp - 1) * W + wp;
-  }
-  const int HW = H * W;
-  int img = m / HW, rem = m - img * HW;
-  int h = rem / W, w = rem - h * W;
-  return img * HpWp + (h + 1) * Wp + w;
-}
+};
 
 // ------------------------------------------------------------ tile scheduler
 // The work of a launch is `units` runs of T consecutive tiles.
@@ -1095,6 +1108,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     // each of the same tile; wider tiles split chunks between the groups.
     // s2d stem (256-row tiles): group h drains sub-tile h, both chunks.
     constexpr int C0S = (kTileSplit || S2D) ? 1 : 2;  // chunk stride of one warp
+    RowRemap rowmap;
+    rowmap.init(a);
     int tile_i = 0, acc = 0;
     int stage_seq = 0;  // staging buffer sequence across all of this warp's chunks
     uint32_t acc_phase = 0;
@@ -1117,7 +1132,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const __nv_bfloat16* res_r = gp.residual[r_];
       void* out_r = gp.out[r_];
       const int my_orow =
-          remap_row(a.M, a.rows_out, a.row_mode, a.H, a.W, m0 + q * 32 + lane, a.gh, a.gw);
+          rowmap.map(m0 + q * 32 + lane);
 
       mbar_wait_sleep(&tfull[acc], acc_phase);
       if (warp == 2) CG_TRACE(5, tile_i);
@@ -1440,6 +1455,9 @@ const int g_pdl = std::getenv("CREDO_NO_PDL") == nullptr ? 1 : 0;
 const bool g_clc = std::getenv("CREDO_NO_CLC") == nullptr;
 // env CREDO_NO_STG4=1: 3 stages for every streamed 256-wide GEMM (A/B)
 const bool g_stg4 = std::getenv("CREDO_NO_STG4") == nullptr;
+// env CREDO_HALO_STAGED=1: remapped halo convs keep epilogue staging (the
+// staged 128-byte-row store path) instead of a deeper halo ring (A/B)
+const bool g_halo_deep = std::getenv("CREDO_HALO_STAGED") == nullptr;
 const double g_unit_ns = std::getenv("CREDO_CLC_UNIT_NS") ? std::atof(std::getenv("CREDO_CLC_UNIT_NS"))
                                                           : 1500.0;
 
@@ -1895,15 +1913,16 @@ void launch_prepared(const PreparedGemm& p, cudaStream_t st, int max_ctas) {
     // small weight sets (one n block, 9 x 64-channel taps): keep B resident
     if (p.BN == 64 && p.args.N <= 64 && p.args.Kc == 64 && p.args.ntaps == 9 &&
         std::getenv("CREDO_NO_RESB") == nullptr) {
-      if (!p.args.out_f32 && p.args.row_mode != kRowIdentity && kDirectRemap && g_stg4)
+      if (!p.args.out_f32 && p.args.row_mode != kRowIdentity && kDirectRemap && g_stg4 &&
+          g_halo_deep)
         launch_t<64, 1, 0, 4, 9>(p, st, max_ctas);  // no staging: a 4th halo slot
       else
         launch_t<64, 1, 0, 3, 9>(p, st, max_ctas);
       return;
     }
     // remapped bf16 rows leave the epilogue staging unused: deeper halo rings
-    const bool deep_halo =
-        !p.args.out_f32 && p.args.row_mode != kRowIdentity && kDirectRemap && g_stg4;
+    const bool deep_halo = !p.args.out_f32 && p.args.row_mode != kRowIdentity && kDirectRemap &&
+                           g_stg4 && g_halo_deep;
     switch (p.BN) {
       case 64:
         if (deep_halo) launch_t<64, 8, 0, 4>(p, st, max_ctas);
