@@ -11,7 +11,10 @@ for r in rows:
         hdr = r
         continue
     if hdr and len(r) == len(hdr):
-        data.append(dict(zip(hdr, r)))
+        d = dict(zip(hdr, r))
+        # CSVs with several metrics per launch: keep the duration rows
+        if d.get("Metric Name", "gpu__time_duration.sum") == "gpu__time_duration.sum":
+            data.append(d)
 start = sys.argv[2] if len(sys.argv) > 2 and not sys.argv[2].startswith("-") else None
 starts = [start] if start else ["chw_to_s2d16", "conv1_im2col"]
 idx = [i for i, d in enumerate(data) if any(x in d["Kernel Name"] for x in starts)]

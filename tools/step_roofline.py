@@ -6,7 +6,10 @@ with the measured peaks (MEASURED_PEAKS.json); launch order = csrc/cnn.cu
 ResNet::ops (conv1, per block c1, c2, c3 (+ the projection shortcut in each
 stage's first block), fc).
 
-  python tools/step_roofline.py <ncu.csv> [B] [replicas]
+  python tools/step_roofline.py <ncu.csv> [B] [replicas] [--json traffic.json]
+
+--json writes the step's GEMM DRAM traffic summary that bench.py reports as
+roofline.traffic (profiles/r02_gemm_step_traffic.json).
 """
 import collections
 import csv
@@ -47,9 +50,15 @@ def plan(B, R, S=224):
 
 
 def main():
-    path = sys.argv[1]
-    B = int(sys.argv[2]) if len(sys.argv) > 2 else 128
-    R = int(sys.argv[3]) if len(sys.argv) > 3 else 3
+    argv = list(sys.argv[1:])
+    out_json = None
+    if "--json" in argv:
+        k = argv.index("--json")
+        out_json = argv[k + 1]
+        del argv[k:k + 2]
+    path = argv[0]
+    B = int(argv[1]) if len(argv) > 1 else 128
+    R = int(argv[2]) if len(argv) > 2 else 3
     pk = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     bw, fl = pk["hbm_gbs"] * 1e9, pk.get("bf16_tflops_sustained", pk["bf16_tflops"]) * 1e12
     rows = list(csv.reader(open(path)))
@@ -74,8 +83,10 @@ def main():
     per = collections.OrderedDict(enumerate(gem))
     print(f"{'launch':30s} {'us':>7s} {'floor':>7s} {'eff':>5s} {'TFLOP/s':>8s} "
           f"{'DRAM TB/s':>9s} {'traffic/compulsory':>9s}")
-    T = F = 0.0
+    T = F = RD = WR = 0.0
     for (name, f, b), d in zip(P, per.values()):
+        RD += d["dram__bytes_read.sum"]
+        WR += d["dram__bytes_write.sum"]
         t = d["gpu__time_duration.sum"]
         traffic = d["dram__bytes_read.sum"] + d["dram__bytes_write.sum"]
         floor = max(f / fl, b / bw) * 1e6
@@ -85,6 +96,18 @@ def main():
               f"{traffic / t / 1e6:9.2f} {traffic / b:9.2f}")
     print(f"{'TOTAL':30s} {T:7.1f} {F:7.1f} {F / T:5.2f}   (peaks: {fl / 1e12:.0f} TFLOP/s, "
           f"{bw / 1e12:.2f} TB/s)")
+    if out_json:
+        with open(out_json, "w") as fo:
+            json.dump({"launches": len(P), "gemm_us_per_step_ncu": round(T, 1),
+                       "dram_read_bytes_per_step": RD, "dram_write_bytes_per_step": WR,
+                       "traffic_bytes_per_step": RD + WR,
+                       "traffic_bytes_per_launch_avg": (RD + WR) / len(P),
+                       "source": "ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,"
+                                 "dram__bytes_write.sum --clock-control none of bench.py --profile: "
+                                 f"the {len(P)} conv_gemm launches of one C2 step (3 replicas "
+                                 "grouped, final round-2 build), cold-cache serialised "
+                                 f"({os.path.relpath(path, ROOT)})"}, fo, indent=1)
+            fo.write("\n")
 
 
 if __name__ == "__main__":
