@@ -329,6 +329,15 @@ def bench_gpu(args, rank, world, local_rank):
     with ClockSampler(local_rank) as clk:
         ms, host_ms, sats, labs = pipeline(grp, ctx, dev_batches, args.steps, D, LAG, stream)
     launches = round((ctx.launch_count() - l0) / args.steps)
+    if world > 1:  # per-rank device times and SM clocks (stderr; the line reports the max)
+        per = torch.zeros(2 * world, dtype=torch.float64, device=f"cuda:{local_rank}")
+        per[rank] = ms
+        per[world + rank] = clk.summary().get("sm_mhz") or 0.0
+        dist.all_reduce(per)
+        if rank == 0:
+            v = per.tolist()
+            print("per-rank ms/step: " + " ".join(f"{x / args.steps:.3f}" for x in v[:world])
+                  + " | SM MHz: " + " ".join(f"{x:.0f}" for x in v[world:]), file=sys.stderr)
     ms = max_over_ranks(ms)
     sat_dev = float(np.mean(np.concatenate(sats)))
     label_frac = float(np.mean(np.concatenate(labs) >= 0))
