@@ -285,6 +285,21 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi), "f"(lo));
   return d;
 }
+// x[0..31] += the bf16 residual of 16-byte chunks J0..J0+3 of this lane's
+// 128-byte row (128B-swizzled residual box row at rbase; row % 8 == lane % 8)
+template <int J0>
+__device__ __forceinline__ void add_res_row(float* x, uint32_t rbase, int lane) {
+#pragma unroll
+  for (int j = 0; j < 4; j++) {
+    const uint4 rv = lds_u4(rbase + (uint32_t)((((J0 + j) ^ (lane & 7))) << 4));
+    const uint32_t w[4] = {rv.x, rv.y, rv.z, rv.w};
+#pragma unroll
+    for (int e = 0; e < 4; e++) {
+      x[8 * j + 2 * e] += __uint_as_float(w[e] << 16);
+      x[8 * j + 2 * e + 1] += __uint_as_float(w[e] & 0xffff0000u);
+    }
+  }
+}
 // ReLU / ReLU6 / none + bf16 pack of 2n floats
 template <int N2>
 __device__ __forceinline__ void act_pack(const float* x, uint32_t* o, int relu) {
@@ -591,8 +606,9 @@ struct TileSched {
 template <int BN, int STAGES, int kResSlots, int HALO, int RESB, int PAIR>
 constexpr int stg_floats() {
   if (!PAIR && BN == 256 && STAGES == 2 && kResSlots == 12) return 1024;  // residual: 6 boxes
-  if (!PAIR && BN == 64 && kResSlots) return 1280;  // 1024-aligned (see below)
-  if (PAIR || kResSlots) return 32 * kStgLd;
+  // staging blocks are 1024-aligned (5 KB >= the generic path's 32 x 36
+  // floats) for the 128B-swizzled 32 x 64 bulk stores of the block path
+  if (PAIR || kResSlots) return 1280;
   if (HALO == 0 && ((BN == 256 && STAGES == 4) || (BN == 128 && STAGES == 6) ||
                     (BN == 64 && STAGES == 8)))
     return 1024;
@@ -602,8 +618,7 @@ constexpr int stg_floats() {
   // 64-wide tiles: one 32 x 128 B staging block per warp, 1024-aligned for
   // the 128B-swizzled bulk store (the s2d stem: 4 KB exactly)
   if (BN == 64 && RESB == 4 && HALO == 12) return 1024;
-  if (BN == 64) return 1280;
-  return 32 * kStgLd;
+  return 1280;
 }
 
 template <int BN, int STAGES, int kResSlots, int HALO, int RESB, int PAIR, int S2D = 0,
@@ -631,6 +646,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   // An accumulator is released (tempty) by exactly the warps that drained it.
   constexpr bool kTileSplit = BN == 64 && !S2D;  // s2d: group h drains sub-tile h
   constexpr int kDrainWarps = kTileSplit ? kEpiWarps / 2 : kEpiWarps;
+  // epilogue block path: whole 64-column blocks per warp (see the epilogue)
+  constexpr int kCPT = BN / 32, kC0S = (kTileSplit || S2D) ? 1 : 2;
+  constexpr bool kBlockPath = !PAIR && stg_floats<BN, STAGES, kResSlots, HALO, RESB, PAIR>() >=
+                                           1024 && ((kC0S == 1 && kCPT == 2) || kC0S == 2);
   // residual ring: 128-row boxes of kResCols columns (64: 128-byte rows, SW128;
   // half the TMA row requests of 32-column SW64 boxes) in kResSlots x 8 KB
   constexpr int kResCols = CG_RES_COLS;
@@ -718,7 +737,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int s = 0; s < kResSlots; s++) {
       mbar_init(&rfull[s], 1);
-      mbar_init(&rempty[s], 4 * (kResCols / 32));  // 4 warps x the box's 32-col chunks
+      // block path: a box is one warp group's 64-column block (4 warps);
+      // chunk path: 4 warps x the box's 32-column chunks
+      mbar_init(&rempty[s], kBlockPath ? 4 : 4 * (kResCols / 32));
     }
     for (int s = 0; s < HALO; s++) {
       mbar_init(&hfull[s], 1);
@@ -1152,11 +1173,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       //    16-byte store instruction writes 4 whole 128-byte row segments
       //    instead of 32 rows' 16-byte pieces.
       constexpr bool kWhole = C0S == 1 && CPT == 2;
-      if constexpr (!PAIR && kStgWarp >= 1024 && (kWhole || C0S == 2)) {
-        if constexpr (kWhole)
-          static_assert((kStgWarp * 4) % 1024 == 0, "64-wide tiles: 1024-aligned staging");
+      if constexpr (kBlockPath) {
+        static_assert((kStgWarp * 4) % 1024 == 0, "block path: 1024-aligned staging");
+        static_assert(kResSlots == 0 || kResCols == 64, "block path: 64-column residual boxes");
         const bool remap_fast = !tma_out && kDirectRemap && !a.out_f32 && !res_r;
-        if ((kWhole && tma_out && !res_tma) || remap_fast) {
+        if ((tma_out && (res_tma || !res_r)) || remap_fast) {
           constexpr int kBlk = BN / 64, kBStep = kWhole ? 1 : 2;
 #pragma unroll 1
           for (int b = kWhole ? 0 : h; b < kBlk; b += kBStep) {
@@ -1173,6 +1194,16 @@ __global__ void __launch_bounds__(kThreads, 1)
               __syncwarp();
               if (lane == 0) mbar_arrive(&tempty[acc]);
             }
+            // residual: box gq of this CTA's ring is block b of this tile
+            // (128 rows x 64 columns, 128B swizzle); this warp's 32 rows
+            uint32_t rbase = 0;
+            int rslot = 0;
+            if (res_tma) {
+              const int gq = tile_i * kBlk + b;
+              rslot = gq % kRS;
+              mbar_wait(&rfull[rslot], (gq / kRS) & 1);
+              rbase = su32(s_res + rslot * kResBox) + (uint32_t)((q * 32 + lane) * 128);
+            }
             uint32_t o[32];
             float x[32];
 #pragma unroll
@@ -1185,6 +1216,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               x[4 * j + 2] = __uint_as_float(v[4 * j + 2]) + b4.z;
               x[4 * j + 3] = __uint_as_float(v[4 * j + 3]) + b4.w;
             }
+            if (res_tma) add_res_row<0>(x, rbase, lane);
             act_pack<16>(x, o, a.relu);
 #pragma unroll
             for (int j = 0; j < 8; j++) {
@@ -1195,6 +1227,11 @@ __global__ void __launch_bounds__(kThreads, 1)
               x[4 * j + 1] = __uint_as_float(w[4 * j + 1]) + b4.y;
               x[4 * j + 2] = __uint_as_float(w[4 * j + 2]) + b4.z;
               x[4 * j + 3] = __uint_as_float(w[4 * j + 3]) + b4.w;
+            }
+            if (res_tma) {
+              add_res_row<4>(x, rbase, lane);
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&rempty[rslot]);
             }
             act_pack<16>(x, o + 16, a.relu);
             if (!remap_fast && lane == 0) bulk_wait_read<0>();  // last store read its buffer
@@ -1221,7 +1258,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               fence_async_smem();
               __syncwarp();
               if (lane == 0) {
-                tma_store_2d(&gp.O[r_], stg_a, nb, m0 + q * 32);
+                tma_store_2d(&gp.O64[r_], stg_a, nb, m0 + q * 32);
                 bulk_commit();
               }
             }
@@ -1868,9 +1905,8 @@ void prepare_conv_gemm(PreparedGemm& p, const ConvGemmGroup& g, const ConvGemmAr
       if (a.ld_out % 8 || reinterpret_cast<uintptr_t>(g.out[r]) % 16)
         throw InvalidArgument("conv_gemm: output must be 16B aligned");
       // 64-wide tiles without a residual: the kernel's one-store-per-warp path
-      if (BN == 64 && !a.pair && !g.residual[r])
-        map_out128(p.gp.O[r], g.out[r], a.ld_out, a.rows_out);
-      else map64(p.gp.O[r], g.out[r], a.ld_out, a.rows_out, 32);
+      map64(p.gp.O[r], g.out[r], a.ld_out, a.rows_out, 32);
+      if (!a.pair) map_out128(p.gp.O64[r], g.out[r], a.ld_out, a.rows_out);
       if (g.residual[r]) {
         if (a.ld_res % 8 || reinterpret_cast<uintptr_t>(g.residual[r]) % 16)
           throw InvalidArgument("conv_gemm: residual must be 16B aligned");

@@ -119,6 +119,7 @@ struct ConvGemmGroup {
 // Kernel parameters of a grouped launch (all tensor maps pre-encoded).
 struct GemmGroupParams {
   CUtensorMap A[kMaxGroup], B[kMaxGroup], R[kMaxGroup], O[kMaxGroup], A2[kMaxGroup];
+  CUtensorMap O64[kMaxGroup];  // output, 64-column x 32-row boxes (128B swizzle)
   const float* bias[kMaxGroup];
   const __nv_bfloat16* residual[kMaxGroup];
   void* out[kMaxGroup];
