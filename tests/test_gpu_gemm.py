@@ -60,7 +60,10 @@ def q(x):
 
 @pytest.mark.parametrize("M,N,Kc,BN,relu,max_ctas", [
     (300, 128, 256, 128, 1, 0), (128, 64, 64, 64, 0, 0), (1000, 512, 128, 256, 1, 0),
-    (2048, 256, 512, 128, 0, 3), (4096, 64, 576, 64, 1, 5), (777, 256, 64, 256, 0, 2)])
+    (2048, 256, 512, 128, 0, 3), (4096, 64, 576, 64, 1, 5), (777, 256, 64, 256, 0, 2),
+    # N not a multiple of the tile: the last tile's upper 64-column block /
+    # 32-column half is clipped (bulk store) or skipped (bias, remap stores)
+    (500, 96, 128, 64, 1, 0), (600, 160, 192, 128, 1, 0), (333, 320, 64, 256, 0, 0)])
 def test_gemm_1x1(ctx, M, N, Kc, BN, relu, max_ctas):
     g = torch.Generator().manual_seed(M + N)
     A = torch.rand(M, Kc, generator=g) * 2 - 1
@@ -92,7 +95,8 @@ def test_gemm_residual_and_f32_tail(ctx):
 
 
 @pytest.mark.parametrize("M,N,Kc,BN", [(700, 512, 640, 256), (1500, 256, 512, 128),
-                                        (333, 128, 1024, 64), (2000, 1024, 256, 256)])
+                                        (333, 128, 1024, 64), (2000, 1024, 256, 256),
+                                        (900, 96, 256, 64), (700, 320, 128, 256)])
 def test_gemm_residual_ring_configs(ctx, M, N, Kc, BN):
     """Both residual-ring layouts (deep ring for short K, more mainloop
     stages for K >= 512) over ragged tails."""
@@ -148,7 +152,8 @@ def test_gemm_pair_taps_remap(ctx):
 
 
 @pytest.mark.parametrize("NB,H,C,Cout,BN", [(3, 7, 64, 128, 128), (2, 14, 128, 64, 64),
-                                            (2, 28, 64, 256, 256)])
+                                            (2, 28, 64, 256, 256), (2, 14, 64, 96, 64),
+                                            (2, 7, 128, 160, 128)])
 def test_conv3x3_padded_grid(ctx, NB, H, C, Cout, BN):
     """3x3/stride-1/pad-1 conv as 9 row-shifted taps over the zero-bordered
     grid (row mode PadToCompact) == torch conv2d."""
