@@ -911,6 +911,48 @@ __global__ void im2col3x3_f64_kernel(const double* __restrict__ in, int B, int S
   *reinterpret_cast<uint4*>(out + row * 64 + chunk * 8) = *reinterpret_cast<uint4*>(o);
 }
 
+// The same operand, one CTA per output image row (n, ho): the 3 input rows
+// x 3 planes it needs are read once, coalesced along w, rounded f64 ->
+// bf16 (the same single rounding) into shared memory with a zero column on
+// each side, then every (pixel, 16-byte K chunk) of the row is assembled
+// from shared memory and stored coalesced (consecutive threads, consecutive
+// 16-byte pieces of the [rows, 64] operand).
+constexpr int kIm2colMaxS = 512;
+__global__ void __launch_bounds__(256) im2col3x3_f64_rows_kernel(const double* __restrict__ in,
+                                                                 int B, int S, int stride,
+                                                                 int Ho, bf16* __restrict__ out) {
+  __shared__ bf16 sm[9][kIm2colMaxS + 2];  // [c * 3 + dr][w + 1]
+  const int n = blockIdx.x / Ho, ho = blockIdx.x - n * Ho;
+  for (int i = threadIdx.x; i < 9 * (S + 2); i += blockDim.x) {
+    const int rr = i / (S + 2), wp = i - rr * (S + 2);
+    const int c = rr / 3, dr = rr - c * 3, h = ho * stride - 1 + dr, w = wp - 1;
+    double x = 0.0;
+    if (h >= 0 && h < S && w >= 0 && w < S) x = __ldg(in + (((size_t)n * 3 + c) * S + h) * S + w);
+    sm[rr][wp] = __double2bfloat16(x);
+  }
+  __syncthreads();
+  uint4* o = reinterpret_cast<uint4*>(out + ((size_t)n * Ho + ho) * Ho * 64);
+  for (int i = threadIdx.x; i < Ho * 8; i += blockDim.x) {
+    const int wo = i >> 3, chunk = i & 7;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (chunk < 4) {
+      __align__(16) bf16 e[8];
+#pragma unroll
+      for (int j = 0; j < 8; j++) {
+        const int k = chunk * 8 + j;  // K = (dr * 3 + ds) * 3 + c
+        bf16 x = __float2bfloat16(0.f);
+        if (k < 27) {
+          const int tap = k / 3, c = k - tap * 3, dr = tap / 3, ds = tap - dr * 3;
+          x = sm[c * 3 + dr][wo * stride + ds];
+        }
+        e[j] = x;
+      }
+      v = *reinterpret_cast<const uint4*>(e);
+    }
+    o[i] = v;
+  }
+}
+
 // 2x2/2 max pool, compact NHWC in; out compact, or the interior of a
 // zero-bordered (H/2+2)^2 grid when padded_out.
 __global__ void maxpool2x2_kernel(const bf16* __restrict__ in, int B, int H, int C,
@@ -1195,8 +1237,13 @@ class SeqNet : public CnnModel {
     if (B > maxB_) reserve(B);
     timer_begin(st, kTimeAux);
     const int Ho = S_ / stride0_;
-    im2col3x3_f64_kernel<<<grid_for((size_t)B * Ho * Ho * 8), 256, 0, st>>>(
-        d_in, (int)B, S_, stride0_, Ho, reinterpret_cast<bf16*>(prepped));
+    if (S_ <= kIm2colMaxS && std::getenv("CREDO_IM2COL_OLD") == nullptr) {
+      im2col3x3_f64_rows_kernel<<<(unsigned)(B * Ho), 256, 0, st>>>(
+          d_in, (int)B, S_, stride0_, Ho, reinterpret_cast<bf16*>(prepped));
+    } else {
+      im2col3x3_f64_kernel<<<grid_for((size_t)B * Ho * Ho * 8), 256, 0, st>>>(
+          d_in, (int)B, S_, stride0_, Ho, reinterpret_cast<bf16*>(prepped));
+    }
     CG_CHECK_LAUNCH();
     timer_end(st, kTimeAux);
   }
