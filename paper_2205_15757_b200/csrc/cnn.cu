@@ -296,6 +296,10 @@ struct Block {
 int kSmallKMaxBN = 256;  // env CREDO_SMALLK_BN overrides (tuning)
 // ResNet stem: the s2d conv (default) or CREDO_NO_S2D=1, the im2col (K = 192)
 const bool kUseS2D = std::getenv("CREDO_NO_S2D") == nullptr;
+// 3x3 convs wider than one halo box (VGG-16 at 224 / 112 pixels) through
+// stacked halo boxes (CREDO_NO_WIDE_HALO=1: the 9 taps stream, A/B)
+const bool kWideHalo = std::getenv("CREDO_NO_WIDE_HALO") == nullptr;
+constexpr int kWideHaloRows = 600;  // = gemm_sm100.cu's slot rows
 // c3 + projection shortcut as one GEMM over concatenated K (or
 // CREDO_NO_FUSE_DS=1: the shortcut GEMM's output read back as a residual)
 const bool kFuseDs = std::getenv("CREDO_NO_FUSE_DS") == nullptr;
@@ -818,13 +822,26 @@ class ResNet final : public CnnModel {
     g.n = R;
     if (d0.s2d) BN = 64;
     if (d0.a2_rpb) BN = 256;  // the strided-A2 kernel variant is BN = 256
+    // wide halos (BM + 2 * halo_lo > 256 rows): stacked boxes of <= 256
+    // rows when a kernel variant fits this shape, else the taps stream
+    int halo_lo = d0.halo_lo, halo_sub = 1, hbox = 128 + 2 * halo_lo;
+    if (halo_lo > 0 && 128 + 2 * halo_lo > 256) {
+      ConvGemmArgs t{};
+      t.N = d0.c->cout;
+      t.Kc = d0.Kc;
+      t.ntaps = d0.ntaps;
+      t.halo_lo = halo_lo;
+      t.out_f32 = d0.out_f32;
+      halo_boxes(halo_lo, halo_sub, hbox);
+      if (!kWideHalo || !wide_halo_fits(BN, t)) halo_lo = 0, halo_sub = 1, hbox = 128;
+    }
     for (int r = 0; r < R; r++) {
       const GemmDesc& d = *ds[r];
       if (d.s2d) {
         make_operand_s2d_a(A[r], d.A, d.rowsA, 128 + d.gw + 3);
         make_operand_s2d_b(Bm[r], d.c->w, 16 * d.c->cout);
       } else {
-        make_operand(A[r], d.A, d.rowsA, d.Kc, 128 + 2 * d.halo_lo);
+        make_operand(A[r], d.A, d.rowsA, d.Kc, hbox);
         make_operand(Bm[r], d.c->w, d.c->cout, d.Kc * d.ntaps + d.kc2, BN);
         if (d.kc2) {
           if (d.a2_rpb) make_operand_s2_view(A2[r], d.A2, d.a2_b, d.a2_h, d.kc2, d.a2_rpb);
@@ -852,7 +869,9 @@ class ResNet final : public CnnModel {
     a.H = d0.H;
     a.W = d0.H;
     a.rows_out = d0.rows_out;
-    a.halo_lo = d0.halo_lo;
+    a.halo_lo = halo_lo;
+    a.halo_sub = halo_sub;
+    a.halo_box = hbox;
     a.s2d = d0.s2d;
     a.kc2 = d0.kc2;
     a.a2_wo = d0.a2_rpb ? d0.a2_h / 2 : 0;
@@ -1423,7 +1442,9 @@ class Vgg16 final : public SeqNet {
           for (int ds = 0; ds < 3; ds++) taps[dr * 3 + ds] = (dr - 1) * G + (ds - 1);
         push_gemm(L, c, in, rows_pad, rows_pad, taps, nullptr, 0, out, c.cout, 0, 1,
                   pool_after_[i] ? kRowPadToCompact : kRowPadToPad, H, b * H * H);
-        if (kUseHalo && 128 + 2 * (G + 1) <= 256) L.back().g.halo_lo = G + 1;
+        // wider than one halo box: stacked boxes (make_gemm_step checks a
+        // kernel variant fits, else the taps stream)
+        if (kUseHalo && 128 + 2 * (G + 1) <= kWideHaloRows) L.back().g.halo_lo = G + 1;
       }
       if (pool_after_[i]) {
         const bf16* src = compact_[i];

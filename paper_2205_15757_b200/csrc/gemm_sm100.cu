@@ -23,6 +23,11 @@ constexpr int BM = 128, BK = 64, kThreads = 352;
 constexpr int kEpiWarps = 8, kStgLd = 36;        // staging row stride (floats)
 constexpr int A_BYTES = BM * BK * 2;
 constexpr int kHaloBytes = 256 * BK * 2;  // largest halo box (BM + 2*halo_lo <= 256 rows)
+// wide-halo slot rows (stacked boxes): 3x3 convs up to 224 pixels wide
+// (BM + 2 * (W + 2) = 580 at W = 224 on the shared-border grid: 3 boxes of
+// 200 rows)
+constexpr int kWideHaloRows = 600;
+constexpr int kWideHaloRows128 = 368;  // 128-wide tiles (streamed weights): up to 112 pixels
 // s2d stem: one box per dy pair, BM + gw + 3 <= 256 rows of 32 bytes (16 channels)
 constexpr int kS2DSlot = 256 * 32;
 #ifndef CG_RES_COLS
@@ -603,8 +608,9 @@ struct TileSched {
 // 0 for halo variants whose remapped bf16 rows go out by direct stores. The
 // launcher picks the reduced variants only for outputs that fit them; the
 // freed shared memory buys mainloop stages / halo slots.
-template <int BN, int STAGES, int kResSlots, int HALO, int RESB, int PAIR>
+template <int BN, int STAGES, int kResSlots, int HALO, int RESB, int PAIR, int HROWS = 256>
 constexpr int stg_floats() {
+  if (HROWS > 256) return 0;  // wide halos: remapped rows, staging-free direct stores
   if (!PAIR && BN == 256 && STAGES == 2 && kResSlots == 12) return 1024;  // residual: 6 boxes
   // staging blocks are 1024-aligned (5 KB >= the generic path's 32 x 36
   // floats) for the 128B-swizzled 32 x 64 bulk stores of the block path
@@ -622,7 +628,7 @@ constexpr int stg_floats() {
 }
 
 template <int BN, int STAGES, int kResSlots, int HALO, int RESB, int PAIR, int S2D = 0,
-          int A2S = 0>
+          int A2S = 0, int HROWS = 256>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_gemm_kernel(const __grid_constant__ GemmGroupParams gp, const ConvGemmArgs a) {
   // A2S (strided second segment): A slots hold up to 4 boxes of 56 rows
@@ -632,11 +638,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   // TMA-store path only (2 x 2 KB per warp; the launcher picks them for bf16
   // outputs, which take the TMA-store or the staging-free direct-store
   // epilogue), which frees the fourth stage
-  constexpr int kStgWarp = stg_floats<BN, STAGES, kResSlots, HALO, RESB, PAIR>();
+  constexpr int kStgWarp = stg_floats<BN, STAGES, kResSlots, HALO, RESB, PAIR, HROWS>();
   static_assert(!PAIR || (RESB == 0 && (HALO == 0 || kResSlots == 0)), "pair: streamed weights");
   static_assert(!S2D || (BN == 64 && RESB == 4 && HALO > 0 && !PAIR), "s2d stem layout");
   // s2d stem: a ring slot holds one dy box (2 planes x (BM + 3) rows x 16 B)
-  constexpr int kHaloSlot = S2D ? kS2DSlot : kHaloBytes;
+  // halo slot: HROWS rows of 128 B (wide halos: several stacked boxes)
+  constexpr int kHaloB = HROWS * BK * 2;
+  constexpr int kHaloSlot = S2D ? kS2DSlot : kHaloB;
   constexpr int B_BYTES = (PAIR ? BN / 2 : BN) * BK * 2;  // this CTA's weight tile
   // s2d stem: 256-row tiles of two 128-row sub-tiles (2 accumulators each)
   constexpr int kSubTiles = S2D ? 2 : 1;
@@ -648,7 +656,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int kDrainWarps = kTileSplit ? kEpiWarps / 2 : kEpiWarps;
   // epilogue block path: whole 64-column blocks per warp (see the epilogue)
   constexpr int kCPT = BN / 32, kC0S = (kTileSplit || S2D) ? 1 : 2;
-  constexpr bool kBlockPath = !PAIR && stg_floats<BN, STAGES, kResSlots, HALO, RESB, PAIR>() >=
+  constexpr bool kBlockPath = !PAIR && stg_floats<BN, STAGES, kResSlots, HALO, RESB, PAIR, HROWS>() >=
                                            1024 && ((kC0S == 1 && kCPT == 2) || kC0S == 2);
   // residual ring: 128-row boxes of kResCols columns (64: 128-byte rows, SW128;
   // half the TMA row requests of 32-column SW64 boxes) in kResSlots x 8 KB
@@ -696,6 +704,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int kpt = S2D ? 4 : a.Kc / BK;  // s2d: kpt = the 4 dy boxes
   const int num_k1 = a.ntaps * kpt, num_k = num_k1 + a.kc2 / BK;  // + second K segment
   (void)num_m;
+  // one halo: halo_sub stacked boxes of hbox rows (one box when halo_sub <= 1)
+  const int hsub = a.halo_sub > 1 ? a.halo_sub : 1;
+  const int hbox = hsub > 1 ? a.halo_box : BM + 2 * a.halo_lo;
+  auto load_halo = [&](const CUtensorMap* map, uint64_t* bar, uint8_t* dst, int x, int y) {
+    mbar_expect_tx(bar, hsub * hbox * BK * 2);
+    for (int j = 0; j < hsub; j++) tma_load_2d(map, bar, dst + j * hbox * BK * 2, x, y + j * hbox);
+  };
+  static_assert(HROWS == 256 || (!PAIR && !S2D), "wide halos: single-SM, non-stem");
   FastDiv div_outer, div_n;  // per_r (RESB) or per_m, and num_n
   div_outer.init(RESB > 0 ? num_mt * num_n : gp.n * num_n);
   div_n.init(num_n);
@@ -830,11 +846,9 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
             continue;
           }
-          const int hrows = BM + 2 * a.halo_lo;
           for (int cb = 0; cb < kpt; cb++) {
             mbar_wait(&hempty[hs], hphase ^ 1);
-            mbar_expect_tx(&hfull[hs], hrows * BK * 2);
-            tma_load_2d(&gp.A[r], &hfull[hs], sA + hs * kHaloBytes, cb * BK, m0 - a.halo_lo);
+            load_halo(&gp.A[r], &hfull[hs], sA + hs * kHaloB, cb * BK, m0 - a.halo_lo);
             if (++hs == HALO) { hs = 0; hphase ^= 1; }
           }
           continue;
@@ -846,7 +860,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int cb = 0; cb < kpt; cb++) {
             mbar_wait(&hempty[hs], hphase ^ 1);
             if (crank == 0) mbar_expect_tx(&hfull[hs], 2 * hrows * BK * 2);
-            tma_load_2d_pair(&gp.A[r], mapa_cluster(&hfull[hs], 0), sA + hs * kHaloBytes, cb * BK,
+            tma_load_2d_pair(&gp.A[r], mapa_cluster(&hfull[hs], 0), sA + hs * kHaloB, cb * BK,
                              m0 - a.halo_lo);
             if (++hs == HALO) { hs = 0; hphase ^= 1; }
             for (int tap = 0; tap < a.ntaps; tap++) {
@@ -861,11 +875,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if constexpr (HALO > 0) {
           // per channel block: one halo box, then the 9 taps' weight tiles
-          const int hrows = BM + 2 * a.halo_lo;
           for (int cb = 0; cb < kpt; cb++) {
             mbar_wait(&hempty[hs], hphase ^ 1);
-            mbar_expect_tx(&hfull[hs], hrows * BK * 2);
-            tma_load_2d(&gp.A[r], &hfull[hs], sA + hs * kHaloBytes, cb * BK, m0 - a.halo_lo);
+            load_halo(&gp.A[r], &hfull[hs], sA + hs * kHaloB, cb * BK, m0 - a.halo_lo);
             if (++hs == HALO) { hs = 0; hphase ^= 1; }
             for (int tap = 0; tap < a.ntaps; tap++) {
               mbar_wait(&empty[stage], phase ^ 1);
@@ -984,7 +996,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait(&hfull[hs], hphase);
             if (cb == 0) CG_TRACE(3, ti);
             tc_fence_after();
-            const uint32_t hbase = sA_u + (uint32_t)(hs * kHaloBytes + a.halo_lo * 128);
+            const uint32_t hbase = sA_u + (uint32_t)(hs * kHaloB + a.halo_lo * 128);
 #pragma unroll
             for (int tap = 0; tap < 9; tap++) {
               const uint64_t ad = smem_desc_sw128_row(hbase + (uint32_t)(a.tap_off[tap] * 128), 0);
@@ -1030,7 +1042,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int cb = 0; cb < kpt; cb++) {
             mbar_wait(&hfull[hs], hphase);
             tc_fence_after();
-            const uint32_t hbase = sA_u + (uint32_t)(hs * kHaloBytes + a.halo_lo * 128);
+            const uint32_t hbase = sA_u + (uint32_t)(hs * kHaloB + a.halo_lo * 128);
 #pragma unroll
             for (int tap = 0; tap < 9; tap++) {
               mbar_wait(&full[stage], phase);
@@ -1055,7 +1067,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int cb = 0; cb < kpt; cb++) {
             mbar_wait(&hfull[hs], hphase);
             tc_fence_after();
-            const uint32_t hbase = sA_u + (uint32_t)(hs * kHaloBytes + a.halo_lo * 128);
+            const uint32_t hbase = sA_u + (uint32_t)(hs * kHaloB + a.halo_lo * 128);
 #pragma unroll
             for (int tap = 0; tap < 9; tap++) {
               mbar_wait(&full[stage], phase);
@@ -1473,14 +1485,14 @@ EncodeFn get_encode() {
 }
 
 template <int BN, int STAGES, int kResSlots, int HALO, int RESB, int PAIR = 0, int S2D = 0,
-          int A2S = 0>
+          int A2S = 0, int HROWS = 256>
 constexpr int smem_bytes() {
   return 1024 +
-         (HALO > 0 ? HALO * (S2D ? kS2DSlot : kHaloBytes)
+         (HALO > 0 ? HALO * (S2D ? kS2DSlot : HROWS * BK * 2)
                    : STAGES * (A2S ? 4 * 56 * 128 : A_BYTES)) +
          (RESB > STAGES ? RESB : STAGES) * (PAIR ? BN / 2 : BN) * BK * 2 +
          kResSlots * 8192 +
-         kEpiWarps * 4 * stg_floats<BN, STAGES, kResSlots, HALO, RESB, PAIR>() +
+         kEpiWarps * 4 * stg_floats<BN, STAGES, kResSlots, HALO, RESB, PAIR, HROWS>() +
          8 * (2 * STAGES + 4 + 2 * (kResSlots > 0 ? kResSlots : 1) + 2 * (HALO > 0 ? HALO : 1)) +
          16 + 48 + 16 + 32 * kClcSlots;
 }
@@ -1510,13 +1522,13 @@ int tiles_per_unit(const ConvGemmArgs& a, int BN, int tiles) {
 }
 
 template <int BN, int STAGES, int RS, int HALO = 0, int RESB = 0, int PAIR = 0, int S2D = 0,
-          int A2S = 0>
+          int A2S = 0, int HROWS = 256>
 void launch_t(const PreparedGemm& p, cudaStream_t st, int max_ctas) {
-  constexpr int smem = smem_bytes<BN, STAGES, RS, HALO, RESB, PAIR, S2D, A2S>();
+  constexpr int smem = smem_bytes<BN, STAGES, RS, HALO, RESB, PAIR, S2D, A2S, HROWS>();
   static_assert(smem <= 232448, "smem budget");
   static std::atomic<uint64_t> attr{0};
   once_per_device(attr, [] {
-    CG_CUDA(cudaFuncSetAttribute(conv_gemm_kernel<BN, STAGES, RS, HALO, RESB, PAIR, S2D, A2S>,
+    CG_CUDA(cudaFuncSetAttribute(conv_gemm_kernel<BN, STAGES, RS, HALO, RESB, PAIR, S2D, A2S, HROWS>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   });
   ConvGemmArgs a = p.args;
@@ -1567,7 +1579,7 @@ void launch_t(const PreparedGemm& p, cudaStream_t st, int max_ctas) {
     at[0].val.programmaticStreamSerializationAllowed = g_pdl;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    CG_CUDA(cudaLaunchKernelEx(&cfg, conv_gemm_kernel<BN, STAGES, RS, HALO, RESB, PAIR, S2D, A2S>,
+    CG_CUDA(cudaLaunchKernelEx(&cfg, conv_gemm_kernel<BN, STAGES, RS, HALO, RESB, PAIR, S2D, A2S, HROWS>,
                                p.gp, a));
     launch_counter_add(1);
   }
@@ -1877,14 +1889,19 @@ void prepare_conv_gemm(PreparedGemm& p, const ConvGemmGroup& g, const ConvGemmAr
   const bool tma_out = a.row_mode == kRowIdentity && !a.out_f32;
   std::memset(&p.gp, 0, sizeof p.gp);
   p.gp.n = g.n;
-  if (a.halo_lo < 0 || BM + 2 * a.halo_lo > 256) throw InvalidArgument("conv_gemm: halo too wide");
+  const int hsub = a.halo_sub > 1 ? a.halo_sub : 1;
+  if (a.halo_lo < 0 || (hsub == 1 && BM + 2 * a.halo_lo > 256) ||
+      (hsub > 1 && (a.pair || a.halo_box % 8 || a.halo_box > 256 ||
+                    hsub * a.halo_box < BM + 2 * a.halo_lo || !wide_halo_fits(BN, a))))
+    throw InvalidArgument("conv_gemm: halo too wide");
   if (a.halo_lo > 0 && a.ntaps != 9) throw InvalidArgument("conv_gemm: halo needs 9 taps");
   for (int t = 0; a.halo_lo > 0 && t < a.ntaps; t++)
     if (a.tap_off[t] < -a.halo_lo || a.tap_off[t] > a.halo_lo)
       throw InvalidArgument("conv_gemm: tap outside the halo");
   for (int r = 0; r < g.n; r++) {
     if (!a.s2d &&
-        (g.A[r]->box_rows != BM + 2 * a.halo_lo || g.B[r]->box_rows != (a.pair ? BN / 2 : BN)))
+        (g.A[r]->box_rows != (hsub > 1 ? a.halo_box : BM + 2 * a.halo_lo) ||
+         g.B[r]->box_rows != (a.pair ? BN / 2 : BN)))
       throw InvalidArgument("conv_gemm: box mismatch");
     if ((g.residual[r] != nullptr) != (g.residual[0] != nullptr))
       throw InvalidArgument("conv_gemm: residual on some replicas only");
@@ -1922,6 +1939,21 @@ void prepare_conv_gemm(PreparedGemm& p, const ConvGemmGroup& g, const ConvGemmAr
   p.res = g.residual[0] != nullptr && tma_out;
 }
 
+void halo_boxes(int halo_lo, int& sub, int& box) {
+  const int rows = BM + 2 * halo_lo;
+  sub = (rows + 255) / 256;
+  box = ((rows + sub - 1) / sub + 7) / 8 * 8;
+  if (box > 256) box = 256, sub = (rows + 255) / 256 + 1;
+}
+
+bool wide_halo_fits(int BN, const ConvGemmArgs& a) {
+  int sub, box;
+  halo_boxes(a.halo_lo, sub, box);
+  if (a.ntaps != 9 || a.pair || a.out_f32) return false;
+  if (BN == 64) return a.N <= 64 && a.Kc == 64 && sub * box <= kWideHaloRows;  // resident B
+  return BN == 128 && sub * box <= kWideHaloRows128;
+}
+
 void launch_prepared(const PreparedGemm& p, cudaStream_t st, int max_ctas) {
   if (p.args.a2_wo) {  // strided second segment (the stride-2 shortcut, no gather)
     if (p.BN != 256 || p.res) throw InvalidArgument("conv_gemm: strided A2 is for BN = 256");
@@ -1946,6 +1978,17 @@ void launch_prepared(const PreparedGemm& p, cudaStream_t st, int max_ctas) {
   }
   if (p.args.halo_lo > 0) {
     if (p.res) throw InvalidArgument("conv_gemm: halo mode has no residual ring");
+    if (p.args.halo_sub > 1) {
+      // wide halos (stacked boxes): remapped bf16 rows, staging-free epilogue
+      if (p.args.out_f32 || p.args.row_mode == kRowIdentity || !kDirectRemap)
+        throw InvalidArgument("conv_gemm: wide halos write remapped bf16 rows");
+      if (wide_halo_fits(p.BN, p.args)) {
+        if (p.BN == 64) launch_t<64, 1, 0, 2, 9, 0, 0, 0, kWideHaloRows>(p, st, max_ctas);
+        else launch_t<128, 8, 0, 2, 0, 0, 0, 0, kWideHaloRows128>(p, st, max_ctas);
+        return;
+      }
+      throw InvalidArgument("conv_gemm: no wide-halo variant for this shape");
+    }
     // small weight sets (one n block, 9 x 64-channel taps): keep B resident
     if (p.BN == 64 && p.args.N <= 64 && p.args.Kc == 64 && p.args.ntaps == 9 &&
         std::getenv("CREDO_NO_RESB") == nullptr) {

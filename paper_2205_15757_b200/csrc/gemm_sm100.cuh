@@ -57,6 +57,10 @@ struct ConvGemmArgs {
   // one BM-row box per tap. 0 = off. The A operand's box must then have
   // BM + 2*halo_lo (<= 256) rows.
   int halo_lo;
+  // Wide halo (BM + 2*halo_lo > 256 rows, e.g. 3x3 convs at 112 / 224
+  // pixels): the halo arrives as halo_sub TMA boxes of the operand's
+  // box_rows rows each, stacked in one shared-memory slot. 0 / 1 = one box.
+  int halo_sub, halo_box;  // halo_box: rows per box (a multiple of 8)
   int pair;  // 1: SM-pair (cta_group::2) 256-row tiles, B operand box = BN/2 rows
   // Tile scheduler, set by the launcher: 0 = static persistent stride, 1 =
   // cluster launch control (one CTA per unit of tile_unit tiles; resident
@@ -137,6 +141,12 @@ struct PreparedGemm {
 // costs one kernel launch (plans cache PreparedGemm per layer).
 void prepare_conv_gemm(PreparedGemm& p, const ConvGemmGroup& g, const ConvGemmArgs& a, int BN);
 void launch_prepared(const PreparedGemm& p, cudaStream_t st, int max_ctas = 0);
+// Whether a wide halo (ConvGemmArgs::halo_sub > 1) has a kernel variant for
+// this tile width and shape (else the 3x3 streams its 9 taps).
+bool wide_halo_fits(int BN, const ConvGemmArgs& a);
+// The stacked boxes of a halo of BM + 2 * halo_lo rows: sub boxes of box rows
+// (<= 256, a multiple of 8 so every box starts on a swizzle-atom boundary).
+void halo_boxes(int halo_lo, int& sub, int& box);
 
 // Cycles per M=128 x N x K=16 SS-mode MMA issued back to back (microbench).
 double mma_rate_bench(int N, int iters, int ctas, int two_acc, cudaStream_t st);
