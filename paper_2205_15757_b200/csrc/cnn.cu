@@ -296,6 +296,9 @@ struct Block {
 int kSmallKMaxBN = 256;  // env CREDO_SMALLK_BN overrides (tuning)
 // ResNet stem: the s2d conv (default) or CREDO_NO_S2D=1, the im2col (K = 192)
 const bool kUseS2D = std::getenv("CREDO_NO_S2D") == nullptr;
+// VGG-16's conv1_1 as the s2d-mode GEMM over a 16-channel grid
+// (CREDO_NO_VGG_GRID16=1: the K = 64 im2col operand, A/B)
+const bool kVggGrid16 = std::getenv("CREDO_NO_VGG_GRID16") == nullptr;
 // 3x3 convs wider than one halo box (VGG-16 at 224 / 112 pixels) through
 // stacked halo boxes (CREDO_NO_WIDE_HALO=1: the 9 taps stream, A/B)
 const bool kWideHalo = std::getenv("CREDO_NO_WIDE_HALO") == nullptr;
@@ -503,6 +506,7 @@ class ResNet final : public CnnModel {
     int ldout = 0, out_f32 = 0, relu = 0, mode = 0, H = 0, rows_out = 0;
     int halo_lo = 0;  // > 0: 3x3 taps fed from one halo box per channel block
     int s2d = 0, gh = 0, gw = 0;  // the s2d stem (ConvGemmArgs::s2d)
+    int s2d_step = 0;             // ConvGemmArgs::s2d_step
     const bf16* A2 = nullptr;     // second K segment operand (ConvGemmArgs::kc2)
     int kc2 = 0;
     int a2_b = 0, a2_h = 0, a2_rpb = 0;  // A2 = x[2h, 2w] of [a2_b, a2_h, a2_h, kc2] in place
@@ -838,7 +842,7 @@ class ResNet final : public CnnModel {
     for (int r = 0; r < R; r++) {
       const GemmDesc& d = *ds[r];
       if (d.s2d) {
-        make_operand_s2d_a(A[r], d.A, d.rowsA, 128 + d.gw + 3);
+        make_operand_s2d_a(A[r], d.A, d.rowsA, 128 + (d.s2d_step == 1 ? 0 : d.gw) + 3);
         make_operand_s2d_b(Bm[r], d.c->w, 16 * d.c->cout);
       } else {
         make_operand(A[r], d.A, d.rowsA, d.Kc, hbox);
@@ -873,6 +877,7 @@ class ResNet final : public CnnModel {
     a.halo_sub = halo_sub;
     a.halo_box = hbox;
     a.s2d = d0.s2d;
+    a.s2d_step = d0.s2d_step;
     a.kc2 = d0.kc2;
     a.a2_wo = d0.a2_rpb ? d0.a2_h / 2 : 0;
     a.a2_rpb = d0.a2_rpb;
@@ -970,6 +975,29 @@ __global__ void __launch_bounds__(256) im2col3x3_f64_rows_kernel(const double* _
     }
     o[i] = v;
   }
+}
+
+// VGG-16's conv1_1 operand: f64 CHW -> a zero-bordered [B][S+3][S+3][16]
+// bf16 grid, pixel (i, j) at grid (i+1, j+1), channels 3..15 zero (one
+// rounding f64 -> bf16). The 3x3 conv then runs as the s2d-mode GEMM: a 4x4
+// with zero fourth taps, one K = 16 MMA per tap (ConvGemmArgs::s2d_step 1).
+__global__ void chw_to_grid16_kernel(const double* __restrict__ in, int B, int S,
+                                     uint4* __restrict__ out) {
+  const int G = S + 3;
+  const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (size_t)B * G * G) return;
+  const int n = (int)(t / ((size_t)G * G)), rem = (int)(t - (size_t)n * G * G);
+  const int i = rem / G - 1, j = rem - (rem / G) * G - 1;
+  __align__(16) bf16 e[16];
+#pragma unroll
+  for (int c = 0; c < 16; c++) e[c] = __float2bfloat16(0.f);
+  if (i >= 0 && i < S && j >= 0 && j < S) {
+#pragma unroll
+    for (int c = 0; c < 3; c++)
+      e[c] = __double2bfloat16(__ldg(in + (((size_t)n * 3 + c) * S + i) * S + j));
+  }
+  out[2 * t] = reinterpret_cast<const uint4*>(e)[0];
+  out[2 * t + 1] = reinterpret_cast<const uint4*>(e)[1];
 }
 
 // 2x2/2 max pool, compact NHWC in; out compact, or the interior of a
@@ -1248,13 +1276,25 @@ class SeqNet : public CnnModel {
     maxB_ = maxB;
     alloc_buffers(maxB);
   }
-  size_t prepared_bytes(uint32_t B) const override { return (size_t)B * rows0_ * 64 * 2; }
+  size_t prepared_bytes(uint32_t B) const override {
+    if (grid16_) return (size_t)B * (S_ + 3) * (S_ + 3) * 32;
+    return (size_t)B * rows0_ * 64 * 2;
+  }
   std::string prep_kind() const override {
+    if (grid16_) return "grid16/" + std::to_string(S_);
     return "im2col3x3s" + std::to_string(stride0_) + "k64/" + std::to_string(S_);
   }
   void prepare_input(const double* d_in, uint32_t B, void* prepped, cudaStream_t st) override {
     if (B > maxB_) reserve(B);
     timer_begin(st, kTimeAux);
+    if (grid16_) {
+      const size_t px = (size_t)B * (S_ + 3) * (S_ + 3);
+      chw_to_grid16_kernel<<<grid_for(px), 256, 0, st>>>(d_in, (int)B, S_,
+                                                         reinterpret_cast<uint4*>(prepped));
+      CG_CHECK_LAUNCH();
+      timer_end(st, kTimeAux);
+      return;
+    }
     const int Ho = S_ / stride0_;
     if (S_ <= kIm2colMaxS && std::getenv("CREDO_IM2COL_OLD") == nullptr) {
       im2col3x3_f64_rows_kernel<<<(unsigned)(B * Ho), 256, 0, st>>>(
@@ -1322,7 +1362,7 @@ class SeqNet : public CnnModel {
     g.M = M;
     g.Kc = c.Kc;
     g.ntaps = c.ntaps;
-    for (int t = 0; t < c.ntaps; t++) g.taps[t] = taps ? taps[t] : 0;
+    for (int t = 0; t < c.ntaps && t < 9; t++) g.taps[t] = taps ? taps[t] : 0;  // s2d: 16, implicit
     g.res = res;
     g.ldres = ldres;
     g.out = out;
@@ -1349,6 +1389,7 @@ class SeqNet : public CnnModel {
   bool softmax_;
   int S_ = 224, stride0_ = 1;
   size_t rows0_ = 0;  // conv0 output pixels per image
+  bool grid16_ = false;  // conv0 as the s2d-mode GEMM over a 16-channel grid (VGG-16)
   double flops_ = 0;
   std::vector<ConvW*> gemms_;
   std::vector<DwW*> dws_;
@@ -1401,6 +1442,23 @@ class Vgg16 final : public SeqNet {
     for (auto& c : fc_) gemms_.push_back(&c);
     stride0_ = 1;
     rows0_ = (size_t)S_ * S_;
+    // conv1_1 as a 4x4 s2d-mode GEMM over the 16-channel grid: tap (dy, dx)
+    // = kernel position (dr, ds) = (dy, dx) for dy, dx < 3, zero otherwise;
+    // [tap][cout][16] like the ResNet stem's resident weight tile
+    ConvW& c0 = convs_[0];
+    grid16_ = kVggGrid16 && S_ + 3 <= 4096 && c0.cout == 64;
+    if (grid16_) {
+      std::vector<uint16_t> w((size_t)16 * 64 * 16, 0);
+      for (int o = 0; o < 64; o++)
+        for (int dr = 0; dr < 3; dr++)
+          for (int ds = 0; ds < 3; ds++)
+            for (int ci = 0; ci < 3; ci++)
+              w[((size_t)(dr * 4 + ds) * 64 + o) * 16 + ci] =
+                  c0.hw[(size_t)o * c0.Kc + (dr * 3 + ds) * 3 + ci];
+      c0.hw.swap(w);
+      c0.Kc = 16;
+      c0.ntaps = 16;
+    }
   }
 
  protected:
@@ -1433,7 +1491,18 @@ class Vgg16 final : public SeqNet {
       ConvW& c = convs_[i];
       const int H = Hs_[i], G = H + 1, rows_pad = b * G * G;  // shared-border grid
       void* out = pool_after_[i] ? (void*)compact_[i] : (void*)pads_[i];
-      if (i == 0) {
+      if (i == 0 && grid16_) {
+        // the s2d-mode GEMM over the 16-channel grid, rows remapped into
+        // conv1_2's shared-border grid (or compact rows before a pool)
+        const int Gg = H + 3;
+        push_gemm(L, c, in, b * Gg * Gg, b * Gg * Gg, nullptr, nullptr, 0, out, c.cout, 0, 1,
+                  pool_after_[i] ? kRowGridToCompact : kRowGridToPad, H, b * H * H);
+        L.back().g.Kc = 16;
+        L.back().g.ntaps = 16;
+        L.back().g.s2d = 1;
+        L.back().g.s2d_step = 1;
+        L.back().g.gh = L.back().g.gw = Gg;
+      } else if (i == 0) {
         push_gemm(L, c, in, b * H * H, b * H * H, nullptr, nullptr, 0, out, c.cout, 0, 1,
                   pool_after_[i] ? kRowIdentity : kRowCompactToPad, H, b * H * H);
       } else {

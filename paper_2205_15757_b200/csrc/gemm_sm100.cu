@@ -458,7 +458,8 @@ struct RowRemap {
     W = a.W;
     Bn = 0;
     switch (mode) {
-      case kRowGridToCompact: d1.init(a.gh * a.gw); d2.init(a.gw); break;
+      case kRowGridToCompact:
+      case kRowGridToPad: d1.init(a.gh * a.gw); d2.init(a.gw); break;
       case kRowPhaseGridToCompact:
       case kRowPadToCompact:
       case kRowPadToPad: d1.init((H + 1) * (W + 1)); d2.init(W + 1); break;
@@ -479,6 +480,8 @@ struct RowRemap {
     switch (mode) {
       case kRowGridToCompact:
       case kRowPhaseGridToCompact: return (i < H && j < W) ? (n * H + i) * W + j : -1;
+      case kRowGridToPad:  // -> the shared-border grid's interior
+        return (i < H && j < W) ? (n * (H + 1) + i + 1) * (W + 1) + j : -1;
       case kRowCompactToPhasePad: {
         const int h = i + 1, w = j + 1, Hq = (H + 2) >> 1, Wq = (W + 2) >> 1;
         return ((((h & 1) * 2 + (w & 1)) * Bn + n) * Hq + (h >> 1)) * Wq + (w >> 1);
@@ -835,13 +838,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             wr = r;
             wl++;
           }
-          if constexpr (S2D) {  // per dy pair, one box per sub-tile: BM + gw + 3 rows
-            for (int h = 0; h < 2; h++)
+          if constexpr (S2D) {
+            // per dy pair (or per dy), one box per sub-tile: BM + gw + 3
+            // (or BM + 3) rows
+            const int step = a.s2d_step == 1 ? 1 : 2, nbox = 4 / step;
+            const int brows = BM + (step - 1) * a.gw + 3;
+            for (int h = 0; h < nbox; h++)
               for (int sub = 0; sub < kSubTiles; sub++) {
                 mbar_wait(&hempty[hs], hphase ^ 1);
-                mbar_expect_tx(&hfull[hs], (BM + a.gw + 3) * 32);
+                mbar_expect_tx(&hfull[hs], brows * 32);
                 tma_load_2d(&gp.A[r], &hfull[hs], sA + hs * kHaloSlot, 0,
-                            m0 + sub * BM + 2 * h * a.gw);
+                            m0 + sub * BM + step * h * a.gw);
                 if (++hs == HALO) { hs = 0; hphase ^= 1; }
               }
             continue;
@@ -964,15 +971,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             // per dy pair: both sub-tiles' boxes (ring slots hs, hs + 1), the
             // two accumulators' MMAs interleaved
             static_assert(kSubTiles == 2 && HALO % 2 == 0, "s2d: sub-tile box pairs");
-            for (int h = 0; h < 2; h++) {
+            const int step = a.s2d_step == 1 ? 1 : 2, nbox = 4 / step;
+            for (int h = 0; h < nbox; h++) {
               mbar_wait(&hfull[hs], hphase);
               mbar_wait(&hfull[hs + 1], hphase);
               if (h == 0) CG_TRACE(3, ti);
               tc_fence_after();
               const uint32_t hb0 = sA_u + (uint32_t)(hs * kHaloSlot), hb1 = hb0 + kHaloSlot;
-#pragma unroll
-              for (int j = 0; j < 2; j++) {  // dy = 2h + j: rows j * gw on of each box
-                const int dy = 2 * h + j;
+              for (int j = 0; j < step; j++) {  // dy = step * h + j: rows j * gw on of each box
+                const int dy = step * h + j;
                 const uint32_t ro = (uint32_t)(j * a.gw * 32);
                 umma_bf16_x4x2_w<2048 / 16>(d, d + BN, smem_desc_sw32_row(hb0 + ro),
                                             smem_desc_sw32_row(hb1 + ro),
@@ -1870,11 +1877,13 @@ static void map128_res(CUtensorMap& m, const void* p, int ld, int rows) {
 void prepare_conv_gemm(PreparedGemm& p, const ConvGemmGroup& g, const ConvGemmArgs& a, int BN) {
   if (a.s2d) {
     if (BN != 64 || a.N != 64 || a.Kc != 16 || a.ntaps != 16 || a.halo_lo || a.pair ||
-        (a.row_mode != kRowGridToCompact && a.row_mode != kRowIdentity) || a.out_f32 ||
+        (a.row_mode != kRowGridToCompact && a.row_mode != kRowIdentity &&
+         a.row_mode != kRowGridToPad) || a.out_f32 ||
         a.gw < 4 || a.gh < 4)
       throw InvalidArgument("conv_gemm: s2d stem is 64 outputs, 16 taps of K = 16, grid rows");
     for (int r = 0; r < g.n; r++)
-      if (g.A[r]->box_rows != BM + a.gw + 3 || BM + a.gw + 3 > 256 || g.B[r]->box_rows != 256 ||
+      if (g.A[r]->box_rows != BM + (a.s2d_step == 1 ? 0 : a.gw) + 3 || g.A[r]->box_rows > 256 ||
+          g.B[r]->box_rows != 256 ||
           g.residual[r])
         throw InvalidArgument("conv_gemm: s2d stem operand mismatch");
   } else if (a.Kc % 64 || a.ntaps < 1 || a.ntaps > 9) {

@@ -32,6 +32,8 @@ enum RowMode : int {
                               // H x W (H, W = output dims)
   kRowGridToCompact = 6,      // m on a per-image gh x gw grid -> compact H x W
                               // (rows with i >= H or j >= W are not stored)
+  kRowGridToPad = 7,          // m on a per-image gh x gw grid -> the interior
+                              // of the shared-border (H+1) x (W+1) grid
 };
 
 struct ConvGemmArgs {
@@ -75,6 +77,10 @@ struct ConvGemmArgs {
   // Rows live on a per-image gh x gw grid (row_mode kRowGridToCompact).
   int s2d;
   int gh, gw;
+  // s2d boxes: 0 / 2 = one box per dy pair (BM + gw + 3 rows <= 256), 1 = one
+  // box per dy (BM + 3 rows; grids wider than 125 columns, e.g. a 3x3 conv
+  // over a 16-channel 224-pixel image as a 4x4 with zero fourth taps)
+  int s2d_step;
   // Second K segment (1x1 convs only): k-blocks Kc/64 .. Kc/64 + kc2/64 - 1
   // read A from the A2 operand (same rows) against weight columns Kc ..
   // Kc + kc2 - 1 -- a bottleneck's c3 and its projection shortcut (ds) as one
