@@ -1166,7 +1166,39 @@ void certify(cg_group* g, uint64_t ticket, const double* precomputed_outputs) {
         }
       }
     }
-    for (uint32_t li = 0; li < nloc && !grouped; li++) {
+    static const bool kHeteroStreams = std::getenv("CREDO_NO_HETERO_STREAMS") == nullptr;
+    if (!grouped && nloc > 1 && g->all_cnn && kHeteroStreams) {
+      if (g->rstreams.size() < nloc) {
+        int lo = 0, hi = 0;
+        CG_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        while (g->rstreams.size() < nloc) {
+          cudaStream_t s2;
+          CG_CUDA(cudaStreamCreateWithPriority(&s2, cudaStreamNonBlocking, lo));
+          g->rstreams.push_back(s2);
+        }
+        while (g->revs.size() < nloc + 1) {
+          cudaEvent_t e;
+          CG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+          g->revs.push_back(e);
+        }
+      }
+      CG_CUDA(cudaEventRecord(g->revs[0], st));
+      for (uint32_t li = 0; li < nloc; li++) {
+        const uint32_t p = first + li;
+        cg_model* m = g->models[li];
+        cudaStream_t rs = g->rstreams[li];
+        float* lg = g->d_pre32.p + (uint64_t)li * B * v;  // per-replica logits
+        CG_CUDA(cudaStreamWaitEvent(rs, g->revs[0], 0));
+        m->cnn->forward(S.d_in_ptr, B, lg, rs, prepped);
+        launch_softmax_topk_f32(lg, v, B, (uint32_t)v, m->softmax, R.d_outs.p + (uint64_t)p * B * v,
+                                v, g->topk, R.d_topi.p + (uint64_t)p * B * g->topk,
+                                R.d_topv.p + (uint64_t)p * B * g->topk, rs);
+        CG_CUDA(cudaEventRecord(g->revs[1 + li], rs));
+      }
+      for (uint32_t li = 0; li < nloc; li++) CG_CUDA(cudaStreamWaitEvent(st, g->revs[1 + li], 0));
+    }
+    const bool concurrent = !grouped && nloc > 1 && g->all_cnn && kHeteroStreams;
+    for (uint32_t li = 0; li < nloc && !grouped && !concurrent; li++) {
       const uint32_t p = first + li;  // provider index of local replica li
       cg_model* m = g->models[li];
       double* outs = R.d_outs.p + (uint64_t)p * B * v;
@@ -1542,6 +1574,11 @@ void cg_group_free(cg_group* g) {
   cudaStreamSynchronize(g->ctx->stream);
   if (g->ctx->tail) cudaStreamSynchronize(g->ctx->tail);
   for (auto& s : g->slots) cudaStreamSynchronize(s->stream);
+  for (cudaStream_t s2 : g->rstreams) {
+    cudaStreamSynchronize(s2);
+    cudaStreamDestroy(s2);
+  }
+  for (cudaEvent_t e : g->revs) cudaEventDestroy(e);
   delete g;
 }
 

@@ -274,6 +274,12 @@ struct cg_group {
   bool all_cnn = false, same_prep = false;
   bool group_plan_ok = std::getenv("CREDO_NO_GROUP") == nullptr;  // false: per replica
   std::unique_ptr<CnnGroupPlan> gplan;   // grouped per-layer launches
+  // heterogeneous CNN groups: each local replica's forward on its own stream
+  // (forked from and joined into the main stream) so one model's small
+  // layers and tails leave SMs to the others (CREDO_NO_HETERO_STREAMS=1:
+  // sequential on the main stream)
+  std::vector<cudaStream_t> rstreams;
+  std::vector<cudaEvent_t> revs;  // [0] fork, [1 + li] replica li done
   std::vector<std::unique_ptr<IngestSlot>> slots;
   uint64_t next_ticket = 1;
   uint32_t last_B = 0;
