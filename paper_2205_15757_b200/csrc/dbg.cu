@@ -299,7 +299,10 @@ static int dbg_conv_gemm(cg_ctx* ctx, const uint16_t* A, int rowsA, const uint16
       CG_CUDA(cudaMemcpy(dres, residual, (size_t)rows_out * N * 2, cudaMemcpyHostToDevice));
     }
     Operand oa, ob;
-    make_operand(oa, dA, rowsA, Kc, 128 + 2 * halo_lo);
+    // halos wider than one 256-row box: stacked boxes (ConvGemmArgs::halo_sub)
+    int hsub = 1, hbox = 128 + 2 * halo_lo;
+    if (halo_lo > 0 && hbox > 256) halo_boxes(halo_lo, hsub, hbox);
+    make_operand(oa, dA, rowsA, Kc, hbox);
     make_operand(ob, dB, N, ntaps * Kc, pair ? BN / 2 : BN);
     ConvGemmArgs a{};
     a.M = M;
@@ -320,6 +323,8 @@ static int dbg_conv_gemm(cg_ctx* ctx, const uint16_t* A, int rowsA, const uint16
     a.W = W;
     a.rows_out = rows_out;
     a.halo_lo = halo_lo;
+    a.halo_sub = hsub;
+    a.halo_box = hbox;
     launch_conv_gemm(oa, ob, a, BN, st, max_ctas);
     CG_CUDA(cudaStreamSynchronize(st));
     CG_CUDA(cudaMemcpy(out, dout, outsz, cudaMemcpyDeviceToHost));

@@ -188,11 +188,15 @@ def run_halo(ctx, A, Bw, N, Kc, taps, bias, H, W, M, rows_out, BN, halo_lo, pair
 
 
 @pytest.mark.parametrize("NB,H,C,Cout,BN", [(3, 7, 64, 128, 128), (2, 14, 128, 64, 64),
-                                            (2, 28, 64, 256, 256), (2, 56, 64, 64, 64)])
+                                            (2, 28, 64, 256, 256), (2, 56, 64, 64, 64),
+                                            # wide halos: 2 / 3 stacked boxes per slot
+                                            (1, 112, 64, 64, 64), (1, 112, 128, 128, 128),
+                                            (1, 224, 64, 64, 64)])
 def test_conv3x3_halo(ctx, NB, H, C, Cout, BN):
     """Halo mode: one (128 + 2*(W+2))-row box per channel block feeds all 9
     taps (MMA descriptors at arbitrary row offsets inside the 128B-swizzled
-    halo) == torch conv2d."""
+    halo) == torch conv2d. Halos wider than 256 rows arrive as stacked boxes
+    (ConvGemmArgs::halo_sub) in one slot."""
     W = H
     g = torch.Generator().manual_seed(H * C + 1)
     x = torch.rand(NB, C, H, W, generator=g) * 2 - 1
