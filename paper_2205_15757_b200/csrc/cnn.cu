@@ -506,7 +506,7 @@ class ResNet final : public CnnModel {
     int ldout = 0, out_f32 = 0, relu = 0, mode = 0, H = 0, rows_out = 0;
     int halo_lo = 0;  // > 0: 3x3 taps fed from one halo box per channel block
     int s2d = 0, gh = 0, gw = 0;  // the s2d stem (ConvGemmArgs::s2d)
-    int s2d_step = 0;             // ConvGemmArgs::s2d_step
+    int s2d_step = 0, s2d_ndy = 0;  // ConvGemmArgs::s2d_step / s2d_ndy
     const bf16* A2 = nullptr;     // second K segment operand (ConvGemmArgs::kc2)
     int kc2 = 0;
     int a2_b = 0, a2_h = 0, a2_rpb = 0;  // A2 = x[2h, 2w] of [a2_b, a2_h, a2_h, kc2] in place
@@ -878,6 +878,7 @@ class ResNet final : public CnnModel {
     a.halo_box = hbox;
     a.s2d = d0.s2d;
     a.s2d_step = d0.s2d_step;
+    a.s2d_ndy = d0.s2d_ndy;
     a.kc2 = d0.kc2;
     a.a2_wo = d0.a2_rpb ? d0.a2_h / 2 : 0;
     a.a2_rpb = d0.a2_rpb;
@@ -1501,6 +1502,7 @@ class Vgg16 final : public SeqNet {
         L.back().g.ntaps = 16;
         L.back().g.s2d = 1;
         L.back().g.s2d_step = 1;
+        L.back().g.s2d_ndy = 3;  // the 3x3's fourth kernel row is all zero: skipped
         L.back().g.gh = L.back().g.gw = Gg;
       } else if (i == 0) {
         push_gemm(L, c, in, b * H * H, b * H * H, nullptr, nullptr, 0, out, c.cout, 0, 1,

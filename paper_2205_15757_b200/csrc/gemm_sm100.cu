@@ -841,7 +841,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           if constexpr (S2D) {
             // per dy pair (or per dy), one box per sub-tile: BM + gw + 3
             // (or BM + 3) rows
-            const int step = a.s2d_step == 1 ? 1 : 2, nbox = 4 / step;
+            const int step = a.s2d_step == 1 ? 1 : 2;
+            const int nbox = step == 1 && a.s2d_ndy > 0 ? a.s2d_ndy : 4 / step;
             const int brows = BM + (step - 1) * a.gw + 3;
             for (int h = 0; h < nbox; h++)
               for (int sub = 0; sub < kSubTiles; sub++) {
@@ -971,7 +972,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             // per dy pair: both sub-tiles' boxes (ring slots hs, hs + 1), the
             // two accumulators' MMAs interleaved
             static_assert(kSubTiles == 2 && HALO % 2 == 0, "s2d: sub-tile box pairs");
-            const int step = a.s2d_step == 1 ? 1 : 2, nbox = 4 / step;
+            const int step = a.s2d_step == 1 ? 1 : 2;
+            const int nbox = step == 1 && a.s2d_ndy > 0 ? a.s2d_ndy : 4 / step;
             for (int h = 0; h < nbox; h++) {
               mbar_wait(&hfull[hs], hphase);
               mbar_wait(&hfull[hs + 1], hphase);
@@ -1876,6 +1878,8 @@ static void map128_res(CUtensorMap& m, const void* p, int ld, int rows) {
 
 void prepare_conv_gemm(PreparedGemm& p, const ConvGemmGroup& g, const ConvGemmArgs& a, int BN) {
   if (a.s2d) {
+    if (a.s2d_ndy < 0 || a.s2d_ndy > 4 || (a.s2d_ndy && a.s2d_step != 1))
+      throw InvalidArgument("conv_gemm: s2d_ndy is for one box per kernel row");
     if (BN != 64 || a.N != 64 || a.Kc != 16 || a.ntaps != 16 || a.halo_lo || a.pair ||
         (a.row_mode != kRowGridToCompact && a.row_mode != kRowIdentity &&
          a.row_mode != kRowGridToPad) || a.out_f32 ||

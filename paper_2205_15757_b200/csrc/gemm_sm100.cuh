@@ -81,6 +81,7 @@ struct ConvGemmArgs {
   // box per dy (BM + 3 rows; grids wider than 125 columns, e.g. a 3x3 conv
   // over a 16-channel 224-pixel image as a 4x4 with zero fourth taps)
   int s2d_step;
+  int s2d_ndy;  // s2d_step 1: kernel rows with non-zero taps (0 = all 4)
   // Second K segment (1x1 convs only): k-blocks Kc/64 .. Kc/64 + kc2/64 - 1
   // read A from the A2 operand (same rows) against weight columns Kc ..
   // Kc + kc2 - 1 -- a bottleneck's c3 and its projection shortcut (ds) as one
